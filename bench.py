@@ -1,0 +1,398 @@
+"""Benchmark of the memory-efficient dense-block hot path on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--config bc100|cfg1|d121|d264k32|d264k48]
+
+One step = forward + backward of every dense block of the configuration
+(BASELINE.json configs[1] by default: DenseNet-BC-100, k=12, batch 64 per
+GPU, 3x32x32 input), on synthetic inputs resident in HBM, through libdpb.so
+(bf16 features, fp32 gradients).  Stem, transitions and head are not part of
+the hot path and are not run.  Prints ONE JSON line on
+rank 0; see DESIGN.md §5 for every field.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import tempfile
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+BATCH = 64
+METRIC = "DenseNet train images/sec (dense blocks fwd+bwd)"
+
+
+def load_peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        d = json.load(open(path))
+        return float(d["hbm_gbs"]), float(d["bf16_tflops"]), float(d.get("bf16_tflops_sustained", d["bf16_tflops"])), "measured"
+    except Exception:
+        return 6650.0, 1590.0, 1400.0, "fallback"
+
+
+def block_shapes(config: str, batch: int):
+    from paper_1707_06990_b200.model import CONFIGS
+    cfg = CONFIGS[config]
+    stem_stride = 4 if cfg.in_shape[1] >= 224 else 1   # ImageNet 7x7/2 + maxpool geometry (F4)
+    return [(s.n, s.h, s.w, s.c0, s.m, s.k, s.bk) for s in cfg.block_shapes(batch, stem_stride)]
+
+
+def algorithmic_per_image(shapes, S=2):
+    """F = sum_l HW [6 c bk + 54 bk k],  B = sum_l HW (22 c + 16 bk + 6 k)."""
+    F = B = 0.0
+    for (n, h, w, c0, m, k, bk) in shapes:
+        hw = h * w
+        for l in range(m):
+            c = c0 + l * k
+            F += hw * (3 * 2 * c * bk + 3 * 2 * 9 * bk * k)
+            B += hw * (22 * c + 16 * bk + 6 * k)
+    return F, B
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    def __init__(self, device_index: int):
+        self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+        q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap")
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", f"--id={device_index}", f"--query-gpu={q}",
+                                       "--format=csv,noheader,nounits", "-lms", "100"],
+                                      stdout=self.f, stderr=subprocess.DEVNULL)
+        except OSError:
+            self.p = None
+
+    def stop(self) -> dict:
+        if self.p is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.p.terminate()
+        self.p.wait()
+        self.f.seek(0)
+        sms, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in self.f.read().splitlines():
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sms.append(float(parts[0]))
+                mx = float(parts[1])
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[3:7]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        os.unlink(self.f.name)
+        sms.sort()
+        return {"sm_mhz": sms[len(sms) // 2] if sms else None, "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(sms)}
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    from oracle import cpu_bench as CB
+    shapes = block_shapes(args.config, 1)
+    runner = CB.CpuRunner(shapes)
+    for i in range(args.warmup):
+        runner.step(seed=i)
+    imgs = secs = 0.0
+    t_budget = time.perf_counter()
+    steps = 0
+    for i in range(args.steps):
+        n, s = runner.step(seed=100 + i)
+        imgs += n
+        secs += s
+        steps += 1
+        if time.perf_counter() - t_budget > args.ref_budget_s:
+            break
+    runner.close()
+    value = imgs / secs
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "images/s", "n_gpus": args.gpus,
+        "steps": steps, "warmup": args.warmup, "ms_per_step": 1000 * secs / steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic",
+        "config": {"workload": f"{args.config} dense blocks fwd+bwd, reference CPU (denseplan ops:: in "
+                               f"GraphPlan order)", "global_batch": runner.procs, "per_process_batch": 1,
+                   "shapes": shapes},
+        "cpu_baseline": {"value": value, "unit": "images/s", "cores": runner.procs, "kind": CB.kind(),
+                         "sample": f"{steps} steps x {runner.procs} processes x 1 image of each "
+                                   f"{args.config} dense block (fwd+bwd), {CB.cpu_model()}"},
+        "e2e": {"value": value, "unit": "images/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="bc100")
+    ap.add_argument("--dtype", default="bf16", choices=["bf16", "fp32"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-budget-s", type=float, default=25.0)
+    ap.add_argument("--ref-budget-s", type=float, default=180.0)
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    if args.impl == "reference":
+        return run_reference(args)
+
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    import paper_1707_06990_b200 as P
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+
+    hbm_peak, bf16_peak, bf16_sust, peak_src = load_peaks()
+    shapes = block_shapes(args.config, BATCH)
+    stream = torch.cuda.Stream(device=dev)
+    g = torch.Generator(device="cpu").manual_seed(1234 + rank)
+
+    blocks = []
+    with torch.cuda.stream(stream):
+        for s in shapes:
+            shp = P.BlockShape(*s)
+            plan = P.BlockPlan(shp, dtype=args.dtype, layout="nhwc", device=local, stream=stream)
+            params = torch.randn(shp.param_elems, generator=g) * 0.1
+            for l, o in enumerate(shp.param_offsets()):
+                c = shp.c_in(l)
+                params[o:o + c] += 1.0
+                gb = o + 2 * c + shp.bk * c
+                params[gb:gb + shp.bk] += 1.0
+            blocks.append(dict(
+                shape=shp, plan=plan, params=params.to(dev),
+                running=shp.initial_running(dev),
+                x=torch.randn(shp.pixels, shp.c0, generator=g).to(dev),
+                gup=torch.randn(shp.pixels, shp.c_out, generator=g).to(dev),
+                acc=torch.empty(shp.pixels, shp.c_out, device=dev),
+                grads=torch.empty(shp.param_elems, device=dev)))
+    flat_grads = None
+    if world > 1:
+        flat_grads = torch.empty(sum(b["grads"].numel() for b in blocks), device=dev)
+
+    def step():
+        for b in blocks:
+            b["plan"].forward(b["x"], b["params"], b["running"], True)
+        for b in reversed(blocks):
+            b["acc"].copy_(b["gup"])          # consumer BN backward writes the block-output grad
+            b["plan"].backward(b["params"], b["acc"], b["grads"])
+        if world > 1:
+            # data-parallel gradient allreduce (per-GPU BN)
+            torch.cat([b["grads"] for b in blocks], out=flat_grads)
+            dist.all_reduce(flat_grads)
+            flat_grads.mul_(1.0 / world)
+
+    with torch.cuda.stream(stream):
+        for _ in range(args.warmup):
+            step()
+    torch.cuda.synchronize(dev)
+    launches_per_step = sum(b["plan"].launch_count for b in blocks)  # last backward only
+    # count forward+backward launches of one step precisely
+    with torch.cuda.stream(stream):
+        fwd_launches = 0
+        for b in blocks:
+            b["plan"].forward(b["x"], b["params"], b["running"], True)
+            fwd_launches += b["plan"].launch_count
+        bwd_launches = 0
+        for b in reversed(blocks):
+            b["acc"].copy_(b["gup"])
+            b["plan"].backward(b["params"], b["acc"], b["grads"])
+            bwd_launches += b["plan"].launch_count
+    launches_per_step = fwd_launches + bwd_launches
+    torch.cuda.synchronize(dev)
+
+    # ---- timed region --------------------------------------------------------
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize(dev)
+    clocks = ClockSampler(local)
+    time.sleep(0.3)
+    t0 = torch.cuda.Event(enable_timing=True)
+    t1 = torch.cuda.Event(enable_timing=True)
+    with torch.cuda.stream(stream):
+        t0.record(stream)
+        for _ in range(args.steps):
+            step()
+        t1.record(stream)
+    torch.cuda.synchronize(dev)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize(dev)
+    ms = t0.elapsed_time(t1)
+    clk = clocks.stop()
+    if world > 1:
+        tt = torch.tensor([ms], device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        ms = float(tt.item())
+    ms_per_step = ms / args.steps
+    value = BATCH * world * args.steps / (ms / 1000.0)
+
+    # ---- per-kernel roofline (separate profiled pass, events on `stream`) -----
+    for b in blocks:
+        b["plan"].profile(True)
+    with torch.cuda.stream(stream):
+        for _ in range(2):
+            for b in blocks:
+                b["plan"].forward(b["x"], b["params"], b["running"], True)
+            for b in reversed(blocks):
+                b["acc"].copy_(b["gup"])
+                b["plan"].backward(b["params"], b["acc"], b["grads"])
+    torch.cuda.synchronize(dev)
+    cats = {}
+    for b in blocks:
+        for name, st in b["plan"].profile_read().items():
+            c = cats.setdefault(name, {"launches": 0, "total_ms": 0.0, "bytes": 0.0, "flops": 0.0})
+            for key in c:
+                c[key] += st[key]
+        b["plan"].profile(False)
+    prof_total = sum(c["total_ms"] for c in cats.values())
+    dom_name, dom = max(cats.items(), key=lambda kv: kv[1]["total_ms"])
+    avg_ms = dom["total_ms"] / dom["launches"]
+    bytes_per_launch = dom["bytes"] / dom["launches"]
+    flops_per_launch = dom["flops"] / dom["launches"]
+    ridge = bf16_peak * 1e12 / (hbm_peak * 1e9)
+    intensity = flops_per_launch / max(bytes_per_launch, 1.0)
+    if intensity < ridge:
+        roof = {"bound": "hbm", "achieved": bytes_per_launch / (avg_ms * 1e-3) / 1e9, "peak": hbm_peak,
+                "unit": "GB/s"}
+    else:
+        roof = {"bound": "tensor", "achieved": flops_per_launch / (avg_ms * 1e-3) / 1e12,
+                "peak": bf16_sust, "unit": "TFLOP/s"}
+    roof["frac"] = roof["achieved"] / roof["peak"]
+    roof["traffic"] = None
+    roof["kernel"] = dom_name
+    roof["kernel_share_of_step"] = dom["total_ms"] / prof_total
+    roof["peak_source"] = peak_src
+    F_img, B_img = algorithmic_per_image(shapes)
+    t_roof = max(F_img / (bf16_peak * 1e12), B_img / (hbm_peak * 1e9))
+    step_roof = {"algorithmic_gflop_per_img": F_img / 1e9, "algorithmic_mb_per_img": B_img / 1e6,
+                 "ceiling_img_per_s_per_gpu": 1.0 / t_roof,
+                 "frac": (value / world) * t_roof}
+    kernels = {k: {"launches": v["launches"], "ms": round(v["total_ms"] / 2, 4),
+                   "GB/s": round(v["bytes"] / max(v["total_ms"], 1e-9) / 1e6, 1),
+                   "TFLOP/s": round(v["flops"] / max(v["total_ms"], 1e-9) / 1e9, 2)}
+               for k, v in sorted(cats.items(), key=lambda kv: -kv[1]["total_ms"])}
+
+    # ---- end to end through the reference-facing C-ABI (host buffers, NCHW) ---
+    e2e = None
+    with torch.cuda.stream(stream):
+        e_blocks = []
+        for b in blocks:
+            shp = b["shape"]
+            plan = P.BlockPlan(shp, dtype=args.dtype, layout="nchw", device=local, stream=stream)
+            e_blocks.append(dict(
+                plan=plan, params=b["params"], running=b["running"],
+                x_h=torch.randn(shp.n, shp.c0, shp.h, shp.w, generator=g).pin_memory(),
+                g_h=torch.randn(shp.n, shp.c_out, shp.h, shp.w, generator=g).pin_memory(),
+                x=torch.empty(shp.n, shp.c0, shp.h, shp.w, device=dev),
+                acc=torch.empty(shp.n, shp.c_out, shp.h, shp.w, device=dev),
+                grads=torch.empty(shp.param_elems, device=dev),
+                grads_h=torch.empty(shp.param_elems).pin_memory()))
+        h2d = sum(e["x_h"].numel() * 4 + e["g_h"].numel() * 4 for e in e_blocks)
+        d2h = sum(e["grads_h"].numel() * 4 for e in e_blocks)
+
+        def e2e_step():
+            for e in e_blocks:
+                e["x"].copy_(e["x_h"], non_blocking=True)
+                e["plan"].forward(e["x"], e["params"], e["running"], True)
+            for e in reversed(e_blocks):
+                e["acc"].copy_(e["g_h"], non_blocking=True)
+                e["plan"].backward(e["params"], e["acc"], e["grads"])
+                e["grads_h"].copy_(e["grads"], non_blocking=True)
+
+        for _ in range(args.warmup):
+            e2e_step()
+        torch.cuda.synchronize(dev)
+        ek = max(3, min(args.steps, 10))
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(ek):
+            e2e_step()
+        e1.record(stream)
+        torch.cuda.synchronize(dev)
+        ems = e0.elapsed_time(e1)
+        if world > 1:
+            tt = torch.tensor([ems], device=dev)
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            ems = float(tt.item())
+        e2e = {"value": BATCH * world * ek / (ems / 1000.0), "unit": "images/s",
+               "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "steps": ek,
+               "path": "dpb_block_forward/backward, NCHW fp32 host-pinned buffers"}
+        for e in e_blocks:
+            e["plan"].close()
+
+    # ---- memory: efficient arena vs naive store-everything ---------------------
+    eff = sum(P.block_memory(b["shape"], args.dtype)[0] for b in blocks)
+    naive = sum(P.block_memory(b["shape"], "fp32")[1] for b in blocks)
+
+    # ---- CPU baseline (rank 0, N=1 only) ---------------------------------------
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        try:
+            from oracle import cpu_bench as CB
+            runner = CB.CpuRunner(block_shapes(args.config, 1))
+            runner.step(seed=1)        # warm (spawn + page-in)
+            imgs, secs, n = 0, 0.0, 0
+            while secs < args.cpu_budget_s and n < 5:
+                a, s = runner.step(seed=10 + n)
+                imgs += a
+                secs += s
+                n += 1
+            runner.close()
+            cpu = {"value": imgs / secs, "unit": "images/s", "cores": runner.procs, "kind": CB.kind(),
+                   "sample": f"{n} steps x {runner.procs} processes x 1 image of each {args.config} "
+                             f"dense block (fwd+bwd, f32), {CB.cpu_model()}"}
+        except Exception as exc:  # the baseline is reported, never the target
+            cpu = {"value": None, "unit": "images/s", "cores": 0, "kind": "port", "sample": f"failed: {exc}"}
+
+    if rank == 0:
+        S = 2 if args.dtype == "bf16" else 4
+        ws_bytes = sum(P.plan_arena(b["shape"], args.dtype, "nhwc")["total_bytes"] for b in blocks)
+        line = {
+            "metric": METRIC, "value": value, "unit": "images/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": args.dtype, "data": "synthetic",
+            "config": {"workload": f"DenseNet-{args.config} dense blocks, fwd+bwd (stem/transitions/head "
+                                   f"not in the hot path)", "model": args.config, "global_batch": BATCH * world,
+                       "per_gpu_batch": BATCH, "blocks": [list(s) for s in shapes],
+                       "parallelism": f"dp{world}",
+                       "l2": f"working set {ws_bytes / 1e6:.0f} MB > 126 MB L2 (no explicit flush)"},
+            "roofline": roof, "step_roofline": step_roof, "kernels": kernels,
+            "cpu_baseline": cpu, "e2e": e2e,
+            "gpu_launches": launches_per_step * args.steps,
+            "memory": {"efficient_arena_bytes": eff, "naive_bytes": naive,
+                       "ratio": eff / naive},
+            "clocks": clk,
+        }
+        print(json.dumps(line), flush=True)
+    for b in blocks:
+        b["plan"].close()
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,235 @@
+/*
+ * dpb.h — C ABI of the B200-native memory-efficient dense block.
+ *
+ * This is the drop-in boundary for the reference's hot path (denseplan,
+ * arXiv 1707.06990): the pre-activation bottleneck dense block
+ *   cat -> BN_a -> ReLU -> conv1x1 -> BN_b -> ReLU -> conv3x3
+ * forward and backward with shared storage and recompute-on-backward.
+ * Plain C: pointers, sizes and status codes only; no C++ or torch types.
+ *
+ * Reference interfaces replaced (paths relative to /root/reference/proj):
+ *   dpb_block_plan          GraphPlan<T>::build pool sizing + PoolRegion /
+ *                           GradPool / BufferPool  include/denseplan/graph.hpp:28-127,
+ *                           :456-482, :602-609 (one block's share)
+ *   dpb_block_forward       GraphPlan<T>::forward layer loop over forward_layer
+ *                           include/denseplan/graph.hpp:747-760, :618-670
+ *   dpb_block_backward      GraphPlan<T>::backward_block -> backward_layer with
+ *                           rematerialize   include/denseplan/graph.hpp:1054-1063,
+ *                           :856-945, :831-854
+ *   dpb_op_*                the per-op kernels of include/denseplan/ops.hpp
+ *                           (batch_statistics :138-162, batchnorm_apply :115-134,
+ *                           batchnorm_backward :206-243, conv2d_forward :315-342,
+ *                           conv2d_backward :346-387)
+ *   dpb_count_parameters,   densenet.hpp:234-275, peak_model.hpp:37-158
+ *   dpb_predict_peak_elements
+ *   status codes            errors.hpp:8-61 (1:1, declaration order)
+ *
+ * Conventions
+ *   - Every entry point returns int status: 0 OK; 1..12 the reference error
+ *     classes in declaration order; >= 100 CUDA / NCCL failures.
+ *     dpb_last_error() returns a thread-local message for the last failure.
+ *   - All tensor pointers passed to device entry points are DEVICE pointers
+ *     owned by the caller; the block handle owns its HBM arena.  Calls are
+ *     asynchronous on the handle's stream; dpb_sync() surfaces async errors.
+ *   - Reference-facing tensors are fp32 NCHW (dp/tensor.hpp:102-108).  The
+ *     block's internal layout is NHWC in the arena.
+ *   - Flat per-block parameter layout (reference registration order,
+ *     graph.hpp:459-478), layer l with c = c0 + l*k input channels:
+ *         gamma_a[c] beta_a[c] W1[bk][c] gamma_b[bk] beta_b[bk] W2[k][bk][3][3]
+ *     Gradients use the same layout.  Statistics / running statistics:
+ *         mean_a[c] var_a[c] mean_b[bk] var_b[bk]       per layer.
+ *   - One handle per GPU, used by one host thread at a time (the reference
+ *     plan is single-threaded, alloctrace.hpp:55-56).
+ */
+#ifndef DPB_H_
+#define DPB_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define DPB_API __attribute__((visibility("default")))
+#else
+#define DPB_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* status codes: errors.hpp declaration order */
+enum {
+  DPB_OK = 0,
+  DPB_SHAPE_ERROR = 1,
+  DPB_BOUNDS_ERROR = 2,
+  DPB_SIZE_OVERFLOW_ERROR = 3,
+  DPB_CAPACITY_ERROR = 4,
+  DPB_ACCOUNTING_ERROR = 5,
+  DPB_CONFIG_ERROR = 6,
+  DPB_FORMAT_ERROR = 7,
+  DPB_LABEL_ERROR = 8,
+  DPB_DEGENERATE_BATCH_ERROR = 9,
+  DPB_PROTOCOL_ERROR = 10,
+  DPB_RANGE_ERROR = 11,
+  DPB_VERIFY_ERROR = 12,
+  DPB_CUDA_ERROR = 100,
+  DPB_NCCL_ERROR = 101
+};
+
+/* storage precision of features / bottleneck outputs inside the arena */
+enum { DPB_FP32 = 0, DPB_BF16 = 1 };
+
+/* layout of the reference-facing block input / gradient tensors */
+enum { DPB_NCHW = 0, DPB_NHWC = 1 };
+
+/* arena tags: alloctrace.hpp:17-24 */
+enum {
+  DPB_ARENA_PARAMS = 0,
+  DPB_ARENA_FEATURE_OWNED = 1,
+  DPB_ARENA_SHARED1 = 2,
+  DPB_ARENA_SHARED2 = 3,
+  DPB_ARENA_SHARED_GRAD = 4,
+  DPB_ARENA_SCRATCH = 5
+};
+
+typedef struct dpb_block_desc {
+  int64_t n, h, w; /* batch and spatial size inside the block */
+  int32_t c0;      /* channels entering the block */
+  int32_t m;       /* bottleneck layers */
+  int32_t k;       /* growth rate */
+  int32_t bk;      /* bottleneck width (4k in DenseNet-BC) */
+  int32_t dtype;   /* DPB_FP32 (1e-4 parity path) or DPB_BF16 (tensor path) */
+  int32_t layout;  /* DPB_NCHW or DPB_NHWC for x_in / grad_acc */
+} dpb_block_desc;
+
+/* Byte layout of one block's HBM arena (host-side plan, no allocation). */
+typedef struct dpb_arena_sizes {
+  int64_t total_bytes;
+  /* persistent over fwd->bwd (FeatureOwned: the O(m) part) */
+  int64_t feat_offset, feat_bytes;   /* [M, c_out] features (x_in | y_1..y_m)  */
+  int64_t z_offset, z_bytes;         /* m x [M, bk] bottleneck outputs          */
+  int64_t stats_offset, stats_bytes; /* per-channel batch mean/var               */
+  /* SharedGrad: block accumulator + two transient slots */
+  int64_t acc_offset, acc_bytes;     /* [M, c_out] fp32                          */
+  int64_t g0_offset, g0_bytes;       /* [M, bk]   fp32 masked 3x3 dgrad          */
+  int64_t g1_offset, g1_bytes;       /* [M, c_max] fp32 masked 1x1 dgrad         */
+  /* Scratch: reduction partials, GEMM-layout weight copies */
+  int64_t scratch_offset, scratch_bytes;
+  /* Shared1/Shared2 of the reference are 0: concat is a zero-copy channel
+   * prefix and BN+ReLU are recomputed inside the conv prologues. */
+  int64_t shared1_bytes, shared2_bytes;
+  int64_t param_elems;   /* flat parameter count of the block             */
+  int64_t stat_elems;    /* flat statistics count of the block            */
+} dpb_arena_sizes;
+
+typedef struct dpb_block dpb_block;
+
+DPB_API const char* dpb_last_error(void);
+DPB_API const char* dpb_version(void);
+
+/* Host-only: validate the descriptor and compute the arena layout. */
+DPB_API int dpb_block_plan(const dpb_block_desc* desc, dpb_arena_sizes* out);
+DPB_API int dpb_block_param_elems(const dpb_block_desc* desc, int64_t* param_elems,
+                          int64_t* stat_elems);
+
+/* Allocate the arena on `device`; `stream` is a cudaStream_t (NULL = legacy
+ * default stream). */
+DPB_API int dpb_block_create(const dpb_block_desc* desc, int device, void* stream,
+                     dpb_block** out);
+DPB_API int dpb_block_destroy(dpb_block* blk);
+DPB_API int dpb_block_set_stream(dpb_block* blk, void* stream);
+DPB_API int dpb_block_arena(dpb_block* blk, dpb_arena_sizes* out, void** base);
+
+/* Forward (train mode).  x_in: [n, c0, h, w] fp32 (or NHWC per desc).
+ * params: flat fp32 device array.  running: flat fp32 running stats, updated
+ * in place with momentum 0.1 / biased variance when update_running != 0
+ * (ops.hpp:185-194).  After the call the arena holds the block output
+ * features, the bottleneck outputs and the batch statistics.  DegenerateBatch
+ * (9) when n*h*w < 2. */
+DPB_API int dpb_block_forward(dpb_block* blk, const float* x_in, const float* params,
+                      float* running, int update_running);
+
+/* Eval mode: normalise with the running statistics (ops.hpp:196-199). */
+DPB_API int dpb_block_forward_eval(dpb_block* blk, const float* x_in,
+                           const float* params, const float* running);
+
+/* Backward.  grad_acc: [n, c_out, h, w] fp32 gradient w.r.t. the block output
+ * (as written by the consumer's BN backward, graph.hpp:1117-1120); on return
+ * it holds the full block-gradient accumulator, whose prefix [0, c0) is the
+ * gradient w.r.t. the block input (graph.hpp:1138, :1172-1173).  grads: flat
+ * fp32, written (not accumulated) like conv2d_backward / batchnorm_backward.
+ * Protocol error (10) if no train-mode forward preceded it. */
+DPB_API int dpb_block_backward(dpb_block* blk, const float* params, float* grad_acc,
+                       float* grads);
+
+/* Read back arena contents in the reference's NCHW fp32 layout. */
+DPB_API int dpb_block_read_feats(dpb_block* blk, float* dst /* [n, c_out, h, w] */);
+DPB_API int dpb_block_read_z(dpb_block* blk, float* dst /* m x [n, bk, h, w] */);
+DPB_API int dpb_block_read_stats(dpb_block* blk, float* dst /* flat stats layout */);
+
+DPB_API int dpb_sync(dpb_block* blk);
+
+/* Number of kernels the last forward/backward launched (bench accounting). */
+DPB_API int64_t dpb_block_launch_count(dpb_block* blk);
+
+/* Optional per-launch profiler: when enabled every kernel launch is bracketed
+ * by CUDA events on the block's stream and tagged with its algorithmic HBM
+ * bytes and FLOPs.  Enabling resets the record; reading
+ * synchronises the stream and returns one entry per kernel category. */
+typedef struct dpb_kernel_stat {
+  char name[32];
+  int64_t launches;
+  double total_ms;
+  double bytes;  /* algorithmic bytes summed over the launches */
+  double flops;  /* algorithmic flops summed over the launches */
+} dpb_kernel_stat;
+DPB_API int dpb_block_profile(dpb_block* blk, int enable);
+DPB_API int dpb_block_profile_read(dpb_block* blk, dpb_kernel_stat* out, int max, int* count);
+/* Peak device bytes the block's arena holds (efficient variant) and what a
+ * naive store-everything variant of the same block would hold. */
+DPB_API int dpb_block_memory(const dpb_block_desc* desc, int64_t* efficient_bytes,
+                     int64_t* naive_bytes);
+
+/* ---- per-op entry points (ops.hpp parity), fp32 NCHW device tensors ---- */
+DPB_API int dpb_op_batch_statistics(const float* x, int64_t n, int64_t c, int64_t h,
+                            int64_t w, float* mean, float* var, void* stream);
+DPB_API int dpb_op_batchnorm_apply(const float* x, int64_t n, int64_t c, int64_t h,
+                           int64_t w, const float* gamma, const float* beta,
+                           const float* mean, const float* var, int relu,
+                           float* dst, void* stream);
+DPB_API int dpb_op_batchnorm_backward(const float* grad_y, const float* x, int64_t n,
+                              int64_t c, int64_t h, int64_t w,
+                              const float* gamma, const float* mean,
+                              const float* var, float* grad_x,
+                              float* grad_gamma, float* grad_beta,
+                              void* stream);
+DPB_API int dpb_op_conv2d_forward(const float* x, int64_t n, int64_t cin, int64_t h,
+                          int64_t w, const float* weights, int64_t cout,
+                          int64_t kernel, int64_t pad, float* dst,
+                          void* stream);
+DPB_API int dpb_op_conv2d_backward(const float* grad_y, const float* x, int64_t n,
+                           int64_t cin, int64_t h, int64_t w,
+                           const float* weights, int64_t cout, int64_t kernel,
+                           int64_t pad, float* grad_x /* may be NULL */,
+                           float* grad_w, void* stream);
+
+/* ---- host-side model arithmetic (densenet.hpp / peak_model.hpp) -------- */
+DPB_API int dpb_count_parameters(int nblocks, const int32_t* blocks, int32_t k,
+                         int32_t bottleneck, double compression,
+                         int32_t classes, int32_t c0, int32_t in_c,
+                         int64_t* out);
+/* strategy: 0 naive, 1 shared-gradient, 2 shared-all; out[6] per arena */
+DPB_API int dpb_predict_peak_elements(int nblocks, const int32_t* blocks, int32_t k,
+                              int32_t bottleneck, double compression,
+                              int32_t classes, int32_t c0, int32_t strategy,
+                              int64_t batch, int32_t in_c, int32_t in_h,
+                              int32_t in_w, int64_t* out);
+
+/* Rng(seed).normal() x count in the reference's draw order (rng.hpp:36-49) */
+DPB_API int dpb_rng_fill_normal(uint64_t seed, float* host_dst, int64_t count);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* DPB_H_ */

@@ -1,0 +1,107 @@
+"""TEST INFRASTRUCTURE — regenerates tests/golden/*.npz from the reference.
+
+Run in the build container (needs /root/reference, i.e. oracle/_ref):
+
+    python -m oracle.gen_golden
+
+Every fixture is produced by the UNMODIFIED reference headers compiled into
+oracle/_ref/libdenseplan_ref.so: the block-level harness over the public
+``ops::`` functions (itself checked bitwise against GraphPlan::step_trace by
+``ref_check_block_harness``), ``GraphPlan::build`` parameter draws,
+``count_parameters`` and ``predict_peak_elements``.  The fixtures are small
+(<1 MB total) and committed; the GPU box never needs /root/reference.
+"""
+from __future__ import annotations
+
+import json
+import os
+
+import numpy as np
+
+from oracle import oracle as O
+
+OUT = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "tests", "golden")
+
+# name -> (BlockShape, params source, dtype)
+CASES = {
+    # perturbed BN gamma/beta (SURVEY §8(d) second parity case)
+    "small_perturbed_f32": (O.BlockShape(2, 5, 6, 8, 3, 4, 16), "perturbed", np.float32),
+    "small_perturbed_f64": (O.BlockShape(2, 5, 6, 8, 3, 4, 16), "perturbed", np.float64),
+    # ragged: odd spatial dims, odd channel counts
+    "ragged_f32": (O.BlockShape(3, 7, 3, 5, 2, 3, 12), "perturbed", np.float32),
+    # minimum non-degenerate batch: n*h*w == 2 (ops.hpp:180-183)
+    "minimal_f32": (O.BlockShape(1, 1, 2, 4, 1, 2, 8), "perturbed", np.float32),
+    # parameters exactly as GraphPlan<float>::build draws them for a
+    # single-block model blocks={4}, k=4, c0=8 (He-normal; gamma=1, beta=0)
+    "graphplan_init_f32": (O.BlockShape(2, 6, 6, 8, 4, 4, 16), "graphplan", np.float32),
+    # the cfg1 channel geometry (c0=24, k=12, bk=48) at a reduced batch/field
+    "cfg1_geometry_f32": (O.BlockShape(2, 8, 8, 24, 3, 12, 48), "perturbed", np.float32),
+}
+
+
+def make_case(name, s, src, dt):
+    seed = 7
+    if src == "graphplan":
+        params = O.ref_block_params([s.m], s.k, True, 1.0, 4, s.c0, (s.n, 3, s.h, s.w), seed, 0)
+    else:
+        params = O.random_block_params(s, seed, dt, perturb_bn=True)
+    params = params.astype(dt)
+    x_in = O.rng_normal(seed + 99, s.n * s.c0 * s.h * s.w, dt).reshape(s.n, s.c0, s.h, s.w)
+    acc_in = O.rng_normal(seed + 100, s.n * s.c_out * s.h * s.w, dt).reshape(s.n, s.c_out, s.h, s.w)
+    # running stats start from a non-trivial state so the momentum rule is exercised
+    running_in = s.initial_running(dt)
+    running_in += (0.25 * O.rng_normal(seed + 101, running_in.size)).astype(dt)
+    running_in = np.abs(running_in).astype(dt)
+    feats, z, stats, running, acc_out, grads = O.ref_block(s, params, x_in, acc_in, running_in, True)
+    np.savez_compressed(
+        os.path.join(OUT, f"{name}.npz"),
+        shape=np.array([s.n, s.h, s.w, s.c0, s.m, s.k, s.bk], dtype=np.int64),
+        params=params, x_in=x_in, acc_in=acc_in, running_in=running_in,
+        feats=feats, z=z, stats=stats, running=running, acc_out=acc_out, grads=grads)
+
+
+def kats():
+    """Known-answer values pinned by the reference's own tests, recomputed
+    by the reference code here (t/densenet_test.cpp:214-231,
+    t/alloctrace_test.cpp:85-124)."""
+    d = {}
+    d["count_parameters"] = {
+        "bc100_k12": O.ref_count_parameters([16, 16, 16], 12, True, 0.5, 10, 24),
+        "d121_k32": O.ref_count_parameters([6, 12, 24, 16], 32, True, 0.5, 1000, 64),
+        "d264_k32": O.ref_count_parameters([6, 12, 64, 48], 32, True, 0.5, 1000, 64),
+        "d264_k48": O.ref_count_parameters([6, 12, 64, 48], 48, True, 0.5, 1000, 96),
+        "bc160_k12": O.ref_count_parameters([26, 26, 26], 12, True, 0.5, 10, 24),
+        "paper264_k48_preset": O.ref_count_parameters([6, 32, 64, 48], 48, True, 0.5, 1000, 96),
+        "paper264_k32_preset": O.ref_count_parameters([6, 32, 64, 48], 32, True, 0.5, 1000, 64),
+    }
+    peaks = {}
+    cfgs = {
+        "tiny_block_k2": ([3], 2, False, 1.0, 2, 2, 1, 1, 4, 4),  # alloctrace_test KAT
+        "cfg1": ([12], 12, True, 1.0, 10, 24, 16, 3, 32, 32),
+        "bc100_b64": ([16, 16, 16], 12, True, 0.5, 10, 24, 64, 3, 32, 32),
+        "d121_b64_56": ([6, 12, 24, 16], 32, True, 0.5, 1000, 64, 64, 3, 56, 56),
+        "d264k32_b64_56": ([6, 12, 64, 48], 32, True, 0.5, 1000, 64, 64, 3, 56, 56),
+        "d264k48_b64_56": ([6, 12, 64, 48], 48, True, 0.5, 1000, 96, 64, 3, 56, 56),
+    }
+    for name, (blocks, k, bott, comp, classes, c0, n, c, h, w) in cfgs.items():
+        peaks[name] = {strat: O.ref_predict_peak_elements(blocks, k, bott, comp, classes, c0,
+                                                          si, n, c, h, w)
+                       for si, strat in enumerate(["naive", "shared_grad", "shared_all"])}
+    d["predict_peak_elements"] = peaks
+    # denseplan::Rng (the reference's own engine + Box-Muller)
+    d["rng_u64_seed7_first4"] = [int(v) for v in O.ref_rng_u64(7, 4)]
+    d["rng_normal_seed106_first8"] = [float(v) for v in O.ref_rng_normal(106, 8)]
+    return d
+
+
+def main():
+    os.makedirs(OUT, exist_ok=True)
+    for name, (s, src, dt) in CASES.items():
+        make_case(name, s, src, dt)
+    with open(os.path.join(OUT, "kats.json"), "w") as f:
+        json.dump(kats(), f, indent=1, sort_keys=True)
+    print("wrote", sorted(os.listdir(OUT)))
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,343 @@
+"""TEST INFRASTRUCTURE — NOT PRODUCT CODE.
+
+ctypes front end for the parity oracle (``_build/liboracle.so``, the plain-C
+restatement in dp_oracle.c) and, when built, the reference itself
+(``_ref/libdenseplan_ref.so``, the unmodified reference headers compiled by
+oracle/Makefile).  Only tests/, ``__graft_entry__.smoke()`` and bench.py's
+cpu_baseline / reference legs may import this module; the product package
+never does.
+
+Array conventions match the reference (NCHW) and the flat per-block layouts
+documented in dp_oracle.c:
+
+* params / grads, per layer l (c = c0 + l*k):
+  ``gamma_a[c] beta_a[c] W1[bk,c] gamma_b[bk] beta_b[bk] W2[k,bk,3,3]``
+* stats / running, per layer: ``mean_a[c] var_a[c] mean_b[bk] var_b[bk]``
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import subprocess
+from dataclasses import dataclass
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+ORACLE_SO = os.path.join(HERE, "_build", "liboracle.so")
+REF_SO = os.path.join(HERE, "_ref", "libdenseplan_ref.so")
+REF_FAST_SO = os.path.join(HERE, "_ref", "libdenseplan_ref_fast.so")
+
+_P = C.c_void_p
+_I64 = C.c_int64
+
+
+def build(ref: bool | None = None) -> None:
+    """Build liboracle.so (always) and _ref (when /root/reference exists)."""
+    targets = ["_build/liboracle.so"]
+    if ref is None:
+        ref = os.path.isdir("/root/reference/proj/include")
+    if ref:
+        targets.append("ref")
+    subprocess.run(["make", "-s", "-C", HERE, *targets], check=True)
+
+
+def _ptr(a: np.ndarray | None):
+    if a is None:
+        return None
+    assert a.flags["C_CONTIGUOUS"]
+    return a.ctypes.data_as(_P)
+
+
+_lib = None
+_ref = {}
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        if not os.path.exists(ORACLE_SO):
+            build(ref=False)
+        _lib = C.CDLL(ORACLE_SO)
+        for suf in ("f32", "f64"):
+            f = getattr(_lib, f"dpo_block_forward_{suf}")
+            f.restype = C.c_int
+            f.argtypes = [_I64] * 7 + [_P] * 5 + [C.c_int]
+            f = getattr(_lib, f"dpo_block_backward_{suf}")
+            f.restype = C.c_int
+            f.argtypes = [_I64] * 7 + [_P] * 6
+        _lib.dpo_fill_normal_f64.argtypes = [C.c_uint64, _P, _I64]
+        _lib.dpo_fill_normal_f32.argtypes = [C.c_uint64, _P, _I64]
+        _lib.dpo_rng_u64_fill.argtypes = [C.c_uint64, _P, _I64]
+    return _lib
+
+
+def ref_lib(fast: bool = False):
+    """The reference itself (oracle/_ref).  Raises if it was not built."""
+    path = REF_FAST_SO if fast else REF_SO
+    if path not in _ref:
+        if not os.path.exists(path):
+            raise FileNotFoundError(f"{path} not built (needs /root/reference; run make -C oracle ref)")
+        L = C.CDLL(path)
+        L.ref_last_error.restype = C.c_char_p
+        for suf in ("f32", "f64"):
+            f = getattr(L, f"ref_block_harness_{suf}")
+            f.restype = C.c_int
+            f.argtypes = [_I64] * 7 + [_P, _P, _P, C.c_int] + [_P] * 5
+            f = getattr(L, f"ref_check_block_harness_{suf}")
+            f.restype = C.c_int
+            f.argtypes = [C.c_int] * 6 + [C.c_uint64]
+        cfg = [C.c_int, _P, C.c_int, C.c_int, C.c_double, C.c_int, C.c_int]
+        L.ref_block_params_f32.restype = C.c_int
+        L.ref_block_params_f32.argtypes = cfg + [C.c_int] * 3 + [_I64, C.c_uint64, C.c_int, _P]
+        L.ref_model_step_f32.restype = C.c_int
+        L.ref_model_step_f32.argtypes = cfg + [C.c_int] * 3 + [_I64, C.c_uint64, C.c_int, _P, _P, _P]
+        L.ref_rng_normal.argtypes = [C.c_uint64, _I64, _P]
+        L.ref_rng_u64.argtypes = [C.c_uint64, _I64, _P]
+        L.ref_count_parameters.restype = C.c_int64
+        L.ref_count_parameters.argtypes = cfg + [C.c_int]
+        L.ref_predict_peak_elements.restype = C.c_int
+        L.ref_predict_peak_elements.argtypes = cfg + [C.c_int, _I64, C.c_int, C.c_int, C.c_int, _P]
+        _ref[path] = L
+    return _ref[path]
+
+
+# ---------------------------------------------------------------------------
+# flat layouts
+
+
+@dataclass(frozen=True)
+class BlockShape:
+    n: int
+    h: int
+    w: int
+    c0: int
+    m: int
+    k: int
+    bk: int
+
+    @property
+    def c_out(self) -> int:
+        return self.c0 + self.m * self.k
+
+    def c_in(self, l: int) -> int:
+        return self.c0 + l * self.k
+
+    def param_layer_size(self, l: int) -> int:
+        c = self.c_in(l)
+        return 2 * c + self.bk * c + 2 * self.bk + 9 * self.k * self.bk
+
+    def param_offsets(self) -> list[int]:
+        offs, o = [], 0
+        for l in range(self.m):
+            offs.append(o)
+            o += self.param_layer_size(l)
+        return offs
+
+    @property
+    def param_size(self) -> int:
+        return sum(self.param_layer_size(l) for l in range(self.m))
+
+    def stat_offsets(self) -> list[int]:
+        offs, o = [], 0
+        for l in range(self.m):
+            offs.append(o)
+            o += 2 * self.c_in(l) + 2 * self.bk
+        return offs
+
+    @property
+    def stat_size(self) -> int:
+        return sum(2 * self.c_in(l) + 2 * self.bk for l in range(self.m))
+
+    def split_params(self, flat: np.ndarray) -> list[dict]:
+        """Per-layer views {gamma_a, beta_a, w1, gamma_b, beta_b, w2}."""
+        out = []
+        for l, o in enumerate(self.param_offsets()):
+            c, bk, k = self.c_in(l), self.bk, self.k
+            d = {}
+            d["gamma_a"] = flat[o:o + c]; o += c
+            d["beta_a"] = flat[o:o + c]; o += c
+            d["w1"] = flat[o:o + bk * c].reshape(bk, c); o += bk * c
+            d["gamma_b"] = flat[o:o + bk]; o += bk
+            d["beta_b"] = flat[o:o + bk]; o += bk
+            d["w2"] = flat[o:o + 9 * k * bk].reshape(k, bk, 3, 3)
+            out.append(d)
+        return out
+
+    def split_stats(self, flat: np.ndarray) -> list[dict]:
+        out = []
+        for l, o in enumerate(self.stat_offsets()):
+            c, bk = self.c_in(l), self.bk
+            out.append({"mean_a": flat[o:o + c], "var_a": flat[o + c:o + 2 * c],
+                        "mean_b": flat[o + 2 * c:o + 2 * c + bk],
+                        "var_b": flat[o + 2 * c + bk:o + 2 * c + 2 * bk]})
+        return out
+
+    def initial_running(self, dtype) -> np.ndarray:
+        r = np.zeros(self.stat_size, dtype=dtype)
+        for l, o in enumerate(self.stat_offsets()):
+            c, bk = self.c_in(l), self.bk
+            r[o + c:o + 2 * c] = 1
+            r[o + 2 * c + bk:o + 2 * c + 2 * bk] = 1
+        return r
+
+
+def _suffix(dtype) -> str:
+    return "f32" if np.dtype(dtype) == np.float32 else "f64"
+
+
+def rng_normal(seed: int, count: int, dtype=np.float64) -> np.ndarray:
+    """Rng(seed).normal() x count (dp/rng.hpp:36-49), cast to dtype."""
+    out = np.empty(count, dtype=np.float64)
+    lib().dpo_fill_normal_f64(seed, _ptr(out), count)
+    return out.astype(dtype)
+
+
+def rng_u64(seed: int, count: int) -> np.ndarray:
+    """Raw std::mt19937_64 draws of the restated engine."""
+    out = np.empty(count, dtype=np.uint64)
+    lib().dpo_rng_u64_fill(seed, _ptr(out), count)
+    return out
+
+
+def ref_rng_normal(seed: int, count: int) -> np.ndarray:
+    out = np.empty(count, dtype=np.float64)
+    ref_lib().ref_rng_normal(seed, count, _ptr(out))
+    return out
+
+
+def ref_rng_u64(seed: int, count: int) -> np.ndarray:
+    out = np.empty(count, dtype=np.uint64)
+    ref_lib().ref_rng_u64(seed, count, _ptr(out))
+    return out
+
+
+def block_forward(s: BlockShape, params, x_in, running=None, update_running=True):
+    """Restated block forward.  Returns (feats, z, stats, running)."""
+    dt = params.dtype
+    feats = np.zeros((s.n, s.c_out, s.h, s.w), dtype=dt)
+    feats[:, :s.c0] = x_in
+    z = np.zeros((s.m, s.n, s.bk, s.h, s.w), dtype=dt)
+    stats = np.zeros(s.stat_size, dtype=dt)
+    run = s.initial_running(dt) if running is None else np.array(running, dtype=dt)
+    rc = getattr(lib(), f"dpo_block_forward_{_suffix(dt)}")(
+        s.n, s.h, s.w, s.c0, s.m, s.k, s.bk, _ptr(np.ascontiguousarray(params)),
+        _ptr(feats), _ptr(z), _ptr(stats), _ptr(run), int(update_running))
+    if rc != 0:
+        raise RuntimeError(f"oracle block_forward status {rc}")
+    return feats, z, stats, run
+
+
+def block_backward(s: BlockShape, params, feats, z, stats, acc):
+    """Restated block backward.  Returns (acc_out, grads)."""
+    dt = params.dtype
+    acc = np.array(acc, dtype=dt, order="C")
+    grads = np.zeros(s.param_size, dtype=dt)
+    rc = getattr(lib(), f"dpo_block_backward_{_suffix(dt)}")(
+        s.n, s.h, s.w, s.c0, s.m, s.k, s.bk, _ptr(np.ascontiguousarray(params)),
+        _ptr(np.ascontiguousarray(feats)), _ptr(np.ascontiguousarray(z)),
+        _ptr(np.ascontiguousarray(stats)), _ptr(acc), _ptr(grads))
+    if rc != 0:
+        raise RuntimeError(f"oracle block_backward status {rc}")
+    return acc, grads
+
+
+def ref_block(s: BlockShape, params, x_in, acc=None, running=None, update_running=True):
+    """The reference's own ops:: run through the block harness (oracle/_ref)."""
+    dt = params.dtype
+    L = ref_lib()
+    feats = np.zeros((s.n, s.c_out, s.h, s.w), dtype=dt)
+    z = np.zeros((s.m, s.n, s.bk, s.h, s.w), dtype=dt)
+    stats = np.zeros(s.stat_size, dtype=dt)
+    run = s.initial_running(dt) if running is None else np.array(running, dtype=dt)
+    grads = np.zeros(s.param_size, dtype=dt)
+    accv = None if acc is None else np.array(acc, dtype=dt, order="C")
+    rc = getattr(L, f"ref_block_harness_{_suffix(dt)}")(
+        s.n, s.h, s.w, s.c0, s.m, s.k, s.bk, _ptr(np.ascontiguousarray(params)),
+        _ptr(np.ascontiguousarray(x_in, dtype=dt)), _ptr(run), int(update_running),
+        _ptr(feats), _ptr(z), _ptr(stats), _ptr(accv), _ptr(grads))
+    if rc != 0:
+        raise RuntimeError(f"reference harness status {rc}: {L.ref_last_error().decode()}")
+    return feats, z, stats, run, accv, grads
+
+
+def random_block_params(s: BlockShape, seed: int, dtype=np.float32, perturb_bn=True) -> np.ndarray:
+    """He-normal conv weights in reference draw order, BN gamma/beta either
+    1/0 (reference init) or 1+0.5N / 0.5N (SURVEY §8(d) second parity case)."""
+    flat = np.zeros(s.param_size, dtype=np.float64)
+    draws = rng_normal(seed, 2 * s.param_size + 16)
+    di = 0
+    for l, o in enumerate(s.param_offsets()):
+        c, bk, k = s.c_in(l), s.bk, s.k
+        views = s.split_params(flat)[l]
+        if perturb_bn:
+            views["gamma_a"][:] = 1 + 0.5 * draws[di:di + c]; di += c
+            views["beta_a"][:] = 0.5 * draws[di:di + c]; di += c
+        else:
+            views["gamma_a"][:] = 1
+        views["w1"][:] = (draws[di:di + bk * c] * np.sqrt(2.0 / c)).reshape(bk, c); di += bk * c
+        if perturb_bn:
+            views["gamma_b"][:] = 1 + 0.5 * draws[di:di + bk]; di += bk
+            views["beta_b"][:] = 0.5 * draws[di:di + bk]; di += bk
+        else:
+            views["gamma_b"][:] = 1
+        views["w2"][:] = (draws[di:di + 9 * k * bk] * np.sqrt(2.0 / (9 * bk))).reshape(k, bk, 3, 3)
+        di += 9 * k * bk
+    return flat.astype(dtype)
+
+
+# ---------------------------------------------------------------------------
+# reference model-level helpers (need _ref)
+
+
+def _cfg_args(blocks, k, bottleneck, compression, classes, c0):
+    arr = (C.c_int * len(blocks))(*blocks)
+    return [len(blocks), C.cast(arr, _P), k, int(bottleneck), float(compression), classes, c0], arr
+
+
+def ref_count_parameters(blocks, k, bottleneck, compression, classes, c0, in_c=3) -> int:
+    args, keep = _cfg_args(blocks, k, bottleneck, compression, classes, c0)
+    return int(ref_lib().ref_count_parameters(*args, in_c))
+
+
+def ref_predict_peak_elements(blocks, k, bottleneck, compression, classes, c0,
+                              strategy, batch, in_c, in_h, in_w) -> list[int]:
+    args, keep = _cfg_args(blocks, k, bottleneck, compression, classes, c0)
+    out = np.zeros(6, dtype=np.int64)
+    rc = ref_lib().ref_predict_peak_elements(*args, strategy, batch, in_c, in_h, in_w, _ptr(out))
+    if rc != 0:
+        raise RuntimeError(ref_lib().ref_last_error().decode())
+    return [int(v) for v in out]
+
+
+def ref_block_params(blocks, k, bottleneck, compression, classes, c0, in_shape, seed, b) -> np.ndarray:
+    """Block b's flat params exactly as GraphPlan<float>::build draws them."""
+    args, keep = _cfg_args(blocks, k, bottleneck, compression, classes, c0)
+    n, c, h, w = in_shape
+    # size of block b
+    cin = c0
+    for bi, mb in enumerate(blocks):
+        if bi == b:
+            break
+        cin = int(np.floor(compression * (cin + mb * k)))
+    s = BlockShape(n, h, w, cin, blocks[b], k, 4 * k)
+    out = np.zeros(s.param_size, dtype=np.float32)
+    rc = ref_lib().ref_block_params_f32(*args, c, h, w, n, seed, b, _ptr(out))
+    if rc != 0:
+        raise RuntimeError(ref_lib().ref_last_error().decode())
+    return out
+
+
+def ref_model_step(blocks, k, bottleneck, compression, classes, c0, in_shape, seed,
+                   steps=1, fast=False):
+    """Times GraphPlan<float>::step_trace (the reference's public API).
+    Returns (loss, best_seconds)."""
+    args, keep = _cfg_args(blocks, k, bottleneck, compression, classes, c0)
+    n, c, h, w = in_shape
+    loss = C.c_double()
+    secs = C.c_double()
+    L = ref_lib(fast=fast)
+    rc = L.ref_model_step_f32(*args, c, h, w, n, seed, steps, C.byref(loss), C.byref(secs), None)
+    if rc != 0:
+        raise RuntimeError(L.ref_last_error().decode())
+    return loss.value, secs.value

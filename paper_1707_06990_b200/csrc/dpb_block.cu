@@ -1,0 +1,559 @@
+// Block plan, HBM arena and the forward/backward orchestration behind the
+// C ABI (include/dpb.h).
+//
+// Reference mapping (paths under /root/reference/proj/include/denseplan):
+//   plan_arena()        PoolRegion/GradPool/BufferPool sizing, graph.hpp:28-127,
+//                       :456-482, :602-609 — but Shared1/Shared2 are 0 here
+//   block_forward()     GraphPlan::forward layer loop, graph.hpp:747-760,
+//                       forward_layer :618-670
+//   block_backward()    backward_block :1054-1063 -> backward_layer :856-945
+//                       with rematerialize :831-854 folded into the kernels
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+#include <new>
+#include <string>
+
+#include "../../include/dpb.h"
+#include "dpb_common.cuh"
+#include "dpb_kernels.cuh"
+#include "dpb_simt.cuh"
+#include "dpb_internal.h"
+
+namespace dpb {
+
+thread_local std::string g_last_error;
+
+const char* const kKernelCatNames[KC_COUNT] = {
+    "pack", "channel_stats", "finalize", "conv1x1_fwd", "conv3x3_fwd", "conv3x3_dgrad",
+    "conv3x3_wgrad", "conv1x1_dgrad", "conv1x1_wgrad", "reduce_wgrad", "bn_apply_accumulate",
+    "running_update"};
+
+static cudaEvent_t next_event(Block* b) {
+  if (b->ev_used == b->ev_pool.size()) {
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    b->ev_pool.push_back(e);
+  }
+  return b->ev_pool[b->ev_used++];
+}
+
+LaunchScope::LaunchScope(Block* blk, int cat, double bytes, double flops) : b(blk) {
+  b->launches++;
+  if (!b->prof) return;
+  ProfRec r{cat, next_event(b), next_event(b), bytes, flops};
+  cudaEventRecord(r.start, b->stream);
+  idx = static_cast<int>(b->recs.size());
+  b->recs.push_back(r);
+}
+
+LaunchScope::~LaunchScope() {
+  if (idx >= 0) cudaEventRecord(b->recs[idx].stop, b->stream);
+}
+
+int fail(int code, const std::string& msg) {
+  g_last_error = msg;
+  return code;
+}
+
+int cuda_fail(cudaError_t e, const char* what) {
+  return fail(DPB_CUDA_ERROR, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+static int64_t align_up(int64_t v, int64_t a) { return (v + a - 1) / a * a; }
+
+int validate(const dpb_block_desc* d) {
+  if (d == nullptr) return fail(DPB_CONFIG_ERROR, "null descriptor");
+  if (d->n < 1 || d->h < 1 || d->w < 1 || d->c0 < 1 || d->m < 1 || d->k < 1 || d->bk < 1)
+    return fail(DPB_SHAPE_ERROR, "invalid block shape (every extent must be >= 1)");
+  if (d->dtype != DPB_FP32 && d->dtype != DPB_BF16)
+    return fail(DPB_CONFIG_ERROR, "dtype must be DPB_FP32 or DPB_BF16");
+  if (d->layout != DPB_NCHW && d->layout != DPB_NHWC)
+    return fail(DPB_CONFIG_ERROR, "layout must be DPB_NCHW or DPB_NHWC");
+  // Shape4::elems overflow guard (tensor.hpp:26-39): int64_max / 16
+  const unsigned __int128 lim = static_cast<unsigned __int128>(INT64_MAX / 16);
+  const int64_t C = static_cast<int64_t>(d->c0) + static_cast<int64_t>(d->m) * d->k;
+  unsigned __int128 p = static_cast<unsigned __int128>(d->n) * d->h;
+  p *= d->w;
+  if (p > lim) return fail(DPB_SIZE_OVERFLOW_ERROR, "pixel count overflows");
+  if (p * static_cast<unsigned __int128>(C) > lim ||
+      p * static_cast<unsigned __int128>(d->bk) * d->m > lim)
+    return fail(DPB_SIZE_OVERFLOW_ERROR, "block tensor overflows element count");
+  if (C > (1 << 20) || d->bk > (1 << 16))
+    return fail(DPB_CONFIG_ERROR, "channel count beyond supported range");
+  return DPB_OK;
+}
+
+Geometry geometry(const dpb_block_desc& d) {
+  Geometry g;
+  g.M = d.n * d.h * d.w;
+  g.C = d.c0 + d.m * d.k;
+  g.cmax = d.c0 + (d.m - 1) * d.k;
+  g.P = static_cast<int>((g.M + 127) / 128);
+  g.S = d.dtype == DPB_BF16 ? 2 : 4;
+  return g;
+}
+
+// Split-K choice for the weight-gradient GEMMs (K = pixels): aim for ~2 waves
+// of 148 SMs, at least 256 pixels per split.
+int64_t wgrad_chunk(int64_t M, int64_t tiles) {
+  int64_t splits = std::max<int64_t>(1, 296 / std::max<int64_t>(1, tiles));
+  splits = std::min<int64_t>(splits, std::max<int64_t>(1, M / 256));
+  int64_t chunk = (M + splits - 1) / splits;
+  chunk = align_up(chunk, kBK);
+  return chunk;
+}
+
+static int bn_tile(int64_t n) {
+  if (n <= 16) return 16;
+  if (n <= 32) return 32;
+  if (n <= 48) return 48;
+  return 64;
+}
+
+void plan_arena(const dpb_block_desc& d, dpb_arena_sizes* s) {
+  const Geometry g = geometry(d);
+  std::memset(s, 0, sizeof(*s));
+  int64_t off = 0;
+  auto take = [&](int64_t bytes, int64_t* o, int64_t* b) {
+    *o = off;
+    *b = bytes;
+    off = align_up(off + bytes, 256);
+  };
+  take(g.M * g.C * g.S, &s->feat_offset, &s->feat_bytes);
+  take(static_cast<int64_t>(d.m) * g.M * d.bk * g.S, &s->z_offset, &s->z_bytes);
+  take((2 * g.C + 2LL * d.m * d.bk) * 4, &s->stats_offset, &s->stats_bytes);
+  take(d.layout == DPB_NCHW ? g.M * g.C * 4 : 0, &s->acc_offset, &s->acc_bytes);
+  take(g.M * d.bk * 4, &s->g0_offset, &s->g0_bytes);
+  take(g.M * g.cmax * 4, &s->g1_offset, &s->g1_bytes);
+  // scratch: partials | wgrad partials | BN-backward coefficients
+  int64_t wmax = 0;
+  for (int l = 0; l < d.m; ++l) {
+    const int64_t c = d.c0 + static_cast<int64_t>(l) * d.k;
+    {
+      const int64_t rows = 9LL * d.bk, cols = d.k;
+      const int bn = bn_tile(cols);
+      const int64_t tiles = ((rows + 127) / 128) * ((cols + bn - 1) / bn);
+      const int64_t chunk = wgrad_chunk(g.M, tiles);
+      const int64_t splits = (g.M + chunk - 1) / chunk;
+      wmax = std::max(wmax, splits * rows * cols);
+    }
+    {
+      const int64_t rows = d.bk, cols = c;
+      const int64_t tiles = ((rows + 63) / 64) * ((cols + 63) / 64);
+      const int64_t chunk = wgrad_chunk(g.M, tiles);
+      const int64_t splits = (g.M + chunk - 1) / chunk;
+      wmax = std::max(wmax, splits * rows * cols);
+    }
+  }
+  const int64_t pbytes = static_cast<int64_t>(g.P) * std::max<int64_t>(g.C, d.bk) * 16;
+  const int64_t scratch = align_up(pbytes, 256) + align_up(wmax * 4, 256) +
+                          align_up((2LL * d.bk + 2 * g.cmax) * 4, 256);
+  take(scratch, &s->scratch_offset, &s->scratch_bytes);
+  s->total_bytes = off;
+  s->shared1_bytes = 0;
+  s->shared2_bytes = 0;
+  int64_t pe = 0, se = 0;
+  for (int l = 0; l < d.m; ++l) {
+    const int64_t c = d.c0 + static_cast<int64_t>(l) * d.k;
+    pe += 2 * c + d.bk * c + 2LL * d.bk + 9LL * d.k * d.bk;
+    se += 2 * c + 2LL * d.bk;
+  }
+  s->param_elems = pe;
+  s->stat_elems = se;
+}
+
+// --- launch helpers -----------------------------------------------------------
+
+template <int BM, int BN, class Op>
+static void launch_gemm(Block* b, const Op& op, dim3 grid, size_t dyn) {
+  static bool configured = false;  // per template instance
+  if (!configured) {
+    cudaFuncSetAttribute(gemm_kernel<BM, BN, Op>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         160 * 1024);
+    configured = true;
+  }
+  gemm_kernel<BM, BN, Op><<<grid, kThreads, dyn, b->stream>>>(op);
+}
+
+// Dispatch on the N tile for ops whose N is a runtime channel count.
+template <int BM, template <typename> class OpT, typename S>
+static void gemm_bn(Block* b, const LayerArgs<S>& a, int64_t rows, int64_t cols, int gz) {
+  OpT<S> op{a};
+  const size_t dyn = OpT<S>::smem(a);
+  const int bn = bn_tile(cols);
+  const dim3 grid(static_cast<unsigned>((rows + BM - 1) / BM),
+                  static_cast<unsigned>((cols + bn - 1) / bn), gz);
+  switch (bn) {
+    case 16: launch_gemm<BM, 16>(b, op, grid, dyn); break;
+    case 32: launch_gemm<BM, 32>(b, op, grid, dyn); break;
+    case 48: launch_gemm<BM, 48>(b, op, grid, dyn); break;
+    default: launch_gemm<BM, 64>(b, op, grid, dyn); break;
+  }
+}
+
+template <int BM, template <typename, int> class OpT, typename S>
+static void gemm_bn2(Block* b, const LayerArgs<S>& a, int64_t rows, int64_t cols, int gz) {
+  const int bn = bn_tile(cols);
+  const unsigned gx = static_cast<unsigned>((rows + BM - 1) / BM);
+  const unsigned gy = static_cast<unsigned>((cols + bn - 1) / bn);
+  switch (bn) {
+    case 16: launch_gemm<BM, 16>(b, OpT<S, 16>{a}, dim3(gx, gy, gz), OpT<S, 16>::smem(a)); break;
+    case 32: launch_gemm<BM, 32>(b, OpT<S, 32>{a}, dim3(gx, gy, gz), OpT<S, 32>::smem(a)); break;
+    case 48: launch_gemm<BM, 48>(b, OpT<S, 48>{a}, dim3(gx, gy, gz), OpT<S, 48>::smem(a)); break;
+    default: launch_gemm<BM, 64>(b, OpT<S, 64>{a}, dim3(gx, gy, gz), OpT<S, 64>::smem(a)); break;
+  }
+}
+
+static unsigned blocks_for(int64_t n, int t) { return static_cast<unsigned>((n + t - 1) / t); }
+
+template <typename S>
+static LayerArgs<S> layer_args(Block* b, const float* params, int l) {
+  const dpb_block_desc& d = b->d;
+  const Geometry& g = b->g;
+  LayerArgs<S> a{};
+  a.M = g.M;
+  a.H = static_cast<int>(d.h);
+  a.W = static_cast<int>(d.w);
+  a.C = static_cast<int>(g.C);
+  a.c = d.c0 + l * d.k;
+  a.bk = d.bk;
+  a.k = d.k;
+  a.feat = static_cast<S*>(b->feat);
+  a.z = static_cast<S*>(b->z) + static_cast<int64_t>(l) * g.M * d.bk;
+  const float* p = params + b->param_off[l];
+  a.gamma_a = p;
+  a.beta_a = p + a.c;
+  a.w1 = p + 2 * a.c;
+  a.gamma_b = a.w1 + static_cast<int64_t>(d.bk) * a.c;
+  a.beta_b = a.gamma_b + d.bk;
+  a.w2 = a.beta_b + d.bk;
+  a.amean = b->fstat;
+  a.avar = b->fstat + g.C;
+  a.bmean = b->zstat + static_cast<int64_t>(l) * 2 * d.bk;
+  a.bvar = a.bmean + d.bk;
+  a.acc = b->acc_cur;
+  a.g0 = b->g0;
+  a.g1 = b->g1;
+  a.bnb_bwd = b->bnb_bwd;
+  a.part = b->part;
+  a.wpart = b->wpart;
+  return a;
+}
+
+template <typename S>
+static void forward_impl(Block* b, const float* x_in, const float* params, float* running,
+                         int update_running, int eval) {
+  const dpb_block_desc& d = b->d;
+  const Geometry& g = b->g;
+  S* feat = static_cast<S*>(b->feat);
+  const int64_t hw = d.h * d.w;
+  const double M = static_cast<double>(g.M), Sb = g.S;
+  // block input -> channels [0, c0) of the feature buffer (zero-copy concat)
+  {
+    LaunchScope ls(b, KC_PACK, M * d.c0 * (4 + Sb), 0);
+    if (d.layout == DPB_NCHW) {
+      dim3 grid(blocks_for(hw, 32), blocks_for(d.c0, 32), static_cast<unsigned>(d.n));
+      k_nchw_to_nhwc<S><<<grid, dim3(32, 8), 0, b->stream>>>(x_in, d.n, d.c0, hw, feat,
+                                                             static_cast<int>(g.C), 0);
+    } else {
+      k_nhwc_copy<S><<<blocks_for(g.M * d.c0, 256), 256, 0, b->stream>>>(
+          x_in, d.c0, g.M, d.c0, feat, static_cast<int>(g.C), 0);
+    }
+  }
+  const double count = M;
+  float* fmean = b->fstat;
+  float* fvar = b->fstat + g.C;
+  if (!eval) {
+    {
+      LaunchScope ls(b, KC_STATS, M * d.c0 * Sb, 0);
+      k_channel_partials<S><<<g.P, 256, 0, b->stream>>>(feat, static_cast<int>(g.C), 0, g.M,
+                                                        d.c0, b->part);
+    }
+    LaunchScope ls(b, KC_FINALIZE, 0, 0);
+    k_finalize_stats<<<blocks_for(32LL * d.c0, 256), 256, 0, b->stream>>>(
+        b->part, g.P, d.c0, count, fmean, fvar, 0);
+  }
+  for (int l = 0; l < d.m; ++l) {
+    LayerArgs<S> a = layer_args<S>(b, params, l);
+    if (eval) {
+      // every BN normalises with its own running statistics (ops.hpp:196-199)
+      const float* r = running + b->stat_off[l];
+      a.amean = r;
+      a.avar = r + a.c;
+      a.bmean = r + 2 * a.c;
+      a.bvar = r + 2 * a.c + d.bk;
+    }
+    {
+      LaunchScope ls(b, KC_C1_FWD, M * (a.c + d.bk) * Sb, 2.0 * M * a.c * d.bk);
+      gemm_bn<128, Conv1x1Fwd>(b, a, g.M, d.bk, 1);
+    }
+    if (!eval) {
+      LaunchScope ls(b, KC_FINALIZE, 0, 0);
+      float* zm = b->zstat + static_cast<int64_t>(l) * 2 * d.bk;
+      k_finalize_stats<<<blocks_for(32LL * d.bk, 256), 256, 0, b->stream>>>(
+          b->part, g.P, d.bk, count, zm, zm + d.bk, 0);
+    }
+    {
+      LaunchScope ls(b, KC_C3_FWD, M * (d.bk + d.k) * Sb, 2.0 * M * 9 * d.bk * d.k);
+      gemm_bn<128, Conv3x3Fwd>(b, a, g.M, d.k, 1);
+    }
+    if (!eval) {
+      LaunchScope ls(b, KC_FINALIZE, 0, 0);
+      k_finalize_stats<<<blocks_for(32LL * d.k, 256), 256, 0, b->stream>>>(
+          b->part, g.P, d.k, count, fmean, fvar, a.c);
+    }
+  }
+  if (!eval && update_running) {
+    LaunchScope ls(b, KC_RUNNING, 0, 0);
+    k_running_update<<<blocks_for(b->sz.stat_elems, 256), 256, 0, b->stream>>>(
+        d.m, d.c0, d.k, d.bk, static_cast<int>(g.C), b->fstat, b->zstat, running,
+        b->sz.stat_elems);
+  }
+}
+
+template <typename S>
+static void backward_impl(Block* b, const float* params, float* grad_acc, float* grads) {
+  const dpb_block_desc& d = b->d;
+  const Geometry& g = b->g;
+  const int64_t hw = d.h * d.w;
+  const double M = static_cast<double>(g.M), Sb = g.S;
+  const double count = M;
+  if (d.layout == DPB_NCHW) {
+    LaunchScope ls(b, KC_PACK, M * g.C * 8, 0);
+    b->acc_cur = b->acc;
+    dim3 grid(blocks_for(hw, 32), blocks_for(g.C, 32), static_cast<unsigned>(d.n));
+    k_nchw_to_nhwc<float><<<grid, dim3(32, 8), 0, b->stream>>>(grad_acc, d.n, g.C, hw,
+                                                               b->acc, static_cast<int>(g.C), 0);
+  } else {
+    b->acc_cur = grad_acc;
+  }
+  for (int l = d.m - 1; l >= 0; --l) {
+    LayerArgs<S> a = layer_args<S>(b, params, l);
+    float* gl = grads + b->param_off[l];
+    float* d_ga = gl;
+    float* d_ba = gl + a.c;
+    float* d_w1 = gl + 2 * a.c;
+    float* d_gb = d_w1 + static_cast<int64_t>(d.bk) * a.c;
+    float* d_bb = d_gb + d.bk;
+    float* d_w2 = d_bb + d.bk;
+    const double f3 = 2.0 * M * 9 * d.bk * d.k, f1 = 2.0 * M * a.c * d.bk;
+    // 3x3: dgrad (+ReLU mask by act_b, BN_b sums) and wgrad (graph.hpp:905-910)
+    {
+      LaunchScope ls(b, KC_C3_DGRAD, M * (4.0 * d.k + Sb * d.bk + 4.0 * d.bk), f3);
+      gemm_bn<128, Conv3x3Dgrad>(b, a, g.M, d.bk, 1);
+    }
+    {
+      const int64_t rows = 9LL * d.bk;
+      const int bn = bn_tile(d.k);
+      const int64_t tiles = ((rows + 127) / 128) * ((d.k + bn - 1) / bn);
+      a.kchunk = wgrad_chunk(g.M, tiles);
+      const int splits = static_cast<int>((g.M + a.kchunk - 1) / a.kchunk);
+      {
+        LaunchScope ls(b, KC_C3_WGRAD, M * (4.0 * d.k + Sb * d.bk), f3);
+        gemm_bn<128, Conv3x3Wgrad>(b, a, rows, d.k, splits);
+      }
+      LaunchScope ls(b, KC_REDUCE_W, 4.0 * splits * rows * d.k, 0);
+      k_reduce_w2<<<blocks_for(9LL * d.k * d.bk, 256), 256, 0, b->stream>>>(
+          b->wpart, splits, d.bk, d.k, d_w2);
+    }
+    // BN_b backward sums -> dgamma_b, dbeta_b, coefficients (graph.hpp:913-916)
+    {
+      LaunchScope ls(b, KC_FINALIZE, 0, 0);
+      k_finalize_bn_bwd<<<blocks_for(32LL * d.bk, 256), 256, 0, b->stream>>>(
+          b->part, g.P, d.bk, count, d_gb, d_bb, b->bnb_bwd);
+    }
+    // 1x1: dgrad (+ReLU mask by act_a, BN_a sums) and wgrad (graph.hpp:920-926)
+    {
+      LaunchScope ls(b, KC_C1_DGRAD, M * ((4.0 + Sb) * d.bk + (Sb + 4.0) * a.c), f1);
+      gemm_bn2<128, Conv1x1Dgrad>(b, a, g.M, a.c, 1);
+    }
+    {
+      const int64_t tiles = ((d.bk + 63) / 64) * ((a.c + 63) / 64);
+      a.kchunk = wgrad_chunk(g.M, tiles);
+      const int splits = static_cast<int>((g.M + a.kchunk - 1) / a.kchunk);
+      {
+        LaunchScope ls(b, KC_C1_WGRAD, M * ((4.0 + Sb) * d.bk + Sb * a.c), f1);
+        gemm_bn2<64, Conv1x1Wgrad>(b, a, d.bk, a.c, splits);
+      }
+      LaunchScope ls(b, KC_REDUCE_W, 4.0 * splits * d.bk * a.c, 0);
+      k_reduce_w1<<<blocks_for(static_cast<int64_t>(d.bk) * a.c, 256), 256, 0, b->stream>>>(
+          b->wpart, splits, d.bk, a.c, d_w1);
+    }
+    // BN_a backward (graph.hpp:929-932) + concat-backward accumulate (:936-941)
+    {
+      LaunchScope ls(b, KC_FINALIZE, 0, 0);
+      k_finalize_bn_bwd<<<blocks_for(32LL * a.c, 256), 256, 0, b->stream>>>(
+          b->part, g.P, a.c, count, d_ga, d_ba, b->bna_bwd);
+    }
+    {
+      LaunchScope ls(b, KC_BN_APPLY_ACC, M * a.c * (4.0 + Sb + 8.0), 0);
+      k_bn_apply_accumulate<S><<<blocks_for(g.M * a.c, 256), 256, 0, b->stream>>>(
+          g.M, a.c, static_cast<int>(g.C), static_cast<const S*>(b->feat), b->g1, a.amean,
+          a.avar, a.gamma_a, b->bna_bwd, b->acc_cur);
+    }
+  }
+  if (d.layout == DPB_NCHW) {
+    LaunchScope ls(b, KC_PACK, M * g.C * 8, 0);
+    dim3 grid(blocks_for(hw, 32), blocks_for(g.C, 32), static_cast<unsigned>(d.n));
+    k_nhwc_to_nchw<float><<<grid, dim3(32, 8), 0, b->stream>>>(b->acc, static_cast<int>(g.C), 0,
+                                                               d.n, g.C, hw, grad_acc);
+  }
+}
+
+int block_forward(Block* b, const float* x_in, const float* params, float* running,
+                  int update_running, int eval) {
+  if (b->g.M < 2 && !eval)
+    return fail(DPB_DEGENERATE_BATCH_ERROR,
+                "train-mode batchnorm needs at least 2 values per channel");
+  if (eval && running == nullptr) return fail(DPB_CONFIG_ERROR, "eval needs running stats");
+  b->launches = 0;
+  if (b->d.dtype == DPB_BF16)
+    forward_impl<__nv_bfloat16>(b, x_in, params, running, update_running, eval);
+  else
+    forward_impl<float>(b, x_in, params, running, update_running, eval);
+  const cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return cuda_fail(e, "block forward launch");
+  b->fwd_done = !eval;
+  return DPB_OK;
+}
+
+int block_backward(Block* b, const float* params, float* grad_acc, float* grads) {
+  if (!b->fwd_done)
+    return fail(DPB_PROTOCOL_ERROR, "backward requires a train-mode forward");
+  b->launches = 0;
+  if (b->d.dtype == DPB_BF16)
+    backward_impl<__nv_bfloat16>(b, params, grad_acc, grads);
+  else
+    backward_impl<float>(b, params, grad_acc, grads);
+  const cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return cuda_fail(e, "block backward launch");
+  return DPB_OK;
+}
+
+template <typename S>
+static void read_feats_impl(Block* b, float* dst) {
+  const dim3 grid(blocks_for(b->d.h * b->d.w, 32), blocks_for(b->g.C, 32),
+                  static_cast<unsigned>(b->d.n));
+  k_nhwc_to_nchw<S><<<grid, dim3(32, 8), 0, b->stream>>>(
+      static_cast<const S*>(b->feat), static_cast<int>(b->g.C), 0, b->d.n,
+      static_cast<int>(b->g.C), b->d.h * b->d.w, dst);
+}
+
+template <typename S>
+static void read_z_impl(Block* b, float* dst) {
+  const int64_t hw = b->d.h * b->d.w;
+  const dim3 grid(blocks_for(hw, 32), blocks_for(b->d.bk, 32), static_cast<unsigned>(b->d.n));
+  for (int l = 0; l < b->d.m; ++l)
+    k_nhwc_to_nchw<S><<<grid, dim3(32, 8), 0, b->stream>>>(
+        static_cast<const S*>(b->z) + static_cast<int64_t>(l) * b->g.M * b->d.bk, b->d.bk, 0,
+        b->d.n, b->d.bk, hw, dst + static_cast<int64_t>(l) * b->g.M * b->d.bk);
+}
+
+int read_feats(Block* b, float* dst) {
+  if (b->d.dtype == DPB_BF16) read_feats_impl<__nv_bfloat16>(b, dst);
+  else read_feats_impl<float>(b, dst);
+  const cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? DPB_OK : cuda_fail(e, "read_feats");
+}
+
+int read_z(Block* b, float* dst) {
+  if (b->d.dtype == DPB_BF16) read_z_impl<__nv_bfloat16>(b, dst);
+  else read_z_impl<float>(b, dst);
+  const cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? DPB_OK : cuda_fail(e, "read_z");
+}
+
+int read_stats(Block* b, float* dst) {
+  k_export_stats<<<blocks_for(b->sz.stat_elems, 256), 256, 0, b->stream>>>(
+      b->d.m, b->d.c0, b->d.k, b->d.bk, static_cast<int>(b->g.C), b->fstat, b->zstat, dst,
+      b->sz.stat_elems);
+  const cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? DPB_OK : cuda_fail(e, "read_stats");
+}
+
+int create(const dpb_block_desc* desc, int device, void* stream, Block** out) {
+  int rc = validate(desc);
+  if (rc) return rc;
+  if (out == nullptr) return fail(DPB_CONFIG_ERROR, "null output handle");
+  cudaError_t e = cudaSetDevice(device);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaSetDevice");
+  Block* b = new (std::nothrow) Block();
+  if (!b) return fail(DPB_CAPACITY_ERROR, "host allocation failed");
+  b->d = *desc;
+  b->device = device;
+  b->stream = static_cast<cudaStream_t>(stream);
+  b->g = geometry(*desc);
+  plan_arena(*desc, &b->sz);
+  e = cudaMalloc(&b->arena, static_cast<size_t>(b->sz.total_bytes));
+  if (e != cudaSuccess) {
+    delete b;
+    return cuda_fail(e, "arena cudaMalloc");
+  }
+  char* base = static_cast<char*>(b->arena);
+  b->feat = base + b->sz.feat_offset;
+  b->z = base + b->sz.z_offset;
+  b->fstat = reinterpret_cast<float*>(base + b->sz.stats_offset);
+  b->zstat = b->fstat + 2 * b->g.C;
+  b->acc = reinterpret_cast<float*>(base + b->sz.acc_offset);
+  b->g0 = reinterpret_cast<float*>(base + b->sz.g0_offset);
+  b->g1 = reinterpret_cast<float*>(base + b->sz.g1_offset);
+  char* sc = base + b->sz.scratch_offset;
+  b->part = reinterpret_cast<double2*>(sc);
+  const int64_t pbytes =
+      align_up(static_cast<int64_t>(b->g.P) * std::max<int64_t>(b->g.C, desc->bk) * 16, 256);
+  b->wpart = reinterpret_cast<float*>(sc + pbytes);
+  // wgrad partial region size = scratch - pbytes - coef region
+  const int64_t coef_bytes = align_up((2LL * desc->bk + 2 * b->g.cmax) * 4, 256);
+  b->bnb_bwd = reinterpret_cast<float*>(sc + b->sz.scratch_bytes - coef_bytes);
+  b->bna_bwd = b->bnb_bwd + 2 * desc->bk;
+  int64_t po = 0, so = 0;
+  for (int l = 0; l < desc->m; ++l) {
+    const int64_t c = desc->c0 + static_cast<int64_t>(l) * desc->k;
+    b->param_off.push_back(po);
+    b->stat_off.push_back(so);
+    po += 2 * c + desc->bk * c + 2LL * desc->bk + 9LL * desc->k * desc->bk;
+    so += 2 * c + 2LL * desc->bk;
+  }
+  *out = b;
+  return DPB_OK;
+}
+
+void destroy(Block* b) {
+  if (!b) return;
+  if (b->arena) cudaFree(b->arena);
+  for (cudaEvent_t e : b->ev_pool) cudaEventDestroy(e);
+  delete b;
+}
+
+void profile_enable(Block* b, int on) {
+  b->prof = on != 0;
+  b->recs.clear();
+  b->ev_used = 0;
+}
+
+int profile_read(Block* b, dpb_kernel_stat* out, int max, int* count) {
+  const cudaError_t e = cudaStreamSynchronize(b->stream);
+  if (e != cudaSuccess) return cuda_fail(e, "profile sync");
+  dpb_kernel_stat acc[KC_COUNT];
+  std::memset(acc, 0, sizeof(acc));
+  for (int c = 0; c < KC_COUNT; ++c)
+    std::snprintf(acc[c].name, sizeof(acc[c].name), "%s", kKernelCatNames[c]);
+  for (const ProfRec& r : b->recs) {
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, r.start, r.stop);
+    acc[r.cat].launches++;
+    acc[r.cat].total_ms += ms;
+    acc[r.cat].bytes += r.bytes;
+    acc[r.cat].flops += r.flops;
+  }
+  int n = 0;
+  for (int c = 0; c < KC_COUNT && n < max; ++c)
+    if (acc[c].launches) out[n++] = acc[c];
+  *count = n;
+  return DPB_OK;
+}
+
+}  // namespace dpb

@@ -1,0 +1,43 @@
+// Shared device helpers for the dense-block kernels.
+#pragma once
+
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace dpb {
+
+constexpr float kEps = 1e-5f;       // BatchNormState::eps, ops.hpp:22
+constexpr float kMomentum = 0.1f;   // BatchNormState::momentum, ops.hpp:23
+
+__device__ __forceinline__ float to_f(float v) { return v; }
+__device__ __forceinline__ float to_f(__nv_bfloat16 v) { return __bfloat162float(v); }
+
+template <typename S>
+__device__ __forceinline__ S from_f(float v);
+template <>
+__device__ __forceinline__ float from_f<float>(float v) { return v; }
+template <>
+__device__ __forceinline__ __nv_bfloat16 from_f<__nv_bfloat16>(float v) {
+  return __float2bfloat16_rn(v);
+}
+
+// 1 / sqrt(var + eps) evaluated like the reference: T(1) / std::sqrt(v + eps)
+// (ops.hpp:124, :219).  IEEE sqrt and division (no fast-math).
+__device__ __forceinline__ float bn_inv(float var) {
+  return __fdiv_rn(1.0f, __fsqrt_rn(__fadd_rn(var, kEps)));
+}
+
+// Per-channel BN forward transform kept in shared memory by the kernels that
+// recompute BN+ReLU in their prologue: y = (x - mean) * (gamma*inv) + beta.
+struct BnFwd {
+  float mean, scale, beta, inv;
+};
+
+// BN backward coefficients of one channel (ops.hpp:206-243):
+//   gx = (gamma*inv) * (g - mg - xhat * mgx),   xhat = (x - mean) * inv
+struct BnBwd {
+  float mean, inv, ginv, mg, mgx;
+};
+
+}  // namespace dpb

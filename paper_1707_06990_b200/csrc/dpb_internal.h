@@ -1,0 +1,90 @@
+// Internal host-side types shared by the C-ABI translation units.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "../../include/dpb.h"
+
+namespace dpb {
+
+struct Geometry {
+  int64_t M = 0;     // pixels N*H*W
+  int64_t C = 0;     // block output channels c0 + m*k (feature pitch)
+  int64_t cmax = 0;  // widest layer input c0 + (m-1)*k
+  int P = 0;         // row CTAs of 128 pixels = partial-sum count
+  int S = 4;         // bytes per stored feature element
+};
+
+// Kernel categories for the optional per-launch profiler (bench.py roofline).
+enum KernelCat {
+  KC_PACK = 0, KC_STATS, KC_FINALIZE, KC_C1_FWD, KC_C3_FWD, KC_C3_DGRAD, KC_C3_WGRAD,
+  KC_C1_DGRAD, KC_C1_WGRAD, KC_REDUCE_W, KC_BN_APPLY_ACC, KC_RUNNING, KC_COUNT
+};
+extern const char* const kKernelCatNames[KC_COUNT];
+
+struct ProfRec {
+  int cat;
+  cudaEvent_t start, stop;
+  double bytes, flops;
+};
+
+struct Block {
+  dpb_block_desc d{};
+  Geometry g;
+  dpb_arena_sizes sz{};
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  void* arena = nullptr;
+  void* feat = nullptr;      // [M, C] S
+  void* z = nullptr;         // m x [M, bk] S
+  float* fstat = nullptr;    // mean[C] | var[C]
+  float* zstat = nullptr;    // per layer mean[bk] | var[bk]
+  float* acc = nullptr;      // [M, C] fp32 (NCHW boundary only)
+  float* acc_cur = nullptr;  // the accumulator in use (arena or caller NHWC)
+  float* g0 = nullptr;       // [M, bk] fp32
+  float* g1 = nullptr;       // [M, cmax] fp32
+  double2* part = nullptr;   // per-CTA partial sums
+  float* wpart = nullptr;    // split-K weight-gradient partials
+  float* bnb_bwd = nullptr;  // [bk][2]
+  float* bna_bwd = nullptr;  // [cmax][2]
+  std::vector<int64_t> param_off, stat_off;
+  bool fwd_done = false;
+  int64_t launches = 0;
+  bool prof = false;
+  std::vector<ProfRec> recs;          // recorded launches (profiling on)
+  std::vector<cudaEvent_t> ev_pool;   // reusable events
+  size_t ev_used = 0;
+};
+
+// Counts one kernel launch; when profiling is on, brackets it with CUDA
+// events on the block's stream and records its algorithmic bytes / flops.
+struct LaunchScope {
+  Block* b;
+  int idx = -1;
+  LaunchScope(Block* blk, int cat, double bytes, double flops);
+  ~LaunchScope();
+};
+
+extern thread_local std::string g_last_error;
+int fail(int code, const std::string& msg);
+int cuda_fail(cudaError_t e, const char* what);
+int validate(const dpb_block_desc* d);
+Geometry geometry(const dpb_block_desc& d);
+void plan_arena(const dpb_block_desc& d, dpb_arena_sizes* s);
+int create(const dpb_block_desc* desc, int device, void* stream, Block** out);
+void destroy(Block* b);
+int block_forward(Block* b, const float* x_in, const float* params, float* running,
+                  int update_running, int eval);
+int block_backward(Block* b, const float* params, float* grad_acc, float* grads);
+int read_feats(Block* b, float* dst);
+int read_z(Block* b, float* dst);
+int read_stats(Block* b, float* dst);
+void profile_enable(Block* b, int on);
+int profile_read(Block* b, dpb_kernel_stat* out, int max, int* count);
+
+}  // namespace dpb
+

@@ -1,0 +1,244 @@
+// Elementwise / reduction kernels of the dense block (HBM-bound work).
+#pragma once
+
+#include "dpb_common.cuh"
+
+namespace dpb {
+
+// --- layout conversion at the reference-facing boundary ----------------------
+// NCHW fp32 [n, c, h, w] (sample stride c*h*w) <-> NHWC rows of pitch P at
+// channel offset c_off.  32x32 shared-memory transpose tiles: coalesced on
+// both sides.
+template <typename S>
+__global__ void k_nchw_to_nhwc(const float* __restrict__ src, int64_t n, int c,
+                               int64_t hw, S* __restrict__ dst, int pitch,
+                               int c_off) {
+  __shared__ float tile[32][33];
+  const int64_t img = blockIdx.z;
+  const int64_t p0 = static_cast<int64_t>(blockIdx.x) * 32;
+  const int c0 = blockIdx.y * 32;
+  for (int r = threadIdx.y; r < 32; r += blockDim.y) {
+    const int ch = c0 + r;
+    const int64_t p = p0 + threadIdx.x;
+    if (ch < c && p < hw) tile[r][threadIdx.x] = src[(img * c + ch) * hw + p];
+  }
+  __syncthreads();
+  for (int r = threadIdx.y; r < 32; r += blockDim.y) {
+    const int64_t p = p0 + r;
+    const int ch = c0 + threadIdx.x;
+    if (ch < c && p < hw) dst[(img * hw + p) * pitch + c_off + ch] = from_f<S>(tile[threadIdx.x][r]);
+  }
+}
+
+template <typename S>
+__global__ void k_nhwc_to_nchw(const S* __restrict__ src, int pitch, int c_off,
+                               int64_t n, int c, int64_t hw,
+                               float* __restrict__ dst) {
+  __shared__ float tile[32][33];
+  const int64_t img = blockIdx.z;
+  const int64_t p0 = static_cast<int64_t>(blockIdx.x) * 32;
+  const int c0 = blockIdx.y * 32;
+  for (int r = threadIdx.y; r < 32; r += blockDim.y) {
+    const int64_t p = p0 + r;
+    const int ch = c0 + threadIdx.x;
+    if (ch < c && p < hw) tile[threadIdx.x][r] = to_f(src[(img * hw + p) * pitch + c_off + ch]);
+  }
+  __syncthreads();
+  for (int r = threadIdx.y; r < 32; r += blockDim.y) {
+    const int ch = c0 + r;
+    const int64_t p = p0 + threadIdx.x;
+    if (ch < c && p < hw) dst[(img * c + ch) * hw + p] = tile[r][threadIdx.x];
+  }
+}
+
+// NHWC strided copy (c channels of pitch sp at offset so) -> (pitch dp, off do)
+template <typename S>
+__global__ void k_nhwc_copy(const float* __restrict__ src, int sp, int64_t M, int c,
+                            S* __restrict__ dst, int dp, int d_off) {
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= M * c) return;
+  const int64_t p = i / c;
+  const int ch = static_cast<int>(i - p * c);
+  dst[p * dp + d_off + ch] = from_f<S>(src[p * sp + ch]);
+}
+
+// --- per-channel partial sums over rows of an NHWC buffer -------------------
+// grid.x = ceil(M / 128) CTAs (the same partial count as the GEMM epilogues);
+// 256 threads = 8 row groups x 32 channel lanes.  Writes part[cta][ch] =
+// {sum x, sum x^2} in fp64.
+template <typename S>
+__global__ void __launch_bounds__(256)
+k_channel_partials(const S* __restrict__ src, int pitch, int c_off, int64_t M,
+                   int nch, double2* __restrict__ part) {
+  __shared__ double r1[8][33], r2[8][33];
+  const int lane = threadIdx.x % 32, grp = threadIdx.x / 32;
+  const int64_t m0 = static_cast<int64_t>(blockIdx.x) * 128;
+  for (int cb = 0; cb < nch; cb += 32) {
+    const int ch = cb + lane;
+    double s1 = 0.0, s2 = 0.0;
+    if (ch < nch) {
+      for (int r = grp; r < 128; r += 8) {
+        const int64_t m = m0 + r;
+        if (m >= M) break;
+        const double v = to_f(src[m * pitch + c_off + ch]);
+        s1 += v;
+        s2 += v * v;
+      }
+    }
+    r1[grp][lane] = s1;
+    r2[grp][lane] = s2;
+    __syncthreads();
+    if (grp == 0 && ch < nch) {
+      double a = 0.0, b = 0.0;
+      for (int g = 0; g < 8; ++g) { a += r1[g][lane]; b += r2[g][lane]; }
+      part[static_cast<int64_t>(blockIdx.x) * nch + ch] = make_double2(a, b);
+    }
+    __syncthreads();
+  }
+}
+
+// Fixed-order fold of P partials for nch channels: one warp per channel, lane
+// l sums p = l, l+32, ..., then a fixed butterfly.  Deterministic.
+__device__ __forceinline__ double2 fold_partials(const double2* part, int P, int nch,
+                                                 int ch) {
+  const int lane = threadIdx.x % 32;
+  double a = 0.0, b = 0.0;
+  for (int p = lane; p < P; p += 32) {
+    const double2 v = part[static_cast<int64_t>(p) * nch + ch];
+    a += v.x;
+    b += v.y;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    a += __shfl_xor_sync(0xffffffffu, a, o);
+    b += __shfl_xor_sync(0xffffffffu, b, o);
+  }
+  return make_double2(a, b);
+}
+
+// Forward statistics: mean = S1/count, biased var = S2/count - mean^2
+// (ops.hpp:138-162 semantics) -> mean_out[first+ch], var_out[first+ch].
+__global__ void k_finalize_stats(const double2* __restrict__ part, int P, int nch,
+                                 double count, float* __restrict__ mean_out,
+                                 float* __restrict__ var_out, int first) {
+  const int ch = (blockIdx.x * blockDim.x + threadIdx.x) / 32;
+  if (ch >= nch) return;
+  const double2 s = fold_partials(part, P, nch, ch);
+  if (threadIdx.x % 32 == 0) {
+    const double mean = s.x / count;
+    double var = s.y / count - mean * mean;
+    if (var < 0.0) var = 0.0;
+    mean_out[first + ch] = static_cast<float>(mean);
+    var_out[first + ch] = static_cast<float>(var);
+  }
+}
+
+// BN backward sums -> dgamma = sum g*xhat, dbeta = sum g (written, ops.hpp:229-230)
+// and the apply coefficients coef[2*ch] = mg, [2*ch+1] = mgx.
+__global__ void k_finalize_bn_bwd(const double2* __restrict__ part, int P, int nch,
+                                  double count, float* __restrict__ dgamma,
+                                  float* __restrict__ dbeta, float* __restrict__ coef) {
+  const int ch = (blockIdx.x * blockDim.x + threadIdx.x) / 32;
+  if (ch >= nch) return;
+  const double2 s = fold_partials(part, P, nch, ch);
+  if (threadIdx.x % 32 == 0) {
+    const float sum_g = static_cast<float>(s.x);
+    const float sum_gx = static_cast<float>(s.y);
+    dgamma[ch] = sum_gx;
+    dbeta[ch] = sum_g;
+    coef[2 * ch] = static_cast<float>(s.x / count);
+    coef[2 * ch + 1] = static_cast<float>(s.y / count);
+  }
+}
+
+// acc[:, 0:c] += (gamma*inv) * (t2 - mg - xhat*mgx)   (BN_a backward apply fused
+// with the concat-backward accumulate, graph.hpp:929-941).  HBM-bound: reads
+// t2 (fp32) and x, read-modify-writes acc.  One thread per 4 channels.
+template <typename S>
+__global__ void __launch_bounds__(256)
+k_bn_apply_accumulate(int64_t M, int c, int C, const S* __restrict__ feat,
+                      const float* __restrict__ g1, const float* __restrict__ amean,
+                      const float* __restrict__ avar,
+                      const float* __restrict__ gamma, const float* __restrict__ coef,
+                      float* __restrict__ acc) {
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= M * c) return;
+  const int64_t p = i / c;
+  const int ch = static_cast<int>(i - p * c);
+  const float mean = amean[ch];
+  const float inv = bn_inv(avar[ch]);
+  const float xh = (to_f(feat[p * C + ch]) - mean) * inv;
+  const float g = g1[i];
+  acc[p * C + ch] += gamma[ch] * inv * (g - coef[2 * ch] - xh * coef[2 * ch + 1]);
+}
+
+// Split-K weight-gradient fold: out = sum over splits in order.
+// dW2: partial row r = tap*bk + j, col o -> flat W2[o][j][tap]
+__global__ void k_reduce_w2(const float* __restrict__ wpart, int splits, int bk, int k,
+                            float* __restrict__ dw2) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;  // flat (o, j, tap)
+  if (i >= k * bk * 9) return;
+  const int tap = i % 9;
+  const int j = (i / 9) % bk;
+  const int o = i / (9 * bk);
+  const int r = tap * bk + j;
+  float s = 0.f;
+  for (int z = 0; z < splits; ++z) s += wpart[(static_cast<int64_t>(z) * 9 * bk + r) * k + o];
+  dw2[i] = s;
+}
+
+// dW1: partial [split][j][i] -> flat W1[j][i]
+__global__ void k_reduce_w1(const float* __restrict__ wpart, int splits, int bk, int c,
+                            float* __restrict__ dw1) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= bk * c) return;
+  float s = 0.f;
+  for (int z = 0; z < splits; ++z) s += wpart[static_cast<int64_t>(z) * bk * c + i];
+  dw1[i] = s;
+}
+
+// Statistics layout in the arena: fstat = mean[C] | var[C] for the feature
+// channels (shared by every BN_a that reads them, F6); zstat = per layer
+// mean[bk] | var[bk].  `stat_at` maps an index of the flat reference layout
+// (per layer mean_a[c] var_a[c] mean_b[bk] var_b[bk]) to its arena value.
+__device__ __forceinline__ float stat_at(int m, int c0, int k, int bk, int C,
+                                         const float* fstat, const float* zstat,
+                                         int64_t i) {
+  int64_t o = 0;
+  for (int l = 0; l < m; ++l) {
+    const int c = c0 + l * k;
+    const int64_t sz = 2 * c + 2 * bk;
+    if (i < o + sz) {
+      const int64_t r = i - o;
+      if (r < c) return fstat[r];
+      if (r < 2 * c) return fstat[C + (r - c)];
+      return zstat[static_cast<int64_t>(l) * 2 * bk + (r - 2 * c)];
+    }
+    o += sz;
+  }
+  return 0.f;
+}
+
+// Running-statistics update for every BN of the block (ops.hpp:185-194):
+// rm = (1-m) rm + m mean ; rv = (1-m) rv + m var_biased.
+__global__ void k_running_update(int m, int c0, int k, int bk, int C,
+                                 const float* __restrict__ fstat,
+                                 const float* __restrict__ zstat,
+                                 float* __restrict__ running, int64_t total) {
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= total) return;
+  const float s = stat_at(m, c0, k, bk, C, fstat, zstat, i);
+  running[i] = (1.0f - kMomentum) * running[i] + kMomentum * s;
+}
+
+// Flat statistics export in the reference layout.
+__global__ void k_export_stats(int m, int c0, int k, int bk, int C,
+                               const float* __restrict__ fstat,
+                               const float* __restrict__ zstat, float* __restrict__ out,
+                               int64_t total) {
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= total) return;
+  out[i] = stat_at(m, c0, k, bk, C, fstat, zstat, i);
+}
+
+}  // namespace dpb

@@ -1,0 +1,74 @@
+"""Per-op device entry points mirroring denseplan::ops (ops.hpp:53-387).
+
+Tensors are fp32 NCHW torch CUDA tensors; every call goes to libdpb.so.
+"""
+from __future__ import annotations
+
+import ctypes as C
+
+import torch
+
+from . import errors
+from ._lib import check, lib
+from .block import _ptr
+
+
+def _stream():
+    return C.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+
+def batch_statistics(x: torch.Tensor) -> tuple[torch.Tensor, torch.Tensor]:
+    """Per-channel mean and biased variance (ops.hpp:138-162)."""
+    n, c, h, w = x.shape
+    mean = torch.empty(c, device=x.device)
+    var = torch.empty(c, device=x.device)
+    check(lib().dpb_op_batch_statistics(_ptr(x), n, c, h, w, _ptr(mean), _ptr(var), _stream()))
+    return mean, var
+
+
+def batchnorm_apply(x, gamma, beta, mean, var, relu: bool = False) -> torch.Tensor:
+    """gamma*(x-mean)*inv + beta (ops.hpp:115-134), optionally + relu."""
+    n, c, h, w = x.shape
+    out = torch.empty_like(x)
+    check(lib().dpb_op_batchnorm_apply(_ptr(x), n, c, h, w, _ptr(gamma), _ptr(beta), _ptr(mean),
+                                       _ptr(var), int(relu), _ptr(out), _stream()))
+    return out
+
+
+def batchnorm_backward(grad_y, x, gamma, mean, var):
+    """Exact train-mode BN gradients (ops.hpp:206-243) -> (gx, dgamma, dbeta)."""
+    n, c, h, w = x.shape
+    if grad_y.shape != x.shape:
+        raise errors.ShapeError("batchnorm_backward shape mismatch")
+    gx = torch.empty_like(x)
+    dg = torch.empty(c, device=x.device)
+    db = torch.empty(c, device=x.device)
+    check(lib().dpb_op_batchnorm_backward(_ptr(grad_y), _ptr(x), n, c, h, w, _ptr(gamma), _ptr(mean),
+                                          _ptr(var), _ptr(gx), _ptr(dg), _ptr(db), _stream()))
+    return gx, dg, db
+
+
+def conv2d_forward(x, weights, padding: int) -> torch.Tensor:
+    """Stride-1 cross-correlation (ops.hpp:315-342)."""
+    n, cin, h, w = x.shape
+    cout, wc, kh, kw = weights.shape
+    if wc != cin:
+        raise errors.ShapeError(f"conv input channels {cin} != weight in_channels {wc}")
+    oh, ow = h + 2 * padding - kh + 1, w + 2 * padding - kw + 1
+    if oh < 1 or ow < 1:
+        raise errors.ShapeError("conv output collapses to zero size")
+    out = torch.empty((n, cout, oh, ow), device=x.device)
+    check(lib().dpb_op_conv2d_forward(_ptr(x), n, cin, h, w, _ptr(weights), cout, kh, padding,
+                                      _ptr(out), _stream()))
+    return out
+
+
+def conv2d_backward(grad_y, x, weights, padding: int, need_grad_x: bool = True):
+    """Exact gradients (ops.hpp:346-387) -> (grad_x or None, grad_w)."""
+    n, cin, h, w = x.shape
+    cout, _, kh, _ = weights.shape
+    gx = torch.empty_like(x) if need_grad_x else None
+    gw = torch.empty_like(weights)
+    check(lib().dpb_op_conv2d_backward(_ptr(grad_y), _ptr(x), n, cin, h, w, _ptr(weights), cout, kh,
+                                       padding, _ptr(gx), _ptr(gw), _stream()))
+    return gx, gw
