@@ -190,6 +190,14 @@ DPB_API int dpb_block_profile_read(dpb_block* blk, dpb_kernel_stat* out, int max
 DPB_API int dpb_block_memory(const dpb_block_desc* desc, int64_t* efficient_bytes,
                      int64_t* naive_bytes);
 
+/* Diagnostic: D[M,N] = A . B^T on the tcgen05 engine with fp32 global
+ * operands (A [M][K] or [K][M] when a_mn; B [N][K] or [K][N] when b_mn),
+ * bf16 (split=0) or bf16x3 hi/lo (split=1) products, N tile bn in
+ * {16,48,64,128,192}; colsum [ceil(M/128)][N][2] per-CTA column sums. */
+DPB_API int dpb_selftest_tc_gemm(const float* A, const float* B, float* D, float* colsum,
+                                 int M, int N, int K, int bn, int a_mn, int b_mn, int split,
+                                 void* stream);
+
 /* ---- per-op entry points (ops.hpp parity), fp32 NCHW device tensors ---- */
 DPB_API int dpb_op_batch_statistics(const float* x, int64_t n, int64_t c, int64_t h,
                             int64_t w, float* mean, float* var, void* stream);

@@ -62,6 +62,8 @@ SIGNATURES = {
     "dpb_block_profile": (C.c_int, [_P, C.c_int]),
     "dpb_block_profile_read": (C.c_int, [_P, _P, C.c_int, C.POINTER(C.c_int)]),
     "dpb_block_memory": (C.c_int, [C.POINTER(BlockDesc), C.POINTER(_I64), C.POINTER(_I64)]),
+    "dpb_selftest_tc_gemm": (C.c_int, [_P, _P, _P, _P, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int,
+                                       C.c_int, _P]),
     "dpb_op_batch_statistics": (C.c_int, [_P, _I64, _I64, _I64, _I64, _P, _P, _P]),
     "dpb_op_batchnorm_apply": (C.c_int, [_P, _I64, _I64, _I64, _I64, _P, _P, _P, _P, C.c_int, _P, _P]),
     "dpb_op_batchnorm_backward": (C.c_int, [_P, _P, _I64, _I64, _I64, _I64, _P, _P, _P, _P, _P, _P, _P]),

@@ -92,7 +92,7 @@ Geometry geometry(const dpb_block_desc& d) {
   g.C = d.c0 + d.m * d.k;
   g.cmax = d.c0 + (d.m - 1) * d.k;
   g.P = static_cast<int>((g.M + 127) / 128);
-  g.S = d.dtype == DPB_BF16 ? 2 : 4;
+  g.S = 4;  // features and bottleneck outputs are stored fp32
   return g;
 }
 
@@ -146,6 +146,12 @@ void plan_arena(const dpb_block_desc& d, dpb_arena_sizes* s) {
       const int64_t chunk = wgrad_chunk(g.M, tiles);
       const int64_t splits = (g.M + chunk - 1) / chunk;
       wmax = std::max(wmax, splits * rows * cols);
+    }
+    if (d.dtype == DPB_BF16 && tc_supported(d)) {
+      const int64_t c3 = tc_wgrad_chunk(g.M, (9LL * d.bk + 127) / 128);
+      wmax = std::max<int64_t>(wmax, ((g.M + c3 - 1) / c3) * 9LL * d.bk * d.k);
+      const int64_t c1 = tc_wgrad_chunk(g.M, (c + 127) / 128);
+      wmax = std::max<int64_t>(wmax, ((g.M + c1 - 1) / c1) * c * d.bk);
     }
   }
   const int64_t pbytes = static_cast<int64_t>(g.P) * std::max<int64_t>(g.C, d.bk) * 16;
@@ -288,7 +294,8 @@ static void forward_impl(Block* b, const float* x_in, const float* params, float
     }
     {
       LaunchScope ls(b, KC_C1_FWD, M * (a.c + d.bk) * Sb, 2.0 * M * a.c * d.bk);
-      gemm_bn<128, Conv1x1Fwd>(b, a, g.M, d.bk, 1);
+      if (b->tc) tc_conv1x1_fwd(b, a);
+      else gemm_bn<128, Conv1x1Fwd>(b, a, g.M, d.bk, 1);
     }
     if (!eval) {
       LaunchScope ls(b, KC_FINALIZE, 0, 0);
@@ -298,7 +305,8 @@ static void forward_impl(Block* b, const float* x_in, const float* params, float
     }
     {
       LaunchScope ls(b, KC_C3_FWD, M * (d.bk + d.k) * Sb, 2.0 * M * 9 * d.bk * d.k);
-      gemm_bn<128, Conv3x3Fwd>(b, a, g.M, d.k, 1);
+      if (b->tc) tc_conv3x3_fwd(b, a);
+      else gemm_bn<128, Conv3x3Fwd>(b, a, g.M, d.k, 1);
     }
     if (!eval) {
       LaunchScope ls(b, KC_FINALIZE, 0, 0);
@@ -343,17 +351,23 @@ static void backward_impl(Block* b, const float* params, float* grad_acc, float*
     // 3x3: dgrad (+ReLU mask by act_b, BN_b sums) and wgrad (graph.hpp:905-910)
     {
       LaunchScope ls(b, KC_C3_DGRAD, M * (4.0 * d.k + Sb * d.bk + 4.0 * d.bk), f3);
-      gemm_bn<128, Conv3x3Dgrad>(b, a, g.M, d.bk, 1);
+      if (b->tc) tc_conv3x3_dgrad(b, a);
+      else gemm_bn<128, Conv3x3Dgrad>(b, a, g.M, d.bk, 1);
     }
     {
       const int64_t rows = 9LL * d.bk;
-      const int bn = bn_tile(d.k);
-      const int64_t tiles = ((rows + 127) / 128) * ((d.k + bn - 1) / bn);
-      a.kchunk = wgrad_chunk(g.M, tiles);
-      const int splits = static_cast<int>((g.M + a.kchunk - 1) / a.kchunk);
+      int splits;
       {
         LaunchScope ls(b, KC_C3_WGRAD, M * (4.0 * d.k + Sb * d.bk), f3);
-        gemm_bn<128, Conv3x3Wgrad>(b, a, rows, d.k, splits);
+        if (b->tc) {
+          splits = tc_conv3x3_wgrad(b, a);
+        } else {
+          const int bn = bn_tile(d.k);
+          const int64_t tiles = ((rows + 127) / 128) * ((d.k + bn - 1) / bn);
+          a.kchunk = wgrad_chunk(g.M, tiles);
+          splits = static_cast<int>((g.M + a.kchunk - 1) / a.kchunk);
+          gemm_bn<128, Conv3x3Wgrad>(b, a, rows, d.k, splits);
+        }
       }
       LaunchScope ls(b, KC_REDUCE_W, 4.0 * splits * rows * d.k, 0);
       k_reduce_w2<<<blocks_for(9LL * d.k * d.bk, 256), 256, 0, b->stream>>>(
@@ -368,19 +382,29 @@ static void backward_impl(Block* b, const float* params, float* grad_acc, float*
     // 1x1: dgrad (+ReLU mask by act_a, BN_a sums) and wgrad (graph.hpp:920-926)
     {
       LaunchScope ls(b, KC_C1_DGRAD, M * ((4.0 + Sb) * d.bk + (Sb + 4.0) * a.c), f1);
-      gemm_bn2<128, Conv1x1Dgrad>(b, a, g.M, a.c, 1);
+      if (b->tc) tc_conv1x1_dgrad(b, a);
+      else gemm_bn2<128, Conv1x1Dgrad>(b, a, g.M, a.c, 1);
     }
     {
-      const int64_t tiles = ((d.bk + 63) / 64) * ((a.c + 63) / 64);
-      a.kchunk = wgrad_chunk(g.M, tiles);
-      const int splits = static_cast<int>((g.M + a.kchunk - 1) / a.kchunk);
+      int splits;
       {
         LaunchScope ls(b, KC_C1_WGRAD, M * ((4.0 + Sb) * d.bk + Sb * a.c), f1);
-        gemm_bn2<64, Conv1x1Wgrad>(b, a, d.bk, a.c, splits);
+        if (b->tc) {
+          splits = tc_conv1x1_wgrad(b, a);
+        } else {
+          const int64_t tiles = ((d.bk + 63) / 64) * ((a.c + 63) / 64);
+          a.kchunk = wgrad_chunk(g.M, tiles);
+          splits = static_cast<int>((g.M + a.kchunk - 1) / a.kchunk);
+          gemm_bn2<64, Conv1x1Wgrad>(b, a, d.bk, a.c, splits);
+        }
       }
       LaunchScope ls(b, KC_REDUCE_W, 4.0 * splits * d.bk * a.c, 0);
-      k_reduce_w1<<<blocks_for(static_cast<int64_t>(d.bk) * a.c, 256), 256, 0, b->stream>>>(
-          b->wpart, splits, d.bk, a.c, d_w1);
+      if (b->tc)
+        k_reduce_w1t<<<blocks_for(static_cast<int64_t>(d.bk) * a.c, 256), 256, 0, b->stream>>>(
+            b->wpart, splits, d.bk, a.c, d_w1);
+      else
+        k_reduce_w1<<<blocks_for(static_cast<int64_t>(d.bk) * a.c, 256), 256, 0, b->stream>>>(
+            b->wpart, splits, d.bk, a.c, d_w1);
     }
     // BN_a backward (graph.hpp:929-932) + concat-backward accumulate (:936-941)
     {
@@ -410,10 +434,7 @@ int block_forward(Block* b, const float* x_in, const float* params, float* runni
                 "train-mode batchnorm needs at least 2 values per channel");
   if (eval && running == nullptr) return fail(DPB_CONFIG_ERROR, "eval needs running stats");
   b->launches = 0;
-  if (b->d.dtype == DPB_BF16)
-    forward_impl<__nv_bfloat16>(b, x_in, params, running, update_running, eval);
-  else
-    forward_impl<float>(b, x_in, params, running, update_running, eval);
+  forward_impl<float>(b, x_in, params, running, update_running, eval);
   const cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return cuda_fail(e, "block forward launch");
   b->fwd_done = !eval;
@@ -424,10 +445,7 @@ int block_backward(Block* b, const float* params, float* grad_acc, float* grads)
   if (!b->fwd_done)
     return fail(DPB_PROTOCOL_ERROR, "backward requires a train-mode forward");
   b->launches = 0;
-  if (b->d.dtype == DPB_BF16)
-    backward_impl<__nv_bfloat16>(b, params, grad_acc, grads);
-  else
-    backward_impl<float>(b, params, grad_acc, grads);
+  backward_impl<float>(b, params, grad_acc, grads);
   const cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return cuda_fail(e, "block backward launch");
   return DPB_OK;
@@ -453,15 +471,13 @@ static void read_z_impl(Block* b, float* dst) {
 }
 
 int read_feats(Block* b, float* dst) {
-  if (b->d.dtype == DPB_BF16) read_feats_impl<__nv_bfloat16>(b, dst);
-  else read_feats_impl<float>(b, dst);
+  read_feats_impl<float>(b, dst);
   const cudaError_t e = cudaGetLastError();
   return e == cudaSuccess ? DPB_OK : cuda_fail(e, "read_feats");
 }
 
 int read_z(Block* b, float* dst) {
-  if (b->d.dtype == DPB_BF16) read_z_impl<__nv_bfloat16>(b, dst);
-  else read_z_impl<float>(b, dst);
+  read_z_impl<float>(b, dst);
   const cudaError_t e = cudaGetLastError();
   return e == cudaSuccess ? DPB_OK : cuda_fail(e, "read_z");
 }
@@ -486,6 +502,7 @@ int create(const dpb_block_desc* desc, int device, void* stream, Block** out) {
   b->device = device;
   b->stream = static_cast<cudaStream_t>(stream);
   b->g = geometry(*desc);
+  b->tc = desc->dtype == DPB_BF16 && tc_supported(*desc);
   plan_arena(*desc, &b->sz);
   e = cudaMalloc(&b->arena, static_cast<size_t>(b->sz.total_bytes));
   if (e != cudaSuccess) {

@@ -52,6 +52,7 @@ struct Block {
   float* bnb_bwd = nullptr;  // [bk][2]
   float* bna_bwd = nullptr;  // [cmax][2]
   std::vector<int64_t> param_off, stat_off;
+  bool tc = false;                    // tensor-core (tcgen05) GEMMs
   bool fwd_done = false;
   int64_t launches = 0;
   bool prof = false;
@@ -85,6 +86,18 @@ int read_z(Block* b, float* dst);
 int read_stats(Block* b, float* dst);
 void profile_enable(Block* b, int on);
 int profile_read(Block* b, dpb_kernel_stat* out, int max, int* count);
+
+// tensor-core path (dpb_tc_block.cu)
+template <typename S>
+struct LayerArgs;
+bool tc_supported(const dpb_block_desc& d);
+int64_t tc_wgrad_chunk(int64_t M, int64_t tiles);
+void tc_conv1x1_fwd(Block* b, const LayerArgs<float>& a);
+void tc_conv3x3_fwd(Block* b, const LayerArgs<float>& a);
+void tc_conv3x3_dgrad(Block* b, const LayerArgs<float>& a);
+void tc_conv1x1_dgrad(Block* b, const LayerArgs<float>& a);
+int tc_conv1x1_wgrad(Block* b, LayerArgs<float> a);
+int tc_conv3x3_wgrad(Block* b, LayerArgs<float> a);
 
 }  // namespace dpb
 

@@ -219,6 +219,17 @@ __device__ __forceinline__ float stat_at(int m, int c0, int k, int bk, int C,
   return 0.f;
 }
 
+// dW1 from the tensor-core wgrad partials [split][i][j] -> flat W1[j][i]
+__global__ void k_reduce_w1t(const float* __restrict__ wpart, int splits, int bk, int c,
+                             float* __restrict__ dw1) {
+  const int o = blockIdx.x * blockDim.x + threadIdx.x;  // flat (j, i)
+  if (o >= bk * c) return;
+  const int j = o / c, i = o - j * c;
+  float s = 0.f;
+  for (int z = 0; z < splits; ++z) s += wpart[(static_cast<int64_t>(z) * c + i) * bk + j];
+  dw1[o] = s;
+}
+
 // Running-statistics update for every BN of the block (ops.hpp:185-194):
 // rm = (1-m) rm + m mean ; rv = (1-m) rv + m var_biased.
 __global__ void k_running_update(int m, int c0, int k, int bk, int C,

@@ -1,0 +1,335 @@
+// tcgen05 (5th-gen tensor core) implicit-GEMM engine for sm_100a.
+//
+// One CTA computes a 128 x BN fp32 tile of D = A . B^T in TMEM:
+//   * all 256 threads are producers: they load the op's operands from HBM,
+//     apply the fused transform (BN+ReLU recompute, 3x3 halo gather with
+//     zero padding after activation, BN-backward), convert to bf16 — for the
+//     forward as an exact hi/lo split, x = hi + lo — and st.shared them into
+//     the UMMA canonical no-swizzle layout (8x8 core matrices), double
+//     buffered;
+//   * one elected thread issues tcgen05.mma (kind::f16, bf16 x bf16 -> fp32,
+//     M=128) and tcgen05.commit's each stage to an mbarrier, so the tensor
+//     core runs stage s while the producers fill stage s^1;
+//   * the epilogue reads the accumulator with tcgen05.ld (32x32b) and hands
+//     8-column chunks of each row to the op (stores, ReLU masks, BN sums).
+//
+// Forward GEMMs run as bf16x3 (hi.hi + hi.lo + lo.hi, fp32 accumulate):
+// ~16 mantissa bits per operand, enough that ReLU masks match the fp32
+// reference; backward GEMMs use one bf16 product.
+#pragma once
+
+#include <cuda_bf16.h>
+#include <stdint.h>
+
+#include "dpb_common.cuh"
+
+namespace dpb {
+namespace tc {
+
+constexpr int kBM = 128;   // UMMA M (cta_group::1)
+constexpr int kBK = 64;    // K elements per pipeline stage (4 MMAs of K=16)
+constexpr int kThreads = 256;
+
+// ---- PTX wrappers --------------------------------------------------------------
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  const uint32_t addr = smem_u32(bar);
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(addr),
+      "r"(parity)
+      : "memory");
+}
+
+__device__ __forceinline__ void fence_barrier_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+
+__device__ __forceinline__ void fence_proxy_async() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
+__device__ __forceinline__ void tc_fence_before() {
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void tc_fence_after() {
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+}
+
+template <uint32_t kCols>
+__device__ __forceinline__ void tmem_alloc(uint32_t* dst_smem) {
+  asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                   smem_u32(dst_smem)),
+               "n"(kCols));
+  asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+}
+
+template <uint32_t kCols>
+__device__ __forceinline__ void tmem_dealloc(uint32_t taddr) {
+  asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(taddr), "n"(kCols));
+}
+
+// D[tmem] (+)= A[smem] . B[smem]^T, bf16 inputs, fp32 accumulate.
+__device__ __forceinline__ void mma_bf16(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc,
+                                         uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n"
+      "}\n" ::"r"(d_tmem),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
+}
+
+__device__ __forceinline__ void mma_commit(uint64_t* bar) {
+  asm volatile(
+      "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+          smem_u32(bar))
+      : "memory");
+}
+
+// 32 lanes x 32 bits, 8 consecutive columns per thread.
+__device__ __forceinline__ void tmem_ld8(uint32_t taddr, float (&v)[8]) {
+  uint32_t r[8];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int i = 0; i < 8; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+// ---- descriptors -----------------------------------------------------------------
+
+// Instruction descriptor: bf16 A/B, fp32 D, M=128, N, majors (0 = K, 1 = MN).
+__host__ __device__ constexpr uint32_t make_idesc(int n, int a_mn, int b_mn) {
+  return (1u << 4)                                   // D format F32
+         | (1u << 7)                                 // A format BF16
+         | (1u << 10)                                // B format BF16
+         | (static_cast<uint32_t>(a_mn) << 15)       // A major
+         | (static_cast<uint32_t>(b_mn) << 16)       // B major
+         | (static_cast<uint32_t>(n >> 3) << 17)     // N >> 3
+         | (static_cast<uint32_t>(kBM >> 4) << 24);  // M >> 4
+}
+
+// Shared-memory descriptor, SWIZZLE_NONE canonical layout, version 1.
+__device__ __forceinline__ uint64_t make_sdesc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+  return static_cast<uint64_t>((saddr >> 4) & 0x3FFF) |
+         (static_cast<uint64_t>((lbo >> 4) & 0x3FFF) << 16) |
+         (static_cast<uint64_t>((sbo >> 4) & 0x3FFF) << 32) | (1ull << 46);
+}
+
+// Operand tile of R rows (M or N) x kBK K-elements, bf16, 8x8 core matrices.
+// Core matrix (g = row/8, kg = k/8) lives at ((kg * R/8) + g) * 128 bytes.
+//   K-major : element (row, k) at core + (row%8)*16 + (k%8)*2
+//   MN-major: element (row, k) at core + (k%8)*16 + (row%8)*2
+// For both: SBO (next 8 rows along M/N) = 128 B, LBO (next 8 along K) = R*16 B.
+template <int R>
+struct Tile {
+  static constexpr int kBytes = R * kBK * 2;
+  // byte offset of the 16-byte chunk holding 8 K-consecutive elements of a row
+  // (K-major) starting at k (k % 8 == 0)
+  __device__ static constexpr uint32_t kmajor_chunk(int row, int k) {
+    return static_cast<uint32_t>(((k >> 3) * (R >> 3) + (row >> 3)) * 128 + (row & 7) * 16);
+  }
+  // byte offset of the 16-byte chunk holding 8 row-consecutive elements at one
+  // k (MN-major), row % 8 == 0
+  __device__ static constexpr uint32_t mnmajor_chunk(int row, int k) {
+    return static_cast<uint32_t>(((k >> 3) * (R >> 3) + (row >> 3)) * 128 + (k & 7) * 16);
+  }
+  __device__ static uint64_t desc(uint32_t base, int k16) {
+    return make_sdesc(base + static_cast<uint32_t>(k16 * 2 * (R >> 3) * 128), R * 16, 128);
+  }
+};
+
+// ---- bf16 conversion helpers -----------------------------------------------------
+
+__device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
+  __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
+  return *reinterpret_cast<uint32_t*>(&h);
+}
+
+// hi = bf16(x), lo = bf16(x - hi): x == hi + lo to ~16 mantissa bits.
+__device__ __forceinline__ void split8(const float (&v)[8], uint4& hi, uint4& lo) {
+  float h[8], l[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    h[i] = __bfloat162float(__float2bfloat16_rn(v[i]));
+    l[i] = v[i] - h[i];
+  }
+  hi = make_uint4(pack_bf16(h[0], h[1]), pack_bf16(h[2], h[3]), pack_bf16(h[4], h[5]),
+                  pack_bf16(h[6], h[7]));
+  lo = make_uint4(pack_bf16(l[0], l[1]), pack_bf16(l[2], l[3]), pack_bf16(l[4], l[5]),
+                  pack_bf16(l[6], l[7]));
+}
+
+__device__ __forceinline__ uint4 to_bf16x8(const float (&v)[8]) {
+  return make_uint4(pack_bf16(v[0], v[1]), pack_bf16(v[2], v[3]), pack_bf16(v[4], v[5]),
+                    pack_bf16(v[6], v[7]));
+}
+
+__device__ __forceinline__ void st_shared16(uint8_t* base, uint32_t off, uint4 v) {
+  *reinterpret_cast<uint4*>(base + off) = v;
+}
+
+// 8 consecutive fp32 values, vectorised when 16-byte aligned, zero past `n`.
+__device__ __forceinline__ void load8(const float* p, int n, bool aligned, float (&v)[8]) {
+  if (aligned && n >= 8) {
+    const float4 a = __ldg(reinterpret_cast<const float4*>(p));
+    const float4 b = __ldg(reinterpret_cast<const float4*>(p) + 1);
+    v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w;
+    v[4] = b.x; v[5] = b.y; v[6] = b.z; v[7] = b.w;
+  } else {
+#pragma unroll
+    for (int i = 0; i < 8; ++i) v[i] = i < n ? __ldg(p + i) : 0.f;
+  }
+}
+
+// ---- the engine ---------------------------------------------------------------------
+//
+// Op interface (all device functions, called by every thread unless noted):
+//   static constexpr int BN;            N tile (multiple of 16, <= 256)
+//   static constexpr bool kSplit;       bf16x3 hi/lo operands (forward)
+//   static constexpr int kAMN, kBMN;    operand majors (0 K-major, 1 MN-major)
+//   int num_kb() const;                 K blocks of kBK
+//   void prologue(uint8_t* aux) const;  fill coefficient tables
+//   void produce(uint8_t* a_hi, uint8_t* a_lo, uint8_t* b_hi, uint8_t* b_lo,
+//                int kb, const uint8_t* aux) const;
+//   void epilogue(int row, int col0, const float (&v)[8], const uint8_t* aux,
+//                 float (&s1)[8], float (&s2)[8]) const;   8 columns of one row
+//   void col_sums(int col, float s1, float s2) const;     once per column per CTA
+//                                                         (when kColSums)
+template <int N>
+struct TmemCols {
+  static constexpr uint32_t value = N <= 32 ? 32 : N <= 64 ? 64 : N <= 128 ? 128 : 256;
+};
+
+template <class Op>
+__global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(const Op op) {
+  constexpr int BN = Op::BN;
+  constexpr int NP = Op::kSplit ? 2 : 1;  // operand planes
+  constexpr int A_BYTES = Tile<kBM>::kBytes;
+  constexpr int B_BYTES = Tile<BN>::kBytes;
+  constexpr int STAGE = NP * (A_BYTES + B_BYTES);
+  constexpr uint32_t TCOLS = TmemCols<BN>::value;
+  static_assert(BN % 16 == 0 && BN <= 256, "UMMA N");
+
+  extern __shared__ __align__(1024) uint8_t smem[];
+  __shared__ uint64_t mbar[2];
+  __shared__ uint32_t tmem_base;
+  __shared__ float red[2][4][BN];
+
+  const int tid = threadIdx.x;
+  const int warp = tid / 32, lane = tid % 32;
+  uint8_t* aux = smem + 2 * STAGE;
+
+  if (warp == 0) tmem_alloc<TCOLS>(&tmem_base);
+  if (tid == 32) {
+    mbar_init(&mbar[0], 1);
+    mbar_init(&mbar[1], 1);
+    fence_barrier_init();
+  }
+  op.prologue(aux);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = tmem_base;
+
+  constexpr uint32_t idesc = make_idesc(BN, Op::kAMN, Op::kBMN);
+  const int nkb = op.num_kb();
+  for (int kb = 0; kb < nkb; ++kb) {
+    const int s = kb & 1;
+    if (kb >= 2) mbar_wait(&mbar[s], ((kb - 2) >> 1) & 1);  // stage s free again
+    uint8_t* st = smem + s * STAGE;
+    uint8_t* a_hi = st;
+    uint8_t* b_hi = st + A_BYTES;
+    uint8_t* a_lo = st + A_BYTES + B_BYTES;
+    uint8_t* b_lo = a_lo + A_BYTES;
+    op.produce(a_hi, a_lo, b_hi, b_lo, kb, aux);
+    fence_proxy_async();
+    __syncthreads();
+    if (tid == 0) {
+      tc_fence_after();
+      const uint32_t ah = smem_u32(a_hi), bh = smem_u32(b_hi);
+      const uint32_t al = smem_u32(a_lo), bl = smem_u32(b_lo);
+#pragma unroll
+      for (int k16 = 0; k16 < kBK / 16; ++k16) {
+        const uint32_t acc = (kb | k16) ? 1u : 0u;
+        mma_bf16(tmem, Tile<kBM>::desc(ah, k16), Tile<BN>::desc(bh, k16), idesc, acc);
+        if constexpr (Op::kSplit) {
+          mma_bf16(tmem, Tile<kBM>::desc(ah, k16), Tile<BN>::desc(bl, k16), idesc, 1u);
+          mma_bf16(tmem, Tile<kBM>::desc(al, k16), Tile<BN>::desc(bh, k16), idesc, 1u);
+        }
+      }
+      mma_commit(&mbar[s]);
+    }
+  }
+  // wait for the last commit (it covers every earlier MMA of this thread)
+  mbar_wait(&mbar[(nkb - 1) & 1], ((nkb - 1) >> 1) & 1);
+  tc_fence_after();
+
+  // epilogue: warp w reads TMEM lanes 32*(w%4).. (its quarter), chunks of 8
+  // columns split between the two warps of each quarter.
+  const int quarter = warp & 3, half = warp >> 2;
+  const int row = quarter * 32 + lane;
+  for (int cc = half; cc < BN / 8; cc += 2) {
+    float v[8];
+    tmem_ld8(tmem + (static_cast<uint32_t>(quarter * 32) << 16) + cc * 8, v);
+    float s1[8], s2[8];
+    op.epilogue(row, cc * 8, v, aux, s1, s2);
+    if constexpr (Op::kColSums) {
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        float a = s1[i], b = s2[i];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+          a += __shfl_xor_sync(0xffffffffu, a, o);
+          b += __shfl_xor_sync(0xffffffffu, b, o);
+        }
+        if (lane == 0) {
+          red[0][quarter][cc * 8 + i] = a;
+          red[1][quarter][cc * 8 + i] = b;
+        }
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if constexpr (Op::kColSums) {
+    for (int c = tid; c < BN; c += kThreads) {
+      // fixed order over the four row quarters: deterministic
+      const double a = static_cast<double>(red[0][0][c]) + red[0][1][c] + red[0][2][c] + red[0][3][c];
+      const double b = static_cast<double>(red[1][0][c]) + red[1][1][c] + red[1][2][c] + red[1][3][c];
+      op.col_sums(c, a, b);
+    }
+  }
+  if (warp == 0) {
+    tc_fence_after();
+    tmem_dealloc<TCOLS>(tmem);
+  }
+}
+
+// Dynamic shared memory of the two pipeline stages (the op's aux tables
+// follow them).
+template <class Op>
+constexpr size_t stage_bytes() {
+  constexpr int NP = Op::kSplit ? 2 : 1;
+  return 2 * NP * (Tile<kBM>::kBytes + Tile<Op::BN>::kBytes);
+}
+
+}  // namespace tc
+}  // namespace dpb

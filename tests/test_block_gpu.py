@@ -2,8 +2,13 @@
 oracle restatement and the reference's own golden vectors.
 
 Tolerances (BASELINE.json north_star):
-  fp32 path: rel_err = |a-b| / max(1, |a|, |b|) <= 1e-4 elementwise
-             (the reference's own metric, dp/gradcheck.hpp:14-17);
+  fp32 path: rel_err = |a-b| / max(1, |a|, |b|) <= 1e-4 elementwise (the
+             reference's own metric, dp/gradcheck.hpp:14-17) against the
+             reference evaluated in float64 (GraphPlan<double> arithmetic);
+             against the reference evaluated in float32 the bound is
+             max(1e-4, 2 x that run's own deviation from float64), because
+             the reference's sequential fp32 sums are themselves off by up to
+             ~2e-4 on cancelling gradient sums;
   bf16 path: ||a-b||_2 / ||b||_2 <= 2e-2 per tensor (normwise, because a
              ReLU-kink flip of a near-zero bf16 pre-activation is legitimate).
 """
@@ -54,6 +59,13 @@ def run_device(s, params, x_in, running_in, acc_in, dtype, layout="nchw"):
     return out
 
 
+def oracle_run(s, params, x, acc, run0, dt):
+    shp = O.BlockShape(*s)
+    feats, z, stats, run = O.block_forward(shp, params.astype(dt), x.astype(dt), run0.astype(dt), True)
+    acc_out, grads = O.block_backward(shp, params.astype(dt), feats, z, stats, acc.astype(dt))
+    return dict(feats=feats, z=z, stats=stats, running=run, acc_out=acc_out, grads=grads)
+
+
 def oracle_case(s, seed, perturb=True):
     shp = O.BlockShape(*s)
     params = O.random_block_params(shp, seed, np.float32, perturb_bn=perturb)
@@ -61,27 +73,36 @@ def oracle_case(s, seed, perturb=True):
     acc = O.rng_normal(seed + 100, shp.n * shp.c_out * shp.h * shp.w, np.float32).reshape(
         shp.n, shp.c_out, shp.h, shp.w)
     run0 = shp.initial_running(np.float32)
-    feats, z, stats, run = O.block_forward(shp, params, x, run0, True)
-    acc_out, grads = O.block_backward(shp, params, feats, z, stats, acc)
-    return dict(params=params, x_in=x, acc_in=acc, running_in=run0, feats=feats, z=z, stats=stats,
-                running=run, acc_out=acc_out, grads=grads)
+    ref = dict(params=params, x_in=x, acc_in=acc, running_in=run0)
+    ref.update(oracle_run(s, params, x, acc, run0, np.float32))
+    ref["f64"] = oracle_run(s, params, x, acc, run0, np.float64)
+    return ref
 
 
 KEYS = ("feats", "z", "stats", "running", "acc_out", "grads")
 
 
 def check(got, ref, dtype, label=""):
+    """ref: reference outputs (float32 or float64 run); ref['f64'] (optional)
+    the same computation in float64."""
     bad = []
+    r64 = ref.get("f64", ref if ref["grads"].dtype == np.float64 else None)
     for key in KEYS:
+        assert np.all(np.isfinite(got[key])), f"{label} {key} has non-finite values"
         if dtype == "fp32":
-            e = rel_err(got[key], ref[key])
-            if not e <= FP32_TOL:
-                bad.append(f"{key}: rel_err {e:.3e}")
+            if r64 is not None:
+                e = rel_err(got[key], r64[key])
+                if not e <= FP32_TOL:
+                    bad.append(f"{key}: rel_err vs f64 {e:.3e}")
+            if ref[key].dtype == np.float32:
+                own = rel_err(ref[key], r64[key]) if r64 is not None else 0.0
+                e = rel_err(got[key], ref[key])
+                if not e <= max(FP32_TOL, 2 * own):
+                    bad.append(f"{key}: rel_err vs f32 {e:.3e} (reference f32 own error {own:.3e})")
         else:
-            e = norm_err(got[key], ref[key])
+            e = norm_err(got[key], (r64 or ref)[key])
             if not e <= BF16_TOL:
                 bad.append(f"{key}: norm_err {e:.3e}")
-        assert np.all(np.isfinite(got[key])), f"{label} {key} has non-finite values"
     assert not bad, f"{label} {dtype}: " + "; ".join(bad)
 
 
@@ -89,6 +110,10 @@ def check(got, ref, dtype, label=""):
 @pytest.mark.parametrize("dtype", ["fp32", "bf16"])
 def test_block_matches_reference_golden(name, dtype):
     g = load_golden(name)
+    if g["params"].dtype == np.float32:
+        # the same inputs through the reference arithmetic in float64
+        g["f64"] = oracle_run(g["shape_tuple"], g["params"], g["x_in"], g["acc_in"], g["running_in"],
+                              np.float64)
     got = run_device(g["shape_tuple"], g["params"], g["x_in"], g["running_in"], g["acc_in"], dtype)
     check(got, g, dtype, name)
 
@@ -166,7 +191,8 @@ def test_backward_is_linear_in_upstream_gradient(dtype):
         lhs = outs[2][i].double()
         rhs = 2.0 * outs[0][i].double() - 3.0 * outs[1][i].double()
         err = (lhs - rhs).norm() / rhs.norm()
-        assert err < 1e-5, err
+        # bf16: the tensor-core backward rounds its GEMM operands to bf16
+        assert err < (1e-5 if dtype == "fp32" else 1e-2), err
 
 
 def test_zero_upstream_gives_zero_gradients():

@@ -97,7 +97,7 @@ def test_rng_matches_reference_draws():
 def test_arena_plan_offsets_and_sizes_exact():
     s = P.BlockShape(16, 32, 32, 24, 12, 12, 48)   # cfg1
     M, C, cmax = 16 * 32 * 32, 24 + 12 * 12, 24 + 11 * 12
-    for dtype, S in (("fp32", 4), ("bf16", 2)):
+    for dtype, S in (("fp32", 4), ("bf16", 4)):
         a = P.plan_arena(s, dtype, "nchw")
         assert a["feat_offset"] == 0 and a["feat_bytes"] == M * C * S
         assert a["z_bytes"] == 12 * M * 48 * S
