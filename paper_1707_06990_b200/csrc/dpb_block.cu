@@ -177,8 +177,10 @@ template <int BM, int BN, class Op>
 static void launch_gemm(Block* b, const Op& op, dim3 grid, size_t dyn) {
   static bool configured = false;  // per template instance
   if (!configured) {
+    cudaFuncAttributes fa{};
+    cudaFuncGetAttributes(&fa, gemm_kernel<BM, BN, Op>);
     cudaFuncSetAttribute(gemm_kernel<BM, BN, Op>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         160 * 1024);
+                         227 * 1024 - static_cast<int>(fa.sharedSizeBytes));
     configured = true;
   }
   gemm_kernel<BM, BN, Op><<<grid, kThreads, dyn, b->stream>>>(op);

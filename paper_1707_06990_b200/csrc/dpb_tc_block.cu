@@ -21,11 +21,14 @@ bool tc_supported(const dpb_block_desc& d) {
 
 template <class Op>
 static void launch(Block* b, const Op& op, dim3 grid, size_t aux) {
-  static bool configured = false;
-  if (!configured) {
+  static int max_dyn = -1;
+  if (max_dyn < 0) {
+    // opt in to the full 227 KB minus the kernel's static shared memory
+    cudaFuncAttributes fa{};
+    cudaFuncGetAttributes(&fa, tc::tc_gemm_kernel<Op>);
+    max_dyn = 227 * 1024 - static_cast<int>(fa.sharedSizeBytes);
     cudaFuncSetAttribute(tc::tc_gemm_kernel<Op>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         227 * 1024);
-    configured = true;
+                         max_dyn);
   }
   const size_t smem = tc::stage_bytes<Op>() + aux;
   tc::tc_gemm_kernel<Op><<<grid, tc::kThreads, smem, b->stream>>>(op);
