@@ -31,8 +31,18 @@ __device__ __forceinline__ float bn_inv(float var) {
 // Per-channel BN forward transform kept in shared memory by the kernels that
 // recompute BN+ReLU in their prologue: y = (x - mean) * (gamma*inv) + beta.
 struct BnFwd {
-  float mean, scale, beta, inv;
+  float mean, scale, beta, inv, gamma;
 };
+
+// The ReLU mask of the backward pass, act > 0, evaluated with the
+// reference's exact float expression gamma * (x - mean) * inv + beta
+// (ops.hpp:130, left to right, no contraction) so that, given the same
+// stored forward values, the mask is bit-identical to the reference's
+// relu_backward predicate (ops.hpp:268-287).
+__device__ __forceinline__ bool relu_mask_ref(const BnFwd& b, float x) {
+  const float t = __fmul_rn(__fmul_rn(b.gamma, __fsub_rn(x, b.mean)), b.inv);
+  return __fadd_rn(t, b.beta) > 0.f;
+}
 
 // BN backward coefficients of one channel (ops.hpp:206-243):
 //   gx = (gamma*inv) * (g - mg - xhat * mgx),   xhat = (x - mean) * inv

@@ -157,7 +157,7 @@ __device__ __forceinline__ void fill_bn_fwd(BnFwd* t, int count, int first,
     const int ch = first + i;
     const float mean = mean_p[ch], var = var_p[ch];
     const float inv = bn_inv(var);
-    t[i] = BnFwd{mean, gamma[ch] * inv, beta[ch], inv};
+    t[i] = BnFwd{mean, gamma[ch] * inv, beta[ch], inv, gamma[ch]};
   }
 }
 
@@ -272,8 +272,7 @@ struct Conv3x3Dgrad {
                            double& s2) const {
     const BnFwd b = reinterpret_cast<const BnFwd*>(d)[j];
     const float zv = to_f(a.z[m * a.bk + j]);
-    const float pre = fmaf(zv - b.mean, b.scale, b.beta);
-    const float g = pre > 0.f ? v : 0.f;  // relu_backward by act_b (ops.hpp:268-287)
+    const float g = relu_mask_ref(b, zv) ? v : 0.f;  // relu_backward by act_b (ops.hpp:268-287)
     a.g0[m * a.bk + j] = g;
     const float xh = (zv - b.mean) * b.inv;
     s1 = g;
@@ -361,8 +360,7 @@ struct Conv1x1Dgrad {
                            double& s1, double& s2) const {
     const BnFwd b = tile_a(d)[i - n0];
     const float x = to_f(a.feat[m * a.C + i]);
-    const float pre = fmaf(x - b.mean, b.scale, b.beta);
-    const float g = pre > 0.f ? v : 0.f;
+    const float g = relu_mask_ref(b, x) ? v : 0.f;
     a.g1[m * a.c + i] = g;
     const float xh = (x - b.mean) * b.inv;
     s1 = g;

@@ -245,8 +245,7 @@ struct Tc3x3Dgrad {
     for (int i = 0; i < 8; ++i) {
       if (i < nv) {
         const BnFwd b = bn[col0 + i];
-        const float pre = fmaf(zv[i] - b.mean, b.scale, b.beta);
-        g[i] = pre > 0.f ? v[i] : 0.f;  // relu_backward by act_b
+        g[i] = relu_mask_ref(b, zv[i]) ? v[i] : 0.f;  // relu_backward by act_b
         s1[i] = g[i];
         s2[i] = g[i] * ((zv[i] - b.mean) * b.inv);
       } else {
@@ -327,8 +326,7 @@ struct Tc1x1Dgrad {
     for (int i = 0; i < 8; ++i) {
       if (i < nv) {
         const BnFwd b = bn[col0 + i];
-        const float pre = fmaf(x[i] - b.mean, b.scale, b.beta);
-        g[i] = pre > 0.f ? v[i] : 0.f;  // relu_backward by act_a
+        g[i] = relu_mask_ref(b, x[i]) ? v[i] : 0.f;  // relu_backward by act_a
         s1[i] = g[i];
         s2[i] = g[i] * ((x[i] - b.mean) * b.inv);
       } else {
