@@ -156,6 +156,23 @@ struct Tile {
   }
 };
 
+// Producer chunk coordinates.  A warp's 128-bit shared stores execute in four
+// phases of 8 threads; these mappings give each phase one whole 128-byte core
+// matrix (8 rows of one K chunk, or 8 K-rows of one row group), so the stores
+// are bank-conflict free.
+// K-major: chunk q -> (row, kc), kc a multiple of 8.
+__device__ __forceinline__ void kmajor_coords(int q, int& row, int& kc) {
+  row = (q & 7) | ((q >> 6) << 3);
+  kc = ((q >> 3) & 7) << 3;
+}
+// MN-major over R rows: chunk q -> (row0, k), row0 a multiple of 8.
+template <int R>
+__device__ __forceinline__ void mnmajor_coords(int q, int& row0, int& k) {
+  const int rest = q >> 3;
+  row0 = (rest % (R / 8)) << 3;
+  k = ((rest / (R / 8)) << 3) | (q & 7);
+}
+
 // ---- bf16 conversion helpers -----------------------------------------------------
 
 __device__ __forceinline__ uint32_t pack_bf16(float a, float b) {

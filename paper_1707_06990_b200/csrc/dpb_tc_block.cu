@@ -86,12 +86,14 @@ void tc_conv1x1_fwd(Block* b, const LayerArgs<float>& a) {
 
 void tc_conv3x3_fwd(Block* b, const LayerArgs<float>& a) {
   const TcArgs t = make_args(a);
-  launch_small<tc::Tc3x3Fwd>(b, pick_bn(a.k), t, dim3(mtiles(a.M)), sizeof(BnFwd) * a.bk);
+  launch_small<tc::Tc3x3Fwd>(b, pick_bn(a.k), t, dim3(mtiles(a.M)),
+                             sizeof(BnFwd) * a.bk + sizeof(int) * tc::kBM);
 }
 
 void tc_conv3x3_dgrad(Block* b, const LayerArgs<float>& a) {
   const TcArgs t = make_args(a);
-  launch_bn<tc::Tc3x3Dgrad>(b, pick_bn(a.bk), t, dim3(mtiles(a.M)), sizeof(BnFwd) * a.bk);
+  launch_bn<tc::Tc3x3Dgrad>(b, pick_bn(a.bk), t, dim3(mtiles(a.M)),
+                            sizeof(BnFwd) * a.bk + sizeof(int) * tc::kBM);
 }
 
 void tc_conv1x1_dgrad(Block* b, const LayerArgs<float>& a) {

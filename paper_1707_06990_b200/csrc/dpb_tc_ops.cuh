@@ -30,6 +30,30 @@ struct TcArgs {
   int n0_unused;
 };
 
+// (y << 16 | x) of the CTA's 128 pixel rows, computed once in the prologue so
+// the 3x3 producers never divide.
+__device__ __forceinline__ void fill_row_yx(int* yx, int64_t m0, int64_t M, int H, int W) {
+  for (int r = threadIdx.x; r < kBM; r += kThreads) {
+    const int64_t p = m0 + r;
+    int v = 0;
+    if (p < M) {
+      const int pix = static_cast<int>(p % (static_cast<int64_t>(H) * W));
+      v = ((pix / W) << 16) | (pix % W);
+    }
+    yx[r] = v;
+  }
+}
+
+// Neighbour pixel p + (dy, dx) of a row with coordinates yx; false when it
+// falls in the zero padding.
+__device__ __forceinline__ bool neighbour(int64_t p, int yx, int H, int W, int dy, int dx,
+                                          int64_t& q) {
+  const int y = (yx >> 16) + dy, x = (yx & 0xFFFF) + dx;
+  if (y < 0 || y >= H || x < 0 || x >= W) return false;
+  q = p + static_cast<int64_t>(dy) * W + dx;
+  return true;
+}
+
 __device__ __forceinline__ void bnrelu8(const BnFwd* t, int ch0, int nvalid, float (&v)[8]) {
 #pragma unroll
   for (int i = 0; i < 8; ++i) v[i] = i < nvalid ? bn_relu(t[ch0 + i], v[i]) : 0.f;
@@ -80,8 +104,10 @@ struct Tc1x1Fwd {
     const LayerArgs<float>& a = t.a;
     const BnFwd* bn = reinterpret_cast<const BnFwd*>(aux);
     const int64_t m0 = static_cast<int64_t>(blockIdx.x) * kBM;
+#pragma unroll
     for (int q = threadIdx.x; q < kBM * kBK / 8; q += kThreads) {
-      const int row = q >> 3, kc = (q & 7) * 8;
+      int row, kc;
+      kmajor_coords(q, row, kc);
       const int ch0 = kb * kBK + kc;
       const int64_t p = m0 + row;
       float v[8];
@@ -94,8 +120,10 @@ struct Tc1x1Fwd {
       }
       put8<true>(ah, al, Tile<kBM>::kmajor_chunk(row, kc), v);
     }
+#pragma unroll
     for (int q = threadIdx.x; q < BN * kBK / 8; q += kThreads) {
-      const int row = q >> 3, kc = (q & 7) * 8;
+      int row, kc;
+      kmajor_coords(q, row, kc);
       const int i0 = kb * kBK + kc;
       float v[8];
       if (row < a.bk && i0 < a.c) load8(a.w1 + static_cast<int64_t>(row) * a.c + i0, a.c - i0, false, v);
@@ -129,9 +157,14 @@ struct Tc3x3Fwd {
   static constexpr int kAMN = 0, kBMN = 0;
   TcArgs t;
   __device__ int num_kb() const { return (9 * t.a.bk + kBK - 1) / kBK; }
+  __device__ const int* row_yx(const uint8_t* aux) const {
+    return reinterpret_cast<const int*>(aux + sizeof(BnFwd) * t.a.bk);
+  }
   __device__ void prologue(uint8_t* aux) const {
     fill_bn_fwd(reinterpret_cast<BnFwd*>(aux), t.a.bk, 0, t.a.bmean, t.a.bvar, t.a.gamma_b,
                 t.a.beta_b);
+    fill_row_yx(const_cast<int*>(row_yx(aux)), static_cast<int64_t>(blockIdx.x) * kBM, t.a.M,
+                t.a.H, t.a.W);
   }
   __device__ void produce(uint8_t* ah, uint8_t* al, uint8_t* bh, uint8_t* bl, int kb,
                           const uint8_t* aux) const {
@@ -139,8 +172,10 @@ struct Tc3x3Fwd {
     const BnFwd* bn = reinterpret_cast<const BnFwd*>(aux);
     const int64_t m0 = static_cast<int64_t>(blockIdx.x) * kBM;
     const int K = 9 * a.bk;
+#pragma unroll
     for (int q = threadIdx.x; q < kBM * kBK / 8; q += kThreads) {
-      const int row = q >> 3, kc = (q & 7) * 8;
+      int row, kc;
+      kmajor_coords(q, row, kc);
       const int k0 = kb * kBK + kc;
       const int64_t p = m0 + row;
       float v[8];
@@ -149,15 +184,17 @@ struct Tc3x3Fwd {
         const int tap = k0 / a.bk, j0 = k0 - tap * a.bk;
         int64_t nb;
         // bk % 8 == 0 (checked at dispatch): a chunk never straddles taps
-        if (shifted(p, a.H, a.W, tap / 3 - 1, tap % 3 - 1, nb)) {
+        if (neighbour(p, row_yx(aux)[row], a.H, a.W, tap / 3 - 1, tap % 3 - 1, nb)) {
           load8(a.z + nb * a.bk + j0, 8, (a.bk & 3) == 0, v);
           bnrelu8(bn, j0, 8, v);
         }
       }
       put8<true>(ah, al, Tile<kBM>::kmajor_chunk(row, kc), v);
     }
+#pragma unroll
     for (int q = threadIdx.x; q < BN * kBK / 8; q += kThreads) {
-      const int o = q >> 3, kc = (q & 7) * 8;
+      int o, kc;
+      kmajor_coords(q, o, kc);
       const int k0 = kb * kBK + kc;
       float v[8];
       zero8(v);
@@ -196,17 +233,24 @@ struct Tc3x3Dgrad {
   static constexpr int kAMN = 0, kBMN = 0;
   TcArgs t;
   __device__ int num_kb() const { return (9 * t.kp + kBK - 1) / kBK; }
+  __device__ const int* row_yx(const uint8_t* aux) const {
+    return reinterpret_cast<const int*>(aux + sizeof(BnFwd) * t.a.bk);
+  }
   __device__ void prologue(uint8_t* aux) const {
     fill_bn_fwd(reinterpret_cast<BnFwd*>(aux), t.a.bk, 0, t.a.bmean, t.a.bvar, t.a.gamma_b,
                 t.a.beta_b);
+    fill_row_yx(const_cast<int*>(row_yx(aux)), static_cast<int64_t>(blockIdx.x) * kBM, t.a.M,
+                t.a.H, t.a.W);
   }
   __device__ void produce(uint8_t* ah, uint8_t* al, uint8_t* bh, uint8_t* bl, int kb,
-                          const uint8_t*) const {
+                          const uint8_t* aux) const {
     const LayerArgs<float>& a = t.a;
     const int64_t m0 = static_cast<int64_t>(blockIdx.x) * kBM;
     const int K = 9 * t.kp;
+#pragma unroll
     for (int q = threadIdx.x; q < kBM * kBK / 8; q += kThreads) {
-      const int row = q >> 3, kc = (q & 7) * 8;
+      int row, kc;
+      kmajor_coords(q, row, kc);
       const int k0 = kb * kBK + kc;
       const int64_t p = m0 + row;
       float v[8];
@@ -214,13 +258,15 @@ struct Tc3x3Dgrad {
       if (p < a.M && k0 < K) {
         const int tap = k0 / t.kp, o0 = k0 - tap * t.kp;
         int64_t src;  // dx[p] = sum_tap dy[p - d_tap] W[tap]
-        if (o0 < a.k && shifted(p, a.H, a.W, 1 - tap / 3, 1 - tap % 3, src))
+        if (o0 < a.k && neighbour(p, row_yx(aux)[row], a.H, a.W, 1 - tap / 3, 1 - tap % 3, src))
           load8(a.acc + src * a.C + a.c + o0, a.k - o0, t.vec, v);
       }
       put8<false>(ah, al, Tile<kBM>::kmajor_chunk(row, kc), v);
     }
+#pragma unroll
     for (int q = threadIdx.x; q < BN * kBK / 8; q += kThreads) {
-      const int j = q >> 3, kc = (q & 7) * 8;
+      int j, kc;
+      kmajor_coords(q, j, kc);
       const int k0 = kb * kBK + kc;
       float v[8];
       zero8(v);
@@ -284,8 +330,10 @@ struct Tc1x1Dgrad {
     const LayerArgs<float>& a = t.a;
     const BnBwd* bb = reinterpret_cast<const BnBwd*>(aux);
     const int64_t m0 = static_cast<int64_t>(blockIdx.x) * kBM;
+#pragma unroll
     for (int q = threadIdx.x; q < kBM * kBK / 8; q += kThreads) {
-      const int row = q >> 3, kc = (q & 7) * 8;
+      int row, kc;
+      kmajor_coords(q, row, kc);
       const int j0 = kb * kBK + kc;
       const int64_t p = m0 + row;
       float v[8];
@@ -303,8 +351,10 @@ struct Tc1x1Dgrad {
     }
     // B(i, j) = W1[j][i]: MN-major, 8 consecutive i of row j per chunk
     const int n0 = blockIdx.y * BN;
+#pragma unroll
     for (int q = threadIdx.x; q < BN * kBK / 8; q += kThreads) {
-      const int kr = q / (BN / 8), rg = (q % (BN / 8)) * 8;
+      int rg, kr;
+      mnmajor_coords<BN>(q, rg, kr);
       const int j = kb * kBK + kr;
       const int i0 = n0 + rg;
       float v[8];
@@ -376,8 +426,10 @@ struct Tc1x1Wgrad {
     const int m0 = blockIdx.x * kBM;
     const int64_t pk = kbeg() + static_cast<int64_t>(kb) * kBK, pe = kend();
     // A: rows = channels i (MN-major), K = pixels
+#pragma unroll
     for (int q = threadIdx.x; q < kBM * kBK / 8; q += kThreads) {
-      const int kr = q / (kBM / 8), rg = (q % (kBM / 8)) * 8;
+      int rg, kr;
+      mnmajor_coords<kBM>(q, rg, kr);
       const int64_t p = pk + kr;
       const int i0 = m0 + rg;
       float v[8];
@@ -391,8 +443,10 @@ struct Tc1x1Wgrad {
       put8<false>(ah, al, Tile<kBM>::mnmajor_chunk(rg, kr), v);
     }
     // B: rows = bk channels j (MN-major), K = pixels, t1 recomputed
+#pragma unroll
     for (int q = threadIdx.x; q < BN * kBK / 8; q += kThreads) {
-      const int kr = q / (BN / 8), rg = (q % (BN / 8)) * 8;
+      int rg, kr;
+      mnmajor_coords<BN>(q, rg, kr);
       const int64_t p = pk + kr;
       float v[8];
       const int nv = a.bk - rg;
@@ -443,8 +497,10 @@ struct Tc3x3Wgrad {
     const int m0 = blockIdx.x * kBM;
     const int R = 9 * a.bk;
     const int64_t pk = kbeg() + static_cast<int64_t>(kb) * kBK, pe = kend();
+#pragma unroll
     for (int q = threadIdx.x; q < kBM * kBK / 8; q += kThreads) {
-      const int kr = q / (kBM / 8), rg = (q % (kBM / 8)) * 8;
+      int rg, kr;
+      mnmajor_coords<kBM>(q, rg, kr);
       const int64_t p = pk + kr;
       const int r0 = m0 + rg;
       float v[8];
@@ -459,8 +515,10 @@ struct Tc3x3Wgrad {
       }
       put8<false>(ah, al, Tile<kBM>::mnmajor_chunk(rg, kr), v);
     }
+#pragma unroll
     for (int q = threadIdx.x; q < BN * kBK / 8; q += kThreads) {
-      const int kr = q / (BN / 8), rg = (q % (BN / 8)) * 8;
+      int rg, kr;
+      mnmajor_coords<BN>(q, rg, kr);
       const int64_t p = pk + kr;
       float v[8];
       if (p < pe && rg < a.k) load8(a.acc + p * a.C + a.c + rg, a.k - rg, t.vec, v);

@@ -33,14 +33,16 @@ struct TestGemm {
       float v[8];
       uint32_t off;
       if (MN == 0) {
-        const int row = q / 8, kc = (q % 8) * 8;
+        int row, kc;
+        kmajor_coords(q, row, kc);
         const int gr = r0 + row, gk = k0 + kc;
 #pragma unroll
         for (int i = 0; i < 8; ++i)
           v[i] = (gr < rows_total && gk + i < K) ? G[static_cast<int64_t>(gr) * K + gk + i] : 0.f;
         off = Tile<R>::kmajor_chunk(row, kc);
       } else {
-        const int kr = q / (R / 8), rg = (q % (R / 8)) * 8;
+        int rg, kr;
+        mnmajor_coords<R>(q, rg, kr);
         const int gk = k0 + kr;
 #pragma unroll
         for (int i = 0; i < 8; ++i)
