@@ -92,6 +92,9 @@ Geometry geometry(const dpb_block_desc& d) {
   g.C = d.c0 + d.m * d.k;
   g.cmax = d.c0 + (d.m - 1) * d.k;
   g.P = static_cast<int>((g.M + 127) / 128);
+  g.Pmax = g.P;
+  if (d.dtype == DPB_BF16 && tc_supported(d))
+    g.Pmax = static_cast<int>(std::max<int64_t>(g.P, tc_halo_partials(d)));
   g.S = 4;  // features and bottleneck outputs are stored fp32
   return g;
 }
@@ -148,13 +151,14 @@ void plan_arena(const dpb_block_desc& d, dpb_arena_sizes* s) {
       wmax = std::max(wmax, splits * rows * cols);
     }
     if (d.dtype == DPB_BF16 && tc_supported(d)) {
+      wmax = std::max<int64_t>(wmax, tc_halo_wgrad_splits(d) * 9LL * d.bk * d.k);
       const int64_t c3 = tc_wgrad_chunk(g.M, (9LL * d.bk + 127) / 128);
       wmax = std::max<int64_t>(wmax, ((g.M + c3 - 1) / c3) * 9LL * d.bk * d.k);
       const int64_t c1 = tc_wgrad_chunk(g.M, (c + 127) / 128);
       wmax = std::max<int64_t>(wmax, ((g.M + c1 - 1) / c1) * c * d.bk);
     }
   }
-  const int64_t pbytes = static_cast<int64_t>(g.P) * std::max<int64_t>(g.C, d.bk) * 16;
+  const int64_t pbytes = static_cast<int64_t>(g.Pmax) * std::max<int64_t>(g.C, d.bk) * 16;
   const int64_t scratch = align_up(pbytes, 256) + align_up(wmax * 4, 256) +
                           align_up((2LL * d.bk + 2 * g.cmax) * 4, 256);
   take(scratch, &s->scratch_offset, &s->scratch_bytes);
@@ -305,15 +309,16 @@ static void forward_impl(Block* b, const float* x_in, const float* params, float
       k_finalize_stats<<<blocks_for(32LL * d.bk, 256), 256, 0, b->stream>>>(
           b->part, g.P, d.bk, count, zm, zm + d.bk, 0);
     }
+    int p3 = g.P;
     {
       LaunchScope ls(b, KC_C3_FWD, M * (d.bk + d.k) * Sb, 2.0 * M * 9 * d.bk * d.k);
-      if (b->tc) tc_conv3x3_fwd(b, a);
+      if (b->tc) p3 = tc_conv3x3_fwd(b, a);
       else gemm_bn<128, Conv3x3Fwd>(b, a, g.M, d.k, 1);
     }
     if (!eval) {
       LaunchScope ls(b, KC_FINALIZE, 0, 0);
       k_finalize_stats<<<blocks_for(32LL * d.k, 256), 256, 0, b->stream>>>(
-          b->part, g.P, d.k, count, fmean, fvar, a.c);
+          b->part, p3, d.k, count, fmean, fvar, a.c);
     }
   }
   if (!eval && update_running) {
@@ -351,9 +356,10 @@ static void backward_impl(Block* b, const float* params, float* grad_acc, float*
     float* d_w2 = d_bb + d.bk;
     const double f3 = 2.0 * M * 9 * d.bk * d.k, f1 = 2.0 * M * a.c * d.bk;
     // 3x3: dgrad (+ReLU mask by act_b, BN_b sums) and wgrad (graph.hpp:905-910)
+    int pd = g.P;
     {
       LaunchScope ls(b, KC_C3_DGRAD, M * (4.0 * d.k + Sb * d.bk + 4.0 * d.bk), f3);
-      if (b->tc) tc_conv3x3_dgrad(b, a);
+      if (b->tc) pd = tc_conv3x3_dgrad(b, a);
       else gemm_bn<128, Conv3x3Dgrad>(b, a, g.M, d.bk, 1);
     }
     {
@@ -379,7 +385,7 @@ static void backward_impl(Block* b, const float* params, float* grad_acc, float*
     {
       LaunchScope ls(b, KC_FINALIZE, 0, 0);
       k_finalize_bn_bwd<<<blocks_for(32LL * d.bk, 256), 256, 0, b->stream>>>(
-          b->part, g.P, d.bk, count, d_gb, d_bb, b->bnb_bwd);
+          b->part, pd, d.bk, count, d_gb, d_bb, b->bnb_bwd);
     }
     // 1x1: dgrad (+ReLU mask by act_a, BN_a sums) and wgrad (graph.hpp:920-926)
     {
@@ -522,7 +528,7 @@ int create(const dpb_block_desc* desc, int device, void* stream, Block** out) {
   char* sc = base + b->sz.scratch_offset;
   b->part = reinterpret_cast<double2*>(sc);
   const int64_t pbytes =
-      align_up(static_cast<int64_t>(b->g.P) * std::max<int64_t>(b->g.C, desc->bk) * 16, 256);
+      align_up(static_cast<int64_t>(b->g.Pmax) * std::max<int64_t>(b->g.C, desc->bk) * 16, 256);
   b->wpart = reinterpret_cast<float*>(sc + pbytes);
   // wgrad partial region size = scratch - pbytes - coef region
   const int64_t coef_bytes = align_up((2LL * desc->bk + 2 * b->g.cmax) * 4, 256);

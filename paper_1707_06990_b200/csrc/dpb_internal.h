@@ -16,6 +16,7 @@ struct Geometry {
   int64_t C = 0;     // block output channels c0 + m*k (feature pitch)
   int64_t cmax = 0;  // widest layer input c0 + (m-1)*k
   int P = 0;         // row CTAs of 128 pixels = partial-sum count
+  int Pmax = 0;      // partial rows allocated (>= P; halo kernels use N * tiles/image)
   int S = 4;         // bytes per stored feature element
 };
 
@@ -93,8 +94,10 @@ struct LayerArgs;
 bool tc_supported(const dpb_block_desc& d);
 int64_t tc_wgrad_chunk(int64_t M, int64_t tiles);
 void tc_conv1x1_fwd(Block* b, const LayerArgs<float>& a);
-void tc_conv3x3_fwd(Block* b, const LayerArgs<float>& a);
-void tc_conv3x3_dgrad(Block* b, const LayerArgs<float>& a);
+int tc_conv3x3_fwd(Block* b, const LayerArgs<float>& a);    // returns partial rows
+int tc_conv3x3_dgrad(Block* b, const LayerArgs<float>& a);  // returns partial rows
+int64_t tc_halo_partials(const dpb_block_desc& d);
+int64_t tc_halo_wgrad_splits(const dpb_block_desc& d);
 void tc_conv1x1_dgrad(Block* b, const LayerArgs<float>& a);
 int tc_conv1x1_wgrad(Block* b, LayerArgs<float> a);
 int tc_conv3x3_wgrad(Block* b, LayerArgs<float> a);

@@ -6,6 +6,7 @@
 #include <algorithm>
 
 #include "dpb_internal.h"
+#include "dpb_tc_halo.cuh"
 #include "dpb_tc_ops.cuh"
 
 namespace dpb {
@@ -84,16 +85,98 @@ void tc_conv1x1_fwd(Block* b, const LayerArgs<float>& a) {
   launch_bn<tc::Tc1x1Fwd>(b, pick_bn(a.bk), t, dim3(mtiles(a.M)), sizeof(BnFwd) * a.c);
 }
 
-void tc_conv3x3_fwd(Block* b, const LayerArgs<float>& a) {
-  const TcArgs t = make_args(a);
-  launch_small<tc::Tc3x3Fwd>(b, pick_bn(a.k), t, dim3(mtiles(a.M)),
-                             sizeof(BnFwd) * a.bk + sizeof(int) * tc::kBM);
+// ---- 3x3 halo kernels ----------------------------------------------------------
+template <class Op>
+static void launch_halo(Block* b, const Op& op, dim3 grid, size_t stage, int nst, size_t aux) {
+  static int max_dyn = -1;
+  if (max_dyn < 0) {
+    cudaFuncAttributes fa{};
+    cudaFuncGetAttributes(&fa, tc::tc_halo_kernel<Op>);
+    max_dyn = 227 * 1024 - static_cast<int>(fa.sharedSizeBytes);
+    cudaFuncSetAttribute(tc::tc_halo_kernel<Op>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         max_dyn);
+  }
+  tc::tc_halo_kernel<Op><<<grid, tc::kThreads, stage * nst + aux, b->stream>>>(op);
 }
 
-void tc_conv3x3_dgrad(Block* b, const LayerArgs<float>& a) {
+static tc::HaloArgs halo_args(const LayerArgs<float>& a, int kc) {
+  tc::HaloArgs h{};
+  h.a = a;
+  h.g = tc::HaloGeom::make(a.H, a.W);
+  h.kc = kc;
+  h.vec = (a.C % 4 == 0) && (a.c % 4 == 0);
+  return h;
+}
+
+static int64_t nimg(const LayerArgs<float>& a) { return a.M / (static_cast<int64_t>(a.H) * a.W); }
+static constexpr size_t kHaloSmemMax = 220 * 1024;
+
+// Returns the number of per-CTA partial rows written (for the finalize).
+int tc_conv3x3_fwd(Block* b, const LayerArgs<float>& a) {
+  const int bn = pick_bn(a.k);
+  for (int kc = std::min(64, a.bk); a.bk % 16 == 0 && bn <= 64 && kc >= 16; kc /= 2) {
+    if (kc % 16 != 0) continue;
+    const tc::HaloArgs h = halo_args(a, kc);
+    const size_t stage = 2ull * (static_cast<size_t>(h.g.R) * kc * 2 + 9ull * bn * kc * 2);
+    const int nst = (a.bk + kc - 1) / kc > 1 ? 2 : 1;
+    const size_t aux = sizeof(BnFwd) * a.bk;
+    if (stage * nst + aux <= kHaloSmemMax) {
+      const dim3 grid(static_cast<unsigned>(nimg(a) * h.g.tpi));
+      switch (bn) {
+        case 16: launch_halo(b, tc::Tc3x3FwdHalo<16>{h}, grid, stage, nst, aux); break;
+        case 32: launch_halo(b, tc::Tc3x3FwdHalo<32>{h}, grid, stage, nst, aux); break;
+        case 48: launch_halo(b, tc::Tc3x3FwdHalo<48>{h}, grid, stage, nst, aux); break;
+        default: launch_halo(b, tc::Tc3x3FwdHalo<64>{h}, grid, stage, nst, aux); break;
+      }
+      return static_cast<int>(grid.x);
+    }
+  }
   const TcArgs t = make_args(a);
-  launch_bn<tc::Tc3x3Dgrad>(b, pick_bn(a.bk), t, dim3(mtiles(a.M)),
+  launch_small<tc::Tc3x3Fwd>(b, bn, t, dim3(mtiles(a.M)),
+                             sizeof(BnFwd) * a.bk + sizeof(int) * tc::kBM);
+  return static_cast<int>(mtiles(a.M));
+}
+
+int tc_conv3x3_dgrad(Block* b, const LayerArgs<float>& a) {
+  const int bn = pick_bn(a.bk);
+  const int kc = round_up(a.k, 16);
+  if (kc <= 64) {
+    const tc::HaloArgs h = halo_args(a, kc);
+    const size_t stage = static_cast<size_t>(h.g.R) * kc * 2 + 9ull * bn * kc * 2;
+    const size_t aux = sizeof(BnFwd) * a.bk;
+    if (stage + aux <= kHaloSmemMax) {
+      const dim3 grid(static_cast<unsigned>(nimg(a) * h.g.tpi));
+      switch (bn) {
+        case 16: launch_halo(b, tc::Tc3x3DgradHalo<16>{h}, grid, stage, 1, aux); break;
+        case 32: launch_halo(b, tc::Tc3x3DgradHalo<32>{h}, grid, stage, 1, aux); break;
+        case 48: launch_halo(b, tc::Tc3x3DgradHalo<48>{h}, grid, stage, 1, aux); break;
+        case 64: launch_halo(b, tc::Tc3x3DgradHalo<64>{h}, grid, stage, 1, aux); break;
+        case 128: launch_halo(b, tc::Tc3x3DgradHalo<128>{h}, grid, stage, 1, aux); break;
+        case 192: launch_halo(b, tc::Tc3x3DgradHalo<192>{h}, grid, stage, 1, aux); break;
+        default: launch_halo(b, tc::Tc3x3DgradHalo<256>{h}, grid, stage, 1, aux); break;
+      }
+      return static_cast<int>(grid.x);
+    }
+  }
+  const TcArgs t = make_args(a);
+  launch_bn<tc::Tc3x3Dgrad>(b, bn, t, dim3(mtiles(a.M)),
                             sizeof(BnFwd) * a.bk + sizeof(int) * tc::kBM);
+  return static_cast<int>(mtiles(a.M));
+}
+
+int64_t tc_halo_partials(const dpb_block_desc& d) {
+  const tc::HaloGeom g = tc::HaloGeom::make(static_cast<int>(d.h), static_cast<int>(d.w));
+  return d.n * g.tpi;
+}
+
+// split count of the halo 3x3 wgrad for a block (used by the arena plan)
+int64_t tc_halo_wgrad_splits(const dpb_block_desc& d) {
+  const tc::HaloGeom g = tc::HaloGeom::make(static_cast<int>(d.h), static_cast<int>(d.w));
+  const int64_t ntiles = d.n * g.tpi;
+  const int64_t gy = (d.bk + tc::kBM - 1) / tc::kBM;
+  const int64_t target = std::max<int64_t>(1, 296 / gy);
+  const int64_t tpc = std::max<int64_t>(1, (ntiles + target - 1) / target);
+  return (ntiles + tpc - 1) / tpc;
 }
 
 void tc_conv1x1_dgrad(Block* b, const LayerArgs<float>& a) {
@@ -125,6 +208,27 @@ int tc_conv1x1_wgrad(Block* b, LayerArgs<float> a) {
 }
 
 int tc_conv3x3_wgrad(Block* b, LayerArgs<float> a) {
+  {
+    const int bn = pick_bn(a.k);
+    const tc::HaloArgs h = halo_args(a, bn);
+    const size_t stage = static_cast<size_t>(h.g.R) * tc::kBM * 2 + static_cast<size_t>(tc::kBM) * bn * 2;
+    const size_t aux = sizeof(BnFwd) * a.bk;
+    if (bn <= 48 && 2 * stage + aux <= kHaloSmemMax) {
+      const int64_t ntiles = nimg(a) * h.g.tpi;
+      const int64_t gy = (a.bk + tc::kBM - 1) / tc::kBM;
+      const int64_t target = std::max<int64_t>(1, 296 / gy);
+      const int tpc = static_cast<int>(std::max<int64_t>(1, (ntiles + target - 1) / target));
+      const int gx = static_cast<int>((ntiles + tpc - 1) / tpc);
+      const dim3 grid(gx, static_cast<unsigned>(gy));
+      const int nst = tpc > 1 ? 2 : 1;
+      switch (bn) {
+        case 16: launch_halo(b, tc::Tc3x3WgradHalo<16>{h, tpc, static_cast<int>(ntiles)}, grid, stage, nst, aux); break;
+        case 32: launch_halo(b, tc::Tc3x3WgradHalo<32>{h, tpc, static_cast<int>(ntiles)}, grid, stage, nst, aux); break;
+        default: launch_halo(b, tc::Tc3x3WgradHalo<48>{h, tpc, static_cast<int>(ntiles)}, grid, stage, nst, aux); break;
+      }
+      return gx;
+    }
+  }
   const int64_t tiles = mtiles(9LL * a.bk);
   a.kchunk = tc_wgrad_chunk(a.M, tiles);
   const int splits = static_cast<int>((a.M + a.kchunk - 1) / a.kchunk);

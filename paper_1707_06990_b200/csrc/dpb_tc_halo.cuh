@@ -1,0 +1,488 @@
+// 3x3 convolutions as tcgen05 GEMMs over a haloed tile in a PADDED pixel space.
+//
+// Each image is viewed as (H+2) x (W+2) padded positions with zero borders.  A
+// CTA owns 128 consecutive positions of one image's band (padded rows 1..H,
+// all W+2 columns).  Its producers transform the tile's halo — positions
+// [s0 - (W+3), s0 + 128 + (W+3)) — ONCE into shared memory (BN+ReLU or plain
+// bf16, zeros at padding), in a layout whose rows are 16 bytes apart.  A 3x3
+// tap (dy, dx) is then a pure row shift: the UMMA descriptor's start address
+// moves by (dy*(W+2) + dx) * 16 bytes.  So the 9x re-gather of the shifted
+// operand that a plain implicit GEMM pays disappears; zero padding AFTER the
+// activation is physical in the halo.  Outputs on padding columns are
+// computed and dropped (2/(W+2) of the rows).
+//
+//   Tc3x3FwdHalo   D[pos][o]        = sum_tap sum_j act_b[pos+d][j] W2[o][j][tap]  (bf16x3)
+//   Tc3x3DgradHalo D[pos][j]        = sum_tap sum_o dY[pos-d][o]    W2[o][j][tap]  (bf16)
+//   Tc3x3WgradHalo D_tap[j][o]      = sum_pos act_b[pos+d][j] dY[pos][o]          (bf16,
+//                                     9 TMEM accumulators, split-K over tiles)
+// Reference semantics: /root/reference/proj/include/denseplan/ops.hpp:315-387
+// (conv2d_forward / conv2d_backward, padding 1) inside graph.hpp:655, :906-907.
+#pragma once
+
+#include "dpb_simt.cuh"
+#include "dpb_tc.cuh"
+
+namespace dpb {
+namespace tc {
+
+// Geometry of the padded band shared by the three ops.
+struct HaloGeom {
+  int H, W, W2;     // W2 = W + 2
+  int tpi;          // tiles per image = ceil(H * W2 / 128)
+  int R;            // halo rows = 128 + 2 * (W2 + 1), rounded up to 8
+  __host__ __device__ static HaloGeom make(int H, int W) {
+    HaloGeom g;
+    g.H = H;
+    g.W = W;
+    g.W2 = W + 2;
+    g.tpi = (H * g.W2 + kBM - 1) / kBM;
+    g.R = (kBM + 2 * (g.W2 + 1) + 7) / 8 * 8;
+    return g;
+  }
+  // padded position of halo row r of tile t (may be < 0 or past the image)
+  __device__ int pos(int t, int r) const { return g_s0(t) - (W2 + 1) + r; }
+  __device__ int g_s0(int t) const { return W2 + t * kBM; }
+  // real pixel (within the image) of padded position q, or -1 for padding
+  __device__ int pixel(int q) const {
+    if (q < 0) return -1;
+    const int py = q / W2, px = q - py * W2;
+    if (py < 1 || py > H || px < 1 || px > W) return -1;
+    return (py - 1) * W + (px - 1);
+  }
+  // halo-row offset of tap (ty, tx) for the forward (source = pos + d)
+  __device__ int fwd_off(int tap) const { return (W2 + 1) + (tap / 3 - 1) * W2 + (tap % 3 - 1); }
+  // ... and for the transposed conv (source = pos - d)
+  __device__ int bwd_off(int tap) const { return (W2 + 1) - (tap / 3 - 1) * W2 - (tap % 3 - 1); }
+};
+
+// K-major halo tile: element (row, k) at (k/8)*R*16 + row*16 + (k%8)*2.
+__device__ __forceinline__ uint32_t halo_kmajor(int R, int row, int k) {
+  return static_cast<uint32_t>((k >> 3) * R * 16 + row * 16);
+}
+// MN-major halo tile (rows = channels j, K = positions): element (j, pos) at
+// (j/8)*R*16 + pos*16 + (j%8)*2.
+__device__ __forceinline__ uint32_t halo_mnmajor(int R, int j, int pos) {
+  return static_cast<uint32_t>((j >> 3) * R * 16 + pos * 16);
+}
+
+// ---- engine ----------------------------------------------------------------------
+// As tc_gemm_kernel, but the op owns the stage layout and the MMA issue
+// pattern (taps = descriptor shifts), and TMEM may hold several accumulators.
+template <class Op>
+__global__ void __launch_bounds__(kThreads, 1) tc_halo_kernel(const Op op) {
+  constexpr uint32_t TCOLS = TmemCols<Op::kTmemCols>::value;
+  constexpr int BN = Op::BN;
+  extern __shared__ __align__(1024) uint8_t smem[];
+  __shared__ uint64_t mbar[2];
+  __shared__ uint32_t tmem_base;
+  __shared__ float red[2][4][BN];
+
+  const int tid = threadIdx.x;
+  const int warp = tid / 32, lane = tid % 32;
+  const uint32_t SB = op.stage_bytes();
+  const int nst = op.num_kb() > 1 ? 2 : 1;  // stages actually used
+  uint8_t* aux = smem + nst * SB;
+
+  if (warp == 0) tmem_alloc<TCOLS>(&tmem_base);
+  if (tid == 32) {
+    mbar_init(&mbar[0], 1);
+    mbar_init(&mbar[1], 1);
+    fence_barrier_init();
+  }
+  op.prologue(aux);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = tmem_base;
+
+  const int nkb = op.num_kb();
+  for (int kb = 0; kb < nkb; ++kb) {
+    const int s = kb & 1;
+    if (kb >= 2) mbar_wait(&mbar[s], ((kb - 2) >> 1) & 1);
+    uint8_t* st = smem + s * SB;
+    op.produce(st, kb, aux);
+    fence_proxy_async();
+    __syncthreads();
+    if (tid == 0) {
+      tc_fence_after();
+      op.issue(smem_u32(st), kb, tmem);
+      mma_commit(&mbar[s]);
+    }
+  }
+  if (nkb > 0) {
+    mbar_wait(&mbar[(nkb - 1) & 1], ((nkb - 1) >> 1) & 1);
+    tc_fence_after();
+  }
+
+  const int quarter = warp & 3, half = warp >> 2;
+  const int row = quarter * 32 + lane;
+  for (int cc = half; cc < Op::kTmemCols / 8; cc += 2) {
+    float v[8];
+    if (nkb > 0) tmem_ld8(tmem + (static_cast<uint32_t>(quarter * 32) << 16) + cc * 8, v);
+    else
+      for (int i = 0; i < 8; ++i) v[i] = 0.f;
+    float s1[8], s2[8];
+    op.epilogue(row, cc * 8, v, aux, s1, s2);
+    if constexpr (Op::kColSums) {
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        float a = s1[i], b = s2[i];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+          a += __shfl_xor_sync(0xffffffffu, a, o);
+          b += __shfl_xor_sync(0xffffffffu, b, o);
+        }
+        if (lane == 0) {
+          red[0][quarter][cc * 8 + i] = a;
+          red[1][quarter][cc * 8 + i] = b;
+        }
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if constexpr (Op::kColSums) {
+    for (int c = tid; c < BN; c += kThreads) {
+      const double a = static_cast<double>(red[0][0][c]) + red[0][1][c] + red[0][2][c] + red[0][3][c];
+      const double b = static_cast<double>(red[1][0][c]) + red[1][1][c] + red[1][2][c] + red[1][3][c];
+      op.col_sums(c, a, b);
+    }
+  }
+  if (warp == 0) {
+    tc_fence_after();
+    tmem_dealloc<TCOLS>(tmem);
+  }
+}
+
+struct HaloArgs {
+  LayerArgs<float> a;
+  HaloGeom g;
+  int kc;    // channels per K chunk (forward) / padded k (backward), multiple of 16
+  int vec;   // 16-byte aligned feature / accumulator rows at channel c
+};
+
+// ---- forward ------------------------------------------------------------------------
+// y = conv3x3(relu(bn_b(z))): per K chunk of kc channels the stage holds the
+// halo (hi, lo) and W2 for all 9 taps (hi, lo).
+template <int BN_>
+struct Tc3x3FwdHalo {
+  static constexpr int BN = BN_;
+  static constexpr int kTmemCols = BN;
+  static constexpr bool kColSums = true;
+  HaloArgs h;
+  __device__ uint32_t halo_bytes() const { return static_cast<uint32_t>(h.g.R * h.kc * 2); }
+  __device__ uint32_t b_bytes() const { return static_cast<uint32_t>(9 * BN * h.kc * 2); }
+  __device__ uint32_t stage_bytes() const { return 2 * (halo_bytes() + b_bytes()); }
+  __device__ int num_kb() const { return (h.a.bk + h.kc - 1) / h.kc; }
+  __device__ int tile() const { return blockIdx.x % h.g.tpi; }
+  __device__ int img() const { return blockIdx.x / h.g.tpi; }
+  __device__ void prologue(uint8_t* aux) const {
+    fill_bn_fwd(reinterpret_cast<BnFwd*>(aux), h.a.bk, 0, h.a.bmean, h.a.bvar, h.a.gamma_b,
+                h.a.beta_b);
+  }
+  __device__ void produce(uint8_t* st, int kb, const uint8_t* aux) const {
+    const LayerArgs<float>& a = h.a;
+    const BnFwd* bn = reinterpret_cast<const BnFwd*>(aux);
+    uint8_t* xh = st;
+    uint8_t* xl = st + halo_bytes();
+    uint8_t* wh = xl + halo_bytes();
+    uint8_t* wl = wh + b_bytes();
+    const int t = tile();
+    const int64_t pix0 = static_cast<int64_t>(img()) * h.g.H * h.g.W;
+    const int j_base = kb * h.kc;
+    // halo: R rows x kc channels, phases of 8 threads = 8 consecutive rows
+    const int nchunk = h.g.R * (h.kc / 8);
+    for (int q = threadIdx.x; q < nchunk; q += kThreads) {
+      const int row = (q & 7) + 8 * (q / (8 * (h.kc / 8)));
+      const int kc = ((q >> 3) % (h.kc / 8)) * 8;
+      const int pp = h.g.pixel(h.g.pos(t, row));
+      float v[8];
+      const int j0 = j_base + kc;
+      if (pp >= 0 && j0 < a.bk) {
+        load8(a.z + (pix0 + pp) * a.bk + j0, a.bk - j0, (a.bk & 3) == 0, v);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) v[i] = j0 + i < a.bk ? bn_relu(bn[j0 + i], v[i]) : 0.f;
+      } else {
+#pragma unroll
+        for (int i = 0; i < 8; ++i) v[i] = 0.f;
+      }
+      uint4 hi, lo;
+      split8(v, hi, lo);
+      const uint32_t off = halo_kmajor(h.g.R, row, kc);
+      st_shared16(xh, off, hi);
+      st_shared16(xl, off, lo);
+    }
+    // W2 for the 9 taps: tile tap*BN + o rows x kc, K-major
+    const int wchunk = 9 * BN * (h.kc / 8);
+    for (int q = threadIdx.x; q < wchunk; q += kThreads) {
+      const int kcn = h.kc / 8;
+      const int row = (q & 7) + 8 * (q / (8 * kcn));  // tap*BN + o
+      const int kc = ((q >> 3) % kcn) * 8;
+      const int tap = row / BN, o = row - tap * BN;
+      const int j0 = j_base + kc;
+      float v[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i)
+        v[i] = (o < a.k && j0 + i < a.bk)
+                   ? __ldg(a.w2 + (static_cast<int64_t>(o) * a.bk + j0 + i) * 9 + tap)
+                   : 0.f;
+      uint4 hi, lo;
+      split8(v, hi, lo);
+      const uint32_t off = halo_kmajor(9 * BN, row, kc);
+      st_shared16(wh, off, hi);
+      st_shared16(wl, off, lo);
+    }
+  }
+  __device__ void issue(uint32_t st, int kb, uint32_t tmem) const {
+    constexpr uint32_t idesc = make_idesc(BN, 0, 0);
+    const uint32_t xh = st, xl = st + halo_bytes();
+    const uint32_t wh = xl + halo_bytes(), wl = wh + b_bytes();
+    const uint32_t RB = static_cast<uint32_t>(h.g.R) * 16, WB = 9u * BN * 16;
+    for (int tap = 0; tap < 9; ++tap) {
+      const uint32_t aoff = static_cast<uint32_t>(h.g.fwd_off(tap)) * 16;
+      const uint32_t boff = static_cast<uint32_t>(tap * BN) * 16;
+      for (int k16 = 0; k16 < h.kc / 16; ++k16) {
+        const uint32_t ka = k16 * 2 * RB, kbo = k16 * 2 * WB;
+        const uint32_t acc = (kb | tap | k16) ? 1u : 0u;
+        mma_bf16(tmem, make_sdesc(xh + aoff + ka, RB, 128), make_sdesc(wh + boff + kbo, WB, 128),
+                 idesc, acc);
+        mma_bf16(tmem, make_sdesc(xh + aoff + ka, RB, 128), make_sdesc(wl + boff + kbo, WB, 128),
+                 idesc, 1u);
+        mma_bf16(tmem, make_sdesc(xl + aoff + ka, RB, 128), make_sdesc(wh + boff + kbo, WB, 128),
+                 idesc, 1u);
+      }
+    }
+  }
+  __device__ void epilogue(int row, int col0, const float (&v)[8], const uint8_t*, float (&s1)[8],
+                           float (&s2)[8]) const {
+    const LayerArgs<float>& a = h.a;
+    const int pp = h.g.pixel(h.g.g_s0(tile()) + row);
+    const int nv = pp >= 0 ? a.k - col0 : 0;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const bool ok = i < nv;
+      s1[i] = ok ? v[i] : 0.f;
+      s2[i] = ok ? v[i] * v[i] : 0.f;
+    }
+    if (nv > 0) {
+      const int64_t p = static_cast<int64_t>(img()) * h.g.H * h.g.W + pp;
+      float* dst = a.feat + p * a.C + a.c + col0;
+      if (h.vec && nv >= 8) {
+        reinterpret_cast<float4*>(dst)[0] = make_float4(v[0], v[1], v[2], v[3]);
+        reinterpret_cast<float4*>(dst)[1] = make_float4(v[4], v[5], v[6], v[7]);
+      } else {
+#pragma unroll
+        for (int i = 0; i < 8; ++i)
+          if (i < nv) dst[i] = v[i];
+      }
+    }
+  }
+  __device__ void col_sums(int c, double s1, double s2) const {
+    if (c < h.a.k) h.a.part[static_cast<int64_t>(blockIdx.x) * h.a.k + c] = make_double2(s1, s2);
+  }
+};
+
+// ---- backward data --------------------------------------------------------------------
+// t0[pos][j] = relu'(act_b) * sum_tap sum_o dY[pos - d][o] W2[o][j][tap]; K per
+// tap = kc (k padded to 16); the stage holds the dY halo and W2^T for 9 taps.
+template <int BN_>
+struct Tc3x3DgradHalo {
+  static constexpr int BN = BN_;
+  static constexpr int kTmemCols = BN;
+  static constexpr bool kColSums = true;
+  HaloArgs h;
+  __device__ uint32_t halo_bytes() const { return static_cast<uint32_t>(h.g.R * h.kc * 2); }
+  __device__ uint32_t b_bytes() const { return static_cast<uint32_t>(9 * BN * h.kc * 2); }
+  __device__ uint32_t stage_bytes() const { return halo_bytes() + b_bytes(); }
+  __device__ int num_kb() const { return 1; }
+  __device__ int tile() const { return blockIdx.x % h.g.tpi; }
+  __device__ int img() const { return blockIdx.x / h.g.tpi; }
+  __device__ void prologue(uint8_t* aux) const {
+    fill_bn_fwd(reinterpret_cast<BnFwd*>(aux), h.a.bk, 0, h.a.bmean, h.a.bvar, h.a.gamma_b,
+                h.a.beta_b);
+  }
+  __device__ void produce(uint8_t* st, int, const uint8_t*) const {
+    const LayerArgs<float>& a = h.a;
+    uint8_t* dy = st;
+    uint8_t* wt = st + halo_bytes();
+    const int t = tile();
+    const int64_t pix0 = static_cast<int64_t>(img()) * h.g.H * h.g.W;
+    const int kcn = h.kc / 8;
+    for (int q = threadIdx.x; q < h.g.R * kcn; q += kThreads) {
+      const int row = (q & 7) + 8 * (q / (8 * kcn));
+      const int kc = ((q >> 3) % kcn) * 8;
+      const int pp = h.g.pixel(h.g.pos(t, row));
+      float v[8];
+      if (pp >= 0 && kc < a.k) {
+        load8(a.acc + (pix0 + pp) * a.C + a.c + kc, a.k - kc, h.vec, v);
+      } else {
+#pragma unroll
+        for (int i = 0; i < 8; ++i) v[i] = 0.f;
+      }
+      st_shared16(dy, halo_kmajor(h.g.R, row, kc), to_bf16x8(v));
+    }
+    // B for tap: rows tap*BN + j, K = o
+    for (int q = threadIdx.x; q < 9 * BN * kcn; q += kThreads) {
+      const int row = (q & 7) + 8 * (q / (8 * kcn));
+      const int kc = ((q >> 3) % kcn) * 8;
+      const int tap = row / BN, j = row - tap * BN;
+      float v[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i)
+        v[i] = (j < a.bk && kc + i < a.k)
+                   ? __ldg(a.w2 + (static_cast<int64_t>(kc + i) * a.bk + j) * 9 + tap)
+                   : 0.f;
+      st_shared16(wt, halo_kmajor(9 * BN, row, kc), to_bf16x8(v));
+    }
+  }
+  __device__ void issue(uint32_t st, int, uint32_t tmem) const {
+    constexpr uint32_t idesc = make_idesc(BN, 0, 0);
+    const uint32_t dy = st, wt = st + halo_bytes();
+    const uint32_t RB = static_cast<uint32_t>(h.g.R) * 16, WB = 9u * BN * 16;
+    for (int tap = 0; tap < 9; ++tap) {
+      const uint32_t aoff = static_cast<uint32_t>(h.g.bwd_off(tap)) * 16;
+      const uint32_t boff = static_cast<uint32_t>(tap * BN) * 16;
+      for (int k16 = 0; k16 < h.kc / 16; ++k16)
+        mma_bf16(tmem, make_sdesc(dy + aoff + k16 * 2 * RB, RB, 128),
+                 make_sdesc(wt + boff + k16 * 2 * WB, WB, 128), idesc, (tap | k16) ? 1u : 0u);
+    }
+  }
+  __device__ void epilogue(int row, int col0, const float (&v)[8], const uint8_t* aux,
+                           float (&s1)[8], float (&s2)[8]) const {
+    const LayerArgs<float>& a = h.a;
+    const BnFwd* bn = reinterpret_cast<const BnFwd*>(aux);
+    const int pp = h.g.pixel(h.g.g_s0(tile()) + row);
+    const int nv = pp >= 0 ? a.bk - col0 : 0;
+    float zv[8], g[8];
+    const int64_t p = static_cast<int64_t>(img()) * h.g.H * h.g.W + (pp >= 0 ? pp : 0);
+    if (nv > 0) load8(a.z + p * a.bk + col0, nv, (a.bk & 3) == 0, zv);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      if (i < nv) {
+        const BnFwd b = bn[col0 + i];
+        g[i] = relu_mask_ref(b, zv[i]) ? v[i] : 0.f;
+        s1[i] = g[i];
+        s2[i] = g[i] * ((zv[i] - b.mean) * b.inv);
+      } else {
+        g[i] = 0.f;
+        s1[i] = 0.f;
+        s2[i] = 0.f;
+      }
+    }
+    if (nv > 0) {
+      float* dst = a.g0 + p * a.bk + col0;
+      if ((a.bk & 3) == 0 && nv >= 8) {
+        reinterpret_cast<float4*>(dst)[0] = make_float4(g[0], g[1], g[2], g[3]);
+        reinterpret_cast<float4*>(dst)[1] = make_float4(g[4], g[5], g[6], g[7]);
+      } else {
+#pragma unroll
+        for (int i = 0; i < 8; ++i)
+          if (i < nv) dst[i] = g[i];
+      }
+    }
+  }
+  __device__ void col_sums(int c, double s1, double s2) const {
+    if (c < h.a.bk) h.a.part[static_cast<int64_t>(blockIdx.x) * h.a.bk + c] = make_double2(s1, s2);
+  }
+};
+
+// ---- backward weights ------------------------------------------------------------------
+// CTA (x, y): tiles [x*tpc, (x+1)*tpc) of the global tile list (all images),
+// channels j in [128*y, 128*y + 128).  Per tile the stage holds act_b's halo
+// (MN-major: rows = channels, K = positions) and dY of the tile's 128
+// positions (MN-major: rows = o).  Tap t accumulates into TMEM columns
+// [t*BN, t*BN + BN).
+template <int BN_>
+struct Tc3x3WgradHalo {
+  static constexpr int BN = BN_;
+  static constexpr int kTmemCols = 9 * BN;
+  static constexpr bool kColSums = false;
+  HaloArgs h;
+  int tpc;      // tiles per CTA
+  int ntiles;   // total tiles = N * tpi
+  __device__ uint32_t halo_bytes() const { return static_cast<uint32_t>(h.g.R * kBM * 2); }
+  __device__ uint32_t b_bytes() const { return static_cast<uint32_t>(kBM * BN * 2); }
+  __device__ uint32_t stage_bytes() const { return halo_bytes() + b_bytes(); }
+  __device__ int num_kb() const {
+    const int t0 = blockIdx.x * tpc;
+    const int n = ntiles - t0;
+    return n < 0 ? 0 : (n < tpc ? n : tpc);
+  }
+  __device__ void prologue(uint8_t* aux) const {
+    fill_bn_fwd(reinterpret_cast<BnFwd*>(aux), h.a.bk, 0, h.a.bmean, h.a.bvar, h.a.gamma_b,
+                h.a.beta_b);
+  }
+  __device__ void produce(uint8_t* st, int kb, const uint8_t* aux) const {
+    const LayerArgs<float>& a = h.a;
+    const BnFwd* bn = reinterpret_cast<const BnFwd*>(aux);
+    uint8_t* xs = st;
+    uint8_t* dys = st + halo_bytes();
+    const int gt = blockIdx.x * tpc + kb;
+    const int im = gt / h.g.tpi, t = gt - im * h.g.tpi;
+    const int64_t pix0 = static_cast<int64_t>(im) * h.g.H * h.g.W;
+    const int j_base = blockIdx.y * kBM;
+    // act_b halo, MN-major: chunk = 8 channels of one position; phase = 8
+    // consecutive positions of one channel group (128 contiguous bytes)
+    const int groups = kBM / 8;
+    for (int q = threadIdx.x; q < h.g.R * groups; q += kThreads) {
+      const int pos = (q & 7) + 8 * (q / (8 * groups));
+      const int jg = ((q >> 3) % groups) * 8;
+      const int j0 = j_base + jg;
+      const int pp = h.g.pixel(h.g.pos(t, pos));
+      float v[8];
+      if (pp >= 0 && j0 < a.bk) {
+        load8(a.z + (pix0 + pp) * a.bk + j0, a.bk - j0, (a.bk & 3) == 0, v);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) v[i] = j0 + i < a.bk ? bn_relu(bn[j0 + i], v[i]) : 0.f;
+      } else {
+#pragma unroll
+        for (int i = 0; i < 8; ++i) v[i] = 0.f;
+      }
+      st_shared16(xs, halo_mnmajor(h.g.R, jg, pos), to_bf16x8(v));
+    }
+    // dY of the tile's 128 positions, MN-major rows = o
+    const int s0 = h.g.g_s0(t);
+    const int og = BN / 8;
+    for (int q = threadIdx.x; q < kBM * og; q += kThreads) {
+      const int pos = (q & 7) + 8 * (q / (8 * og));
+      const int o0 = ((q >> 3) % og) * 8;
+      const int pp = h.g.pixel(s0 + pos);
+      float v[8];
+      if (pp >= 0 && o0 < a.k) {
+        load8(a.acc + (pix0 + pp) * a.C + a.c + o0, a.k - o0, h.vec, v);
+      } else {
+#pragma unroll
+        for (int i = 0; i < 8; ++i) v[i] = 0.f;
+      }
+      st_shared16(dys, halo_mnmajor(kBM, o0, pos), to_bf16x8(v));
+    }
+  }
+  __device__ void issue(uint32_t st, int kb, uint32_t tmem) const {
+    constexpr uint32_t idesc = make_idesc(BN, 1, 1);
+    const uint32_t xs = st, dys = st + halo_bytes();
+    const uint32_t RB = static_cast<uint32_t>(h.g.R) * 16;
+    for (int tap = 0; tap < 9; ++tap) {
+      const uint32_t aoff = static_cast<uint32_t>(h.g.fwd_off(tap)) * 16;
+      for (int k16 = 0; k16 < kBM / 16; ++k16)
+        // A: M = channels (SBO = R*16 between channel groups), K = positions
+        // shifted by the tap (LBO = 128 between groups of 8 positions)
+        mma_bf16(tmem + tap * BN, make_sdesc(xs + aoff + k16 * 256, 128, RB),
+                 make_sdesc(dys + k16 * 256, 128, kBM * 16), idesc, (kb | k16) ? 1u : 0u);
+    }
+  }
+  __device__ void epilogue(int row, int col0, const float (&v)[8], const uint8_t*, float (&)[8],
+                           float (&)[8]) const {
+    const LayerArgs<float>& a = h.a;
+    const int tap = col0 / BN, o0 = col0 - tap * BN;
+    const int j = blockIdx.y * kBM + row;
+    const int nv = j < a.bk ? a.k - o0 : 0;
+    float* dst = a.wpart + (static_cast<int64_t>(blockIdx.x) * 9 * a.bk + tap * a.bk + j) * a.k + o0;
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+      if (i < nv) dst[i] = v[i];
+  }
+  __device__ void col_sums(int, double, double) const {}
+};
+
+}  // namespace tc
+}  // namespace dpb
