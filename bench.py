@@ -143,6 +143,7 @@ def main():
     ap.add_argument("--config", default="bc100")
     ap.add_argument("--dtype", default="bf16", choices=["bf16", "fp32"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-graph", action="store_true", help="launch kernels directly (no CUDA graph)")
     ap.add_argument("--cpu-budget-s", type=float, default=25.0)
     ap.add_argument("--ref-budget-s", type=float, default=180.0)
     args = ap.parse_args()
@@ -222,6 +223,23 @@ def main():
     launches_per_step = fwd_launches + bwd_launches
     torch.cuda.synchronize(dev)
 
+    # ---- capture one step as a CUDA graph (launch overhead off the host) -----
+    graph = None
+    if not args.no_graph:
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph, stream=stream):
+            step()
+        with torch.cuda.stream(stream):
+            for _ in range(2):
+                graph.replay()
+        torch.cuda.synchronize(dev)
+
+    def timed_step():
+        if graph is not None:
+            graph.replay()
+        else:
+            step()
+
     # ---- timed region --------------------------------------------------------
     if world > 1:
         dist.barrier()
@@ -233,7 +251,7 @@ def main():
     with torch.cuda.stream(stream):
         t0.record(stream)
         for _ in range(args.steps):
-            step()
+            timed_step()
         t1.record(stream)
     torch.cuda.synchronize(dev)
     if world > 1:
@@ -378,6 +396,7 @@ def main():
                                    f"not in the hot path)", "model": args.config, "global_batch": BATCH * world,
                        "per_gpu_batch": BATCH, "blocks": [list(s) for s in shapes],
                        "parallelism": f"dp{world}",
+                       "cuda_graph": graph is not None,
                        "l2": f"working set {ws_bytes / 1e6:.0f} MB > 126 MB L2 (no explicit flush)"},
             "roofline": roof, "step_roofline": step_roof, "kernels": kernels,
             "cpu_baseline": cpu, "e2e": e2e,

@@ -23,7 +23,7 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler", "-fvisibility=hidden",
-         "--expt-relaxed-constexpr", "-Xptxas", "-warn-spills",
+         "--expt-relaxed-constexpr", "--extended-lambda", "-Xptxas", "-warn-spills",
          f"-I{os.path.join(ROOT, 'include')}", f"-I{CSRC}"]
 
 

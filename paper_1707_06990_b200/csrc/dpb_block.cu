@@ -378,7 +378,7 @@ static void backward_impl(Block* b, const float* params, float* grad_acc, float*
         }
       }
       LaunchScope ls(b, KC_REDUCE_W, 4.0 * splits * rows * d.k, 0);
-      k_reduce_w2<<<blocks_for(9LL * d.k * d.bk, 256), 256, 0, b->stream>>>(
+      k_reduce_w2<<<blocks_for(9LL * d.k * d.bk, 32), dim3(32, 8), 0, b->stream>>>(
           b->wpart, splits, d.bk, d.k, d_w2);
     }
     // BN_b backward sums -> dgamma_b, dbeta_b, coefficients (graph.hpp:913-916)
@@ -408,11 +408,11 @@ static void backward_impl(Block* b, const float* params, float* grad_acc, float*
       }
       LaunchScope ls(b, KC_REDUCE_W, 4.0 * splits * d.bk * a.c, 0);
       if (b->tc)
-        k_reduce_w1t<<<blocks_for(static_cast<int64_t>(d.bk) * a.c, 256), 256, 0, b->stream>>>(
-            b->wpart, splits, d.bk, a.c, d_w1);
+        k_reduce_w1t<<<blocks_for(static_cast<int64_t>(d.bk) * a.c, 32), dim3(32, 8), 0,
+                       b->stream>>>(b->wpart, splits, d.bk, a.c, d_w1);
       else
-        k_reduce_w1<<<blocks_for(static_cast<int64_t>(d.bk) * a.c, 256), 256, 0, b->stream>>>(
-            b->wpart, splits, d.bk, a.c, d_w1);
+        k_reduce_w1<<<blocks_for(static_cast<int64_t>(d.bk) * a.c, 32), dim3(32, 8), 0,
+                      b->stream>>>(b->wpart, splits, d.bk, a.c, d_w1);
     }
     // BN_a backward (graph.hpp:929-932) + concat-backward accumulate (:936-941)
     {

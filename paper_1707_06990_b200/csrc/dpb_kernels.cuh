@@ -172,29 +172,53 @@ k_bn_apply_accumulate(int64_t M, int c, int C, const S* __restrict__ feat,
   acc[p * C + ch] += gamma[ch] * inv * (g - coef[2 * ch] - xh * coef[2 * ch + 1]);
 }
 
-// Split-K weight-gradient fold: out = sum over splits in order.
-// dW2: partial row r = tap*bk + j, col o -> flat W2[o][j][tap]
-__global__ void k_reduce_w2(const float* __restrict__ wpart, int splits, int bk, int k,
-                            float* __restrict__ dw2) {
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;  // flat (o, j, tap)
-  if (i >= k * bk * 9) return;
-  const int tap = i % 9;
-  const int j = (i / 9) % bk;
-  const int o = i / (9 * bk);
-  const int r = tap * bk + j;
+// Split-K weight-gradient folds.  Block (32 x 8): 32 consecutive partial
+// elements (coalesced) x 8 split groups; each thread sums its group's splits
+// in order, then the 8 group sums are added in a fixed order — deterministic.
+template <class Index>
+__device__ __forceinline__ void fold_splits(const float* __restrict__ wpart, int splits,
+                                            int64_t n, Index out_index, float* __restrict__ out) {
+  __shared__ float red[8][33];
+  const int64_t e = static_cast<int64_t>(blockIdx.x) * 32 + threadIdx.x;
   float s = 0.f;
-  for (int z = 0; z < splits; ++z) s += wpart[(static_cast<int64_t>(z) * 9 * bk + r) * k + o];
-  dw2[i] = s;
+  if (e < n)
+    for (int z = threadIdx.y; z < splits; z += 8) s += wpart[static_cast<int64_t>(z) * n + e];
+  red[threadIdx.y][threadIdx.x] = s;
+  __syncthreads();
+  if (threadIdx.y == 0 && e < n) {
+    float t = 0.f;
+#pragma unroll
+    for (int g = 0; g < 8; ++g) t += red[g][threadIdx.x];
+    out[out_index(e)] = t;
+  }
 }
 
-// dW1: partial [split][j][i] -> flat W1[j][i]
+// dW2: partial element e = r*k + o with r = tap*bk + j -> flat W2[o][j][tap]
+__global__ void k_reduce_w2(const float* __restrict__ wpart, int splits, int bk, int k,
+                            float* __restrict__ dw2) {
+  const int64_t n = 9LL * bk * k;
+  fold_splits(wpart, splits, n, [=] __device__(int64_t e) {
+    const int o = static_cast<int>(e % k);
+    const int r = static_cast<int>(e / k);
+    const int tap = r / bk, j = r - tap * bk;
+    return (static_cast<int64_t>(o) * bk + j) * 9 + tap;
+  }, dw2);
+}
+
+// dW1 (SIMT partials [split][j][i]) -> flat W1[j][i]
 __global__ void k_reduce_w1(const float* __restrict__ wpart, int splits, int bk, int c,
                             float* __restrict__ dw1) {
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= bk * c) return;
-  float s = 0.f;
-  for (int z = 0; z < splits; ++z) s += wpart[static_cast<int64_t>(z) * bk * c + i];
-  dw1[i] = s;
+  fold_splits(wpart, splits, static_cast<int64_t>(bk) * c, [] __device__(int64_t e) { return e; },
+              dw1);
+}
+
+// dW1 from the tensor-core partials [split][i][j] -> flat W1[j][i]
+__global__ void k_reduce_w1t(const float* __restrict__ wpart, int splits, int bk, int c,
+                             float* __restrict__ dw1) {
+  fold_splits(wpart, splits, static_cast<int64_t>(bk) * c, [=] __device__(int64_t e) {
+    const int64_t i = e / bk, j = e - i * bk;
+    return j * c + i;
+  }, dw1);
 }
 
 // Statistics layout in the arena: fstat = mean[C] | var[C] for the feature
@@ -217,17 +241,6 @@ __device__ __forceinline__ float stat_at(int m, int c0, int k, int bk, int C,
     o += sz;
   }
   return 0.f;
-}
-
-// dW1 from the tensor-core wgrad partials [split][i][j] -> flat W1[j][i]
-__global__ void k_reduce_w1t(const float* __restrict__ wpart, int splits, int bk, int c,
-                             float* __restrict__ dw1) {
-  const int o = blockIdx.x * blockDim.x + threadIdx.x;  // flat (j, i)
-  if (o >= bk * c) return;
-  const int j = o / c, i = o - j * c;
-  float s = 0.f;
-  for (int z = 0; z < splits; ++z) s += wpart[(static_cast<int64_t>(z) * c + i) * bk + j];
-  dw1[o] = s;
 }
 
 // Running-statistics update for every BN of the block (ops.hpp:185-194):
