@@ -300,7 +300,9 @@ static void forward_impl(Block* b, const float* x_in, const float* params, float
     }
     {
       LaunchScope ls(b, KC_C1_FWD, M * (a.c + d.bk) * Sb, 2.0 * M * a.c * d.bk);
-      if (b->tc) tc_conv1x1_fwd(b, a);
+      if (b->tc) {
+        if (!tc2_conv1x1_fwd(b, a)) tc_conv1x1_fwd(b, a);
+      }
       else gemm_bn<128, Conv1x1Fwd>(b, a, g.M, d.bk, 1);
     }
     if (!eval) {

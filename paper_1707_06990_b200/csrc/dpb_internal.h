@@ -100,6 +100,7 @@ int64_t tc_halo_partials(const dpb_block_desc& d);
 int64_t tc_halo_wgrad_splits(const dpb_block_desc& d);
 void tc_conv1x1_dgrad(Block* b, const LayerArgs<float>& a);
 int tc_conv1x1_wgrad(Block* b, LayerArgs<float> a);
+bool tc2_conv1x1_fwd(Block* b, const LayerArgs<float>& a);
 int tc_conv3x3_wgrad(Block* b, LayerArgs<float> a);
 
 }  // namespace dpb

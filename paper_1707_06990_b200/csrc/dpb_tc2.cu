@@ -1,0 +1,96 @@
+// Launchers of the persistent TMA-fed engine (dpb_tc2.cuh) and the host-side
+// TMA tensor-map encoding (driver entry point cuTensorMapEncodeTiled).
+#include <cuda.h>
+#include <cudaTypedefs.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+
+#include "dpb_internal.h"
+#include "dpb_tc2.cuh"
+
+namespace dpb {
+
+static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    cudaDriverEntryPointQueryResult q;
+    void* p = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }
+  return fn;
+}
+
+// 2D fp32 tensor map over rows x cols (row pitch in elements), box
+// {box_cols, box_rows}, 128-byte swizzle, zero fill out of bounds.
+bool make_map_f32(CUtensorMap* m, const float* base, int64_t cols, int64_t rows, int64_t pitch,
+                  int box_cols, int box_rows) {
+  auto fn = encode_fn();
+  if (!fn || (reinterpret_cast<uintptr_t>(base) & 15) || (pitch * 4) % 16 != 0) return false;
+  cuuint64_t dims[2] = {static_cast<cuuint64_t>(cols), static_cast<cuuint64_t>(rows)};
+  cuuint64_t strides[1] = {static_cast<cuuint64_t>(pitch) * 4};
+  cuuint32_t box[2] = {static_cast<cuuint32_t>(box_cols), static_cast<cuuint32_t>(box_rows)};
+  cuuint32_t es[2] = {1, 1};
+  return fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(base), dims, strides, box, es,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+static int num_sms() {
+  static int n = 0;
+  if (!n) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+  }
+  return n;
+}
+
+template <class Op>
+static void launch2(Block* b, const Op& op, int ntiles, size_t aux) {
+  static bool configured = false;
+  if (!configured) {
+    cudaFuncAttributes fa{};
+    cudaFuncGetAttributes(&fa, tc2::tc2_kernel<Op>);
+    cudaFuncSetAttribute(tc2::tc2_kernel<Op>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         227 * 1024 - static_cast<int>(fa.sharedSizeBytes));
+    configured = true;
+  }
+  const size_t smem = 1024 + Op::kNR * Op::kRawBytes + Op::kNS * Op::kOpBytes + aux;
+  const int grid = std::min(ntiles, num_sms());
+  tc2::tc2_kernel<Op><<<grid, tc2::kThreads, smem, b->stream>>>(op);
+}
+
+template <class Op>
+static constexpr size_t fixed_smem() {
+  return 1024 + Op::kNR * Op::kRawBytes + Op::kNS * Op::kOpBytes;
+}
+
+// 1x1 forward on the v2 engine; false when the shape is not supported (the
+// caller then uses the v1 kernel).
+bool tc2_conv1x1_fwd(Block* b, const LayerArgs<float>& a) {
+  if (a.C % 4 != 0) return false;
+  const int ntiles = static_cast<int>((a.M + tc::kBM - 1) / tc::kBM);
+  const size_t aux = sizeof(BnFwd) * a.c;
+  auto go = [&](auto tag) -> bool {
+    using Op = decltype(tag);
+    if (fixed_smem<Op>() + aux > 220 * 1024) return false;
+    Op op{};
+    if (!make_map_f32(&op.xmap, a.feat, a.C, a.M, a.C, 32, tc::kBM)) return false;
+    op.a = a;
+    launch2(b, op, ntiles, aux);
+    return true;
+  };
+  const int n = (a.bk + 15) / 16 * 16;
+  if (n <= 16) return go(tc2::Fwd1x1<16>{});
+  if (n <= 32) return go(tc2::Fwd1x1<32>{});
+  if (n <= 48) return go(tc2::Fwd1x1<48>{});
+  if (n <= 64) return go(tc2::Fwd1x1<64>{});
+  if (n <= 128) return go(tc2::Fwd1x1<128>{});
+  if (n <= 192) return go(tc2::Fwd1x1<192>{});
+  return false;
+}
+
+}  // namespace dpb

@@ -1,0 +1,318 @@
+// Persistent, warp-specialised tcgen05 engine fed by TMA (engine v2).
+//
+// One CTA per SM loops over output tiles (tile = blockIdx.x, += gridDim.x).
+// Warp roles (448 threads):
+//   warp 0        TMA: streams the op's raw fp32 tiles (2D tensor maps,
+//                 128-byte swizzle) into a ring of kNR raw stages
+//   warp 1        MMA: one elected thread issues tcgen05.mma per operand
+//                 stage into one of two TMEM accumulators, commits stages
+//                 back to the transform warps and finished accumulators to
+//                 the epilogue
+//   warps 2-5     epilogue: tcgen05.ld the accumulator of tile i while the
+//                 MMA already accumulates tile i+1 into the other buffer
+//   warps 6-13    transform: raw fp32 smem -> fused BN/ReLU (or BN backward)
+//                 -> bf16 (hi/lo for the bf16x3 forward) UMMA operand stages
+// Every hand-off is an mbarrier (TMA tx-count, tcgen05.commit, or warp
+// arrivals), so HBM loads, operand transforms, MMAs and epilogues of
+// different tiles overlap — the per-tile latency chain of the v1 engine is
+// gone.  Deterministic: each tile's column reductions are written to its own
+// partial slot.
+#pragma once
+
+#include <cuda.h>
+
+#include "dpb_simt.cuh"
+#include "dpb_tc.cuh"
+#include "dpb_tc_ops.cuh"
+
+namespace dpb {
+namespace tc2 {
+
+using tc::kBK;
+using tc::kBM;
+
+constexpr int kTmaWarp = 0, kMmaWarp = 1, kEpiWarp0 = 2, kNumEpiWarps = 4;
+constexpr int kXfWarp0 = 6, kNumXfWarps = 8;
+constexpr int kXfThreads = 32 * kNumXfWarps;
+constexpr int kThreads = 32 * (kXfWarp0 + kNumXfWarps);  // 448
+
+// ---- PTX ----------------------------------------------------------------------
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(tc::smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(tc::smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap* map, int c0, int c1,
+                                            uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes "
+      "[%0], [%1, {%2, %3}], [%4];" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(tc::smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void prefetch_tmap(const CUtensorMap* map) {
+  asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(map)) : "memory");
+}
+__device__ __forceinline__ void named_sync(int id, int count) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(count) : "memory");
+}
+
+// Raw fp32 tile loaded by TMA with 128-byte swizzle: box = 32 channels x rows.
+// Element (row, ch) of box b lives at b*box_bytes + row*128 + (((ch/4) ^ (row%8))*16) + (ch%4)*4.
+// Reads 8 consecutive channels (two 16-byte chunks) starting at ch (ch % 8 == 0).
+__device__ __forceinline__ void raw_read8(const uint8_t* box, int row, int ch, float (&v)[8]) {
+  const int c4 = ch >> 2;
+  const float4 a = *reinterpret_cast<const float4*>(box + row * 128 + (((c4) ^ (row & 7)) << 4));
+  const float4 b = *reinterpret_cast<const float4*>(box + row * 128 + (((c4 + 1) ^ (row & 7)) << 4));
+  v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w;
+  v[4] = b.x; v[5] = b.y; v[6] = b.z; v[7] = b.w;
+}
+
+// ---- the engine ------------------------------------------------------------------
+// Op interface:
+//   static constexpr int BN, kTmemCols, kNR, kNS, kRawBytes, kOpBytes; bool kColSums
+//   int num_tiles() const;  int num_kb(int tile) const;  void prefetch() const;
+//   void prologue(uint8_t* aux) const;                         all threads
+//   void tma(int tile, int kb, uint32_t raw, uint64_t* bar) const;   one thread; issues
+//                                                              exactly kRawBytes
+//   void transform(int tile, int kb, const uint8_t* raw, uint8_t* opnd,
+//                  const uint8_t* aux, int xt) const;          256 transform threads
+//   void mma(uint32_t opnd, uint32_t tmem, int kb) const;      one thread
+//   void epilogue(int tile, int row, int col0, const float (&v)[8], const uint8_t* aux,
+//                 float (&s1)[8], float (&s2)[8]) const;       128 epilogue threads
+//   void col_sums(int tile, int col, double s1, double s2) const;
+template <class Op>
+__global__ void __launch_bounds__(kThreads, 1) tc2_kernel(const __grid_constant__ Op op) {
+  constexpr int NR = Op::kNR, NS = Op::kNS, BN = Op::BN;
+  constexpr uint32_t TC = tc::TmemCols<Op::kTmemCols>::value;
+  static_assert(2 * TC <= 512, "two TMEM accumulators");
+  extern __shared__ __align__(1024) uint8_t smem_dyn[];
+  // TMA 128-byte swizzle needs 1024-byte aligned destinations
+  uint8_t* smem = smem_dyn + ((1024 - (tc::smem_u32(smem_dyn) & 1023)) & 1023);
+  __shared__ uint64_t raw_full[NR], raw_empty[NR], op_full[NS], op_empty[NS];
+  __shared__ uint64_t acc_full[2], acc_empty[2];
+  __shared__ uint32_t tmem_base;
+  __shared__ float red[2][4][BN];
+
+  uint8_t* raw_ring = smem;
+  uint8_t* op_ring = smem + NR * Op::kRawBytes;
+  uint8_t* aux = op_ring + NS * Op::kOpBytes;
+
+  const int tid = threadIdx.x;
+  const int warp = tid / 32, lane = tid % 32;
+  if (tid == 0) {
+    for (int i = 0; i < NR; ++i) {
+      tc::mbar_init(&raw_full[i], 1);
+      tc::mbar_init(&raw_empty[i], kNumXfWarps);
+    }
+    for (int i = 0; i < NS; ++i) {
+      tc::mbar_init(&op_full[i], kNumXfWarps);
+      tc::mbar_init(&op_empty[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      tc::mbar_init(&acc_full[i], 1);
+      tc::mbar_init(&acc_empty[i], kNumEpiWarps);
+    }
+    tc::fence_barrier_init();
+  }
+  if (warp == kMmaWarp) tc::tmem_alloc<2 * TC>(&tmem_base);
+  op.prologue(aux);
+  tc::tc_fence_before();
+  __syncthreads();
+  tc::tc_fence_after();
+  const uint32_t tmem = tmem_base;
+  const int ntiles = op.num_tiles();
+
+  if (warp == kTmaWarp) {
+    if (lane == 0) {
+      op.prefetch();
+      int it = 0;
+      for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x)
+        for (int kb = 0; kb < op.num_kb(tile); ++kb, ++it) {
+          const int r = it % NR;
+          tc::mbar_wait(&raw_empty[r], ((it / NR) & 1) ^ 1);
+          mbar_expect_tx(&raw_full[r], Op::kRawBytes);
+          op.tma(tile, kb, tc::smem_u32(raw_ring + r * Op::kRawBytes), &raw_full[r]);
+        }
+    }
+  } else if (warp == kMmaWarp) {
+    if (lane == 0) {
+      int it = 0, at = 0;
+      for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++at) {
+        const int a = at & 1;
+        tc::mbar_wait(&acc_empty[a], ((at >> 1) & 1) ^ 1);
+        tc::tc_fence_after();
+        for (int kb = 0; kb < op.num_kb(tile); ++kb, ++it) {
+          const int s = it % NS;
+          tc::mbar_wait(&op_full[s], (it / NS) & 1);
+          tc::tc_fence_after();
+          op.mma(tc::smem_u32(op_ring + s * Op::kOpBytes), tmem + a * TC, kb);
+          tc::mma_commit(&op_empty[s]);
+        }
+        tc::mma_commit(&acc_full[a]);
+      }
+    }
+  } else if (warp >= kEpiWarp0 && warp < kEpiWarp0 + kNumEpiWarps) {
+    const int quarter = warp & 3;
+    const int row = quarter * 32 + lane;
+    const int et = tid - kEpiWarp0 * 32;  // 0..127
+    int at = 0;
+    for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++at) {
+      const int a = at & 1;
+      tc::mbar_wait(&acc_full[a], (at >> 1) & 1);
+      tc::tc_fence_after();
+      for (int cc = 0; cc < Op::kTmemCols / 8; ++cc) {
+        float v[8];
+        tc::tmem_ld8(tmem + a * TC + (static_cast<uint32_t>(quarter * 32) << 16) + cc * 8, v);
+        float s1[8], s2[8];
+        op.epilogue(tile, row, cc * 8, v, aux, s1, s2);
+        if constexpr (Op::kColSums) {
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            float x = s1[i], y = s2[i];
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) {
+              x += __shfl_xor_sync(0xffffffffu, x, o);
+              y += __shfl_xor_sync(0xffffffffu, y, o);
+            }
+            if (lane == 0 && cc * 8 + i < BN) {
+              red[0][quarter][cc * 8 + i] = x;
+              red[1][quarter][cc * 8 + i] = y;
+            }
+          }
+        }
+      }
+      tc::tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&acc_empty[a]);
+      if constexpr (Op::kColSums) {
+        named_sync(1, 32 * kNumEpiWarps);
+        for (int c = et; c < BN; c += 32 * kNumEpiWarps) {
+          const double x = static_cast<double>(red[0][0][c]) + red[0][1][c] + red[0][2][c] + red[0][3][c];
+          const double y = static_cast<double>(red[1][0][c]) + red[1][1][c] + red[1][2][c] + red[1][3][c];
+          op.col_sums(tile, c, x, y);
+        }
+        named_sync(1, 32 * kNumEpiWarps);
+      }
+    }
+  } else {
+    const int xt = tid - kXfWarp0 * 32;  // 0..255
+    int it = 0;
+    for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x)
+      for (int kb = 0; kb < op.num_kb(tile); ++kb, ++it) {
+        const int r = it % NR, s = it % NS;
+        tc::mbar_wait(&raw_full[r], (it / NR) & 1);
+        tc::mbar_wait(&op_empty[s], ((it / NS) & 1) ^ 1);
+        op.transform(tile, kb, raw_ring + r * Op::kRawBytes, op_ring + s * Op::kOpBytes, aux, xt);
+        tc::fence_proxy_async();
+        __syncwarp();
+        if (lane == 0) {
+          mbar_arrive(&op_full[s]);
+          mbar_arrive(&raw_empty[r]);
+        }
+      }
+  }
+  tc::tc_fence_before();
+  __syncthreads();
+  if (warp == kMmaWarp) {
+    tc::tc_fence_after();
+    tc::tmem_dealloc<2 * TC>(tmem);
+  }
+}
+
+// ---- 1x1 forward: z = relu(bn_a(x)) . W1^T (bf16x3) ---------------------------------
+// raw stage: x rows [m0, m0+128) x channels [64 kb, 64 kb + 64) as two
+// 32-channel TMA boxes; operand stage: A hi | A lo | B hi | B lo.
+template <int BN_>
+struct Fwd1x1 {
+  static constexpr int BN = BN_;
+  static constexpr int kTmemCols = BN;
+  static constexpr bool kColSums = true;
+  static constexpr int kNR = 3;
+  static constexpr int kNS = BN <= 64 ? 2 : 1;
+  static constexpr int kBox = 32 * kBM * 4;                    // 16 KB
+  static constexpr int kRawBytes = 2 * kBox;
+  static constexpr int kABytes = tc::Tile<kBM>::kBytes;         // 16 KB
+  static constexpr int kBBytes = tc::Tile<BN>::kBytes;
+  static constexpr int kOpBytes = 2 * (kABytes + kBBytes);
+  CUtensorMap xmap;  // feat [M][C] fp32, box {32, 128}, swizzle 128B
+  LayerArgs<float> a;
+
+  __device__ void prefetch() const { prefetch_tmap(&xmap); }
+  __device__ int num_tiles() const { return static_cast<int>((a.M + kBM - 1) / kBM); }
+  __device__ int num_kb(int) const { return (a.c + kBK - 1) / kBK; }
+  __device__ void prologue(uint8_t* aux) const {
+    fill_bn_fwd(reinterpret_cast<BnFwd*>(aux), a.c, 0, a.amean, a.avar, a.gamma_a, a.beta_a);
+  }
+  __device__ void tma(int tile, int kb, uint32_t raw, uint64_t* bar) const {
+    tma_load_2d(raw, &xmap, kb * kBK, tile * kBM, bar);
+    tma_load_2d(raw + kBox, &xmap, kb * kBK + 32, tile * kBM, bar);
+  }
+  __device__ void transform(int, int kb, const uint8_t* raw, uint8_t* op, const uint8_t* aux,
+                            int xt) const {
+    const BnFwd* bn = reinterpret_cast<const BnFwd*>(aux);
+    uint8_t* ah = op;
+    uint8_t* al = op + kABytes;
+    uint8_t* bh = op + 2 * kABytes;
+    uint8_t* bl = bh + kBBytes;
+#pragma unroll
+    for (int i = 0; i < kBM * kBK / 8 / kXfThreads; ++i) {
+      int row, kc;
+      tc::kmajor_coords(xt + i * kXfThreads, row, kc);
+      float v[8];
+      raw_read8(raw + (kc >> 5) * kBox, row, kc & 31, v);
+      const int ch0 = kb * kBK + kc;
+      tc::bnrelu8(bn, ch0, a.c - ch0, v);
+      uint4 h, l;
+      tc::split8(v, h, l);
+      const uint32_t off = tc::Tile<kBM>::kmajor_chunk(row, kc);
+      tc::st_shared16(ah, off, h);
+      tc::st_shared16(al, off, l);
+    }
+    for (int q = xt; q < BN * kBK / 8; q += kXfThreads) {
+      int row, kc;
+      tc::kmajor_coords(q, row, kc);
+      const int i0 = kb * kBK + kc;
+      float v[8];
+      if (row < a.bk && i0 < a.c) tc::load8(a.w1 + static_cast<int64_t>(row) * a.c + i0, a.c - i0, false, v);
+      else tc::zero8(v);
+      uint4 h, l;
+      tc::split8(v, h, l);
+      const uint32_t off = tc::Tile<BN>::kmajor_chunk(row, kc);
+      tc::st_shared16(bh, off, h);
+      tc::st_shared16(bl, off, l);
+    }
+  }
+  __device__ void mma(uint32_t op, uint32_t tmem, int kb) const {
+    constexpr uint32_t idesc = tc::make_idesc(BN, 0, 0);
+    const uint32_t ah = op, al = op + kABytes, bh = op + 2 * kABytes, bl = bh + kBBytes;
+#pragma unroll
+    for (int k16 = 0; k16 < kBK / 16; ++k16) {
+      const uint32_t acc = (kb | k16) ? 1u : 0u;
+      tc::mma_bf16(tmem, tc::Tile<kBM>::desc(ah, k16), tc::Tile<BN>::desc(bh, k16), idesc, acc);
+      tc::mma_bf16(tmem, tc::Tile<kBM>::desc(ah, k16), tc::Tile<BN>::desc(bl, k16), idesc, 1u);
+      tc::mma_bf16(tmem, tc::Tile<kBM>::desc(al, k16), tc::Tile<BN>::desc(bh, k16), idesc, 1u);
+    }
+  }
+  __device__ void epilogue(int tile, int row, int col0, const float (&v)[8], const uint8_t*,
+                           float (&s1)[8], float (&s2)[8]) const {
+    const int64_t p = static_cast<int64_t>(tile) * kBM + row;
+    const int nv = p < a.M ? a.bk - col0 : 0;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const bool ok = i < nv;
+      s1[i] = ok ? v[i] : 0.f;
+      s2[i] = ok ? v[i] * v[i] : 0.f;
+    }
+    if (nv > 0) tc::store8(a.z + p * a.bk + col0, nv, (a.bk & 3) == 0, v);
+  }
+  __device__ void col_sums(int tile, int c, double s1, double s2) const {
+    if (c < a.bk) a.part[static_cast<int64_t>(tile) * a.bk + c] = make_double2(s1, s2);
+  }
+};
+
+}  // namespace tc2
+}  // namespace dpb
