@@ -162,6 +162,13 @@ void plan_arena(const dpb_block_desc& d, dpb_arena_sizes* s) {
   const int64_t scratch = align_up(pbytes, 256) + align_up(wmax * 4, 256) +
                           align_up((2LL * d.bk + 2 * g.cmax) * 4, 256);
   take(scratch, &s->scratch_offset, &s->scratch_bytes);
+  // pre-tiled bf16 weight operands of the tensor-core path (counted as scratch)
+  if (d.dtype == DPB_BF16 && tc_supported(d)) {
+    int64_t wt = 0;
+    for (int l = 0; l < d.m; ++l) wt += tc2_w1_tile_bytes(d, l);
+    s->scratch_bytes += align_up(wt, 256);
+    off = align_up(off + align_up(wt, 256), 256);
+  }
   s->total_bytes = off;
   s->shared1_bytes = 0;
   s->shared2_bytes = 0;
@@ -275,6 +282,11 @@ static void forward_impl(Block* b, const float* x_in, const float* params, float
           x_in, d.c0, g.M, d.c0, feat, static_cast<int>(g.C), 0);
     }
   }
+  if (b->tc) {
+    LaunchScope ls(b, KC_PACK, 0, 0);
+    b->launches--;  // counted inside tc2_pretile_w1
+    tc2_pretile_w1(b, params);
+  }
   const double count = M;
   float* fmean = b->fstat;
   float* fvar = b->fstat + g.C;
@@ -301,7 +313,7 @@ static void forward_impl(Block* b, const float* x_in, const float* params, float
     {
       LaunchScope ls(b, KC_C1_FWD, M * (a.c + d.bk) * Sb, 2.0 * M * a.c * d.bk);
       if (b->tc) {
-        if (!tc2_conv1x1_fwd(b, a)) tc_conv1x1_fwd(b, a);
+        if (!tc2_conv1x1_fwd(b, a, l)) tc_conv1x1_fwd(b, a);
       }
       else gemm_bn<128, Conv1x1Fwd>(b, a, g.M, d.bk, 1);
     }
@@ -534,8 +546,25 @@ int create(const dpb_block_desc* desc, int device, void* stream, Block** out) {
   b->wpart = reinterpret_cast<float*>(sc + pbytes);
   // wgrad partial region size = scratch - pbytes - coef region
   const int64_t coef_bytes = align_up((2LL * desc->bk + 2 * b->g.cmax) * 4, 256);
-  b->bnb_bwd = reinterpret_cast<float*>(sc + b->sz.scratch_bytes - coef_bytes);
+  int64_t wsum_all = 0;
+  if (b->tc)
+    for (int l = 0; l < desc->m; ++l) wsum_all += tc2_w1_tile_bytes(*desc, l);
+  const int64_t wt_bytes = wsum_all > 0 ? align_up(wsum_all, 256) : 0;
+  b->bnb_bwd = reinterpret_cast<float*>(sc + b->sz.scratch_bytes - wt_bytes - coef_bytes);
   b->bna_bwd = b->bnb_bwd + 2 * desc->bk;
+  if (b->tc) {
+    // the pre-tiled weights follow the scratch partials/coefficients
+    int64_t wt = 0, wsum = 0;
+    for (int l = 0; l < desc->m; ++l) wsum += tc2_w1_tile_bytes(*desc, l);
+    if (wsum > 0) {
+      b->wtile = reinterpret_cast<uint8_t*>(base + b->sz.scratch_offset + b->sz.scratch_bytes -
+                                            align_up(wsum, 256));
+      for (int l = 0; l < desc->m; ++l) {
+        b->wtile_off.push_back(wt);
+        wt += tc2_w1_tile_bytes(*desc, l);
+      }
+    }
+  }
   int64_t po = 0, so = 0;
   for (int l = 0; l < desc->m; ++l) {
     const int64_t c = desc->c0 + static_cast<int64_t>(l) * desc->k;

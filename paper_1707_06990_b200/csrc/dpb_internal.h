@@ -53,6 +53,8 @@ struct Block {
   float* bnb_bwd = nullptr;  // [bk][2]
   float* bna_bwd = nullptr;  // [cmax][2]
   std::vector<int64_t> param_off, stat_off;
+  uint8_t* wtile = nullptr;           // pre-tiled bf16 W1 operands (tensor-core path)
+  std::vector<int64_t> wtile_off;
   bool tc = false;                    // tensor-core (tcgen05) GEMMs
   bool fwd_done = false;
   int64_t launches = 0;
@@ -100,7 +102,9 @@ int64_t tc_halo_partials(const dpb_block_desc& d);
 int64_t tc_halo_wgrad_splits(const dpb_block_desc& d);
 void tc_conv1x1_dgrad(Block* b, const LayerArgs<float>& a);
 int tc_conv1x1_wgrad(Block* b, LayerArgs<float> a);
-bool tc2_conv1x1_fwd(Block* b, const LayerArgs<float>& a);
+bool tc2_conv1x1_fwd(Block* b, const LayerArgs<float>& a, int l);
+int64_t tc2_w1_tile_bytes(const dpb_block_desc& d, int l);
+void tc2_pretile_w1(Block* b, const float* params);
 int tc_conv3x3_wgrad(Block* b, LayerArgs<float> a);
 
 }  // namespace dpb

@@ -68,29 +68,67 @@ static constexpr size_t fixed_smem() {
   return 1024 + Op::kNR * Op::kRawBytes + Op::kNS * Op::kOpBytes;
 }
 
+int tc2_bn_1x1(int bk) {
+  const int n = (bk + 15) / 16 * 16;
+  if (n <= 16) return 16;
+  if (n <= 32) return 32;
+  if (n <= 48) return 48;
+  if (n <= 64) return 64;
+  if (n <= 128) return 128;
+  if (n <= 192) return 192;
+  return 0;
+}
+
+// bytes of the pre-tiled W1 operands of layer l (0 when unsupported)
+int64_t tc2_w1_tile_bytes(const dpb_block_desc& d, int l) {
+  const int bn = tc2_bn_1x1(d.bk);
+  if (!bn) return 0;
+  const int c = d.c0 + l * d.k;
+  return static_cast<int64_t>((c + tc::kBK - 1) / tc::kBK) * 2 * (bn * tc::kBK * 2);
+}
+
+void tc2_pretile_w1(Block* b, const float* params) {
+  const dpb_block_desc& d = b->d;
+  const int bn = tc2_bn_1x1(d.bk);
+  if (!bn || !b->wtile) return;
+  const dim3 grid(16, d.m);
+  switch (bn) {
+    case 16: tc2::k_pretile_w1_all<16><<<grid, 256, 0, b->stream>>>(params, d.c0, d.k, d.bk, d.m, b->wtile); break;
+    case 32: tc2::k_pretile_w1_all<32><<<grid, 256, 0, b->stream>>>(params, d.c0, d.k, d.bk, d.m, b->wtile); break;
+    case 48: tc2::k_pretile_w1_all<48><<<grid, 256, 0, b->stream>>>(params, d.c0, d.k, d.bk, d.m, b->wtile); break;
+    case 64: tc2::k_pretile_w1_all<64><<<grid, 256, 0, b->stream>>>(params, d.c0, d.k, d.bk, d.m, b->wtile); break;
+    case 128: tc2::k_pretile_w1_all<128><<<grid, 256, 0, b->stream>>>(params, d.c0, d.k, d.bk, d.m, b->wtile); break;
+    default: tc2::k_pretile_w1_all<192><<<grid, 256, 0, b->stream>>>(params, d.c0, d.k, d.bk, d.m, b->wtile); break;
+  }
+  b->launches++;
+}
+
 // 1x1 forward on the v2 engine; false when the shape is not supported (the
 // caller then uses the v1 kernel).
-bool tc2_conv1x1_fwd(Block* b, const LayerArgs<float>& a) {
-  if (a.C % 4 != 0) return false;
+bool tc2_conv1x1_fwd(Block* b, const LayerArgs<float>& a, int l) {
+  if (a.C % 4 != 0 || !b->wtile) return false;
   const int ntiles = static_cast<int>((a.M + tc::kBM - 1) / tc::kBM);
   const size_t aux = sizeof(BnFwd) * a.c;
+  const uint8_t* w1t = b->wtile + b->wtile_off[l];
   auto go = [&](auto tag) -> bool {
     using Op = decltype(tag);
     if (fixed_smem<Op>() + aux > 220 * 1024) return false;
     Op op{};
     if (!make_map_f32(&op.xmap, a.feat, a.C, a.M, a.C, 32, tc::kBM)) return false;
     op.a = a;
+    op.w1t = w1t;
     launch2(b, op, ntiles, aux);
     return true;
   };
-  const int n = (a.bk + 15) / 16 * 16;
-  if (n <= 16) return go(tc2::Fwd1x1<16>{});
-  if (n <= 32) return go(tc2::Fwd1x1<32>{});
-  if (n <= 48) return go(tc2::Fwd1x1<48>{});
-  if (n <= 64) return go(tc2::Fwd1x1<64>{});
-  if (n <= 128) return go(tc2::Fwd1x1<128>{});
-  if (n <= 192) return go(tc2::Fwd1x1<192>{});
-  return false;
+  switch (tc2_bn_1x1(a.bk)) {
+    case 16: return go(tc2::Fwd1x1<16>{});
+    case 32: return go(tc2::Fwd1x1<32>{});
+    case 48: return go(tc2::Fwd1x1<48>{});
+    case 64: return go(tc2::Fwd1x1<64>{});
+    case 128: return go(tc2::Fwd1x1<128>{});
+    case 192: return go(tc2::Fwd1x1<192>{});
+    default: return false;
+  }
 }
 
 }  // namespace dpb

@@ -53,6 +53,14 @@ __device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap* map
       "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(tc::smem_u32(bar))
       : "memory");
 }
+__device__ __forceinline__ void bulk_load(uint32_t dst, const void* src, uint32_t bytes,
+                                          uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          dst),
+      "l"(reinterpret_cast<uint64_t>(src)), "r"(bytes), "r"(tc::smem_u32(bar))
+      : "memory");
+}
 __device__ __forceinline__ void prefetch_tmap(const CUtensorMap* map) {
   asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(map)) : "memory");
 }
@@ -76,11 +84,13 @@ __device__ __forceinline__ void raw_read8(const uint8_t* box, int row, int ch, f
 //   static constexpr int BN, kTmemCols, kNR, kNS, kRawBytes, kOpBytes; bool kColSums
 //   int num_tiles() const;  int num_kb(int tile) const;  void prefetch() const;
 //   void prologue(uint8_t* aux) const;                         all threads
-//   void tma(int tile, int kb, uint32_t raw, uint64_t* bar) const;   one thread; issues
-//                                                              exactly kRawBytes
+//   uint32_t raw_bytes(int tile, int kb) const;                bytes the stage's copies land
+//   void tma(int tile, int kb, uint32_t raw, uint64_t* bar) const;   one thread
+//   static constexpr bool kMmaReadsRaw;                         MMA reads pre-tiled B from
+//                                                              the raw stage
 //   void transform(int tile, int kb, const uint8_t* raw, uint8_t* opnd,
 //                  const uint8_t* aux, int xt) const;          256 transform threads
-//   void mma(uint32_t opnd, uint32_t tmem, int kb) const;      one thread
+//   void mma(uint32_t opnd, uint32_t raw, uint32_t tmem, int kb) const;   one thread
 //   void epilogue(int tile, int row, int col0, const float (&v)[8], const uint8_t* aux,
 //                 float (&s1)[8], float (&s2)[8]) const;       128 epilogue threads
 //   void col_sums(int tile, int col, double s1, double s2) const;
@@ -106,7 +116,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc2_kernel(const __grid_constant_
   if (tid == 0) {
     for (int i = 0; i < NR; ++i) {
       tc::mbar_init(&raw_full[i], 1);
-      tc::mbar_init(&raw_empty[i], kNumXfWarps);
+      tc::mbar_init(&raw_empty[i], kNumXfWarps + (Op::kMmaReadsRaw ? 1 : 0));
     }
     for (int i = 0; i < NS; ++i) {
       tc::mbar_init(&op_full[i], kNumXfWarps);
@@ -134,7 +144,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc2_kernel(const __grid_constant_
         for (int kb = 0; kb < op.num_kb(tile); ++kb, ++it) {
           const int r = it % NR;
           tc::mbar_wait(&raw_empty[r], ((it / NR) & 1) ^ 1);
-          mbar_expect_tx(&raw_full[r], Op::kRawBytes);
+          mbar_expect_tx(&raw_full[r], op.raw_bytes(tile, kb));
           op.tma(tile, kb, tc::smem_u32(raw_ring + r * Op::kRawBytes), &raw_full[r]);
         }
     }
@@ -146,11 +156,13 @@ __global__ void __launch_bounds__(kThreads, 1) tc2_kernel(const __grid_constant_
         tc::mbar_wait(&acc_empty[a], ((at >> 1) & 1) ^ 1);
         tc::tc_fence_after();
         for (int kb = 0; kb < op.num_kb(tile); ++kb, ++it) {
-          const int s = it % NS;
+          const int s = it % NS, r = it % NR;
           tc::mbar_wait(&op_full[s], (it / NS) & 1);
           tc::tc_fence_after();
-          op.mma(tc::smem_u32(op_ring + s * Op::kOpBytes), tmem + a * TC, kb);
+          op.mma(tc::smem_u32(op_ring + s * Op::kOpBytes), tc::smem_u32(raw_ring + r * Op::kRawBytes),
+                 tmem + a * TC, kb);
           tc::mma_commit(&op_empty[s]);
+          if constexpr (Op::kMmaReadsRaw) tc::mma_commit(&raw_empty[r]);
         }
         tc::mma_commit(&acc_full[a]);
       }
@@ -224,71 +236,68 @@ __global__ void __launch_bounds__(kThreads, 1) tc2_kernel(const __grid_constant_
 }
 
 // ---- 1x1 forward: z = relu(bn_a(x)) . W1^T (bf16x3) ---------------------------------
-// raw stage: x rows [m0, m0+128) x channels [64 kb, 64 kb + 64) as two
-// 32-channel TMA boxes; operand stage: A hi | A lo | B hi | B lo.
+// raw stage: x rows [m0, m0+128) x channels [64 kb, 64 kb + 64) as one or two
+// 32-channel TMA boxes (only the boxes that hold channels < c), then W1's
+// pre-tiled bf16 hi | lo operand tiles for this K block (1D bulk copy; the
+// MMA reads them in place).  Operand stage: A hi | A lo.
 template <int BN_>
 struct Fwd1x1 {
   static constexpr int BN = BN_;
   static constexpr int kTmemCols = BN;
   static constexpr bool kColSums = true;
-  static constexpr int kNR = 3;
-  static constexpr int kNS = BN <= 64 ? 2 : 1;
+  static constexpr bool kMmaReadsRaw = true;
   static constexpr int kBox = 32 * kBM * 4;                    // 16 KB
-  static constexpr int kRawBytes = 2 * kBox;
-  static constexpr int kABytes = tc::Tile<kBM>::kBytes;         // 16 KB
   static constexpr int kBBytes = tc::Tile<BN>::kBytes;
-  static constexpr int kOpBytes = 2 * (kABytes + kBBytes);
-  CUtensorMap xmap;  // feat [M][C] fp32, box {32, 128}, swizzle 128B
+  static constexpr int kRawBytes = 2 * kBox + 2 * kBBytes;
+  static constexpr int kNR = BN <= 64 ? 3 : 2;
+  static constexpr int kABytes = tc::Tile<kBM>::kBytes;         // 16 KB
+  static constexpr int kOpBytes = 2 * kABytes;
+  static constexpr int kNS = 2;
+  CUtensorMap xmap;        // feat [M][C] fp32, box {32, 128}, swizzle 128B
   LayerArgs<float> a;
+  const uint8_t* w1t;      // pre-tiled W1: per K block, hi tile | lo tile (Tile<BN> K-major)
 
   __device__ void prefetch() const { prefetch_tmap(&xmap); }
   __device__ int num_tiles() const { return static_cast<int>((a.M + kBM - 1) / kBM); }
   __device__ int num_kb(int) const { return (a.c + kBK - 1) / kBK; }
+  __device__ int boxes(int kb) const { return a.c - kb * kBK > 32 ? 2 : 1; }
+  __device__ uint32_t raw_bytes(int, int kb) const { return boxes(kb) * kBox + 2 * kBBytes; }
   __device__ void prologue(uint8_t* aux) const {
     fill_bn_fwd(reinterpret_cast<BnFwd*>(aux), a.c, 0, a.amean, a.avar, a.gamma_a, a.beta_a);
   }
   __device__ void tma(int tile, int kb, uint32_t raw, uint64_t* bar) const {
     tma_load_2d(raw, &xmap, kb * kBK, tile * kBM, bar);
-    tma_load_2d(raw + kBox, &xmap, kb * kBK + 32, tile * kBM, bar);
+    if (boxes(kb) == 2) tma_load_2d(raw + kBox, &xmap, kb * kBK + 32, tile * kBM, bar);
+    bulk_load(raw + 2 * kBox, w1t + static_cast<int64_t>(kb) * 2 * kBBytes, 2 * kBBytes, bar);
   }
   __device__ void transform(int, int kb, const uint8_t* raw, uint8_t* op, const uint8_t* aux,
                             int xt) const {
     const BnFwd* bn = reinterpret_cast<const BnFwd*>(aux);
     uint8_t* ah = op;
     uint8_t* al = op + kABytes;
-    uint8_t* bh = op + 2 * kABytes;
-    uint8_t* bl = bh + kBBytes;
 #pragma unroll
     for (int i = 0; i < kBM * kBK / 8 / kXfThreads; ++i) {
       int row, kc;
       tc::kmajor_coords(xt + i * kXfThreads, row, kc);
-      float v[8];
-      raw_read8(raw + (kc >> 5) * kBox, row, kc & 31, v);
       const int ch0 = kb * kBK + kc;
-      tc::bnrelu8(bn, ch0, a.c - ch0, v);
+      float v[8];
+      if (ch0 < a.c) {
+        raw_read8(raw + (kc >> 5) * kBox, row, kc & 31, v);
+        tc::bnrelu8(bn, ch0, a.c - ch0, v);
+      } else {
+        tc::zero8(v);
+      }
       uint4 h, l;
       tc::split8(v, h, l);
       const uint32_t off = tc::Tile<kBM>::kmajor_chunk(row, kc);
       tc::st_shared16(ah, off, h);
       tc::st_shared16(al, off, l);
     }
-    for (int q = xt; q < BN * kBK / 8; q += kXfThreads) {
-      int row, kc;
-      tc::kmajor_coords(q, row, kc);
-      const int i0 = kb * kBK + kc;
-      float v[8];
-      if (row < a.bk && i0 < a.c) tc::load8(a.w1 + static_cast<int64_t>(row) * a.c + i0, a.c - i0, false, v);
-      else tc::zero8(v);
-      uint4 h, l;
-      tc::split8(v, h, l);
-      const uint32_t off = tc::Tile<BN>::kmajor_chunk(row, kc);
-      tc::st_shared16(bh, off, h);
-      tc::st_shared16(bl, off, l);
-    }
   }
-  __device__ void mma(uint32_t op, uint32_t tmem, int kb) const {
+  __device__ void mma(uint32_t op, uint32_t raw, uint32_t tmem, int kb) const {
     constexpr uint32_t idesc = tc::make_idesc(BN, 0, 0);
-    const uint32_t ah = op, al = op + kABytes, bh = op + 2 * kABytes, bl = bh + kBBytes;
+    const uint32_t ah = op, al = op + kABytes;
+    const uint32_t bh = raw + 2 * kBox, bl = bh + kBBytes;
 #pragma unroll
     for (int k16 = 0; k16 < kBK / 16; ++k16) {
       const uint32_t acc = (kb | k16) ? 1u : 0u;
@@ -313,6 +322,38 @@ struct Fwd1x1 {
     if (c < a.bk) a.part[static_cast<int64_t>(tile) * a.bk + c] = make_double2(s1, s2);
   }
 };
+
+// All layers of a block in one launch: blockIdx.y = layer.
+template <int BN>
+__global__ void k_pretile_w1_all(const float* __restrict__ params, int c0, int k, int bk, int m,
+                                 uint8_t* __restrict__ out) {
+  const int l = blockIdx.y;
+  int64_t poff = 0, toff = 0;
+  for (int j = 0; j < l; ++j) {
+    const int cj = c0 + j * k;
+    poff += 2LL * cj + static_cast<int64_t>(bk) * cj + 2LL * bk + 9LL * k * bk;
+    toff += static_cast<int64_t>((cj + kBK - 1) / kBK) * 2 * tc::Tile<BN>::kBytes;
+  }
+  const int c = c0 + l * k;
+  const float* w1 = params + poff + 2 * c;
+  const int nkb = (c + kBK - 1) / kBK;
+  const int chunks = BN * kBK / 8;
+  for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < nkb * chunks; q += gridDim.x * blockDim.x) {
+    const int kb = q / chunks, qq = q - kb * chunks;
+    const int row = qq / 8, kc = (qq % 8) * 8;
+    const int i0 = kb * kBK + kc;
+    float v[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+      v[i] = (row < bk && i0 + i < c) ? w1[static_cast<int64_t>(row) * c + i0 + i] : 0.f;
+    uint4 h, lo;
+    tc::split8(v, h, lo);
+    uint8_t* t = out + toff + static_cast<int64_t>(kb) * 2 * tc::Tile<BN>::kBytes;
+    const uint32_t off = tc::Tile<BN>::kmajor_chunk(row, kc);
+    *reinterpret_cast<uint4*>(t + off) = h;
+    *reinterpret_cast<uint4*>(t + tc::Tile<BN>::kBytes + off) = lo;
+  }
+}
 
 }  // namespace tc2
 }  // namespace dpb
