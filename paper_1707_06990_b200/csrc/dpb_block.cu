@@ -116,6 +116,16 @@ static int bn_tile(int64_t n) {
   return 64;
 }
 
+// Pre-tiled bf16 weight images of the tensor-core path: W1 (1x1 forward) per
+// layer, then W2 (halo forward) and W2^T (halo dgrad) per layer.
+static int64_t weight_image_bytes(const dpb_block_desc& d) {
+  int64_t w1 = 0;
+  for (int l = 0; l < d.m; ++l) w1 += tc2_w1_tile_bytes(d, l);
+  const HaloPlan hp = tc_halo_plan(d);
+  return align_up(w1, 256) + align_up(hp.fwd_layer_bytes * d.m, 256) +
+         align_up(hp.bwd_layer_bytes * d.m, 256);
+}
+
 void plan_arena(const dpb_block_desc& d, dpb_arena_sizes* s) {
   const Geometry g = geometry(d);
   std::memset(s, 0, sizeof(*s));
@@ -164,10 +174,9 @@ void plan_arena(const dpb_block_desc& d, dpb_arena_sizes* s) {
   take(scratch, &s->scratch_offset, &s->scratch_bytes);
   // pre-tiled bf16 weight operands of the tensor-core path (counted as scratch)
   if (d.dtype == DPB_BF16 && tc_supported(d)) {
-    int64_t wt = 0;
-    for (int l = 0; l < d.m; ++l) wt += tc2_w1_tile_bytes(d, l);
-    s->scratch_bytes += align_up(wt, 256);
-    off = align_up(off + align_up(wt, 256), 256);
+    const int64_t wt = weight_image_bytes(d);
+    s->scratch_bytes += wt;
+    off = align_up(off + wt, 256);
   }
   s->total_bytes = off;
   s->shared1_bytes = 0;
@@ -286,6 +295,7 @@ static void forward_impl(Block* b, const float* x_in, const float* params, float
     LaunchScope ls(b, KC_PACK, 0, 0);
     b->launches--;  // counted inside tc2_pretile_w1
     tc2_pretile_w1(b, params);
+    tc_pretile_w2(b, params, true);
   }
   const double count = M;
   float* fmean = b->fstat;
@@ -326,7 +336,7 @@ static void forward_impl(Block* b, const float* x_in, const float* params, float
     int p3 = g.P;
     {
       LaunchScope ls(b, KC_C3_FWD, M * (d.bk + d.k) * Sb, 2.0 * M * 9 * d.bk * d.k);
-      if (b->tc) p3 = tc_conv3x3_fwd(b, a);
+      if (b->tc) p3 = tc_conv3x3_fwd(b, a, l);
       else gemm_bn<128, Conv3x3Fwd>(b, a, g.M, d.k, 1);
     }
     if (!eval) {
@@ -359,6 +369,11 @@ static void backward_impl(Block* b, const float* params, float* grad_acc, float*
   } else {
     b->acc_cur = grad_acc;
   }
+  if (b->tc) {
+    LaunchScope ls(b, KC_PACK, 0, 0);
+    b->launches--;
+    tc_pretile_w2(b, params, false);
+  }
   for (int l = d.m - 1; l >= 0; --l) {
     LayerArgs<S> a = layer_args<S>(b, params, l);
     float* gl = grads + b->param_off[l];
@@ -373,7 +388,7 @@ static void backward_impl(Block* b, const float* params, float* grad_acc, float*
     int pd = g.P;
     {
       LaunchScope ls(b, KC_C3_DGRAD, M * (4.0 * d.k + Sb * d.bk + 4.0 * d.bk), f3);
-      if (b->tc) pd = tc_conv3x3_dgrad(b, a);
+      if (b->tc) pd = tc_conv3x3_dgrad(b, a, l);
       else gemm_bn<128, Conv3x3Dgrad>(b, a, g.M, d.bk, 1);
     }
     {
@@ -546,24 +561,23 @@ int create(const dpb_block_desc* desc, int device, void* stream, Block** out) {
   b->wpart = reinterpret_cast<float*>(sc + pbytes);
   // wgrad partial region size = scratch - pbytes - coef region
   const int64_t coef_bytes = align_up((2LL * desc->bk + 2 * b->g.cmax) * 4, 256);
-  int64_t wsum_all = 0;
-  if (b->tc)
-    for (int l = 0; l < desc->m; ++l) wsum_all += tc2_w1_tile_bytes(*desc, l);
-  const int64_t wt_bytes = wsum_all > 0 ? align_up(wsum_all, 256) : 0;
+  const int64_t wt_bytes = b->tc ? weight_image_bytes(*desc) : 0;
   b->bnb_bwd = reinterpret_cast<float*>(sc + b->sz.scratch_bytes - wt_bytes - coef_bytes);
   b->bna_bwd = b->bnb_bwd + 2 * desc->bk;
   if (b->tc) {
-    // the pre-tiled weights follow the scratch partials/coefficients
-    int64_t wt = 0, wsum = 0;
-    for (int l = 0; l < desc->m; ++l) wsum += tc2_w1_tile_bytes(*desc, l);
-    if (wsum > 0) {
-      b->wtile = reinterpret_cast<uint8_t*>(base + b->sz.scratch_offset + b->sz.scratch_bytes -
-                                            align_up(wsum, 256));
-      for (int l = 0; l < desc->m; ++l) {
-        b->wtile_off.push_back(wt);
-        wt += tc2_w1_tile_bytes(*desc, l);
-      }
+    // the pre-tiled weight images follow the scratch partials/coefficients
+    b->halo = tc_halo_plan(*desc);
+    uint8_t* wbase = reinterpret_cast<uint8_t*>(sc + b->sz.scratch_bytes - wt_bytes);
+    int64_t w1 = 0;
+    for (int l = 0; l < desc->m; ++l) {
+      b->wtile_off.push_back(w1);
+      w1 += tc2_w1_tile_bytes(*desc, l);
     }
+    if (w1 > 0) b->wtile = wbase;
+    uint8_t* p = wbase + align_up(w1, 256);
+    if (b->halo.fwd_ok) b->w2f = p;
+    p += align_up(b->halo.fwd_layer_bytes * desc->m, 256);
+    if (b->halo.bwd_ok) b->w2b = p;
   }
   int64_t po = 0, so = 0;
   for (int l = 0; l < desc->m; ++l) {

@@ -33,6 +33,13 @@ struct ProfRec {
   double bytes, flops;
 };
 
+// Tile choices of the 3x3 halo kernels (dpb_tc_block.cu tc_halo_plan).
+struct HaloPlan {
+  bool fwd_ok = false, bwd_ok = false;
+  int fwd_bn = 0, fwd_kc = 0, bwd_bn = 0, bwd_kc = 0;
+  int64_t fwd_layer_bytes = 0, bwd_layer_bytes = 0;  // pre-tiled W2 image per layer
+};
+
 struct Block {
   dpb_block_desc d{};
   Geometry g;
@@ -55,6 +62,9 @@ struct Block {
   std::vector<int64_t> param_off, stat_off;
   uint8_t* wtile = nullptr;           // pre-tiled bf16 W1 operands (tensor-core path)
   std::vector<int64_t> wtile_off;
+  HaloPlan halo;
+  uint8_t* w2f = nullptr;             // pre-tiled W2 (halo forward), per layer
+  uint8_t* w2b = nullptr;             // pre-tiled W2^T (halo dgrad), per layer
   bool tc = false;                    // tensor-core (tcgen05) GEMMs
   bool fwd_done = false;
   int64_t launches = 0;
@@ -96,8 +106,10 @@ struct LayerArgs;
 bool tc_supported(const dpb_block_desc& d);
 int64_t tc_wgrad_chunk(int64_t M, int64_t tiles);
 void tc_conv1x1_fwd(Block* b, const LayerArgs<float>& a);
-int tc_conv3x3_fwd(Block* b, const LayerArgs<float>& a);    // returns partial rows
-int tc_conv3x3_dgrad(Block* b, const LayerArgs<float>& a);  // returns partial rows
+int tc_conv3x3_fwd(Block* b, const LayerArgs<float>& a, int l);    // returns partial rows
+int tc_conv3x3_dgrad(Block* b, const LayerArgs<float>& a, int l);  // returns partial rows
+HaloPlan tc_halo_plan(const dpb_block_desc& d);
+void tc_pretile_w2(Block* b, const float* params, bool fwd);
 int64_t tc_halo_partials(const dpb_block_desc& d);
 int64_t tc_halo_wgrad_splits(const dpb_block_desc& d);
 void tc_conv1x1_dgrad(Block* b, const LayerArgs<float>& a);

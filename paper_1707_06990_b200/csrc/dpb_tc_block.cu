@@ -111,16 +111,75 @@ static tc::HaloArgs halo_args(const LayerArgs<float>& a, int kc) {
 static int64_t nimg(const LayerArgs<float>& a) { return a.M / (static_cast<int64_t>(a.H) * a.W); }
 static constexpr size_t kHaloSmemMax = 220 * 1024;
 
-// Returns the number of per-CTA partial rows written (for the finalize).
-int tc_conv3x3_fwd(Block* b, const LayerArgs<float>& a) {
-  const int bn = pick_bn(a.k);
-  for (int kc = std::min(64, a.bk); a.bk % 16 == 0 && bn <= 64 && kc >= 16; kc /= 2) {
+// Static choice of the halo kernels' tiles for a block (shared by the arena
+// plan, the weight pre-tiling and the launches).
+HaloPlan tc_halo_plan(const dpb_block_desc& d) {
+  HaloPlan p{};
+  const tc::HaloGeom g = tc::HaloGeom::make(static_cast<int>(d.h), static_cast<int>(d.w));
+  const int bn = pick_bn(d.k);
+  for (int kc = std::min(64, d.bk); d.bk % 16 == 0 && bn <= 64 && kc >= 16; kc /= 2) {
     if (kc % 16 != 0) continue;
-    const tc::HaloArgs h = halo_args(a, kc);
+    const size_t stage = 2ull * (static_cast<size_t>(g.R) * kc * 2 + 9ull * bn * kc * 2);
+    const int nkb = (d.bk + kc - 1) / kc;
+    const int nst = nkb > 1 ? 2 : 1;
+    if (stage * nst + sizeof(BnFwd) * d.bk <= kHaloSmemMax) {
+      p.fwd_ok = true;
+      p.fwd_bn = bn;
+      p.fwd_kc = kc;
+      p.fwd_layer_bytes = static_cast<int64_t>(nkb) * 2 * (9LL * bn * kc * 2);
+      break;
+    }
+  }
+  const int bnd = pick_bn(d.bk);
+  const int kcd = round_up(d.k, 16);
+  const size_t stage_d = static_cast<size_t>(g.R) * kcd * 2 + 9ull * bnd * kcd * 2;
+  if (kcd <= 64 && stage_d + sizeof(BnFwd) * d.bk <= kHaloSmemMax) {
+    p.bwd_ok = true;
+    p.bwd_bn = bnd;
+    p.bwd_kc = kcd;
+    p.bwd_layer_bytes = 9LL * bnd * kcd * 2;
+  }
+  return p;
+}
+
+void tc_pretile_w2(Block* b, const float* params, bool fwd) {
+  const dpb_block_desc& d = b->d;
+  const HaloPlan& p = b->halo;
+  const dim3 grid(8, d.m);
+  if (fwd && p.fwd_ok && b->w2f) {
+    switch (p.fwd_bn) {
+      case 16: tc::k_pretile_w2_fwd<16><<<grid, 256, 0, b->stream>>>(params, d.c0, d.k, d.bk, p.fwd_kc, b->w2f); break;
+      case 32: tc::k_pretile_w2_fwd<32><<<grid, 256, 0, b->stream>>>(params, d.c0, d.k, d.bk, p.fwd_kc, b->w2f); break;
+      case 48: tc::k_pretile_w2_fwd<48><<<grid, 256, 0, b->stream>>>(params, d.c0, d.k, d.bk, p.fwd_kc, b->w2f); break;
+      default: tc::k_pretile_w2_fwd<64><<<grid, 256, 0, b->stream>>>(params, d.c0, d.k, d.bk, p.fwd_kc, b->w2f); break;
+    }
+    b->launches++;
+  }
+  if (!fwd && p.bwd_ok && b->w2b) {
+    switch (p.bwd_bn) {
+      case 16: tc::k_pretile_w2_bwd<16><<<grid, 256, 0, b->stream>>>(params, d.c0, d.k, d.bk, p.bwd_kc, b->w2b); break;
+      case 32: tc::k_pretile_w2_bwd<32><<<grid, 256, 0, b->stream>>>(params, d.c0, d.k, d.bk, p.bwd_kc, b->w2b); break;
+      case 48: tc::k_pretile_w2_bwd<48><<<grid, 256, 0, b->stream>>>(params, d.c0, d.k, d.bk, p.bwd_kc, b->w2b); break;
+      case 64: tc::k_pretile_w2_bwd<64><<<grid, 256, 0, b->stream>>>(params, d.c0, d.k, d.bk, p.bwd_kc, b->w2b); break;
+      case 128: tc::k_pretile_w2_bwd<128><<<grid, 256, 0, b->stream>>>(params, d.c0, d.k, d.bk, p.bwd_kc, b->w2b); break;
+      case 192: tc::k_pretile_w2_bwd<192><<<grid, 256, 0, b->stream>>>(params, d.c0, d.k, d.bk, p.bwd_kc, b->w2b); break;
+      default: tc::k_pretile_w2_bwd<256><<<grid, 256, 0, b->stream>>>(params, d.c0, d.k, d.bk, p.bwd_kc, b->w2b); break;
+    }
+    b->launches++;
+  }
+}
+
+// Returns the number of per-CTA partial rows written (for the finalize).
+int tc_conv3x3_fwd(Block* b, const LayerArgs<float>& a, int l) {
+  const int bn = pick_bn(a.k);
+  if (b->halo.fwd_ok && b->w2f) {
+    const int kc = b->halo.fwd_kc;
+    tc::HaloArgs h = halo_args(a, kc);
+    h.wt = b->w2f + static_cast<int64_t>(l) * b->halo.fwd_layer_bytes;
     const size_t stage = 2ull * (static_cast<size_t>(h.g.R) * kc * 2 + 9ull * bn * kc * 2);
     const int nst = (a.bk + kc - 1) / kc > 1 ? 2 : 1;
     const size_t aux = sizeof(BnFwd) * a.bk;
-    if (stage * nst + aux <= kHaloSmemMax) {
+    {
       const dim3 grid(static_cast<unsigned>(nimg(a) * h.g.tpi));
       switch (bn) {
         case 16: launch_halo(b, tc::Tc3x3FwdHalo<16>{h}, grid, stage, nst, aux); break;
@@ -137,14 +196,15 @@ int tc_conv3x3_fwd(Block* b, const LayerArgs<float>& a) {
   return static_cast<int>(mtiles(a.M));
 }
 
-int tc_conv3x3_dgrad(Block* b, const LayerArgs<float>& a) {
+int tc_conv3x3_dgrad(Block* b, const LayerArgs<float>& a, int l) {
   const int bn = pick_bn(a.bk);
   const int kc = round_up(a.k, 16);
-  if (kc <= 64) {
-    const tc::HaloArgs h = halo_args(a, kc);
+  if (b->halo.bwd_ok && b->w2b) {
+    tc::HaloArgs h = halo_args(a, kc);
+    h.wt = b->w2b + static_cast<int64_t>(l) * b->halo.bwd_layer_bytes;
     const size_t stage = static_cast<size_t>(h.g.R) * kc * 2 + 9ull * bn * kc * 2;
     const size_t aux = sizeof(BnFwd) * a.bk;
-    if (stage + aux <= kHaloSmemMax) {
+    {
       const dim3 grid(static_cast<unsigned>(nimg(a) * h.g.tpi));
       switch (bn) {
         case 16: launch_halo(b, tc::Tc3x3DgradHalo<16>{h}, grid, stage, 1, aux); break;

@@ -159,7 +159,76 @@ struct HaloArgs {
   HaloGeom g;
   int kc;    // channels per K chunk (forward) / padded k (backward), multiple of 16
   int vec;   // 16-byte aligned feature / accumulator rows at channel c
+  const uint8_t* wt;  // pre-tiled W2 operand image of this layer (smem layout)
 };
+
+// Copy `bytes` (multiple of 16) of a pre-tiled operand image into shared memory.
+__device__ __forceinline__ void copy_image(uint8_t* dst, const uint8_t* src, int bytes) {
+  const uint4* s = reinterpret_cast<const uint4*>(src);
+  uint4* d = reinterpret_cast<uint4*>(dst);
+  for (int q = threadIdx.x; q < bytes / 16; q += kThreads) d[q] = __ldg(s + q);
+}
+
+// W2 for the halo forward: per K chunk kb of kc channels, rows tap*BN + o,
+// K-major (R = 9*BN), bf16 hi plane then lo plane.
+template <int BN>
+__global__ void k_pretile_w2_fwd(const float* __restrict__ params, int c0, int k, int bk, int kc,
+                                 uint8_t* __restrict__ out) {
+  const int l = blockIdx.y;
+  int64_t poff = 0;
+  for (int j = 0; j < l; ++j) {
+    const int cj = c0 + j * k;
+    poff += 2LL * cj + static_cast<int64_t>(bk) * cj + 2LL * bk + 9LL * k * bk;
+  }
+  const int c = c0 + l * k;
+  const float* w2 = params + poff + 2 * c + static_cast<int64_t>(bk) * c + 2 * bk;
+  const int nkb = (bk + kc - 1) / kc;
+  const int plane = 9 * BN * kc * 2;
+  uint8_t* o_l = out + static_cast<int64_t>(l) * nkb * 2 * plane;
+  const int kcn = kc / 8;
+  const int per = 9 * BN * kcn;
+  for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < nkb * per; q += gridDim.x * blockDim.x) {
+    const int kb = q / per, qq = q - kb * per;
+    const int row = qq / kcn, kk = (qq % kcn) * 8;
+    const int tap = row / BN, o = row - tap * BN;
+    const int j0 = kb * kc + kk;
+    float v[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+      v[i] = (o < k && j0 + i < bk) ? w2[(static_cast<int64_t>(o) * bk + j0 + i) * 9 + tap] : 0.f;
+    uint4 h, lo;
+    split8(v, h, lo);
+    uint8_t* t = o_l + static_cast<int64_t>(kb) * 2 * plane;
+    const uint32_t off = halo_kmajor(9 * BN, row, kk);
+    *reinterpret_cast<uint4*>(t + off) = h;
+    *reinterpret_cast<uint4*>(t + plane + off) = lo;
+  }
+}
+
+// W2^T for the halo dgrad: rows tap*BN + j, K = o (kc = k padded), bf16.
+template <int BN>
+__global__ void k_pretile_w2_bwd(const float* __restrict__ params, int c0, int k, int bk, int kc,
+                                 uint8_t* __restrict__ out) {
+  const int l = blockIdx.y;
+  int64_t poff = 0;
+  for (int j = 0; j < l; ++j) {
+    const int cj = c0 + j * k;
+    poff += 2LL * cj + static_cast<int64_t>(bk) * cj + 2LL * bk + 9LL * k * bk;
+  }
+  const int c = c0 + l * k;
+  const float* w2 = params + poff + 2 * c + static_cast<int64_t>(bk) * c + 2 * bk;
+  uint8_t* o_l = out + static_cast<int64_t>(l) * 9 * BN * kc * 2;
+  const int kcn = kc / 8;
+  for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < 9 * BN * kcn; q += gridDim.x * blockDim.x) {
+    const int row = q / kcn, kk = (q % kcn) * 8;
+    const int tap = row / BN, j = row - tap * BN;
+    float v[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+      v[i] = (j < bk && kk + i < k) ? w2[(static_cast<int64_t>(kk + i) * bk + j) * 9 + tap] : 0.f;
+    *reinterpret_cast<uint4*>(o_l + halo_kmajor(9 * BN, row, kk)) = to_bf16x8(v);
+  }
+}
 
 // ---- forward ------------------------------------------------------------------------
 // y = conv3x3(relu(bn_b(z))): per K chunk of kc channels the stage holds the
@@ -212,26 +281,8 @@ struct Tc3x3FwdHalo {
       st_shared16(xh, off, hi);
       st_shared16(xl, off, lo);
     }
-    // W2 for the 9 taps: tile tap*BN + o rows x kc, K-major
-    const int wchunk = 9 * BN * (h.kc / 8);
-    for (int q = threadIdx.x; q < wchunk; q += kThreads) {
-      const int kcn = h.kc / 8;
-      const int row = (q & 7) + 8 * (q / (8 * kcn));  // tap*BN + o
-      const int kc = ((q >> 3) % kcn) * 8;
-      const int tap = row / BN, o = row - tap * BN;
-      const int j0 = j_base + kc;
-      float v[8];
-#pragma unroll
-      for (int i = 0; i < 8; ++i)
-        v[i] = (o < a.k && j0 + i < a.bk)
-                   ? __ldg(a.w2 + (static_cast<int64_t>(o) * a.bk + j0 + i) * 9 + tap)
-                   : 0.f;
-      uint4 hi, lo;
-      split8(v, hi, lo);
-      const uint32_t off = halo_kmajor(9 * BN, row, kc);
-      st_shared16(wh, off, hi);
-      st_shared16(wl, off, lo);
-    }
+    // W2 for the 9 taps (hi | lo), pre-tiled image of this K chunk
+    copy_image(wh, h.wt + static_cast<int64_t>(kb) * 2 * b_bytes(), 2 * b_bytes());
   }
   __device__ void issue(uint32_t st, int kb, uint32_t tmem) const {
     constexpr uint32_t idesc = make_idesc(BN, 0, 0);
@@ -321,19 +372,8 @@ struct Tc3x3DgradHalo {
       }
       st_shared16(dy, halo_kmajor(h.g.R, row, kc), to_bf16x8(v));
     }
-    // B for tap: rows tap*BN + j, K = o
-    for (int q = threadIdx.x; q < 9 * BN * kcn; q += kThreads) {
-      const int row = (q & 7) + 8 * (q / (8 * kcn));
-      const int kc = ((q >> 3) % kcn) * 8;
-      const int tap = row / BN, j = row - tap * BN;
-      float v[8];
-#pragma unroll
-      for (int i = 0; i < 8; ++i)
-        v[i] = (j < a.bk && kc + i < a.k)
-                   ? __ldg(a.w2 + (static_cast<int64_t>(kc + i) * a.bk + j) * 9 + tap)
-                   : 0.f;
-      st_shared16(wt, halo_kmajor(9 * BN, row, kc), to_bf16x8(v));
-    }
+    // W2^T for the 9 taps, pre-tiled image
+    copy_image(wt, h.wt, b_bytes());
   }
   __device__ void issue(uint32_t st, int, uint32_t tmem) const {
     constexpr uint32_t idesc = make_idesc(BN, 0, 0);
