@@ -108,10 +108,11 @@ void tc2_pretile_w1(Block* b, const float* params) {
 bool tc2_conv1x1_fwd(Block* b, const LayerArgs<float>& a, int l) {
   if (a.C % 4 != 0 || !b->wtile) return false;
   const int ntiles = static_cast<int>((a.M + tc::kBM - 1) / tc::kBM);
-  const size_t aux = sizeof(BnFwd) * a.c;
   const uint8_t* w1t = b->wtile + b->wtile_off[l];
   auto go = [&](auto tag) -> bool {
     using Op = decltype(tag);
+    const int nkb = (a.c + tc::kBK - 1) / tc::kBK;
+    const size_t aux = sizeof(BnFwd) * a.c + (Op::kMmaReadsRaw ? 0 : nkb * 2 * Op::kBBytes);
     if (fixed_smem<Op>() + aux > 220 * 1024) return false;
     Op op{};
     if (!make_map_f32(&op.xmap, a.feat, a.C, a.M, a.C, 32, tc::kBM)) return false;
@@ -120,13 +121,14 @@ bool tc2_conv1x1_fwd(Block* b, const LayerArgs<float>& a, int l) {
     launch2(b, op, ntiles, aux);
     return true;
   };
+  // B resident in shared memory when all of W1's tiles fit, else streamed
   switch (tc2_bn_1x1(a.bk)) {
-    case 16: return go(tc2::Fwd1x1<16>{});
-    case 32: return go(tc2::Fwd1x1<32>{});
-    case 48: return go(tc2::Fwd1x1<48>{});
-    case 64: return go(tc2::Fwd1x1<64>{});
-    case 128: return go(tc2::Fwd1x1<128>{});
-    case 192: return go(tc2::Fwd1x1<192>{});
+    case 16: return go(tc2::Fwd1x1<16, true>{}) || go(tc2::Fwd1x1<16, false>{});
+    case 32: return go(tc2::Fwd1x1<32, true>{}) || go(tc2::Fwd1x1<32, false>{});
+    case 48: return go(tc2::Fwd1x1<48, true>{}) || go(tc2::Fwd1x1<48, false>{});
+    case 64: return go(tc2::Fwd1x1<64, true>{}) || go(tc2::Fwd1x1<64, false>{});
+    case 128: return go(tc2::Fwd1x1<128, true>{}) || go(tc2::Fwd1x1<128, false>{});
+    case 192: return go(tc2::Fwd1x1<192, true>{}) || go(tc2::Fwd1x1<192, false>{});
     default: return false;
   }
 }

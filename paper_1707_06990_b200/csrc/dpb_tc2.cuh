@@ -79,6 +79,44 @@ __device__ __forceinline__ void raw_read8(const uint8_t* box, int row, int ch, f
   v[4] = b.x; v[5] = b.y; v[6] = b.z; v[7] = b.w;
 }
 
+// Warp reduction of 8 columns x 32 rows in 9 shuffles (transpose-reduce): on
+// return lane L holds the full column sum of column (L >> 2) & 7 in v[0].
+__device__ __forceinline__ float warp_colsum8(float (&v)[8], int lane) {
+  // step 1: exchange halves of the 8 values with lane ^ 16
+  {
+    const bool up = lane & 16;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const float send = up ? v[i] : v[i + 4];
+      const float recv = __shfl_xor_sync(0xffffffffu, send, 16);
+      v[i] = (up ? v[i + 4] : v[i]) + recv;
+    }
+  }
+  // lanes with bit 4 set now hold columns 4..7 in v[0..3], others 0..3
+  {
+    const bool up = lane & 8;
+#pragma unroll
+    for (int i = 0; i < 2; ++i) {
+      const float send = up ? v[i] : v[i + 2];
+      const float recv = __shfl_xor_sync(0xffffffffu, send, 8);
+      v[i] = (up ? v[i + 2] : v[i]) + recv;
+    }
+  }
+  {
+    const bool up = lane & 4;
+    const float send = up ? v[0] : v[1];
+    const float recv = __shfl_xor_sync(0xffffffffu, send, 4);
+    v[0] = (up ? v[1] : v[0]) + recv;
+  }
+  v[0] += __shfl_xor_sync(0xffffffffu, v[0], 2);
+  v[0] += __shfl_xor_sync(0xffffffffu, v[0], 1);
+  // column held by this lane: bit4 -> +4, bit3 -> +2, bit2 -> +1
+  return v[0];
+}
+__device__ __forceinline__ int colsum8_column(int lane) {
+  return ((lane >> 4) & 1) * 4 + ((lane >> 3) & 1) * 2 + ((lane >> 2) & 1);
+}
+
 // ---- the engine ------------------------------------------------------------------
 // Op interface:
 //   static constexpr int BN, kTmemCols, kNR, kNS, kRawBytes, kOpBytes; bool kColSums
@@ -90,7 +128,7 @@ __device__ __forceinline__ void raw_read8(const uint8_t* box, int row, int ch, f
 //                                                              the raw stage
 //   void transform(int tile, int kb, const uint8_t* raw, uint8_t* opnd,
 //                  const uint8_t* aux, int xt) const;          256 transform threads
-//   void mma(uint32_t opnd, uint32_t raw, uint32_t tmem, int kb) const;   one thread
+//   void mma(uint32_t opnd, uint32_t raw, uint32_t aux, uint32_t tmem, int kb) const;
 //   void epilogue(int tile, int row, int col0, const float (&v)[8], const uint8_t* aux,
 //                 float (&s1)[8], float (&s2)[8]) const;       128 epilogue threads
 //   void col_sums(int tile, int col, double s1, double s2) const;
@@ -109,7 +147,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc2_kernel(const __grid_constant_
 
   uint8_t* raw_ring = smem;
   uint8_t* op_ring = smem + NR * Op::kRawBytes;
-  uint8_t* aux = op_ring + NS * Op::kOpBytes;
+  uint8_t* aux = op_ring + NS * Op::kOpBytes;  // op tables; resident B images first
 
   const int tid = threadIdx.x;
   const int warp = tid / 32, lane = tid % 32;
@@ -130,6 +168,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc2_kernel(const __grid_constant_
   }
   if (warp == kMmaWarp) tc::tmem_alloc<2 * TC>(&tmem_base);
   op.prologue(aux);
+  tc::fence_proxy_async();  // resident operand images written by generic stores
   tc::tc_fence_before();
   __syncthreads();
   tc::tc_fence_after();
@@ -160,7 +199,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc2_kernel(const __grid_constant_
           tc::mbar_wait(&op_full[s], (it / NS) & 1);
           tc::tc_fence_after();
           op.mma(tc::smem_u32(op_ring + s * Op::kOpBytes), tc::smem_u32(raw_ring + r * Op::kRawBytes),
-                 tmem + a * TC, kb);
+                 tc::smem_u32(aux), tmem + a * TC, kb);
           tc::mma_commit(&op_empty[s]);
           if constexpr (Op::kMmaReadsRaw) tc::mma_commit(&raw_empty[r]);
         }
@@ -182,18 +221,12 @@ __global__ void __launch_bounds__(kThreads, 1) tc2_kernel(const __grid_constant_
         float s1[8], s2[8];
         op.epilogue(tile, row, cc * 8, v, aux, s1, s2);
         if constexpr (Op::kColSums) {
-#pragma unroll
-          for (int i = 0; i < 8; ++i) {
-            float x = s1[i], y = s2[i];
-#pragma unroll
-            for (int o = 16; o > 0; o >>= 1) {
-              x += __shfl_xor_sync(0xffffffffu, x, o);
-              y += __shfl_xor_sync(0xffffffffu, y, o);
-            }
-            if (lane == 0 && cc * 8 + i < BN) {
-              red[0][quarter][cc * 8 + i] = x;
-              red[1][quarter][cc * 8 + i] = y;
-            }
+          const float x = warp_colsum8(s1, lane);
+          const float y = warp_colsum8(s2, lane);
+          if ((lane & 3) == 0) {
+            const int col = cc * 8 + colsum8_column(lane);
+            red[0][quarter][col] = x;
+            red[1][quarter][col] = y;
           }
         }
       }
@@ -237,19 +270,21 @@ __global__ void __launch_bounds__(kThreads, 1) tc2_kernel(const __grid_constant_
 
 // ---- 1x1 forward: z = relu(bn_a(x)) . W1^T (bf16x3) ---------------------------------
 // raw stage: x rows [m0, m0+128) x channels [64 kb, 64 kb + 64) as one or two
-// 32-channel TMA boxes (only the boxes that hold channels < c), then W1's
-// pre-tiled bf16 hi | lo operand tiles for this K block (1D bulk copy; the
-// MMA reads them in place).  Operand stage: A hi | A lo.
-template <int BN_>
+// 32-channel TMA boxes (only the boxes that hold channels < c).  W1's
+// pre-tiled bf16 hi | lo operand tiles are either resident in shared memory
+// for the whole persistent CTA (RES: copied once in the prologue) or
+// streamed per K block into the raw stage by a 1D bulk copy (large c).
+// Operand stage: A hi | A lo.
+template <int BN_, bool RES>
 struct Fwd1x1 {
   static constexpr int BN = BN_;
   static constexpr int kTmemCols = BN;
   static constexpr bool kColSums = true;
-  static constexpr bool kMmaReadsRaw = true;
+  static constexpr bool kMmaReadsRaw = !RES;
   static constexpr int kBox = 32 * kBM * 4;                    // 16 KB
   static constexpr int kBBytes = tc::Tile<BN>::kBytes;
-  static constexpr int kRawBytes = 2 * kBox + 2 * kBBytes;
-  static constexpr int kNR = BN <= 64 ? 3 : 2;
+  static constexpr int kRawBytes = 2 * kBox + (RES ? 0 : 2 * kBBytes);
+  static constexpr int kNR = RES ? 3 : (BN <= 64 ? 3 : 2);
   static constexpr int kABytes = tc::Tile<kBM>::kBytes;         // 16 KB
   static constexpr int kOpBytes = 2 * kABytes;
   static constexpr int kNS = 2;
@@ -261,18 +296,29 @@ struct Fwd1x1 {
   __device__ int num_tiles() const { return static_cast<int>((a.M + kBM - 1) / kBM); }
   __device__ int num_kb(int) const { return (a.c + kBK - 1) / kBK; }
   __device__ int boxes(int kb) const { return a.c - kb * kBK > 32 ? 2 : 1; }
-  __device__ uint32_t raw_bytes(int, int kb) const { return boxes(kb) * kBox + 2 * kBBytes; }
+  __device__ uint32_t raw_bytes(int, int kb) const {
+    return boxes(kb) * kBox + (RES ? 0 : 2 * kBBytes);
+  }
+  __device__ uint32_t b_all() const { return static_cast<uint32_t>(num_kb(0) * 2 * kBBytes); }
+  __device__ const BnFwd* bn_table(const uint8_t* aux) const {
+    return reinterpret_cast<const BnFwd*>(aux + (RES ? b_all() : 0));
+  }
   __device__ void prologue(uint8_t* aux) const {
-    fill_bn_fwd(reinterpret_cast<BnFwd*>(aux), a.c, 0, a.amean, a.avar, a.gamma_a, a.beta_a);
+    if (RES) {
+      const uint4* src = reinterpret_cast<const uint4*>(w1t);
+      uint4* dst = reinterpret_cast<uint4*>(aux);
+      for (int q = threadIdx.x; q < static_cast<int>(b_all() / 16); q += kThreads) dst[q] = __ldg(src + q);
+    }
+    fill_bn_fwd(const_cast<BnFwd*>(bn_table(aux)), a.c, 0, a.amean, a.avar, a.gamma_a, a.beta_a);
   }
   __device__ void tma(int tile, int kb, uint32_t raw, uint64_t* bar) const {
     tma_load_2d(raw, &xmap, kb * kBK, tile * kBM, bar);
     if (boxes(kb) == 2) tma_load_2d(raw + kBox, &xmap, kb * kBK + 32, tile * kBM, bar);
-    bulk_load(raw + 2 * kBox, w1t + static_cast<int64_t>(kb) * 2 * kBBytes, 2 * kBBytes, bar);
+    if (!RES) bulk_load(raw + 2 * kBox, w1t + static_cast<int64_t>(kb) * 2 * kBBytes, 2 * kBBytes, bar);
   }
   __device__ void transform(int, int kb, const uint8_t* raw, uint8_t* op, const uint8_t* aux,
                             int xt) const {
-    const BnFwd* bn = reinterpret_cast<const BnFwd*>(aux);
+    const BnFwd* bn = bn_table(aux);
     uint8_t* ah = op;
     uint8_t* al = op + kABytes;
 #pragma unroll
@@ -294,10 +340,10 @@ struct Fwd1x1 {
       tc::st_shared16(al, off, l);
     }
   }
-  __device__ void mma(uint32_t op, uint32_t raw, uint32_t tmem, int kb) const {
+  __device__ void mma(uint32_t op, uint32_t raw, uint32_t aux, uint32_t tmem, int kb) const {
     constexpr uint32_t idesc = tc::make_idesc(BN, 0, 0);
     const uint32_t ah = op, al = op + kABytes;
-    const uint32_t bh = raw + 2 * kBox, bl = bh + kBBytes;
+    const uint32_t bh = RES ? aux + kb * 2 * kBBytes : raw + 2 * kBox, bl = bh + kBBytes;
 #pragma unroll
     for (int k16 = 0; k16 < kBK / 16; ++k16) {
       const uint32_t acc = (kb | k16) ? 1u : 0u;
