@@ -194,6 +194,23 @@ __device__ __forceinline__ void split8(const float (&v)[8], uint4& hi, uint4& lo
                   pack_bf16(l[6], l[7]));
 }
 
+// Fast exact split for the bf16x3 operands: hi = x with the low 16 mantissa
+// bits cleared (exact), lo = bf16_rn(x - hi) (x - hi is exact in fp32), so
+// hi + lo == x to 2^-16 relative; two elements packed per instruction.
+__device__ __forceinline__ void split8_fast(const float (&v)[8], uint4& hi, uint4& lo) {
+  uint32_t h[4], l[4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const uint32_t a = __float_as_uint(v[2 * i]), b = __float_as_uint(v[2 * i + 1]);
+    h[i] = __byte_perm(a, b, 0x7632);  // upper halves: a -> low 16 bits, b -> high
+    const float ra = v[2 * i] - __uint_as_float(a & 0xFFFF0000u);
+    const float rb = v[2 * i + 1] - __uint_as_float(b & 0xFFFF0000u);
+    l[i] = pack_bf16(ra, rb);
+  }
+  hi = make_uint4(h[0], h[1], h[2], h[3]);
+  lo = make_uint4(l[0], l[1], l[2], l[3]);
+}
+
 __device__ __forceinline__ uint4 to_bf16x8(const float (&v)[8]) {
   return make_uint4(pack_bf16(v[0], v[1]), pack_bf16(v[2], v[3]), pack_bf16(v[4], v[5]),
                     pack_bf16(v[6], v[7]));

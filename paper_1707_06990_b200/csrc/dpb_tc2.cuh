@@ -321,20 +321,36 @@ struct Fwd1x1 {
     const BnFwd* bn = bn_table(aux);
     uint8_t* ah = op;
     uint8_t* al = op + kABytes;
+    // every chunk of this thread covers the same 8 channels (kmajor_coords):
+    // BN as one FMA per element with per-stage register coefficients
+    int row0, kc;
+    tc::kmajor_coords(xt, row0, kc);
+    const int ch0 = kb * kBK + kc;
+    float sc[8], sh[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      if (ch0 + i < a.c) {
+        const BnFwd b = bn[ch0 + i];
+        sc[i] = b.scale;
+        sh[i] = fmaf(-b.mean, b.scale, b.beta);
+      } else {
+        sc[i] = 0.f;  // channels past c contribute zero
+        sh[i] = 0.f;
+      }
+    }
 #pragma unroll
     for (int i = 0; i < kBM * kBK / 8 / kXfThreads; ++i) {
-      int row, kc;
-      tc::kmajor_coords(xt + i * kXfThreads, row, kc);
-      const int ch0 = kb * kBK + kc;
+      const int row = row0 + i * (kXfThreads / 8);
       float v[8];
       if (ch0 < a.c) {
         raw_read8(raw + (kc >> 5) * kBox, row, kc & 31, v);
-        tc::bnrelu8(bn, ch0, a.c - ch0, v);
+#pragma unroll
+        for (int e = 0; e < 8; ++e) v[e] = fmaxf(fmaf(v[e], sc[e], sh[e]), 0.f);
       } else {
         tc::zero8(v);
       }
       uint4 h, l;
-      tc::split8(v, h, l);
+      tc::split8_fast(v, h, l);
       const uint32_t off = tc::Tile<kBM>::kmajor_chunk(row, kc);
       tc::st_shared16(ah, off, h);
       tc::st_shared16(al, off, l);
