@@ -299,3 +299,13 @@ int tc_conv3x3_wgrad(Block* b, LayerArgs<float> a) {
 }
 
 }  // namespace dpb
+
+// Debug-only (not part of dpb.h): enable / read the halo engine's phase clocks.
+extern "C" __attribute__((visibility("default"))) int dpb_debug_phase_clocks(int enable, long long* host,
+                                                                             int n) {
+  if (enable >= 0) {
+    cudaMemcpyToSymbol(dpb::tc::g_phase_on, &enable, sizeof(int));
+    return 0;
+  }
+  return cudaMemcpyFromSymbol(host, dpb::tc::g_phase_clock, sizeof(long long) * 6 * n);
+}

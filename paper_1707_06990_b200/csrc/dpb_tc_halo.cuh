@@ -65,6 +65,11 @@ __device__ __forceinline__ uint32_t halo_mnmajor(int R, int j, int pos) {
   return static_cast<uint32_t>((j >> 3) * R * 16 + pos * 16);
 }
 
+// Debug phase clocks (dpb_debug_phase_clocks): thread 0 of the first 4096
+// CTAs records globaltimer-free clock64 stamps at the phase boundaries.
+__device__ long long g_phase_clock[4096][6];
+__device__ int g_phase_on;
+
 // ---- engine ----------------------------------------------------------------------
 // As tc_gemm_kernel, but the op owns the stage layout and the MMA issue
 // pattern (taps = descriptor shifts), and TMEM may hold several accumulators.
@@ -74,11 +79,15 @@ __global__ void __launch_bounds__(kThreads, 1) tc_halo_kernel(const Op op) {
   constexpr int BN = Op::BN;
   extern __shared__ __align__(1024) uint8_t smem[];
   __shared__ uint64_t mbar[2];
+  __shared__ uint64_t bbar[2];  // async bulk copies of pre-tiled weight images
   __shared__ uint32_t tmem_base;
   __shared__ float red[2][4][BN];
 
   const int tid = threadIdx.x;
   const int warp = tid / 32, lane = tid % 32;
+  const bool dbg = g_phase_on && tid == 0 && blockIdx.x + blockIdx.y * gridDim.x < 4096;
+  const int dbg_id = blockIdx.x + blockIdx.y * gridDim.x;
+  if (dbg) g_phase_clock[dbg_id][0] = clock64();
   const uint32_t SB = op.stage_bytes();
   const int nst = op.num_kb() > 1 ? 2 : 1;  // stages actually used
   uint8_t* aux = smem + nst * SB;
@@ -87,6 +96,8 @@ __global__ void __launch_bounds__(kThreads, 1) tc_halo_kernel(const Op op) {
   if (tid == 32) {
     mbar_init(&mbar[0], 1);
     mbar_init(&mbar[1], 1);
+    mbar_init(&bbar[0], 1);
+    mbar_init(&bbar[1], 1);
     fence_barrier_init();
   }
   op.prologue(aux);
@@ -94,25 +105,32 @@ __global__ void __launch_bounds__(kThreads, 1) tc_halo_kernel(const Op op) {
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = tmem_base;
+  if (dbg) g_phase_clock[dbg_id][1] = clock64();
 
   const int nkb = op.num_kb();
   for (int kb = 0; kb < nkb; ++kb) {
     const int s = kb & 1;
     if (kb >= 2) mbar_wait(&mbar[s], ((kb - 2) >> 1) & 1);
     uint8_t* st = smem + s * SB;
+    if constexpr (Op::kBulk)
+      if (tid == 0) op.bulk(smem_u32(st), kb, &bbar[s]);
     op.produce(st, kb, aux);
     fence_proxy_async();
     __syncthreads();
+    if (dbg && kb == nkb - 1) g_phase_clock[dbg_id][2] = clock64();
     if (tid == 0) {
+      if constexpr (Op::kBulk) mbar_wait(&bbar[s], (kb >> 1) & 1);
       tc_fence_after();
       op.issue(smem_u32(st), kb, tmem);
       mma_commit(&mbar[s]);
     }
+    if (dbg && kb == nkb - 1) g_phase_clock[dbg_id][3] = clock64();
   }
   if (nkb > 0) {
     mbar_wait(&mbar[(nkb - 1) & 1], ((nkb - 1) >> 1) & 1);
     tc_fence_after();
   }
+  if (dbg) g_phase_clock[dbg_id][4] = clock64();
 
   const int quarter = warp & 3, half = warp >> 2;
   const int row = quarter * 32 + lane;
@@ -152,6 +170,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_halo_kernel(const Op op) {
     tc_fence_after();
     tmem_dealloc<TCOLS>(tmem);
   }
+  if (dbg) g_phase_clock[dbg_id][5] = clock64();
 }
 
 struct HaloArgs {
@@ -232,12 +251,16 @@ __global__ void k_pretile_w2_bwd(const float* __restrict__ params, int c0, int k
 
 // ---- forward ------------------------------------------------------------------------
 // y = conv3x3(relu(bn_b(z))): per K chunk of kc channels the stage holds the
-// halo (hi, lo) and W2 for all 9 taps (hi, lo).
+// halo (hi, lo) and W2 for all 9 taps (hi, lo).  The W2 image arrives by an
+// asynchronous bulk copy while the threads build the halo; each thread issues
+// all of its halo loads before converting any (one memory latency per stage).
 template <int BN_>
 struct Tc3x3FwdHalo {
   static constexpr int BN = BN_;
   static constexpr int kTmemCols = BN;
   static constexpr bool kColSums = true;
+  static constexpr bool kBulk = true;
+  static constexpr int kMaxChunks = 8;  // per thread: R <= 256 rows x kc <= 64 / 8 / 256
   HaloArgs h;
   __device__ uint32_t halo_bytes() const { return static_cast<uint32_t>(h.g.R * h.kc * 2); }
   __device__ uint32_t b_bytes() const { return static_cast<uint32_t>(9 * BN * h.kc * 2); }
@@ -249,58 +272,68 @@ struct Tc3x3FwdHalo {
     fill_bn_fwd(reinterpret_cast<BnFwd*>(aux), h.a.bk, 0, h.a.bmean, h.a.bvar, h.a.gamma_b,
                 h.a.beta_b);
   }
+  __device__ void bulk(uint32_t st, int kb, uint64_t* bar) const {
+    mbar_expect_tx(bar, 2 * b_bytes());
+    bulk_load(st + 2 * halo_bytes(), h.wt + static_cast<int64_t>(kb) * 2 * b_bytes(), 2 * b_bytes(),
+              bar);
+  }
   __device__ void produce(uint8_t* st, int kb, const uint8_t* aux) const {
     const LayerArgs<float>& a = h.a;
     const BnFwd* bn = reinterpret_cast<const BnFwd*>(aux);
     uint8_t* xh = st;
     uint8_t* xl = st + halo_bytes();
-    uint8_t* wh = xl + halo_bytes();
-    uint8_t* wl = wh + b_bytes();
     const int t = tile();
     const int64_t pix0 = static_cast<int64_t>(img()) * h.g.H * h.g.W;
     const int j_base = kb * h.kc;
-    // halo: R rows x kc channels, phases of 8 threads = 8 consecutive rows
-    const int nchunk = h.g.R * (h.kc / 8);
-    for (int q = threadIdx.x; q < nchunk; q += kThreads) {
-      const int row = (q & 7) + 8 * (q / (8 * (h.kc / 8)));
-      const int kc = ((q >> 3) % (h.kc / 8)) * 8;
-      const int pp = h.g.pixel(h.g.pos(t, row));
-      float v[8];
-      const int j0 = j_base + kc;
-      if (pp >= 0 && j0 < a.bk) {
-        load8(a.z + (pix0 + pp) * a.bk + j0, a.bk - j0, (a.bk & 3) == 0, v);
+    const int kcn = h.kc / 8;
+    const int nchunk = h.g.R * kcn;
+    float v[kMaxChunks][8];
+    int rr[kMaxChunks], kk[kMaxChunks];
+    bool ok[kMaxChunks];
 #pragma unroll
-        for (int i = 0; i < 8; ++i) v[i] = j0 + i < a.bk ? bn_relu(bn[j0 + i], v[i]) : 0.f;
-      } else {
+    for (int i = 0; i < kMaxChunks; ++i) {  // all loads first
+      const int q = threadIdx.x + i * kThreads;
+      rr[i] = (q & 7) + 8 * (q / (8 * kcn));
+      kk[i] = ((q >> 3) % kcn) * 8;
+      const int pp = q < nchunk ? h.g.pixel(h.g.pos(t, rr[i])) : -1;
+      const int j0 = j_base + kk[i];
+      ok[i] = pp >= 0 && j0 < a.bk;  // false: zero padding (after activation)
+      if (ok[i]) load8(a.z + (pix0 + pp) * a.bk + j0, a.bk - j0, (a.bk & 3) == 0, v[i]);
+      if (q >= nchunk) rr[i] = -1;
+    }
 #pragma unroll
-        for (int i = 0; i < 8; ++i) v[i] = 0.f;
-      }
+    for (int i = 0; i < kMaxChunks; ++i) {
+      if (rr[i] < 0) continue;
+      const int j0 = j_base + kk[i];
+#pragma unroll
+      for (int e = 0; e < 8; ++e) v[i][e] = ok[i] && j0 + e < a.bk ? bn_relu(bn[j0 + e], v[i][e]) : 0.f;
       uint4 hi, lo;
-      split8(v, hi, lo);
-      const uint32_t off = halo_kmajor(h.g.R, row, kc);
+      split8(v[i], hi, lo);
+      const uint32_t off = halo_kmajor(h.g.R, rr[i], kk[i]);
       st_shared16(xh, off, hi);
       st_shared16(xl, off, lo);
     }
-    // W2 for the 9 taps (hi | lo), pre-tiled image of this K chunk
-    copy_image(wh, h.wt + static_cast<int64_t>(kb) * 2 * b_bytes(), 2 * b_bytes());
   }
   __device__ void issue(uint32_t st, int kb, uint32_t tmem) const {
     constexpr uint32_t idesc = make_idesc(BN, 0, 0);
-    const uint32_t xh = st, xl = st + halo_bytes();
-    const uint32_t wh = xl + halo_bytes(), wl = wh + b_bytes();
     const uint32_t RB = static_cast<uint32_t>(h.g.R) * 16, WB = 9u * BN * 16;
+    const uint32_t xh = sdesc_lo(st, RB), xl = sdesc_lo(st + halo_bytes(), RB);
+    const uint32_t wh = sdesc_lo(st + 2 * halo_bytes(), WB);
+    const uint32_t wl = sdesc_lo(st + 2 * halo_bytes() + b_bytes(), WB);
+    const uint32_t hi = sdesc_hi(128);
+    const int nk16 = h.kc / 16;
+#pragma unroll
     for (int tap = 0; tap < 9; ++tap) {
-      const uint32_t aoff = static_cast<uint32_t>(h.g.fwd_off(tap)) * 16;
-      const uint32_t boff = static_cast<uint32_t>(tap * BN) * 16;
-      for (int k16 = 0; k16 < h.kc / 16; ++k16) {
-        const uint32_t ka = k16 * 2 * RB, kbo = k16 * 2 * WB;
+      const uint32_t aoff = static_cast<uint32_t>(h.g.fwd_off(tap));  // 16-byte units
+      const uint32_t boff = static_cast<uint32_t>(tap * BN);
+#pragma unroll
+      for (int k16 = 0; k16 < 4; ++k16) {
+        if (k16 >= nk16) break;
+        const uint32_t da = aoff + k16 * 2 * (RB >> 4), db = boff + k16 * 2 * (WB >> 4);
         const uint32_t acc = (kb | tap | k16) ? 1u : 0u;
-        mma_bf16(tmem, make_sdesc(xh + aoff + ka, RB, 128), make_sdesc(wh + boff + kbo, WB, 128),
-                 idesc, acc);
-        mma_bf16(tmem, make_sdesc(xh + aoff + ka, RB, 128), make_sdesc(wl + boff + kbo, WB, 128),
-                 idesc, 1u);
-        mma_bf16(tmem, make_sdesc(xl + aoff + ka, RB, 128), make_sdesc(wh + boff + kbo, WB, 128),
-                 idesc, 1u);
+        mma_bf16_lh(tmem, xh + da, hi, wh + db, hi, idesc, acc);
+        mma_bf16_lh(tmem, xh + da, hi, wl + db, hi, idesc, 1u);
+        mma_bf16_lh(tmem, xl + da, hi, wh + db, hi, idesc, 1u);
       }
     }
   }
@@ -341,6 +374,8 @@ struct Tc3x3DgradHalo {
   static constexpr int BN = BN_;
   static constexpr int kTmemCols = BN;
   static constexpr bool kColSums = true;
+  static constexpr bool kBulk = true;
+  static constexpr int kMaxChunks = 8;
   HaloArgs h;
   __device__ uint32_t halo_bytes() const { return static_cast<uint32_t>(h.g.R * h.kc * 2); }
   __device__ uint32_t b_bytes() const { return static_cast<uint32_t>(9 * BN * h.kc * 2); }
@@ -352,39 +387,53 @@ struct Tc3x3DgradHalo {
     fill_bn_fwd(reinterpret_cast<BnFwd*>(aux), h.a.bk, 0, h.a.bmean, h.a.bvar, h.a.gamma_b,
                 h.a.beta_b);
   }
+  __device__ void bulk(uint32_t st, int, uint64_t* bar) const {
+    mbar_expect_tx(bar, b_bytes());
+    bulk_load(st + halo_bytes(), h.wt, b_bytes(), bar);
+  }
   __device__ void produce(uint8_t* st, int, const uint8_t*) const {
     const LayerArgs<float>& a = h.a;
     uint8_t* dy = st;
-    uint8_t* wt = st + halo_bytes();
     const int t = tile();
     const int64_t pix0 = static_cast<int64_t>(img()) * h.g.H * h.g.W;
     const int kcn = h.kc / 8;
-    for (int q = threadIdx.x; q < h.g.R * kcn; q += kThreads) {
-      const int row = (q & 7) + 8 * (q / (8 * kcn));
-      const int kc = ((q >> 3) % kcn) * 8;
-      const int pp = h.g.pixel(h.g.pos(t, row));
-      float v[8];
-      if (pp >= 0 && kc < a.k) {
-        load8(a.acc + (pix0 + pp) * a.C + a.c + kc, a.k - kc, h.vec, v);
-      } else {
+    const int nchunk = h.g.R * kcn;
+    for (int base = 0; base < nchunk; base += kMaxChunks * kThreads) {
+      float v[kMaxChunks][8];
+      int rr[kMaxChunks], kk[kMaxChunks];
 #pragma unroll
-        for (int i = 0; i < 8; ++i) v[i] = 0.f;
+      for (int i = 0; i < kMaxChunks; ++i) {
+        const int q = base + threadIdx.x + i * kThreads;
+        rr[i] = (q & 7) + 8 * (q / (8 * kcn));
+        kk[i] = ((q >> 3) % kcn) * 8;
+        const int pp = q < nchunk ? h.g.pixel(h.g.pos(t, rr[i])) : -1;
+        if (pp >= 0 && kk[i] < a.k) load8(a.acc + (pix0 + pp) * a.C + a.c + kk[i], a.k - kk[i], h.vec, v[i]);
+        else
+#pragma unroll
+          for (int e = 0; e < 8; ++e) v[i][e] = 0.f;
+        if (q >= nchunk) rr[i] = -1;
       }
-      st_shared16(dy, halo_kmajor(h.g.R, row, kc), to_bf16x8(v));
+#pragma unroll
+      for (int i = 0; i < kMaxChunks; ++i)
+        if (rr[i] >= 0) st_shared16(dy, halo_kmajor(h.g.R, rr[i], kk[i]), to_bf16x8(v[i]));
     }
-    // W2^T for the 9 taps, pre-tiled image
-    copy_image(wt, h.wt, b_bytes());
   }
   __device__ void issue(uint32_t st, int, uint32_t tmem) const {
     constexpr uint32_t idesc = make_idesc(BN, 0, 0);
-    const uint32_t dy = st, wt = st + halo_bytes();
     const uint32_t RB = static_cast<uint32_t>(h.g.R) * 16, WB = 9u * BN * 16;
+    const uint32_t dy = sdesc_lo(st, RB), wt = sdesc_lo(st + halo_bytes(), WB);
+    const uint32_t hi = sdesc_hi(128);
+    const int nk16 = h.kc / 16;
+#pragma unroll
     for (int tap = 0; tap < 9; ++tap) {
-      const uint32_t aoff = static_cast<uint32_t>(h.g.bwd_off(tap)) * 16;
-      const uint32_t boff = static_cast<uint32_t>(tap * BN) * 16;
-      for (int k16 = 0; k16 < h.kc / 16; ++k16)
-        mma_bf16(tmem, make_sdesc(dy + aoff + k16 * 2 * RB, RB, 128),
-                 make_sdesc(wt + boff + k16 * 2 * WB, WB, 128), idesc, (tap | k16) ? 1u : 0u);
+      const uint32_t aoff = static_cast<uint32_t>(h.g.bwd_off(tap));
+      const uint32_t boff = static_cast<uint32_t>(tap * BN);
+#pragma unroll
+      for (int k16 = 0; k16 < 4; ++k16) {
+        if (k16 >= nk16) break;
+        mma_bf16_lh(tmem, dy + aoff + k16 * 2 * (RB >> 4), hi, wt + boff + k16 * 2 * (WB >> 4), hi,
+                    idesc, (tap | k16) ? 1u : 0u);
+      }
     }
   }
   __device__ void epilogue(int row, int col0, const float (&v)[8], const uint8_t* aux,
@@ -437,6 +486,8 @@ struct Tc3x3WgradHalo {
   static constexpr int BN = BN_;
   static constexpr int kTmemCols = 9 * BN;
   static constexpr bool kColSums = false;
+  static constexpr bool kBulk = false;
+  static constexpr int kMaxChunks = 8;
   HaloArgs h;
   int tpc;      // tiles per CTA
   int ntiles;   // total tiles = N * tpi
@@ -452,6 +503,7 @@ struct Tc3x3WgradHalo {
     fill_bn_fwd(reinterpret_cast<BnFwd*>(aux), h.a.bk, 0, h.a.bmean, h.a.bvar, h.a.gamma_b,
                 h.a.beta_b);
   }
+  __device__ void bulk(uint32_t, int, uint64_t*) const {}
   __device__ void produce(uint8_t* st, int kb, const uint8_t* aux) const {
     const LayerArgs<float>& a = h.a;
     const BnFwd* bn = reinterpret_cast<const BnFwd*>(aux);
@@ -461,53 +513,73 @@ struct Tc3x3WgradHalo {
     const int im = gt / h.g.tpi, t = gt - im * h.g.tpi;
     const int64_t pix0 = static_cast<int64_t>(im) * h.g.H * h.g.W;
     const int j_base = blockIdx.y * kBM;
-    // act_b halo, MN-major: chunk = 8 channels of one position; phase = 8
-    // consecutive positions of one channel group (128 contiguous bytes)
     const int groups = kBM / 8;
-    for (int q = threadIdx.x; q < h.g.R * groups; q += kThreads) {
-      const int pos = (q & 7) + 8 * (q / (8 * groups));
-      const int jg = ((q >> 3) % groups) * 8;
-      const int j0 = j_base + jg;
-      const int pp = h.g.pixel(h.g.pos(t, pos));
-      float v[8];
-      if (pp >= 0 && j0 < a.bk) {
-        load8(a.z + (pix0 + pp) * a.bk + j0, a.bk - j0, (a.bk & 3) == 0, v);
-#pragma unroll
-        for (int i = 0; i < 8; ++i) v[i] = j0 + i < a.bk ? bn_relu(bn[j0 + i], v[i]) : 0.f;
-      } else {
-#pragma unroll
-        for (int i = 0; i < 8; ++i) v[i] = 0.f;
-      }
-      st_shared16(xs, halo_mnmajor(h.g.R, jg, pos), to_bf16x8(v));
-    }
-    // dY of the tile's 128 positions, MN-major rows = o
-    const int s0 = h.g.g_s0(t);
+    const int nchunk = h.g.R * groups;  // act_b halo chunks; then dY chunks
     const int og = BN / 8;
-    for (int q = threadIdx.x; q < kBM * og; q += kThreads) {
-      const int pos = (q & 7) + 8 * (q / (8 * og));
-      const int o0 = ((q >> 3) % og) * 8;
-      const int pp = h.g.pixel(s0 + pos);
-      float v[8];
-      if (pp >= 0 && o0 < a.k) {
-        load8(a.acc + (pix0 + pp) * a.C + a.c + o0, a.k - o0, h.vec, v);
-      } else {
+    const int ndy = kBM * og;
+    const int s0 = h.g.g_s0(t);
+    const int total = nchunk + ndy;
+    for (int base = 0; base < total; base += kMaxChunks * kThreads) {
+      float v[kMaxChunks][8];
+      uint32_t off[kMaxChunks];
+      uint8_t kind[kMaxChunks];  // 0 skip, 1 halo, 2 dY
+      int jj[kMaxChunks];
 #pragma unroll
-        for (int i = 0; i < 8; ++i) v[i] = 0.f;
+      for (int i = 0; i < kMaxChunks; ++i) {
+        const int q = base + threadIdx.x + i * kThreads;
+        kind[i] = 0;
+#pragma unroll
+        for (int e = 0; e < 8; ++e) v[i][e] = 0.f;
+        if (q < nchunk) {
+          // act_b halo, MN-major: phase = 8 consecutive positions of one group
+          const int pos = (q & 7) + 8 * (q / (8 * groups));
+          const int jg = ((q >> 3) % groups) * 8;
+          const int j0 = j_base + jg;
+          const int pp = h.g.pixel(h.g.pos(t, pos));
+          const bool valid = pp >= 0 && j0 < a.bk;
+          if (valid) load8(a.z + (pix0 + pp) * a.bk + j0, a.bk - j0, (a.bk & 3) == 0, v[i]);
+          kind[i] = valid ? 1 : 3;  // 3: zero padding (after activation)
+          jj[i] = j0;
+          off[i] = halo_mnmajor(h.g.R, jg, pos);
+        } else if (q < total) {
+          const int r = q - nchunk;
+          const int pos = (r & 7) + 8 * (r / (8 * og));
+          const int o0 = ((r >> 3) % og) * 8;
+          const int pp = h.g.pixel(s0 + pos);
+          if (pp >= 0 && o0 < a.k) load8(a.acc + (pix0 + pp) * a.C + a.c + o0, a.k - o0, h.vec, v[i]);
+          kind[i] = 2;
+          off[i] = halo_mnmajor(kBM, o0, pos);
+        }
       }
-      st_shared16(dys, halo_mnmajor(kBM, o0, pos), to_bf16x8(v));
+#pragma unroll
+      for (int i = 0; i < kMaxChunks; ++i) {
+        if (kind[i] == 1) {
+#pragma unroll
+          for (int e = 0; e < 8; ++e)
+            v[i][e] = jj[i] + e < a.bk ? bn_relu(bn[jj[i] + e], v[i][e]) : 0.f;
+          st_shared16(xs, off[i], to_bf16x8(v[i]));
+        } else if (kind[i] == 2) {
+          st_shared16(dys, off[i], to_bf16x8(v[i]));
+        } else if (kind[i] == 3) {
+          st_shared16(xs, off[i], make_uint4(0, 0, 0, 0));
+        }
+      }
     }
   }
   __device__ void issue(uint32_t st, int kb, uint32_t tmem) const {
     constexpr uint32_t idesc = make_idesc(BN, 1, 1);
-    const uint32_t xs = st, dys = st + halo_bytes();
     const uint32_t RB = static_cast<uint32_t>(h.g.R) * 16;
+    // A: M = channels (SBO = R*16 between channel groups), K = positions
+    // shifted by the tap (LBO = 128 between groups of 8 positions)
+    const uint32_t xs = sdesc_lo(st, 128), dys = sdesc_lo(st + halo_bytes(), 128);
+    const uint32_t ahi = sdesc_hi(RB), bhi = sdesc_hi(kBM * 16);
+#pragma unroll
     for (int tap = 0; tap < 9; ++tap) {
-      const uint32_t aoff = static_cast<uint32_t>(h.g.fwd_off(tap)) * 16;
+      const uint32_t aoff = static_cast<uint32_t>(h.g.fwd_off(tap));
+#pragma unroll
       for (int k16 = 0; k16 < kBM / 16; ++k16)
-        // A: M = channels (SBO = R*16 between channel groups), K = positions
-        // shifted by the tap (LBO = 128 between groups of 8 positions)
-        mma_bf16(tmem + tap * BN, make_sdesc(xs + aoff + k16 * 256, 128, RB),
-                 make_sdesc(dys + k16 * 256, 128, kBM * 16), idesc, (kb | k16) ? 1u : 0u);
+        mma_bf16_lh(tmem + tap * BN, xs + aoff + k16 * 16, ahi, dys + k16 * 16, bhi, idesc,
+                    (kb | k16) ? 1u : 0u);
     }
   }
   __device__ void epilogue(int row, int col0, const float (&v)[8], const uint8_t*, float (&)[8],

@@ -1,0 +1,30 @@
+"""Debug: per-phase CTA timing of the halo 3x3 forward (dpb_debug_phase_clocks)."""
+import ctypes as C, sys
+import numpy as np, torch
+sys.path.insert(0, ".")
+import paper_1707_06990_b200 as P
+from paper_1707_06990_b200._lib import lib
+L = lib()
+f = L.dpb_debug_phase_clocks
+f.argtypes = [C.c_int, C.c_void_p, C.c_int]
+shp = P.BlockShape(64, 32, 32, 24, 4, 12, 48)
+plan = P.BlockPlan(shp, dtype="bf16", layout="nhwc")
+p = torch.randn(shp.param_elems, device="cuda") * 0.1 + 0.5
+x = torch.randn(shp.pixels, shp.c0, device="cuda")
+run = shp.initial_running()
+for _ in range(3):
+    plan.forward(x, p, run, True)
+torch.cuda.synchronize()
+f(1, None, 0)
+plan.forward(x, p, run, True)   # the last halo forward launch wins (layer 3)
+torch.cuda.synchronize()
+f(0, None, 0)
+buf = np.zeros((4096, 6), dtype=np.int64)
+f(-1, C.c_void_p(buf.ctypes.data), 576)
+b = buf[:576]
+t0 = b[:, 0].min()
+ph = np.diff(b, axis=1)
+print("CTAs", len(b), "span cycles", b[:, 5].max() - t0)
+for i, name in enumerate(["prologue+alloc", "produce", "issue", "mma wait", "epilogue+dealloc"]):
+    print(f"{name:18s} mean {ph[:, i].mean():8.0f}  p50 {np.median(ph[:, i]):8.0f}  max {ph[:, i].max():8.0f}")
+print("CTA lifetime mean", (b[:, 5] - b[:, 0]).mean(), "start spread", np.percentile(b[:, 0] - t0, [0, 50, 100]))
