@@ -74,7 +74,7 @@ __device__ int g_phase_on;
 // As tc_gemm_kernel, but the op owns the stage layout and the MMA issue
 // pattern (taps = descriptor shifts), and TMEM may hold several accumulators.
 template <class Op>
-__global__ void __launch_bounds__(kThreads, 1) tc_halo_kernel(const Op op) {
+__global__ void __launch_bounds__(kThreads, 2) tc_halo_kernel(const Op op) {
   constexpr uint32_t TCOLS = TmemCols<Op::kTmemCols>::value;
   constexpr int BN = Op::BN;
   extern __shared__ __align__(1024) uint8_t smem[];
@@ -94,8 +94,9 @@ __global__ void __launch_bounds__(kThreads, 1) tc_halo_kernel(const Op op) {
 
   if (warp == 0) tmem_alloc<TCOLS>(&tmem_base);
   if (tid == 32) {
-    mbar_init(&mbar[0], 1);
-    mbar_init(&mbar[1], 1);
+    // each stage completes when every issuing warp's MMAs have completed
+    mbar_init(&mbar[0], Op::kIssuers);
+    mbar_init(&mbar[1], Op::kIssuers);
     mbar_init(&bbar[0], 1);
     mbar_init(&bbar[1], 1);
     fence_barrier_init();
@@ -118,10 +119,14 @@ __global__ void __launch_bounds__(kThreads, 1) tc_halo_kernel(const Op op) {
     fence_proxy_async();
     __syncthreads();
     if (dbg && kb == nkb - 1) g_phase_clock[dbg_id][2] = clock64();
-    if (tid == 0) {
+    // the MMAs are issued by lane 0 of kIssuers warps in parallel (each into
+    // its own accumulator or disjoint columns): a tcgen05.mma issue costs
+    // ~60 cycles of uniform-register setup, several times the execution time
+    // of these narrow-N MMAs
+    if (lane == 0 && warp < Op::kIssuers) {
       if constexpr (Op::kBulk) mbar_wait(&bbar[s], (kb >> 1) & 1);
       tc_fence_after();
-      op.issue(smem_u32(st), kb, tmem);
+      op.issue(smem_u32(st), kb, tmem, warp);
       mma_commit(&mbar[s]);
     }
     if (dbg && kb == nkb - 1) g_phase_clock[dbg_id][3] = clock64();
@@ -134,11 +139,21 @@ __global__ void __launch_bounds__(kThreads, 1) tc_halo_kernel(const Op op) {
 
   const int quarter = warp & 3, half = warp >> 2;
   const int row = quarter * 32 + lane;
-  for (int cc = half; cc < Op::kTmemCols / 8; cc += 2) {
+  constexpr int kOutCols = Op::kTmemCols / Op::kAccCopies;  // summed accumulator copies
+  for (int cc = half; cc < kOutCols / 8; cc += 2) {
     float v[8];
-    if (nkb > 0) tmem_ld8(tmem + (static_cast<uint32_t>(quarter * 32) << 16) + cc * 8, v);
-    else
+    if (nkb > 0) {
+      tmem_ld8(tmem + (static_cast<uint32_t>(quarter * 32) << 16) + cc * 8, v);
+#pragma unroll
+      for (int c2 = 1; c2 < Op::kAccCopies; ++c2) {
+        float w[8];
+        tmem_ld8(tmem + (static_cast<uint32_t>(quarter * 32) << 16) + c2 * kOutCols + cc * 8, w);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) v[i] += w[i];
+      }
+    } else {
       for (int i = 0; i < 8; ++i) v[i] = 0.f;
+    }
     float s1[8], s2[8];
     op.epilogue(row, cc * 8, v, aux, s1, s2);
     if constexpr (Op::kColSums) {
@@ -257,10 +272,11 @@ __global__ void k_pretile_w2_bwd(const float* __restrict__ params, int c0, int k
 template <int BN_>
 struct Tc3x3FwdHalo {
   static constexpr int BN = BN_;
-  static constexpr int kTmemCols = BN;
+  static constexpr int kIssuers = 3, kAccCopies = 3;  // taps t = warp, warp+3, warp+6
+  static constexpr int kTmemCols = BN * kAccCopies;
   static constexpr bool kColSums = true;
   static constexpr bool kBulk = true;
-  static constexpr int kMaxChunks = 8;  // per thread: R <= 256 rows x kc <= 64 / 8 / 256
+  static constexpr int kMaxChunks = 4;
   HaloArgs h;
   __device__ uint32_t halo_bytes() const { return static_cast<uint32_t>(h.g.R * h.kc * 2); }
   __device__ uint32_t b_bytes() const { return static_cast<uint32_t>(9 * BN * h.kc * 2); }
@@ -314,8 +330,9 @@ struct Tc3x3FwdHalo {
       st_shared16(xl, off, lo);
     }
   }
-  __device__ void issue(uint32_t st, int kb, uint32_t tmem) const {
+  __device__ void issue(uint32_t st, int kb, uint32_t tmem_base, int part) const {
     constexpr uint32_t idesc = make_idesc(BN, 0, 0);
+    const uint32_t tmem = tmem_base + part * BN;
     const uint32_t RB = static_cast<uint32_t>(h.g.R) * 16, WB = 9u * BN * 16;
     const uint32_t xh = sdesc_lo(st, RB), xl = sdesc_lo(st + halo_bytes(), RB);
     const uint32_t wh = sdesc_lo(st + 2 * halo_bytes(), WB);
@@ -323,14 +340,15 @@ struct Tc3x3FwdHalo {
     const uint32_t hi = sdesc_hi(128);
     const int nk16 = h.kc / 16;
 #pragma unroll
-    for (int tap = 0; tap < 9; ++tap) {
+    for (int ti = 0; ti < 3; ++ti) {
+      const int tap = part + 3 * ti;
       const uint32_t aoff = static_cast<uint32_t>(h.g.fwd_off(tap));  // 16-byte units
       const uint32_t boff = static_cast<uint32_t>(tap * BN);
 #pragma unroll
       for (int k16 = 0; k16 < 4; ++k16) {
         if (k16 >= nk16) break;
         const uint32_t da = aoff + k16 * 2 * (RB >> 4), db = boff + k16 * 2 * (WB >> 4);
-        const uint32_t acc = (kb | tap | k16) ? 1u : 0u;
+        const uint32_t acc = (kb | ti | k16) ? 1u : 0u;
         mma_bf16_lh(tmem, xh + da, hi, wh + db, hi, idesc, acc);
         mma_bf16_lh(tmem, xh + da, hi, wl + db, hi, idesc, 1u);
         mma_bf16_lh(tmem, xl + da, hi, wh + db, hi, idesc, 1u);
@@ -372,10 +390,11 @@ struct Tc3x3FwdHalo {
 template <int BN_>
 struct Tc3x3DgradHalo {
   static constexpr int BN = BN_;
-  static constexpr int kTmemCols = BN;
+  static constexpr int kIssuers = BN <= 64 ? 3 : 1, kAccCopies = kIssuers;
+  static constexpr int kTmemCols = BN * kAccCopies;
   static constexpr bool kColSums = true;
   static constexpr bool kBulk = true;
-  static constexpr int kMaxChunks = 8;
+  static constexpr int kMaxChunks = 4;
   HaloArgs h;
   __device__ uint32_t halo_bytes() const { return static_cast<uint32_t>(h.g.R * h.kc * 2); }
   __device__ uint32_t b_bytes() const { return static_cast<uint32_t>(9 * BN * h.kc * 2); }
@@ -418,21 +437,23 @@ struct Tc3x3DgradHalo {
         if (rr[i] >= 0) st_shared16(dy, halo_kmajor(h.g.R, rr[i], kk[i]), to_bf16x8(v[i]));
     }
   }
-  __device__ void issue(uint32_t st, int, uint32_t tmem) const {
+  __device__ void issue(uint32_t st, int, uint32_t tmem_base, int part) const {
     constexpr uint32_t idesc = make_idesc(BN, 0, 0);
+    const uint32_t tmem = tmem_base + part * BN;
     const uint32_t RB = static_cast<uint32_t>(h.g.R) * 16, WB = 9u * BN * 16;
     const uint32_t dy = sdesc_lo(st, RB), wt = sdesc_lo(st + halo_bytes(), WB);
     const uint32_t hi = sdesc_hi(128);
     const int nk16 = h.kc / 16;
 #pragma unroll
-    for (int tap = 0; tap < 9; ++tap) {
+    for (int ti = 0; ti < 9 / kIssuers; ++ti) {
+      const int tap = part + kIssuers * ti;
       const uint32_t aoff = static_cast<uint32_t>(h.g.bwd_off(tap));
       const uint32_t boff = static_cast<uint32_t>(tap * BN);
 #pragma unroll
       for (int k16 = 0; k16 < 4; ++k16) {
         if (k16 >= nk16) break;
         mma_bf16_lh(tmem, dy + aoff + k16 * 2 * (RB >> 4), hi, wt + boff + k16 * 2 * (WB >> 4), hi,
-                    idesc, (tap | k16) ? 1u : 0u);
+                    idesc, (ti | k16) ? 1u : 0u);
       }
     }
   }
@@ -484,10 +505,11 @@ struct Tc3x3DgradHalo {
 template <int BN_>
 struct Tc3x3WgradHalo {
   static constexpr int BN = BN_;
+  static constexpr int kIssuers = 3, kAccCopies = 1;  // taps t = warp, warp+3, warp+6
   static constexpr int kTmemCols = 9 * BN;
   static constexpr bool kColSums = false;
   static constexpr bool kBulk = false;
-  static constexpr int kMaxChunks = 8;
+  static constexpr int kMaxChunks = 4;
   HaloArgs h;
   int tpc;      // tiles per CTA
   int ntiles;   // total tiles = N * tpi
@@ -566,7 +588,7 @@ struct Tc3x3WgradHalo {
       }
     }
   }
-  __device__ void issue(uint32_t st, int kb, uint32_t tmem) const {
+  __device__ void issue(uint32_t st, int kb, uint32_t tmem, int part) const {
     constexpr uint32_t idesc = make_idesc(BN, 1, 1);
     const uint32_t RB = static_cast<uint32_t>(h.g.R) * 16;
     // A: M = channels (SBO = R*16 between channel groups), K = positions
@@ -574,7 +596,8 @@ struct Tc3x3WgradHalo {
     const uint32_t xs = sdesc_lo(st, 128), dys = sdesc_lo(st + halo_bytes(), 128);
     const uint32_t ahi = sdesc_hi(RB), bhi = sdesc_hi(kBM * 16);
 #pragma unroll
-    for (int tap = 0; tap < 9; ++tap) {
+    for (int ti = 0; ti < 3; ++ti) {
+      const int tap = part + 3 * ti;
       const uint32_t aoff = static_cast<uint32_t>(h.g.fwd_off(tap));
 #pragma unroll
       for (int k16 = 0; k16 < kBM / 16; ++k16)
