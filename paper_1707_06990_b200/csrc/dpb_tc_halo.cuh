@@ -303,12 +303,13 @@ struct Tc3x3FwdHalo {
     const int j_base = kb * h.kc;
     const int kcn = h.kc / 8;
     const int nchunk = h.g.R * kcn;
+    for (int base = 0; base < nchunk; base += kMaxChunks * kThreads) {
     float v[kMaxChunks][8];
     int rr[kMaxChunks], kk[kMaxChunks];
     bool ok[kMaxChunks];
 #pragma unroll
     for (int i = 0; i < kMaxChunks; ++i) {  // all loads first
-      const int q = threadIdx.x + i * kThreads;
+      const int q = base + threadIdx.x + i * kThreads;
       rr[i] = (q & 7) + 8 * (q / (8 * kcn));
       kk[i] = ((q >> 3) % kcn) * 8;
       const int pp = q < nchunk ? h.g.pixel(h.g.pos(t, rr[i])) : -1;
@@ -328,6 +329,7 @@ struct Tc3x3FwdHalo {
       const uint32_t off = halo_kmajor(h.g.R, rr[i], kk[i]);
       st_shared16(xh, off, hi);
       st_shared16(xl, off, lo);
+    }
     }
   }
   __device__ void issue(uint32_t st, int kb, uint32_t tmem_base, int part) const {
