@@ -139,7 +139,7 @@ void plan_arena(const dpb_block_desc& d, dpb_arena_sizes* s) {
   take(static_cast<int64_t>(d.m) * g.M * d.bk * g.S, &s->z_offset, &s->z_bytes);
   take((2 * g.C + 2LL * d.m * d.bk) * 4, &s->stats_offset, &s->stats_bytes);
   take(d.layout == DPB_NCHW ? g.M * g.C * 4 : 0, &s->acc_offset, &s->acc_bytes);
-  take(g.M * d.bk * 4, &s->g0_offset, &s->g0_bytes);
+  take(2 * g.M * d.bk * 4, &s->g0_offset, &s->g0_bytes);
   take(g.M * g.cmax * 4, &s->g1_offset, &s->g1_bytes);
   // scratch: partials | wgrad partials | BN-backward coefficients
   int64_t wmax = 0;
@@ -170,7 +170,7 @@ void plan_arena(const dpb_block_desc& d, dpb_arena_sizes* s) {
   }
   const int64_t pbytes = static_cast<int64_t>(g.Pmax) * std::max<int64_t>(g.C, d.bk) * 16;
   const int64_t scratch = align_up(pbytes, 256) + align_up(wmax * 4, 256) +
-                          align_up((2LL * d.bk + 2 * g.cmax) * 4, 256);
+                          align_up((4LL * d.bk + 2 * g.cmax) * 4, 256);
   take(scratch, &s->scratch_offset, &s->scratch_bytes);
   // pre-tiled bf16 weight operands of the tensor-core path (counted as scratch)
   if (d.dtype == DPB_BF16 && tc_supported(d)) {
@@ -374,8 +374,18 @@ static void backward_impl(Block* b, const float* params, float* grad_acc, float*
     b->launches--;
     tc_pretile_w2(b, params, false);
   }
+  // Two streams: the data-gradient chain (3x3 dgrad -> BN_b bwd -> 1x1 dgrad
+  // -> BN_a bwd + accumulate) on the main stream, the weight-gradient branch
+  // (3x3 wgrad -> fold, 1x1 wgrad -> fold) on the side stream.  g0 and the BN_b
+  // coefficients are double-buffered by layer parity, so the side branch of
+  // layer l overlaps the main chain of layers l and l-1.
+  const bool fork = b->side != nullptr && !b->prof;
+  cudaStream_t main_st = b->stream;
+  auto ev = [&](int l, int which) { return b->fork_ev[3 * l + which]; };
   for (int l = d.m - 1; l >= 0; --l) {
     LayerArgs<S> a = layer_args<S>(b, params, l);
+    a.g0 = b->g0 + (l & 1) * g.M * d.bk;
+    a.bnb_bwd = b->bnb_bwd + (l & 1) * 2 * d.bk;
     float* gl = grads + b->param_off[l];
     float* d_ga = gl;
     float* d_ba = gl + a.c;
@@ -384,13 +394,13 @@ static void backward_impl(Block* b, const float* params, float* grad_acc, float*
     float* d_bb = d_gb + d.bk;
     float* d_w2 = d_bb + d.bk;
     const double f3 = 2.0 * M * 9 * d.bk * d.k, f1 = 2.0 * M * a.c * d.bk;
-    // 3x3: dgrad (+ReLU mask by act_b, BN_b sums) and wgrad (graph.hpp:905-910)
-    int pd = g.P;
-    {
-      LaunchScope ls(b, KC_C3_DGRAD, M * (4.0 * d.k + Sb * d.bk + 4.0 * d.bk), f3);
-      if (b->tc) pd = tc_conv3x3_dgrad(b, a, l);
-      else gemm_bn<128, Conv3x3Dgrad>(b, a, g.M, d.bk, 1);
+    if (fork) {
+      if (l + 2 < d.m) cudaStreamWaitEvent(main_st, ev(l + 2, 2), 0);  // buffers of parity l
+      cudaEventRecord(ev(l, 0), main_st);
+      cudaStreamWaitEvent(b->side, ev(l, 0), 0);
     }
+    // ---- weight branch, part 1: 3x3 wgrad (graph.hpp:905-907) ----
+    if (fork) b->stream = b->side;
     {
       const int64_t rows = 9LL * d.bk;
       int splits;
@@ -410,18 +420,26 @@ static void backward_impl(Block* b, const float* params, float* grad_acc, float*
       k_reduce_w2<<<blocks_for(9LL * d.k * d.bk, 32), dim3(32, 8), 0, b->stream>>>(
           b->wpart, splits, d.bk, d.k, d_w2);
     }
+    b->stream = main_st;
+    // ---- data chain: 3x3 dgrad (+ReLU mask by act_b, BN_b sums) ----
+    int pd = g.P;
+    {
+      LaunchScope ls(b, KC_C3_DGRAD, M * (4.0 * d.k + Sb * d.bk + 4.0 * d.bk), f3);
+      if (b->tc) pd = tc_conv3x3_dgrad(b, a, l);
+      else gemm_bn<128, Conv3x3Dgrad>(b, a, g.M, d.bk, 1);
+    }
     // BN_b backward sums -> dgamma_b, dbeta_b, coefficients (graph.hpp:913-916)
     {
       LaunchScope ls(b, KC_FINALIZE, 0, 0);
       k_finalize_bn_bwd<<<blocks_for(32LL * d.bk, 256), 256, 0, b->stream>>>(
-          b->part, pd, d.bk, count, d_gb, d_bb, b->bnb_bwd);
+          b->part, pd, d.bk, count, d_gb, d_bb, const_cast<float*>(a.bnb_bwd));
     }
-    // 1x1: dgrad (+ReLU mask by act_a, BN_a sums) and wgrad (graph.hpp:920-926)
-    {
-      LaunchScope ls(b, KC_C1_DGRAD, M * ((4.0 + Sb) * d.bk + (Sb + 4.0) * a.c), f1);
-      if (b->tc) tc_conv1x1_dgrad(b, a);
-      else gemm_bn2<128, Conv1x1Dgrad>(b, a, g.M, a.c, 1);
+    if (fork) {
+      cudaEventRecord(ev(l, 1), main_st);
+      cudaStreamWaitEvent(b->side, ev(l, 1), 0);
     }
+    // ---- weight branch, part 2: 1x1 wgrad (graph.hpp:920-922) ----
+    if (fork) b->stream = b->side;
     {
       int splits;
       {
@@ -443,6 +461,14 @@ static void backward_impl(Block* b, const float* params, float* grad_acc, float*
         k_reduce_w1<<<blocks_for(static_cast<int64_t>(d.bk) * a.c, 32), dim3(32, 8), 0,
                       b->stream>>>(b->wpart, splits, d.bk, a.c, d_w1);
     }
+    if (fork) cudaEventRecord(ev(l, 2), b->side);
+    b->stream = main_st;
+    // ---- data chain: 1x1 dgrad (+ReLU mask by act_a, BN_a sums) ----
+    {
+      LaunchScope ls(b, KC_C1_DGRAD, M * ((4.0 + Sb) * d.bk + (Sb + 4.0) * a.c), f1);
+      if (b->tc) tc_conv1x1_dgrad(b, a);
+      else gemm_bn2<128, Conv1x1Dgrad>(b, a, g.M, a.c, 1);
+    }
     // BN_a backward (graph.hpp:929-932) + concat-backward accumulate (:936-941)
     {
       LaunchScope ls(b, KC_FINALIZE, 0, 0);
@@ -455,6 +481,10 @@ static void backward_impl(Block* b, const float* params, float* grad_acc, float*
           g.M, a.c, static_cast<int>(g.C), static_cast<const S*>(b->feat), b->g1, a.amean,
           a.avar, a.gamma_a, b->bna_bwd, b->acc_cur);
     }
+  }
+  if (fork) {  // join: the caller's stream sees every weight gradient
+    cudaStreamWaitEvent(main_st, ev(0, 2), 0);
+    if (d.m > 1) cudaStreamWaitEvent(main_st, ev(1, 2), 0);
   }
   if (d.layout == DPB_NCHW) {
     LaunchScope ls(b, KC_PACK, M * g.C * 8, 0);
@@ -560,10 +590,10 @@ int create(const dpb_block_desc* desc, int device, void* stream, Block** out) {
       align_up(static_cast<int64_t>(b->g.Pmax) * std::max<int64_t>(b->g.C, desc->bk) * 16, 256);
   b->wpart = reinterpret_cast<float*>(sc + pbytes);
   // wgrad partial region size = scratch - pbytes - coef region
-  const int64_t coef_bytes = align_up((2LL * desc->bk + 2 * b->g.cmax) * 4, 256);
+  const int64_t coef_bytes = align_up((4LL * desc->bk + 2 * b->g.cmax) * 4, 256);
   const int64_t wt_bytes = b->tc ? weight_image_bytes(*desc) : 0;
   b->bnb_bwd = reinterpret_cast<float*>(sc + b->sz.scratch_bytes - wt_bytes - coef_bytes);
-  b->bna_bwd = b->bnb_bwd + 2 * desc->bk;
+  b->bna_bwd = b->bnb_bwd + 4 * desc->bk;
   if (b->tc) {
     // the pre-tiled weight images follow the scratch partials/coefficients
     b->halo = tc_halo_plan(*desc);
@@ -578,6 +608,12 @@ int create(const dpb_block_desc* desc, int device, void* stream, Block** out) {
     if (b->halo.fwd_ok) b->w2f = p;
     p += align_up(b->halo.fwd_layer_bytes * desc->m, 256);
     if (b->halo.bwd_ok) b->w2b = p;
+  }
+  if (cudaStreamCreateWithFlags(&b->side, cudaStreamNonBlocking) != cudaSuccess) b->side = nullptr;
+  for (int i = 0; b->side && i < 3 * desc->m; ++i) {
+    cudaEvent_t e;
+    cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
+    b->fork_ev.push_back(e);
   }
   int64_t po = 0, so = 0;
   for (int l = 0; l < desc->m; ++l) {
@@ -595,6 +631,8 @@ void destroy(Block* b) {
   if (!b) return;
   if (b->arena) cudaFree(b->arena);
   for (cudaEvent_t e : b->ev_pool) cudaEventDestroy(e);
+  for (cudaEvent_t e : b->fork_ev) cudaEventDestroy(e);
+  if (b->side) cudaStreamDestroy(b->side);
   delete b;
 }
 

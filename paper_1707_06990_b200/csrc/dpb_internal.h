@@ -53,11 +53,13 @@ struct Block {
   float* zstat = nullptr;    // per layer mean[bk] | var[bk]
   float* acc = nullptr;      // [M, C] fp32 (NCHW boundary only)
   float* acc_cur = nullptr;  // the accumulator in use (arena or caller NHWC)
-  float* g0 = nullptr;       // [M, bk] fp32
+  float* g0 = nullptr;       // [M, bk] fp32 (x2: double-buffered across layers)
+  cudaStream_t side = nullptr;        // weight-gradient branch of the backward
+  std::vector<cudaEvent_t> fork_ev;   // per layer: start, bn_b done, side done
   float* g1 = nullptr;       // [M, cmax] fp32
   double2* part = nullptr;   // per-CTA partial sums
   float* wpart = nullptr;    // split-K weight-gradient partials
-  float* bnb_bwd = nullptr;  // [bk][2]
+  float* bnb_bwd = nullptr;  // [bk][2] (x2: double-buffered across layers)
   float* bna_bwd = nullptr;  // [cmax][2]
   std::vector<int64_t> param_off, stat_off;
   uint8_t* wtile = nullptr;           // pre-tiled bf16 W1 operands (tensor-core path)
