@@ -12,6 +12,7 @@
 
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <new>
 #include <string>
@@ -40,10 +41,10 @@ static cudaEvent_t next_event(Block* b) {
   return b->ev_pool[b->ev_used++];
 }
 
-LaunchScope::LaunchScope(Block* blk, int cat, double bytes, double flops) : b(blk) {
+LaunchScope::LaunchScope(Block* blk, int cat_, double bytes, double flops) : b(blk), cat(cat_) {
   b->launches++;
   if (!b->prof) return;
-  ProfRec r{cat, next_event(b), next_event(b), bytes, flops};
+  ProfRec r{cat_, next_event(b), next_event(b), bytes, flops};
   cudaEventRecord(r.start, b->stream);
   idx = static_cast<int>(b->recs.size());
   b->recs.push_back(r);
@@ -51,6 +52,15 @@ LaunchScope::LaunchScope(Block* blk, int cat, double bytes, double flops) : b(bl
 
 LaunchScope::~LaunchScope() {
   if (idx >= 0) cudaEventRecord(b->recs[idx].stop, b->stream);
+  // debugging aid: DPB_DEBUG_SYNC=1 synchronizes after every launch and names
+  // the first launch that faults (category, launch ordinal)
+  static const bool dbg = std::getenv("DPB_DEBUG_SYNC") != nullptr;
+  if (dbg) {
+    const cudaError_t e = cudaDeviceSynchronize();
+    if (e != cudaSuccess)
+      std::fprintf(stderr, "[dpb] launch %lld (category %d) failed: %s\n",
+                   static_cast<long long>(b->launches), cat, cudaGetErrorString(e));
+  }
 }
 
 int fail(int code, const std::string& msg) {
@@ -379,7 +389,9 @@ static void backward_impl(Block* b, const float* params, float* grad_acc, float*
   // (3x3 wgrad -> fold, 1x1 wgrad -> fold) on the side stream.  g0 and the BN_b
   // coefficients are double-buffered by layer parity, so the side branch of
   // layer l overlaps the main chain of layers l and l-1.
-  const bool fork = b->side != nullptr && !b->prof;
+  // DPB_NO_FORK=1 (debugging aid) keeps the whole backward on one stream.
+  static const bool no_fork = std::getenv("DPB_NO_FORK") != nullptr;
+  const bool fork = b->side != nullptr && !b->prof && !no_fork;
   cudaStream_t main_st = b->stream;
   auto ev = [&](int l, int which) { return b->fork_ev[3 * l + which]; };
   for (int l = d.m - 1; l >= 0; --l) {

@@ -81,6 +81,7 @@ struct Block {
 struct LaunchScope {
   Block* b;
   int idx = -1;
+  int cat = 0;
   LaunchScope(Block* blk, int cat, double bytes, double flops);
   ~LaunchScope();
 };

@@ -306,9 +306,12 @@ __device__ __forceinline__ void load8(const float* p, int n, bool aligned, float
 //                 float (&s1)[8], float (&s2)[8]) const;   8 columns of one row
 //   void col_sums(int col, float s1, float s2) const;     once per column per CTA
 //                                                         (when kColSums)
+// TMEM columns to allocate for N accumulator columns (a power of two >= 32).
 template <int N>
 struct TmemCols {
-  static constexpr uint32_t value = N <= 32 ? 32 : N <= 64 ? 64 : N <= 128 ? 128 : 256;
+  static_assert(N >= 1 && N <= 512, "TMEM holds at most 512 fp32 columns per SM");
+  static constexpr uint32_t value =
+      N <= 32 ? 32 : N <= 64 ? 64 : N <= 128 ? 128 : N <= 256 ? 256 : 512;
 };
 
 template <class Op>
