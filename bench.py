@@ -55,6 +55,20 @@ def algorithmic_per_image(shapes, S=2):
     return F, B
 
 
+def committed_traffic(kernel: str, config: str, dtype: str):
+    """DRAM bytes per launch of `kernel` from the committed ncu launch list of one
+    bench step (profiles/r*_traffic.json, tools/ncu_summary.py), or None."""
+    import glob
+    for path in sorted(glob.glob(os.path.join(ROOT, "profiles", "r*_traffic.json")), reverse=True):
+        try:
+            d = json.load(open(path))
+        except (OSError, ValueError):
+            continue
+        if d.get("config") == config and d.get("dtype") == dtype and kernel in d.get("categories", {}):
+            return d["categories"][kernel]["dram_bytes_per_launch"]
+    return None
+
+
 class ClockSampler:
     """nvidia-smi clocks + throttle reasons sampled during the timed region."""
 
@@ -146,6 +160,9 @@ def main():
     ap.add_argument("--no-graph", action="store_true", help="launch kernels directly (no CUDA graph)")
     ap.add_argument("--cpu-budget-s", type=float, default=25.0)
     ap.add_argument("--ref-budget-s", type=float, default=180.0)
+    ap.add_argument("--ncu-step", action="store_true",
+                    help="after warm-up, run ONE step inside cudaProfilerStart/Stop and exit "
+                         "(for `ncu --profile-from-start off`; prints no bench line)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     if args.impl == "reference":
@@ -240,6 +257,18 @@ def main():
         else:
             step()
 
+    if args.ncu_step:
+        torch.cuda.synchronize(dev)
+        torch.cuda.profiler.start()
+        with torch.cuda.stream(stream):
+            timed_step()
+        torch.cuda.synchronize(dev)
+        torch.cuda.profiler.stop()
+        print(json.dumps({"ncu_step": True, "launches_per_step": launches_per_step}), flush=True)
+        for b in blocks:
+            b["plan"].close()
+        return 0
+
     # ---- timed region --------------------------------------------------------
     if world > 1:
         dist.barrier()
@@ -298,7 +327,7 @@ def main():
         roof = {"bound": "tensor", "achieved": flops_per_launch / (avg_ms * 1e-3) / 1e12,
                 "peak": bf16_sust, "unit": "TFLOP/s"}
     roof["frac"] = roof["achieved"] / roof["peak"]
-    roof["traffic"] = None
+    roof["traffic"] = committed_traffic(dom_name, args.config, args.dtype)
     roof["kernel"] = dom_name
     roof["kernel_share_of_step"] = dom["total_ms"] / prof_total
     roof["peak_source"] = peak_src
