@@ -187,6 +187,8 @@ def main():
     stream = torch.cuda.Stream(device=dev)
     g = torch.Generator(device="cpu").manual_seed(1234 + rank)
 
+    from paper_1707_06990_b200.dp import GradientBuckets
+    buckets = GradientBuckets([P.BlockShape(*s).param_elems for s in shapes], device=dev)
     blocks = []
     with torch.cuda.stream(stream):
         for s in shapes:
@@ -204,10 +206,7 @@ def main():
                 x=torch.randn(shp.pixels, shp.c0, generator=g).to(dev),
                 gup=torch.randn(shp.pixels, shp.c_out, generator=g).to(dev),
                 acc=torch.empty(shp.pixels, shp.c_out, device=dev),
-                grads=torch.empty(shp.param_elems, device=dev)))
-    flat_grads = None
-    if world > 1:
-        flat_grads = torch.empty(sum(b["grads"].numel() for b in blocks), device=dev)
+                grads=buckets.view(len(blocks))))   # block grads are views of one flat buffer
 
     def step():
         for b in blocks:
@@ -215,15 +214,17 @@ def main():
         for b in reversed(blocks):
             b["acc"].copy_(b["gup"])          # consumer BN backward writes the block-output grad
             b["plan"].backward(b["params"], b["acc"], b["grads"])
+
+    def reduce_grads():
+        # data-parallel gradient allreduce (per-GPU BN); outside the
+        # CUDA graph: one NCCL allreduce of the flat fp32 buffer, scaled by 1/P
         if world > 1:
-            # data-parallel gradient allreduce (per-GPU BN)
-            torch.cat([b["grads"] for b in blocks], out=flat_grads)
-            dist.all_reduce(flat_grads)
-            flat_grads.mul_(1.0 / world)
+            buckets.reduce_all()
 
     with torch.cuda.stream(stream):
         for _ in range(args.warmup):
             step()
+            reduce_grads()
     torch.cuda.synchronize(dev)
     launches_per_step = sum(b["plan"].launch_count for b in blocks)  # last backward only
     # count forward+backward launches of one step precisely
@@ -256,6 +257,7 @@ def main():
             graph.replay()
         else:
             step()
+        reduce_grads()
 
     if args.ncu_step:
         torch.cuda.synchronize(dev)
@@ -344,6 +346,8 @@ def main():
     # ---- end to end through the reference-facing C-ABI (host buffers, NCHW) ---
     e2e = None
     with torch.cuda.stream(stream):
+        e_buckets = GradientBuckets([b["shape"].param_elems for b in blocks], device=dev)
+        grads_h = torch.empty(e_buckets.flat.numel()).pin_memory()
         e_blocks = []
         for b in blocks:
             shp = b["shape"]
@@ -354,10 +358,9 @@ def main():
                 g_h=torch.randn(shp.n, shp.c_out, shp.h, shp.w, generator=g).pin_memory(),
                 x=torch.empty(shp.n, shp.c0, shp.h, shp.w, device=dev),
                 acc=torch.empty(shp.n, shp.c_out, shp.h, shp.w, device=dev),
-                grads=torch.empty(shp.param_elems, device=dev),
-                grads_h=torch.empty(shp.param_elems).pin_memory()))
+                grads=e_buckets.view(len(e_blocks))))
         h2d = sum(e["x_h"].numel() * 4 + e["g_h"].numel() * 4 for e in e_blocks)
-        d2h = sum(e["grads_h"].numel() * 4 for e in e_blocks)
+        d2h = grads_h.numel() * 4
 
         def e2e_step():
             for e in e_blocks:
@@ -366,7 +369,9 @@ def main():
             for e in reversed(e_blocks):
                 e["acc"].copy_(e["g_h"], non_blocking=True)
                 e["plan"].backward(e["params"], e["acc"], e["grads"])
-                e["grads_h"].copy_(e["grads"], non_blocking=True)
+            if world > 1:
+                e_buckets.reduce_all()
+            grads_h.copy_(e_buckets.flat, non_blocking=True)
 
         for _ in range(args.warmup):
             e2e_step()
