@@ -129,11 +129,14 @@ static int bn_tile(int64_t n) {
 // Pre-tiled bf16 weight images of the tensor-core path: W1 (1x1 forward) per
 // layer, then W2 (halo forward) and W2^T (halo dgrad) per layer.
 static int64_t weight_image_bytes(const dpb_block_desc& d) {
-  int64_t w1 = 0;
-  for (int l = 0; l < d.m; ++l) w1 += tc2_w1_tile_bytes(d, l);
+  int64_t w1 = 0, w1b = 0;
+  for (int l = 0; l < d.m; ++l) {
+    w1 += tc2_w1_tile_bytes(d, l);
+    w1b += tc2_w1b_layer_bytes(d, l);
+  }
   const HaloPlan hp = tc_halo_plan(d);
   return align_up(w1, 256) + align_up(hp.fwd_layer_bytes * d.m, 256) +
-         align_up(hp.bwd_layer_bytes * d.m, 256);
+         align_up(hp.bwd_layer_bytes * d.m, 256) + align_up(w1b, 256);
 }
 
 void plan_arena(const dpb_block_desc& d, dpb_arena_sizes* s) {
@@ -176,6 +179,7 @@ void plan_arena(const dpb_block_desc& d, dpb_arena_sizes* s) {
       wmax = std::max<int64_t>(wmax, ((g.M + c3 - 1) / c3) * 9LL * d.bk * d.k);
       const int64_t c1 = tc_wgrad_chunk(g.M, (c + 127) / 128);
       wmax = std::max<int64_t>(wmax, ((g.M + c1 - 1) / c1) * c * d.bk);
+      wmax = std::max<int64_t>(wmax, tc2_wgrad_wpart_elems(d, l));
     }
   }
   const int64_t pbytes = static_cast<int64_t>(g.Pmax) * std::max<int64_t>(g.C, d.bk) * 16;
@@ -382,7 +386,8 @@ static void backward_impl(Block* b, const float* params, float* grad_acc, float*
   if (b->tc) {
     LaunchScope ls(b, KC_PACK, 0, 0);
     b->launches--;
-    tc_pretile_w2(b, params, false);
+    tc_pretile_w2(b, params, false);  // each pretile counts its own launch
+    tc2_pretile_w1t(b, params);
   }
   // Two streams: the data-gradient chain (3x3 dgrad -> BN_b bwd -> 1x1 dgrad
   // -> BN_a bwd + accumulate) on the main stream, the weight-gradient branch
@@ -454,10 +459,13 @@ static void backward_impl(Block* b, const float* params, float* grad_acc, float*
     if (fork) b->stream = b->side;
     {
       int splits;
+      bool v2 = false;  // v2 partials are [split][j][i] like the SIMT ones
       {
         LaunchScope ls(b, KC_C1_WGRAD, M * ((4.0 + Sb) * d.bk + Sb * a.c), f1);
         if (b->tc) {
-          splits = tc_conv1x1_wgrad(b, a);
+          splits = tc2_conv1x1_wgrad(b, a);
+          v2 = splits > 0;
+          if (!v2) splits = tc_conv1x1_wgrad(b, a);
         } else {
           const int64_t tiles = ((d.bk + 63) / 64) * ((a.c + 63) / 64);
           a.kchunk = wgrad_chunk(g.M, tiles);
@@ -466,7 +474,7 @@ static void backward_impl(Block* b, const float* params, float* grad_acc, float*
         }
       }
       LaunchScope ls(b, KC_REDUCE_W, 4.0 * splits * d.bk * a.c, 0);
-      if (b->tc)
+      if (b->tc && !v2)
         k_reduce_w1t<<<blocks_for(static_cast<int64_t>(d.bk) * a.c, 32), dim3(32, 8), 0,
                        b->stream>>>(b->wpart, splits, d.bk, a.c, d_w1);
       else
@@ -478,7 +486,9 @@ static void backward_impl(Block* b, const float* params, float* grad_acc, float*
     // ---- data chain: 1x1 dgrad (+ReLU mask by act_a, BN_a sums) ----
     {
       LaunchScope ls(b, KC_C1_DGRAD, M * ((4.0 + Sb) * d.bk + (Sb + 4.0) * a.c), f1);
-      if (b->tc) tc_conv1x1_dgrad(b, a);
+      if (b->tc) {
+        if (!tc2_conv1x1_dgrad(b, a, l)) tc_conv1x1_dgrad(b, a);
+      }
       else gemm_bn2<128, Conv1x1Dgrad>(b, a, g.M, a.c, 1);
     }
     // BN_a backward (graph.hpp:929-932) + concat-backward accumulate (:936-941)
@@ -620,6 +630,13 @@ int create(const dpb_block_desc* desc, int device, void* stream, Block** out) {
     if (b->halo.fwd_ok) b->w2f = p;
     p += align_up(b->halo.fwd_layer_bytes * desc->m, 256);
     if (b->halo.bwd_ok) b->w2b = p;
+    p += align_up(b->halo.bwd_layer_bytes * desc->m, 256);
+    int64_t w1b = 0;
+    for (int l = 0; l < desc->m; ++l) {
+      b->w1b_off.push_back(w1b);
+      w1b += tc2_w1b_layer_bytes(*desc, l);
+    }
+    if (w1b > 0) b->w1b = p;
   }
   if (cudaStreamCreateWithFlags(&b->side, cudaStreamNonBlocking) != cudaSuccess) b->side = nullptr;
   for (int i = 0; b->side && i < 3 * desc->m; ++i) {

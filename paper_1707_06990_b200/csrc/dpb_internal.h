@@ -65,6 +65,8 @@ struct Block {
   uint8_t* wtile = nullptr;           // pre-tiled bf16 W1 operands (tensor-core path)
   std::vector<int64_t> wtile_off;
   HaloPlan halo;
+  uint8_t* w1b = nullptr;             // pre-tiled W1^T (v2 1x1 dgrad), per layer
+  std::vector<int64_t> w1b_off;
   uint8_t* w2f = nullptr;             // pre-tiled W2 (halo forward), per layer
   uint8_t* w2b = nullptr;             // pre-tiled W2^T (halo dgrad), per layer
   bool tc = false;                    // tensor-core (tcgen05) GEMMs
@@ -120,6 +122,12 @@ int tc_conv1x1_wgrad(Block* b, LayerArgs<float> a);
 bool tc2_conv1x1_fwd(Block* b, const LayerArgs<float>& a, int l);
 int64_t tc2_w1_tile_bytes(const dpb_block_desc& d, int l);
 void tc2_pretile_w1(Block* b, const float* params);
+int tc2_bwd_bn(const dpb_block_desc& d);
+int64_t tc2_w1b_layer_bytes(const dpb_block_desc& d, int l);
+void tc2_pretile_w1t(Block* b, const float* params);
+bool tc2_conv1x1_dgrad(Block* b, const LayerArgs<float>& a, int l);
+int64_t tc2_wgrad_wpart_elems(const dpb_block_desc& d, int l);
+int tc2_conv1x1_wgrad(Block* b, const LayerArgs<float>& a);
 int tc_conv3x3_wgrad(Block* b, LayerArgs<float> a);
 
 }  // namespace dpb

@@ -49,7 +49,12 @@ static int num_sms() {
 }
 
 template <class Op>
-static void launch2(Block* b, const Op& op, int ntiles, size_t aux) {
+static constexpr size_t fixed_smem() {
+  return 1024 + Op::kNR * Op::kRawBytes + Op::kNS * Op::kOpBytes + Op::kNE * Op::kEpiBytes;
+}
+
+template <class Op>
+static void launch2(Block* b, const Op& op, dim3 grid, size_t aux) {
   static bool configured = false;
   if (!configured) {
     cudaFuncAttributes fa{};
@@ -58,14 +63,7 @@ static void launch2(Block* b, const Op& op, int ntiles, size_t aux) {
                          227 * 1024 - static_cast<int>(fa.sharedSizeBytes));
     configured = true;
   }
-  const size_t smem = 1024 + Op::kNR * Op::kRawBytes + Op::kNS * Op::kOpBytes + aux;
-  const int grid = std::min(ntiles, num_sms());
-  tc2::tc2_kernel<Op><<<grid, tc2::kThreads, smem, b->stream>>>(op);
-}
-
-template <class Op>
-static constexpr size_t fixed_smem() {
-  return 1024 + Op::kNR * Op::kRawBytes + Op::kNS * Op::kOpBytes;
+  tc2::tc2_kernel<Op><<<grid, tc2::Roles<Op>::kThreads, fixed_smem<Op>() + aux, b->stream>>>(op);
 }
 
 int tc2_bn_1x1(int bk) {
@@ -118,7 +116,7 @@ bool tc2_conv1x1_fwd(Block* b, const LayerArgs<float>& a, int l) {
     if (!make_map_f32(&op.xmap, a.feat, a.C, a.M, a.C, 32, tc::kBM)) return false;
     op.a = a;
     op.w1t = w1t;
-    launch2(b, op, ntiles, aux);
+    launch2(b, op, dim3(std::min(ntiles, num_sms())), aux);
     return true;
   };
   // B resident in shared memory when all of W1's tiles fit, else streamed
@@ -133,4 +131,107 @@ bool tc2_conv1x1_fwd(Block* b, const LayerArgs<float>& a, int l) {
   }
 }
 
+// ---- 1x1 backward data on the v2 engine ------------------------------------------
+// Column-tile width bound of Dgrad1x1 for a block (0: not supported).
+int tc2_bwd_bn(const dpb_block_desc& d) { return d.bk <= 64 ? 256 : 128; }
+
+int64_t tc2_w1b_layer_bytes(const dpb_block_desc& d, int l) {
+  const int bn = tc2_bwd_bn(d);
+  int nn, nw;
+  tc2::bwd_ntiles(d.c0 + l * d.k, bn, nn, nw);
+  return static_cast<int64_t>(nn) * tc2::bwd_nkb(d.bk) * bn * 64;
+}
+
+void tc2_pretile_w1t(Block* b, const float* params) {
+  const dpb_block_desc& d = b->d;
+  if (!b->w1b) return;
+  const dim3 grid(16, d.m);
+  if (tc2_bwd_bn(d) == 256)
+    tc2::k_pretile_w1t_all<256><<<grid, 256, 0, b->stream>>>(params, d.c0, d.k, d.bk, b->w1b);
+  else
+    tc2::k_pretile_w1t_all<128><<<grid, 256, 0, b->stream>>>(params, d.c0, d.k, d.bk, b->w1b);
+  b->launches++;
+}
+
+bool tc2_conv1x1_dgrad(Block* b, const LayerArgs<float>& a, int l) {
+  if (a.C % 4 != 0 || a.c % 4 != 0 || !b->w1b) return false;
+  const int ntiles = static_cast<int>((a.M + tc::kBM - 1) / tc::kBM);
+  auto go = [&](auto tag) -> bool {
+    using Op = decltype(tag);
+    const size_t aux = static_cast<size_t>(tc2::bwd_nkb(a.bk)) * Op::kBTile +
+                       (sizeof(BnBwd) * a.bk + 15) / 16 * 16 + sizeof(BnFwd) * Op::BN;
+    if (fixed_smem<Op>() + aux > 220 * 1024) return false;
+    Op op{};
+    if (!make_map_f32(&op.gmap, a.g0, a.bk, a.M, a.bk, 32, tc::kBM) ||
+        !make_map_f32(&op.zmap, a.z, a.bk, a.M, a.bk, 32, tc::kBM) ||
+        !make_map_f32(&op.fmap, a.feat, a.C, a.M, a.C, 32, tc::kBM) ||
+        !make_map_f32(&op.omap, a.g1, a.c, a.M, a.c, 32, tc::kBM))
+      return false;
+    op.a = a;
+    op.w1t = b->w1b + b->w1b_off[l];
+    int nn, nw;
+    tc2::bwd_ntiles(a.c, Op::BN, nn, nw);
+    op.nw = nw;
+    const int gx = std::max(1, std::min(ntiles, num_sms() / nn));
+    launch2(b, op, dim3(gx, nn), aux);
+    return true;
+  };
+  return tc2_bwd_bn(b->d) == 256 ? go(tc2::Dgrad1x1<256>{}) : go(tc2::Dgrad1x1<128>{});
+}
+
+// ---- 1x1 backward weights on the v2 engine -----------------------------------------
+// Upper bound of the split count (CTAs along x) for the arena plan.
+int64_t tc2_wgrad_wpart_elems(const dpb_block_desc& d, int l) {
+  const int c = d.c0 + l * d.k;
+  const int bn = d.bk <= 64 ? 256 : 128;
+  int nn, nw;
+  tc2::bwd_ntiles(c, bn, nn, nw);
+  return static_cast<int64_t>(std::max(1, 160 / nn)) * d.bk * c;
+}
+
+// Returns the number of splits written to wpart ([split][j][i]), 0 when the
+// shape is not supported (the caller then uses the v1 kernel).
+int tc2_conv1x1_wgrad(Block* b, const LayerArgs<float>& a) {
+  if (a.C % 4 != 0 || a.c % 4 != 0 || a.bk % 8 != 0 || a.bk > 192) return 0;
+  int splits = 0;
+  auto go = [&](auto tag) -> bool {
+    using Op = decltype(tag);
+    const size_t aux = (sizeof(BnBwd) * a.bk + 15) / 16 * 16 + sizeof(BnFwd) * Op::BN;
+    if (fixed_smem<Op>() + aux > 220 * 1024) return false;
+    Op op{};
+    if (!make_map_f32(&op.gmap, a.g0, a.bk, a.M, a.bk, 32, Op::kBoxP) ||
+        !make_map_f32(&op.zmap, a.z, a.bk, a.M, a.bk, 32, Op::kBoxP) ||
+        !make_map_f32(&op.fmap, a.feat, a.C, a.M, a.C, 32, Op::kBoxP))
+      return false;
+    op.a = a;
+    int nn, nw;
+    tc2::bwd_ntiles(a.c, Op::BN, nn, nw);
+    op.nw = nw;
+    op.nblk = static_cast<int>((a.M + Op::kBoxP - 1) / Op::kBoxP);
+    const int target = std::max(1, num_sms() / nn);
+    op.kchunk = (op.nblk + target - 1) / target;
+    const int gx = (op.nblk + op.kchunk - 1) / op.kchunk;  // every CTA owns >= 1 block
+    launch2(b, op, dim3(gx, nn), aux);
+    splits = gx;
+    return true;
+  };
+  const int jb = (a.bk + 31) / 32;
+  const bool ok = jb <= 2 ? go(tc2::Wgrad1x1<256, 2>{})
+                  : jb <= 4 ? go(tc2::Wgrad1x1<128, 4>{})
+                            : go(tc2::Wgrad1x1<128, 6>{});
+  return ok ? splits : 0;
+}
+
 }  // namespace dpb
+
+// Debug-only (not part of dpb.h): arm the v2 engine's phase clocks for launches
+// with layer width c (c <= 0 disarms), or read them (host: 148 x 28 int64).
+extern "C" __attribute__((visibility("default"))) int dpb_debug_tc2_clocks(int c, long long* host) {
+  if (host == nullptr) {
+    const int flags = c >> 16;
+    c &= 0xffff;
+    cudaMemcpyToSymbol(dpb::tc2::g_tc2_dbg_flags, &flags, sizeof(int));
+    return cudaMemcpyToSymbol(dpb::tc2::g_tc2_dbg_c, &c, sizeof(int));
+  }
+  return cudaMemcpyFromSymbol(host, dpb::tc2::g_tc2_clock, sizeof(long long) * 148 * 28);
+}
