@@ -22,6 +22,7 @@
 #include "dpb_kernels.cuh"
 #include "dpb_simt.cuh"
 #include "dpb_internal.h"
+#include "dpb_launch.h"
 
 namespace dpb {
 
@@ -217,7 +218,7 @@ static void launch_gemm(Block* b, const Op& op, dim3 grid, size_t dyn) {
                          227 * 1024 - static_cast<int>(fa.sharedSizeBytes));
     configured = true;
   }
-  gemm_kernel<BM, BN, Op><<<grid, kThreads, dyn, b->stream>>>(op);
+  launch(gemm_kernel<BM, BN, Op>, grid, kThreads, dyn, b->stream, op);
 }
 
 // Dispatch on the N tile for ops whose N is a runtime channel count.
@@ -298,10 +299,10 @@ static void forward_impl(Block* b, const float* x_in, const float* params, float
     LaunchScope ls(b, KC_PACK, M * d.c0 * (4 + Sb), 0);
     if (d.layout == DPB_NCHW) {
       dim3 grid(blocks_for(hw, 32), blocks_for(d.c0, 32), static_cast<unsigned>(d.n));
-      k_nchw_to_nhwc<S><<<grid, dim3(32, 8), 0, b->stream>>>(x_in, d.n, d.c0, hw, feat,
+      launch(k_nchw_to_nhwc<S>, grid, dim3(32, 8), 0, b->stream, x_in, d.n, d.c0, hw, feat,
                                                              static_cast<int>(g.C), 0);
     } else {
-      k_nhwc_copy<S><<<blocks_for(g.M * d.c0, 256), 256, 0, b->stream>>>(
+      launch(k_nhwc_copy<S>, blocks_for(g.M * d.c0, 256), 256, 0, b->stream, 
           x_in, d.c0, g.M, d.c0, feat, static_cast<int>(g.C), 0);
     }
   }
@@ -317,11 +318,11 @@ static void forward_impl(Block* b, const float* x_in, const float* params, float
   if (!eval) {
     {
       LaunchScope ls(b, KC_STATS, M * d.c0 * Sb, 0);
-      k_channel_partials<S><<<g.P, 256, 0, b->stream>>>(feat, static_cast<int>(g.C), 0, g.M,
+      launch(k_channel_partials<S>, g.P, 256, 0, b->stream, feat, static_cast<int>(g.C), 0, g.M,
                                                         d.c0, b->part);
     }
     LaunchScope ls(b, KC_FINALIZE, 0, 0);
-    k_finalize_stats<<<blocks_for(32LL * d.c0, 256), 256, 0, b->stream>>>(
+    launch(k_finalize_stats, blocks_for(32LL * d.c0, 256), 256, 0, b->stream, 
         b->part, g.P, d.c0, count, fmean, fvar, 0);
   }
   for (int l = 0; l < d.m; ++l) {
@@ -344,7 +345,7 @@ static void forward_impl(Block* b, const float* x_in, const float* params, float
     if (!eval) {
       LaunchScope ls(b, KC_FINALIZE, 0, 0);
       float* zm = b->zstat + static_cast<int64_t>(l) * 2 * d.bk;
-      k_finalize_stats<<<blocks_for(32LL * d.bk, 256), 256, 0, b->stream>>>(
+      launch(k_finalize_stats, blocks_for(32LL * d.bk, 256), 256, 0, b->stream, 
           b->part, g.P, d.bk, count, zm, zm + d.bk, 0);
     }
     int p3 = g.P;
@@ -355,13 +356,13 @@ static void forward_impl(Block* b, const float* x_in, const float* params, float
     }
     if (!eval) {
       LaunchScope ls(b, KC_FINALIZE, 0, 0);
-      k_finalize_stats<<<blocks_for(32LL * d.k, 256), 256, 0, b->stream>>>(
+      launch(k_finalize_stats, blocks_for(32LL * d.k, 256), 256, 0, b->stream, 
           b->part, p3, d.k, count, fmean, fvar, a.c);
     }
   }
   if (!eval && update_running) {
     LaunchScope ls(b, KC_RUNNING, 0, 0);
-    k_running_update<<<blocks_for(b->sz.stat_elems, 256), 256, 0, b->stream>>>(
+    launch(k_running_update, blocks_for(b->sz.stat_elems, 256), 256, 0, b->stream, 
         d.m, d.c0, d.k, d.bk, static_cast<int>(g.C), b->fstat, b->zstat, running,
         b->sz.stat_elems);
   }
@@ -378,7 +379,7 @@ static void backward_impl(Block* b, const float* params, float* grad_acc, float*
     LaunchScope ls(b, KC_PACK, M * g.C * 8, 0);
     b->acc_cur = b->acc;
     dim3 grid(blocks_for(hw, 32), blocks_for(g.C, 32), static_cast<unsigned>(d.n));
-    k_nchw_to_nhwc<float><<<grid, dim3(32, 8), 0, b->stream>>>(grad_acc, d.n, g.C, hw,
+    launch(k_nchw_to_nhwc<float>, grid, dim3(32, 8), 0, b->stream, grad_acc, d.n, g.C, hw,
                                                                b->acc, static_cast<int>(g.C), 0);
   } else {
     b->acc_cur = grad_acc;
@@ -434,7 +435,7 @@ static void backward_impl(Block* b, const float* params, float* grad_acc, float*
         }
       }
       LaunchScope ls(b, KC_REDUCE_W, 4.0 * splits * rows * d.k, 0);
-      k_reduce_w2<<<blocks_for(9LL * d.k * d.bk, 32), dim3(32, 8), 0, b->stream>>>(
+      launch(k_reduce_w2, blocks_for(9LL * d.k * d.bk, 32), dim3(32, 8), 0, b->stream, 
           b->wpart, splits, d.bk, d.k, d_w2);
     }
     b->stream = main_st;
@@ -448,7 +449,7 @@ static void backward_impl(Block* b, const float* params, float* grad_acc, float*
     // BN_b backward sums -> dgamma_b, dbeta_b, coefficients (graph.hpp:913-916)
     {
       LaunchScope ls(b, KC_FINALIZE, 0, 0);
-      k_finalize_bn_bwd<<<blocks_for(32LL * d.bk, 256), 256, 0, b->stream>>>(
+      launch(k_finalize_bn_bwd, blocks_for(32LL * d.bk, 256), 256, 0, b->stream, 
           b->part, pd, d.bk, count, d_gb, d_bb, const_cast<float*>(a.bnb_bwd));
     }
     if (fork) {
@@ -475,11 +476,9 @@ static void backward_impl(Block* b, const float* params, float* grad_acc, float*
       }
       LaunchScope ls(b, KC_REDUCE_W, 4.0 * splits * d.bk * a.c, 0);
       if (b->tc && !v2)
-        k_reduce_w1t<<<blocks_for(static_cast<int64_t>(d.bk) * a.c, 32), dim3(32, 8), 0,
-                       b->stream>>>(b->wpart, splits, d.bk, a.c, d_w1);
+        launch(k_reduce_w1t, blocks_for(static_cast<int64_t>(d.bk) * a.c, 32), dim3(32, 8), 0, b->stream, b->wpart, splits, d.bk, a.c, d_w1);
       else
-        k_reduce_w1<<<blocks_for(static_cast<int64_t>(d.bk) * a.c, 32), dim3(32, 8), 0,
-                      b->stream>>>(b->wpart, splits, d.bk, a.c, d_w1);
+        launch(k_reduce_w1, blocks_for(static_cast<int64_t>(d.bk) * a.c, 32), dim3(32, 8), 0, b->stream, b->wpart, splits, d.bk, a.c, d_w1);
     }
     if (fork) cudaEventRecord(ev(l, 2), b->side);
     b->stream = main_st;
@@ -494,12 +493,12 @@ static void backward_impl(Block* b, const float* params, float* grad_acc, float*
     // BN_a backward (graph.hpp:929-932) + concat-backward accumulate (:936-941)
     {
       LaunchScope ls(b, KC_FINALIZE, 0, 0);
-      k_finalize_bn_bwd<<<blocks_for(32LL * a.c, 256), 256, 0, b->stream>>>(
+      launch(k_finalize_bn_bwd, blocks_for(32LL * a.c, 256), 256, 0, b->stream, 
           b->part, g.P, a.c, count, d_ga, d_ba, b->bna_bwd);
     }
     {
       LaunchScope ls(b, KC_BN_APPLY_ACC, M * a.c * (4.0 + Sb + 8.0), 0);
-      k_bn_apply_accumulate<S><<<blocks_for(g.M * a.c, 256), 256, 0, b->stream>>>(
+      launch(k_bn_apply_accumulate<S>, blocks_for(g.M * a.c, 256), 256, 0, b->stream, 
           g.M, a.c, static_cast<int>(g.C), static_cast<const S*>(b->feat), b->g1, a.amean,
           a.avar, a.gamma_a, b->bna_bwd, b->acc_cur);
     }
@@ -511,7 +510,7 @@ static void backward_impl(Block* b, const float* params, float* grad_acc, float*
   if (d.layout == DPB_NCHW) {
     LaunchScope ls(b, KC_PACK, M * g.C * 8, 0);
     dim3 grid(blocks_for(hw, 32), blocks_for(g.C, 32), static_cast<unsigned>(d.n));
-    k_nhwc_to_nchw<float><<<grid, dim3(32, 8), 0, b->stream>>>(b->acc, static_cast<int>(g.C), 0,
+    launch(k_nhwc_to_nchw<float>, grid, dim3(32, 8), 0, b->stream, b->acc, static_cast<int>(g.C), 0,
                                                                d.n, g.C, hw, grad_acc);
   }
 }
@@ -544,7 +543,7 @@ template <typename S>
 static void read_feats_impl(Block* b, float* dst) {
   const dim3 grid(blocks_for(b->d.h * b->d.w, 32), blocks_for(b->g.C, 32),
                   static_cast<unsigned>(b->d.n));
-  k_nhwc_to_nchw<S><<<grid, dim3(32, 8), 0, b->stream>>>(
+  launch(k_nhwc_to_nchw<S>, grid, dim3(32, 8), 0, b->stream, 
       static_cast<const S*>(b->feat), static_cast<int>(b->g.C), 0, b->d.n,
       static_cast<int>(b->g.C), b->d.h * b->d.w, dst);
 }
@@ -554,7 +553,7 @@ static void read_z_impl(Block* b, float* dst) {
   const int64_t hw = b->d.h * b->d.w;
   const dim3 grid(blocks_for(hw, 32), blocks_for(b->d.bk, 32), static_cast<unsigned>(b->d.n));
   for (int l = 0; l < b->d.m; ++l)
-    k_nhwc_to_nchw<S><<<grid, dim3(32, 8), 0, b->stream>>>(
+    launch(k_nhwc_to_nchw<S>, grid, dim3(32, 8), 0, b->stream, 
         static_cast<const S*>(b->z) + static_cast<int64_t>(l) * b->g.M * b->d.bk, b->d.bk, 0,
         b->d.n, b->d.bk, hw, dst + static_cast<int64_t>(l) * b->g.M * b->d.bk);
 }
@@ -572,7 +571,7 @@ int read_z(Block* b, float* dst) {
 }
 
 int read_stats(Block* b, float* dst) {
-  k_export_stats<<<blocks_for(b->sz.stat_elems, 256), 256, 0, b->stream>>>(
+  launch(k_export_stats, blocks_for(b->sz.stat_elems, 256), 256, 0, b->stream, 
       b->d.m, b->d.c0, b->d.k, b->d.bk, static_cast<int>(b->g.C), b->fstat, b->zstat, dst,
       b->sz.stat_elems);
   const cudaError_t e = cudaGetLastError();

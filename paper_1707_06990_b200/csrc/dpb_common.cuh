@@ -50,4 +50,18 @@ struct BnBwd {
   float mean, inv, ginv, mg, mgx;
 };
 
+// Programmatic dependent launch (PDL): every block-path kernel is launched with
+// programmatic stream serialization (dpb_launch.h).  A kernel waits for its
+// predecessor's completion (griddepcontrol.wait) before its first global read
+// of data written by a kernel, then lets its own dependents start launching:
+// triggering only after the wait guarantees that, when a kernel starts, every
+// kernel but its immediate predecessor has completed.  Both are no-ops for a
+// launch without the attribute.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+__device__ __forceinline__ void pdl_enter() {
+  pdl_wait();
+  pdl_trigger();
+}
+
 }  // namespace dpb

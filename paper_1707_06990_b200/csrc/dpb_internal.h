@@ -36,6 +36,7 @@ struct ProfRec {
 // Tile choices of the 3x3 halo kernels (dpb_tc_block.cu tc_halo_plan).
 struct HaloPlan {
   bool fwd_ok = false, bwd_ok = false;
+  bool fwd_taps = false;  // forward as one GEMM over all 9 taps (Tc3x3FwdTaps)
   int fwd_bn = 0, fwd_kc = 0, bwd_bn = 0, bwd_kc = 0;
   int64_t fwd_layer_bytes = 0, bwd_layer_bytes = 0;  // pre-tiled W2 image per layer
 };

@@ -13,6 +13,7 @@ template <typename S>
 __global__ void k_nchw_to_nhwc(const float* __restrict__ src, int64_t n, int c,
                                int64_t hw, S* __restrict__ dst, int pitch,
                                int c_off) {
+  pdl_enter();
   __shared__ float tile[32][33];
   const int64_t img = blockIdx.z;
   const int64_t p0 = static_cast<int64_t>(blockIdx.x) * 32;
@@ -34,6 +35,7 @@ template <typename S>
 __global__ void k_nhwc_to_nchw(const S* __restrict__ src, int pitch, int c_off,
                                int64_t n, int c, int64_t hw,
                                float* __restrict__ dst) {
+  pdl_enter();
   __shared__ float tile[32][33];
   const int64_t img = blockIdx.z;
   const int64_t p0 = static_cast<int64_t>(blockIdx.x) * 32;
@@ -55,6 +57,7 @@ __global__ void k_nhwc_to_nchw(const S* __restrict__ src, int pitch, int c_off,
 template <typename S>
 __global__ void k_nhwc_copy(const float* __restrict__ src, int sp, int64_t M, int c,
                             S* __restrict__ dst, int dp, int d_off) {
+  pdl_enter();
   const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (i >= M * c) return;
   const int64_t p = i / c;
@@ -70,6 +73,7 @@ template <typename S>
 __global__ void __launch_bounds__(256)
 k_channel_partials(const S* __restrict__ src, int pitch, int c_off, int64_t M,
                    int nch, double2* __restrict__ part) {
+  pdl_enter();
   __shared__ double r1[8][33], r2[8][33];
   const int lane = threadIdx.x % 32, grp = threadIdx.x / 32;
   const int64_t m0 = static_cast<int64_t>(blockIdx.x) * 128;
@@ -121,6 +125,7 @@ __device__ __forceinline__ double2 fold_partials(const double2* part, int P, int
 __global__ void k_finalize_stats(const double2* __restrict__ part, int P, int nch,
                                  double count, float* __restrict__ mean_out,
                                  float* __restrict__ var_out, int first) {
+  pdl_enter();
   const int ch = (blockIdx.x * blockDim.x + threadIdx.x) / 32;
   if (ch >= nch) return;
   const double2 s = fold_partials(part, P, nch, ch);
@@ -138,6 +143,7 @@ __global__ void k_finalize_stats(const double2* __restrict__ part, int P, int nc
 __global__ void k_finalize_bn_bwd(const double2* __restrict__ part, int P, int nch,
                                   double count, float* __restrict__ dgamma,
                                   float* __restrict__ dbeta, float* __restrict__ coef) {
+  pdl_enter();
   const int ch = (blockIdx.x * blockDim.x + threadIdx.x) / 32;
   if (ch >= nch) return;
   const double2 s = fold_partials(part, P, nch, ch);
@@ -161,6 +167,7 @@ k_bn_apply_accumulate(int64_t M, int c, int C, const S* __restrict__ feat,
                       const float* __restrict__ avar,
                       const float* __restrict__ gamma, const float* __restrict__ coef,
                       float* __restrict__ acc) {
+  pdl_enter();
   const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (i >= M * c) return;
   const int64_t p = i / c;
@@ -196,6 +203,7 @@ __device__ __forceinline__ void fold_splits(const float* __restrict__ wpart, int
 // dW2: partial element e = r*k + o with r = tap*bk + j -> flat W2[o][j][tap]
 __global__ void k_reduce_w2(const float* __restrict__ wpart, int splits, int bk, int k,
                             float* __restrict__ dw2) {
+  pdl_enter();
   const int64_t n = 9LL * bk * k;
   fold_splits(wpart, splits, n, [=] __device__(int64_t e) {
     const int o = static_cast<int>(e % k);
@@ -208,6 +216,7 @@ __global__ void k_reduce_w2(const float* __restrict__ wpart, int splits, int bk,
 // dW1 (SIMT partials [split][j][i]) -> flat W1[j][i]
 __global__ void k_reduce_w1(const float* __restrict__ wpart, int splits, int bk, int c,
                             float* __restrict__ dw1) {
+  pdl_enter();
   fold_splits(wpart, splits, static_cast<int64_t>(bk) * c, [] __device__(int64_t e) { return e; },
               dw1);
 }
@@ -215,6 +224,7 @@ __global__ void k_reduce_w1(const float* __restrict__ wpart, int splits, int bk,
 // dW1 from the tensor-core partials [split][i][j] -> flat W1[j][i]
 __global__ void k_reduce_w1t(const float* __restrict__ wpart, int splits, int bk, int c,
                              float* __restrict__ dw1) {
+  pdl_enter();
   fold_splits(wpart, splits, static_cast<int64_t>(bk) * c, [=] __device__(int64_t e) {
     const int64_t i = e / bk, j = e - i * bk;
     return j * c + i;
@@ -249,6 +259,7 @@ __global__ void k_running_update(int m, int c0, int k, int bk, int C,
                                  const float* __restrict__ fstat,
                                  const float* __restrict__ zstat,
                                  float* __restrict__ running, int64_t total) {
+  pdl_enter();
   const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (i >= total) return;
   const float s = stat_at(m, c0, k, bk, C, fstat, zstat, i);
@@ -260,6 +271,7 @@ __global__ void k_export_stats(int m, int c0, int k, int bk, int C,
                                const float* __restrict__ fstat,
                                const float* __restrict__ zstat, float* __restrict__ out,
                                int64_t total) {
+  pdl_enter();
   const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (i >= total) return;
   out[i] = stat_at(m, c0, k, bk, C, fstat, zstat, i);

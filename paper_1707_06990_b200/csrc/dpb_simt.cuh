@@ -34,6 +34,7 @@ __global__ void __launch_bounds__(kThreads) gemm_kernel(Op op) {
   const int tx = tid % 16, ty = tid / 16;
   const int64_t m0 = static_cast<int64_t>(blockIdx.x) * BM;
   const int n0 = blockIdx.y * BN;
+  pdl_enter();
   op.prologue(dyn, n0);
   __syncthreads();
   int64_t kbeg, kend;

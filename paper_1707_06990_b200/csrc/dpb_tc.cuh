@@ -113,6 +113,36 @@ __device__ __forceinline__ void mma_bf16_lh(uint32_t d_tmem, uint32_t alo, uint3
 
 // Low / high 32 bits of a no-swizzle smem descriptor; adding (bytes >> 4) to
 // the low half moves the start address.
+// Warp-collective forms: every lane of a convergent warp executes them with
+// warp-uniform operands and one elected lane issues, so the compiler keeps the
+// descriptors in uniform registers (no per-MMA R2UR waterfall).
+__device__ __forceinline__ void mma_bf16_lh_w(uint32_t d_tmem, uint32_t alo, uint32_t ahi,
+                                              uint32_t blo, uint32_t bhi, uint32_t idesc,
+                                              uint32_t accumulate) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p, e;\n"
+      ".reg .b64 da, db;\n"
+      "mov.b64 da, {%1, %2};\n"
+      "mov.b64 db, {%3, %4};\n"
+      "setp.ne.b32 p, %6, 0;\n"
+      "elect.sync _|e, 0xffffffff;\n"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], da, db, %5, p;\n"
+      "}\n" ::"r"(d_tmem),
+      "r"(alo), "r"(ahi), "r"(blo), "r"(bhi), "r"(idesc), "r"(accumulate));
+}
+__device__ __forceinline__ void mma_commit_w(uint64_t* bar) {
+  asm volatile(
+      "{\n"
+      ".reg .pred e;\n"
+      "elect.sync _|e, 0xffffffff;\n"
+      "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n"
+      "}\n" ::"r"(smem_u32(bar))
+      : "memory");
+}
+// warp-uniform copy of a value every lane holds
+__device__ __forceinline__ uint32_t uniform(uint32_t v) { return __shfl_sync(0xffffffffu, v, 0); }
+
 __device__ __forceinline__ uint32_t sdesc_lo(uint32_t saddr, uint32_t lbo) {
   return ((saddr >> 4) & 0x3FFF) | (((lbo >> 4) & 0x3FFF) << 16);
 }
@@ -139,6 +169,14 @@ __device__ __forceinline__ void tmem_ld8(uint32_t taddr, float (&v)[8]) {
 #pragma unroll
   for (int i = 0; i < 8; ++i) v[i] = __uint_as_float(r[i]);
 }
+
+// 4 consecutive TMEM columns of this warp's 32 lanes (no wait: tmem_wait_ld).
+__device__ __forceinline__ void tmem_ld4_nowait(uint32_t taddr, uint32_t (&r)[4]) {
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0, %1, %2, %3}, [%4];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+               : "r"(taddr));
+}
+__device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 
 // 16 consecutive TMEM columns of this warp's 32 lanes (one wait).
 __device__ __forceinline__ void tmem_ld16(uint32_t taddr, float (&v)[16]) {
@@ -171,6 +209,44 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&v)[32]) {
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 #pragma unroll
   for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+// Warp reduction of 8 columns x 32 rows in 9 shuffles (transpose-reduce): on
+// return lane L holds the full column sum of column (L >> 2) & 7 in v[0].
+__device__ __forceinline__ float warp_colsum8(float (&v)[8], int lane) {
+  // step 1: exchange halves of the 8 values with lane ^ 16
+  {
+    const bool up = lane & 16;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const float send = up ? v[i] : v[i + 4];
+      const float recv = __shfl_xor_sync(0xffffffffu, send, 16);
+      v[i] = (up ? v[i + 4] : v[i]) + recv;
+    }
+  }
+  // lanes with bit 4 set now hold columns 4..7 in v[0..3], others 0..3
+  {
+    const bool up = lane & 8;
+#pragma unroll
+    for (int i = 0; i < 2; ++i) {
+      const float send = up ? v[i] : v[i + 2];
+      const float recv = __shfl_xor_sync(0xffffffffu, send, 8);
+      v[i] = (up ? v[i + 2] : v[i]) + recv;
+    }
+  }
+  {
+    const bool up = lane & 4;
+    const float send = up ? v[0] : v[1];
+    const float recv = __shfl_xor_sync(0xffffffffu, send, 4);
+    v[0] = (up ? v[1] : v[0]) + recv;
+  }
+  v[0] += __shfl_xor_sync(0xffffffffu, v[0], 2);
+  v[0] += __shfl_xor_sync(0xffffffffu, v[0], 1);
+  // column held by this lane: bit4 -> +4, bit3 -> +2, bit2 -> +1
+  return v[0];
+}
+__device__ __forceinline__ int colsum8_column(int lane) {
+  return ((lane >> 4) & 1) * 4 + ((lane >> 3) & 1) * 2 + ((lane >> 2) & 1);
 }
 
 // ---- async-copy / barrier PTX (mbarrier tx counts, TMA, bulk copies) ---------
@@ -390,6 +466,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(const Op op) {
     mbar_init(&mbar[1], 1);
     fence_barrier_init();
   }
+  pdl_enter();  // barrier init / TMEM alloc above overlap the predecessor
   op.prologue(aux);
   tc_fence_before();
   __syncthreads();

@@ -7,6 +7,7 @@
 #include <algorithm>
 
 #include "dpb_internal.h"
+#include "dpb_launch.h"
 #include "dpb_tc2.cuh"
 
 namespace dpb {
@@ -63,7 +64,7 @@ static void launch2(Block* b, const Op& op, dim3 grid, size_t aux) {
                          227 * 1024 - static_cast<int>(fa.sharedSizeBytes));
     configured = true;
   }
-  tc2::tc2_kernel<Op><<<grid, tc2::Roles<Op>::kThreads, fixed_smem<Op>() + aux, b->stream>>>(op);
+  launch(tc2::tc2_kernel<Op>, grid, tc2::Roles<Op>::kThreads, fixed_smem<Op>() + aux, b->stream, op);
 }
 
 int tc2_bn_1x1(int bk) {
@@ -91,12 +92,12 @@ void tc2_pretile_w1(Block* b, const float* params) {
   if (!bn || !b->wtile) return;
   const dim3 grid(16, d.m);
   switch (bn) {
-    case 16: tc2::k_pretile_w1_all<16><<<grid, 256, 0, b->stream>>>(params, d.c0, d.k, d.bk, d.m, b->wtile); break;
-    case 32: tc2::k_pretile_w1_all<32><<<grid, 256, 0, b->stream>>>(params, d.c0, d.k, d.bk, d.m, b->wtile); break;
-    case 48: tc2::k_pretile_w1_all<48><<<grid, 256, 0, b->stream>>>(params, d.c0, d.k, d.bk, d.m, b->wtile); break;
-    case 64: tc2::k_pretile_w1_all<64><<<grid, 256, 0, b->stream>>>(params, d.c0, d.k, d.bk, d.m, b->wtile); break;
-    case 128: tc2::k_pretile_w1_all<128><<<grid, 256, 0, b->stream>>>(params, d.c0, d.k, d.bk, d.m, b->wtile); break;
-    default: tc2::k_pretile_w1_all<192><<<grid, 256, 0, b->stream>>>(params, d.c0, d.k, d.bk, d.m, b->wtile); break;
+    case 16: launch(tc2::k_pretile_w1_all<16>, grid, 256, 0, b->stream, params, d.c0, d.k, d.bk, d.m, b->wtile); break;
+    case 32: launch(tc2::k_pretile_w1_all<32>, grid, 256, 0, b->stream, params, d.c0, d.k, d.bk, d.m, b->wtile); break;
+    case 48: launch(tc2::k_pretile_w1_all<48>, grid, 256, 0, b->stream, params, d.c0, d.k, d.bk, d.m, b->wtile); break;
+    case 64: launch(tc2::k_pretile_w1_all<64>, grid, 256, 0, b->stream, params, d.c0, d.k, d.bk, d.m, b->wtile); break;
+    case 128: launch(tc2::k_pretile_w1_all<128>, grid, 256, 0, b->stream, params, d.c0, d.k, d.bk, d.m, b->wtile); break;
+    default: launch(tc2::k_pretile_w1_all<192>, grid, 256, 0, b->stream, params, d.c0, d.k, d.bk, d.m, b->wtile); break;
   }
   b->launches++;
 }
@@ -147,9 +148,9 @@ void tc2_pretile_w1t(Block* b, const float* params) {
   if (!b->w1b) return;
   const dim3 grid(16, d.m);
   if (tc2_bwd_bn(d) == 256)
-    tc2::k_pretile_w1t_all<256><<<grid, 256, 0, b->stream>>>(params, d.c0, d.k, d.bk, b->w1b);
+    launch(tc2::k_pretile_w1t_all<256>, grid, 256, 0, b->stream, params, d.c0, d.k, d.bk, b->w1b);
   else
-    tc2::k_pretile_w1t_all<128><<<grid, 256, 0, b->stream>>>(params, d.c0, d.k, d.bk, b->w1b);
+    launch(tc2::k_pretile_w1t_all<128>, grid, 256, 0, b->stream, params, d.c0, d.k, d.bk, b->w1b);
   b->launches++;
 }
 

@@ -76,43 +76,8 @@ __device__ __forceinline__ void raw_write8(uint8_t* box, int row, int ch, const 
   *reinterpret_cast<float4*>(box + row * 128 + (((c4 + 1) ^ (row & 7)) << 4)) = make_float4(v[4], v[5], v[6], v[7]);
 }
 
-// Warp reduction of 8 columns x 32 rows in 9 shuffles (transpose-reduce): on
-// return lane L holds the full column sum of column (L >> 2) & 7 in v[0].
-__device__ __forceinline__ float warp_colsum8(float (&v)[8], int lane) {
-  // step 1: exchange halves of the 8 values with lane ^ 16
-  {
-    const bool up = lane & 16;
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      const float send = up ? v[i] : v[i + 4];
-      const float recv = __shfl_xor_sync(0xffffffffu, send, 16);
-      v[i] = (up ? v[i + 4] : v[i]) + recv;
-    }
-  }
-  // lanes with bit 4 set now hold columns 4..7 in v[0..3], others 0..3
-  {
-    const bool up = lane & 8;
-#pragma unroll
-    for (int i = 0; i < 2; ++i) {
-      const float send = up ? v[i] : v[i + 2];
-      const float recv = __shfl_xor_sync(0xffffffffu, send, 8);
-      v[i] = (up ? v[i + 2] : v[i]) + recv;
-    }
-  }
-  {
-    const bool up = lane & 4;
-    const float send = up ? v[0] : v[1];
-    const float recv = __shfl_xor_sync(0xffffffffu, send, 4);
-    v[0] = (up ? v[1] : v[0]) + recv;
-  }
-  v[0] += __shfl_xor_sync(0xffffffffu, v[0], 2);
-  v[0] += __shfl_xor_sync(0xffffffffu, v[0], 1);
-  // column held by this lane: bit4 -> +4, bit3 -> +2, bit2 -> +1
-  return v[0];
-}
-__device__ __forceinline__ int colsum8_column(int lane) {
-  return ((lane >> 4) & 1) * 4 + ((lane >> 3) & 1) * 2 + ((lane >> 2) & 1);
-}
+using tc::colsum8_column;
+using tc::warp_colsum8;
 
 // Debug-only phase clocks (dpb_debug_tc2_clocks): when g_tc2_dbg_c equals the
 // launch's layer width a.c, CTA x (< 148, column tile 0) stamps clock64() at
@@ -195,6 +160,7 @@ __global__ void __launch_bounds__(Roles<Op>::kThreads, 1) tc2_kernel(const __gri
     tc::fence_barrier_init();
   }
   if (warp == kMmaWarp) tc::tmem_alloc<2 * TC>(&tmem_base);
+  pdl_enter();  // barrier init / TMEM alloc above overlap the predecessor
   op.prologue(aux);
   tc::fence_proxy_async();  // resident operand images written by generic stores
   tc::tc_fence_before();
@@ -762,6 +728,7 @@ struct Wgrad1x1 {
 template <int BN>
 __global__ void k_pretile_w1t_all(const float* __restrict__ params, int c0, int k, int bk,
                                   uint8_t* __restrict__ out) {
+  pdl_enter();
   const int l = blockIdx.y;
   const int nkb = bwd_nkb(bk);
   int64_t poff = 0, toff = 0;
@@ -796,6 +763,7 @@ __global__ void k_pretile_w1t_all(const float* __restrict__ params, int c0, int 
 template <int BN>
 __global__ void k_pretile_w1_all(const float* __restrict__ params, int c0, int k, int bk, int m,
                                  uint8_t* __restrict__ out) {
+  pdl_enter();
   const int l = blockIdx.y;
   int64_t poff = 0, toff = 0;
   for (int j = 0; j < l; ++j) {

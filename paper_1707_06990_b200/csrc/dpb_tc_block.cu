@@ -6,6 +6,7 @@
 #include <algorithm>
 
 #include "dpb_internal.h"
+#include "dpb_launch.h"
 #include "dpb_tc_halo.cuh"
 #include "dpb_tc_ops.cuh"
 
@@ -21,7 +22,7 @@ bool tc_supported(const dpb_block_desc& d) {
 }
 
 template <class Op>
-static void launch(Block* b, const Op& op, dim3 grid, size_t aux) {
+static void launch_tc(Block* b, const Op& op, dim3 grid, size_t aux) {
   static int max_dyn = -1;
   if (max_dyn < 0) {
     // opt in to the full 227 KB minus the kernel's static shared memory
@@ -32,7 +33,7 @@ static void launch(Block* b, const Op& op, dim3 grid, size_t aux) {
                          max_dyn);
   }
   const size_t smem = tc::stage_bytes<Op>() + aux;
-  tc::tc_gemm_kernel<Op><<<grid, tc::kThreads, smem, b->stream>>>(op);
+  launch(tc::tc_gemm_kernel<Op>, grid, tc::kThreads, smem, b->stream, op);
 }
 
 // N tile for an N of `n` channels from the instantiated set.
@@ -50,23 +51,23 @@ static int pick_bn(int n) {
 template <template <int> class Op>
 static void launch_bn(Block* b, int bn, const TcArgs& t, dim3 grid, size_t aux) {
   switch (bn) {
-    case 16: launch(b, Op<16>{t}, grid, aux); break;
-    case 32: launch(b, Op<32>{t}, grid, aux); break;
-    case 48: launch(b, Op<48>{t}, grid, aux); break;
-    case 64: launch(b, Op<64>{t}, grid, aux); break;
-    case 128: launch(b, Op<128>{t}, grid, aux); break;
-    case 192: launch(b, Op<192>{t}, grid, aux); break;
-    default: launch(b, Op<256>{t}, grid, aux); break;
+    case 16: launch_tc(b, Op<16>{t}, grid, aux); break;
+    case 32: launch_tc(b, Op<32>{t}, grid, aux); break;
+    case 48: launch_tc(b, Op<48>{t}, grid, aux); break;
+    case 64: launch_tc(b, Op<64>{t}, grid, aux); break;
+    case 128: launch_tc(b, Op<128>{t}, grid, aux); break;
+    case 192: launch_tc(b, Op<192>{t}, grid, aux); break;
+    default: launch_tc(b, Op<256>{t}, grid, aux); break;
   }
 }
 
 template <template <int> class Op>
 static void launch_small(Block* b, int bn, const TcArgs& t, dim3 grid, size_t aux) {
   switch (bn) {
-    case 16: launch(b, Op<16>{t}, grid, aux); break;
-    case 32: launch(b, Op<32>{t}, grid, aux); break;
-    case 48: launch(b, Op<48>{t}, grid, aux); break;
-    default: launch(b, Op<64>{t}, grid, aux); break;
+    case 16: launch_tc(b, Op<16>{t}, grid, aux); break;
+    case 32: launch_tc(b, Op<32>{t}, grid, aux); break;
+    case 48: launch_tc(b, Op<48>{t}, grid, aux); break;
+    default: launch_tc(b, Op<64>{t}, grid, aux); break;
   }
 }
 
@@ -96,7 +97,7 @@ static void launch_halo(Block* b, const Op& op, dim3 grid, size_t stage, int nst
     cudaFuncSetAttribute(tc::tc_halo_kernel<Op>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          max_dyn);
   }
-  tc::tc_halo_kernel<Op><<<grid, tc::kThreads, stage * nst + aux, b->stream>>>(op);
+  launch(tc::tc_halo_kernel<Op>, grid, tc::kThreads, stage * nst + aux, b->stream, op);
 }
 
 static tc::HaloArgs halo_args(const LayerArgs<float>& a, int kc) {
@@ -127,6 +128,9 @@ HaloPlan tc_halo_plan(const dpb_block_desc& d) {
       p.fwd_bn = bn;
       p.fwd_kc = kc;
       p.fwd_layer_bytes = static_cast<int64_t>(nkb) * 2 * (9LL * bn * kc * 2);
+      // all taps as GEMM columns: N = 9k <= 128 (two 128-column accumulators),
+      // 4-column TMEM loads per tap, both 128-row M blocks inside the halo
+      p.fwd_taps = bn == 16 && d.k % 4 == 0 && 9 * d.k <= 128 && g.R <= 2 * tc::kBM;
       break;
     }
   }
@@ -146,24 +150,29 @@ void tc_pretile_w2(Block* b, const float* params, bool fwd) {
   const dpb_block_desc& d = b->d;
   const HaloPlan& p = b->halo;
   const dim3 grid(8, d.m);
-  if (fwd && p.fwd_ok && b->w2f) {
+  if (fwd && p.fwd_ok && b->w2f && p.fwd_taps) {
+    const int np = (9 * d.k + 15) / 16 * 16;
+    launch(tc::k_pretile_w2_taps, grid, 256, 0, b->stream, params, d.c0, d.k, d.bk, p.fwd_kc, np,
+                                                        p.fwd_layer_bytes, b->w2f);
+    b->launches++;
+  } else if (fwd && p.fwd_ok && b->w2f) {
     switch (p.fwd_bn) {
-      case 16: tc::k_pretile_w2_fwd<16><<<grid, 256, 0, b->stream>>>(params, d.c0, d.k, d.bk, p.fwd_kc, b->w2f); break;
-      case 32: tc::k_pretile_w2_fwd<32><<<grid, 256, 0, b->stream>>>(params, d.c0, d.k, d.bk, p.fwd_kc, b->w2f); break;
-      case 48: tc::k_pretile_w2_fwd<48><<<grid, 256, 0, b->stream>>>(params, d.c0, d.k, d.bk, p.fwd_kc, b->w2f); break;
-      default: tc::k_pretile_w2_fwd<64><<<grid, 256, 0, b->stream>>>(params, d.c0, d.k, d.bk, p.fwd_kc, b->w2f); break;
+      case 16: launch(tc::k_pretile_w2_fwd<16>, grid, 256, 0, b->stream, params, d.c0, d.k, d.bk, p.fwd_kc, b->w2f); break;
+      case 32: launch(tc::k_pretile_w2_fwd<32>, grid, 256, 0, b->stream, params, d.c0, d.k, d.bk, p.fwd_kc, b->w2f); break;
+      case 48: launch(tc::k_pretile_w2_fwd<48>, grid, 256, 0, b->stream, params, d.c0, d.k, d.bk, p.fwd_kc, b->w2f); break;
+      default: launch(tc::k_pretile_w2_fwd<64>, grid, 256, 0, b->stream, params, d.c0, d.k, d.bk, p.fwd_kc, b->w2f); break;
     }
     b->launches++;
   }
   if (!fwd && p.bwd_ok && b->w2b) {
     switch (p.bwd_bn) {
-      case 16: tc::k_pretile_w2_bwd<16><<<grid, 256, 0, b->stream>>>(params, d.c0, d.k, d.bk, p.bwd_kc, b->w2b); break;
-      case 32: tc::k_pretile_w2_bwd<32><<<grid, 256, 0, b->stream>>>(params, d.c0, d.k, d.bk, p.bwd_kc, b->w2b); break;
-      case 48: tc::k_pretile_w2_bwd<48><<<grid, 256, 0, b->stream>>>(params, d.c0, d.k, d.bk, p.bwd_kc, b->w2b); break;
-      case 64: tc::k_pretile_w2_bwd<64><<<grid, 256, 0, b->stream>>>(params, d.c0, d.k, d.bk, p.bwd_kc, b->w2b); break;
-      case 128: tc::k_pretile_w2_bwd<128><<<grid, 256, 0, b->stream>>>(params, d.c0, d.k, d.bk, p.bwd_kc, b->w2b); break;
-      case 192: tc::k_pretile_w2_bwd<192><<<grid, 256, 0, b->stream>>>(params, d.c0, d.k, d.bk, p.bwd_kc, b->w2b); break;
-      default: tc::k_pretile_w2_bwd<256><<<grid, 256, 0, b->stream>>>(params, d.c0, d.k, d.bk, p.bwd_kc, b->w2b); break;
+      case 16: launch(tc::k_pretile_w2_bwd<16>, grid, 256, 0, b->stream, params, d.c0, d.k, d.bk, p.bwd_kc, b->w2b); break;
+      case 32: launch(tc::k_pretile_w2_bwd<32>, grid, 256, 0, b->stream, params, d.c0, d.k, d.bk, p.bwd_kc, b->w2b); break;
+      case 48: launch(tc::k_pretile_w2_bwd<48>, grid, 256, 0, b->stream, params, d.c0, d.k, d.bk, p.bwd_kc, b->w2b); break;
+      case 64: launch(tc::k_pretile_w2_bwd<64>, grid, 256, 0, b->stream, params, d.c0, d.k, d.bk, p.bwd_kc, b->w2b); break;
+      case 128: launch(tc::k_pretile_w2_bwd<128>, grid, 256, 0, b->stream, params, d.c0, d.k, d.bk, p.bwd_kc, b->w2b); break;
+      case 192: launch(tc::k_pretile_w2_bwd<192>, grid, 256, 0, b->stream, params, d.c0, d.k, d.bk, p.bwd_kc, b->w2b); break;
+      default: launch(tc::k_pretile_w2_bwd<256>, grid, 256, 0, b->stream, params, d.c0, d.k, d.bk, p.bwd_kc, b->w2b); break;
     }
     b->launches++;
   }
@@ -179,6 +188,16 @@ int tc_conv3x3_fwd(Block* b, const LayerArgs<float>& a, int l) {
     const size_t stage = 2ull * (static_cast<size_t>(h.g.R) * kc * 2 + 9ull * bn * kc * 2);
     const int nst = (a.bk + kc - 1) / kc > 1 ? 2 : 1;
     const size_t aux = sizeof(BnFwd) * a.bk;
+    if (b->halo.fwd_taps) {
+      const dim3 grid(static_cast<unsigned>(nimg(a) * h.g.tpi));
+      const size_t np = (9 * a.k + 15) / 16 * 16;
+      const size_t tstage = 2ull * (static_cast<size_t>(h.g.R) * kc * 2 + np * kc * 2);
+      // the epilogue's per-tap output slices [9][128][k] fp32 reuse the stages
+      const size_t ytap = 9ull * tc::kBM * a.k * 4;
+      const size_t taux = std::max(aux, ytap > tstage * nst ? ytap - tstage * nst : size_t{0});
+      launch_halo(b, tc::Tc3x3FwdTaps{h}, grid, tstage, nst, taux);
+      return static_cast<int>(grid.x);
+    }
     {
       const dim3 grid(static_cast<unsigned>(nimg(a) * h.g.tpi));
       switch (bn) {
@@ -244,8 +263,8 @@ void tc_conv1x1_dgrad(Block* b, const LayerArgs<float>& a) {
   const int bn = a.c <= 64 ? 64 : 128;
   const size_t aux = (sizeof(BnBwd) * a.bk + 15) / 16 * 16 + sizeof(BnFwd) * bn;
   const dim3 grid(mtiles(a.M), static_cast<unsigned>((a.c + bn - 1) / bn));
-  if (bn == 64) launch(b, tc::Tc1x1Dgrad<64>{t}, grid, aux);
-  else launch(b, tc::Tc1x1Dgrad<128>{t}, grid, aux);
+  if (bn == 64) launch_tc(b, tc::Tc1x1Dgrad<64>{t}, grid, aux);
+  else launch_tc(b, tc::Tc1x1Dgrad<128>{t}, grid, aux);
 }
 
 // Split-K over pixels for the weight gradients: ~2 waves of 148 SMs, chunks

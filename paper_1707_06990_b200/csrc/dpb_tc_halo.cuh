@@ -101,6 +101,7 @@ __global__ void __launch_bounds__(kThreads, 2) tc_halo_kernel(const Op op) {
     mbar_init(&bbar[1], 1);
     fence_barrier_init();
   }
+  pdl_enter();  // barrier init / TMEM alloc above overlap the predecessor
   op.prologue(aux);
   tc_fence_before();
   __syncthreads();
@@ -139,10 +140,63 @@ __global__ void __launch_bounds__(kThreads, 2) tc_halo_kernel(const Op op) {
 
   const int quarter = warp & 3, half = warp >> 2;
   const int row = quarter * 32 + lane;
-  constexpr int kOutCols = Op::kTmemCols / Op::kAccCopies;  // summed accumulator copies
+  float* ytap = reinterpret_cast<float*>(smem);  // kTapCols: [9][128][k], over the dead stages
+  if constexpr (Op::kTapCols) {
+    // all taps in one GEMM: D[r][tap*k + o] over halo rows r (M blocks of 128);
+    // y[p] = sum_tap D[p + off_tap][tap*k + o].  Each tap's rows land in their
+    // own slice (a bijection r -> p, no write conflicts, no barriers between
+    // taps); the output pass sums the slices in tap order (deterministic).
+    const int mb = warp >> 2;  // M block of this warp (TMEM lanes = its quarter)
+    const int r = mb * kBM + row;
+    const int k = op.tap_k();
+    const uint32_t lane_base = tmem + (static_cast<uint32_t>(quarter * 32) << 16) + mb * kBM;
+#pragma unroll 1
+    for (int t0 = 0; t0 < 9; t0 += 3) {
+      uint32_t u[3][4][4];
+#pragma unroll
+      for (int t = 0; t < 3; ++t)
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+          if (4 * i < k) tmem_ld4_nowait(lane_base + op.tap_col(t0 + t) + 4 * i, u[t][i]);
+      tmem_wait_ld();
+#pragma unroll
+      for (int t = 0; t < 3; ++t) {
+        const int p = r - op.tap_off(t0 + t);
+        if (p >= 0 && p < kBM && r < op.rows()) {
+          float* dst = ytap + ((t0 + t) * kBM + p) * k;
+#pragma unroll
+          for (int i = 0; i < 4; ++i)
+            if (4 * i < k)
+              reinterpret_cast<float4*>(dst)[i] =
+                  make_float4(__uint_as_float(u[t][i][0]), __uint_as_float(u[t][i][1]),
+                              __uint_as_float(u[t][i][2]), __uint_as_float(u[t][i][3]));
+        }
+      }
+    }
+    __syncthreads();
+  }
+  constexpr int kOutCols = Op::kTapCols ? BN : Op::kTmemCols / Op::kAccCopies;  // summed copies
   for (int cc = half; cc < kOutCols / 8; cc += 2) {
     float v[8];
-    if (nkb > 0) {
+    if constexpr (Op::kTapCols) {
+      // 16-byte reads (row stride k floats, k % 4 == 0: conflict-free phases)
+      const int k = op.tap_k();
+#pragma unroll
+      for (int i = 0; i < 8; ++i) v[i] = 0.f;
+#pragma unroll
+      for (int h4 = 0; h4 < 2; ++h4) {
+        if (cc * 8 + 4 * h4 < k) {
+#pragma unroll
+          for (int tap = 0; tap < 9; ++tap) {
+            const float4 q = *reinterpret_cast<const float4*>(ytap + (tap * kBM + row) * k + cc * 8 + 4 * h4);
+            v[4 * h4 + 0] += q.x;
+            v[4 * h4 + 1] += q.y;
+            v[4 * h4 + 2] += q.z;
+            v[4 * h4 + 3] += q.w;
+          }
+        }
+      }
+    } else if (nkb > 0) {
       tmem_ld8(tmem + (static_cast<uint32_t>(quarter * 32) << 16) + cc * 8, v);
 #pragma unroll
       for (int c2 = 1; c2 < Op::kAccCopies; ++c2) {
@@ -157,18 +211,12 @@ __global__ void __launch_bounds__(kThreads, 2) tc_halo_kernel(const Op op) {
     float s1[8], s2[8];
     op.epilogue(row, cc * 8, v, aux, s1, s2);
     if constexpr (Op::kColSums) {
-#pragma unroll
-      for (int i = 0; i < 8; ++i) {
-        float a = s1[i], b = s2[i];
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
-          a += __shfl_xor_sync(0xffffffffu, a, o);
-          b += __shfl_xor_sync(0xffffffffu, b, o);
-        }
-        if (lane == 0) {
-          red[0][quarter][cc * 8 + i] = a;
-          red[1][quarter][cc * 8 + i] = b;
-        }
+      const float x = warp_colsum8(s1, lane);
+      const float y = warp_colsum8(s2, lane);
+      if ((lane & 3) == 0) {
+        const int col = cc * 8 + colsum8_column(lane);
+        red[0][quarter][col] = x;
+        red[1][quarter][col] = y;
       }
     }
   }
@@ -208,6 +256,7 @@ __device__ __forceinline__ void copy_image(uint8_t* dst, const uint8_t* src, int
 template <int BN>
 __global__ void k_pretile_w2_fwd(const float* __restrict__ params, int c0, int k, int bk, int kc,
                                  uint8_t* __restrict__ out) {
+  pdl_enter();
   const int l = blockIdx.y;
   int64_t poff = 0;
   for (int j = 0; j < l; ++j) {
@@ -243,6 +292,7 @@ __global__ void k_pretile_w2_fwd(const float* __restrict__ params, int c0, int k
 template <int BN>
 __global__ void k_pretile_w2_bwd(const float* __restrict__ params, int c0, int k, int bk, int kc,
                                  uint8_t* __restrict__ out) {
+  pdl_enter();
   const int l = blockIdx.y;
   int64_t poff = 0;
   for (int j = 0; j < l; ++j) {
@@ -272,11 +322,15 @@ __global__ void k_pretile_w2_bwd(const float* __restrict__ params, int c0, int k
 template <int BN_>
 struct Tc3x3FwdHalo {
   static constexpr int BN = BN_;
-  static constexpr int kIssuers = 3, kAccCopies = 3;  // taps t = warp, warp+3, warp+6
+  // (tap, k16) pairs are dealt round-robin to kIssuers warps, each issuing into
+  // its own accumulator copy (summed by the epilogue): eight issuers while the
+  // copies fit two CTAs' TMEM, else three
+  static constexpr int kIssuers = BN <= 32 ? 8 : 3, kAccCopies = kIssuers;
   static constexpr int kTmemCols = BN * kAccCopies;
+  static constexpr bool kTapCols = false;
   static constexpr bool kColSums = true;
   static constexpr bool kBulk = true;
-  static constexpr int kMaxChunks = 4;
+  static constexpr int kMaxChunks = 5;  // W=32 halos (1188 chunks) in one load batch
   HaloArgs h;
   __device__ uint32_t halo_bytes() const { return static_cast<uint32_t>(h.g.R * h.kc * 2); }
   __device__ uint32_t b_bytes() const { return static_cast<uint32_t>(9 * BN * h.kc * 2); }
@@ -340,21 +394,16 @@ struct Tc3x3FwdHalo {
     const uint32_t wh = sdesc_lo(st + 2 * halo_bytes(), WB);
     const uint32_t wl = sdesc_lo(st + 2 * halo_bytes() + b_bytes(), WB);
     const uint32_t hi = sdesc_hi(128);
-    const int nk16 = h.kc / 16;
-#pragma unroll
-    for (int ti = 0; ti < 3; ++ti) {
-      const int tap = part + 3 * ti;
+    const int nk16 = h.kc / 16;  // 9 * nk16 >= 9 pairs: every copy gets at least one
+    for (int q = part; q < 9 * nk16; q += kIssuers) {
+      const int tap = q / nk16, k16 = q - tap * nk16;
       const uint32_t aoff = static_cast<uint32_t>(h.g.fwd_off(tap));  // 16-byte units
       const uint32_t boff = static_cast<uint32_t>(tap * BN);
-#pragma unroll
-      for (int k16 = 0; k16 < 4; ++k16) {
-        if (k16 >= nk16) break;
-        const uint32_t da = aoff + k16 * 2 * (RB >> 4), db = boff + k16 * 2 * (WB >> 4);
-        const uint32_t acc = (kb | ti | k16) ? 1u : 0u;
-        mma_bf16_lh(tmem, xh + da, hi, wh + db, hi, idesc, acc);
-        mma_bf16_lh(tmem, xh + da, hi, wl + db, hi, idesc, 1u);
-        mma_bf16_lh(tmem, xl + da, hi, wh + db, hi, idesc, 1u);
-      }
+      const uint32_t da = aoff + k16 * 2 * (RB >> 4), db = boff + k16 * 2 * (WB >> 4);
+      const uint32_t acc = (kb > 0 || q != part) ? 1u : 0u;
+      mma_bf16_lh(tmem, xh + da, hi, wh + db, hi, idesc, acc);
+      mma_bf16_lh(tmem, xh + da, hi, wl + db, hi, idesc, 1u);
+      mma_bf16_lh(tmem, xl + da, hi, wh + db, hi, idesc, 1u);
     }
   }
   __device__ void epilogue(int row, int col0, const float (&v)[8], const uint8_t*, float (&s1)[8],
@@ -386,6 +435,83 @@ struct Tc3x3FwdHalo {
   }
 };
 
+// Forward with all 9 taps as GEMM columns (k <= 14, k % 4 == 0): B = W2 rows
+// tap*k + o (N = 9k padded to 16), A = the whole halo as two M blocks of 128
+// rows with no tap shift, so each MMA reads the halo once instead of once per
+// tap (the narrow per-tap MMAs are bound by shared-memory operand reads).  The
+// engine adds the tap columns at row offsets (kTapCols epilogue).  Produce and
+// output epilogue are those of Tc3x3FwdHalo.
+struct Tc3x3FwdTaps : Tc3x3FwdHalo<16> {
+  static constexpr int kIssuers = 2, kAccCopies = 1;  // one issuer per M block
+  static constexpr int kTmemCols = 2 * kBM;           // M block b at columns [128 b, 128 b + N)
+  static constexpr bool kTapCols = true;
+  __device__ int np() const { return (9 * h.a.k + 15) / 16 * 16; }
+  __device__ uint32_t b_bytes() const { return static_cast<uint32_t>(np() * h.kc * 2); }
+  __device__ uint32_t stage_bytes() const { return 2 * (halo_bytes() + b_bytes()); }
+  __device__ int tap_k() const { return h.a.k; }
+  __device__ int tap_col(int tap) const { return tap * h.a.k; }
+  __device__ int tap_off(int tap) const { return h.g.fwd_off(tap); }
+  __device__ int rows() const { return h.g.R; }
+  __device__ void bulk(uint32_t st, int kb, uint64_t* bar) const {
+    mbar_expect_tx(bar, 2 * b_bytes());
+    bulk_load(st + 2 * halo_bytes(), h.wt + static_cast<int64_t>(kb) * 2 * b_bytes(), 2 * b_bytes(), bar);
+  }
+  __device__ void issue(uint32_t st, int kb, uint32_t tmem_base, int part) const {
+    const uint32_t idesc = make_idesc(np(), 0, 0);
+    const uint32_t tmem = tmem_base + part * kBM;
+    const uint32_t RB = static_cast<uint32_t>(h.g.R) * 16, WB = static_cast<uint32_t>(np()) * 16;
+    const uint32_t xh = sdesc_lo(st, RB), xl = sdesc_lo(st + halo_bytes(), RB);
+    const uint32_t wh = sdesc_lo(st + 2 * halo_bytes(), WB);
+    const uint32_t wl = sdesc_lo(st + 2 * halo_bytes() + b_bytes(), WB);
+    const uint32_t hi = sdesc_hi(128);
+    const int nk16 = h.kc / 16;
+    for (int k16 = 0; k16 < nk16; ++k16) {
+      // rows are 16 bytes apart in the core-matrix layout: M block b starts 128 b rows in
+      const uint32_t da = part * kBM + k16 * 2 * (RB >> 4), db = k16 * 2 * (WB >> 4);
+      const uint32_t acc = (kb | k16) ? 1u : 0u;
+      mma_bf16_lh(tmem, xh + da, hi, wh + db, hi, idesc, acc);
+      mma_bf16_lh(tmem, xh + da, hi, wl + db, hi, idesc, 1u);
+      mma_bf16_lh(tmem, xl + da, hi, wh + db, hi, idesc, 1u);
+    }
+  }
+};
+
+// W2 for Tc3x3FwdTaps: per K chunk, rows tap*k + o (np rows, zero past 9k),
+// K-major, hi plane then lo plane; layer stride `layer_bytes`.
+__global__ void k_pretile_w2_taps(const float* __restrict__ params, int c0, int k, int bk, int kc,
+                                  int np, int64_t layer_bytes, uint8_t* __restrict__ out) {
+  pdl_enter();
+  const int l = blockIdx.y;
+  int64_t poff = 0;
+  for (int j = 0; j < l; ++j) {
+    const int cj = c0 + j * k;
+    poff += 2LL * cj + static_cast<int64_t>(bk) * cj + 2LL * bk + 9LL * k * bk;
+  }
+  const int c = c0 + l * k;
+  const float* w2 = params + poff + 2 * c + static_cast<int64_t>(bk) * c + 2 * bk;
+  const int nkb = (bk + kc - 1) / kc;
+  const int plane = np * kc * 2;
+  uint8_t* o_l = out + static_cast<int64_t>(l) * layer_bytes;
+  const int kcn = kc / 8;
+  const int per = np * kcn;
+  for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < nkb * per; q += gridDim.x * blockDim.x) {
+    const int kb = q / per, qq = q - kb * per;
+    const int row = qq / kcn, kk = (qq % kcn) * 8;
+    const int tap = row / k, o = row - tap * k;
+    const int j0 = kb * kc + kk;
+    float v[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+      v[i] = (row < 9 * k && j0 + i < bk) ? w2[(static_cast<int64_t>(o) * bk + j0 + i) * 9 + tap] : 0.f;
+    uint4 hh, lo;
+    split8(v, hh, lo);
+    uint8_t* t = o_l + static_cast<int64_t>(kb) * 2 * plane;
+    const uint32_t off = halo_kmajor(np, row, kk);
+    *reinterpret_cast<uint4*>(t + off) = hh;
+    *reinterpret_cast<uint4*>(t + plane + off) = lo;
+  }
+}
+
 // ---- backward data --------------------------------------------------------------------
 // t0[pos][j] = relu'(act_b) * sum_tap sum_o dY[pos - d][o] W2[o][j][tap]; K per
 // tap = kc (k padded to 16); the stage holds the dY halo and W2^T for 9 taps.
@@ -393,6 +519,7 @@ template <int BN_>
 struct Tc3x3DgradHalo {
   static constexpr int BN = BN_;
   static constexpr int kIssuers = BN <= 64 ? 3 : 1, kAccCopies = kIssuers;
+  static constexpr bool kTapCols = false;
   static constexpr int kTmemCols = BN * kAccCopies;
   static constexpr bool kColSums = true;
   static constexpr bool kBulk = true;
@@ -508,6 +635,7 @@ template <int BN_>
 struct Tc3x3WgradHalo {
   static constexpr int BN = BN_;
   static constexpr int kIssuers = 3, kAccCopies = 1;  // taps t = warp, warp+3, warp+6
+  static constexpr bool kTapCols = false;
   static constexpr int kTmemCols = 9 * BN;
   static constexpr bool kColSums = false;
   static constexpr bool kBulk = false;
