@@ -14,6 +14,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <type_traits>
 #include <new>
 #include <string>
 
@@ -498,9 +499,17 @@ static void backward_impl(Block* b, const float* params, float* grad_acc, float*
     }
     {
       LaunchScope ls(b, KC_BN_APPLY_ACC, M * a.c * (4.0 + Sb + 8.0), 0);
-      launch(k_bn_apply_accumulate<S>, blocks_for(g.M * a.c, 256), 256, 0, b->stream, 
-          g.M, a.c, static_cast<int>(g.C), static_cast<const S*>(b->feat), b->g1, a.amean,
-          a.avar, a.gamma_a, b->bna_bwd, b->acc_cur);
+      const bool quads = std::is_same<S, float>::value && a.c % 4 == 0 && g.C % 4 == 0 &&
+                         (reinterpret_cast<uintptr_t>(b->acc_cur) & 15) == 0;
+      if (quads)
+        launch(k_bn_apply_accumulate4,
+               blocks_for((g.M + kApplyRows - 1) / kApplyRows * (a.c / 4), 256), 256, 0, b->stream,
+               g.M, a.c, static_cast<int>(g.C), static_cast<const float*>(b->feat), b->g1, a.amean,
+               a.avar, a.gamma_a, b->bna_bwd, b->acc_cur);
+      else
+        launch(k_bn_apply_accumulate<S>, blocks_for(g.M * a.c, 256), 256, 0, b->stream,
+               g.M, a.c, static_cast<int>(g.C), static_cast<const S*>(b->feat), b->g1, a.amean,
+               a.avar, a.gamma_a, b->bna_bwd, b->acc_cur);
     }
   }
   if (fork) {  // join: the caller's stream sees every weight gradient
