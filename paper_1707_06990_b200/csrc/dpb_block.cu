@@ -45,6 +45,7 @@ static cudaEvent_t next_event(Block* b) {
 
 LaunchScope::LaunchScope(Block* blk, int cat_, double bytes, double flops) : b(blk), cat(cat_) {
   b->launches++;
+  current_cat() = cat_;
   if (!b->prof) return;
   ProfRec r{cat_, next_event(b), next_event(b), bytes, flops};
   cudaEventRecord(r.start, b->stream);
@@ -53,6 +54,7 @@ LaunchScope::LaunchScope(Block* blk, int cat_, double bytes, double flops) : b(b
 }
 
 LaunchScope::~LaunchScope() {
+  current_cat() = -1;
   if (idx >= 0) cudaEventRecord(b->recs[idx].stop, b->stream);
   // debugging aid: DPB_DEBUG_SYNC=1 synchronizes after every launch and names
   // the first launch that faults (category, launch ordinal)

@@ -107,6 +107,7 @@ __device__ __forceinline__ double2 fold_partials(const double2* part, int P, int
                                                  int ch) {
   const int lane = threadIdx.x % 32;
   double a = 0.0, b = 0.0;
+#pragma unroll 8
   for (int p = lane; p < P; p += 32) {
     const double2 v = part[static_cast<int64_t>(p) * nch + ch];
     a += v.x;
@@ -238,8 +239,10 @@ __device__ __forceinline__ void fold_splits(const float* __restrict__ wpart, int
   __shared__ float red[8][33];
   const int64_t e = static_cast<int64_t>(blockIdx.x) * 32 + threadIdx.x;
   float s = 0.f;
-  if (e < n)
+  if (e < n) {
+#pragma unroll 8
     for (int z = threadIdx.y; z < splits; z += 8) s += wpart[static_cast<int64_t>(z) * n + e];
+  }
   red[threadIdx.y][threadIdx.x] = s;
   __syncthreads();
   if (threadIdx.y == 0 && e < n) {

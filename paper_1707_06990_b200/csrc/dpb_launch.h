@@ -11,6 +11,18 @@
 
 namespace dpb {
 
+// Debugging aid for what-if timing: DPB_SKIP_MASK=<bitmask over KernelCat>
+// drops every launch made inside a LaunchScope of those categories (results
+// are wrong; bench timing only).
+inline int& current_cat() {
+  static thread_local int cat = -1;
+  return cat;
+}
+inline int skip_mask() {
+  static const int m = std::getenv("DPB_SKIP_MASK") ? std::atoi(std::getenv("DPB_SKIP_MASK")) : 0;
+  return m;
+}
+
 inline bool pdl_enabled() {
   static const bool on = std::getenv("DPB_NO_PDL") == nullptr;
   return on;
@@ -19,6 +31,7 @@ inline bool pdl_enabled() {
 template <typename... KArgs, typename... Args>
 inline void launch(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t stream,
                    Args&&... args) {
+  if (current_cat() >= 0 && (skip_mask() >> current_cat() & 1)) return;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = grid;
   cfg.blockDim = block;

@@ -19,6 +19,7 @@ from paper_1707_06990_b200._lib import lib  # noqa: E402
 
 c = int(sys.argv[1]) if len(sys.argv) > 1 else 204
 flags = int(sys.argv[2]) if len(sys.argv) > 2 else 0  # A/B: 1 skip g1 stores, 2 skip column sums
+fwd_only = len(sys.argv) > 3 and sys.argv[3] == "fwd"  # stamps of the layer's last forward launch (3x3)
 L = lib()
 f = L.dpb_debug_tc2_clocks
 f.argtypes = [C.c_int, C.c_void_p]
@@ -35,7 +36,8 @@ for _ in range(2):
 torch.cuda.synchronize()
 f(c | (flags << 16), None)
 plan.forward(x, p, run, True)
-plan.backward(p, acc.clone(), grads)
+if not fwd_only:
+    plan.backward(p, acc.clone(), grads)
 torch.cuda.synchronize()
 f(0, None)
 buf = np.zeros((148, 28), dtype=np.int64)
