@@ -316,7 +316,11 @@ def main():
                 c[key] += st[key]
         b["plan"].profile(False)
     prof_total = sum(c["total_ms"] for c in cats.values())
-    dom_name, dom = max(cats.items(), key=lambda kv: kv[1]["total_ms"])
+    # dominant kernel among the categories that move algorithmic HBM bytes
+    # (SURVEY 8(d) model); BN-statistic folds (finalize) carry none and are
+    # reported beside it
+    dom_name, dom = max(((k, v) for k, v in cats.items() if v["bytes"] > 0),
+                        key=lambda kv: kv[1]["total_ms"])
     avg_ms = dom["total_ms"] / dom["launches"]
     bytes_per_launch = dom["bytes"] / dom["launches"]
     flops_per_launch = dom["flops"] / dom["launches"]
@@ -332,6 +336,8 @@ def main():
     roof["traffic"] = committed_traffic(dom_name, args.config, args.dtype)
     roof["kernel"] = dom_name
     roof["kernel_share_of_step"] = dom["total_ms"] / prof_total
+    roof["excluded_zero_byte_kernels"] = {k: round(v["total_ms"] / prof_total, 4)
+                                          for k, v in cats.items() if v["bytes"] <= 0}
     roof["peak_source"] = peak_src
     F_img, B_img = algorithmic_per_image(shapes)
     t_roof = max(F_img / (bf16_peak * 1e12), B_img / (hbm_peak * 1e9))
