@@ -34,6 +34,13 @@ struct BnFwd {
   float mean, scale, beta, inv, gamma;
 };
 
+// Compact forward BN affine of one channel, y = x * scale + shift with
+// scale = gamma*inv, shift = beta - mean*scale: 8 bytes per channel, so the 1x1
+// forward can keep a table of every input channel (c up to ~4k) in shared memory.
+struct BnAff {
+  float scale, shift;
+};
+
 // The ReLU mask of the backward pass, act > 0, evaluated with the
 // reference's exact float expression gamma * (x - mean) * inv + beta
 // (ops.hpp:130, left to right, no contraction) so that, given the same

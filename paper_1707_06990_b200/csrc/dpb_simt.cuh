@@ -162,6 +162,16 @@ __device__ __forceinline__ void fill_bn_fwd(BnFwd* t, int count, int first,
   }
 }
 
+__device__ __forceinline__ void fill_bn_aff(BnAff* t, int count, int first, const float* mean_p,
+                                            const float* var_p, const float* gamma,
+                                            const float* beta) {
+  for (int i = threadIdx.x; i < count; i += blockDim.x) {
+    const int ch = first + i;
+    const float scale = gamma[ch] * bn_inv(var_p[ch]);
+    t[i] = BnAff{scale, fmaf(-mean_p[ch], scale, beta[ch])};
+  }
+}
+
 __device__ __forceinline__ float bn_relu(const BnFwd& b, float x) {
   const float t = fmaf(x - b.mean, b.scale, b.beta);
   return t > 0.f ? t : 0.f;

@@ -111,7 +111,7 @@ bool tc2_conv1x1_fwd(Block* b, const LayerArgs<float>& a, int l) {
   auto go = [&](auto tag) -> bool {
     using Op = decltype(tag);
     const int nkb = (a.c + tc::kBK - 1) / tc::kBK;
-    const size_t aux = sizeof(BnFwd) * a.c + (Op::kMmaReadsRaw ? 0 : nkb * 2 * Op::kBBytes);
+    const size_t aux = sizeof(BnAff) * a.c + (Op::kMmaReadsRaw ? 0 : nkb * 2 * Op::kBBytes);
     if (fixed_smem<Op>() + aux > 220 * 1024) return false;
     Op op{};
     if (!make_map_f32(&op.xmap, a.feat, a.C, a.M, a.C, 32, tc::kBM)) return false;

@@ -370,8 +370,8 @@ struct Fwd1x1 {
     return boxes(kb) * kBox + (RES ? 0 : 2 * kBBytes);
   }
   __device__ uint32_t b_all() const { return static_cast<uint32_t>(num_kb(0) * 2 * kBBytes); }
-  __device__ const BnFwd* bn_table(const uint8_t* aux) const {
-    return reinterpret_cast<const BnFwd*>(aux + (RES ? b_all() : 0));
+  __device__ const BnAff* bn_table(const uint8_t* aux) const {
+    return reinterpret_cast<const BnAff*>(aux + (RES ? b_all() : 0));
   }
   __device__ void prologue(uint8_t* aux) const {
     if (RES) {
@@ -379,7 +379,7 @@ struct Fwd1x1 {
       uint4* dst = reinterpret_cast<uint4*>(aux);
       for (int q = threadIdx.x; q < static_cast<int>(b_all() / 16); q += blockDim.x) dst[q] = __ldg(src + q);
     }
-    fill_bn_fwd(const_cast<BnFwd*>(bn_table(aux)), a.c, 0, a.amean, a.avar, a.gamma_a, a.beta_a);
+    fill_bn_aff(const_cast<BnAff*>(bn_table(aux)), a.c, 0, a.amean, a.avar, a.gamma_a, a.beta_a);
   }
   __device__ void tma(int tile, int kb, uint32_t raw, uint64_t* bar) const {
     tma_load_2d(raw, &xmap, kb * kBK, tile * kBM, bar);
@@ -388,7 +388,7 @@ struct Fwd1x1 {
   }
   __device__ void transform(int, int kb, const uint8_t* raw, uint8_t* op, const uint8_t* aux,
                             int xt) const {
-    const BnFwd* bn = bn_table(aux);
+    const BnAff* bn = bn_table(aux);
     uint8_t* ah = op;
     uint8_t* al = op + kABytes;
     // every chunk of this thread covers the same 8 channels (kmajor_coords):
@@ -400,9 +400,8 @@ struct Fwd1x1 {
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
       if (ch0 + i < a.c) {
-        const BnFwd b = bn[ch0 + i];
-        sc[i] = b.scale;
-        sh[i] = fmaf(-b.mean, b.scale, b.beta);
+        sc[i] = bn[ch0 + i].scale;
+        sh[i] = bn[ch0 + i].shift;
       } else {
         sc[i] = 0.f;  // channels past c contribute zero
         sh[i] = 0.f;

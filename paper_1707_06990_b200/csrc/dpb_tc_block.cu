@@ -83,7 +83,7 @@ static unsigned mtiles(int64_t rows) { return static_cast<unsigned>((rows + tc::
 
 void tc_conv1x1_fwd(Block* b, const LayerArgs<float>& a) {
   const TcArgs t = make_args(a);
-  launch_bn<tc::Tc1x1Fwd>(b, pick_bn(a.bk), t, dim3(mtiles(a.M)), sizeof(BnFwd) * a.c);
+  launch_bn<tc::Tc1x1Fwd>(b, pick_bn(a.bk), t, dim3(mtiles(a.M)), sizeof(BnAff) * a.c);
 }
 
 // ---- 3x3 halo kernels ----------------------------------------------------------

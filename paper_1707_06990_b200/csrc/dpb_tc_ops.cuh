@@ -96,13 +96,13 @@ struct Tc1x1Fwd {
   TcArgs t;
   __device__ int num_kb() const { return (t.a.c + kBK - 1) / kBK; }
   __device__ void prologue(uint8_t* aux) const {
-    fill_bn_fwd(reinterpret_cast<BnFwd*>(aux), t.a.c, 0, t.a.amean, t.a.avar, t.a.gamma_a,
+    fill_bn_aff(reinterpret_cast<BnAff*>(aux), t.a.c, 0, t.a.amean, t.a.avar, t.a.gamma_a,
                 t.a.beta_a);
   }
   __device__ void produce(uint8_t* ah, uint8_t* al, uint8_t* bh, uint8_t* bl, int kb,
                           const uint8_t* aux) const {
     const LayerArgs<float>& a = t.a;
-    const BnFwd* bn = reinterpret_cast<const BnFwd*>(aux);
+    const BnAff* bn = reinterpret_cast<const BnAff*>(aux);
     const int64_t m0 = static_cast<int64_t>(blockIdx.x) * kBM;
 #pragma unroll
     for (int q = threadIdx.x; q < kBM * kBK / 8; q += kThreads) {
@@ -114,7 +114,9 @@ struct Tc1x1Fwd {
       const int nv = a.c - ch0;
       if (p < a.M && nv > 0) {
         load8(a.feat + p * a.C + ch0, nv, t.vec, v);
-        bnrelu8(bn, ch0, nv, v);
+#pragma unroll
+        for (int i = 0; i < 8; ++i)
+          v[i] = i < nv ? fmaxf(fmaf(v[i], bn[ch0 + i].scale, bn[ch0 + i].shift), 0.f) : 0.f;
       } else {
         zero8(v);
       }
