@@ -236,6 +236,44 @@ DPB_API int dpb_predict_peak_elements(int nblocks, const int32_t* blocks, int32_
 /* Rng(seed).normal() x count in the reference's draw order (rng.hpp:36-49) */
 DPB_API int dpb_rng_fill_normal(uint64_t seed, float* host_dst, int64_t count);
 
+/* ---- whole-network training step ----------------------
+ * Replaces GraphPlan<T>::forward + compute_loss + backward
+ * (graph.hpp:731-809, :811-826, :1065-1183) for the CIFAR-type network:
+ *   stem conv3x3 -> [dense block -> transition (BN-ReLU-1x1 conv-2x2 avgpool)]*
+ *   -> dense block -> head (BN-ReLU-global avgpool-linear) -> softmax-xent.
+ * Dense blocks run through dpb_block_* (NHWC arenas); the transition computes
+ * avgpool before its 1x1 conv (the two commute), on a quarter of the pixels.
+ * Parameters and gradients: one flat fp32 buffer in the reference's
+ * registration order (graph.hpp:356-390, :456-600):
+ *   stem.w[c0][in_c][3][3]; per block its dpb_block layout; per transition
+ *   bn.gamma[C] bn.beta[C] conv.w[c_out][C]; head.bn.gamma[C] head.bn.beta[C]
+ *   head.linear.w[classes][C] head.linear.b[classes].
+ * Running statistics in network order: block 0 (its dpb_block layout),
+ * transition 0 mean[C] var[C], block 1, ..., last block, head mean[C] var[C].
+ * Bottleneck networks only. */
+typedef struct dpb_model dpb_model;
+typedef struct dpb_model_desc {
+  int32_t nblocks;      /* 1..8 */
+  int32_t blocks[8];    /* layers per block */
+  int32_t k;            /* growth rate; bottleneck width 4k */
+  double compression;   /* transition theta in (0, 1] */
+  int32_t classes;
+  int32_t c0;           /* stem output channels */
+  int32_t in_c, in_h, in_w;
+  int64_t batch;
+  int32_t dtype;        /* DPB_FP32 | DPB_BF16 (dense blocks) */
+} dpb_model_desc;
+
+DPB_API int dpb_model_sizes(const dpb_model_desc* desc, int64_t* param_elems, int64_t* running_elems);
+DPB_API int dpb_model_create(const dpb_model_desc* desc, int device, void* stream, dpb_model** out);
+DPB_API void dpb_model_destroy(dpb_model* model);
+/* One training step: input NCHW [batch, in_c, in_h, in_w], labels int32
+ * [batch] (device); writes grads (flat, registration order), updates running
+ * statistics (momentum 0.1) and writes the mean loss to *loss (device float). */
+DPB_API int dpb_model_step(dpb_model* model, const float* input, const int32_t* labels,
+                           const float* params, float* running, float* grads, float* loss);
+DPB_API int dpb_model_sync(dpb_model* model);
+
 #ifdef __cplusplus
 }
 #endif

@@ -94,10 +94,31 @@ def kats():
     return d
 
 
+# Whole-network training steps: the reference's own
+# GraphPlan<float>::build parameters, synthetic input Rng(seed+99), labels
+# i % classes, and one step_trace's loss and gradients (registration order).
+MODEL_CASES = {
+    # blocks, k, compression, classes, c0, (n, c, h, w), seed
+    "model_small": ((2, 2, 2), 4, 0.5, 10, 8, (4, 3, 8, 8), 7),
+    "model_bc": ((3, 3, 3), 12, 0.5, 10, 24, (8, 3, 16, 16), 11),
+}
+
+
+def make_model_case(name, blocks, k, comp, classes, c0, in_shape, seed):
+    params, x = O.ref_model_params(blocks, k, 1, comp, classes, c0, in_shape, seed)
+    loss, grads = O.ref_model_grads(blocks, k, 1, comp, classes, c0, in_shape, seed)
+    labels = (np.arange(in_shape[0]) % classes).astype(np.int32)
+    np.savez_compressed(os.path.join(OUT, f"{name}.npz"), blocks=np.array(blocks), k=k, compression=comp,
+                        classes=classes, c0=c0, in_shape=np.array(in_shape), seed=seed, params=params,
+                        x=x, labels=labels, loss=np.float64(loss), grads=grads)
+
+
 def main():
     os.makedirs(OUT, exist_ok=True)
     for name, (s, src, dt) in CASES.items():
         make_case(name, s, src, dt)
+    for name, args in MODEL_CASES.items():
+        make_model_case(name, *args)
     with open(os.path.join(OUT, "kats.json"), "w") as f:
         json.dump(kats(), f, indent=1, sort_keys=True)
     print("wrote", sorted(os.listdir(OUT)))

@@ -92,6 +92,8 @@ def ref_lib(fast: bool = False):
         L.ref_block_params_f32.argtypes = cfg + [C.c_int] * 3 + [_I64, C.c_uint64, C.c_int, _P]
         L.ref_model_step_f32.restype = C.c_int
         L.ref_model_step_f32.argtypes = cfg + [C.c_int] * 3 + [_I64, C.c_uint64, C.c_int, _P, _P, _P]
+        L.ref_model_params_f32.restype = C.c_int
+        L.ref_model_params_f32.argtypes = cfg + [C.c_int] * 3 + [_I64, C.c_uint64, _P, _P]
         L.ref_rng_normal.argtypes = [C.c_uint64, _I64, _P]
         L.ref_rng_u64.argtypes = [C.c_uint64, _I64, _P]
         L.ref_count_parameters.restype = C.c_int64
@@ -326,6 +328,35 @@ def ref_block_params(blocks, k, bottleneck, compression, classes, c0, in_shape, 
     if rc != 0:
         raise RuntimeError(ref_lib().ref_last_error().decode())
     return out
+
+
+def ref_model_params(blocks, k, bottleneck, compression, classes, c0, in_shape, seed):
+    """All parameters of GraphPlan<float>::build in registration order and the
+    reference's synthetic NCHW input (Rng(seed+99).normal())."""
+    args, keep = _cfg_args(blocks, k, bottleneck, compression, classes, c0)
+    n, c, h, w = in_shape
+    count = ref_lib().ref_count_parameters(*args, c)
+    params = np.zeros(count, dtype=np.float32)
+    x = np.zeros((n, c, h, w), dtype=np.float32)
+    rc = ref_lib().ref_model_params_f32(*args, c, h, w, n, seed, _ptr(params), _ptr(x))
+    if rc != 0:
+        raise RuntimeError(ref_lib().ref_last_error().decode())
+    return params, x
+
+
+def ref_model_grads(blocks, k, bottleneck, compression, classes, c0, in_shape, seed):
+    """One GraphPlan<float>::step_trace: (loss, all parameter gradients in
+    registration order).  Labels are i % classes (ref_driver make_labels)."""
+    args, keep = _cfg_args(blocks, k, bottleneck, compression, classes, c0)
+    n, c, h, w = in_shape
+    count = ref_lib().ref_count_parameters(*args, c)
+    grads = np.zeros(count, dtype=np.float32)
+    loss = C.c_double()
+    secs = C.c_double()
+    rc = ref_lib().ref_model_step_f32(*args, c, h, w, n, seed, 1, C.byref(loss), C.byref(secs), _ptr(grads))
+    if rc != 0:
+        raise RuntimeError(ref_lib().ref_last_error().decode())
+    return loss.value, grads
 
 
 def ref_model_step(blocks, k, bottleneck, compression, classes, c0, in_shape, seed,

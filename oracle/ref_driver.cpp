@@ -428,6 +428,33 @@ int ref_block_params_f32(int nblocks, const int* blocks, int k, int bottleneck,
   });
 }
 
+// Every parameter of a freshly built GraphPlan in registration order
+// (stem.w, b*.l*, t*.bn/conv, head.bn, head.linear) and the reference's
+// synthetic input Rng(seed+99).normal() (NCHW).  Either pointer may be null.
+int ref_model_params_f32(int nblocks, const int* blocks, int k, int bottleneck,
+                         double compression, int classes, int c0, int in_c,
+                         int in_h, int in_w, std::int64_t batch,
+                         std::uint64_t seed, float* params, float* input) {
+  return guarded([&] {
+    const DenseNetConfig cfg = model_cfg(nblocks, blocks, k, bottleneck,
+                                         compression, classes, c0);
+    const Shape4 in{batch, in_c, in_h, in_w};
+    if (params != nullptr) {
+      GraphPlan<float> plan =
+          GraphPlan<float>::build(cfg, ExecutionStrategy::SharedAll, in, seed);
+      std::size_t off = 0;
+      for (const auto& p : plan.params()) {
+        to_flat(p.value, params + off);
+        off += static_cast<std::size_t>(p.value.elems());
+      }
+    }
+    if (input != nullptr) {
+      MemoryTracker data_tr;
+      to_flat(make_input<float>(in, seed + 99, data_tr), input);
+    }
+  });
+}
+
 // One reference training step (GraphPlan::step_trace, SharedAll) on the
 // reference's synthetic input Rng(seed+99).normal() / labels i % classes.
 // Writes the loss, the step wall time in seconds, and (when `grads` is not

@@ -41,6 +41,12 @@ class KernelStat(C.Structure):
                 ("bytes", C.c_double), ("flops", C.c_double)]
 
 
+class ModelDesc(C.Structure):
+    _fields_ = [("nblocks", _I32), ("blocks", _I32 * 8), ("k", _I32), ("compression", C.c_double),
+                ("classes", _I32), ("c0", _I32), ("in_c", _I32), ("in_h", _I32), ("in_w", _I32),
+                ("batch", _I64), ("dtype", _I32)]
+
+
 # every symbol the header declares: (name, restype, argtypes)
 SIGNATURES = {
     "dpb_last_error": (C.c_char_p, []),
@@ -73,6 +79,11 @@ SIGNATURES = {
     "dpb_predict_peak_elements": (C.c_int, [C.c_int, _P, _I32, _I32, C.c_double, _I32, _I32, _I32, _I64,
                                             _I32, _I32, _I32, _P]),
     "dpb_rng_fill_normal": (C.c_int, [C.c_uint64, _P, _I64]),
+    "dpb_model_sizes": (C.c_int, [C.POINTER(ModelDesc), C.POINTER(_I64), C.POINTER(_I64)]),
+    "dpb_model_create": (C.c_int, [C.POINTER(ModelDesc), C.c_int, _P, C.POINTER(_P)]),
+    "dpb_model_destroy": (None, [_P]),
+    "dpb_model_step": (C.c_int, [_P, _P, _P, _P, _P, _P, _P]),
+    "dpb_model_sync": (C.c_int, [_P]),
 }
 
 _lib = None

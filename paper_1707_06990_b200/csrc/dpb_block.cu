@@ -526,6 +526,16 @@ static void backward_impl(Block* b, const float* params, float* grad_acc, float*
   }
 }
 
+// Folds shared with the whole-network step (dpb_model.cu).
+void launch_finalize_bn_bwd(cudaStream_t st, const double2* part, int P, int nch, double count,
+                            float* dgamma, float* dbeta, float* coef) {
+  launch(k_finalize_bn_bwd, blocks_for(32LL * nch, 256), 256, 0, st, part, P, nch, count, dgamma, dbeta,
+         coef);
+}
+void launch_fold_splits(cudaStream_t st, const float* wpart, int splits, int64_t n, float* out) {
+  launch(k_reduce_w1, blocks_for(n, 32), dim3(32, 8), 0, st, wpart, splits, 1, static_cast<int>(n), out);
+}
+
 int block_forward(Block* b, const float* x_in, const float* params, float* running,
                   int update_running, int eval) {
   if (b->g.M < 2 && !eval)

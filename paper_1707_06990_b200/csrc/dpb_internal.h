@@ -104,6 +104,9 @@ int read_feats(Block* b, float* dst);
 int read_z(Block* b, float* dst);
 int read_stats(Block* b, float* dst);
 void profile_enable(Block* b, int on);
+void launch_finalize_bn_bwd(cudaStream_t st, const double2* part, int P, int nch, double count,
+                            float* dgamma, float* dbeta, float* coef);
+void launch_fold_splits(cudaStream_t st, const float* wpart, int splits, int64_t n, float* out);
 int profile_read(Block* b, dpb_kernel_stat* out, int max, int* count);
 
 // tensor-core path (dpb_tc_block.cu)

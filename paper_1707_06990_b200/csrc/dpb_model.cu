@@ -1,0 +1,687 @@
+// Whole-network training step around the dense blocks:
+// stem, transitions, head and loss of GraphPlan<T> (dp/graph.hpp:731-826,
+// :1065-1183, ops dp/ops.hpp:392-560), on the GPU.  The dense blocks run
+// through the block path (dpb_block.cu); everything here is small next to
+// them (the transitions' 1x1 convs are ~3% of BC-100's FLOPs), so these
+// kernels are plain fp32 CUDA-core code with fixed-order reductions
+// (deterministic).  Activations are NHWC fp32 like the block arenas.
+//
+// Transition: BN (batch statistics of every feature channel are already in
+// the block's arena, F6) -> ReLU -> 2x2 average pool -> 1x1 conv.  The
+// reference convolves first and pools after (graph.hpp:774-782); both are
+// linear per pixel, so pooling first is the same map on a quarter of the
+// pixels.  Its backward mirrors that: dW from the pooled activations,
+// the pooled-input gradient spread back over each 2x2 window.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdint>
+#include <cstring>
+#include <vector>
+
+#include "dpb_common.cuh"
+#include "dpb_internal.h"
+#include "dpb_launch.h"
+
+struct dpb_model;
+
+namespace dpb {
+namespace {
+
+constexpr float kMomentum = 0.1f;  // ops.hpp batchnorm_forward running update
+
+__device__ __forceinline__ float bn_ref(float x, float mean, float inv, float gamma, float beta) {
+  // the reference's expression gamma * (x - mean) * inv + beta (ops.hpp:130)
+  return __fadd_rn(__fmul_rn(__fmul_rn(gamma, __fsub_rn(x, mean)), inv), beta);
+}
+
+// ---- stem: conv3x3, stride 1, pad 1 (graph.hpp:739-742) ----------------------------
+// in NCHW [N, cin, H, W] -> out NHWC rows of pitch `ld` (channels [0, c0)).
+__global__ void k_stem_fwd(const float* __restrict__ in, int64_t N, int cin, int H, int W,
+                           const float* __restrict__ w, int c0, float* __restrict__ out, int ld) {
+  pdl_enter();
+  const int64_t p = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (p >= N * H * W) return;
+  const int64_t n = p / (static_cast<int64_t>(H) * W);
+  const int rem = static_cast<int>(p - n * H * W);
+  const int y = rem / W, x = rem - (rem / W) * W;
+  for (int o = 0; o < c0; ++o) {
+    float acc = 0.f;
+    for (int ci = 0; ci < cin; ++ci)
+      for (int ky = 0; ky < 3; ++ky) {
+        const int yy = y + ky - 1;
+        if (yy < 0 || yy >= H) continue;
+        for (int kx = 0; kx < 3; ++kx) {
+          const int xx = x + kx - 1;
+          if (xx < 0 || xx >= W) continue;
+          acc += __ldg(w + ((o * cin + ci) * 3 + ky) * 3 + kx) *
+                 __ldg(in + ((n * cin + ci) * H + yy) * W + xx);
+        }
+      }
+    out[p * ld + o] = acc;
+  }
+}
+
+// stem dW partials: split s sums pixels [s*chunk, ...) for every weight
+// (o, ci, ky, kx) -> wpart[s][widx]; g = NHWC rows of pitch ld, channels [0, c0).
+__global__ void k_stem_wgrad(const float* __restrict__ in, int64_t N, int cin, int H, int W,
+                             const float* __restrict__ g, int ld, int c0, int64_t chunk,
+                             float* __restrict__ wpart) {
+  pdl_enter();
+  const int nw = c0 * cin * 9;
+  const int64_t M = N * H * W;
+  const int64_t p0 = static_cast<int64_t>(blockIdx.x) * chunk;
+  const int64_t p1 = p0 + chunk < M ? p0 + chunk : M;
+  for (int wi = threadIdx.x; wi < nw; wi += blockDim.x) {
+    const int kx = wi % 3, ky = (wi / 3) % 3, ci = (wi / 9) % cin, o = wi / (9 * cin);
+    float acc = 0.f;
+    for (int64_t p = p0; p < p1; ++p) {
+      const int64_t n = p / (static_cast<int64_t>(H) * W);
+      const int rem = static_cast<int>(p - n * H * W);
+      const int yy = rem / W + ky - 1, xx = rem % W + kx - 1;
+      if (yy < 0 || yy >= H || xx < 0 || xx >= W) continue;
+      acc += g[p * ld + o] * __ldg(in + ((n * cin + ci) * H + yy) * W + xx);
+    }
+    wpart[static_cast<int64_t>(blockIdx.x) * nw + wi] = acc;
+  }
+}
+
+// ---- transition forward: P = avgpool2x2(relu(bn(feat))) --------------------------------
+// feat NHWC [N*H*W, C] (pitch C), P [N*Ho*Wo, C]; Ho = H/2, Wo = W/2 (floor,
+// ops.hpp:392-402).  bn from the block's batch statistics.
+__global__ void k_trans_pool(const float* __restrict__ feat, int64_t N, int H, int W, int C,
+                             const float* __restrict__ mean, const float* __restrict__ var,
+                             const float* __restrict__ gamma, const float* __restrict__ beta,
+                             float* __restrict__ P) {
+  pdl_enter();
+  const int Ho = H / 2, Wo = W / 2;
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= N * Ho * Wo * C) return;
+  const int c = static_cast<int>(i % C);
+  const int64_t q = i / C;
+  const int64_t n = q / (static_cast<int64_t>(Ho) * Wo);
+  const int r = static_cast<int>(q - n * Ho * Wo);
+  const int oy = r / Wo, ox = r - (r / Wo) * Wo;
+  const float inv = bn_inv(var[c]);
+  float acc = 0.f;
+  for (int ky = 0; ky < 2; ++ky)
+    for (int kx = 0; kx < 2; ++kx) {
+      const int64_t p = (n * H + 2 * oy + ky) * W + 2 * ox + kx;
+      acc += fmaxf(bn_ref(feat[p * C + c], mean[c], inv, gamma[c], beta[c]), 0.f);
+    }
+  P[i] = acc * 0.25f;
+}
+
+// running statistics momentum update from a block's batch statistics (biased var)
+__global__ void k_running(int C, const float* __restrict__ mean, const float* __restrict__ var,
+                          float* __restrict__ run_mean, float* __restrict__ run_var) {
+  pdl_enter();
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= C) return;
+  run_mean[c] = (1.f - kMomentum) * run_mean[c] + kMomentum * mean[c];
+  run_var[c] = (1.f - kMomentum) * run_var[c] + kMomentum * var[c];
+}
+
+// ---- fp32 SIMT GEMM: C[m][n] (+split z) = sum_k A(m,k) B(k,n) ------------------------
+// A(m,k) = TA ? A[k*lda + m] : A[m*lda + k];  B(k,n) = TB ? B[n*ldb + k] : B[k*ldb + n].
+// Split z covers k in [z*kchunk, ...) and writes Cm + z*M*ldc.  64x64 tiles.
+template <bool TA, bool TB>
+__global__ void __launch_bounds__(256) k_gemm(int M, int N, int K, const float* __restrict__ A, int lda,
+                                              const float* __restrict__ B, int ldb, float* __restrict__ Cm,
+                                              int ldc, int kchunk) {
+  pdl_enter();
+  __shared__ float As[16][64 + 4];
+  __shared__ float Bs[16][64 + 4];
+  const int tid = threadIdx.x, tx = tid % 16, ty = tid / 16;
+  const int m0 = blockIdx.x * 64, n0 = blockIdx.y * 64;
+  const int kb = blockIdx.z * kchunk;
+  const int ke = kb + kchunk < K ? kb + kchunk : K;
+  float acc[4][4] = {};
+  for (int k0 = kb; k0 < ke; k0 += 16) {
+    for (int e = tid; e < 16 * 64; e += 256) {
+      const int kk = e / 64, mm = e % 64;
+      const int gk = k0 + kk, gm = m0 + mm, gn = n0 + mm;
+      As[kk][mm] = (gk < ke && gm < M) ? (TA ? A[static_cast<int64_t>(gk) * lda + gm]
+                                             : A[static_cast<int64_t>(gm) * lda + gk])
+                                       : 0.f;
+      Bs[kk][mm] = (gk < ke && gn < N) ? (TB ? B[static_cast<int64_t>(gn) * ldb + gk]
+                                             : B[static_cast<int64_t>(gk) * ldb + gn])
+                                       : 0.f;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int kk = 0; kk < 16; ++kk) {
+      float a[4], b[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) a[i] = As[kk][ty * 4 + i];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) b[j] = Bs[kk][tx * 4 + j];
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j] += a[i] * b[j];
+    }
+    __syncthreads();
+  }
+  float* out = Cm + static_cast<int64_t>(blockIdx.z) * M * ldc;
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int gm = m0 + ty * 4 + i, gn = n0 + tx * 4 + j;
+      if (gm < M && gn < N) out[static_cast<int64_t>(gm) * ldc + gn] = acc[i][j];
+    }
+}
+
+// ---- head forward: gap[n][c] = mean_hw relu(bn(feat)) ---------------------------------
+__global__ void k_head_gap(const float* __restrict__ feat, int64_t N, int HW, int C,
+                           const float* __restrict__ mean, const float* __restrict__ var,
+                           const float* __restrict__ gamma, const float* __restrict__ beta,
+                           float* __restrict__ gap) {
+  pdl_enter();
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= N * C) return;
+  const int c = static_cast<int>(i % C);
+  const int64_t n = i / C;
+  const float inv = bn_inv(var[c]);
+  float acc = 0.f;
+  for (int p = 0; p < HW; ++p)
+    acc += fmaxf(bn_ref(feat[(n * HW + p) * C + c], mean[c], inv, gamma[c], beta[c]), 0.f);
+  gap[i] = acc * (1.f / static_cast<float>(HW));
+}
+
+// logits = gap . W^T + b; softmax cross entropy (ops.hpp:528-559): one CTA per
+// sample; per-sample loss (mean taken by k_loss_mean), g_logits = (p - onehot)/N.
+__global__ void k_head_loss(const float* __restrict__ gap, int64_t N, int C, const float* __restrict__ Wl,
+                            const float* __restrict__ bl, int classes, const int32_t* __restrict__ labels,
+                            float* __restrict__ logits, float* __restrict__ g_logits,
+                            float* __restrict__ loss_n, int* __restrict__ bad_label) {
+  pdl_enter();
+  __shared__ float red[256];
+  const int64_t n = blockIdx.x;
+  float* lg = logits + n * classes;
+  for (int o = threadIdx.x; o < classes; o += blockDim.x) {
+    float acc = bl[o];
+    for (int c = 0; c < C; ++c) acc += Wl[static_cast<int64_t>(o) * C + c] * gap[n * C + c];
+    lg[o] = acc;
+  }
+  __syncthreads();
+  // max and sum of exp, fixed-order tree over the CTA
+  float mx = -INFINITY;
+  for (int o = threadIdx.x; o < classes; o += blockDim.x) mx = fmaxf(mx, lg[o]);
+  red[threadIdx.x] = mx;
+  __syncthreads();
+  for (int s = blockDim.x / 2; s > 0; s >>= 1) {
+    if (threadIdx.x < s) red[threadIdx.x] = fmaxf(red[threadIdx.x], red[threadIdx.x + s]);
+    __syncthreads();
+  }
+  mx = red[0];
+  __syncthreads();
+  float sm = 0.f;
+  for (int o = threadIdx.x; o < classes; o += blockDim.x) sm += expf(lg[o] - mx);
+  red[threadIdx.x] = sm;
+  __syncthreads();
+  for (int s = blockDim.x / 2; s > 0; s >>= 1) {
+    if (threadIdx.x < s) red[threadIdx.x] += red[threadIdx.x + s];
+    __syncthreads();
+  }
+  const float log_sum = logf(red[0]) + mx;
+  const int label = labels[n];
+  if (label < 0 || label >= classes) {
+    if (threadIdx.x == 0) *bad_label = 1;
+    return;
+  }
+  for (int o = threadIdx.x; o < classes; o += blockDim.x) {
+    const float p = expf(lg[o] - log_sum);
+    g_logits[n * classes + o] = (p - (o == label ? 1.f : 0.f)) / static_cast<float>(N);
+  }
+  if (threadIdx.x == 0) loss_n[n] = log_sum - lg[label];
+}
+
+__global__ void k_loss_mean(const float* __restrict__ loss_n, int64_t N, float* __restrict__ loss) {
+  pdl_enter();
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  float s = 0.f;
+  for (int64_t i = 0; i < N; ++i) s += loss_n[i];
+  *loss = s / static_cast<float>(N);
+}
+
+// linear backward (ops.hpp:487-523): g_gap = g_logits . W, dW = g_logits^T . gap,
+// db = sum_n g_logits.  One thread per output element, fixed-order sums.
+__global__ void k_head_linear_bwd(const float* __restrict__ g_logits, const float* __restrict__ gap,
+                                  const float* __restrict__ Wl, int64_t N, int C, int classes,
+                                  float* __restrict__ g_gap, float* __restrict__ dW, float* __restrict__ db) {
+  pdl_enter();
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int64_t n_gg = N * C, n_dw = static_cast<int64_t>(classes) * C;
+  if (i < n_gg) {
+    const int64_t n = i / C;
+    const int c = static_cast<int>(i % C);
+    float acc = 0.f;
+    for (int o = 0; o < classes; ++o) acc += Wl[static_cast<int64_t>(o) * C + c] * g_logits[n * classes + o];
+    g_gap[i] = acc;
+  } else if (i < n_gg + n_dw) {
+    const int64_t j = i - n_gg;
+    const int o = static_cast<int>(j / C), c = static_cast<int>(j % C);
+    float acc = 0.f;
+    for (int64_t n = 0; n < N; ++n) acc += g_logits[n * classes + o] * gap[n * C + c];
+    dW[j] = acc;
+  } else if (i < n_gg + n_dw + classes) {
+    const int o = static_cast<int>(i - n_gg - n_dw);
+    float acc = 0.f;
+    for (int64_t n = 0; n < N; ++n) acc += g_logits[n * classes + o];
+    db[o] = acc;
+  }
+}
+
+// ---- BN backward of a transition / the head -------------------------------------------
+// Upstream gradient of act = relu(bn(x)) at pixel p, channel c:
+//   head:        g_gap[n][c] / HW
+//   transition:  g_P[q(p)][c] / 4 inside the pooled windows, 0 outside
+struct HeadGrad {
+  const float* g_gap;
+  int HW, C;
+  __device__ float operator()(int64_t p, int c) const {
+    return g_gap[(p / HW) * C + c] * (1.f / static_cast<float>(HW));
+  }
+};
+struct PoolGrad {
+  const float* g_P;  // [N*Ho*Wo, C]
+  int H, W, C;
+  __device__ float operator()(int64_t p, int c) const {
+    const int Ho = H / 2, Wo = W / 2;
+    const int64_t n = p / (static_cast<int64_t>(H) * W);
+    const int r = static_cast<int>(p - n * H * W);
+    const int y = r / W, x = r - (r / W) * W;
+    if (y >= 2 * Ho || x >= 2 * Wo) return 0.f;
+    return g_P[((n * Ho + y / 2) * Wo + x / 2) * C + c] * 0.25f;
+  }
+};
+
+// per-split partial sums (sum g, sum g*xhat) of g = relu'(act) * upstream, over
+// pixels [s*chunk, ...): thread = channel, fixed pixel order -> part[s][c]
+template <class G>
+__global__ void k_bnb_partials(const float* __restrict__ feat, int64_t M, int C, const float* __restrict__ mean,
+                               const float* __restrict__ var, const float* __restrict__ gamma,
+                               const float* __restrict__ beta, G up, int64_t chunk, double2* __restrict__ part) {
+  pdl_enter();
+  const int c = blockIdx.y * blockDim.x + threadIdx.x;
+  if (c >= C) return;
+  const float inv = bn_inv(var[c]);
+  const int64_t p0 = static_cast<int64_t>(blockIdx.x) * chunk;
+  const int64_t p1 = p0 + chunk < M ? p0 + chunk : M;
+  double s1 = 0.0, s2 = 0.0;
+  for (int64_t p = p0; p < p1; ++p) {
+    const float x = feat[p * C + c];
+    if (!(bn_ref(x, mean[c], inv, gamma[c], beta[c]) > 0.f)) continue;  // relu_backward
+    const float g = up(p, c);
+    s1 += g;
+    s2 += g * ((x - mean[c]) * inv);
+  }
+  part[static_cast<int64_t>(blockIdx.x) * C + c] = make_double2(s1, s2);
+}
+
+// out[p][c] = (gamma*inv) * (g - mg - xhat*mgx)  (written, ops.hpp:232-241)
+template <class G>
+__global__ void k_bnb_apply(const float* __restrict__ feat, int64_t M, int C, const float* __restrict__ mean,
+                            const float* __restrict__ var, const float* __restrict__ gamma,
+                            const float* __restrict__ beta, G up, const float* __restrict__ coef,
+                            float* __restrict__ out) {
+  pdl_enter();
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= M * C) return;
+  const int c = static_cast<int>(i % C);
+  const int64_t p = i / C;
+  const float x = feat[i];
+  const float inv = bn_inv(var[c]);
+  const float g = bn_ref(x, mean[c], inv, gamma[c], beta[c]) > 0.f ? up(p, c) : 0.f;
+  const float xh = (x - mean[c]) * inv;
+  out[i] = gamma[c] * inv * (g - coef[2 * c] - xh * coef[2 * c + 1]);
+}
+
+unsigned blocks_of(int64_t n, int t) { return static_cast<unsigned>((n + t - 1) / t); }
+
+}  // namespace
+
+// ---- the network plan ------------------------------------------------------------------
+struct ModelBlock {
+  Block* blk = nullptr;
+  int64_t M = 0;
+  int h = 0, w = 0, c0 = 0, m = 0, C = 0;
+  int64_t poff = 0, pelems = 0, roff = 0, relems = 0;
+  float* x = nullptr;    // NHWC [M, c0] block input
+  float* acc = nullptr;  // NHWC [M, C] block output gradient (in/out)
+};
+struct ModelTrans {
+  int C = 0, cout = 0;  // in (block C) / out channels
+  int64_t Mq = 0;       // pooled pixels
+  int64_t gamma = 0, beta = 0, w = 0, run = 0;  // offsets
+  float* P = nullptr;   // [Mq, C] pooled activations
+  float* gP = nullptr;  // [Mq, C]
+};
+
+}  // namespace dpb
+
+struct dpb_model {
+  dpb_model_desc d{};
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  std::vector<dpb::ModelBlock> blocks;
+  std::vector<dpb::ModelTrans> trans;
+  int64_t params = 0, running = 0;
+  int64_t head_gamma = 0, head_beta = 0, head_w = 0, head_b = 0, head_run = 0;
+  void* mem = nullptr;
+  float *gap = nullptr, *logits = nullptr, *g_logits = nullptr, *g_gap = nullptr, *loss_n = nullptr;
+  float* wpart = nullptr;
+  double2* part = nullptr;
+  float* coef = nullptr;
+  int* bad_label = nullptr;
+  int64_t wpart_elems = 0, part_rows = 0;
+};
+
+namespace dpb {
+namespace {
+
+constexpr int kSplitsMax = 148;
+
+int model_geometry(const dpb_model_desc* d, dpb_model* m) {
+  if (d == nullptr) return fail(DPB_CONFIG_ERROR, "null model descriptor");
+  if (d->nblocks < 1 || d->nblocks > 8) return fail(DPB_CONFIG_ERROR, "nblocks must be in [1, 8]");
+  if (d->k < 1 || d->c0 < 1 || d->classes < 1 || d->in_c < 1 || d->batch < 1)
+    return fail(DPB_SHAPE_ERROR, "invalid network geometry");
+  if (!(d->compression > 0.0) || d->compression > 1.0)
+    return fail(DPB_CONFIG_ERROR, "compression must be in (0, 1]");
+  if (d->dtype != DPB_FP32 && d->dtype != DPB_BF16) return fail(DPB_CONFIG_ERROR, "dtype");
+  int h = d->in_h, w = d->in_w, c = d->c0;
+  int64_t po = static_cast<int64_t>(d->c0) * d->in_c * 9, ro = 0;
+  const int bk = 4 * d->k;
+  m->blocks.clear();
+  m->trans.clear();
+  for (int b = 0; b < d->nblocks; ++b) {
+    if (d->blocks[b] < 1) return fail(DPB_SHAPE_ERROR, "every block needs >= 1 layer");
+    if (h < 1 || w < 1) return fail(DPB_SHAPE_ERROR, "spatial size collapses to zero");
+    ModelBlock mb;
+    mb.M = d->batch * h * w;
+    mb.h = h;
+    mb.w = w;
+    mb.c0 = c;
+    mb.m = d->blocks[b];
+    mb.C = c + mb.m * d->k;
+    dpb_block_desc bd{d->batch, h, w, c, mb.m, d->k, bk, d->dtype, DPB_NHWC};
+    dpb_arena_sizes sz{};
+    int rc = validate(&bd);
+    if (rc) return rc;
+    plan_arena(bd, &sz);
+    mb.poff = po;
+    mb.pelems = sz.param_elems;
+    mb.roff = ro;
+    mb.relems = sz.stat_elems;
+    po += sz.param_elems;
+    ro += sz.stat_elems;
+    m->blocks.push_back(mb);
+    if (b + 1 < d->nblocks) {
+      ModelTrans t;
+      t.C = mb.C;
+      t.cout = static_cast<int>(std::floor(d->compression * mb.C));  // densenet.hpp:118
+      if (t.cout < 1) return fail(DPB_CONFIG_ERROR, "compression collapses channels to 0");
+      if (h < 2 || w < 2) return fail(DPB_SHAPE_ERROR, "avgpool output collapses to zero size");
+      t.Mq = d->batch * (h / 2) * (w / 2);
+      t.gamma = po;
+      t.beta = po + t.C;
+      t.w = po + 2 * t.C;
+      po += 2 * t.C + static_cast<int64_t>(t.cout) * t.C;
+      t.run = ro;
+      ro += 2 * t.C;
+      m->trans.push_back(t);
+      c = t.cout;
+      h /= 2;
+      w /= 2;
+    }
+  }
+  const int C = m->blocks.back().C;
+  m->head_gamma = po;
+  m->head_beta = po + C;
+  m->head_w = po + 2 * C;
+  m->head_b = m->head_w + static_cast<int64_t>(d->classes) * C;
+  po = m->head_b + d->classes;
+  m->head_run = ro;
+  ro += 2 * C;
+  m->params = po;
+  m->running = ro;
+  return DPB_OK;
+}
+
+}  // namespace
+}  // namespace dpb
+
+using namespace dpb;
+
+extern "C" {
+
+DPB_API int dpb_model_sizes(const dpb_model_desc* desc, int64_t* param_elems, int64_t* running_elems) {
+  dpb_model m;
+  const int rc = model_geometry(desc, &m);
+  if (rc) return rc;
+  if (param_elems) *param_elems = m.params;
+  if (running_elems) *running_elems = m.running;
+  return DPB_OK;
+}
+
+DPB_API void dpb_model_destroy(dpb_model* m) {
+  if (!m) return;
+  for (auto& b : m->blocks)
+    if (b.blk) destroy(b.blk);
+  if (m->mem) cudaFree(m->mem);
+  delete m;
+}
+
+DPB_API int dpb_model_create(const dpb_model_desc* desc, int device, void* stream, dpb_model** out) {
+  if (out == nullptr) return fail(DPB_CONFIG_ERROR, "null output handle");
+  dpb_model* m = new (std::nothrow) dpb_model();
+  if (!m) return fail(DPB_CAPACITY_ERROR, "host allocation failed");
+  int rc = model_geometry(desc, m);
+  if (rc) {
+    delete m;
+    return rc;
+  }
+  m->d = *desc;
+  m->device = device;
+  m->stream = static_cast<cudaStream_t>(stream);
+  cudaError_t e = cudaSetDevice(device);
+  if (e != cudaSuccess) {
+    delete m;
+    return cuda_fail(e, "cudaSetDevice");
+  }
+  const int bk = 4 * desc->k;
+  for (auto& b : m->blocks) {
+    dpb_block_desc bd{desc->batch, b.h, b.w, b.c0, b.m, desc->k, bk, desc->dtype, DPB_NHWC};
+    rc = create(&bd, device, stream, &b.blk);
+    if (rc) {
+      dpb_model_destroy(m);
+      return rc;
+    }
+  }
+  // device buffers: block inputs and accumulators, transition P / gP, head,
+  // split-K partials, BN-backward partials and coefficients
+  int64_t bytes = 0;
+  auto take = [&](int64_t n) {
+    const int64_t o = bytes;
+    bytes += (n * 4 + 255) / 256 * 256;
+    return o;
+  };
+  std::vector<int64_t> off;
+  for (auto& b : m->blocks) {
+    off.push_back(take(b.M * b.c0));
+    off.push_back(take(b.M * b.C));
+  }
+  for (auto& t : m->trans) {
+    off.push_back(take(t.Mq * t.C));
+    off.push_back(take(t.Mq * t.C));
+  }
+  const int Cl = m->blocks.back().C;
+  const int64_t N = desc->batch;
+  const int64_t o_gap = take(N * Cl), o_log = take(N * desc->classes), o_glog = take(N * desc->classes),
+                o_ggap = take(N * Cl), o_loss = take(N);
+  int64_t wmax = static_cast<int64_t>(desc->c0) * desc->in_c * 9, cmax = Cl;
+  for (auto& t : m->trans) {
+    wmax = std::max<int64_t>(wmax, static_cast<int64_t>(t.cout) * t.C);
+    cmax = std::max<int64_t>(cmax, t.C);
+  }
+  m->wpart_elems = kSplitsMax * wmax;
+  const int64_t o_wpart = take(m->wpart_elems);
+  m->part_rows = kSplitsMax;
+  const int64_t o_part = take(4 * kSplitsMax * cmax);  // double2 = 4 floats
+  const int64_t o_coef = take(2 * cmax);
+  const int64_t o_bad = take(1);
+  e = cudaMalloc(&m->mem, static_cast<size_t>(bytes));
+  if (e != cudaSuccess) {
+    dpb_model_destroy(m);
+    return cuda_fail(e, "model cudaMalloc");
+  }
+  char* base = static_cast<char*>(m->mem);
+  size_t k = 0;
+  for (auto& b : m->blocks) {
+    b.x = reinterpret_cast<float*>(base + off[k++]);
+    b.acc = reinterpret_cast<float*>(base + off[k++]);
+  }
+  for (auto& t : m->trans) {
+    t.P = reinterpret_cast<float*>(base + off[k++]);
+    t.gP = reinterpret_cast<float*>(base + off[k++]);
+  }
+  m->gap = reinterpret_cast<float*>(base + o_gap);
+  m->logits = reinterpret_cast<float*>(base + o_log);
+  m->g_logits = reinterpret_cast<float*>(base + o_glog);
+  m->g_gap = reinterpret_cast<float*>(base + o_ggap);
+  m->loss_n = reinterpret_cast<float*>(base + o_loss);
+  m->wpart = reinterpret_cast<float*>(base + o_wpart);
+  m->part = reinterpret_cast<double2*>(base + o_part);
+  m->coef = reinterpret_cast<float*>(base + o_coef);
+  m->bad_label = reinterpret_cast<int*>(base + o_bad);
+  *out = m;
+  return DPB_OK;
+}
+
+DPB_API int dpb_model_sync(dpb_model* m) {
+  if (!m) return fail(DPB_CONFIG_ERROR, "null model");
+  const cudaError_t e = cudaStreamSynchronize(m->stream);
+  if (e != cudaSuccess) return cuda_fail(e, "model sync");
+  int bad = 0;
+  cudaMemcpy(&bad, m->bad_label, sizeof(int), cudaMemcpyDeviceToHost);
+  if (bad) {
+    cudaMemset(m->bad_label, 0, sizeof(int));
+    return fail(DPB_LABEL_ERROR, "label out of range [0, classes)");
+  }
+  return DPB_OK;
+}
+
+DPB_API int dpb_model_step(dpb_model* m, const float* input, const int32_t* labels, const float* params,
+                           float* running, float* grads, float* loss) {
+  if (!m || !input || !labels || !params || !running || !grads || !loss)
+    return fail(DPB_CONFIG_ERROR, "null pointer argument");
+  const dpb_model_desc& d = m->d;
+  cudaStream_t st = m->stream;
+  const int64_t N = d.batch;
+  const int nb = static_cast<int>(m->blocks.size());
+  // split-K of a reduction over `rows` pixels into at most kSplitsMax chunks
+  auto splits_of = [](int64_t rows, int64_t& chunk) {
+    const int64_t s = std::min<int64_t>(kSplitsMax, std::max<int64_t>(1, rows / 64));
+    chunk = (rows + s - 1) / s;
+    return static_cast<int>((rows + chunk - 1) / chunk);
+  };
+
+  // ---- forward --------------------------------------------------------------------
+  ModelBlock& b0 = m->blocks[0];
+  launch(k_stem_fwd, blocks_of(b0.M, 256), 256, 0, st, input, N, d.in_c, d.in_h, d.in_w, params, d.c0, b0.x,
+         b0.c0);
+  for (int b = 0; b < nb; ++b) {
+    ModelBlock& mb = m->blocks[b];
+    int rc = block_forward(mb.blk, mb.x, params + mb.poff, running + mb.roff, 1, 0);
+    if (rc) return rc;
+    const float* feat = static_cast<const float*>(mb.blk->feat);
+    const float* mean = mb.blk->fstat;
+    const float* var = mb.blk->fstat + mb.blk->g.C;
+    if (b + 1 < nb) {
+      ModelTrans& t = m->trans[b];
+      ModelBlock& nx = m->blocks[b + 1];
+      launch(k_trans_pool, blocks_of(t.Mq * t.C, 256), 256, 0, st, feat, N, mb.h, mb.w, t.C, mean, var,
+             params + t.gamma, params + t.beta, t.P);
+      launch(k_gemm<false, true>, dim3(blocks_of(t.Mq, 64), blocks_of(t.cout, 64), 1), 256, 0, st,
+             static_cast<int>(t.Mq), t.cout, t.C, static_cast<const float*>(t.P), t.C, params + t.w, t.C, nx.x,
+             nx.c0, t.C);
+      launch(k_running, blocks_of(t.C, 256), 256, 0, st, t.C, mean, var, running + t.run,
+             running + t.run + t.C);
+    } else {
+      const int HW = mb.h * mb.w;
+      launch(k_head_gap, blocks_of(N * mb.C, 256), 256, 0, st, feat, N, HW, mb.C, mean, var,
+             params + m->head_gamma, params + m->head_beta, m->gap);
+      launch(k_head_loss, static_cast<unsigned>(N), 256, 0, st, static_cast<const float*>(m->gap), N, mb.C,
+             params + m->head_w, params + m->head_b, d.classes, labels, m->logits, m->g_logits, m->loss_n,
+             m->bad_label);
+      launch(k_loss_mean, 1, 32, 0, st, static_cast<const float*>(m->loss_n), N, loss);
+      launch(k_running, blocks_of(mb.C, 256), 256, 0, st, mb.C, mean, var, running + m->head_run,
+             running + m->head_run + mb.C);
+    }
+  }
+
+  // ---- backward -------------------------------------------------------------------
+  {
+    ModelBlock& mb = m->blocks[nb - 1];
+    const int C = mb.C, HW = mb.h * mb.w;
+    launch(k_head_linear_bwd, blocks_of(N * C + static_cast<int64_t>(d.classes) * C + d.classes, 256), 256, 0,
+           st, static_cast<const float*>(m->g_logits), static_cast<const float*>(m->gap), params + m->head_w,
+           N, C, d.classes, m->g_gap, grads + m->head_w, grads + m->head_b);
+    const float* feat = static_cast<const float*>(mb.blk->feat);
+    const float* mean = mb.blk->fstat;
+    const float* var = mb.blk->fstat + mb.blk->g.C;
+    HeadGrad up{m->g_gap, HW, C};
+    int64_t chunk;
+    const int S = splits_of(mb.M, chunk);
+    launch(k_bnb_partials<HeadGrad>, dim3(S, blocks_of(C, 256)), 256, 0, st, feat, mb.M, C, mean, var,
+           params + m->head_gamma, params + m->head_beta, up, chunk, m->part);
+    launch_finalize_bn_bwd(st, m->part, S, C, static_cast<double>(mb.M), grads + m->head_gamma,
+                           grads + m->head_beta, m->coef);
+    launch(k_bnb_apply<HeadGrad>, blocks_of(mb.M * C, 256), 256, 0, st, feat, mb.M, C, mean, var,
+           params + m->head_gamma, params + m->head_beta, up, static_cast<const float*>(m->coef), mb.acc);
+  }
+  for (int b = nb - 1; b >= 0; --b) {
+    ModelBlock& mb = m->blocks[b];
+    int rc = block_backward(mb.blk, params + mb.poff, mb.acc, grads + mb.poff);
+    if (rc) return rc;
+    if (b > 0) {
+      ModelTrans& t = m->trans[b - 1];
+      ModelBlock& pv = m->blocks[b - 1];
+      // g_pool = mb.acc[:, :t.cout] (pitch mb.C); dW = g_pool^T . P (split-K), g_P = g_pool . W
+      int64_t chunk;
+      const int S = splits_of(t.Mq, chunk);
+      launch(k_gemm<true, false>, dim3(blocks_of(t.cout, 64), blocks_of(t.C, 64), S), 256, 0, st, t.cout, t.C,
+             static_cast<int>(t.Mq), static_cast<const float*>(mb.acc), mb.C, static_cast<const float*>(t.P), t.C,
+             m->wpart, t.C, static_cast<int>(chunk));
+      launch_fold_splits(st, m->wpart, S, static_cast<int64_t>(t.cout) * t.C, grads + t.w);
+      launch(k_gemm<false, false>, dim3(blocks_of(t.Mq, 64), blocks_of(t.C, 64), 1), 256, 0, st,
+             static_cast<int>(t.Mq), t.C, t.cout, static_cast<const float*>(mb.acc), mb.C, params + t.w, t.C, t.gP,
+             t.C, t.cout);
+      const float* feat = static_cast<const float*>(pv.blk->feat);
+      const float* mean = pv.blk->fstat;
+      const float* var = pv.blk->fstat + pv.blk->g.C;
+      PoolGrad up{t.gP, pv.h, pv.w, t.C};
+      const int S2 = splits_of(pv.M, chunk);
+      launch(k_bnb_partials<PoolGrad>, dim3(S2, blocks_of(t.C, 256)), 256, 0, st, feat, pv.M, t.C, mean, var,
+             params + t.gamma, params + t.beta, up, chunk, m->part);
+      launch_finalize_bn_bwd(st, m->part, S2, t.C, static_cast<double>(pv.M), grads + t.gamma, grads + t.beta,
+                             m->coef);
+      launch(k_bnb_apply<PoolGrad>, blocks_of(pv.M * t.C, 256), 256, 0, st, feat, pv.M, t.C, mean, var,
+             params + t.gamma, params + t.beta, up, static_cast<const float*>(m->coef), pv.acc);
+    } else {
+      int64_t chunk;
+      const int S = splits_of(mb.M, chunk);
+      launch(k_stem_wgrad, S, 256, 0, st, input, N, d.in_c, d.in_h, d.in_w, static_cast<const float*>(mb.acc),
+             mb.C, d.c0, chunk, m->wpart);
+      launch_fold_splits(st, m->wpart, S, static_cast<int64_t>(d.c0) * d.in_c * 9, grads);
+    }
+  }
+  const cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? DPB_OK : cuda_fail(e, "model step launch");
+}
+
+}  // extern "C"

@@ -90,3 +90,74 @@ CONFIGS = {
     "d264k32": DenseNetConfig((6, 12, 64, 48), 32, True, 0.5, 1000, 64, (3, 224, 224)),
     "d264k48": DenseNetConfig((6, 12, 64, 48), 48, True, 0.5, 1000, 96, (3, 224, 224)),
 }
+
+
+class ModelPlan:
+    """Whole-network training step on the GPU (``dpb_model_*``): the stem,
+    dense blocks, transitions, head and softmax cross-entropy of
+    GraphPlan<T>::forward / compute_loss / backward (graph.hpp:731-826,
+    :1065-1183).  Parameters and gradients are flat in the reference's
+    registration order (include/dpb.h)."""
+
+    def __init__(self, cfg: DenseNetConfig, batch: int, dtype: str = "fp32", device: int | None = None,
+                 stream=None):
+        import torch
+
+        from ._lib import ModelDesc
+        self.cfg = cfg
+        self.batch = batch
+        d = ModelDesc()
+        d.nblocks = len(cfg.block_sizes)
+        for i, m in enumerate(cfg.block_sizes):
+            d.blocks[i] = m
+        d.k = cfg.growth_rate
+        d.compression = float(cfg.compression)
+        d.classes = cfg.num_classes
+        d.c0 = cfg.c0
+        d.in_c, d.in_h, d.in_w = cfg.in_shape
+        d.batch = batch
+        d.dtype = {"fp32": 0, "bf16": 1}[dtype]
+        if not cfg.bottleneck:
+            raise ValueError("ModelPlan supports bottleneck (DenseNet-B/BC) networks only")
+        self._desc = d
+        pe, re_ = C.c_int64(), C.c_int64()
+        check(lib().dpb_model_sizes(C.byref(d), C.byref(pe), C.byref(re_)))
+        self.param_elems, self.running_elems = pe.value, re_.value
+        self.device = torch.cuda.current_device() if device is None else device
+        h = C.c_void_p()
+        s = None if stream is None else C.c_void_p(stream.cuda_stream)
+        check(lib().dpb_model_create(C.byref(d), self.device, s, C.byref(h)))
+        self._h = h
+
+    def initial_running(self, device="cuda"):
+        """Running means 0 / variances 1 in the model's running layout."""
+        import torch
+        parts = []
+        shapes = self.cfg.block_shapes(self.batch)
+        for b, shp in enumerate(shapes):
+            parts.append(shp.initial_running("cpu"))
+            C_ = shp.c_out
+            parts.append(torch.cat([torch.zeros(C_), torch.ones(C_)]))  # transition b or head
+        return torch.cat(parts).to(device)
+
+    def step(self, x, labels, params, running, grads, loss) -> None:
+        """x NCHW fp32, labels int32 [batch], params / grads flat fp32, running
+        flat fp32 (updated), loss a 1-element fp32 device tensor."""
+        def ptr(t):
+            return C.c_void_p(t.data_ptr())
+        check(lib().dpb_model_step(self._h, ptr(x), ptr(labels), ptr(params), ptr(running), ptr(grads),
+                                   ptr(loss)))
+
+    def sync(self) -> None:
+        check(lib().dpb_model_sync(self._h))
+
+    def close(self) -> None:
+        if getattr(self, "_h", None) is not None and self._h.value:
+            lib().dpb_model_destroy(self._h)
+            self._h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

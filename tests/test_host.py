@@ -152,3 +152,39 @@ def test_block_shapes_match_geometry():
     assert shapes[2].c_out == 384 + 64 * 48 == 3456
     bc = model.CONFIGS["bc100"].block_shapes(64)
     assert [(s.h, s.c0, s.c_out) for s in bc] == [(32, 24, 216), (16, 108, 300), (8, 150, 342)]
+
+
+def test_model_sizes_match_reference_parameter_count():
+    # dpb_model_sizes (registration-order layout) == densenet.hpp count_parameters
+    from paper_1707_06990_b200.model import CONFIGS, DenseNetConfig, ModelPlan  # noqa: F401
+    import ctypes as C
+    from paper_1707_06990_b200._lib import ModelDesc, lib
+    cases = [DenseNetConfig((2, 2, 2), 4, True, 0.5, 10, 8, (3, 8, 8)),
+             DenseNetConfig((3, 3, 3), 12, True, 0.5, 10, 24, (3, 16, 16)),
+             CONFIGS["bc100"]]
+    for cfg in cases:
+        d = ModelDesc()
+        d.nblocks = len(cfg.block_sizes)
+        for i, m in enumerate(cfg.block_sizes):
+            d.blocks[i] = m
+        d.k, d.compression, d.classes, d.c0 = cfg.growth_rate, cfg.compression, cfg.num_classes, cfg.c0
+        d.in_c, d.in_h, d.in_w = cfg.in_shape
+        d.batch, d.dtype = 4, 1
+        pe, re_ = C.c_int64(), C.c_int64()
+        assert lib().dpb_model_sizes(C.byref(d), C.byref(pe), C.byref(re_)) == 0
+        assert pe.value == P.count_parameters(cfg)
+        # running: per block its stats, per transition / head 2C
+        shapes = cfg.block_shapes(4)
+        assert re_.value == sum(s.stat_elems + 2 * s.c_out for s in shapes)
+
+
+def test_model_sizes_rejects_bad_geometry():
+    import ctypes as C
+    from paper_1707_06990_b200._lib import ModelDesc, lib
+    d = ModelDesc()
+    d.nblocks, d.k, d.compression, d.classes, d.c0 = 2, 4, 0.0, 10, 8
+    d.blocks[0] = d.blocks[1] = 2
+    d.in_c, d.in_h, d.in_w, d.batch = 3, 8, 8, 2
+    assert lib().dpb_model_sizes(C.byref(d), None, None) == 6      # ConfigError (compression)
+    d.compression, d.nblocks = 0.5, 0
+    assert lib().dpb_model_sizes(C.byref(d), None, None) == 6
