@@ -24,7 +24,7 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 BATCH = 64
-METRIC = "DenseNet train images/sec (dense blocks fwd+bwd)"
+METRIC = "DenseNet train images/sec"
 
 
 def load_peaks():
@@ -110,13 +110,27 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sms)}
 
 
+def cpu_runner(config: str):
+    """The reference CPU workload matching the GPU arm: its whole training step
+    (GraphPlan::step_trace, one image per process) for CIFAR-type networks,
+    else one image of every dense block (fwd+bwd)."""
+    from oracle import cpu_bench as CB
+    from paper_1707_06990_b200.model import CONFIGS
+    cfg = CONFIGS[config]
+    if cfg.in_shape[1] < 64 and CB.kind() == "reference":
+        net = (tuple(cfg.block_sizes), cfg.growth_rate, cfg.compression, cfg.num_classes, cfg.c0,
+               tuple(cfg.in_shape))
+        return CB.CpuModelRunner(net, batch=1), f"1 image, {config} full training step (GraphPlan::step_trace)"
+    return CB.CpuRunner(block_shapes(config, 1)), f"1 image of each {config} dense block (fwd+bwd, f32)"
+
+
 def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return 0
     from oracle import cpu_bench as CB
+    runner, what = cpu_runner(args.config)
     shapes = block_shapes(args.config, 1)
-    runner = CB.CpuRunner(shapes)
     for i in range(args.warmup):
         runner.step(seed=i)
     imgs = secs = 0.0
@@ -136,12 +150,11 @@ def run_reference(args):
         "steps": steps, "warmup": args.warmup, "ms_per_step": 1000 * secs / steps,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
         "data": "synthetic",
-        "config": {"workload": f"{args.config} dense blocks fwd+bwd, reference CPU (denseplan ops:: in "
-                               f"GraphPlan order)", "global_batch": runner.procs, "per_process_batch": 1,
+        "config": {"workload": f"{args.config}: {what}, reference CPU", "global_batch": runner.procs,
+                   "per_process_batch": 1,
                    "shapes": shapes},
         "cpu_baseline": {"value": value, "unit": "images/s", "cores": runner.procs, "kind": CB.kind(),
-                         "sample": f"{steps} steps x {runner.procs} processes x 1 image of each "
-                                   f"{args.config} dense block (fwd+bwd), {CB.cpu_model()}"},
+                         "sample": f"{steps} steps x {runner.procs} processes x {what}, {CB.cpu_model()}"},
         "e2e": {"value": value, "unit": "images/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -160,6 +173,8 @@ def main():
     ap.add_argument("--no-graph", action="store_true", help="launch kernels directly (no CUDA graph)")
     ap.add_argument("--cpu-budget-s", type=float, default=25.0)
     ap.add_argument("--ref-budget-s", type=float, default=180.0)
+    ap.add_argument("--ncu-what", default="blocks", choices=["blocks", "model"],
+                    help="with --ncu-step: the dense blocks alone or the whole network step")
     ap.add_argument("--ncu-step", action="store_true",
                     help="after warm-up, run ONE step inside cudaProfilerStart/Stop and exit "
                          "(for `ncu --profile-from-start off`; prints no bench line)")
@@ -259,43 +274,102 @@ def main():
             step()
         reduce_grads()
 
-    if args.ncu_step:
+    def ncu_step_and_exit(fn, what):
         torch.cuda.synchronize(dev)
         torch.cuda.profiler.start()
         with torch.cuda.stream(stream):
-            timed_step()
+            fn()
         torch.cuda.synchronize(dev)
         torch.cuda.profiler.stop()
-        print(json.dumps({"ncu_step": True, "launches_per_step": launches_per_step}), flush=True)
-        for b in blocks:
-            b["plan"].close()
+        print(json.dumps({"ncu_step": what, "launches_per_step": launches_per_step}), flush=True)
         return 0
 
-    # ---- timed region --------------------------------------------------------
-    if world > 1:
-        dist.barrier()
-    torch.cuda.synchronize(dev)
-    clocks = ClockSampler(local)
-    time.sleep(0.3)
-    t0 = torch.cuda.Event(enable_timing=True)
-    t1 = torch.cuda.Event(enable_timing=True)
-    with torch.cuda.stream(stream):
-        t0.record(stream)
-        for _ in range(args.steps):
-            timed_step()
-        t1.record(stream)
-    torch.cuda.synchronize(dev)
-    if world > 1:
-        dist.barrier()
-    torch.cuda.synchronize(dev)
-    ms = t0.elapsed_time(t1)
-    clk = clocks.stop()
-    if world > 1:
-        tt = torch.tensor([ms], device=dev)
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        ms = float(tt.item())
-    ms_per_step = ms / args.steps
-    value = BATCH * world * args.steps / (ms / 1000.0)
+    if args.ncu_step and args.ncu_what == "blocks":
+        return ncu_step_and_exit(timed_step, "dense blocks")
+
+    def time_steps(fn):
+        """K steps of fn between barriers + syncs, CUDA events on `stream`, nvidia-smi
+        clocks sampled during the region; returns (ms per step, max over ranks; clocks)."""
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize(dev)
+        clocks = ClockSampler(local)
+        time.sleep(0.3)
+        t0 = torch.cuda.Event(enable_timing=True)
+        t1 = torch.cuda.Event(enable_timing=True)
+        with torch.cuda.stream(stream):
+            t0.record(stream)
+            for _ in range(args.steps):
+                fn()
+            t1.record(stream)
+        torch.cuda.synchronize(dev)
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize(dev)
+        ms = t0.elapsed_time(t1)
+        clk = clocks.stop()
+        if world > 1:
+            tt = torch.tensor([ms], device=dev)
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            ms = float(tt.item())
+        return ms / args.steps, clk
+
+    # ---- dense blocks alone (the hot path) --------------------------------------
+    blocks_ms, blocks_clk = time_steps(timed_step)
+    blocks_value = BATCH * world / (blocks_ms / 1000.0)
+
+    # ---- the whole network (headline for CIFAR-type configs: the 3x3 stem) -------
+    from paper_1707_06990_b200.model import CONFIGS, ModelPlan
+    cfg = CONFIGS[args.config]
+    whole = cfg.in_shape[1] < 64
+    mplan = None
+    if whole:
+        mplan = ModelPlan(cfg, BATCH, dtype=args.dtype, device=local, stream=stream)
+        m_params = mplan.init_params(seed=1234 + rank, device=dev)
+        m_run = mplan.initial_running(dev)
+        m_x = torch.randn(BATCH, *cfg.in_shape, generator=g).to(dev)
+        m_labels = (torch.arange(BATCH, dtype=torch.int32) % cfg.num_classes).to(dev)
+        m_grads = torch.empty(mplan.param_elems, device=dev)
+        m_loss = torch.zeros(1, device=dev)
+
+        def model_step():
+            mplan.step(m_x, m_labels, m_params, m_run, m_grads, m_loss)
+
+        def model_reduce():
+            if world > 1:   # DP allreduce of the flat gradients (per-GPU BN), outside the graph
+                dist.all_reduce(m_grads)
+                m_grads.mul_(1.0 / world)
+
+        with torch.cuda.stream(stream):
+            for _ in range(args.warmup):
+                model_step()
+                model_reduce()
+        torch.cuda.synchronize(dev)
+        m_graph = None
+        if not args.no_graph:
+            m_graph = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(m_graph, stream=stream):
+                model_step()
+            with torch.cuda.stream(stream):
+                for _ in range(2):
+                    m_graph.replay()
+            torch.cuda.synchronize(dev)
+
+        def model_timed():
+            if m_graph is not None:
+                m_graph.replay()
+            else:
+                model_step()
+            model_reduce()
+
+        if args.ncu_step:
+            return ncu_step_and_exit(model_timed, "whole network")
+        ms_per_step, clk = time_steps(model_timed)
+        value = BATCH * world / (ms_per_step / 1000.0)
+        # block launches + stem / transitions / head kernels of dpb_model_step
+        launches_per_step += 11 + 9 * (len(cfg.block_sizes) - 1)
+    else:
+        ms_per_step, clk, value = blocks_ms, blocks_clk, blocks_value
 
     # ---- per-kernel roofline (separate profiled pass, events on `stream`) -----
     for b in blocks:
@@ -349,42 +423,86 @@ def main():
                    "TFLOP/s": round(v["flops"] / max(v["total_ms"], 1e-9) / 1e9, 2)}
                for k, v in sorted(cats.items(), key=lambda kv: -kv[1]["total_ms"])}
 
-    # ---- end to end through the reference-facing C-ABI (host buffers, NCHW) ---
-    # HostBlockChain: per step, H2D of every block's input and upstream gradient
-    # from pinned host memory (copy stream, per-block events), the block
-    # forwards/backwards, the DP allreduce (N > 1) and the D2H of the flat fp32
-    # gradients, all inside the timed region.
-    from paper_1707_06990_b200.host import HostBlockChain
-    chain = HostBlockChain([b["shape"] for b in blocks], [b["params"] for b in blocks],
-                           [b["running"] for b in blocks], dtype=args.dtype, layout="nchw",
-                           device=dev, stream=stream, group=None)
-    x_h = [torch.randn(b["shape"].n, b["shape"].c0, b["shape"].h, b["shape"].w, generator=g).pin_memory()
-           for b in blocks]
-    g_h = [torch.randn(b["shape"].n, b["shape"].c_out, b["shape"].h, b["shape"].w, generator=g).pin_memory()
-           for b in blocks]
-    for _ in range(args.warmup):
-        chain.step(x_h, g_h)
-    torch.cuda.synchronize(dev)
-    ek = max(3, min(args.steps, 10))
-    e0 = torch.cuda.Event(enable_timing=True)
-    e1 = torch.cuda.Event(enable_timing=True)
-    with torch.cuda.stream(stream):
-        e0.record(stream)
-    for _ in range(ek):
-        chain.step(x_h, g_h)
-    with torch.cuda.stream(stream):
-        e1.record(stream)
-    torch.cuda.synchronize(dev)
-    ems = e0.elapsed_time(e1)
-    if world > 1:
-        tt = torch.tensor([ems], device=dev)
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        ems = float(tt.item())
-    e2e = {"value": BATCH * world * ek / (ems / 1000.0), "unit": "images/s",
-           "h2d_bytes_per_step": chain.h2d_bytes(), "d2h_bytes_per_step": chain.d2h_bytes(), "steps": ek,
-           "path": "HostBlockChain.step: dpb_block_forward/backward (NCHW), pinned host buffers, "
-                   "H2D on a copy stream overlapping compute"}
-    chain.close()
+    # ---- end to end through the public API with host buffers --------------------
+    if whole:
+        # ModelPlan.step per step: H2D of the images and labels from pinned host
+        # memory, the training step, the DP allreduce (N > 1), D2H of the flat
+        # fp32 gradients and the loss
+        x_h = torch.randn(BATCH, *cfg.in_shape, generator=g).pin_memory()
+        l_h = (torch.arange(BATCH, dtype=torch.int32) % cfg.num_classes).pin_memory()
+        grads_h = torch.empty(mplan.param_elems).pin_memory()
+        loss_h = torch.empty(1).pin_memory()
+        e_x = torch.empty_like(m_x)
+        e_l = torch.empty_like(m_labels)
+
+        def e2e_step():
+            e_x.copy_(x_h, non_blocking=True)
+            e_l.copy_(l_h, non_blocking=True)
+            mplan.step(e_x, e_l, m_params, m_run, m_grads, m_loss)
+            model_reduce()
+            grads_h.copy_(m_grads, non_blocking=True)
+            loss_h.copy_(m_loss, non_blocking=True)
+
+        with torch.cuda.stream(stream):
+            for _ in range(args.warmup):
+                e2e_step()
+        torch.cuda.synchronize(dev)
+        ek = max(3, min(args.steps, 10))
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        with torch.cuda.stream(stream):
+            e0.record(stream)
+            for _ in range(ek):
+                e2e_step()
+            e1.record(stream)
+        torch.cuda.synchronize(dev)
+        ems = e0.elapsed_time(e1)
+        if world > 1:
+            tt = torch.tensor([ems], device=dev)
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            ems = float(tt.item())
+        e2e = {"value": BATCH * world * ek / (ems / 1000.0), "unit": "images/s",
+               "h2d_bytes_per_step": x_h.numel() * 4 + l_h.numel() * 4,
+               "d2h_bytes_per_step": grads_h.numel() * 4 + 4, "steps": ek,
+               "path": "ModelPlan.step (dpb_model_step): pinned host images/labels -> training step -> "
+                       "host gradients and loss"}
+    else:
+        # HostBlockChain: per step, H2D of every block's input and upstream gradient
+        # from pinned host memory (copy stream, per-block events), the block
+        # forwards/backwards, the DP allreduce (N > 1) and the D2H of the flat fp32
+        # gradients, all inside the timed region.
+        from paper_1707_06990_b200.host import HostBlockChain
+        chain = HostBlockChain([b["shape"] for b in blocks], [b["params"] for b in blocks],
+                               [b["running"] for b in blocks], dtype=args.dtype, layout="nchw",
+                               device=dev, stream=stream, group=None)
+        x_h = [torch.randn(b["shape"].n, b["shape"].c0, b["shape"].h, b["shape"].w, generator=g).pin_memory()
+               for b in blocks]
+        g_h = [torch.randn(b["shape"].n, b["shape"].c_out, b["shape"].h, b["shape"].w, generator=g).pin_memory()
+               for b in blocks]
+        for _ in range(args.warmup):
+            chain.step(x_h, g_h)
+        torch.cuda.synchronize(dev)
+        ek = max(3, min(args.steps, 10))
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        with torch.cuda.stream(stream):
+            e0.record(stream)
+        for _ in range(ek):
+            chain.step(x_h, g_h)
+        with torch.cuda.stream(stream):
+            e1.record(stream)
+        torch.cuda.synchronize(dev)
+        ems = e0.elapsed_time(e1)
+        if world > 1:
+            tt = torch.tensor([ems], device=dev)
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            ems = float(tt.item())
+        e2e = {"value": BATCH * world * ek / (ems / 1000.0), "unit": "images/s",
+               "h2d_bytes_per_step": chain.h2d_bytes(), "d2h_bytes_per_step": chain.d2h_bytes(), "steps": ek,
+               "path": "HostBlockChain.step: dpb_block_forward/backward (NCHW), pinned host buffers, "
+                       "H2D on a copy stream overlapping compute"}
+        chain.close()
+
 
     # ---- memory: efficient arena vs naive store-everything ---------------------
     eff = sum(P.block_memory(b["shape"], args.dtype)[0] for b in blocks)
@@ -395,7 +513,7 @@ def main():
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
             from oracle import cpu_bench as CB
-            runner = CB.CpuRunner(block_shapes(args.config, 1))
+            runner, what = cpu_runner(args.config)
             runner.step(seed=1)        # warm (spawn + page-in)
             imgs, secs, n = 0, 0.0, 0
             while secs < args.cpu_budget_s and n < 5:
@@ -405,8 +523,7 @@ def main():
                 n += 1
             runner.close()
             cpu = {"value": imgs / secs, "unit": "images/s", "cores": runner.procs, "kind": CB.kind(),
-                   "sample": f"{n} steps x {runner.procs} processes x 1 image of each {args.config} "
-                             f"dense block (fwd+bwd, f32), {CB.cpu_model()}"}
+                   "sample": f"{n} steps x {runner.procs} processes x {what}, {CB.cpu_model()}"}
         except Exception as exc:  # the baseline is reported, never the target
             cpu = {"value": None, "unit": "images/s", "cores": 0, "kind": "port", "sample": f"failed: {exc}"}
 
@@ -417,12 +534,17 @@ def main():
             "metric": METRIC, "value": value, "unit": "images/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": args.dtype, "data": "synthetic",
-            "config": {"workload": f"DenseNet-{args.config} dense blocks, fwd+bwd (stem/transitions/head "
-                                   f"not in the hot path)", "model": args.config, "global_batch": BATCH * world,
+            "config": {"workload": (f"DenseNet-{args.config} full training step: stem, dense blocks, transitions, "
+                                    f"head, softmax-xent, fwd+bwd" if whole else
+                                    f"DenseNet-{args.config} dense blocks, fwd+bwd (the {cfg.in_shape[1]}px "
+                                    f"7x7/2 stem is not built)"),
+                       "model": args.config, "global_batch": BATCH * world,
                        "per_gpu_batch": BATCH, "blocks": [list(s) for s in shapes],
                        "parallelism": f"dp{world}",
                        "cuda_graph": graph is not None,
                        "l2": f"working set {ws_bytes / 1e6:.0f} MB > 126 MB L2 (no explicit flush)"},
+            "dense_blocks": {"value": blocks_value, "unit": "images/s", "ms_per_step": blocks_ms,
+                             "note": "the dense blocks alone (the hot path), graph-captured"},
             "roofline": roof, "step_roofline": step_roof, "kernels": kernels,
             "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": launches_per_step * args.steps,
@@ -433,6 +555,8 @@ def main():
         print(json.dumps(line), flush=True)
     for b in blocks:
         b["plan"].close()
+    if mplan is not None:
+        mplan.close()
     if world > 1:
         dist.destroy_process_group()
     return 0

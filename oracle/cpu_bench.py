@@ -1,13 +1,17 @@
 """TEST INFRASTRUCTURE — CPU timing legs of bench.py (cpu_baseline and
 ``--impl reference``).  Imported only by bench.py; never by the product.
 
-Times the reference CPU implementation of the hot path — the dense-block
-forward + backward of ``denseplan`` (its public ``ops::`` in GraphPlan's
-order, oracle/_ref built from /root/reference by oracle/Makefile) — on the
-same block shapes the GPU arm runs, with one image per process and one
-process per host core (the reference is single-threaded).  When
-oracle/_ref was not built, the plain-C restatement (liboracle.so) is timed
-instead and reported as kind "port".
+Times the reference CPU implementation, built from /root/reference by
+oracle/Makefile into oracle/_ref, with one process per host core (the
+reference is single-threaded):
+
+- CpuModelRunner: the whole training step, GraphPlan<float>::step_trace (the
+  reference's public API), on the same network the GPU arm runs, with a small
+  batch per process.
+- CpuRunner: the dense-block forward + backward alone (the reference's public
+  ops:: in GraphPlan's order), one image of each block shape per process.
+  When oracle/_ref was not built, the plain-C restatement (liboracle.so) is
+  timed instead and reported as kind "port".
 
 This module must not import torch: workers are spawned processes.
 """
@@ -75,6 +79,36 @@ class CpuRunner:
         self.pool.map(_worker, [(self.shapes, seed + 1000 * i) for i in range(self.procs)])
         wall = time.perf_counter() - t0
         return self.procs * self.images_per_worker, wall
+
+    def close(self):
+        self.pool.close()
+        self.pool.join()
+
+
+def _model_worker(args):
+    net, batch, seed = args
+    blocks, k, comp, classes, c0, in_shape = net
+    loss, secs = O.ref_model_step(blocks, k, 1, comp, classes, c0, (batch,) + tuple(in_shape), seed,
+                                  steps=1, fast=True)
+    return secs
+
+
+class CpuModelRunner:
+    """`procs` spawned single-threaded workers, each timing one reference
+    training step (GraphPlan::step_trace) of the network at `batch` images;
+    a step returns (images, seconds of the slowest worker's step)."""
+
+    def __init__(self, net, batch: int = 1, procs: int | None = None):
+        if kind() != "reference":
+            raise FileNotFoundError("oracle/_ref (the reference build) is required for the model runner")
+        self.net = net
+        self.batch = batch
+        self.procs = procs or os.cpu_count() or 1
+        self.pool = mp.get_context("spawn").Pool(self.procs)
+
+    def step(self, seed: int = 0):
+        secs = self.pool.map(_model_worker, [(self.net, self.batch, seed + i) for i in range(self.procs)])
+        return self.procs * self.batch, max(secs)
 
     def close(self):
         self.pool.close()

@@ -41,48 +41,71 @@ __device__ __forceinline__ float bn_ref(float x, float mean, float inv, float ga
 __global__ void k_stem_fwd(const float* __restrict__ in, int64_t N, int cin, int H, int W,
                            const float* __restrict__ w, int c0, float* __restrict__ out, int ld) {
   pdl_enter();
+  extern __shared__ float ws[];  // c0 x cin x 9 weights
+  for (int i = threadIdx.x; i < c0 * cin * 9; i += blockDim.x) ws[i] = w[i];
+  __syncthreads();
   const int64_t p = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (p >= N * H * W) return;
-  const int64_t n = p / (static_cast<int64_t>(H) * W);
-  const int rem = static_cast<int>(p - n * H * W);
+  const int hw = H * W;
+  const int n = static_cast<int>(p / hw);
+  const int rem = static_cast<int>(p - static_cast<int64_t>(n) * hw);
   const int y = rem / W, x = rem - (rem / W) * W;
+  float win[4 * 9];  // cin <= 4 (dpb_model_create)
+  for (int ci = 0; ci < cin; ++ci)
+#pragma unroll
+    for (int t = 0; t < 9; ++t) {
+      const int yy = y + t / 3 - 1, xx = x + t % 3 - 1;
+      win[ci * 9 + t] = (yy >= 0 && yy < H && xx >= 0 && xx < W)
+                            ? __ldg(in + ((static_cast<int64_t>(n) * cin + ci) * H + yy) * W + xx)
+                            : 0.f;
+    }
   for (int o = 0; o < c0; ++o) {
     float acc = 0.f;
-    for (int ci = 0; ci < cin; ++ci)
-      for (int ky = 0; ky < 3; ++ky) {
-        const int yy = y + ky - 1;
-        if (yy < 0 || yy >= H) continue;
-        for (int kx = 0; kx < 3; ++kx) {
-          const int xx = x + kx - 1;
-          if (xx < 0 || xx >= W) continue;
-          acc += __ldg(w + ((o * cin + ci) * 3 + ky) * 3 + kx) *
-                 __ldg(in + ((n * cin + ci) * H + yy) * W + xx);
-        }
-      }
+    for (int i = 0; i < cin * 9; ++i) acc += ws[o * cin * 9 + i] * win[i];
     out[p * ld + o] = acc;
   }
 }
 
-// stem dW partials: split s sums pixels [s*chunk, ...) for every weight
-// (o, ci, ky, kx) -> wpart[s][widx]; g = NHWC rows of pitch ld, channels [0, c0).
+// stem dW partials: split s covers pixels [s*kStemChunk, ...): the chunk's
+// upstream gradients (g rows of pitch ld, channels [0, c0)) and its 3x3xcin
+// input windows are staged in shared memory, then every weight (o, ci, ky, kx)
+// sums its products over the chunk in pixel order -> wpart[s][widx].
+__host__ __device__ inline int stem_chunk(int c0, int cin) {  // pixels per split, <= 40 KB staged
+  const int c = (40 * 1024) / ((c0 + cin * 9) * 4);
+  return c < 16 ? 16 : (c > 128 ? 128 : c);
+}
 __global__ void k_stem_wgrad(const float* __restrict__ in, int64_t N, int cin, int H, int W,
-                             const float* __restrict__ g, int ld, int c0, int64_t chunk,
-                             float* __restrict__ wpart) {
+                             const float* __restrict__ g, int ld, int c0, float* __restrict__ wpart) {
+  const int kStemChunk = stem_chunk(c0, cin);
   pdl_enter();
-  const int nw = c0 * cin * 9;
-  const int64_t M = N * H * W;
-  const int64_t p0 = static_cast<int64_t>(blockIdx.x) * chunk;
-  const int64_t p1 = p0 + chunk < M ? p0 + chunk : M;
+  extern __shared__ float sm[];
+  float* gs = sm;                        // [kStemChunk][c0]
+  float* xs = sm + kStemChunk * c0;      // [kStemChunk][cin*9]
+  const int nt = cin * 9, nw = c0 * nt;
+  const int hw = H * W;
+  const int64_t M = N * hw;
+  const int64_t p0 = static_cast<int64_t>(blockIdx.x) * kStemChunk;
+  const int np = static_cast<int>(M - p0 < kStemChunk ? M - p0 : kStemChunk);
+  for (int e = threadIdx.x; e < np * c0; e += blockDim.x) {
+    const int r = e / c0, o = e - r * c0;
+    gs[e] = g[(p0 + r) * ld + o];
+  }
+  for (int e = threadIdx.x; e < np * nt; e += blockDim.x) {
+    const int r = e / nt, t = e - r * nt;
+    const int64_t p = p0 + r;
+    const int n = static_cast<int>(p / hw);
+    const int rem = static_cast<int>(p - static_cast<int64_t>(n) * hw);
+    const int ci = t / 9, tap = t - ci * 9;
+    const int yy = rem / W + tap / 3 - 1, xx = rem % W + tap % 3 - 1;
+    xs[e] = (yy >= 0 && yy < H && xx >= 0 && xx < W)
+                ? __ldg(in + ((static_cast<int64_t>(n) * cin + ci) * H + yy) * W + xx)
+                : 0.f;
+  }
+  __syncthreads();
   for (int wi = threadIdx.x; wi < nw; wi += blockDim.x) {
-    const int kx = wi % 3, ky = (wi / 3) % 3, ci = (wi / 9) % cin, o = wi / (9 * cin);
+    const int o = wi / nt, t = wi - o * nt;
     float acc = 0.f;
-    for (int64_t p = p0; p < p1; ++p) {
-      const int64_t n = p / (static_cast<int64_t>(H) * W);
-      const int rem = static_cast<int>(p - n * H * W);
-      const int yy = rem / W + ky - 1, xx = rem % W + kx - 1;
-      if (yy < 0 || yy >= H || xx < 0 || xx >= W) continue;
-      acc += g[p * ld + o] * __ldg(in + ((n * cin + ci) * H + yy) * W + xx);
-    }
+    for (int r = 0; r < np; ++r) acc += gs[r * c0 + o] * xs[r * nt + t];
     wpart[static_cast<int64_t>(blockIdx.x) * nw + wi] = acc;
   }
 }
@@ -95,22 +118,23 @@ __global__ void k_trans_pool(const float* __restrict__ feat, int64_t N, int H, i
                              const float* __restrict__ gamma, const float* __restrict__ beta,
                              float* __restrict__ P) {
   pdl_enter();
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= C) return;
   const int Ho = H / 2, Wo = W / 2;
-  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (i >= N * Ho * Wo * C) return;
-  const int c = static_cast<int>(i % C);
-  const int64_t q = i / C;
-  const int64_t n = q / (static_cast<int64_t>(Ho) * Wo);
-  const int r = static_cast<int>(q - n * Ho * Wo);
-  const int oy = r / Wo, ox = r - (r / Wo) * Wo;
-  const float inv = bn_inv(var[c]);
-  float acc = 0.f;
-  for (int ky = 0; ky < 2; ++ky)
-    for (int kx = 0; kx < 2; ++kx) {
-      const int64_t p = (n * H + 2 * oy + ky) * W + 2 * ox + kx;
-      acc += fmaxf(bn_ref(feat[p * C + c], mean[c], inv, gamma[c], beta[c]), 0.f);
-    }
-  P[i] = acc * 0.25f;
+  const float mu = mean[c], inv = bn_inv(var[c]), ga = gamma[c], be = beta[c];
+  const int64_t Mq = N * Ho * Wo;
+  for (int64_t q = blockIdx.y; q < Mq; q += gridDim.y) {
+    const int n = static_cast<int>(q / (Ho * Wo));
+    const int r = static_cast<int>(q - static_cast<int64_t>(n) * Ho * Wo);
+    const int oy = r / Wo, ox = r - (r / Wo) * Wo;
+    const int64_t p = (static_cast<int64_t>(n) * H + 2 * oy) * W + 2 * ox;
+    float acc = 0.f;
+    acc += fmaxf(bn_ref(feat[p * C + c], mu, inv, ga, be), 0.f);
+    acc += fmaxf(bn_ref(feat[(p + 1) * C + c], mu, inv, ga, be), 0.f);
+    acc += fmaxf(bn_ref(feat[(p + W) * C + c], mu, inv, ga, be), 0.f);
+    acc += fmaxf(bn_ref(feat[(p + W + 1) * C + c], mu, inv, ga, be), 0.f);
+    P[q * C + c] = acc * 0.25f;
+  }
 }
 
 // running statistics momentum update from a block's batch statistics (biased var)
@@ -201,10 +225,14 @@ __global__ void k_head_loss(const float* __restrict__ gap, int64_t N, int C, con
   __shared__ float red[256];
   const int64_t n = blockIdx.x;
   float* lg = logits + n * classes;
-  for (int o = threadIdx.x; o < classes; o += blockDim.x) {
-    float acc = bl[o];
-    for (int c = 0; c < C; ++c) acc += Wl[static_cast<int64_t>(o) * C + c] * gap[n * C + c];
-    lg[o] = acc;
+  // one warp per class: lanes stride over C (coalesced), fixed butterfly
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32, nwarps = blockDim.x / 32;
+  for (int o = warp; o < classes; o += nwarps) {
+    float acc = 0.f;
+    for (int c = lane; c < C; c += 32) acc += Wl[static_cast<int64_t>(o) * C + c] * gap[n * C + c];
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
+    if (lane == 0) lg[o] = bl[o] + acc;
   }
   __syncthreads();
   // max and sum of exp, fixed-order tree over the CTA
@@ -283,19 +311,19 @@ struct HeadGrad {
   const float* g_gap;
   int HW, C;
   __device__ float operator()(int64_t p, int c) const {
-    return g_gap[(p / HW) * C + c] * (1.f / static_cast<float>(HW));
+    return g_gap[static_cast<int64_t>(static_cast<int>(p / HW)) * C + c] * (1.f / static_cast<float>(HW));
   }
 };
 struct PoolGrad {
   const float* g_P;  // [N*Ho*Wo, C]
   int H, W, C;
   __device__ float operator()(int64_t p, int c) const {
-    const int Ho = H / 2, Wo = W / 2;
-    const int64_t n = p / (static_cast<int64_t>(H) * W);
-    const int r = static_cast<int>(p - n * H * W);
+    const int Ho = H / 2, Wo = W / 2, hw = H * W;
+    const int n = static_cast<int>(p / hw);
+    const int r = static_cast<int>(p - static_cast<int64_t>(n) * hw);
     const int y = r / W, x = r - (r / W) * W;
     if (y >= 2 * Ho || x >= 2 * Wo) return 0.f;
-    return g_P[((n * Ho + y / 2) * Wo + x / 2) * C + c] * 0.25f;
+    return g_P[((static_cast<int64_t>(n) * Ho + y / 2) * Wo + x / 2) * C + c] * 0.25f;
   }
 };
 
@@ -312,6 +340,7 @@ __global__ void k_bnb_partials(const float* __restrict__ feat, int64_t M, int C,
   const int64_t p0 = static_cast<int64_t>(blockIdx.x) * chunk;
   const int64_t p1 = p0 + chunk < M ? p0 + chunk : M;
   double s1 = 0.0, s2 = 0.0;
+#pragma unroll 4
   for (int64_t p = p0; p < p1; ++p) {
     const float x = feat[p * C + c];
     if (!(bn_ref(x, mean[c], inv, gamma[c], beta[c]) > 0.f)) continue;  // relu_backward
@@ -322,22 +351,24 @@ __global__ void k_bnb_partials(const float* __restrict__ feat, int64_t M, int C,
   part[static_cast<int64_t>(blockIdx.x) * C + c] = make_double2(s1, s2);
 }
 
-// out[p][c] = (gamma*inv) * (g - mg - xhat*mgx)  (written, ops.hpp:232-241)
+// out[p][c] = (gamma*inv) * (g - mg - xhat*mgx)  (written, ops.hpp:232-241);
+// thread = channel (coalesced), grid.y strides over pixels
 template <class G>
 __global__ void k_bnb_apply(const float* __restrict__ feat, int64_t M, int C, const float* __restrict__ mean,
                             const float* __restrict__ var, const float* __restrict__ gamma,
                             const float* __restrict__ beta, G up, const float* __restrict__ coef,
                             float* __restrict__ out) {
   pdl_enter();
-  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (i >= M * C) return;
-  const int c = static_cast<int>(i % C);
-  const int64_t p = i / C;
-  const float x = feat[i];
-  const float inv = bn_inv(var[c]);
-  const float g = bn_ref(x, mean[c], inv, gamma[c], beta[c]) > 0.f ? up(p, c) : 0.f;
-  const float xh = (x - mean[c]) * inv;
-  out[i] = gamma[c] * inv * (g - coef[2 * c] - xh * coef[2 * c + 1]);
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= C) return;
+  const float mu = mean[c], inv = bn_inv(var[c]), ga = gamma[c], be = beta[c];
+  const float gi = ga * inv, mg = coef[2 * c], mgx = coef[2 * c + 1];
+  for (int64_t p = blockIdx.y; p < M; p += gridDim.y) {
+    const float x = feat[p * C + c];
+    const float g = bn_ref(x, mu, inv, ga, be) > 0.f ? up(p, c) : 0.f;
+    const float xh = (x - mu) * inv;
+    out[p * C + c] = gi * (g - mg - xh * mgx);
+  }
 }
 
 unsigned blocks_of(int64_t n, int t) { return static_cast<unsigned>((n + t - 1) / t); }
@@ -383,13 +414,15 @@ struct dpb_model {
 namespace dpb {
 namespace {
 
-constexpr int kSplitsMax = 148;
+constexpr int kSplitsMax = 148;      // split-K of the transition dW GEMM
+constexpr int kRowSplitsMax = 2048;  // pixel chunks of the BN-backward sums and the stem dW
 
 int model_geometry(const dpb_model_desc* d, dpb_model* m) {
   if (d == nullptr) return fail(DPB_CONFIG_ERROR, "null model descriptor");
   if (d->nblocks < 1 || d->nblocks > 8) return fail(DPB_CONFIG_ERROR, "nblocks must be in [1, 8]");
   if (d->k < 1 || d->c0 < 1 || d->classes < 1 || d->in_c < 1 || d->batch < 1)
     return fail(DPB_SHAPE_ERROR, "invalid network geometry");
+  if (d->in_c > 4) return fail(DPB_CONFIG_ERROR, "the 3x3 stem supports at most 4 input channels");
   if (!(d->compression > 0.0) || d->compression > 1.0)
     return fail(DPB_CONFIG_ERROR, "compression must be in (0, 1]");
   if (d->dtype != DPB_FP32 && d->dtype != DPB_BF16) return fail(DPB_CONFIG_ERROR, "dtype");
@@ -528,10 +561,12 @@ DPB_API int dpb_model_create(const dpb_model_desc* desc, int device, void* strea
     wmax = std::max<int64_t>(wmax, static_cast<int64_t>(t.cout) * t.C);
     cmax = std::max<int64_t>(cmax, t.C);
   }
-  m->wpart_elems = kSplitsMax * wmax;
+  const int64_t stem_splits = (m->blocks[0].M + stem_chunk(desc->c0, desc->in_c) - 1) /
+                              stem_chunk(desc->c0, desc->in_c);
+  m->wpart_elems = std::max<int64_t>(kSplitsMax * wmax, stem_splits * desc->c0 * desc->in_c * 9);
   const int64_t o_wpart = take(m->wpart_elems);
-  m->part_rows = kSplitsMax;
-  const int64_t o_part = take(4 * kSplitsMax * cmax);  // double2 = 4 floats
+  m->part_rows = kRowSplitsMax;
+  const int64_t o_part = take(4 * kRowSplitsMax * cmax);  // double2 = 4 floats
   const int64_t o_coef = take(2 * cmax);
   const int64_t o_bad = take(1);
   e = cudaMalloc(&m->mem, static_cast<size_t>(bytes));
@@ -583,17 +618,17 @@ DPB_API int dpb_model_step(dpb_model* m, const float* input, const int32_t* labe
   cudaStream_t st = m->stream;
   const int64_t N = d.batch;
   const int nb = static_cast<int>(m->blocks.size());
-  // split-K of a reduction over `rows` pixels into at most kSplitsMax chunks
-  auto splits_of = [](int64_t rows, int64_t& chunk) {
-    const int64_t s = std::min<int64_t>(kSplitsMax, std::max<int64_t>(1, rows / 64));
-    chunk = (rows + s - 1) / s;
+  // split-K of a reduction over `rows` pixels into at most `smax` chunks of at
+  // least `min_chunk` rows (short per-thread chains, many CTAs)
+  auto splits_of = [](int64_t rows, int64_t& chunk, int64_t smax = kSplitsMax, int64_t min_chunk = 64) {
+    chunk = std::max<int64_t>(min_chunk, (rows + smax - 1) / smax);
     return static_cast<int>((rows + chunk - 1) / chunk);
   };
 
   // ---- forward --------------------------------------------------------------------
   ModelBlock& b0 = m->blocks[0];
-  launch(k_stem_fwd, blocks_of(b0.M, 256), 256, 0, st, input, N, d.in_c, d.in_h, d.in_w, params, d.c0, b0.x,
-         b0.c0);
+  launch(k_stem_fwd, blocks_of(b0.M, 256), 256, sizeof(float) * d.c0 * d.in_c * 9, st, input, N, d.in_c,
+         d.in_h, d.in_w, params, d.c0, b0.x, b0.c0);
   for (int b = 0; b < nb; ++b) {
     ModelBlock& mb = m->blocks[b];
     int rc = block_forward(mb.blk, mb.x, params + mb.poff, running + mb.roff, 1, 0);
@@ -604,8 +639,8 @@ DPB_API int dpb_model_step(dpb_model* m, const float* input, const int32_t* labe
     if (b + 1 < nb) {
       ModelTrans& t = m->trans[b];
       ModelBlock& nx = m->blocks[b + 1];
-      launch(k_trans_pool, blocks_of(t.Mq * t.C, 256), 256, 0, st, feat, N, mb.h, mb.w, t.C, mean, var,
-             params + t.gamma, params + t.beta, t.P);
+      launch(k_trans_pool, dim3(blocks_of(t.C, 128), static_cast<unsigned>(std::min<int64_t>(t.Mq, 65535))), 128,
+             0, st, feat, N, mb.h, mb.w, t.C, mean, var, params + t.gamma, params + t.beta, t.P);
       launch(k_gemm<false, true>, dim3(blocks_of(t.Mq, 64), blocks_of(t.cout, 64), 1), 256, 0, st,
              static_cast<int>(t.Mq), t.cout, t.C, static_cast<const float*>(t.P), t.C, params + t.w, t.C, nx.x,
              nx.c0, t.C);
@@ -636,12 +671,13 @@ DPB_API int dpb_model_step(dpb_model* m, const float* input, const int32_t* labe
     const float* var = mb.blk->fstat + mb.blk->g.C;
     HeadGrad up{m->g_gap, HW, C};
     int64_t chunk;
-    const int S = splits_of(mb.M, chunk);
+    const int S = splits_of(mb.M, chunk, kRowSplitsMax, 16);
     launch(k_bnb_partials<HeadGrad>, dim3(S, blocks_of(C, 256)), 256, 0, st, feat, mb.M, C, mean, var,
            params + m->head_gamma, params + m->head_beta, up, chunk, m->part);
     launch_finalize_bn_bwd(st, m->part, S, C, static_cast<double>(mb.M), grads + m->head_gamma,
                            grads + m->head_beta, m->coef);
-    launch(k_bnb_apply<HeadGrad>, blocks_of(mb.M * C, 256), 256, 0, st, feat, mb.M, C, mean, var,
+    launch(k_bnb_apply<HeadGrad>, dim3(blocks_of(C, 128), static_cast<unsigned>(std::min<int64_t>(mb.M, 65535))),
+           128, 0, st, feat, mb.M, C, mean, var,
            params + m->head_gamma, params + m->head_beta, up, static_cast<const float*>(m->coef), mb.acc);
   }
   for (int b = nb - 1; b >= 0; --b) {
@@ -665,18 +701,20 @@ DPB_API int dpb_model_step(dpb_model* m, const float* input, const int32_t* labe
       const float* mean = pv.blk->fstat;
       const float* var = pv.blk->fstat + pv.blk->g.C;
       PoolGrad up{t.gP, pv.h, pv.w, t.C};
-      const int S2 = splits_of(pv.M, chunk);
+      const int S2 = splits_of(pv.M, chunk, kRowSplitsMax, 16);
       launch(k_bnb_partials<PoolGrad>, dim3(S2, blocks_of(t.C, 256)), 256, 0, st, feat, pv.M, t.C, mean, var,
              params + t.gamma, params + t.beta, up, chunk, m->part);
       launch_finalize_bn_bwd(st, m->part, S2, t.C, static_cast<double>(pv.M), grads + t.gamma, grads + t.beta,
                              m->coef);
-      launch(k_bnb_apply<PoolGrad>, blocks_of(pv.M * t.C, 256), 256, 0, st, feat, pv.M, t.C, mean, var,
+      launch(k_bnb_apply<PoolGrad>,
+             dim3(blocks_of(t.C, 128), static_cast<unsigned>(std::min<int64_t>(pv.M, 65535))), 128, 0, st, feat,
+             pv.M, t.C, mean, var,
              params + t.gamma, params + t.beta, up, static_cast<const float*>(m->coef), pv.acc);
     } else {
-      int64_t chunk;
-      const int S = splits_of(mb.M, chunk);
-      launch(k_stem_wgrad, S, 256, 0, st, input, N, d.in_c, d.in_h, d.in_w, static_cast<const float*>(mb.acc),
-             mb.C, d.c0, chunk, m->wpart);
+      const int chunk = stem_chunk(d.c0, d.in_c);
+      const int S = static_cast<int>((mb.M + chunk - 1) / chunk);
+      launch(k_stem_wgrad, S, 256, sizeof(float) * chunk * (d.c0 + d.in_c * 9), st, input, N, d.in_c,
+             d.in_h, d.in_w, static_cast<const float*>(mb.acc), mb.C, d.c0, m->wpart);
       launch_fold_splits(st, m->wpart, S, static_cast<int64_t>(d.c0) * d.in_c * 9, grads);
     }
   }

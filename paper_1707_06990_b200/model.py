@@ -129,6 +129,46 @@ class ModelPlan:
         check(lib().dpb_model_create(C.byref(d), self.device, s, C.byref(h)))
         self._h = h
 
+    def param_segments(self) -> list[tuple[str, int, int]]:
+        """(name, elements, fan_in) of every parameter tensor in registration
+        order; fan_in 0 marks BN gamma (1) / beta and the linear bias (0)."""
+        cfg = self.cfg
+        k, bk, in_c = cfg.growth_rate, 4 * cfg.growth_rate, cfg.in_shape[0]
+        segs = [("stem.w", cfg.c0 * in_c * 9, in_c * 9)]
+        shapes = cfg.block_shapes(self.batch)
+        for b, shp in enumerate(shapes):
+            for l in range(shp.m):
+                c = shp.c_in(l)
+                segs += [(f"b{b}.l{l}.bn_a.gamma", c, 0), (f"b{b}.l{l}.bn_a.beta", c, 0),
+                         (f"b{b}.l{l}.conv_a.w", bk * c, c), (f"b{b}.l{l}.bn_b.gamma", bk, 0),
+                         (f"b{b}.l{l}.bn_b.beta", bk, 0), (f"b{b}.l{l}.conv_b.w", k * bk * 9, bk * 9)]
+            C_ = shp.c_out
+            if b + 1 < len(shapes):
+                cout = int(np.floor(cfg.compression * C_))
+                segs += [(f"t{b}.bn.gamma", C_, 0), (f"t{b}.bn.beta", C_, 0), (f"t{b}.conv.w", cout * C_, C_)]
+            else:
+                segs += [("head.bn.gamma", C_, 0), ("head.bn.beta", C_, 0),
+                         ("head.linear.w", cfg.num_classes * C_, -C_), ("head.linear.b", cfg.num_classes, 0)]
+        return segs
+
+    def init_params(self, seed: int = 0, device="cuda"):
+        """Parameters drawn like GraphPlan::build (graph.hpp:351-390, 582-590):
+        He-normal convs, BN gamma 1 / beta 0, classifier N(0, 1/C), bias 0
+        (the distributions, not the reference's Rng stream)."""
+        import torch
+        g = torch.Generator(device="cpu").manual_seed(seed)
+        parts = []
+        for name, n, fan in self.param_segments():
+            if fan > 0:
+                parts.append(torch.randn(n, generator=g) * float(np.sqrt(2.0 / fan)))
+            elif fan < 0:
+                parts.append(torch.randn(n, generator=g) * float(np.sqrt(1.0 / -fan)))
+            else:
+                parts.append(torch.ones(n) if name.endswith("gamma") else torch.zeros(n))
+        out = torch.cat(parts)
+        assert out.numel() == self.param_elems
+        return out.to(device)
+
     def initial_running(self, device="cuda"):
         """Running means 0 / variances 1 in the model's running layout."""
         import torch

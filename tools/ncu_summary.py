@@ -26,6 +26,10 @@ CATEGORIES = [
     ("Tc3x3DgradHalo", "conv3x3_dgrad"), ("Tc3x3Dgrad", "conv3x3_dgrad"),
     ("Tc3x3FwdHalo", "conv3x3_fwd"), ("Tc3x3Fwd", "conv3x3_fwd"), ("Conv3x3Fwd", "conv3x3_fwd"),
     ("Tc1x1Dgrad", "conv1x1_dgrad"), ("Tc1x1Wgrad", "conv1x1_wgrad"),
+    ("Dgrad1x1", "conv1x1_dgrad"), ("Wgrad1x1", "conv1x1_wgrad"),
+    ("k_stem", "model: stem"), ("k_trans_pool", "model: transition fwd"), ("k_gemm", "model: transition GEMMs"),
+    ("k_bnb_", "model: transition/head BN bwd"), ("k_head", "model: head"), ("k_loss", "model: head"),
+    ("k_running", "model: running stats"),
     ("Fwd1x1", "conv1x1_fwd"), ("Tc1x1Fwd", "conv1x1_fwd"),
     ("Conv3x3Dgrad", "conv3x3_dgrad"), ("Conv3x3Wgrad", "conv3x3_wgrad"),
     ("Conv1x1Dgrad", "conv1x1_dgrad"), ("Conv1x1Wgrad", "conv1x1_wgrad"), ("Conv1x1Fwd", "conv1x1_fwd"),
