@@ -330,7 +330,9 @@ def main():
         m_x = torch.randn(BATCH, *cfg.in_shape, generator=g).to(dev)
         m_labels = (torch.arange(BATCH, dtype=torch.int32) % cfg.num_classes).to(dev)
         m_grads = torch.empty(mplan.param_elems, device=dev)
+        m_vel = torch.zeros(mplan.param_elems, device=dev)
         m_loss = torch.zeros(1, device=dev)
+        from paper_1707_06990_b200.ops import sgd_step
 
         def model_step():
             mplan.step(m_x, m_labels, m_params, m_run, m_grads, m_loss)
@@ -339,6 +341,8 @@ def main():
             if world > 1:   # DP allreduce of the flat gradients (per-GPU BN), outside the graph
                 dist.all_reduce(m_grads)
                 m_grads.mul_(1.0 / world)
+            # momentum SGD + weight decay on the averaged gradients (train.hpp:43-70)
+            sgd_step(m_params, m_grads, m_vel, lr=0.1, momentum=0.9, weight_decay=1e-4, stream=stream)
 
         with torch.cuda.stream(stream):
             for _ in range(args.warmup):
@@ -366,8 +370,8 @@ def main():
             return ncu_step_and_exit(model_timed, "whole network")
         ms_per_step, clk = time_steps(model_timed)
         value = BATCH * world / (ms_per_step / 1000.0)
-        # block launches + stem / transitions / head kernels of dpb_model_step
-        launches_per_step += 11 + 9 * (len(cfg.block_sizes) - 1)
+        # block launches + stem / transitions / head kernels of dpb_model_step + SGD
+        launches_per_step += 11 + 9 * (len(cfg.block_sizes) - 1) + 1
     else:
         ms_per_step, clk, value = blocks_ms, blocks_clk, blocks_value
 
@@ -535,7 +539,7 @@ def main():
             "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": args.dtype, "data": "synthetic",
             "config": {"workload": (f"DenseNet-{args.config} full training step: stem, dense blocks, transitions, "
-                                    f"head, softmax-xent, fwd+bwd" if whole else
+                                    f"head, softmax-xent, fwd+bwd, momentum-SGD update" if whole else
                                     f"DenseNet-{args.config} dense blocks, fwd+bwd (the {cfg.in_shape[1]}px "
                                     f"7x7/2 stem is not built)"),
                        "model": args.config, "global_batch": BATCH * world,

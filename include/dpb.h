@@ -274,6 +274,17 @@ DPB_API int dpb_model_step(dpb_model* model, const float* input, const int32_t* 
                            const float* params, float* running, float* grads, float* loss);
 DPB_API int dpb_model_sync(dpb_model* model);
 
+/* ---- optimizer -------------------------------------------
+ * dpb_sgd_step replaces sgd_step (train.hpp:43-70) over a flat fp32 buffer:
+ *   d = g + wd*p;  v = mu*v + d;  p -= lr * (nesterov ? d + mu*v : v)
+ * bit-identical to the reference's float loop; device pointers, async on
+ * `stream`.  dpb_lr_at replaces lr_at (schedule.hpp:46-62): kind 0 = step
+ * (milestones, factor), 1 = cosine (floor); RangeError outside [0, epochs). */
+DPB_API int dpb_sgd_step(float* params, const float* grads, float* velocity, int64_t n, double lr,
+                         double momentum, double weight_decay, int nesterov, void* stream);
+DPB_API int dpb_lr_at(int kind, double base_lr, int total_epochs, const int32_t* milestones,
+                      int nmilestones, double factor, double floor_lr, int epoch, double* out);
+
 #ifdef __cplusplus
 }
 #endif

@@ -94,6 +94,11 @@ def ref_lib(fast: bool = False):
         L.ref_model_step_f32.argtypes = cfg + [C.c_int] * 3 + [_I64, C.c_uint64, C.c_int, _P, _P, _P]
         L.ref_model_params_f32.restype = C.c_int
         L.ref_model_params_f32.argtypes = cfg + [C.c_int] * 3 + [_I64, C.c_uint64, _P, _P]
+        L.ref_sgd_step_f32.restype = C.c_int
+        L.ref_sgd_step_f32.argtypes = [_P, _P, _P, _I64, C.c_double, C.c_double, C.c_double, C.c_int]
+        L.ref_lr_at.restype = C.c_int
+        L.ref_lr_at.argtypes = [C.c_int, C.c_double, C.c_int, _P, C.c_int, C.c_double, C.c_double, C.c_int,
+                                C.POINTER(C.c_double)]
         L.ref_rng_normal.argtypes = [C.c_uint64, _I64, _P]
         L.ref_rng_u64.argtypes = [C.c_uint64, _I64, _P]
         L.ref_count_parameters.restype = C.c_int64
@@ -372,3 +377,44 @@ def ref_model_step(blocks, k, bottleneck, compression, classes, c0, in_shape, se
     if rc != 0:
         raise RuntimeError(L.ref_last_error().decode())
     return loss.value, secs.value
+
+
+# ---- optimizer -------------------------------------------------------
+def sgd_step(p, g, v, lr, momentum, weight_decay, nesterov):
+    """train.hpp:43-70 restated in float32 numpy (every op rounded, no FMA):
+    d = g + wd*p; v = mu*v + d; p -= lr*(nesterov ? d + mu*v : v).  In place."""
+    f = np.float32
+    mu, wd, eta = f(momentum), f(weight_decay), f(lr)
+    d = g + wd * p
+    v[:] = mu * v + d
+    p -= eta * ((d + mu * v) if nesterov else v)
+
+
+def ref_sgd_step(p, g, v, lr, momentum, weight_decay, nesterov):
+    """The reference's own sgd_step (oracle/_ref), in place."""
+    rc = ref_lib().ref_sgd_step_f32(_ptr(p), _ptr(g), _ptr(v), p.size, lr, momentum, weight_decay, int(nesterov))
+    if rc != 0:
+        raise RuntimeError(ref_lib().ref_last_error().decode())
+
+
+def lr_at(kind, base_lr, total_epochs, epoch, milestones=(), factor=0.1, floor=0.0):
+    """schedule.hpp:46-62 restated."""
+    if not 0 <= epoch < total_epochs:
+        raise ValueError("epoch out of range")
+    if kind == "cosine":
+        return floor + (base_lr - floor) / 2.0 * (np.cos(np.pi * epoch / total_epochs) + 1.0)
+    lr = base_lr
+    for m in milestones:
+        if epoch >= m:
+            lr *= factor
+    return lr
+
+
+def ref_lr_at(kind, base_lr, total_epochs, epoch, milestones=(), factor=0.1, floor=0.0):
+    arr = (C.c_int * max(1, len(milestones)))(*milestones)
+    out = C.c_double()
+    rc = ref_lib().ref_lr_at({"step": 0, "cosine": 1}[kind], base_lr, total_epochs, C.cast(arr, C.c_void_p),
+                             len(milestones), factor, floor, epoch, C.byref(out))
+    if rc != 0:
+        raise RuntimeError(ref_lib().ref_last_error().decode())
+    return out.value

@@ -25,6 +25,8 @@
 #include "denseplan/errors.hpp"
 #include "denseplan/graph.hpp"
 #include "denseplan/ops.hpp"
+#include "denseplan/schedule.hpp"
+#include "denseplan/train.hpp"
 #include "denseplan/peak_model.hpp"
 #include "denseplan/rng.hpp"
 #include "denseplan/tensor.hpp"
@@ -489,6 +491,40 @@ int ref_model_step_f32(int nblocks, const int* blocks, int k, int bottleneck,
         off += static_cast<std::size_t>(p.grad.elems());
       }
     }
+  });
+}
+
+// The reference's sgd_step (train.hpp:43-70) over one flat parameter of n
+// elements: params / velocity updated in place from grads.
+int ref_sgd_step_f32(float* params, const float* grads, float* velocity, std::int64_t n, double lr,
+                     double momentum, double weight_decay, int nesterov) {
+  return guarded([&] {
+    MemoryTracker tr;
+    std::vector<ParamEntry<float>> reg;
+    reg.push_back({"p", from_flat(params, Shape4{1, n, 1, 1}, tr), from_flat(grads, Shape4{1, n, 1, 1}, tr)});
+    OptimizerState<float> opt = OptimizerState<float>::create(reg);
+    std::memcpy(opt.velocity[0].data(), velocity, sizeof(float) * static_cast<std::size_t>(n));
+    opt.momentum = momentum;
+    opt.weight_decay = weight_decay;
+    opt.nesterov = nesterov != 0;
+    sgd_step(reg, opt, lr);
+    to_flat(reg[0].value, params);
+    to_flat(opt.velocity[0], velocity);
+  });
+}
+
+// lr_at (schedule.hpp:46-62): kind 0 = Step (milestones, factor), 1 = Cosine (floor).
+int ref_lr_at(int kind, double base_lr, int total_epochs, const int* milestones, int nmilestones,
+              double factor, double floor, int epoch, double* out) {
+  return guarded([&] {
+    LrSchedule s;
+    s.kind = kind == 1 ? ScheduleKind::Cosine : ScheduleKind::Step;
+    s.base_lr = base_lr;
+    s.total_epochs = total_epochs;
+    s.milestones.assign(milestones, milestones + nmilestones);
+    s.factor = factor;
+    s.floor = floor;
+    *out = lr_at(s, epoch);
   });
 }
 

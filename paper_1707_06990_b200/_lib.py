@@ -84,6 +84,9 @@ SIGNATURES = {
     "dpb_model_destroy": (None, [_P]),
     "dpb_model_step": (C.c_int, [_P, _P, _P, _P, _P, _P, _P]),
     "dpb_model_sync": (C.c_int, [_P]),
+    "dpb_sgd_step": (C.c_int, [_P, _P, _P, _I64, C.c_double, C.c_double, C.c_double, C.c_int, _P]),
+    "dpb_lr_at": (C.c_int, [C.c_int, C.c_double, C.c_int, _P, C.c_int, C.c_double, C.c_double, C.c_int,
+                            C.POINTER(C.c_double)]),
 }
 
 _lib = None

@@ -72,3 +72,29 @@ def conv2d_backward(grad_y, x, weights, padding: int, need_grad_x: bool = True):
     check(lib().dpb_op_conv2d_backward(_ptr(grad_y), _ptr(x), n, cin, h, w, _ptr(weights), cout, kh,
                                        padding, _ptr(gx), _ptr(gw), _stream()))
     return gx, gw
+
+
+# ---- optimizer (train.hpp:43-70, schedule.hpp:46-62) -----------------------------------
+def sgd_step(params, grads, velocity, lr: float, momentum: float = 0.9, weight_decay: float = 1e-4,
+             nesterov: bool = False, stream=None) -> None:
+    """In-place momentum SGD over flat fp32 CUDA tensors (dpb_sgd_step)."""
+    import ctypes as C
+    n = params.numel()
+    if grads.numel() != n or velocity.numel() != n:
+        raise ValueError("params / grads / velocity sizes differ")
+    s = None if stream is None else C.c_void_p(stream.cuda_stream)
+    check(lib().dpb_sgd_step(C.c_void_p(params.data_ptr()), C.c_void_p(grads.data_ptr()),
+                             C.c_void_p(velocity.data_ptr()), n, float(lr), float(momentum),
+                             float(weight_decay), int(nesterov), s))
+
+
+def lr_at(kind: str, base_lr: float, total_epochs: int, epoch: int, milestones=(), factor: float = 0.1,
+          floor: float = 0.0) -> float:
+    """Learning rate of `epoch` for a step ("step") or cosine ("cosine") schedule."""
+    import ctypes as C
+    arr = (C.c_int32 * max(1, len(milestones)))(*milestones)
+    out = C.c_double()
+    check(lib().dpb_lr_at({"step": 0, "cosine": 1}[kind], float(base_lr), int(total_epochs),
+                          C.cast(arr, C.c_void_p), len(milestones), float(factor), float(floor), int(epoch),
+                          C.byref(out)))
+    return out.value
