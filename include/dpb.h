@@ -285,6 +285,18 @@ DPB_API int dpb_sgd_step(float* params, const float* grads, float* velocity, int
 DPB_API int dpb_lr_at(int kind, double base_lr, int total_epochs, const int32_t* milestones,
                       int nmilestones, double factor, double floor_lr, int epoch, double* out);
 
+/* ---- DPLN checkpoints ---------------------------------------
+ * save_checkpoint / load_checkpoint (checkpoint.hpp:121-198), fp32: `count`
+ * entries with NUL-terminated names, dims[4*i .. 4*i+3] = (n, c, h, w) and
+ * their elements concatenated in `data` (HOST memory).  Training checkpoints
+ * (train.hpp:149-172) are the parameters in registration order followed by
+ * "velocity.<name>" for each.  Load validates magic, version, element size,
+ * count, names, shapes and the CRC-32 (FormatError otherwise). */
+DPB_API int dpb_checkpoint_save(const char* path, int count, const char* const* names, const int64_t* dims,
+                                const float* data, int epoch);
+DPB_API int dpb_checkpoint_load(const char* path, int count, const char* const* names, const int64_t* dims,
+                                float* data, int* epoch);
+
 #ifdef __cplusplus
 }
 #endif

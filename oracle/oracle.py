@@ -94,6 +94,8 @@ def ref_lib(fast: bool = False):
         L.ref_model_step_f32.argtypes = cfg + [C.c_int] * 3 + [_I64, C.c_uint64, C.c_int, _P, _P, _P]
         L.ref_model_params_f32.restype = C.c_int
         L.ref_model_params_f32.argtypes = cfg + [C.c_int] * 3 + [_I64, C.c_uint64, _P, _P]
+        L.ref_save_training_checkpoint.restype = C.c_int
+        L.ref_save_training_checkpoint.argtypes = cfg + [C.c_int] * 3 + [_I64, C.c_uint64, C.c_char_p, C.c_int]
         L.ref_sgd_step_f32.restype = C.c_int
         L.ref_sgd_step_f32.argtypes = [_P, _P, _P, _I64, C.c_double, C.c_double, C.c_double, C.c_int]
         L.ref_lr_at.restype = C.c_int
@@ -418,3 +420,12 @@ def ref_lr_at(kind, base_lr, total_epochs, epoch, milestones=(), factor=0.1, flo
     if rc != 0:
         raise RuntimeError(ref_lib().ref_last_error().decode())
     return out.value
+
+
+def ref_save_training_checkpoint(blocks, k, compression, classes, c0, in_shape, seed, path, epoch):
+    """The reference writes a DPLN training checkpoint (velocities 0.5 * params)."""
+    args, keep = _cfg_args(blocks, k, 1, compression, classes, c0)
+    n, c, h, w = in_shape
+    rc = ref_lib().ref_save_training_checkpoint(*args, c, h, w, n, seed, path.encode(), epoch)
+    if rc != 0:
+        raise RuntimeError(ref_lib().ref_last_error().decode())

@@ -513,6 +513,24 @@ int ref_sgd_step_f32(float* params, const float* grads, float* velocity, std::in
   });
 }
 
+// The reference's save_training_checkpoint (train.hpp:157-162) of a fresh
+// GraphPlan (seed) with velocities v_i = 0.5 * p_i.
+int ref_save_training_checkpoint(int nblocks, const int* blocks, int k, int bottleneck, double compression,
+                                 int classes, int c0, int in_c, int in_h, int in_w, std::int64_t batch,
+                                 std::uint64_t seed, const char* path, int epoch) {
+  return guarded([&] {
+    const DenseNetConfig cfg = model_cfg(nblocks, blocks, k, bottleneck, compression, classes, c0);
+    GraphPlan<float> plan =
+        GraphPlan<float>::build(cfg, ExecutionStrategy::SharedAll, Shape4{batch, in_c, in_h, in_w}, seed);
+    OptimizerState<float> opt = OptimizerState<float>::create(plan.params());
+    for (std::size_t i = 0; i < opt.velocity.size(); ++i) {
+      const Tensor<float>& p = plan.params()[i].value;
+      for (std::int64_t j = 0; j < p.elems(); ++j) opt.velocity[i].data()[j] = 0.5f * p.data()[j];
+    }
+    save_training_checkpoint(path, plan, opt, epoch);
+  });
+}
+
 // lr_at (schedule.hpp:46-62): kind 0 = Step (milestones, factor), 1 = Cosine (floor).
 int ref_lr_at(int kind, double base_lr, int total_epochs, const int* milestones, int nmilestones,
               double factor, double floor, int epoch, double* out) {

@@ -87,6 +87,8 @@ SIGNATURES = {
     "dpb_sgd_step": (C.c_int, [_P, _P, _P, _I64, C.c_double, C.c_double, C.c_double, C.c_int, _P]),
     "dpb_lr_at": (C.c_int, [C.c_int, C.c_double, C.c_int, _P, C.c_int, C.c_double, C.c_double, C.c_int,
                             C.POINTER(C.c_double)]),
+    "dpb_checkpoint_save": (C.c_int, [C.c_char_p, C.c_int, _P, _P, _P, C.c_int]),
+    "dpb_checkpoint_load": (C.c_int, [C.c_char_p, C.c_int, _P, _P, _P, C.POINTER(C.c_int)]),
 }
 
 _lib = None

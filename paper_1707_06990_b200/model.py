@@ -92,6 +92,85 @@ CONFIGS = {
 }
 
 
+def param_segments(cfg: DenseNetConfig) -> list[tuple[str, int, int]]:
+    """(name, elements, fan_in) of every parameter tensor in registration
+    order; fan_in 0 marks BN gamma (1) / beta and the linear bias (0)."""
+    k, bk, in_c = cfg.growth_rate, 4 * cfg.growth_rate, cfg.in_shape[0]
+    segs = [("stem.conv.w", cfg.c0 * in_c * 9, in_c * 9)]
+    shapes = cfg.block_shapes(1)
+    for b, shp in enumerate(shapes):
+        for l in range(shp.m):
+            c = shp.c_in(l)
+            segs += [(f"b{b}.l{l}.bn_a.gamma", c, 0), (f"b{b}.l{l}.bn_a.beta", c, 0),
+                     (f"b{b}.l{l}.conv_a.w", bk * c, c), (f"b{b}.l{l}.bn_b.gamma", bk, 0),
+                     (f"b{b}.l{l}.bn_b.beta", bk, 0), (f"b{b}.l{l}.conv_b.w", k * bk * 9, bk * 9)]
+        C_ = shp.c_out
+        if b + 1 < len(shapes):
+            cout = int(np.floor(cfg.compression * C_))
+            segs += [(f"t{b}.bn.gamma", C_, 0), (f"t{b}.bn.beta", C_, 0), (f"t{b}.conv.w", cout * C_, C_)]
+        else:
+            segs += [("head.bn.gamma", C_, 0), ("head.bn.beta", C_, 0),
+                     ("head.linear.w", cfg.num_classes * C_, -C_), ("head.linear.b", cfg.num_classes, 0)]
+    return segs
+
+def param_shapes(cfg: DenseNetConfig) -> list[tuple[str, tuple]]:
+    """(registered name, (n, c, h, w)) of every parameter (graph.hpp:351-390,
+    :430-600), in registration order."""
+    k, bk, in_c = cfg.growth_rate, 4 * cfg.growth_rate, cfg.in_shape[0]
+    out = []
+    for name, n, fan in param_segments(cfg):
+        if name == "stem.conv.w":
+            shape = (cfg.c0, in_c, 3, 3)
+        elif name.endswith(".conv_b.w"):
+            shape = (k, bk, 3, 3)
+        elif name.endswith(".conv_a.w"):
+            shape = (bk, n // bk, 1, 1)
+        elif name.endswith(".conv.w"):
+            shape = (n // fan, fan, 1, 1)
+        elif name == "head.linear.w":
+            shape = (cfg.num_classes, n // cfg.num_classes, 1, 1)
+        else:  # bn gamma / beta, linear bias
+            shape = (1, n, 1, 1)
+        assert int(np.prod(shape)) == n, name
+        out.append((name, shape))
+    return out
+
+def _ckpt_tables(cfg: DenseNetConfig, with_velocity: bool):
+    entries = param_shapes(cfg)
+    if with_velocity:
+        entries = entries + [("velocity." + n, s) for n, s in entries]
+    names = (C.c_char_p * len(entries))(*[n.encode() for n, _ in entries])
+    dims = np.array([s for _, s in entries], dtype=np.int64).reshape(-1)
+    return entries, names, dims
+
+def save_checkpoint(cfg: DenseNetConfig, path: str, params, velocity=None, epoch: int = 0) -> None:
+    """DPLN checkpoint of the parameters (+ SGD velocities as a training
+    checkpoint, train.hpp:149-172); device or host tensors."""
+    import torch
+    entries, names, dims = _ckpt_tables(cfg, velocity is not None)
+    data = params.detach().float().cpu()
+    if velocity is not None:
+        data = torch.cat([data, velocity.detach().float().cpu()])
+    data = np.ascontiguousarray(data.numpy())
+    check(lib().dpb_checkpoint_save(path.encode(), len(entries), C.cast(names, C.c_void_p),
+                                    dims.ctypes.data, data.ctypes.data, int(epoch)))
+
+def load_checkpoint(cfg: DenseNetConfig, path: str, with_velocity: bool = False):
+    """Returns (params, velocity or None, epoch) as host fp32 tensors."""
+    import torch
+    entries, names, dims = _ckpt_tables(cfg, with_velocity)
+    pe = sum(n for _, n, _ in param_segments(cfg))
+    n = pe * (2 if with_velocity else 1)
+    data = np.zeros(n, dtype=np.float32)
+    ep = C.c_int()
+    check(lib().dpb_checkpoint_load(path.encode(), len(entries), C.cast(names, C.c_void_p),
+                                    dims.ctypes.data, data.ctypes.data, C.byref(ep)))
+    t = torch.from_numpy(data)
+    if with_velocity:
+        return t[:pe].clone(), t[pe:].clone(), ep.value
+    return t, None, ep.value
+
+
 class ModelPlan:
     """Whole-network training step on the GPU (``dpb_model_*``): the stem,
     dense blocks, transitions, head and softmax cross-entropy of
@@ -130,26 +209,16 @@ class ModelPlan:
         self._h = h
 
     def param_segments(self) -> list[tuple[str, int, int]]:
-        """(name, elements, fan_in) of every parameter tensor in registration
-        order; fan_in 0 marks BN gamma (1) / beta and the linear bias (0)."""
-        cfg = self.cfg
-        k, bk, in_c = cfg.growth_rate, 4 * cfg.growth_rate, cfg.in_shape[0]
-        segs = [("stem.w", cfg.c0 * in_c * 9, in_c * 9)]
-        shapes = cfg.block_shapes(self.batch)
-        for b, shp in enumerate(shapes):
-            for l in range(shp.m):
-                c = shp.c_in(l)
-                segs += [(f"b{b}.l{l}.bn_a.gamma", c, 0), (f"b{b}.l{l}.bn_a.beta", c, 0),
-                         (f"b{b}.l{l}.conv_a.w", bk * c, c), (f"b{b}.l{l}.bn_b.gamma", bk, 0),
-                         (f"b{b}.l{l}.bn_b.beta", bk, 0), (f"b{b}.l{l}.conv_b.w", k * bk * 9, bk * 9)]
-            C_ = shp.c_out
-            if b + 1 < len(shapes):
-                cout = int(np.floor(cfg.compression * C_))
-                segs += [(f"t{b}.bn.gamma", C_, 0), (f"t{b}.bn.beta", C_, 0), (f"t{b}.conv.w", cout * C_, C_)]
-            else:
-                segs += [("head.bn.gamma", C_, 0), ("head.bn.beta", C_, 0),
-                         ("head.linear.w", cfg.num_classes * C_, -C_), ("head.linear.b", cfg.num_classes, 0)]
-        return segs
+        return param_segments(self.cfg)
+
+    def param_shapes(self) -> list[tuple[str, tuple]]:
+        return param_shapes(self.cfg)
+
+    def save_checkpoint(self, path: str, params, velocity=None, epoch: int = 0) -> None:
+        save_checkpoint(self.cfg, path, params, velocity, epoch)
+
+    def load_checkpoint(self, path: str, with_velocity: bool = False):
+        return load_checkpoint(self.cfg, path, with_velocity)
 
     def init_params(self, seed: int = 0, device="cuda"):
         """Parameters drawn like GraphPlan::build (graph.hpp:351-390, 582-590):
