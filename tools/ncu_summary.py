@@ -29,7 +29,7 @@ CATEGORIES = [
     ("Dgrad1x1", "conv1x1_dgrad"), ("Wgrad1x1", "conv1x1_wgrad"),
     ("k_stem", "model: stem"), ("k_trans_pool", "model: transition fwd"), ("k_gemm", "model: transition GEMMs"),
     ("k_bnb_", "model: transition/head BN bwd"), ("k_head", "model: head"), ("k_loss", "model: head"),
-    ("k_running", "model: running stats"),
+    ("k_running", "model: running stats"), ("k_sgd", "optimizer (SGD)"),
     ("Fwd1x1", "conv1x1_fwd"), ("Tc1x1Fwd", "conv1x1_fwd"),
     ("Conv3x3Dgrad", "conv3x3_dgrad"), ("Conv3x3Wgrad", "conv3x3_wgrad"),
     ("Conv1x1Dgrad", "conv1x1_dgrad"), ("Conv1x1Wgrad", "conv1x1_wgrad"), ("Conv1x1Fwd", "conv1x1_fwd"),
@@ -80,11 +80,13 @@ def main():
     total_launches = sum(c["launches"] for c in cats.values())
 
     os.makedirs(args.out, exist_ok=True)
-    md = [f"# {args.round}: ncu launch list of one bench step ({args.config}, {args.dtype}, batch 64)",
+    md = [f"# {args.round}: ncu launch list of one whole-network training step ({args.config}, {args.dtype}, "
+          f"batch 64)",
           "",
           "Source: `bash tools/ncu_round.sh` on one B200 (`ncu --profile-from-start off --metrics "
           "gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none` over "
-          "`python bench.py --ncu-step --no-cpu-baseline`, which replays ONE CUDA-graph step between "
+          "`python bench.py --ncu-step --ncu-what model --no-cpu-baseline`, which replays ONE CUDA-graph "
+          "training step (stem, dense blocks, transitions, head, loss, backward) plus the SGD update between "
           "cudaProfilerStart/Stop).  ncu serialises launches and flushes caches before each: times are "
           "cold-cache and sum above the graph-timed step; compare SHARES with bench.py `kernels`.",
           "",
