@@ -516,18 +516,12 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(const Op op) {
     float s1[8], s2[8];
     op.epilogue(row, cc * 8, v, aux, s1, s2);
     if constexpr (Op::kColSums) {
-#pragma unroll
-      for (int i = 0; i < 8; ++i) {
-        float a = s1[i], b = s2[i];
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
-          a += __shfl_xor_sync(0xffffffffu, a, o);
-          b += __shfl_xor_sync(0xffffffffu, b, o);
-        }
-        if (lane == 0) {
-          red[0][quarter][cc * 8 + i] = a;
-          red[1][quarter][cc * 8 + i] = b;
-        }
+      const float x = warp_colsum8(s1, lane);
+      const float y = warp_colsum8(s2, lane);
+      if ((lane & 3) == 0) {
+        const int col = cc * 8 + colsum8_column(lane);
+        red[0][quarter][col] = x;
+        red[1][quarter][col] = y;
       }
     }
   }

@@ -268,10 +268,11 @@ void tc_conv1x1_dgrad(Block* b, const LayerArgs<float>& a) {
 }
 
 // Split-K over pixels for the weight gradients: ~2 waves of 148 SMs, chunks
-// a multiple of the K block.
+// a multiple of the K block and at least one K block (small M: many short
+// splits rather than a few long latency chains).
 int64_t tc_wgrad_chunk(int64_t M, int64_t tiles) {
   int64_t splits = std::max<int64_t>(1, 296 / std::max<int64_t>(1, tiles));
-  splits = std::min<int64_t>(splits, std::max<int64_t>(1, M / 512));
+  splits = std::min<int64_t>(splits, std::max<int64_t>(1, M / tc::kBK));
   int64_t chunk = (M + splits - 1) / splits;
   return (chunk + tc::kBK - 1) / tc::kBK * tc::kBK;
 }
