@@ -104,7 +104,9 @@ Geometry geometry(const dpb_block_desc& d) {
   Geometry g;
   g.M = d.n * d.h * d.w;
   g.C = d.c0 + d.m * d.k;
+  g.Cp = (g.C + 3) / 4 * 4;
   g.cmax = d.c0 + (d.m - 1) * d.k;
+  g.cmaxp = (g.cmax + 3) / 4 * 4;
   g.P = static_cast<int>((g.M + 127) / 128);
   g.Pmax = g.P;
   if (d.dtype == DPB_BF16 && tc_supported(d))
@@ -152,12 +154,12 @@ void plan_arena(const dpb_block_desc& d, dpb_arena_sizes* s) {
     *b = bytes;
     off = align_up(off + bytes, 256);
   };
-  take(g.M * g.C * g.S, &s->feat_offset, &s->feat_bytes);
+  take(g.M * g.Cp * g.S, &s->feat_offset, &s->feat_bytes);
   take(static_cast<int64_t>(d.m) * g.M * d.bk * g.S, &s->z_offset, &s->z_bytes);
-  take((2 * g.C + 2LL * d.m * d.bk) * 4, &s->stats_offset, &s->stats_bytes);
-  take(d.layout == DPB_NCHW ? g.M * g.C * 4 : 0, &s->acc_offset, &s->acc_bytes);
+  take((2 * g.Cp + 2LL * d.m * d.bk) * 4, &s->stats_offset, &s->stats_bytes);
+  take(d.layout == DPB_NCHW ? g.M * g.Cp * 4 : 0, &s->acc_offset, &s->acc_bytes);
   take(2 * g.M * d.bk * 4, &s->g0_offset, &s->g0_bytes);
-  take(g.M * g.cmax * 4, &s->g1_offset, &s->g1_bytes);
+  take(g.M * g.cmaxp * 4, &s->g1_offset, &s->g1_bytes);
   // scratch: partials | wgrad partials | BN-backward coefficients
   int64_t wmax = 0;
   for (int l = 0; l < d.m; ++l) {
@@ -188,7 +190,7 @@ void plan_arena(const dpb_block_desc& d, dpb_arena_sizes* s) {
   }
   const int64_t pbytes = static_cast<int64_t>(g.Pmax) * std::max<int64_t>(g.C, d.bk) * 16;
   const int64_t scratch = align_up(pbytes, 256) + align_up(wmax * 4, 256) +
-                          align_up((4LL * d.bk + 2 * g.cmax) * 4, 256);
+                          align_up((4LL * d.bk + 2 * g.cmaxp) * 4, 256);
   take(scratch, &s->scratch_offset, &s->scratch_bytes);
   // pre-tiled bf16 weight operands of the tensor-core path (counted as scratch)
   if (d.dtype == DPB_BF16 && tc_supported(d)) {
@@ -263,8 +265,10 @@ static LayerArgs<S> layer_args(Block* b, const float* params, int l) {
   a.M = g.M;
   a.H = static_cast<int>(d.h);
   a.W = static_cast<int>(d.w);
-  a.C = static_cast<int>(g.C);
+  a.C = static_cast<int>(g.Cp);
+  a.Ca = static_cast<int>(b->acc_pitch > 0 ? b->acc_pitch : g.Cp);
   a.c = d.c0 + l * d.k;
+  a.cg = (a.c + 3) / 4 * 4;
   a.bk = d.bk;
   a.k = d.k;
   a.feat = static_cast<S*>(b->feat);
@@ -277,7 +281,7 @@ static LayerArgs<S> layer_args(Block* b, const float* params, int l) {
   a.beta_b = a.gamma_b + d.bk;
   a.w2 = a.beta_b + d.bk;
   a.amean = b->fstat;
-  a.avar = b->fstat + g.C;
+  a.avar = b->fstat + g.Cp;
   a.bmean = b->zstat + static_cast<int64_t>(l) * 2 * d.bk;
   a.bvar = a.bmean + d.bk;
   a.acc = b->acc_cur;
@@ -303,10 +307,10 @@ static void forward_impl(Block* b, const float* x_in, const float* params, float
     if (d.layout == DPB_NCHW) {
       dim3 grid(blocks_for(hw, 32), blocks_for(d.c0, 32), static_cast<unsigned>(d.n));
       launch(k_nchw_to_nhwc<S>, grid, dim3(32, 8), 0, b->stream, x_in, d.n, d.c0, hw, feat,
-                                                             static_cast<int>(g.C), 0);
+                                                             static_cast<int>(g.Cp), 0);
     } else {
       launch(k_nhwc_copy<S>, blocks_for(g.M * d.c0, 256), 256, 0, b->stream, 
-          x_in, d.c0, g.M, d.c0, feat, static_cast<int>(g.C), 0);
+          x_in, d.c0, g.M, d.c0, feat, static_cast<int>(g.Cp), 0);
     }
   }
   if (b->tc) {
@@ -317,11 +321,11 @@ static void forward_impl(Block* b, const float* x_in, const float* params, float
   }
   const double count = M;
   float* fmean = b->fstat;
-  float* fvar = b->fstat + g.C;
+  float* fvar = b->fstat + g.Cp;
   if (!eval) {
     {
       LaunchScope ls(b, KC_STATS, M * d.c0 * Sb, 0);
-      launch(k_channel_partials<S>, g.P, 256, 0, b->stream, feat, static_cast<int>(g.C), 0, g.M,
+      launch(k_channel_partials<S>, g.P, 256, 0, b->stream, feat, static_cast<int>(g.Cp), 0, g.M,
                                                         d.c0, b->part);
     }
     LaunchScope ls(b, KC_FINALIZE, 0, 0);
@@ -366,7 +370,7 @@ static void forward_impl(Block* b, const float* x_in, const float* params, float
   if (!eval && update_running) {
     LaunchScope ls(b, KC_RUNNING, 0, 0);
     launch(k_running_update, blocks_for(b->sz.stat_elems, 256), 256, 0, b->stream, 
-        d.m, d.c0, d.k, d.bk, static_cast<int>(g.C), b->fstat, b->zstat, running,
+        d.m, d.c0, d.k, d.bk, static_cast<int>(g.Cp), b->fstat, b->zstat, running,
         b->sz.stat_elems);
   }
 }
@@ -383,7 +387,7 @@ static void backward_impl(Block* b, const float* params, float* grad_acc, float*
     b->acc_cur = b->acc;
     dim3 grid(blocks_for(hw, 32), blocks_for(g.C, 32), static_cast<unsigned>(d.n));
     launch(k_nchw_to_nhwc<float>, grid, dim3(32, 8), 0, b->stream, grad_acc, d.n, g.C, hw,
-                                                               b->acc, static_cast<int>(g.C), 0);
+                                                               b->acc, static_cast<int>(g.Cp), 0);
   } else {
     b->acc_cur = grad_acc;
   }
@@ -501,16 +505,16 @@ static void backward_impl(Block* b, const float* params, float* grad_acc, float*
     }
     {
       LaunchScope ls(b, KC_BN_APPLY_ACC, M * a.c * (4.0 + Sb + 8.0), 0);
-      const bool quads = std::is_same<S, float>::value && a.c % 4 == 0 && g.C % 4 == 0 &&
+      const bool quads = std::is_same<S, float>::value && a.Ca % 4 == 0 &&
                          (reinterpret_cast<uintptr_t>(b->acc_cur) & 15) == 0;
       if (quads)
         launch(k_bn_apply_accumulate4,
-               blocks_for((g.M + kApplyRows - 1) / kApplyRows * (a.c / 4), 256), 256, 0, b->stream,
-               g.M, a.c, static_cast<int>(g.C), static_cast<const float*>(b->feat), b->g1, a.amean,
+               blocks_for((g.M + kApplyRows - 1) / kApplyRows * ((a.c + 3) / 4), 256), 256, 0, b->stream,
+               g.M, a.c, a.C, a.Ca, a.cg, static_cast<const float*>(b->feat), b->g1, a.amean,
                a.avar, a.gamma_a, b->bna_bwd, b->acc_cur);
       else
         launch(k_bn_apply_accumulate<S>, blocks_for(g.M * a.c, 256), 256, 0, b->stream,
-               g.M, a.c, static_cast<int>(g.C), static_cast<const S*>(b->feat), b->g1, a.amean,
+               g.M, a.c, a.C, a.Ca, a.cg, static_cast<const S*>(b->feat), b->g1, a.amean,
                a.avar, a.gamma_a, b->bna_bwd, b->acc_cur);
     }
   }
@@ -521,7 +525,7 @@ static void backward_impl(Block* b, const float* params, float* grad_acc, float*
   if (d.layout == DPB_NCHW) {
     LaunchScope ls(b, KC_PACK, M * g.C * 8, 0);
     dim3 grid(blocks_for(hw, 32), blocks_for(g.C, 32), static_cast<unsigned>(d.n));
-    launch(k_nhwc_to_nchw<float>, grid, dim3(32, 8), 0, b->stream, b->acc, static_cast<int>(g.C), 0,
+    launch(k_nhwc_to_nchw<float>, grid, dim3(32, 8), 0, b->stream, b->acc, static_cast<int>(g.Cp), 0,
                                                                d.n, g.C, hw, grad_acc);
   }
 }
@@ -550,9 +554,13 @@ int block_forward(Block* b, const float* x_in, const float* params, float* runni
   return DPB_OK;
 }
 
-int block_backward(Block* b, const float* params, float* grad_acc, float* grads) {
+int block_backward(Block* b, const float* params, float* grad_acc, float* grads, int64_t acc_pitch) {
   if (!b->fwd_done)
     return fail(DPB_PROTOCOL_ERROR, "backward requires a train-mode forward");
+  if (b->d.layout == DPB_NHWC && acc_pitch > 0 && acc_pitch < b->g.C)
+    return fail(DPB_SHAPE_ERROR, "accumulator pitch below the block's channel count");
+  // NCHW callers: the arena accumulator (pitch Cp); NHWC callers: their buffer
+  b->acc_pitch = b->d.layout == DPB_NCHW ? b->g.Cp : (acc_pitch > 0 ? acc_pitch : b->g.C);
   b->launches = 0;
   backward_impl<float>(b, params, grad_acc, grads);
   const cudaError_t e = cudaGetLastError();
@@ -565,7 +573,7 @@ static void read_feats_impl(Block* b, float* dst) {
   const dim3 grid(blocks_for(b->d.h * b->d.w, 32), blocks_for(b->g.C, 32),
                   static_cast<unsigned>(b->d.n));
   launch(k_nhwc_to_nchw<S>, grid, dim3(32, 8), 0, b->stream, 
-      static_cast<const S*>(b->feat), static_cast<int>(b->g.C), 0, b->d.n,
+      static_cast<const S*>(b->feat), static_cast<int>(b->g.Cp), 0, b->d.n,
       static_cast<int>(b->g.C), b->d.h * b->d.w, dst);
 }
 
@@ -593,7 +601,7 @@ int read_z(Block* b, float* dst) {
 
 int read_stats(Block* b, float* dst) {
   launch(k_export_stats, blocks_for(b->sz.stat_elems, 256), 256, 0, b->stream, 
-      b->d.m, b->d.c0, b->d.k, b->d.bk, static_cast<int>(b->g.C), b->fstat, b->zstat, dst,
+      b->d.m, b->d.c0, b->d.k, b->d.bk, static_cast<int>(b->g.Cp), b->fstat, b->zstat, dst,
       b->sz.stat_elems);
   const cudaError_t e = cudaGetLastError();
   return e == cudaSuccess ? DPB_OK : cuda_fail(e, "read_stats");
@@ -622,7 +630,7 @@ int create(const dpb_block_desc* desc, int device, void* stream, Block** out) {
   b->feat = base + b->sz.feat_offset;
   b->z = base + b->sz.z_offset;
   b->fstat = reinterpret_cast<float*>(base + b->sz.stats_offset);
-  b->zstat = b->fstat + 2 * b->g.C;
+  b->zstat = b->fstat + 2 * b->g.Cp;
   b->acc = reinterpret_cast<float*>(base + b->sz.acc_offset);
   b->g0 = reinterpret_cast<float*>(base + b->sz.g0_offset);
   b->g1 = reinterpret_cast<float*>(base + b->sz.g1_offset);
@@ -632,7 +640,7 @@ int create(const dpb_block_desc* desc, int device, void* stream, Block** out) {
       align_up(static_cast<int64_t>(b->g.Pmax) * std::max<int64_t>(b->g.C, desc->bk) * 16, 256);
   b->wpart = reinterpret_cast<float*>(sc + pbytes);
   // wgrad partial region size = scratch - pbytes - coef region
-  const int64_t coef_bytes = align_up((4LL * desc->bk + 2 * b->g.cmax) * 4, 256);
+  const int64_t coef_bytes = align_up((4LL * desc->bk + 2 * b->g.cmaxp) * 4, 256);
   const int64_t wt_bytes = b->tc ? weight_image_bytes(*desc) : 0;
   b->bnb_bwd = reinterpret_cast<float*>(sc + b->sz.scratch_bytes - wt_bytes - coef_bytes);
   b->bna_bwd = b->bnb_bwd + 4 * desc->bk;

@@ -13,8 +13,10 @@ namespace dpb {
 
 struct Geometry {
   int64_t M = 0;     // pixels N*H*W
-  int64_t C = 0;     // block output channels c0 + m*k (feature pitch)
+  int64_t C = 0;     // block output channels c0 + m*k
+  int64_t Cp = 0;    // feature-arena row pitch: C rounded up to 4 floats (16-byte rows for TMA)
   int64_t cmax = 0;  // widest layer input c0 + (m-1)*k
+  int64_t cmaxp = 0; // cmax rounded up to 4 (g1 rows)
   int P = 0;         // row CTAs of 128 pixels = partial-sum count
   int Pmax = 0;      // partial rows allocated (>= P; halo kernels use N * tiles/image)
   int S = 4;         // bytes per stored feature element
@@ -54,6 +56,7 @@ struct Block {
   float* zstat = nullptr;    // per layer mean[bk] | var[bk]
   float* acc = nullptr;      // [M, C] fp32 (NCHW boundary only)
   float* acc_cur = nullptr;  // the accumulator in use (arena or caller NHWC)
+  int64_t acc_pitch = 0;     // its row pitch (arena: Cp; caller NHWC: C or the caller's)
   float* g0 = nullptr;       // [M, bk] fp32 (x2: double-buffered across layers)
   cudaStream_t side = nullptr;        // weight-gradient branch of the backward
   std::vector<cudaEvent_t> fork_ev;   // per layer: start, bn_b done, side done
@@ -99,7 +102,8 @@ int create(const dpb_block_desc* desc, int device, void* stream, Block** out);
 void destroy(Block* b);
 int block_forward(Block* b, const float* x_in, const float* params, float* running,
                   int update_running, int eval);
-int block_backward(Block* b, const float* params, float* grad_acc, float* grads);
+// acc_pitch: row pitch of an NHWC grad_acc (<= 0: the block's C)
+int block_backward(Block* b, const float* params, float* grad_acc, float* grads, int64_t acc_pitch = 0);
 int read_feats(Block* b, float* dst);
 int read_z(Block* b, float* dst);
 int read_stats(Block* b, float* dst);

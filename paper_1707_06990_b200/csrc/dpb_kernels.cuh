@@ -163,7 +163,7 @@ __global__ void k_finalize_bn_bwd(const double2* __restrict__ part, int P, int n
 // t2 (fp32) and x, read-modify-writes acc.  One thread per 4 channels.
 template <typename S>
 __global__ void __launch_bounds__(256)
-k_bn_apply_accumulate(int64_t M, int c, int C, const S* __restrict__ feat,
+k_bn_apply_accumulate(int64_t M, int c, int C, int Ca, int cg, const S* __restrict__ feat,
                       const float* __restrict__ g1, const float* __restrict__ amean,
                       const float* __restrict__ avar,
                       const float* __restrict__ gamma, const float* __restrict__ coef,
@@ -176,21 +176,23 @@ k_bn_apply_accumulate(int64_t M, int c, int C, const S* __restrict__ feat,
   const float mean = amean[ch];
   const float inv = bn_inv(avar[ch]);
   const float xh = (to_f(feat[p * C + ch]) - mean) * inv;
-  const float g = g1[i];
-  acc[p * C + ch] += gamma[ch] * inv * (g - coef[2 * ch] - xh * coef[2 * ch + 1]);
+  const float g = g1[p * cg + ch];
+  acc[p * Ca + ch] += gamma[ch] * inv * (g - coef[2 * ch] - xh * coef[2 * ch + 1]);
 }
 
-// As k_bn_apply_accumulate for c % 4 == 0 and C % 4 == 0 (fp32 storage): a
-// thread owns one 4-channel quad for kApplyRows consecutive pixels
-// (coefficients computed once, 16-byte loads/stores, warps coalesced along the row).
+// As k_bn_apply_accumulate with 16-byte rows (feature pitch C, accumulator
+// pitch Ca, g1 pitch cg all multiples of 4; fp32 storage): a thread owns one
+// 4-channel quad for kApplyRows consecutive pixels (coefficients computed
+// once, 16-byte loads/stores, warps coalesced along the row).  The last quad
+// of a layer with c % 4 != 0 updates only its channels < c.
 constexpr int kApplyRows = 8;
 __global__ void __launch_bounds__(256)
-k_bn_apply_accumulate4(int64_t M, int c, int C, const float* __restrict__ feat,
+k_bn_apply_accumulate4(int64_t M, int c, int C, int Ca, int cg, const float* __restrict__ feat,
                        const float* __restrict__ g1, const float* __restrict__ amean,
                        const float* __restrict__ avar, const float* __restrict__ gamma,
                        const float* __restrict__ coef, float* __restrict__ acc) {
   pdl_enter();
-  const int cq = c >> 2;
+  const int cq = (c + 3) >> 2;
   const int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   const int64_t pg = t / cq;
   const int q = static_cast<int>(t - pg * cq);
@@ -205,15 +207,14 @@ k_bn_apply_accumulate4(int64_t M, int c, int C, const float* __restrict__ feat,
   const float inv[4] = {bn_inv(var.x), bn_inv(var.y), bn_inv(var.z), bn_inv(var.w)};
   const float mg[4] = {c01.x, c01.z, c23.x, c23.z};
   const float mgx[4] = {c01.y, c01.w, c23.y, c23.w};
+  const int live = c - ch < 4 ? c - ch : 4;  // channels of this quad inside the layer
   float gi[4];
 #pragma unroll
-  for (int e = 0; e < 4; ++e) gi[e] = gamma[ch + e] * inv[e];
+  for (int e = 0; e < 4; ++e) gi[e] = e < live ? gamma[ch + e] * inv[e] : 0.f;
   const int64_t pe = p0 + kApplyRows < M ? p0 + kApplyRows : M;
   for (int64_t p = p0; p < pe; ++p) {
     const float4 x4 = *reinterpret_cast<const float4*>(feat + p * C + ch);
-    const float4 g4 = *reinterpret_cast<const float4*>(g1 + p * c + ch);
-    float4* a4 = reinterpret_cast<float4*>(acc + p * C + ch);
-    float4 a = *a4;
+    const float4 g4 = *reinterpret_cast<const float4*>(g1 + p * cg + ch);
     const float x[4] = {x4.x, x4.y, x4.z, x4.w};
     const float g[4] = {g4.x, g4.y, g4.z, g4.w};
     float r[4];
@@ -222,11 +223,17 @@ k_bn_apply_accumulate4(int64_t M, int c, int C, const float* __restrict__ feat,
       const float xh = (x[e] - m[e]) * inv[e];
       r[e] = gi[e] * (g[e] - mg[e] - xh * mgx[e]);
     }
-    a.x += r[0];
-    a.y += r[1];
-    a.z += r[2];
-    a.w += r[3];
-    *a4 = a;
+    float* arow = acc + p * Ca + ch;
+    if (live == 4) {
+      float4 a = *reinterpret_cast<float4*>(arow);
+      a.x += r[0];
+      a.y += r[1];
+      a.z += r[2];
+      a.w += r[3];
+      *reinterpret_cast<float4*>(arow) = a;
+    } else {  // last quad of a layer with c % 4 != 0: channels >= c belong to later layers
+      for (int e = 0; e < live; ++e) arow[e] += r[e];
+    }
   }
 }
 

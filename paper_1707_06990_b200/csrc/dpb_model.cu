@@ -113,7 +113,7 @@ __global__ void k_stem_wgrad(const float* __restrict__ in, int64_t N, int cin, i
 // ---- transition forward: P = avgpool2x2(relu(bn(feat))) --------------------------------
 // feat NHWC [N*H*W, C] (pitch C), P [N*Ho*Wo, C]; Ho = H/2, Wo = W/2 (floor,
 // ops.hpp:392-402).  bn from the block's batch statistics.
-__global__ void k_trans_pool(const float* __restrict__ feat, int64_t N, int H, int W, int C,
+__global__ void k_trans_pool(const float* __restrict__ feat, int ld, int64_t N, int H, int W, int C,
                              const float* __restrict__ mean, const float* __restrict__ var,
                              const float* __restrict__ gamma, const float* __restrict__ beta,
                              float* __restrict__ P) {
@@ -129,10 +129,10 @@ __global__ void k_trans_pool(const float* __restrict__ feat, int64_t N, int H, i
     const int oy = r / Wo, ox = r - (r / Wo) * Wo;
     const int64_t p = (static_cast<int64_t>(n) * H + 2 * oy) * W + 2 * ox;
     float acc = 0.f;
-    acc += fmaxf(bn_ref(feat[p * C + c], mu, inv, ga, be), 0.f);
-    acc += fmaxf(bn_ref(feat[(p + 1) * C + c], mu, inv, ga, be), 0.f);
-    acc += fmaxf(bn_ref(feat[(p + W) * C + c], mu, inv, ga, be), 0.f);
-    acc += fmaxf(bn_ref(feat[(p + W + 1) * C + c], mu, inv, ga, be), 0.f);
+    acc += fmaxf(bn_ref(feat[p * ld + c], mu, inv, ga, be), 0.f);
+    acc += fmaxf(bn_ref(feat[(p + 1) * ld + c], mu, inv, ga, be), 0.f);
+    acc += fmaxf(bn_ref(feat[(p + W) * ld + c], mu, inv, ga, be), 0.f);
+    acc += fmaxf(bn_ref(feat[(p + W + 1) * ld + c], mu, inv, ga, be), 0.f);
     P[q * C + c] = acc * 0.25f;
   }
 }
@@ -199,7 +199,7 @@ __global__ void __launch_bounds__(256) k_gemm(int M, int N, int K, const float* 
 }
 
 // ---- head forward: gap[n][c] = mean_hw relu(bn(feat)) ---------------------------------
-__global__ void k_head_gap(const float* __restrict__ feat, int64_t N, int HW, int C,
+__global__ void k_head_gap(const float* __restrict__ feat, int ld, int64_t N, int HW, int C,
                            const float* __restrict__ mean, const float* __restrict__ var,
                            const float* __restrict__ gamma, const float* __restrict__ beta,
                            float* __restrict__ gap) {
@@ -211,7 +211,7 @@ __global__ void k_head_gap(const float* __restrict__ feat, int64_t N, int HW, in
   const float inv = bn_inv(var[c]);
   float acc = 0.f;
   for (int p = 0; p < HW; ++p)
-    acc += fmaxf(bn_ref(feat[(n * HW + p) * C + c], mean[c], inv, gamma[c], beta[c]), 0.f);
+    acc += fmaxf(bn_ref(feat[(n * HW + p) * ld + c], mean[c], inv, gamma[c], beta[c]), 0.f);
   gap[i] = acc * (1.f / static_cast<float>(HW));
 }
 
@@ -330,7 +330,7 @@ struct PoolGrad {
 // per-split partial sums (sum g, sum g*xhat) of g = relu'(act) * upstream, over
 // pixels [s*chunk, ...): thread = channel, fixed pixel order -> part[s][c]
 template <class G>
-__global__ void k_bnb_partials(const float* __restrict__ feat, int64_t M, int C, const float* __restrict__ mean,
+__global__ void k_bnb_partials(const float* __restrict__ feat, int ld, int64_t M, int C, const float* __restrict__ mean,
                                const float* __restrict__ var, const float* __restrict__ gamma,
                                const float* __restrict__ beta, G up, int64_t chunk, double2* __restrict__ part) {
   pdl_enter();
@@ -342,7 +342,7 @@ __global__ void k_bnb_partials(const float* __restrict__ feat, int64_t M, int C,
   double s1 = 0.0, s2 = 0.0;
 #pragma unroll 4
   for (int64_t p = p0; p < p1; ++p) {
-    const float x = feat[p * C + c];
+    const float x = feat[p * ld + c];
     if (!(bn_ref(x, mean[c], inv, gamma[c], beta[c]) > 0.f)) continue;  // relu_backward
     const float g = up(p, c);
     s1 += g;
@@ -354,20 +354,20 @@ __global__ void k_bnb_partials(const float* __restrict__ feat, int64_t M, int C,
 // out[p][c] = (gamma*inv) * (g - mg - xhat*mgx)  (written, ops.hpp:232-241);
 // thread = channel (coalesced), grid.y strides over pixels
 template <class G>
-__global__ void k_bnb_apply(const float* __restrict__ feat, int64_t M, int C, const float* __restrict__ mean,
+__global__ void k_bnb_apply(const float* __restrict__ feat, int ld, int64_t M, int C, const float* __restrict__ mean,
                             const float* __restrict__ var, const float* __restrict__ gamma,
                             const float* __restrict__ beta, G up, const float* __restrict__ coef,
-                            float* __restrict__ out) {
+                            float* __restrict__ out, int ldo) {
   pdl_enter();
   const int c = blockIdx.x * blockDim.x + threadIdx.x;
   if (c >= C) return;
   const float mu = mean[c], inv = bn_inv(var[c]), ga = gamma[c], be = beta[c];
   const float gi = ga * inv, mg = coef[2 * c], mgx = coef[2 * c + 1];
   for (int64_t p = blockIdx.y; p < M; p += gridDim.y) {
-    const float x = feat[p * C + c];
+    const float x = feat[p * ld + c];
     const float g = bn_ref(x, mu, inv, ga, be) > 0.f ? up(p, c) : 0.f;
     const float xh = (x - mu) * inv;
-    out[p * C + c] = gi * (g - mg - xh * mgx);
+    out[p * ldo + c] = gi * (g - mg - xh * mgx);
   }
 }
 
@@ -380,6 +380,7 @@ struct ModelBlock {
   Block* blk = nullptr;
   int64_t M = 0;
   int h = 0, w = 0, c0 = 0, m = 0, C = 0;
+  int Cp = 0;            // padded row pitch of the block's features and of acc
   int64_t poff = 0, pelems = 0, roff = 0, relems = 0;
   float* x = nullptr;    // NHWC [M, c0] block input
   float* acc = nullptr;  // NHWC [M, C] block output gradient (in/out)
@@ -441,6 +442,7 @@ int model_geometry(const dpb_model_desc* d, dpb_model* m) {
     mb.c0 = c;
     mb.m = d->blocks[b];
     mb.C = c + mb.m * d->k;
+    mb.Cp = (mb.C + 3) / 4 * 4;
     dpb_block_desc bd{d->batch, h, w, c, mb.m, d->k, bk, d->dtype, DPB_NHWC};
     dpb_arena_sizes sz{};
     int rc = validate(&bd);
@@ -546,7 +548,7 @@ DPB_API int dpb_model_create(const dpb_model_desc* desc, int device, void* strea
   std::vector<int64_t> off;
   for (auto& b : m->blocks) {
     off.push_back(take(b.M * b.c0));
-    off.push_back(take(b.M * b.C));
+    off.push_back(take(b.M * b.Cp));
   }
   for (auto& t : m->trans) {
     off.push_back(take(t.Mq * t.C));
@@ -635,12 +637,12 @@ DPB_API int dpb_model_step(dpb_model* m, const float* input, const int32_t* labe
     if (rc) return rc;
     const float* feat = static_cast<const float*>(mb.blk->feat);
     const float* mean = mb.blk->fstat;
-    const float* var = mb.blk->fstat + mb.blk->g.C;
+    const float* var = mb.blk->fstat + mb.blk->g.Cp;
     if (b + 1 < nb) {
       ModelTrans& t = m->trans[b];
       ModelBlock& nx = m->blocks[b + 1];
       launch(k_trans_pool, dim3(blocks_of(t.C, 128), static_cast<unsigned>(std::min<int64_t>(t.Mq, 65535))), 128,
-             0, st, feat, N, mb.h, mb.w, t.C, mean, var, params + t.gamma, params + t.beta, t.P);
+             0, st, feat, mb.Cp, N, mb.h, mb.w, t.C, mean, var, params + t.gamma, params + t.beta, t.P);
       launch(k_gemm<false, true>, dim3(blocks_of(t.Mq, 64), blocks_of(t.cout, 64), 1), 256, 0, st,
              static_cast<int>(t.Mq), t.cout, t.C, static_cast<const float*>(t.P), t.C, params + t.w, t.C, nx.x,
              nx.c0, t.C);
@@ -648,7 +650,7 @@ DPB_API int dpb_model_step(dpb_model* m, const float* input, const int32_t* labe
              running + t.run + t.C);
     } else {
       const int HW = mb.h * mb.w;
-      launch(k_head_gap, blocks_of(N * mb.C, 256), 256, 0, st, feat, N, HW, mb.C, mean, var,
+      launch(k_head_gap, blocks_of(N * mb.C, 256), 256, 0, st, feat, mb.Cp, N, HW, mb.C, mean, var,
              params + m->head_gamma, params + m->head_beta, m->gap);
       launch(k_head_loss, static_cast<unsigned>(N), 256, 0, st, static_cast<const float*>(m->gap), N, mb.C,
              params + m->head_w, params + m->head_b, d.classes, labels, m->logits, m->g_logits, m->loss_n,
@@ -668,21 +670,21 @@ DPB_API int dpb_model_step(dpb_model* m, const float* input, const int32_t* labe
            N, C, d.classes, m->g_gap, grads + m->head_w, grads + m->head_b);
     const float* feat = static_cast<const float*>(mb.blk->feat);
     const float* mean = mb.blk->fstat;
-    const float* var = mb.blk->fstat + mb.blk->g.C;
+    const float* var = mb.blk->fstat + mb.blk->g.Cp;
     HeadGrad up{m->g_gap, HW, C};
     int64_t chunk;
     const int S = splits_of(mb.M, chunk, kRowSplitsMax, 16);
-    launch(k_bnb_partials<HeadGrad>, dim3(S, blocks_of(C, 256)), 256, 0, st, feat, mb.M, C, mean, var,
+    launch(k_bnb_partials<HeadGrad>, dim3(S, blocks_of(C, 256)), 256, 0, st, feat, mb.Cp, mb.M, C, mean, var,
            params + m->head_gamma, params + m->head_beta, up, chunk, m->part);
     launch_finalize_bn_bwd(st, m->part, S, C, static_cast<double>(mb.M), grads + m->head_gamma,
                            grads + m->head_beta, m->coef);
     launch(k_bnb_apply<HeadGrad>, dim3(blocks_of(C, 128), static_cast<unsigned>(std::min<int64_t>(mb.M, 65535))),
-           128, 0, st, feat, mb.M, C, mean, var,
-           params + m->head_gamma, params + m->head_beta, up, static_cast<const float*>(m->coef), mb.acc);
+           128, 0, st, feat, mb.Cp, mb.M, C, mean, var,
+           params + m->head_gamma, params + m->head_beta, up, static_cast<const float*>(m->coef), mb.acc, mb.Cp);
   }
   for (int b = nb - 1; b >= 0; --b) {
     ModelBlock& mb = m->blocks[b];
-    int rc = block_backward(mb.blk, params + mb.poff, mb.acc, grads + mb.poff);
+    int rc = block_backward(mb.blk, params + mb.poff, mb.acc, grads + mb.poff, mb.Cp);
     if (rc) return rc;
     if (b > 0) {
       ModelTrans& t = m->trans[b - 1];
@@ -691,30 +693,30 @@ DPB_API int dpb_model_step(dpb_model* m, const float* input, const int32_t* labe
       int64_t chunk;
       const int S = splits_of(t.Mq, chunk);
       launch(k_gemm<true, false>, dim3(blocks_of(t.cout, 64), blocks_of(t.C, 64), S), 256, 0, st, t.cout, t.C,
-             static_cast<int>(t.Mq), static_cast<const float*>(mb.acc), mb.C, static_cast<const float*>(t.P), t.C,
+             static_cast<int>(t.Mq), static_cast<const float*>(mb.acc), mb.Cp, static_cast<const float*>(t.P), t.C,
              m->wpart, t.C, static_cast<int>(chunk));
       launch_fold_splits(st, m->wpart, S, static_cast<int64_t>(t.cout) * t.C, grads + t.w);
       launch(k_gemm<false, false>, dim3(blocks_of(t.Mq, 64), blocks_of(t.C, 64), 1), 256, 0, st,
-             static_cast<int>(t.Mq), t.C, t.cout, static_cast<const float*>(mb.acc), mb.C, params + t.w, t.C, t.gP,
+             static_cast<int>(t.Mq), t.C, t.cout, static_cast<const float*>(mb.acc), mb.Cp, params + t.w, t.C, t.gP,
              t.C, t.cout);
       const float* feat = static_cast<const float*>(pv.blk->feat);
       const float* mean = pv.blk->fstat;
-      const float* var = pv.blk->fstat + pv.blk->g.C;
+      const float* var = pv.blk->fstat + pv.blk->g.Cp;
       PoolGrad up{t.gP, pv.h, pv.w, t.C};
       const int S2 = splits_of(pv.M, chunk, kRowSplitsMax, 16);
-      launch(k_bnb_partials<PoolGrad>, dim3(S2, blocks_of(t.C, 256)), 256, 0, st, feat, pv.M, t.C, mean, var,
+      launch(k_bnb_partials<PoolGrad>, dim3(S2, blocks_of(t.C, 256)), 256, 0, st, feat, pv.Cp, pv.M, t.C, mean, var,
              params + t.gamma, params + t.beta, up, chunk, m->part);
       launch_finalize_bn_bwd(st, m->part, S2, t.C, static_cast<double>(pv.M), grads + t.gamma, grads + t.beta,
                              m->coef);
       launch(k_bnb_apply<PoolGrad>,
              dim3(blocks_of(t.C, 128), static_cast<unsigned>(std::min<int64_t>(pv.M, 65535))), 128, 0, st, feat,
-             pv.M, t.C, mean, var,
-             params + t.gamma, params + t.beta, up, static_cast<const float*>(m->coef), pv.acc);
+             pv.Cp, pv.M, t.C, mean, var,
+             params + t.gamma, params + t.beta, up, static_cast<const float*>(m->coef), pv.acc, pv.Cp);
     } else {
       const int chunk = stem_chunk(d.c0, d.in_c);
       const int S = static_cast<int>((mb.M + chunk - 1) / chunk);
       launch(k_stem_wgrad, S, 256, sizeof(float) * chunk * (d.c0 + d.in_c * 9), st, input, N, d.in_c,
-             d.in_h, d.in_w, static_cast<const float*>(mb.acc), mb.C, d.c0, m->wpart);
+             d.in_h, d.in_w, static_cast<const float*>(mb.acc), mb.Cp, d.c0, m->wpart);
       launch_fold_splits(st, m->wpart, S, static_cast<int64_t>(d.c0) * d.in_c * 9, grads);
     }
   }

@@ -131,8 +131,10 @@ template <typename S>
 struct LayerArgs {
   int64_t M;      // pixels N*H*W (GEMM rows)
   int H, W;       // spatial extent for 3x3 neighbourhoods
-  int C;          // feature-buffer pitch (block output channels)
+  int C;          // feature-arena row pitch (block output channels, padded to 4)
+  int Ca;         // row pitch of the accumulator acc
   int c;          // this layer's input channels (concat prefix)
+  int cg;         // row pitch of g1 (c padded to 4)
   int bk, k;      // bottleneck width, growth rate
   S* feat;        // [M, C]  NHWC features
   S* z;           // [M, bk] this layer's bottleneck output
@@ -272,7 +274,7 @@ struct Conv3x3Dgrad {
     const int o = static_cast<int>(kk - static_cast<int64_t>(tap) * a.k);
     int64_t q;  // dx[p] = sum_tap dy[p - d_tap] W[tap]
     if (!shifted(m, a.H, a.W, 1 - tap / 3, 1 - tap % 3, q)) return 0.f;
-    return a.acc[q * a.C + a.c + o];
+    return a.acc[q * a.Ca + a.c + o];
   }
   __device__ float load_b(const char*, int64_t kk, int j) const {
     const int tap = static_cast<int>(kk / a.k);
@@ -316,7 +318,7 @@ struct Conv3x3Wgrad {
     return bn_relu(reinterpret_cast<const BnFwd*>(d)[j], to_f(a.z[q * a.bk + j]));
   }
   __device__ float load_b(const char*, int64_t p, int o) const {
-    return a.acc[p * a.C + a.c + o];
+    return a.acc[p * a.Ca + a.c + o];
   }
   __device__ void epilogue(const char*, int, int64_t, int, float, double&, double&) const {}
   __device__ void store(int64_t r, int o, float v) const {
@@ -372,7 +374,7 @@ struct Conv1x1Dgrad {
     const BnFwd b = tile_a(d)[i - n0];
     const float x = to_f(a.feat[m * a.C + i]);
     const float g = relu_mask_ref(b, x) ? v : 0.f;
-    a.g1[m * a.c + i] = g;
+    a.g1[m * a.cg + i] = g;
     const float xh = (x - b.mean) * b.inv;
     s1 = g;
     s2 = static_cast<double>(g) * xh;

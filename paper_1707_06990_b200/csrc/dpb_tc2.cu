@@ -155,7 +155,7 @@ void tc2_pretile_w1t(Block* b, const float* params) {
 }
 
 bool tc2_conv1x1_dgrad(Block* b, const LayerArgs<float>& a, int l) {
-  if (a.C % 4 != 0 || a.c % 4 != 0 || !b->w1b) return false;
+  if (a.C % 4 != 0 || a.cg % 4 != 0 || !b->w1b) return false;
   const int ntiles = static_cast<int>((a.M + tc::kBM - 1) / tc::kBM);
   auto go = [&](auto tag) -> bool {
     using Op = decltype(tag);
@@ -166,7 +166,7 @@ bool tc2_conv1x1_dgrad(Block* b, const LayerArgs<float>& a, int l) {
     if (!make_map_f32(&op.gmap, a.g0, a.bk, a.M, a.bk, 32, tc::kBM) ||
         !make_map_f32(&op.zmap, a.z, a.bk, a.M, a.bk, 32, tc::kBM) ||
         !make_map_f32(&op.fmap, a.feat, a.C, a.M, a.C, 32, tc::kBM) ||
-        !make_map_f32(&op.omap, a.g1, a.c, a.M, a.c, 32, tc::kBM))
+        !make_map_f32(&op.omap, a.g1, a.c, a.M, a.cg, 32, tc::kBM))
       return false;
     op.a = a;
     op.w1t = b->w1b + b->w1b_off[l];
@@ -193,7 +193,7 @@ int64_t tc2_wgrad_wpart_elems(const dpb_block_desc& d, int l) {
 // Returns the number of splits written to wpart ([split][j][i]), 0 when the
 // shape is not supported (the caller then uses the v1 kernel).
 int tc2_conv1x1_wgrad(Block* b, const LayerArgs<float>& a) {
-  if (a.C % 4 != 0 || a.c % 4 != 0 || a.bk % 8 != 0 || a.bk > 192) return 0;
+  if (a.C % 4 != 0 || a.bk % 8 != 0 || a.bk > 192) return 0;
   int splits = 0;
   auto go = [&](auto tag) -> bool {
     using Op = decltype(tag);

@@ -715,7 +715,7 @@ struct Wgrad1x1 {
     const int j = mt * kBM + row;
     if (j < a.bk && i0 < ncols()) {
       const int nv = ncols() - i0 < 8 ? ncols() - i0 : 8;
-      tc::store8(a.wpart + (static_cast<int64_t>(tile) * a.bk + j) * a.c + n0() + i0, nv, true, v);
+      tc::store8(a.wpart + (static_cast<int64_t>(tile) * a.bk + j) * a.c + n0() + i0, nv, (a.c & 3) == 0, v);
     }
   }
   __device__ void col_sums(int, int, double, double) const {}

@@ -75,7 +75,7 @@ static TcArgs make_args(const LayerArgs<float>& a) {
   TcArgs t{};
   t.a = a;
   t.kp = round_up(a.k, 8);
-  t.vec = (a.C % 4 == 0) && (a.c % 4 == 0);
+  t.vec = (a.C % 4 == 0) && (a.Ca % 4 == 0) && (a.c % 4 == 0);
   return t;
 }
 
@@ -105,7 +105,7 @@ static tc::HaloArgs halo_args(const LayerArgs<float>& a, int kc) {
   h.a = a;
   h.g = tc::HaloGeom::make(a.H, a.W);
   h.kc = kc;
-  h.vec = (a.C % 4 == 0) && (a.c % 4 == 0);
+  h.vec = (a.C % 4 == 0) && (a.Ca % 4 == 0) && (a.c % 4 == 0);
   return h;
 }
 

@@ -555,7 +555,7 @@ struct Tc3x3DgradHalo {
         rr[i] = (q & 7) + 8 * (q / (8 * kcn));
         kk[i] = ((q >> 3) % kcn) * 8;
         const int pp = q < nchunk ? h.g.pixel(h.g.pos(t, rr[i])) : -1;
-        if (pp >= 0 && kk[i] < a.k) load8(a.acc + (pix0 + pp) * a.C + a.c + kk[i], a.k - kk[i], h.vec, v[i]);
+        if (pp >= 0 && kk[i] < a.k) load8(a.acc + (pix0 + pp) * a.Ca + a.c + kk[i], a.k - kk[i], h.vec, v[i]);
         else
 #pragma unroll
           for (int e = 0; e < 8; ++e) v[i][e] = 0.f;
@@ -698,7 +698,7 @@ struct Tc3x3WgradHalo {
           const int pos = (r & 7) + 8 * (r / (8 * og));
           const int o0 = ((r >> 3) % og) * 8;
           const int pp = h.g.pixel(s0 + pos);
-          if (pp >= 0 && o0 < a.k) load8(a.acc + (pix0 + pp) * a.C + a.c + o0, a.k - o0, h.vec, v[i]);
+          if (pp >= 0 && o0 < a.k) load8(a.acc + (pix0 + pp) * a.Ca + a.c + o0, a.k - o0, h.vec, v[i]);
           kind[i] = 2;
           off[i] = halo_mnmajor(kBM, o0, pos);
         }

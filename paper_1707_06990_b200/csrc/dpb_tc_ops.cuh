@@ -261,7 +261,7 @@ struct Tc3x3Dgrad {
         const int tap = k0 / t.kp, o0 = k0 - tap * t.kp;
         int64_t src;  // dx[p] = sum_tap dy[p - d_tap] W[tap]
         if (o0 < a.k && neighbour(p, row_yx(aux)[row], a.H, a.W, 1 - tap / 3, 1 - tap % 3, src))
-          load8(a.acc + src * a.C + a.c + o0, a.k - o0, t.vec, v);
+          load8(a.acc + src * a.Ca + a.c + o0, a.k - o0, t.vec, v);
       }
       put8<false>(ah, al, Tile<kBM>::kmajor_chunk(row, kc), v);
     }
@@ -387,7 +387,7 @@ struct Tc1x1Dgrad {
         s2[i] = 0.f;
       }
     }
-    if (nv > 0) store8(a.g1 + p * a.c + i0, nv, (a.c & 3) == 0, g);
+    if (nv > 0) store8(a.g1 + p * a.cg + i0, nv, (a.cg & 3) == 0, g);
   }
   __device__ void col_sums(int c, double s1, double s2) const {
     const int i = blockIdx.y * BN + c;
@@ -523,7 +523,7 @@ struct Tc3x3Wgrad {
       mnmajor_coords<BN>(q, rg, kr);
       const int64_t p = pk + kr;
       float v[8];
-      if (p < pe && rg < a.k) load8(a.acc + p * a.C + a.c + rg, a.k - rg, t.vec, v);
+      if (p < pe && rg < a.k) load8(a.acc + p * a.Ca + a.c + rg, a.k - rg, t.vec, v);
       else zero8(v);
       put8<false>(bh, bl, Tile<BN>::mnmajor_chunk(rg, kr), v);
     }
