@@ -391,6 +391,7 @@ struct ModelTrans {
   int64_t gamma = 0, beta = 0, w = 0, run = 0;  // offsets
   float* P = nullptr;   // [Mq, C] pooled activations
   float* gP = nullptr;  // [Mq, C]
+  float* wpart = nullptr;  // split-K partials of its dW (side stream)
 };
 
 }  // namespace dpb
@@ -399,6 +400,8 @@ struct dpb_model {
   dpb_model_desc d{};
   int device = 0;
   cudaStream_t stream = nullptr;
+  cudaStream_t side = nullptr;             // transition dW GEMMs + folds (gradient-only work)
+  std::vector<cudaEvent_t> ev;             // per transition: fork; plus one join
   std::vector<dpb::ModelBlock> blocks;
   std::vector<dpb::ModelTrans> trans;
   int64_t params = 0, running = 0;
@@ -505,6 +508,8 @@ DPB_API int dpb_model_sizes(const dpb_model_desc* desc, int64_t* param_elems, in
 
 DPB_API void dpb_model_destroy(dpb_model* m) {
   if (!m) return;
+  for (cudaEvent_t e : m->ev) cudaEventDestroy(e);
+  if (m->side) cudaStreamDestroy(m->side);
   for (auto& b : m->blocks)
     if (b.blk) destroy(b.blk);
   if (m->mem) cudaFree(m->mem);
@@ -553,6 +558,7 @@ DPB_API int dpb_model_create(const dpb_model_desc* desc, int device, void* strea
   for (auto& t : m->trans) {
     off.push_back(take(t.Mq * t.C));
     off.push_back(take(t.Mq * t.C));
+    off.push_back(take(static_cast<int64_t>(kSplitsMax) * t.cout * t.C));
   }
   const int Cl = m->blocks.back().C;
   const int64_t N = desc->batch;
@@ -585,6 +591,7 @@ DPB_API int dpb_model_create(const dpb_model_desc* desc, int device, void* strea
   for (auto& t : m->trans) {
     t.P = reinterpret_cast<float*>(base + off[k++]);
     t.gP = reinterpret_cast<float*>(base + off[k++]);
+    t.wpart = reinterpret_cast<float*>(base + off[k++]);
   }
   m->gap = reinterpret_cast<float*>(base + o_gap);
   m->logits = reinterpret_cast<float*>(base + o_log);
@@ -595,6 +602,12 @@ DPB_API int dpb_model_create(const dpb_model_desc* desc, int device, void* strea
   m->part = reinterpret_cast<double2*>(base + o_part);
   m->coef = reinterpret_cast<float*>(base + o_coef);
   m->bad_label = reinterpret_cast<int*>(base + o_bad);
+  if (cudaStreamCreateWithFlags(&m->side, cudaStreamNonBlocking) != cudaSuccess) m->side = nullptr;
+  for (size_t i = 0; m->side && i < m->trans.size() + 1; ++i) {
+    cudaEvent_t e;
+    cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
+    m->ev.push_back(e);
+  }
   *out = m;
   return DPB_OK;
 }
@@ -692,10 +705,18 @@ DPB_API int dpb_model_step(dpb_model* m, const float* input, const int32_t* labe
       // g_pool = mb.acc[:, :t.cout] (pitch mb.C); dW = g_pool^T . P (split-K), g_P = g_pool . W
       int64_t chunk;
       const int S = splits_of(t.Mq, chunk);
-      launch(k_gemm<true, false>, dim3(blocks_of(t.cout, 64), blocks_of(t.C, 64), S), 256, 0, st, t.cout, t.C,
+      // dW (gradient-only) on the side stream, overlapping g_P / BN backward and the
+      // next block's backward; t.wpart is private to this transition
+      cudaStream_t ws = st;
+      if (m->side) {
+        cudaEventRecord(m->ev[b - 1], st);
+        cudaStreamWaitEvent(m->side, m->ev[b - 1], 0);
+        ws = m->side;
+      }
+      launch(k_gemm<true, false>, dim3(blocks_of(t.cout, 64), blocks_of(t.C, 64), S), 256, 0, ws, t.cout, t.C,
              static_cast<int>(t.Mq), static_cast<const float*>(mb.acc), mb.Cp, static_cast<const float*>(t.P), t.C,
-             m->wpart, t.C, static_cast<int>(chunk));
-      launch_fold_splits(st, m->wpart, S, static_cast<int64_t>(t.cout) * t.C, grads + t.w);
+             t.wpart, t.C, static_cast<int>(chunk));
+      launch_fold_splits(ws, t.wpart, S, static_cast<int64_t>(t.cout) * t.C, grads + t.w);
       launch(k_gemm<false, false>, dim3(blocks_of(t.Mq, 64), blocks_of(t.C, 64), 1), 256, 0, st,
              static_cast<int>(t.Mq), t.C, t.cout, static_cast<const float*>(mb.acc), mb.Cp, params + t.w, t.C, t.gP,
              t.C, t.cout);
@@ -719,6 +740,10 @@ DPB_API int dpb_model_step(dpb_model* m, const float* input, const int32_t* labe
              d.in_h, d.in_w, static_cast<const float*>(mb.acc), mb.Cp, d.c0, m->wpart);
       launch_fold_splits(st, m->wpart, S, static_cast<int64_t>(d.c0) * d.in_c * 9, grads);
     }
+  }
+  if (m->side && !m->trans.empty()) {  // join: the caller's stream sees every gradient
+    cudaEventRecord(m->ev.back(), m->side);
+    cudaStreamWaitEvent(st, m->ev.back(), 0);
   }
   const cudaError_t e = cudaGetLastError();
   return e == cudaSuccess ? DPB_OK : cuda_fail(e, "model step launch");
