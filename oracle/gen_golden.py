@@ -101,6 +101,8 @@ MODEL_CASES = {
     # blocks, k, compression, classes, c0, (n, c, h, w), seed
     "model_small": ((2, 2, 2), 4, 0.5, 10, 8, (4, 3, 8, 8), 7),
     "model_bc": ((3, 3, 3), 12, 0.5, 10, 24, (8, 3, 16, 16), 11),
+    # k = 32 (DenseNet-121 / 264-k32 growth, bk = 128): per-tap 3x3 kernels, bk > 64 1x1 variants
+    "model_k32": ((2, 2), 32, 0.5, 10, 64, (4, 3, 8, 8), 13),
 }
 
 

@@ -16,7 +16,7 @@ from paper_1707_06990_b200.model import DenseNetConfig, ModelPlan
 
 pytestmark = pytest.mark.gpu
 
-CASES = ["model_small", "model_bc"]
+CASES = ["model_small", "model_bc", "model_k32"]
 TOL = {"fp32": 1e-4, "bf16": 2e-2}
 
 
