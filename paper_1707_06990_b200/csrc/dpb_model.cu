@@ -163,15 +163,19 @@ __global__ void __launch_bounds__(256) k_gemm(int M, int N, int K, const float* 
   const int ke = kb + kchunk < K ? kb + kchunk : K;
   float acc[4][4] = {};
   for (int k0 = kb; k0 < ke; k0 += 16) {
+    // consecutive threads read consecutive addresses: along M (N) for a
+    // transposed A (a plain B), along K within a row otherwise
     for (int e = tid; e < 16 * 64; e += 256) {
-      const int kk = e / 64, mm = e % 64;
-      const int gk = k0 + kk, gm = m0 + mm, gn = n0 + mm;
-      As[kk][mm] = (gk < ke && gm < M) ? (TA ? A[static_cast<int64_t>(gk) * lda + gm]
-                                             : A[static_cast<int64_t>(gm) * lda + gk])
-                                       : 0.f;
-      Bs[kk][mm] = (gk < ke && gn < N) ? (TB ? B[static_cast<int64_t>(gn) * ldb + gk]
-                                             : B[static_cast<int64_t>(gk) * ldb + gn])
-                                       : 0.f;
+      const int ka = TA ? e / 64 : e % 16, ma = TA ? e % 64 : e / 16;
+      const int kb2 = TB ? e % 16 : e / 64, nb = TB ? e / 16 : e % 64;
+      const int gka = k0 + ka, gm = m0 + ma;
+      const int gkb = k0 + kb2, gn = n0 + nb;
+      As[ka][ma] = (gka < ke && gm < M) ? (TA ? A[static_cast<int64_t>(gka) * lda + gm]
+                                              : A[static_cast<int64_t>(gm) * lda + gka])
+                                        : 0.f;
+      Bs[kb2][nb] = (gkb < ke && gn < N) ? (TB ? B[static_cast<int64_t>(gn) * ldb + gkb]
+                                               : B[static_cast<int64_t>(gkb) * ldb + gn])
+                                         : 0.f;
     }
     __syncthreads();
 #pragma unroll
@@ -368,6 +372,92 @@ __global__ void k_bnb_apply(const float* __restrict__ feat, int ld, int64_t M, i
     const float g = bn_ref(x, mu, inv, ga, be) > 0.f ? up(p, c) : 0.f;
     const float xh = (x - mu) * inv;
     out[p * ldo + c] = gi * (g - mg - xh * mgx);
+  }
+}
+
+// Transition BN backward for even H, W: every pixel lies in exactly one 2x2
+// pooling window, so both passes walk the pooled pixels q (n, oy, ox) of a
+// contiguous range with stepped indices (no divisions), loading g_P once per
+// window.  Thread = channel (coalesced); partial rows = ranges (fixed order).
+__device__ __forceinline__ void pool_walk_start(int64_t q, int Ho, int Wo, int64_t& n, int& oy, int& ox) {
+  n = q / (static_cast<int64_t>(Ho) * Wo);
+  const int r = static_cast<int>(q - n * Ho * Wo);
+  oy = r / Wo;
+  ox = r - oy * Wo;
+}
+
+__global__ void k_pool_bnb_partials(const float* __restrict__ feat, int ld, int H, int W, int C,
+                                    const float* __restrict__ mean, const float* __restrict__ var,
+                                    const float* __restrict__ gamma, const float* __restrict__ beta,
+                                    const float* __restrict__ g_P, int64_t Mq, int64_t chunk,
+                                    double2* __restrict__ part) {
+  pdl_enter();
+  const int c = blockIdx.y * blockDim.x + threadIdx.x;
+  if (c >= C) return;
+  const float mu = mean[c], inv = bn_inv(var[c]), ga = gamma[c], be = beta[c];
+  const int Ho = H / 2, Wo = W / 2;
+  const int64_t q0 = static_cast<int64_t>(blockIdx.x) * chunk;
+  const int64_t q1 = q0 + chunk < Mq ? q0 + chunk : Mq;
+  int64_t n;
+  int oy, ox;
+  pool_walk_start(q0, Ho, Wo, n, oy, ox);
+  double s1 = 0.0, s2 = 0.0;
+  for (int64_t q = q0; q < q1; ++q) {
+    const float g = g_P[q * C + c] * 0.25f;
+    const int64_t p = (n * H + 2 * oy) * W + 2 * ox;
+    const int64_t ps[4] = {p, p + 1, p + W, p + W + 1};
+#pragma unroll
+    for (int t = 0; t < 4; ++t) {
+      const float x = feat[ps[t] * ld + c];
+      if (bn_ref(x, mu, inv, ga, be) > 0.f) {
+        s1 += g;
+        s2 += g * ((x - mu) * inv);
+      }
+    }
+    if (++ox == Wo) {
+      ox = 0;
+      if (++oy == Ho) {
+        oy = 0;
+        ++n;
+      }
+    }
+  }
+  part[static_cast<int64_t>(blockIdx.x) * C + c] = make_double2(s1, s2);
+}
+
+__global__ void k_pool_bnb_apply(const float* __restrict__ feat, int ld, int H, int W, int C,
+                                 const float* __restrict__ mean, const float* __restrict__ var,
+                                 const float* __restrict__ gamma, const float* __restrict__ beta,
+                                 const float* __restrict__ g_P, int64_t Mq, int64_t chunk,
+                                 const float* __restrict__ coef, float* __restrict__ out, int ldo) {
+  pdl_enter();
+  const int c = blockIdx.y * blockDim.x + threadIdx.x;
+  if (c >= C) return;
+  const float mu = mean[c], inv = bn_inv(var[c]), ga = gamma[c], be = beta[c];
+  const float gi = ga * inv, mg = coef[2 * c], mgx = coef[2 * c + 1];
+  const int Ho = H / 2, Wo = W / 2;
+  const int64_t q0 = static_cast<int64_t>(blockIdx.x) * chunk;
+  const int64_t q1 = q0 + chunk < Mq ? q0 + chunk : Mq;
+  int64_t n;
+  int oy, ox;
+  pool_walk_start(q0, Ho, Wo, n, oy, ox);
+  for (int64_t q = q0; q < q1; ++q) {
+    const float g = g_P[q * C + c] * 0.25f;
+    const int64_t p = (n * H + 2 * oy) * W + 2 * ox;
+    const int64_t ps[4] = {p, p + 1, p + W, p + W + 1};
+#pragma unroll
+    for (int t = 0; t < 4; ++t) {
+      const float x = feat[ps[t] * ld + c];
+      const float gg = bn_ref(x, mu, inv, ga, be) > 0.f ? g : 0.f;
+      out[ps[t] * ldo + c] = gi * (gg - mg - ((x - mu) * inv) * mgx);
+    }
+    if (++ox == Wo) {
+      ox = 0;
+      if (++oy == Ho) {
+        oy = 0;
+        ++n;
+      }
+    }
   }
 }
 
@@ -723,16 +813,28 @@ DPB_API int dpb_model_step(dpb_model* m, const float* input, const int32_t* labe
       const float* feat = static_cast<const float*>(pv.blk->feat);
       const float* mean = pv.blk->fstat;
       const float* var = pv.blk->fstat + pv.blk->g.Cp;
-      PoolGrad up{t.gP, pv.h, pv.w, t.C};
-      const int S2 = splits_of(pv.M, chunk, kRowSplitsMax, 16);
-      launch(k_bnb_partials<PoolGrad>, dim3(S2, blocks_of(t.C, 256)), 256, 0, st, feat, pv.Cp, pv.M, t.C, mean, var,
-             params + t.gamma, params + t.beta, up, chunk, m->part);
-      launch_finalize_bn_bwd(st, m->part, S2, t.C, static_cast<double>(pv.M), grads + t.gamma, grads + t.beta,
-                             m->coef);
-      launch(k_bnb_apply<PoolGrad>,
-             dim3(blocks_of(t.C, 128), static_cast<unsigned>(std::min<int64_t>(pv.M, 65535))), 128, 0, st, feat,
-             pv.Cp, pv.M, t.C, mean, var,
-             params + t.gamma, params + t.beta, up, static_cast<const float*>(m->coef), pv.acc, pv.Cp);
+      if (pv.h % 2 == 0 && pv.w % 2 == 0) {  // every pixel in one pooling window: walk the windows
+        const int S2 = splits_of(t.Mq, chunk, kRowSplitsMax, 8);
+        launch(k_pool_bnb_partials, dim3(S2, blocks_of(t.C, 128)), 128, 0, st, feat, pv.Cp, pv.h, pv.w, t.C,
+               mean, var, params + t.gamma, params + t.beta, static_cast<const float*>(t.gP), t.Mq, chunk,
+               m->part);
+        launch_finalize_bn_bwd(st, m->part, S2, t.C, static_cast<double>(pv.M), grads + t.gamma,
+                               grads + t.beta, m->coef);
+        launch(k_pool_bnb_apply, dim3(S2, blocks_of(t.C, 128)), 128, 0, st, feat, pv.Cp, pv.h, pv.w, t.C, mean,
+               var, params + t.gamma, params + t.beta, static_cast<const float*>(t.gP), t.Mq, chunk,
+               static_cast<const float*>(m->coef), pv.acc, pv.Cp);
+      } else {
+        PoolGrad up{t.gP, pv.h, pv.w, t.C};
+        const int S2 = splits_of(pv.M, chunk, kRowSplitsMax, 16);
+        launch(k_bnb_partials<PoolGrad>, dim3(S2, blocks_of(t.C, 256)), 256, 0, st, feat, pv.Cp, pv.M, t.C, mean,
+               var, params + t.gamma, params + t.beta, up, chunk, m->part);
+        launch_finalize_bn_bwd(st, m->part, S2, t.C, static_cast<double>(pv.M), grads + t.gamma,
+                               grads + t.beta, m->coef);
+        launch(k_bnb_apply<PoolGrad>,
+               dim3(blocks_of(t.C, 128), static_cast<unsigned>(std::min<int64_t>(pv.M, 65535))), 128, 0, st, feat,
+               pv.Cp, pv.M, t.C, mean, var,
+               params + t.gamma, params + t.beta, up, static_cast<const float*>(m->coef), pv.acc, pv.Cp);
+      }
     } else {
       const int chunk = stem_chunk(d.c0, d.in_c);
       const int S = static_cast<int>((mb.M + chunk - 1) / chunk);
