@@ -1,0 +1,42 @@
+"""Debug: per-phase CTA timing of the halo 3x3 dgrad (dpb_debug_phase_clocks).
+Run with DPB_NO_FORK=1: the backward is then serial and its last halo launch
+is layer 0's 3x3 dgrad (BC-100 block-1 geometry)."""
+import ctypes as C
+import os
+import sys
+
+import numpy as np
+import torch
+
+sys.path.insert(0, ".")
+import paper_1707_06990_b200 as P  # noqa: E402
+from paper_1707_06990_b200._lib import lib  # noqa: E402
+
+assert os.environ.get("DPB_NO_FORK"), "run with DPB_NO_FORK=1"
+L = lib()
+f = L.dpb_debug_phase_clocks
+f.argtypes = [C.c_int, C.c_void_p, C.c_int]
+shp = P.BlockShape(64, 32, 32, 24, 4, 12, 48)
+plan = P.BlockPlan(shp, dtype="bf16", layout="nhwc")
+p = torch.randn(shp.param_elems, device="cuda") * 0.1 + 0.5
+x = torch.randn(shp.pixels, shp.c0, device="cuda")
+acc = torch.randn(shp.pixels, shp.c_out, device="cuda")
+g = torch.empty(shp.param_elems, device="cuda")
+run = shp.initial_running()
+for _ in range(2):
+    plan.forward(x, p, run, True)
+    plan.backward(p, acc.clone(), g)
+torch.cuda.synchronize()
+plan.forward(x, p, run, True)
+torch.cuda.synchronize()
+f(1, None, 0)
+plan.backward(p, acc.clone(), g)
+torch.cuda.synchronize()
+f(0, None, 0)
+buf = np.zeros((4096, 6), dtype=np.int64)
+f(-1, C.c_void_p(buf.ctypes.data), 576)
+b = buf[:576]
+ph = np.diff(b, axis=1)
+for i, name in enumerate(["prologue+alloc", "produce", "issue", "mma wait", "epilogue+dealloc"]):
+    print(f"{name:18s} mean {ph[:, i].mean():8.0f}  p50 {np.median(ph[:, i]):8.0f}  max {ph[:, i].max():8.0f}")
+print("CTA lifetime mean", (b[:, 5] - b[:, 0]).mean())
