@@ -155,8 +155,8 @@ __global__ void __launch_bounds__(256) k_gemm(int M, int N, int K, const float* 
                                               const float* __restrict__ B, int ldb, float* __restrict__ Cm,
                                               int ldc, int kchunk) {
   pdl_enter();
-  __shared__ float As[16][64 + 4];
-  __shared__ float Bs[16][64 + 4];
+  __shared__ __align__(16) float As[16][64 + 4];
+  __shared__ __align__(16) float Bs[16][64 + 4];
   const int tid = threadIdx.x, tx = tid % 16, ty = tid / 16;
   const int m0 = blockIdx.x * 64, n0 = blockIdx.y * 64;
   const int kb = blockIdx.z * kchunk;
@@ -180,11 +180,11 @@ __global__ void __launch_bounds__(256) k_gemm(int M, int N, int K, const float* 
     __syncthreads();
 #pragma unroll
     for (int kk = 0; kk < 16; ++kk) {
-      float a[4], b[4];
-#pragma unroll
-      for (int i = 0; i < 4; ++i) a[i] = As[kk][ty * 4 + i];
-#pragma unroll
-      for (int j = 0; j < 4; ++j) b[j] = Bs[kk][tx * 4 + j];
+      // 16-byte shared loads (rows of 68 floats: ty*4 / tx*4 offsets stay aligned)
+      const float4 a4 = *reinterpret_cast<const float4*>(&As[kk][ty * 4]);
+      const float4 b4 = *reinterpret_cast<const float4*>(&Bs[kk][tx * 4]);
+      const float a[4] = {a4.x, a4.y, a4.z, a4.w};
+      const float b[4] = {b4.x, b4.y, b4.z, b4.w};
 #pragma unroll
       for (int i = 0; i < 4; ++i)
 #pragma unroll
