@@ -74,7 +74,7 @@ __device__ int g_phase_on;
 // As tc_gemm_kernel, but the op owns the stage layout and the MMA issue
 // pattern (taps = descriptor shifts), and TMEM may hold several accumulators.
 template <class Op>
-__global__ void __launch_bounds__(kThreads, 2) tc_halo_kernel(const Op op) {
+__global__ void __launch_bounds__(kThreads, Op::kMinBlocks) tc_halo_kernel(const Op op) {
   constexpr uint32_t TCOLS = TmemCols<Op::kTmemCols>::value;
   constexpr int BN = Op::BN;
   extern __shared__ __align__(1024) uint8_t smem[];
@@ -328,6 +328,7 @@ struct Tc3x3FwdHalo {
   static constexpr int kIssuers = BN <= 32 ? 8 : 3, kAccCopies = kIssuers;
   static constexpr int kTmemCols = BN * kAccCopies;
   static constexpr bool kTapCols = false;
+  static constexpr int kMinBlocks = 2;
   static constexpr bool kColSums = true;
   static constexpr bool kBulk = true;
   static constexpr int kMaxChunks = 5;  // W=32 halos (1188 chunks) in one load batch
@@ -445,6 +446,7 @@ struct Tc3x3FwdTaps : Tc3x3FwdHalo<16> {
   static constexpr int kIssuers = 2, kAccCopies = 1;  // one issuer per M block
   static constexpr int kTmemCols = 2 * kBM;           // M block b at columns [128 b, 128 b + N)
   static constexpr bool kTapCols = true;
+  static constexpr int kMinBlocks = 2;
   __device__ int np() const { return (9 * h.a.k + 15) / 16 * 16; }
   __device__ uint32_t b_bytes() const { return static_cast<uint32_t>(np() * h.kc * 2); }
   __device__ uint32_t stage_bytes() const { return 2 * (halo_bytes() + b_bytes()); }
@@ -518,8 +520,12 @@ __global__ void k_pretile_w2_taps(const float* __restrict__ params, int c0, int 
 template <int BN_>
 struct Tc3x3DgradHalo {
   static constexpr int BN = BN_;
-  static constexpr int kIssuers = BN <= 64 ? 3 : 1, kAccCopies = kIssuers;
+  // one issuer, one accumulator: the 9 tap MMAs per tile are few, and the
+  // small TMEM / register / smem footprint lets three CTAs share an SM, whose
+  // phases (halo loads, MMAs, the z-dependent epilogue) then overlap
+  static constexpr int kIssuers = 1, kAccCopies = 1;
   static constexpr bool kTapCols = false;
+  static constexpr int kMinBlocks = BN <= 64 ? 3 : 2;
   static constexpr int kTmemCols = BN * kAccCopies;
   static constexpr bool kColSums = true;
   static constexpr bool kBulk = true;
@@ -636,6 +642,7 @@ struct Tc3x3WgradHalo {
   static constexpr int BN = BN_;
   static constexpr int kIssuers = 3, kAccCopies = 1;  // taps t = warp, warp+3, warp+6
   static constexpr bool kTapCols = false;
+  static constexpr int kMinBlocks = 2;
   static constexpr int kTmemCols = 9 * BN;
   static constexpr bool kColSums = false;
   static constexpr bool kBulk = false;
