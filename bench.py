@@ -419,9 +419,12 @@ def main():
     roof["peak_source"] = peak_src
     F_img, B_img = algorithmic_per_image(shapes)
     t_roof = max(F_img / (bf16_peak * 1e12), B_img / (hbm_peak * 1e9))
-    step_roof = {"algorithmic_gflop_per_img": F_img / 1e9, "algorithmic_mb_per_img": B_img / 1e6,
+    # SURVEY 8(d) byte / FLOP model of the dense blocks: measured against the
+    # dense-blocks-only rate (the network's stem / transitions / head are outside it)
+    step_roof = {"scope": "dense blocks (SURVEY 8(d) model)",
+                 "algorithmic_gflop_per_img": F_img / 1e9, "algorithmic_mb_per_img": B_img / 1e6,
                  "ceiling_img_per_s_per_gpu": 1.0 / t_roof,
-                 "frac": (value / world) * t_roof}
+                 "frac": (blocks_value / world) * t_roof}
     kernels = {k: {"launches": v["launches"], "ms": round(v["total_ms"] / 2, 4),
                    "GB/s": round(v["bytes"] / max(v["total_ms"], 1e-9) / 1e6, 1),
                    "TFLOP/s": round(v["flops"] / max(v["total_ms"], 1e-9) / 1e9, 2)}
