@@ -7,7 +7,7 @@ runs in ``_build/libdpb.so`` (hand-written CUDA for sm_100a).
 """
 from . import errors
 from .block import BlockPlan, BlockShape, block_memory, plan_arena
-from .model import CONFIGS, DenseNetConfig, count_parameters, predict_peak_elements, rng_normal
+from .model import CONFIGS, DenseNetConfig, ModelPlan, count_parameters, predict_peak_elements, rng_normal
 
 __all__ = ["errors", "BlockPlan", "BlockShape", "block_memory", "plan_arena", "CONFIGS",
-           "DenseNetConfig", "count_parameters", "predict_peak_elements", "rng_normal"]
+           "DenseNetConfig", "ModelPlan", "count_parameters", "predict_peak_elements", "rng_normal"]
