@@ -3,12 +3,15 @@
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
                     [--config bc100|cfg1|d121|d264k32|d264k48]
 
-One step = forward + backward of every dense block of the configuration
-(BASELINE.json configs[1] by default: DenseNet-BC-100, k=12, batch 64 per
-GPU, 3x32x32 input), on synthetic inputs resident in HBM, through libdpb.so
-(bf16 features, fp32 gradients).  Stem, transitions and head are not part of
-the hot path and are not run.  Prints ONE JSON line on
-rank 0; see DESIGN.md §5 for every field.
+One step = one whole training step of the configuration (BASELINE.json
+configs[1] by default: DenseNet-BC-100, k=12, batch 64 per GPU, 3x32x32
+input): stem, dense blocks, transitions, head, softmax cross-entropy, forward
++ backward and the momentum-SGD update, on synthetic inputs resident in HBM,
+through libdpb.so (bf16 tensor-core GEMMs, fp32 arena and gradients), CUDA-
+graph captured.  The dense blocks alone (the hot path) are reported beside it
+under "dense_blocks".  ImageNet-shaped configs, whose 7x7/2 stem is not built,
+time the dense blocks only.  Prints ONE JSON line on rank 0; see DESIGN.md §5
+for every field.
 """
 from __future__ import annotations
 
@@ -124,6 +127,42 @@ def cpu_runner(config: str):
     return CB.CpuRunner(block_shapes(config, 1)), f"1 image of each {config} dense block (fwd+bwd, f32)"
 
 
+def measure_naive_block(shape, dtype):
+    """The reference's Naive strategy on the device (paper_1707_06990_b200.naive,
+    unfused per-op kernels, every intermediate kept): one fwd+bwd of `shape`,
+    its allocator peak and held bytes against the efficient arena of the same
+    block.  Outside the timed region; a memory comparison, not a speed claim."""
+    import torch
+    import paper_1707_06990_b200 as P
+    from paper_1707_06990_b200.naive import NaiveBlock
+    g = torch.Generator(device="cpu").manual_seed(5)
+    p = (torch.randn(shape.param_elems, generator=g) * 0.1 + 0.5).cuda()
+    x = torch.randn((shape.n, shape.c0, shape.h, shape.w), generator=g).cuda()
+    acc = torch.randn((shape.n, shape.c_out, shape.h, shape.w), generator=g).cuda()
+    grads = torch.empty_like(p)
+    torch.cuda.synchronize()
+    base = torch.cuda.memory_allocated()
+    torch.cuda.reset_peak_memory_stats()
+    nb = NaiveBlock(shape, "naive")
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    nb.forward(x, p)
+    nb.backward(p, acc, grads)
+    e1.record()
+    torch.cuda.synchronize()
+    out = {"block": [shape.n, shape.h, shape.w, shape.c0, shape.m, shape.k, shape.bk],
+           "accounted_bytes": nb.retained_bytes() + 4 * x.numel(),
+           "held_bytes": torch.cuda.memory_allocated() - base + 4 * x.numel(),
+           "allocator_peak_bytes": torch.cuda.max_memory_allocated() - base + 4 * x.numel(),
+           "efficient_arena_bytes": P.block_memory(shape, dtype)[0],
+           "ms": e0.elapsed_time(e1),
+           "note": "Naive strategy on the device, unfused per-op kernels, fp32; bytes include the block input"}
+    out["efficient_over_held"] = out["efficient_arena_bytes"] / out["held_bytes"]
+    del nb
+    torch.cuda.empty_cache()
+    return out
+
+
 def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
@@ -173,6 +212,8 @@ def main():
     ap.add_argument("--no-graph", action="store_true", help="launch kernels directly (no CUDA graph)")
     ap.add_argument("--cpu-budget-s", type=float, default=25.0)
     ap.add_argument("--ref-budget-s", type=float, default=180.0)
+    ap.add_argument("--no-naive", action="store_true",
+                    help="skip the measured Naive store-everything block (memory comparison)")
     ap.add_argument("--ncu-what", default="blocks", choices=["blocks", "model"],
                     help="with --ncu-step: the dense blocks alone or the whole network step")
     ap.add_argument("--ncu-step", action="store_true",
@@ -514,6 +555,9 @@ def main():
     # ---- memory: efficient arena vs naive store-everything ---------------------
     eff = sum(P.block_memory(b["shape"], args.dtype)[0] for b in blocks)
     naive = sum(P.block_memory(b["shape"], "fp32")[1] for b in blocks)
+    naive_measured = None
+    if rank == 0 and world == 1 and not args.no_naive and P.block_memory(blocks[0]["shape"], "fp32")[1] < 40e9:
+        naive_measured = measure_naive_block(blocks[0]["shape"], args.dtype)
 
     # ---- CPU baseline (rank 0, N=1 only) ---------------------------------------
     cpu = None
@@ -556,7 +600,7 @@ def main():
             "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": launches_per_step * args.steps,
             "memory": {"efficient_arena_bytes": eff, "naive_bytes": naive,
-                       "ratio": eff / naive},
+                       "ratio": eff / naive, "naive_measured": naive_measured},
             "clocks": clk,
         }
         print(json.dumps(line), flush=True)

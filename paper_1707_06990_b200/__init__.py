@@ -7,7 +7,8 @@ runs in ``_build/libdpb.so`` (hand-written CUDA for sm_100a).
 """
 from . import errors
 from .block import BlockPlan, BlockShape, block_memory, plan_arena
+from .naive import NaiveBlock
 from .model import CONFIGS, DenseNetConfig, ModelPlan, count_parameters, predict_peak_elements, rng_normal
 
 __all__ = ["errors", "BlockPlan", "BlockShape", "block_memory", "plan_arena", "CONFIGS",
-           "DenseNetConfig", "ModelPlan", "count_parameters", "predict_peak_elements", "rng_normal"]
+           "DenseNetConfig", "ModelPlan", "NaiveBlock", "count_parameters", "predict_peak_elements", "rng_normal"]

@@ -1,0 +1,148 @@
+"""Naive and SharedGradient dense blocks on the GPU.
+
+These are the reference's two store-everything execution strategies
+(ExecutionStrategy::Naive / ::SharedGradient, graph.hpp:273-310).  The peak
+model (peak_model.hpp:57-90, 139-146) accounts for them per pre-activation
+bottleneck layer with c input channels (x N*H*W elements):
+
+    cat    the concatenation copy                    c
+    bn     BN_a+ReLU output c, BN_b+ReLU output bk   c + bk
+    owned  z (bk) and y (k)                          bk + k
+    grad   transients g_b, g_z (bk), g_a, g_cat (c)  2bk + 2c
+
+Per block, cat also holds the block-output concatenation (C) and grad holds
+the block accumulator (C).  Under Naive every gradient transient lives until
+the end of the step.  Under SharedGradient they come from one gradient region
+of four slots, each sized to the largest transient or accumulator: two
+accumulators that overlap at the block handoff, and two transient slots.
+
+`NaiveBlock` runs either strategy with the unfused per-op kernels of the C ABI
+(`ops.batch_statistics / batchnorm_apply / batchnorm_backward / conv2d_*`,
+fp32 NCHW).  It materialises each of these tensors, so the footprint is a
+device measurement: `accounting()` sums the live storage per arena, and
+tests/test_naive_gpu.py checks it against `predict_peak_elements`.  It is the
+memory and speed baseline of the memory-efficient path (`BlockPlan`), not a
+product path.  Flat parameters and gradients use the dpb_block layout
+(block.py BlockShape.param_offsets).  The ReLU masks and the concatenation
+copies are plain device elementwise / copy ops.
+"""
+from __future__ import annotations
+
+import torch
+
+from . import ops
+from .block import BlockShape
+
+STRATEGIES = ("naive", "shared-gradient")
+
+
+class NaiveBlock:
+    def __init__(self, shape: BlockShape, strategy: str = "naive", device="cuda"):
+        if strategy not in STRATEGIES:
+            raise ValueError(f"strategy must be one of {STRATEGIES}, got {strategy!r}")
+        self.s = shape
+        self.strategy = strategy
+        self.device = device
+        self.saved: list[dict] = []
+        self.out_cat = None
+        self.keep: list[torch.Tensor] = []   # Naive: every gradient transient of the step
+        self.acc = None                      # Naive: the block accumulator
+        self.region = None                   # SharedGradient: [4, slot] gradient region
+        if strategy == "shared-gradient":
+            s = shape
+            slot = max(s.bk, s.c_in(s.m - 1), s.c_out) * s.pixels
+            self.region = torch.empty((4, slot), device=device)
+
+    def _slot(self, i: int, shape) -> torch.Tensor:
+        n = 1
+        for d in shape:
+            n *= d
+        return self.region[i, :n].view(shape)
+
+    def _layer_params(self, params, l):
+        s = self.s
+        c = s.c_in(l)
+        o = s.param_offsets()[l]
+        ga, ba = params[o:o + c], params[o + c:o + 2 * c]
+        w1 = params[o + 2 * c:o + 2 * c + s.bk * c].view(s.bk, c, 1, 1)
+        o2 = o + 2 * c + s.bk * c
+        gb, bb = params[o2:o2 + s.bk], params[o2 + s.bk:o2 + 2 * s.bk]
+        w2 = params[o2 + 2 * s.bk:o2 + 2 * s.bk + 9 * s.k * s.bk].view(s.k, s.bk, 3, 3)
+        return ga, ba, w1, gb, bb, w2
+
+    def forward(self, x_in: torch.Tensor, params: torch.Tensor) -> torch.Tensor:
+        """x_in NCHW [n, c0, h, w]; returns the block-output concatenation."""
+        s = self.s
+        feats = [x_in]
+        self.saved = []
+        for l in range(s.m):
+            ga, ba, w1, gb, bb, w2 = self._layer_params(params, l)
+            cat = torch.cat(feats, dim=1)                             # cat (c)
+            ma, va = ops.batch_statistics(cat)
+            a = ops.batchnorm_apply(cat, ga, ba, ma, va, relu=True)   # bn (c)
+            z = ops.conv2d_forward(a, w1, 0)                          # owned (bk)
+            mb, vb = ops.batch_statistics(z)
+            b = ops.batchnorm_apply(z, gb, bb, mb, vb, relu=True)     # bn (bk)
+            y = ops.conv2d_forward(b, w2, 1)                          # owned (k)
+            self.saved.append(dict(cat=cat, a=a, z=z, b=b, y=y, ma=ma, va=va, mb=mb, vb=vb))
+            feats.append(y)
+        self.out_cat = torch.cat(feats, dim=1)                        # cat (C)
+        return self.out_cat
+
+    def backward(self, params: torch.Tensor, grad_acc: torch.Tensor, grads: torch.Tensor) -> torch.Tensor:
+        """grad_acc NCHW [n, C, h, w]: the block-output gradient, accumulated in
+        place like dpb_block_backward (graph.hpp backward walk).  grads is flat,
+        in the dpb_block layout."""
+        s = self.s
+        shared = self.strategy == "shared-gradient"
+        # the accumulator: slot 0 of the region, or a tensor of its own kept to step end
+        acc = self._slot(0, grad_acc.shape) if shared else torch.empty_like(grad_acc)
+        acc.copy_(grad_acc)
+        self.acc = None if shared else acc
+        self.keep = []
+        n, h, w = s.n, s.h, s.w
+        for l in reversed(range(s.m)):
+            ga, ba, w1, gb, bb, w2 = self._layer_params(params, l)
+            sv = self.saved[l]
+            c = s.c_in(l)
+            g_y = acc[:, c:c + s.k].contiguous()
+            tb = self._slot(2, (n, s.bk, h, w)) if shared else None
+            g_b, dw2 = ops.conv2d_backward(g_y, sv["b"], w2, 1, out=tb)            # grad (bk)
+            g_b.masked_fill_(sv["b"] <= 0, 0.0)
+            tz = self._slot(3, (n, s.bk, h, w)) if shared else None
+            g_z, dgb, dbb = ops.batchnorm_backward(g_b, sv["z"], gb, sv["mb"], sv["vb"], out=tz)  # (bk)
+            ta = self._slot(2, (n, c, h, w)) if shared else None
+            g_a, dw1 = ops.conv2d_backward(g_z, sv["a"], w1, 0, out=ta)            # grad (c)
+            g_a.masked_fill_(sv["a"] <= 0, 0.0)
+            tc = self._slot(3, (n, c, h, w)) if shared else None
+            g_cat, dga, dba = ops.batchnorm_backward(g_a, sv["cat"], ga, sv["ma"], sv["va"], out=tc)  # (c)
+            acc[:, :c] += g_cat
+            if not shared:
+                self.keep += [g_b, g_z, g_a, g_cat]
+            o = s.param_offsets()[l]
+            o2 = o + 2 * c + s.bk * c
+            grads[o:o + c] = dga
+            grads[o + c:o + 2 * c] = dba
+            grads[o + 2 * c:o2] = dw1.reshape(-1)
+            grads[o2:o2 + s.bk] = dgb
+            grads[o2 + s.bk:o2 + 2 * s.bk] = dbb
+            grads[o2 + 2 * s.bk:o2 + 2 * s.bk + 9 * s.k * s.bk] = dw2.reshape(-1)
+        grad_acc.copy_(acc)
+        return grad_acc
+
+    def accounting(self) -> dict:
+        """Elements held at the end of the step, per arena, counted from the live
+        storage (peak_model.hpp:139-146 arena split): cat, bn, owned, and grad
+        (Naive: every transient plus the accumulator; SharedGradient: the
+        four-slot region)."""
+        cat = sum(sv["cat"].numel() for sv in self.saved) + self.out_cat.numel()
+        bn = sum(sv["a"].numel() + sv["b"].numel() for sv in self.saved)
+        owned = sum(sv["z"].numel() + sv["y"].numel() for sv in self.saved)
+        if self.strategy == "naive":
+            grad = sum(t.numel() for t in self.keep) + (self.acc.numel() if self.acc is not None else 0)
+        else:
+            grad = self.region.numel()
+        return {"cat": cat, "bn": bn, "owned": owned, "grad": grad}
+
+    def retained_bytes(self) -> int:
+        return 4 * sum(self.accounting().values())

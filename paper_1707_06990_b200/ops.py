@@ -17,6 +17,14 @@ def _stream():
     return C.c_void_p(torch.cuda.current_stream().cuda_stream)
 
 
+def _out(out, shape, device):
+    if out is None:
+        return torch.empty(shape, device=device)
+    if tuple(out.shape) != tuple(shape) or out.dtype != torch.float32 or not out.is_contiguous():
+        raise errors.ShapeError(f"output buffer {tuple(out.shape)} does not match {tuple(shape)}")
+    return out
+
+
 def batch_statistics(x: torch.Tensor) -> tuple[torch.Tensor, torch.Tensor]:
     """Per-channel mean and biased variance (ops.hpp:138-162)."""
     n, c, h, w = x.shape
@@ -35,12 +43,13 @@ def batchnorm_apply(x, gamma, beta, mean, var, relu: bool = False) -> torch.Tens
     return out
 
 
-def batchnorm_backward(grad_y, x, gamma, mean, var):
-    """Exact train-mode BN gradients (ops.hpp:206-243) -> (gx, dgamma, dbeta)."""
+def batchnorm_backward(grad_y, x, gamma, mean, var, out=None):
+    """Exact train-mode BN gradients (ops.hpp:206-243) -> (gx, dgamma, dbeta).
+    `out`, if given, is a contiguous fp32 buffer of x's shape that receives gx."""
     n, c, h, w = x.shape
     if grad_y.shape != x.shape:
         raise errors.ShapeError("batchnorm_backward shape mismatch")
-    gx = torch.empty_like(x)
+    gx = _out(out, x.shape, x.device)
     dg = torch.empty(c, device=x.device)
     db = torch.empty(c, device=x.device)
     check(lib().dpb_op_batchnorm_backward(_ptr(grad_y), _ptr(x), n, c, h, w, _ptr(gamma), _ptr(mean),
@@ -63,11 +72,12 @@ def conv2d_forward(x, weights, padding: int) -> torch.Tensor:
     return out
 
 
-def conv2d_backward(grad_y, x, weights, padding: int, need_grad_x: bool = True):
-    """Exact gradients (ops.hpp:346-387) -> (grad_x or None, grad_w)."""
+def conv2d_backward(grad_y, x, weights, padding: int, need_grad_x: bool = True, out=None):
+    """Exact gradients (ops.hpp:346-387) -> (grad_x or None, grad_w).
+    `out`, if given, receives grad_x (contiguous fp32, x's shape)."""
     n, cin, h, w = x.shape
     cout, _, kh, _ = weights.shape
-    gx = torch.empty_like(x) if need_grad_x else None
+    gx = _out(out, x.shape, x.device) if need_grad_x else None
     gw = torch.empty_like(weights)
     check(lib().dpb_op_conv2d_backward(_ptr(grad_y), _ptr(x), n, cin, h, w, _ptr(weights), cout, kh,
                                        padding, _ptr(gx), _ptr(gw), _stream()))

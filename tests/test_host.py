@@ -188,3 +188,9 @@ def test_model_sizes_rejects_bad_geometry():
     assert lib().dpb_model_sizes(C.byref(d), None, None) == 6      # ConfigError (compression)
     d.compression, d.nblocks = 0.5, 0
     assert lib().dpb_model_sizes(C.byref(d), None, None) == 6
+
+
+def test_naive_block_rejects_unknown_strategy():
+    from paper_1707_06990_b200.naive import NaiveBlock
+    with pytest.raises(ValueError):
+        NaiveBlock(P.BlockShape(1, 4, 4, 8, 2, 4, 16), "shared-all")
