@@ -80,11 +80,18 @@ using tc::colsum8_column;
 using tc::warp_colsum8;
 
 // Debug-only phase clocks (dpb_debug_tc2_clocks): when g_tc2_dbg_c equals the
-// launch's layer width a.c, CTA x (< 148, column tile 0) stamps clock64() at
+// launch's layer width a.c, CTA x (< 148, column tile 0) stamps %globaltimer (ns) at
 //   [0] start [1] prologue done [2+t] TMA first load of tile t
 //   [6+t] transform of tile t done [10+t] MMA of tile t committed
 //   [14+t] epilogue of tile t starts [18+t] ends [22] exit   (t < 4)
-__device__ long long g_tc2_clock[148][28];  // [23] / [24]: epi_full wait cycles, warp 2 / warp 6
+__device__ __forceinline__ long long dbg_now() {  // ns, synchronised across SMs
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return static_cast<long long>(t);
+}
+// [23] / [24]: epi_full wait, warp 2 / warp 6; [25] / [26]: transform warp 0 wait for
+// raw_full / op_empty; [27]: TMA thread wait for raw_empty (ns summed over the launch)
+__device__ long long g_tc2_clock[148][28];
 __device__ int g_tc2_dbg_c;
 __device__ int g_tc2_dbg_flags;  // A/B timing: bit 0 skips g1 stores, bit 1 skips column sums
 
@@ -134,11 +141,11 @@ __global__ void __launch_bounds__(Roles<Op>::kThreads, 1) tc2_kernel(const __gri
 
   const int tid = threadIdx.x;
   const int warp = tid / 32, lane = tid % 32;
-  const bool dbg = g_tc2_dbg_c == op.a.c && blockIdx.x < 148 && blockIdx.y == 0;
+  const bool dbg = Op::kColSums && g_tc2_dbg_c == op.a.c && blockIdx.x < 148 && blockIdx.y == 0;
   long long* clk = g_tc2_clock[blockIdx.x < 148 ? blockIdx.x : 0];
   if (dbg && tid == 0) {
-    clk[0] = clock64();
-    clk[23] = clk[24] = 0;
+    clk[0] = dbg_now();
+    clk[23] = clk[24] = clk[25] = clk[26] = clk[27] = 0;
   }
   if (tid == 0) {
     for (int i = 0; i < NR; ++i) {
@@ -168,7 +175,7 @@ __global__ void __launch_bounds__(Roles<Op>::kThreads, 1) tc2_kernel(const __gri
   tc::tc_fence_after();
   const uint32_t tmem = tmem_base;
   const int ntiles = op.num_tiles();
-  if (dbg && tid == 0) clk[1] = clock64();
+  if (dbg && tid == 0) clk[1] = dbg_now();
 
   if (warp == kTmaWarp) {
     if (lane == 0) {
@@ -177,9 +184,11 @@ __global__ void __launch_bounds__(Roles<Op>::kThreads, 1) tc2_kernel(const __gri
       for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x)
         for (int kb = 0; kb < op.num_kb(tile); ++kb, ++it) {
           const int r = it % NR;
+          const long long w0 = dbg ? dbg_now() : 0;
           tc::mbar_wait(&raw_empty[r], ((it / NR) & 1) ^ 1);
+          if (dbg) clk[27] += dbg_now() - w0;
           const int t = (tile - static_cast<int>(blockIdx.x)) / static_cast<int>(gridDim.x);
-          if (dbg && kb == 0 && t < 4) clk[2 + t] = clock64();
+          if (dbg && kb == 0 && t < 4) clk[2 + t] = dbg_now();
           mbar_expect_tx(&raw_full[r], op.raw_bytes(tile, kb));
           op.tma(tile, kb, tc::smem_u32(raw_ring + r * Op::kRawBytes), &raw_full[r]);
         }
@@ -201,7 +210,7 @@ __global__ void __launch_bounds__(Roles<Op>::kThreads, 1) tc2_kernel(const __gri
           if constexpr (Op::kMmaReadsRaw) tc::mma_commit(&raw_empty[r]);
         }
         tc::mma_commit(&acc_full[a]);
-        if (dbg && at < 4) clk[10 + at] = clock64();
+        if (dbg && at < 4) clk[10 + at] = dbg_now();
       }
     }
   } else if (warp >= kEpiWarp0 && warp < R::kXfWarp0) {
@@ -214,17 +223,17 @@ __global__ void __launch_bounds__(Roles<Op>::kThreads, 1) tc2_kernel(const __gri
       const int a = at & 1;
       tc::mbar_wait(&acc_full[a], (at >> 1) & 1);
       tc::tc_fence_after();
-      if (dbg && tid == kEpiWarp0 * 32 && at < 4) clk[14 + at] = clock64();
+      if (dbg && tid == kEpiWarp0 * 32 && at < 4) clk[14 + at] = dbg_now();
       const int nch = op.epi_chunks(tile);
       const int ngrp = (nch + 3) / 4;
       for (int gi = grp; gi < ngrp; gi += R::kGroups) {
         uint8_t* ebox = nullptr;
         const int e = e0 + gi;
         if constexpr (Op::kNE > 0) {
-          const long long w0 = dbg ? clock64() : 0;
+          const long long w0 = dbg ? dbg_now() : 0;
           tc::mbar_wait(&epi_full[e % NE], (e / NE) & 1);
           if (dbg && lane == 0 && (warp == kEpiWarp0 || warp == kEpiWarp0 + 4))
-            clk[warp == kEpiWarp0 ? 23 : 24] += clock64() - w0;
+            clk[warp == kEpiWarp0 ? 23 : 24] += dbg_now() - w0;
           ebox = epi_ring + (e % NE) * Op::kEpiBytes;
         }
 #pragma unroll
@@ -260,7 +269,7 @@ __global__ void __launch_bounds__(Roles<Op>::kThreads, 1) tc2_kernel(const __gri
         }
       }
       e0 += ngrp;
-      if (dbg && tid == kEpiWarp0 * 32 && at < 4) clk[18 + at] = clock64();
+      if (dbg && tid == kEpiWarp0 * 32 && at < 4) clk[18 + at] = dbg_now();
       tc::tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&acc_empty[a]);
@@ -306,8 +315,14 @@ __global__ void __launch_bounds__(Roles<Op>::kThreads, 1) tc2_kernel(const __gri
     for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x)
       for (int kb = 0; kb < op.num_kb(tile); ++kb, ++it) {
         const int r = it % NR, s = it % NS;
+        const long long w0 = dbg ? dbg_now() : 0;
         tc::mbar_wait(&raw_full[r], (it / NR) & 1);
+        const long long w1 = dbg ? dbg_now() : 0;
         tc::mbar_wait(&op_empty[s], ((it / NS) & 1) ^ 1);
+        if (dbg && tid == R::kXfWarp0 * 32) {
+          clk[25] += w1 - w0;
+          clk[26] += dbg_now() - w1;
+        }
         op.transform(tile, kb, raw_ring + r * Op::kRawBytes, op_ring + s * Op::kOpBytes, aux, xt);
         tc::fence_proxy_async();
         __syncwarp();
@@ -317,7 +332,7 @@ __global__ void __launch_bounds__(Roles<Op>::kThreads, 1) tc2_kernel(const __gri
         }
         if (dbg && tid == R::kXfWarp0 * 32 && kb == op.num_kb(tile) - 1) {
           const int t = (tile - static_cast<int>(blockIdx.x)) / static_cast<int>(gridDim.x);
-          if (t < 4) clk[6 + t] = clock64();
+          if (t < 4) clk[6 + t] = dbg_now();
         }
       }
   }
@@ -327,7 +342,7 @@ __global__ void __launch_bounds__(Roles<Op>::kThreads, 1) tc2_kernel(const __gri
     tc::tc_fence_after();
     tc::tmem_dealloc<2 * TC>(tmem);
   }
-  if (dbg && tid == 0) clk[22] = clock64();
+  if (dbg && tid == 0) clk[22] = dbg_now();
 }
 
 // ---- 1x1 forward: z = relu(bn_a(x)) . W1^T (bf16x3) ---------------------------------

@@ -66,9 +66,12 @@ __device__ __forceinline__ uint32_t halo_mnmajor(int R, int j, int pos) {
 }
 
 // Debug phase clocks (dpb_debug_phase_clocks): thread 0 of the first 4096
-// CTAs records globaltimer-free clock64 stamps at the phase boundaries.
-__device__ long long g_phase_clock[4096][6];
+// CTAs records clock64 stamps at the phase boundaries: start, prologue done,
+// last produce, last issue, MMAs complete, epilogue loop done, epilogue
+// barrier passed, column sums written, exit.
+__device__ long long g_phase_clock[4096][9];
 __device__ int g_phase_on;
+__device__ int g_phase_flags;  // A/B: 1 skip z load, 2 skip t0 store, 4 skip column sums, 8 skip mask
 
 // ---- engine ----------------------------------------------------------------------
 // As tc_gemm_kernel, but the op owns the stage layout and the MMA issue
@@ -210,7 +213,7 @@ __global__ void __launch_bounds__(kThreads, Op::kMinBlocks) tc_halo_kernel(const
     }
     float s1[8], s2[8];
     op.epilogue(row, cc * 8, v, aux, s1, s2);
-    if constexpr (Op::kColSums) {
+    if (Op::kColSums && !(g_phase_flags & 4)) {
       const float x = warp_colsum8(s1, lane);
       const float y = warp_colsum8(s2, lane);
       if ((lane & 3) == 0) {
@@ -220,8 +223,10 @@ __global__ void __launch_bounds__(kThreads, Op::kMinBlocks) tc_halo_kernel(const
       }
     }
   }
+  if (dbg) g_phase_clock[dbg_id][5] = clock64();
   tc_fence_before();
   __syncthreads();
+  if (dbg) g_phase_clock[dbg_id][6] = clock64();
   if constexpr (Op::kColSums) {
     for (int c = tid; c < BN; c += kThreads) {
       const double a = static_cast<double>(red[0][0][c]) + red[0][1][c] + red[0][2][c] + red[0][3][c];
@@ -229,11 +234,12 @@ __global__ void __launch_bounds__(kThreads, Op::kMinBlocks) tc_halo_kernel(const
       op.col_sums(c, a, b);
     }
   }
+  if (dbg) g_phase_clock[dbg_id][7] = clock64();
   if (warp == 0) {
     tc_fence_after();
     tmem_dealloc<TCOLS>(tmem);
   }
-  if (dbg) g_phase_clock[dbg_id][5] = clock64();
+  if (dbg) g_phase_clock[dbg_id][8] = clock64();
 }
 
 struct HaloArgs {
@@ -525,7 +531,7 @@ struct Tc3x3DgradHalo {
   // phases (halo loads, MMAs, the z-dependent epilogue) then overlap
   static constexpr int kIssuers = 1, kAccCopies = 1;
   static constexpr bool kTapCols = false;
-  static constexpr int kMinBlocks = BN <= 64 ? 3 : 2;
+  static constexpr int kMinBlocks = BN <= 64 ? 4 : 2;
   static constexpr int kTmemCols = BN * kAccCopies;
   static constexpr bool kColSums = true;
   static constexpr bool kBulk = true;
@@ -600,12 +606,16 @@ struct Tc3x3DgradHalo {
     const int nv = pp >= 0 ? a.bk - col0 : 0;
     float zv[8], g[8];
     const int64_t p = static_cast<int64_t>(img()) * h.g.H * h.g.W + (pp >= 0 ? pp : 0);
-    if (nv > 0) load8(a.z + p * a.bk + col0, nv, (a.bk & 3) == 0, zv);
+    const int fl = g_phase_flags;
+    if (nv > 0 && !(fl & 1)) load8(a.z + p * a.bk + col0, nv, (a.bk & 3) == 0, zv);
+    else
+#pragma unroll
+      for (int i = 0; i < 8; ++i) zv[i] = v[i];
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
       if (i < nv) {
         const BnFwd b = bn[col0 + i];
-        g[i] = relu_mask_ref(b, zv[i]) ? v[i] : 0.f;
+        g[i] = (fl & 8) || relu_mask_ref(b, zv[i]) ? v[i] : 0.f;
         s1[i] = g[i];
         s2[i] = g[i] * ((zv[i] - b.mean) * b.inv);
       } else {
@@ -614,7 +624,7 @@ struct Tc3x3DgradHalo {
         s2[i] = 0.f;
       }
     }
-    if (nv > 0) {
+    if (nv > 0 && !(fl & 2)) {
       float* dst = a.g0 + p * a.bk + col0;
       if ((a.bk & 3) == 0 && nv >= 8) {
         reinterpret_cast<float4*>(dst)[0] = make_float4(g[0], g[1], g[2], g[3]);

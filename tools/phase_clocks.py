@@ -19,12 +19,12 @@ f(1, None, 0)
 plan.forward(x, p, run, True)   # the last halo forward launch wins (layer 3)
 torch.cuda.synchronize()
 f(0, None, 0)
-buf = np.zeros((4096, 6), dtype=np.int64)
+buf = np.zeros((4096, 9), dtype=np.int64)
 f(-1, C.c_void_p(buf.ctypes.data), 576)
 b = buf[:576]
 t0 = b[:, 0].min()
 ph = np.diff(b, axis=1)
-print("CTAs", len(b), "span cycles", b[:, 5].max() - t0)
-for i, name in enumerate(["prologue+alloc", "produce", "issue", "mma wait", "epilogue+dealloc"]):
+print("CTAs", len(b), "span cycles", b[:, 8].max() - t0)
+for i, name in enumerate(["prologue+alloc", "produce", "issue", "mma wait", "epilogue loop", "epi barrier", "col sums", "dealloc"]):
     print(f"{name:18s} mean {ph[:, i].mean():8.0f}  p50 {np.median(ph[:, i]):8.0f}  max {ph[:, i].max():8.0f}")
-print("CTA lifetime mean", (b[:, 5] - b[:, 0]).mean(), "start spread", np.percentile(b[:, 0] - t0, [0, 50, 100]))
+print("CTA lifetime mean", (b[:, 8] - b[:, 0]).mean(), "start spread", np.percentile(b[:, 0] - t0, [0, 50, 100]))

@@ -29,14 +29,15 @@ for _ in range(2):
 torch.cuda.synchronize()
 plan.forward(x, p, run, True)
 torch.cuda.synchronize()
-f(1, None, 0)
+FLAGS = int(sys.argv[1]) if len(sys.argv) > 1 else 0
+f(1 | (FLAGS << 16), None, 0)
 plan.backward(p, acc.clone(), g)
 torch.cuda.synchronize()
 f(0, None, 0)
-buf = np.zeros((4096, 6), dtype=np.int64)
+buf = np.zeros((4096, 9), dtype=np.int64)
 f(-1, C.c_void_p(buf.ctypes.data), 576)
 b = buf[:576]
 ph = np.diff(b, axis=1)
-for i, name in enumerate(["prologue+alloc", "produce", "issue", "mma wait", "epilogue+dealloc"]):
+for i, name in enumerate(["prologue+alloc", "produce", "issue", "mma wait", "epilogue loop", "epi barrier", "col sums", "dealloc"]):
     print(f"{name:18s} mean {ph[:, i].mean():8.0f}  p50 {np.median(ph[:, i]):8.0f}  max {ph[:, i].max():8.0f}")
-print("CTA lifetime mean", (b[:, 5] - b[:, 0]).mean())
+print("CTA lifetime mean", (b[:, 8] - b[:, 0]).mean())
