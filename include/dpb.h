@@ -269,7 +269,10 @@ DPB_API int dpb_model_create(const dpb_model_desc* desc, int device, void* strea
 DPB_API void dpb_model_destroy(dpb_model* model);
 /* One training step: input NCHW [batch, in_c, in_h, in_w], labels int32
  * [batch] (device); writes grads (flat, registration order), updates running
- * statistics (momentum 0.1) and writes the mean loss to *loss (device float). */
+ * statistics (momentum 0.1) and writes the mean loss to *loss (device float).
+ * On a created stream that is not being captured, the first call captures the
+ * step's launches into a CUDA graph and later calls with the same six buffers
+ * replay it (DPB_MODEL_NO_GRAPH=1: always launch eagerly). */
 DPB_API int dpb_model_step(dpb_model* model, const float* input, const int32_t* labels,
                            const float* params, float* running, float* grads, float* loss);
 DPB_API int dpb_model_sync(dpb_model* model);

@@ -503,6 +503,9 @@ struct dpb_model {
   float* coef = nullptr;
   int* bad_label = nullptr;
   int64_t wpart_elems = 0, part_rows = 0;
+  // CUDA graph of the whole step, replayed while the step's buffers stay the same
+  cudaGraphExec_t graph = nullptr;
+  const void* graph_key[6] = {};
 };
 
 namespace dpb {
@@ -598,6 +601,7 @@ DPB_API int dpb_model_sizes(const dpb_model_desc* desc, int64_t* param_elems, in
 
 DPB_API void dpb_model_destroy(dpb_model* m) {
   if (!m) return;
+  if (m->graph) cudaGraphExecDestroy(m->graph);
   for (cudaEvent_t e : m->ev) cudaEventDestroy(e);
   if (m->side) cudaStreamDestroy(m->side);
   for (auto& b : m->blocks)
@@ -715,10 +719,13 @@ DPB_API int dpb_model_sync(dpb_model* m) {
   return DPB_OK;
 }
 
-DPB_API int dpb_model_step(dpb_model* m, const float* input, const int32_t* labels, const float* params,
-                           float* running, float* grads, float* loss) {
-  if (!m || !input || !labels || !params || !running || !grads || !loss)
-    return fail(DPB_CONFIG_ERROR, "null pointer argument");
+}  // extern "C"
+
+namespace {
+
+// Every launch of one training step on m->stream (and the side stream).
+int model_step_launch(dpb_model* m, const float* input, const int32_t* labels, const float* params,
+                      float* running, float* grads, float* loss) {
   const dpb_model_desc& d = m->d;
   cudaStream_t st = m->stream;
   const int64_t N = d.batch;
@@ -849,6 +856,55 @@ DPB_API int dpb_model_step(dpb_model* m, const float* input, const int32_t* labe
   }
   const cudaError_t e = cudaGetLastError();
   return e == cudaSuccess ? DPB_OK : cuda_fail(e, "model step launch");
+}
+
+}  // namespace
+
+extern "C" {
+
+// The step is ~700 launches; replaying them as one CUDA graph removes the
+// per-launch host cost and the gaps it leaves on the device.  The graph is
+// captured on the first call and replayed while (input, labels, params,
+// running, grads, loss) are the same buffers; the stream must be a created
+// stream that is not itself being captured (a caller capturing its own graph,
+// or the legacy default stream, gets the eager launches).  DPB_MODEL_NO_GRAPH=1
+// always launches eagerly.
+DPB_API int dpb_model_step(dpb_model* m, const float* input, const int32_t* labels, const float* params,
+                           float* running, float* grads, float* loss) {
+  if (!m || !input || !labels || !params || !running || !grads || !loss)
+    return fail(DPB_CONFIG_ERROR, "null pointer argument");
+  cudaStream_t st = m->stream;
+  static const bool no_graph = std::getenv("DPB_MODEL_NO_GRAPH") != nullptr;
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  const bool legacy = st == nullptr || st == cudaStreamLegacy || st == cudaStreamPerThread;
+  if (no_graph || legacy || cudaStreamIsCapturing(st, &cs) != cudaSuccess || cs != cudaStreamCaptureStatusNone)
+    return model_step_launch(m, input, labels, params, running, grads, loss);
+  const void* key[6] = {input, labels, params, running, grads, loss};
+  if (m->graph == nullptr || std::memcmp(key, m->graph_key, sizeof(key)) != 0) {
+    if (m->graph) {
+      cudaGraphExecDestroy(m->graph);
+      m->graph = nullptr;
+    }
+    cudaError_t e = cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal);
+    if (e != cudaSuccess) return cuda_fail(e, "model step capture");
+    const int rc = model_step_launch(m, input, labels, params, running, grads, loss);
+    cudaGraph_t g = nullptr;
+    e = cudaStreamEndCapture(st, &g);
+    if (rc != DPB_OK) {
+      if (g) cudaGraphDestroy(g);
+      return rc;
+    }
+    if (e != cudaSuccess) return cuda_fail(e, "model step capture");
+    e = cudaGraphInstantiate(&m->graph, g, 0);
+    cudaGraphDestroy(g);
+    if (e != cudaSuccess) {
+      m->graph = nullptr;
+      return cuda_fail(e, "model step graph instantiate");
+    }
+    std::memcpy(m->graph_key, key, sizeof(key));
+  }
+  const cudaError_t e = cudaGraphLaunch(m->graph, st);
+  return e == cudaSuccess ? DPB_OK : cuda_fail(e, "model step graph launch");
 }
 
 }  // extern "C"

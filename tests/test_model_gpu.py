@@ -111,3 +111,42 @@ def test_model_bad_label_raises():
     with pytest.raises(LabelError):
         plan.sync()
     plan.close()
+
+
+def test_model_graph_replay_matches_eager():
+    """dpb_model_step on a created stream captures the step into a CUDA graph and
+    replays it while the buffers stay the same, re-capturing when they change:
+    bit-identical to the eager launches (DPB_MODEL_NO_GRAPH semantics: a default
+    stream launches eagerly)."""
+    g = _load("model_bc")
+    n, cin, h, w = (int(v) for v in g["in_shape"])
+    cfg = DenseNetConfig(tuple(int(b) for b in g["blocks"]), int(g["k"]), True, float(g["compression"]),
+                         int(g["classes"]), int(g["c0"]), (cin, h, w))
+    params = torch.from_numpy(g["params"]).cuda()
+    x = torch.from_numpy(g["x"]).cuda()
+    labels = torch.from_numpy(g["labels"]).cuda()
+
+    def run(stream):
+        plan = ModelPlan(cfg, n, dtype="bf16", stream=stream)
+        running = plan.initial_running()
+        loss = torch.zeros(1, device="cuda")
+        grads = torch.empty(plan.param_elems, device="cuda")
+        outs = []
+        for step in range(4):
+            if step == 2:  # new buffers: the graph is captured again
+                grads = torch.empty(plan.param_elems, device="cuda")
+            grads.fill_(float("nan"))
+            torch.cuda.synchronize()
+            plan.step(x, labels, params, running, grads, loss)
+            plan.sync()
+            torch.cuda.synchronize()
+            outs.append((grads.cpu().numpy().copy(), loss.cpu().numpy().copy(), running.cpu().numpy().copy()))
+        plan.close()
+        return outs
+
+    eager = run(None)
+    graphed = run(torch.cuda.Stream())
+    for step, (a, b) in enumerate(zip(eager, graphed)):
+        for t_a, t_b, what in zip(a, b, ("grads", "loss", "running")):
+            assert np.isfinite(t_b).all(), f"step {step} {what}"
+            assert np.array_equal(t_a, t_b), f"step {step} {what} differs between graph replay and eager"
