@@ -88,7 +88,8 @@ __global__ void __launch_bounds__(kThreads, Op::kMinBlocks) tc_halo_kernel(const
 
   const int tid = threadIdx.x;
   const int warp = tid / 32, lane = tid % 32;
-  const bool dbg = g_phase_on && tid == 0 && blockIdx.x + blockIdx.y * gridDim.x < 4096;
+  // g_phase_on: 1 stamps the ops with column sums (forward, dgrad), 2 the wgrad
+  const bool dbg = g_phase_on == (Op::kColSums ? 1 : 2) && tid == 0 && blockIdx.x + blockIdx.y * gridDim.x < 4096;
   const int dbg_id = blockIdx.x + blockIdx.y * gridDim.x;
   if (dbg) g_phase_clock[dbg_id][0] = clock64();
   const uint32_t SB = op.stage_bytes();
@@ -656,7 +657,7 @@ struct Tc3x3WgradHalo {
   static constexpr int kTmemCols = 9 * BN;
   static constexpr bool kColSums = false;
   static constexpr bool kBulk = false;
-  static constexpr int kMaxChunks = 4;
+  static constexpr int kMaxChunks = 6;  // bk = 48 at W = 32: 1456 chunks, one load batch
   HaloArgs h;
   int tpc;      // tiles per CTA
   int ntiles;   // total tiles = N * tpi
@@ -682,7 +683,10 @@ struct Tc3x3WgradHalo {
     const int im = gt / h.g.tpi, t = gt - im * h.g.tpi;
     const int64_t pix0 = static_cast<int64_t>(im) * h.g.H * h.g.W;
     const int j_base = blockIdx.y * kBM;
-    const int groups = kBM / 8;
+    // only the channel groups below bk: the A rows j >= bk feed only D rows the
+    // epilogue drops (an MMA row depends on its own A row), so they stay unwritten
+    const int jn = a.bk - j_base < kBM ? a.bk - j_base : kBM;
+    const int groups = (jn + 7) / 8;
     const int nchunk = h.g.R * groups;  // act_b halo chunks; then dY chunks
     const int og = BN / 8;
     const int ndy = kBM * og;

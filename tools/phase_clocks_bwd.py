@@ -30,13 +30,15 @@ torch.cuda.synchronize()
 plan.forward(x, p, run, True)
 torch.cuda.synchronize()
 FLAGS = int(sys.argv[1]) if len(sys.argv) > 1 else 0
-f(1 | (FLAGS << 16), None, 0)
+WHICH = 2 if len(sys.argv) > 2 and sys.argv[2] == "wgrad" else 1
+f(WHICH | (FLAGS << 16), None, 0)
 plan.backward(p, acc.clone(), g)
 torch.cuda.synchronize()
 f(0, None, 0)
 buf = np.zeros((4096, 9), dtype=np.int64)
-f(-1, C.c_void_p(buf.ctypes.data), 576)
-b = buf[:576]
+NCTA = 576 if WHICH == 1 else 288
+f(-1, C.c_void_p(buf.ctypes.data), NCTA)
+b = buf[:NCTA]
 ph = np.diff(b, axis=1)
 for i, name in enumerate(["prologue+alloc", "produce", "issue", "mma wait", "epilogue loop", "epi barrier", "col sums", "dealloc"]):
     print(f"{name:18s} mean {ph[:, i].mean():8.0f}  p50 {np.median(ph[:, i]):8.0f}  max {ph[:, i].max():8.0f}")
