@@ -324,9 +324,8 @@ int tc_conv3x3_wgrad(Block* b, LayerArgs<float> a) {
 extern "C" __attribute__((visibility("default"))) int dpb_debug_phase_clocks(int enable, long long* host,
                                                                              int n) {
   if (enable >= 0) {
-    const int on = enable & 0xFFFF, flags = enable >> 16;
+    const int on = enable & 0xFFFF;
     cudaMemcpyToSymbol(dpb::tc::g_phase_on, &on, sizeof(int));
-    cudaMemcpyToSymbol(dpb::tc::g_phase_flags, &flags, sizeof(int));
     return 0;
   }
   return cudaMemcpyFromSymbol(host, dpb::tc::g_phase_clock, sizeof(long long) * 9 * n);

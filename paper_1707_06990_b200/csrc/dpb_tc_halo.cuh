@@ -71,7 +71,6 @@ __device__ __forceinline__ uint32_t halo_mnmajor(int R, int j, int pos) {
 // barrier passed, column sums written, exit.
 __device__ long long g_phase_clock[4096][9];
 __device__ int g_phase_on;
-__device__ int g_phase_flags;  // A/B: 1 skip z load, 2 skip t0 store, 4 skip column sums, 8 skip mask
 
 // ---- engine ----------------------------------------------------------------------
 // As tc_gemm_kernel, but the op owns the stage layout and the MMA issue
@@ -214,7 +213,7 @@ __global__ void __launch_bounds__(kThreads, Op::kMinBlocks) tc_halo_kernel(const
     }
     float s1[8], s2[8];
     op.epilogue(row, cc * 8, v, aux, s1, s2);
-    if (Op::kColSums && !(g_phase_flags & 4)) {
+    if constexpr (Op::kColSums) {
       const float x = warp_colsum8(s1, lane);
       const float y = warp_colsum8(s2, lane);
       if ((lane & 3) == 0) {
@@ -607,16 +606,12 @@ struct Tc3x3DgradHalo {
     const int nv = pp >= 0 ? a.bk - col0 : 0;
     float zv[8], g[8];
     const int64_t p = static_cast<int64_t>(img()) * h.g.H * h.g.W + (pp >= 0 ? pp : 0);
-    const int fl = g_phase_flags;
-    if (nv > 0 && !(fl & 1)) load8(a.z + p * a.bk + col0, nv, (a.bk & 3) == 0, zv);
-    else
-#pragma unroll
-      for (int i = 0; i < 8; ++i) zv[i] = v[i];
+    if (nv > 0) load8(a.z + p * a.bk + col0, nv, (a.bk & 3) == 0, zv);
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
       if (i < nv) {
         const BnFwd b = bn[col0 + i];
-        g[i] = (fl & 8) || relu_mask_ref(b, zv[i]) ? v[i] : 0.f;
+        g[i] = relu_mask_ref(b, zv[i]) ? v[i] : 0.f;
         s1[i] = g[i];
         s2[i] = g[i] * ((zv[i] - b.mean) * b.inv);
       } else {
@@ -625,7 +620,7 @@ struct Tc3x3DgradHalo {
         s2[i] = 0.f;
       }
     }
-    if (nv > 0 && !(fl & 2)) {
+    if (nv > 0) {
       float* dst = a.g0 + p * a.bk + col0;
       if ((a.bk & 3) == 0 && nv >= 8) {
         reinterpret_cast<float4*>(dst)[0] = make_float4(g[0], g[1], g[2], g[3]);

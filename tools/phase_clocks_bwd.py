@@ -1,6 +1,7 @@
 """Debug: per-phase CTA timing of the halo 3x3 dgrad (dpb_debug_phase_clocks).
 Run with DPB_NO_FORK=1: the backward is then serial and its last halo launch
-is layer 0's 3x3 dgrad (BC-100 block-1 geometry)."""
+is layer 0's 3x3 dgrad (BC-100 block-1 geometry).  `python tools/phase_clocks_bwd.py wgrad`
+stamps the 3x3 wgrad instead."""
 import ctypes as C
 import os
 import sys
@@ -29,9 +30,8 @@ for _ in range(2):
 torch.cuda.synchronize()
 plan.forward(x, p, run, True)
 torch.cuda.synchronize()
-FLAGS = int(sys.argv[1]) if len(sys.argv) > 1 else 0
-WHICH = 2 if len(sys.argv) > 2 and sys.argv[2] == "wgrad" else 1
-f(WHICH | (FLAGS << 16), None, 0)
+WHICH = 2 if len(sys.argv) > 1 and sys.argv[1] == "wgrad" else 1
+f(WHICH, None, 0)
 plan.backward(p, acc.clone(), g)
 torch.cuda.synchronize()
 f(0, None, 0)
