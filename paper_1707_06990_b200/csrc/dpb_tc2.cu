@@ -229,9 +229,7 @@ int tc2_conv1x1_wgrad(Block* b, const LayerArgs<float>& a) {
 // with layer width c (c <= 0 disarms), or read them (host: 148 x 28 int64).
 extern "C" __attribute__((visibility("default"))) int dpb_debug_tc2_clocks(int c, long long* host) {
   if (host == nullptr) {
-    const int flags = c >> 16;
     c &= 0xffff;
-    cudaMemcpyToSymbol(dpb::tc2::g_tc2_dbg_flags, &flags, sizeof(int));
     return cudaMemcpyToSymbol(dpb::tc2::g_tc2_dbg_c, &c, sizeof(int));
   }
   return cudaMemcpyFromSymbol(host, dpb::tc2::g_tc2_clock, sizeof(long long) * 148 * 28);

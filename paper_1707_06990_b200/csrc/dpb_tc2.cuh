@@ -93,7 +93,6 @@ __device__ __forceinline__ long long dbg_now() {  // ns, synchronised across SMs
 // raw_full / op_empty; [27]: TMA thread wait for raw_empty (ns summed over the launch)
 __device__ long long g_tc2_clock[148][28];
 __device__ int g_tc2_dbg_c;
-__device__ int g_tc2_dbg_flags;  // A/B timing: bit 0 skips g1 stores, bit 1 skips column sums
 
 // ---- the engine ------------------------------------------------------------------
 // Op interface:
@@ -249,7 +248,7 @@ __global__ void __launch_bounds__(Roles<Op>::kThreads, 1) tc2_kernel(const __gri
             float s1[8], s2[8];
             op.epilogue(tile, row, cc * 8, *reinterpret_cast<const float(*)[8]>(&v[q2 * 8]), aux, ebox,
                         s1, s2);
-            if (Op::kColSums && !(g_tc2_dbg_flags & 2)) {
+            if constexpr (Op::kColSums) {
               const float x = warp_colsum8(s1, lane);
               const float y = warp_colsum8(s2, lane);
               if ((lane & 3) == 0) {

@@ -1,13 +1,12 @@
 """Debug: per-tile phase timing of the v2 engine (dpb_debug_tc2_clocks).
 
-    python tools/tc2_clocks.py [c] [flags] [fwd|bwd] [block]
+    python tools/tc2_clocks.py [c] [0] [fwd|bwd] [block]      (second argument reserved)
 
 c: the layer input width whose v2 launches stamp (default 204: BC-100 block 0,
 layer 15); block: the BC-100 block geometry (0, 1, 2).  The stamps are
 %globaltimer (ns, one clock for every SM), shown in us since the earliest CTA
 start of the recorded launch.  'fwd' records the layer's 1x1 forward; by
 default the backward runs last and its 1x1 dgrad's stamps are read.
-flags (A/B timing): 1 skip g1 stores, 2 skip column sums.
 """
 import ctypes as C
 import sys
