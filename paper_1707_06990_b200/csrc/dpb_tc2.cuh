@@ -106,6 +106,8 @@ __device__ int g_tc2_dbg_c;
 //   int epi_boxes(int tile) const;  void epi_tma(int tile, int b, uint32_t dst, uint64_t* bar) const;
 //                                                              one box per 4 chunks (32 columns)
 //   void epi_store(int tile, int b, uint32_t src) const;
+//   void prologue_early(uint8_t* aux) const;                   all threads, before the
+//                                                              grid-dependency wait
 //   void prologue(uint8_t* aux) const;                         all threads
 //   uint32_t raw_bytes(int tile, int kb) const;                bytes the stage's copies land
 //   void tma(int tile, int kb, uint32_t raw, uint64_t* bar) const;   one thread
@@ -166,7 +168,11 @@ __global__ void __launch_bounds__(Roles<Op>::kThreads, 1) tc2_kernel(const __gri
     tc::fence_barrier_init();
   }
   if (warp == kMmaWarp) tc::tmem_alloc<2 * TC>(&tmem_base);
-  pdl_enter();  // barrier init / TMEM alloc above overlap the predecessor
+  // Before the grid-dependency wait a kernel may read what the launches two or
+  // more back wrote (its predecessor passed its own wait before triggering this
+  // launch): the resident weight images, tiled at the start of the pass.
+  op.prologue_early(aux);
+  pdl_enter();  // barrier init / TMEM alloc / weight copies above overlap the predecessor
   op.prologue(aux);
   tc::fence_proxy_async();  // resident operand images written by generic stores
   tc::tc_fence_before();
@@ -387,12 +393,14 @@ struct Fwd1x1 {
   __device__ const BnAff* bn_table(const uint8_t* aux) const {
     return reinterpret_cast<const BnAff*>(aux + (RES ? b_all() : 0));
   }
-  __device__ void prologue(uint8_t* aux) const {
+  __device__ void prologue_early(uint8_t* aux) const {
     if (RES) {
       const uint4* src = reinterpret_cast<const uint4*>(w1t);
       uint4* dst = reinterpret_cast<uint4*>(aux);
       for (int q = threadIdx.x; q < static_cast<int>(b_all() / 16); q += blockDim.x) dst[q] = __ldg(src + q);
     }
+  }
+  __device__ void prologue(uint8_t* aux) const {
     fill_bn_aff(const_cast<BnAff*>(bn_table(aux)), a.c, 0, a.amean, a.avar, a.gamma_a, a.beta_a);
   }
   __device__ void tma(int tile, int kb, uint32_t raw, uint64_t* bar) const {
@@ -531,10 +539,12 @@ struct Dgrad1x1 {
   __device__ const BnFwd* bna(const uint8_t* aux) const {
     return reinterpret_cast<const BnFwd*>(aux + nkb() * kBTile + ((sizeof(BnBwd) * a.bk + 15) / 16) * 16);
   }
-  __device__ void prologue(uint8_t* aux) const {
+  __device__ void prologue_early(uint8_t* aux) const {
     const uint4* src = reinterpret_cast<const uint4*>(w1t + static_cast<int64_t>(blockIdx.y) * nkb() * kBTile);
     uint4* dst = reinterpret_cast<uint4*>(aux);
     for (int q = threadIdx.x; q < nkb() * kBTile / 16; q += blockDim.x) dst[q] = __ldg(src + q);
+  }
+  __device__ void prologue(uint8_t* aux) const {
     fill_bn_bwd(const_cast<BnBwd*>(bnb(aux)), a);
     fill_bn_fwd(const_cast<BnFwd*>(bna(aux)), ncols(), n0(), a.amean, a.avar, a.gamma_a, a.beta_a);
   }
@@ -667,6 +677,7 @@ struct Wgrad1x1 {
   __device__ const BnFwd* bna(const uint8_t* aux) const {
     return reinterpret_cast<const BnFwd*>(aux + ((sizeof(BnBwd) * a.bk + 15) / 16) * 16);
   }
+  __device__ void prologue_early(uint8_t*) const {}
   __device__ void prologue(uint8_t* aux) const {
     fill_bn_bwd(const_cast<BnBwd*>(bnb(aux)), a);
     fill_bn_fwd(const_cast<BnFwd*>(bna(aux)), ncols(), n0(), a.amean, a.avar, a.gamma_a, a.beta_a);
