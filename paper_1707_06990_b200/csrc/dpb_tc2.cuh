@@ -108,6 +108,8 @@ __device__ int g_tc2_dbg_c;
 //   void epi_store(int tile, int b, uint32_t src) const;
 //   void prologue_early(uint8_t* aux) const;                   all threads, before the
 //                                                              grid-dependency wait
+//   static constexpr bool kEarlyLoads;                          the first NR stages' TMA
+//                                                              loads may precede the wait
 //   void prologue(uint8_t* aux) const;                         all threads
 //   uint32_t raw_bytes(int tile, int kb) const;                bytes the stage's copies land
 //   void tma(int tile, int kb, uint32_t raw, uint64_t* bar) const;   one thread
@@ -172,6 +174,21 @@ __global__ void __launch_bounds__(Roles<Op>::kThreads, 1) tc2_kernel(const __gri
   // more back wrote (its predecessor passed its own wait before triggering this
   // launch): the resident weight images, tiled at the start of the pass.
   op.prologue_early(aux);
+  // ... and, for ops whose TMA operands are at least two launches old
+  // (kEarlyLoads), the first ring stages: the TMA thread initialised the
+  // barriers itself, and the ring starts empty.
+  int early = 0;
+  if constexpr (Op::kEarlyLoads) {
+    if (tid == 0) {
+      op.prefetch();
+      const int nt = op.num_tiles();
+      for (int tile = blockIdx.x; tile < nt && early < NR; tile += gridDim.x)
+        for (int kb = 0; kb < op.num_kb(tile) && early < NR; ++kb, ++early) {
+          mbar_expect_tx(&raw_full[early], op.raw_bytes(tile, kb));
+          op.tma(tile, kb, tc::smem_u32(raw_ring + early * Op::kRawBytes), &raw_full[early]);
+        }
+    }
+  }
   pdl_enter();  // barrier init / TMEM alloc / weight copies above overlap the predecessor
   op.prologue(aux);
   tc::fence_proxy_async();  // resident operand images written by generic stores
@@ -188,6 +205,7 @@ __global__ void __launch_bounds__(Roles<Op>::kThreads, 1) tc2_kernel(const __gri
       int it = 0;
       for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x)
         for (int kb = 0; kb < op.num_kb(tile); ++kb, ++it) {
+          if (it < early) continue;  // issued before the wait
           const int r = it % NR;
           const long long w0 = dbg ? dbg_now() : 0;
           tc::mbar_wait(&raw_empty[r], ((it / NR) & 1) ^ 1);
@@ -361,6 +379,7 @@ template <int BN_, bool RES>
 struct Fwd1x1 {
   static constexpr int BN = BN_;
   static constexpr int kTmemCols = BN;
+  static constexpr bool kEarlyLoads = true;  // features / g0 / z: >= two launches old
   static constexpr bool kColSums = true;
   static constexpr bool kMmaReadsRaw = !RES;
   static constexpr int kBox = 32 * kBM * 4;                    // 16 KB
@@ -499,6 +518,7 @@ template <int BN_>
 struct Dgrad1x1 {
   static constexpr int BN = BN_;
   static constexpr int kTmemCols = BN;
+  static constexpr bool kEarlyLoads = true;  // g0 (3x3 dgrad) and z: >= two launches old
   static constexpr bool kColSums = true;
   static constexpr bool kMmaReadsRaw = false;
   static constexpr int kBox = 32 * kBM * 4;        // 16 KB: 128 rows x 32 fp32 channels
@@ -635,6 +655,7 @@ struct Wgrad1x1 {
   static constexpr int BN = BN_;
   static constexpr int kMT = (JB * 32 + 127) / 128;
   static constexpr int kTmemCols = kMT * BN;
+  static constexpr bool kEarlyLoads = false;  // side stream: behind an event, not a PDL edge
   static constexpr bool kColSums = false;
   static constexpr bool kMmaReadsRaw = false;
   static constexpr int kBoxP = 32;                       // pixels per K block
