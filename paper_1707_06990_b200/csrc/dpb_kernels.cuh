@@ -191,16 +191,31 @@ k_bn_apply_accumulate4(int64_t M, int c, int C, int Ca, int cg, const float* __r
                        const float* __restrict__ g1, const float* __restrict__ amean,
                        const float* __restrict__ avar, const float* __restrict__ gamma,
                        const float* __restrict__ coef, float* __restrict__ acc) {
-  pdl_enter();
   const int cq = (c + 3) >> 2;
   const int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   const int64_t pg = t / cq;
   const int q = static_cast<int>(t - pg * cq);
   const int64_t p0 = pg * kApplyRows;
-  if (p0 >= M) return;
+  if (p0 >= M) {
+    pdl_enter();
+    return;
+  }
   const int ch = 4 * q;
+  // Only the BN_a coefficients come from the predecessor (the finalize); g1 is
+  // the 1x1 dgrad's output two launches back, and the features, statistics and
+  // accumulator are older.  So the first rows are loaded before the
+  // grid-dependency wait.
   const float4 mean = *reinterpret_cast<const float4*>(amean + ch);
   const float4 var = *reinterpret_cast<const float4*>(avar + ch);
+  constexpr int kPre = 2;
+  float4 xp[kPre], gp[kPre];
+#pragma unroll
+  for (int i = 0; i < kPre; ++i) {
+    const int64_t p = p0 + i < M ? p0 + i : p0;
+    xp[i] = *reinterpret_cast<const float4*>(feat + p * C + ch);
+    gp[i] = *reinterpret_cast<const float4*>(g1 + p * cg + ch);
+  }
+  pdl_enter();
   const float4 c01 = *reinterpret_cast<const float4*>(coef + 2 * ch);      // mg0 mgx0 mg1 mgx1
   const float4 c23 = *reinterpret_cast<const float4*>(coef + 2 * ch + 4);  // mg2 mgx2 mg3 mgx3
   const float m[4] = {mean.x, mean.y, mean.z, mean.w};
@@ -212,9 +227,7 @@ k_bn_apply_accumulate4(int64_t M, int c, int C, int Ca, int cg, const float* __r
 #pragma unroll
   for (int e = 0; e < 4; ++e) gi[e] = e < live ? gamma[ch + e] * inv[e] : 0.f;
   const int64_t pe = p0 + kApplyRows < M ? p0 + kApplyRows : M;
-  for (int64_t p = p0; p < pe; ++p) {
-    const float4 x4 = *reinterpret_cast<const float4*>(feat + p * C + ch);
-    const float4 g4 = *reinterpret_cast<const float4*>(g1 + p * cg + ch);
+  auto row = [&](int64_t p, const float4 x4, const float4 g4) {
     const float x[4] = {x4.x, x4.y, x4.z, x4.w};
     const float g[4] = {g4.x, g4.y, g4.z, g4.w};
     float r[4];
@@ -234,7 +247,12 @@ k_bn_apply_accumulate4(int64_t M, int c, int C, int Ca, int cg, const float* __r
     } else {  // last quad of a layer with c % 4 != 0: channels >= c belong to later layers
       for (int e = 0; e < live; ++e) arow[e] += r[e];
     }
-  }
+  };
+#pragma unroll
+  for (int i = 0; i < kPre; ++i)
+    if (p0 + i < pe) row(p0 + i, xp[i], gp[i]);
+  for (int64_t p = p0 + kPre; p < pe; ++p)
+    row(p, *reinterpret_cast<const float4*>(feat + p * C + ch), *reinterpret_cast<const float4*>(g1 + p * cg + ch));
 }
 
 // Split-K weight-gradient folds.  Block (32 x 8): 32 consecutive partial
