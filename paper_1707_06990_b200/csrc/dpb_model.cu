@@ -4,7 +4,9 @@
 // through the block path (dpb_block.cu); everything here is small next to
 // them (the transitions' 1x1 convs are ~3% of BC-100's FLOPs), so these
 // kernels are plain fp32 CUDA-core code with fixed-order reductions
-// (deterministic).  Activations are NHWC fp32 like the block arenas.
+// (deterministic), except the transitions' forward and pooled-input-gradient
+// GEMMs of the bf16 path (TransGemm on the tcgen05 engine, bf16x3 products).
+// Activations are NHWC fp32 like the block arenas.
 //
 // Transition: BN (batch statistics of every feature channel are already in
 // the block's arena, F6) -> ReLU -> 2x2 average pool -> 1x1 conv.  The
@@ -23,6 +25,7 @@
 #include "dpb_common.cuh"
 #include "dpb_internal.h"
 #include "dpb_launch.h"
+#include "dpb_tc.cuh"
 
 struct dpb_model;
 
@@ -200,6 +203,104 @@ __global__ void __launch_bounds__(256) k_gemm(int M, int N, int K, const float* 
       const int gm = m0 + ty * 4 + i, gn = n0 + tx * 4 + j;
       if (gm < M && gn < N) out[static_cast<int64_t>(gm) * ldc + gn] = acc[i][j];
     }
+}
+
+// Transition GEMMs of the bf16 path on the tcgen05 engine (tc_gemm_kernel):
+// D[M][N] = A . B^T with fp32 operands split into bf16 hi | lo (three MMAs per
+// K step, ~16-bit products), fp32 accumulation in TMEM.  A is K-major with row
+// pitch lda; B is K-major ([N][K], pitch ldb) or MN-major ([K][N], BMN);
+// D has row pitch ldd.  Used for the forward conv (P . W^T) and the pooled-input
+// gradient (g_pool . W); the fp32 path keeps k_gemm.
+template <int BMN>
+struct TransGemm {
+  static constexpr int BN = 128;
+  static constexpr bool kSplit = true;
+  static constexpr int kAMN = 0, kBMN = BMN;
+  static constexpr bool kColSums = false;
+  const float* A;
+  const float* B;
+  float* D;
+  int M, N, K, lda, ldb, ldd;
+
+  __device__ int num_kb() const { return (K + tc::kBK - 1) / tc::kBK; }
+  __device__ void prologue(uint8_t*) const {}
+  // 8 consecutive elements of row `r` (pitch ld, `n` valid), vectorised when aligned
+  __device__ static void load8(const float* G, int64_t ld, int r, int rows, int c0, int n, float (&v)[8]) {
+    if (r < rows && c0 + 8 <= n && (ld & 3) == 0) {
+      const float4* q = reinterpret_cast<const float4*>(G + static_cast<int64_t>(r) * ld + c0);
+      const float4 a = __ldg(q), b = __ldg(q + 1);
+      v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w;
+      v[4] = b.x; v[5] = b.y; v[6] = b.z; v[7] = b.w;
+    } else {
+#pragma unroll
+      for (int i = 0; i < 8; ++i)
+        v[i] = (r < rows && c0 + i < n) ? __ldg(G + static_cast<int64_t>(r) * ld + c0 + i) : 0.f;
+    }
+  }
+  __device__ void produce(uint8_t* a_hi, uint8_t* a_lo, uint8_t* b_hi, uint8_t* b_lo, int kb,
+                          const uint8_t*) const {
+    const int k0 = kb * tc::kBK;
+    for (int q = threadIdx.x; q < tc::kBM * tc::kBK / 8; q += tc::kThreads) {
+      int row, kc;
+      tc::kmajor_coords(q, row, kc);
+      float v[8];
+      load8(A, lda, blockIdx.x * tc::kBM + row, M, k0 + kc, K, v);
+      uint4 h, l;
+      tc::split8_fast(v, h, l);
+      const uint32_t off = tc::Tile<tc::kBM>::kmajor_chunk(row, kc);
+      tc::st_shared16(a_hi, off, h);
+      tc::st_shared16(a_lo, off, l);
+    }
+    for (int q = threadIdx.x; q < BN * tc::kBK / 8; q += tc::kThreads) {
+      float v[8];
+      uint32_t off;
+      if (BMN == 0) {
+        int row, kc;
+        tc::kmajor_coords(q, row, kc);
+        load8(B, ldb, blockIdx.y * BN + row, N, k0 + kc, K, v);
+        off = tc::Tile<BN>::kmajor_chunk(row, kc);
+      } else {
+        int rg, kr;
+        tc::mnmajor_coords<BN>(q, rg, kr);
+        load8(B, ldb, k0 + kr, K, blockIdx.y * BN + rg, N, v);  // row k of [K][N]
+        off = tc::Tile<BN>::mnmajor_chunk(rg, kr);
+      }
+      uint4 h, l;
+      tc::split8_fast(v, h, l);
+      tc::st_shared16(b_hi, off, h);
+      tc::st_shared16(b_lo, off, l);
+    }
+  }
+  __device__ void epilogue(int row, int col0, const float (&v)[8], const uint8_t*, float (&)[8],
+                           float (&)[8]) const {
+    const int gr = blockIdx.x * tc::kBM + row, gc = blockIdx.y * BN + col0;
+    if (gr >= M) return;
+    float* d = D + static_cast<int64_t>(gr) * ldd + gc;
+    if (gc + 8 <= N && (ldd & 3) == 0) {
+      reinterpret_cast<float4*>(d)[0] = make_float4(v[0], v[1], v[2], v[3]);
+      reinterpret_cast<float4*>(d)[1] = make_float4(v[4], v[5], v[6], v[7]);
+    } else {
+#pragma unroll
+      for (int i = 0; i < 8; ++i)
+        if (gc + i < N) d[i] = v[i];
+    }
+  }
+  __device__ void col_sums(int, double, double) const {}
+};
+
+template <int BMN>
+void trans_gemm(cudaStream_t st, int M, int N, int K, const float* A, int lda, const float* B, int ldb,
+                float* D, int ldd) {
+  using Op = TransGemm<BMN>;
+  static bool init = false;
+  if (!init) {
+    cudaFuncSetAttribute(tc::tc_gemm_kernel<Op>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         static_cast<int>(tc::stage_bytes<Op>()));
+    init = true;
+  }
+  const Op op{A, B, D, M, N, K, lda, ldb, ldd};
+  launch(tc::tc_gemm_kernel<Op>, dim3((M + tc::kBM - 1) / tc::kBM, (N + Op::BN - 1) / Op::BN), tc::kThreads,
+         tc::stage_bytes<Op>(), st, op);
 }
 
 // ---- head forward: gap[n][c] = mean_hw relu(bn(feat)) ---------------------------------
@@ -753,9 +854,12 @@ int model_step_launch(dpb_model* m, const float* input, const int32_t* labels, c
       ModelBlock& nx = m->blocks[b + 1];
       launch(k_trans_pool, dim3(blocks_of(t.C, 128), static_cast<unsigned>(std::min<int64_t>(t.Mq, 65535))), 128,
              0, st, feat, mb.Cp, N, mb.h, mb.w, t.C, mean, var, params + t.gamma, params + t.beta, t.P);
-      launch(k_gemm<false, true>, dim3(blocks_of(t.Mq, 64), blocks_of(t.cout, 64), 1), 256, 0, st,
-             static_cast<int>(t.Mq), t.cout, t.C, static_cast<const float*>(t.P), t.C, params + t.w, t.C, nx.x,
-             nx.c0, t.C);
+      if (d.dtype == DPB_BF16)
+        trans_gemm<0>(st, static_cast<int>(t.Mq), t.cout, t.C, t.P, t.C, params + t.w, t.C, nx.x, nx.c0);
+      else
+        launch(k_gemm<false, true>, dim3(blocks_of(t.Mq, 64), blocks_of(t.cout, 64), 1), 256, 0, st,
+               static_cast<int>(t.Mq), t.cout, t.C, static_cast<const float*>(t.P), t.C, params + t.w, t.C, nx.x,
+               nx.c0, t.C);
       launch(k_running, blocks_of(t.C, 256), 256, 0, st, t.C, mean, var, running + t.run,
              running + t.run + t.C);
     } else {
@@ -814,9 +918,12 @@ int model_step_launch(dpb_model* m, const float* input, const int32_t* labels, c
              static_cast<int>(t.Mq), static_cast<const float*>(mb.acc), mb.Cp, static_cast<const float*>(t.P), t.C,
              t.wpart, t.C, static_cast<int>(chunk));
       launch_fold_splits(ws, t.wpart, S, static_cast<int64_t>(t.cout) * t.C, grads + t.w);
-      launch(k_gemm<false, false>, dim3(blocks_of(t.Mq, 64), blocks_of(t.C, 64), 1), 256, 0, st,
-             static_cast<int>(t.Mq), t.C, t.cout, static_cast<const float*>(mb.acc), mb.Cp, params + t.w, t.C, t.gP,
-             t.C, t.cout);
+      if (d.dtype == DPB_BF16)
+        trans_gemm<1>(st, static_cast<int>(t.Mq), t.C, t.cout, mb.acc, mb.Cp, params + t.w, t.C, t.gP, t.C);
+      else
+        launch(k_gemm<false, false>, dim3(blocks_of(t.Mq, 64), blocks_of(t.C, 64), 1), 256, 0, st,
+               static_cast<int>(t.Mq), t.C, t.cout, static_cast<const float*>(mb.acc), mb.Cp, params + t.w, t.C,
+               t.gP, t.C, t.cout);
       const float* feat = static_cast<const float*>(pv.blk->feat);
       const float* mean = pv.blk->fstat;
       const float* var = pv.blk->fstat + pv.blk->g.Cp;
