@@ -563,10 +563,11 @@ struct Dgrad1x1 {
     const uint4* src = reinterpret_cast<const uint4*>(w1t + static_cast<int64_t>(blockIdx.y) * nkb() * kBTile);
     uint4* dst = reinterpret_cast<uint4*>(aux);
     for (int q = threadIdx.x; q < nkb() * kBTile / 16; q += blockDim.x) dst[q] = __ldg(src + q);
+    // BN_a forward statistics and parameters: old
+    fill_bn_fwd(const_cast<BnFwd*>(bna(aux)), ncols(), n0(), a.amean, a.avar, a.gamma_a, a.beta_a);
   }
   __device__ void prologue(uint8_t* aux) const {
-    fill_bn_bwd(const_cast<BnBwd*>(bnb(aux)), a);
-    fill_bn_fwd(const_cast<BnFwd*>(bna(aux)), ncols(), n0(), a.amean, a.avar, a.gamma_a, a.beta_a);
+    fill_bn_bwd(const_cast<BnBwd*>(bnb(aux)), a);  // the BN_b coefficients: the predecessor's output
   }
   __device__ void tma(int tile, int kb, uint32_t raw, uint64_t* bar) const {
     tma_load_2d(raw, &gmap, kb * 32, tile * kBM, bar);

@@ -104,8 +104,11 @@ __global__ void __launch_bounds__(kThreads, Op::kMinBlocks) tc_halo_kernel(const
     mbar_init(&bbar[1], 1);
     fence_barrier_init();
   }
-  pdl_enter();  // barrier init / TMEM alloc above overlap the predecessor
-  op.prologue(aux);
+  // tables built from data two or more launches old (see dpb_tc2.cuh) are
+  // filled before the grid-dependency wait
+  if constexpr (Op::kEarlyPrologue) op.prologue(aux);
+  pdl_enter();  // barrier init / TMEM alloc / early tables above overlap the predecessor
+  if constexpr (!Op::kEarlyPrologue) op.prologue(aux);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -334,6 +337,7 @@ struct Tc3x3FwdHalo {
   static constexpr int kIssuers = BN <= 32 ? 8 : 3, kAccCopies = kIssuers;
   static constexpr int kTmemCols = BN * kAccCopies;
   static constexpr bool kTapCols = false;
+  static constexpr bool kEarlyPrologue = false;  // BN_b statistics: the predecessor's output
   static constexpr int kMinBlocks = 2;
   static constexpr bool kColSums = true;
   static constexpr bool kBulk = true;
@@ -531,6 +535,7 @@ struct Tc3x3DgradHalo {
   // phases (halo loads, MMAs, the z-dependent epilogue) then overlap
   static constexpr int kIssuers = 1, kAccCopies = 1;
   static constexpr bool kTapCols = false;
+  static constexpr bool kEarlyPrologue = true;  // BN_b forward statistics and parameters
   static constexpr int kMinBlocks = BN <= 64 ? 4 : 2;
   static constexpr int kTmemCols = BN * kAccCopies;
   static constexpr bool kColSums = true;
@@ -648,6 +653,7 @@ struct Tc3x3WgradHalo {
   static constexpr int BN = BN_;
   static constexpr int kIssuers = 3, kAccCopies = 1;  // taps t = warp, warp+3, warp+6
   static constexpr bool kTapCols = false;
+  static constexpr bool kEarlyPrologue = true;  // BN_b forward statistics and parameters
   static constexpr int kMinBlocks = 2;
   static constexpr int kTmemCols = 9 * BN;
   static constexpr bool kColSums = false;
