@@ -5,6 +5,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 
 #include "dpb_internal.h"
 #include "dpb_launch.h"
@@ -102,6 +103,19 @@ void tc2_pretile_w1(Block* b, const float* params) {
   b->launches++;
 }
 
+// Persistent CTAs for `ntiles` tiles on `slots` SMs: as many rounds as the
+// full grid needs, but no more CTAs than those rounds require (512 tiles on
+// 148 SMs: 128 CTAs x 4 tiles, not 148 CTAs of 3-4), so the SMs a short last
+// round leaves idle are free for the other stream and the next launch.
+// DPB_NO_BALANCE=1: one CTA per SM.
+static int balanced_ctas(int ntiles, int slots) {
+  static const bool off = std::getenv("DPB_NO_BALANCE") != nullptr;
+  slots = std::max(1, slots);
+  if (off) return std::max(1, std::min(ntiles, slots));
+  const int rounds = (ntiles + slots - 1) / slots;
+  return std::max(1, (ntiles + rounds - 1) / rounds);
+}
+
 // 1x1 forward on the v2 engine; false when the shape is not supported (the
 // caller then uses the v1 kernel).
 bool tc2_conv1x1_fwd(Block* b, const LayerArgs<float>& a, int l) {
@@ -117,7 +131,7 @@ bool tc2_conv1x1_fwd(Block* b, const LayerArgs<float>& a, int l) {
     if (!make_map_f32(&op.xmap, a.feat, a.C, a.M, a.C, 32, tc::kBM)) return false;
     op.a = a;
     op.w1t = w1t;
-    launch2(b, op, dim3(std::min(ntiles, num_sms())), aux);
+    launch2(b, op, dim3(balanced_ctas(ntiles, num_sms())), aux);
     return true;
   };
   // B resident in shared memory when all of W1's tiles fit, else streamed
@@ -173,7 +187,7 @@ bool tc2_conv1x1_dgrad(Block* b, const LayerArgs<float>& a, int l) {
     int nn, nw;
     tc2::bwd_ntiles(a.c, Op::BN, nn, nw);
     op.nw = nw;
-    const int gx = std::max(1, std::min(ntiles, num_sms() / nn));
+    const int gx = balanced_ctas(ntiles, std::max(1, num_sms() / nn));
     launch2(b, op, dim3(gx, nn), aux);
     return true;
   };
