@@ -14,6 +14,7 @@ oracle/_ref/libdenseplan_ref.so: the block-level harness over the public
 from __future__ import annotations
 
 import json
+import sys
 import os
 
 import numpy as np
@@ -115,8 +116,66 @@ def make_model_case(name, blocks, k, comp, classes, c0, in_shape, seed):
                         x=x, labels=labels, loss=np.float64(loss), grads=grads)
 
 
+# Config text KATs (densenet.hpp:86-115, 276-377): every preset through
+# config_to_text, and texts through config_from_key_values(parse_key_values),
+# including the reference's error class and message for the malformed ones.
+CONFIG_PRESETS = ["desk", "tiny", "paper-264-k48", "paper-264-k32", "paper-232-k48", "bc-160-k12", "nope"]
+CONFIG_TEXTS = [
+    "",
+    "blocks=16,16,16\ngrowth_rate=12\nbottleneck=1\ncompression=0.5\ninitial_channels=24\n"
+    "activation=pre\nnum_classes=10\n",
+    "  # comment line\n\nblocks=6,12 # trailing comment\n  growth_rate=32  \n\tbottleneck=1\r\n",
+    "blocks = 1",
+    "blocks=1,,2",
+    "blocks=1,2,",
+    "blocks=,1",
+    "blocks=1\ngarbage",
+    "blocks=1\ngrowth_rate=abc",
+    "blocks=1\ngrowth_rate=12abc",
+    "blocks=1\ncompression=1.5",
+    "blocks=1\ncompression=0.25e0",
+    "blocks=1\ncompression=.75",
+    "blocks=1\ncompression=0x1p-2",
+    "blocks=1\ncompression=nan",
+    "blocks=1\ncompression=inf",
+    "blocks=1\ncompression=1e999",
+    "blocks=1\ncompression=x",
+    "blocks=1\nactivation=mid",
+    "blocks=1\nactivation=post",
+    "blocks=0",
+    "blocks=2\nbottleneck=7",
+    "blocks=3\nblocks=4",
+    "blocks=+3",
+    "blocks= 3",
+    "blocks=3 ,4",
+    "growth_rate=-1\nblocks=1",
+    "initial_channels=0\nblocks=1",
+    "num_classes=0\nblocks=1",
+    "a=b=c\nblocks=1",
+    "=5\nblocks=1",
+    "blocks=99999999999",
+    "growth_rate=99999999999\nblocks=1",
+    "blocks=2,2\ngrowth_rate=8\ncompression=0.333333333\ninitial_channels=-5",
+    "blocks=1\nnum_classes=1000\ncompression=1",
+    "blocks=2,2\ngrowth_rate=8\ncompression=0.333333333\ninitial_channels=5",
+    "blocks=2\ncompression=0.1234567",
+    "blocks=2\ncompression=1e-7",
+]
+
+
+def config_kats():
+    presets = {name: O.ref_preset_text(name) for name in CONFIG_PRESETS}
+    texts = [{"text": t, "result": O.ref_parse_config(t), "roundtrip": O.ref_config_roundtrip(t)}
+             for t in CONFIG_TEXTS]
+    return {"presets": presets, "texts": texts}
+
+
 def main():
     os.makedirs(OUT, exist_ok=True)
+    with open(os.path.join(OUT, "config_kats.json"), "w") as f:
+        json.dump(config_kats(), f, indent=1, sort_keys=True)
+    if "--config-only" in sys.argv:
+        return
     for name, (s, src, dt) in CASES.items():
         make_case(name, s, src, dt)
     for name, args in MODEL_CASES.items():

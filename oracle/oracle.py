@@ -105,6 +105,12 @@ def ref_lib(fast: bool = False):
         L.ref_rng_u64.argtypes = [C.c_uint64, _I64, _P]
         L.ref_count_parameters.restype = C.c_int64
         L.ref_count_parameters.argtypes = cfg + [C.c_int]
+        L.ref_preset_text.restype = C.c_int
+        L.ref_preset_text.argtypes = [C.c_char_p, C.c_char_p, C.c_int]
+        L.ref_config_roundtrip.restype = C.c_int
+        L.ref_config_roundtrip.argtypes = [C.c_char_p, C.c_char_p, C.c_int]
+        L.ref_parse_config.restype = C.c_int
+        L.ref_parse_config.argtypes = [C.c_char_p, _P, C.c_int] + [_P] * 7
         L.ref_predict_peak_elements.restype = C.c_int
         L.ref_predict_peak_elements.argtypes = cfg + [C.c_int, _I64, C.c_int, C.c_int, C.c_int, _P]
         _ref[path] = L
@@ -429,3 +435,37 @@ def ref_save_training_checkpoint(blocks, k, compression, classes, c0, in_shape, 
     rc = ref_lib().ref_save_training_checkpoint(*args, c, h, w, n, seed, path.encode(), epoch)
     if rc != 0:
         raise RuntimeError(ref_lib().ref_last_error().decode())
+
+
+def ref_preset_text(name: str):
+    """config_to_text(preset_config(name)) from the reference, or (status, message)."""
+    buf = C.create_string_buffer(4096)
+    rc = ref_lib().ref_preset_text(name.encode(), buf, len(buf))
+    if rc:
+        return {"status": rc, "message": ref_lib().ref_last_error().decode()}
+    return {"text": buf.value.decode()}
+
+
+def ref_parse_config(text: str):
+    """The reference's config_from_key_values(parse_key_values(text)) as a dict,
+    or its error {status, message} (status = errors.hpp class index)."""
+    blocks = np.zeros(64, dtype=np.int32)
+    ints = [C.c_int() for _ in range(6)]
+    comp = C.c_double()
+    nb, k, bott, c0, post, classes = ints
+    rc = ref_lib().ref_parse_config(text.encode(), C.c_void_p(blocks.ctypes.data), 64, C.byref(nb), C.byref(k),
+                                    C.byref(bott), C.byref(comp), C.byref(c0), C.byref(post), C.byref(classes))
+    if rc:
+        return {"status": rc, "message": ref_lib().ref_last_error().decode()}
+    return {"blocks": [int(b) for b in blocks[:nb.value]], "growth_rate": k.value, "bottleneck": bool(bott.value),
+            "compression": comp.value, "initial_channels": c0.value,
+            "activation": "post" if post.value else "pre", "num_classes": classes.value}
+
+
+def ref_config_roundtrip(text: str):
+    """config_to_text of the reference's parse of `text`, or its error."""
+    buf = C.create_string_buffer(4096)
+    rc = ref_lib().ref_config_roundtrip(text.encode(), buf, len(buf))
+    if rc:
+        return {"status": rc, "message": ref_lib().ref_last_error().decode()}
+    return {"text": buf.value.decode()}

@@ -16,8 +16,10 @@
 #include <algorithm>
 #include <chrono>
 #include <cstdint>
+#include <cstdio>
 #include <cstring>
 #include <exception>
+#include <sstream>
 #include <string>
 #include <vector>
 
@@ -528,6 +530,41 @@ int ref_save_training_checkpoint(int nblocks, const int* blocks, int k, int bott
       for (std::int64_t j = 0; j < p.elems(); ++j) opt.velocity[i].data()[j] = 0.5f * p.data()[j];
     }
     save_training_checkpoint(path, plan, opt, epoch);
+  });
+}
+
+// config_to_text(preset_config(name)) (densenet.hpp:89-115, 279-297) into out[cap].
+int ref_preset_text(const char* name, char* out, int cap) {
+  return guarded([&] {
+    const std::string t = config_to_text(preset_config(name));
+    std::snprintf(out, static_cast<std::size_t>(cap), "%s", t.c_str());
+  });
+}
+
+// config_to_text(config_from_key_values(parse_key_values(text))): the round trip.
+int ref_config_roundtrip(const char* text, char* out, int cap) {
+  return guarded([&] {
+    std::istringstream in(text);
+    const std::string t = config_to_text(config_from_key_values(parse_key_values(in)));
+    std::snprintf(out, static_cast<std::size_t>(cap), "%s", t.c_str());
+  });
+}
+
+// config_from_key_values(parse_key_values(text)) (densenet.hpp:300-370): the
+// parsed configuration's fields, or the reference's error (ref_last_error).
+int ref_parse_config(const char* text, int* blocks, int cap, int* nblocks, int* k, int* bottleneck,
+                     double* compression, int* c0, int* post, int* classes) {
+  return guarded([&] {
+    std::istringstream in(text);
+    const DenseNetConfig cfg = config_from_key_values(parse_key_values(in));
+    *nblocks = static_cast<int>(cfg.block_sizes.size());
+    for (int i = 0; i < *nblocks && i < cap; ++i) blocks[i] = cfg.block_sizes[i];
+    *k = cfg.growth_rate;
+    *bottleneck = cfg.bottleneck ? 1 : 0;
+    *compression = cfg.compression;
+    *c0 = cfg.initial_channels;
+    *post = cfg.activation_order == ActivationOrder::PostActivation ? 1 : 0;
+    *classes = cfg.num_classes;
   });
 }
 

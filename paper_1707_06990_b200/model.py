@@ -29,6 +29,7 @@ class DenseNetConfig:
     num_classes: int = 10
     initial_channels: int = -1
     in_shape: tuple = (3, 32, 32)   # (c, h, w) of the network input
+    activation: str = "pre"         # "pre" | "post" (densenet.hpp ActivationOrder)
 
     @property
     def c0(self) -> int:
@@ -196,8 +197,9 @@ class ModelPlan:
         d.in_c, d.in_h, d.in_w = cfg.in_shape
         d.batch = batch
         d.dtype = {"fp32": 0, "bf16": 1}[dtype]
-        if not cfg.bottleneck:
-            raise ValueError("ModelPlan supports bottleneck (DenseNet-B/BC) networks only")
+        if not cfg.bottleneck or cfg.activation != "pre":
+            from .errors import ConfigError
+            raise ConfigError("ModelPlan implements pre-activation bottleneck (DenseNet-B/BC) networks only")
         self._desc = d
         pe, re_ = C.c_int64(), C.c_int64()
         check(lib().dpb_model_sizes(C.byref(d), C.byref(pe), C.byref(re_)))
