@@ -329,7 +329,7 @@ static void forward_impl(Block* b, const float* x_in, const float* params, float
                                                         d.c0, b->part);
     }
     LaunchScope ls(b, KC_FINALIZE, 0, 0);
-    launch(k_finalize_stats, blocks_for(32LL * d.c0, 256), 256, 0, b->stream, 
+    launch(k_finalize_stats, static_cast<unsigned>((d.c0 + kFinCh - 1) / kFinCh), kFinThreads, 0, b->stream, 
         b->part, g.P, d.c0, count, fmean, fvar, 0);
   }
   for (int l = 0; l < d.m; ++l) {
@@ -352,7 +352,7 @@ static void forward_impl(Block* b, const float* x_in, const float* params, float
     if (!eval) {
       LaunchScope ls(b, KC_FINALIZE, 0, 0);
       float* zm = b->zstat + static_cast<int64_t>(l) * 2 * d.bk;
-      launch(k_finalize_stats, blocks_for(32LL * d.bk, 256), 256, 0, b->stream, 
+      launch(k_finalize_stats, static_cast<unsigned>((d.bk + kFinCh - 1) / kFinCh), kFinThreads, 0, b->stream, 
           b->part, g.P, d.bk, count, zm, zm + d.bk, 0);
     }
     int p3 = g.P;
@@ -363,7 +363,7 @@ static void forward_impl(Block* b, const float* x_in, const float* params, float
     }
     if (!eval) {
       LaunchScope ls(b, KC_FINALIZE, 0, 0);
-      launch(k_finalize_stats, blocks_for(32LL * d.k, 256), 256, 0, b->stream, 
+      launch(k_finalize_stats, static_cast<unsigned>((d.k + kFinCh - 1) / kFinCh), kFinThreads, 0, b->stream, 
           b->part, p3, d.k, count, fmean, fvar, a.c);
     }
   }
@@ -456,7 +456,7 @@ static void backward_impl(Block* b, const float* params, float* grad_acc, float*
     // BN_b backward sums -> dgamma_b, dbeta_b, coefficients (graph.hpp:913-916)
     {
       LaunchScope ls(b, KC_FINALIZE, 0, 0);
-      launch(k_finalize_bn_bwd, blocks_for(32LL * d.bk, 256), 256, 0, b->stream, 
+      launch(k_finalize_bn_bwd, static_cast<unsigned>((d.bk + kFinCh - 1) / kFinCh), kFinThreads, 0, b->stream, 
           b->part, pd, d.bk, count, d_gb, d_bb, const_cast<float*>(a.bnb_bwd));
     }
     if (fork) {
@@ -500,7 +500,7 @@ static void backward_impl(Block* b, const float* params, float* grad_acc, float*
     // BN_a backward (graph.hpp:929-932) + concat-backward accumulate (:936-941)
     {
       LaunchScope ls(b, KC_FINALIZE, 0, 0);
-      launch(k_finalize_bn_bwd, blocks_for(32LL * a.c, 256), 256, 0, b->stream, 
+      launch(k_finalize_bn_bwd, static_cast<unsigned>((a.c + kFinCh - 1) / kFinCh), kFinThreads, 0, b->stream, 
           b->part, g.P, a.c, count, d_ga, d_ba, b->bna_bwd);
     }
     {
@@ -533,7 +533,7 @@ static void backward_impl(Block* b, const float* params, float* grad_acc, float*
 // Folds shared with the whole-network step (dpb_model.cu).
 void launch_finalize_bn_bwd(cudaStream_t st, const double2* part, int P, int nch, double count,
                             float* dgamma, float* dbeta, float* coef) {
-  launch(k_finalize_bn_bwd, blocks_for(32LL * nch, 256), 256, 0, st, part, P, nch, count, dgamma, dbeta,
+  launch(k_finalize_bn_bwd, static_cast<unsigned>((nch + kFinCh - 1) / kFinCh), kFinThreads, 0, st, part, P, nch, count, dgamma, dbeta,
          coef);
 }
 void launch_fold_splits(cudaStream_t st, const float* wpart, int splits, int64_t n, float* out) {

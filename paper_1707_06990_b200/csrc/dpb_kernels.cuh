@@ -101,36 +101,49 @@ k_channel_partials(const S* __restrict__ src, int pitch, int c_off, int64_t M,
   }
 }
 
-// Fixed-order fold of P partials for nch channels: one warp per channel, lane
-// l sums p = l, l+32, ..., then a fixed butterfly.  Deterministic.
-__device__ __forceinline__ double2 fold_partials(const double2* part, int P, int nch,
-                                                 int ch) {
-  const int lane = threadIdx.x % 32;
+// Block-wide fixed-order fold for the finalize kernels: a CTA of kFinThreads
+// owns kFinCh channels; thread (lane, ch) sums partials p = lane, lane +
+// kFinLanes, ... (each row read is kFinCh consecutive double2: coalesced), then
+// thread (0, ch) adds the kFinLanes sums in lane order.  Deterministic; at most
+// ~P / 64 loads per thread, all independent (the finalize sits on the
+// critical path between two big kernels, so its latency is what matters).
+constexpr int kFinCh = 16, kFinLanes = 64, kFinThreads = kFinCh * kFinLanes;
+__device__ __forceinline__ bool fold_block(const double2* part, int P, int nch, int& ch, double2& out) {
+  __shared__ double2 red[kFinLanes][kFinCh + 1];
+  const int tx = threadIdx.x % kFinCh, ty = threadIdx.x / kFinCh;
+  ch = blockIdx.x * kFinCh + tx;
   double a = 0.0, b = 0.0;
-#pragma unroll 8
-  for (int p = lane; p < P; p += 32) {
-    const double2 v = part[static_cast<int64_t>(p) * nch + ch];
-    a += v.x;
-    b += v.y;
+  if (ch < nch) {
+#pragma unroll 9
+    for (int p = ty; p < P; p += kFinLanes) {
+      const double2 v = part[static_cast<int64_t>(p) * nch + ch];
+      a += v.x;
+      b += v.y;
+    }
   }
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-    a += __shfl_xor_sync(0xffffffffu, a, o);
-    b += __shfl_xor_sync(0xffffffffu, b, o);
+  red[ty][tx] = make_double2(a, b);
+  __syncthreads();
+  if (ty != 0 || ch >= nch) return false;
+  double sa = 0.0, sb = 0.0;
+#pragma unroll 16
+  for (int i = 0; i < kFinLanes; ++i) {
+    sa += red[i][tx].x;
+    sb += red[i][tx].y;
   }
-  return make_double2(a, b);
+  out = make_double2(sa, sb);
+  return true;
 }
 
 // Forward statistics: mean = S1/count, biased var = S2/count - mean^2
 // (ops.hpp:138-162 semantics) -> mean_out[first+ch], var_out[first+ch].
-__global__ void k_finalize_stats(const double2* __restrict__ part, int P, int nch,
+// Grid ceil(nch / kFinCh) x kFinThreads.
+__global__ void __launch_bounds__(kFinThreads) k_finalize_stats(const double2* __restrict__ part, int P, int nch,
                                  double count, float* __restrict__ mean_out,
                                  float* __restrict__ var_out, int first) {
   pdl_enter();
-  const int ch = (blockIdx.x * blockDim.x + threadIdx.x) / 32;
-  if (ch >= nch) return;
-  const double2 s = fold_partials(part, P, nch, ch);
-  if (threadIdx.x % 32 == 0) {
+  int ch;
+  double2 s;
+  if (fold_block(part, P, nch, ch, s)) {
     const double mean = s.x / count;
     double var = s.y / count - mean * mean;
     if (var < 0.0) var = 0.0;
@@ -141,14 +154,13 @@ __global__ void k_finalize_stats(const double2* __restrict__ part, int P, int nc
 
 // BN backward sums -> dgamma = sum g*xhat, dbeta = sum g (written, ops.hpp:229-230)
 // and the apply coefficients coef[2*ch] = mg, [2*ch+1] = mgx.
-__global__ void k_finalize_bn_bwd(const double2* __restrict__ part, int P, int nch,
+__global__ void __launch_bounds__(kFinThreads) k_finalize_bn_bwd(const double2* __restrict__ part, int P, int nch,
                                   double count, float* __restrict__ dgamma,
                                   float* __restrict__ dbeta, float* __restrict__ coef) {
   pdl_enter();
-  const int ch = (blockIdx.x * blockDim.x + threadIdx.x) / 32;
-  if (ch >= nch) return;
-  const double2 s = fold_partials(part, P, nch, ch);
-  if (threadIdx.x % 32 == 0) {
+  int ch;
+  double2 s;
+  if (fold_block(part, P, nch, ch, s)) {
     const float sum_g = static_cast<float>(s.x);
     const float sum_gx = static_cast<float>(s.y);
     dgamma[ch] = sum_gx;
