@@ -310,7 +310,7 @@ __global__ void __launch_bounds__(Roles<Op>::kThreads, 1) tc2_kernel(const __gri
     if constexpr (Op::kNE > 0) {
       if (lane == 0) {
         int e = 0;
-        int slot_tile[NE], slot_box[NE];  // box held by each slot (for the store)
+        int slot_tile[NE] = {}, slot_box[NE] = {};  // box held by each slot (for the store)
         auto retire = [&](int s, int ee) {  // wait for box ee (slot s) to be processed
           tc::mbar_wait(&epi_done[s], (ee / NE) & 1);
           if constexpr (Op::kEpiStore) {
