@@ -25,6 +25,11 @@ ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler", "-fvisibility=hidden",
          "--expt-relaxed-constexpr", "--extended-lambda", "-Xptxas", "-warn-spills",
          f"-I{os.path.join(ROOT, 'include')}", f"-I{CSRC}"]
+# DPB_PHASE_CLOCKS=1 at build time compiles the per-phase clock stamps of the
+# tcgen05 engines in (tools/phase_clocks*.py, tools/tc2_clocks.py); the default
+# build carries no debug reads on the kernels' critical path.
+if os.environ.get("DPB_PHASE_CLOCKS"):
+    FLAGS.append("-DDPB_PHASE_CLOCKS")
 
 
 def _deps_mtime() -> float:
@@ -32,9 +37,20 @@ def _deps_mtime() -> float:
     return max(os.path.getmtime(f) for f in files)
 
 
-def _compile(src: str, verbose: bool) -> str:
+def _flags_changed() -> bool:
+    """Record the compile flags; True when they differ from the last build's."""
+    stamp = os.path.join(OUT, "flags.txt")
+    now = " ".join(ARCH + FLAGS)
+    old = open(stamp).read() if os.path.exists(stamp) else None
+    if old != now:
+        with open(stamp, "w") as f:
+            f.write(now)
+    return old != now
+
+
+def _compile(src: str, verbose: bool, force: bool = False) -> str:
     obj = os.path.join(OUT, os.path.basename(src) + ".o")
-    if os.path.exists(obj) and os.path.getmtime(obj) >= _deps_mtime():
+    if not force and os.path.exists(obj) and os.path.getmtime(obj) >= _deps_mtime():
         return obj
     cmd = [NVCC, *ARCH, *FLAGS, "-c", src, "-o", obj]
     if verbose:
@@ -50,8 +66,9 @@ def _compile(src: str, verbose: bool) -> str:
 def build(verbose: bool = False) -> str:
     os.makedirs(OUT, exist_ok=True)
     srcs = sorted(glob.glob(os.path.join(CSRC, "*.cu")))
+    force = _flags_changed()
     with cf.ThreadPoolExecutor(max_workers=min(8, len(srcs))) as ex:
-        objs = list(ex.map(lambda s: _compile(s, verbose), srcs))
+        objs = list(ex.map(lambda s: _compile(s, verbose, force), srcs))
     if not os.path.exists(LIB) or os.path.getmtime(LIB) < max(os.path.getmtime(o) for o in objs):
         cmd = [NVCC, *ARCH, "-shared", "-cudart", "static", "-o", LIB, *objs]
         r = subprocess.run(cmd, capture_output=True, text=True)

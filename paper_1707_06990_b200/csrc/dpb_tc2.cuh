@@ -144,7 +144,11 @@ __global__ void __launch_bounds__(Roles<Op>::kThreads, 1) tc2_kernel(const __gri
 
   const int tid = threadIdx.x;
   const int warp = tid / 32, lane = tid % 32;
+#ifdef DPB_PHASE_CLOCKS  // debug stamps (a global flag read at kernel entry)
   const bool dbg = Op::kColSums && g_tc2_dbg_c == op.a.c && blockIdx.x < 148 && blockIdx.y == 0;
+#else
+  constexpr bool dbg = false;
+#endif
   long long* clk = g_tc2_clock[blockIdx.x < 148 ? blockIdx.x : 0];
   if (dbg && tid == 0) {
     clk[0] = dbg_now();

@@ -87,8 +87,14 @@ __global__ void __launch_bounds__(kThreads, Op::kMinBlocks) tc_halo_kernel(const
 
   const int tid = threadIdx.x;
   const int warp = tid / 32, lane = tid % 32;
-  // g_phase_on: 1 stamps the ops with column sums (forward, dgrad), 2 the wgrad
+  // g_phase_on: 1 stamps the ops with column sums (forward, dgrad), 2 the wgrad.
+  // Compiled in only with DPB_PHASE_CLOCKS: reading the flag is a global load
+  // at kernel entry that every CTA would wait on.
+#ifdef DPB_PHASE_CLOCKS
   const bool dbg = g_phase_on == (Op::kColSums ? 1 : 2) && tid == 0 && blockIdx.x + blockIdx.y * gridDim.x < 4096;
+#else
+  constexpr bool dbg = false;
+#endif
   const int dbg_id = blockIdx.x + blockIdx.y * gridDim.x;
   if (dbg) g_phase_clock[dbg_id][0] = clock64();
   const uint32_t SB = op.stage_bytes();

@@ -1,4 +1,6 @@
-"""Debug: per-phase CTA timing of the halo 3x3 forward (dpb_debug_phase_clocks)."""
+"""Debug: per-phase CTA timing of the halo 3x3 forward (dpb_debug_phase_clocks).
+Needs a build with the stamps compiled in: rm -rf paper_1707_06990_b200/_build &&
+DPB_PHASE_CLOCKS=1 python -m paper_1707_06990_b200.build (the default build has none)."""
 import ctypes as C, sys
 import numpy as np, torch
 sys.path.insert(0, ".")

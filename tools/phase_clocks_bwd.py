@@ -1,4 +1,6 @@
 """Debug: per-phase CTA timing of the halo 3x3 dgrad (dpb_debug_phase_clocks).
+Needs a build with the stamps compiled in: rm -rf paper_1707_06990_b200/_build &&
+DPB_PHASE_CLOCKS=1 python -m paper_1707_06990_b200.build (the default build has none).
 Run with DPB_NO_FORK=1: the backward is then serial and its last halo launch
 is layer 0's 3x3 dgrad (BC-100 block-1 geometry).  `python tools/phase_clocks_bwd.py wgrad`
 stamps the 3x3 wgrad instead."""

@@ -1,4 +1,6 @@
 """Debug: per-tile phase timing of the v2 engine (dpb_debug_tc2_clocks).
+Needs a build with the stamps compiled in: rm -rf paper_1707_06990_b200/_build &&
+DPB_PHASE_CLOCKS=1 python -m paper_1707_06990_b200.build (the default build has none).
 
     python tools/tc2_clocks.py [c] [0] [fwd|bwd] [block]      (second argument reserved)
 
