@@ -104,6 +104,9 @@ MODEL_CASES = {
     "model_bc": ((3, 3, 3), 12, 0.5, 10, 24, (8, 3, 16, 16), 11),
     # k = 32 (DenseNet-121 / 264-k32 growth, bk = 128): per-tap 3x3 kernels, bk > 64 1x1 variants
     "model_k32": ((2, 2), 32, 0.5, 10, 64, (4, 3, 8, 8), 13),
+    # odd spatial size: 9x9 -> the transition pools (9-2)/2+1 = 4, so the pooling
+    # windows do not tile the input (the partial-window backward path)
+    "model_odd": ((2, 2), 8, 0.5, 10, 16, (4, 3, 9, 9), 17),
 }
 
 
@@ -175,6 +178,10 @@ def main():
     with open(os.path.join(OUT, "config_kats.json"), "w") as f:
         json.dump(config_kats(), f, indent=1, sort_keys=True)
     if "--config-only" in sys.argv:
+        return
+    if "--model" in sys.argv:  # one model case only: python -m oracle.gen_golden --model NAME
+        name = sys.argv[sys.argv.index("--model") + 1]
+        make_model_case(name, *MODEL_CASES[name])
         return
     for name, (s, src, dt) in CASES.items():
         make_case(name, s, src, dt)

@@ -16,7 +16,7 @@ from paper_1707_06990_b200.model import DenseNetConfig, ModelPlan
 
 pytestmark = pytest.mark.gpu
 
-CASES = ["model_small", "model_bc", "model_k32"]
+CASES = ["model_small", "model_bc", "model_k32", "model_odd"]
 TOL = {"fp32": 1e-4, "bf16": 2e-2}
 
 
