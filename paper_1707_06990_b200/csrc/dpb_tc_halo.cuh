@@ -770,9 +770,18 @@ struct Tc3x3WgradHalo {
     const int j = blockIdx.y * kBM + row;
     const int nv = j < a.bk ? a.k - o0 : 0;
     float* dst = a.wpart + (static_cast<int64_t>(blockIdx.x) * 9 * a.bk + tap * a.bk + j) * a.k + o0;
+    if ((a.k & 3) == 0 && nv >= 4) {  // rows of k floats, o0 % 8 == 0: 16-byte aligned quads
+      reinterpret_cast<float4*>(dst)[0] = make_float4(v[0], v[1], v[2], v[3]);
+      if (nv >= 8) reinterpret_cast<float4*>(dst)[1] = make_float4(v[4], v[5], v[6], v[7]);
+      else
 #pragma unroll
-    for (int i = 0; i < 8; ++i)
-      if (i < nv) dst[i] = v[i];
+        for (int i = 4; i < 8; ++i)
+          if (i < nv) dst[i] = v[i];
+    } else {
+#pragma unroll
+      for (int i = 0; i < 8; ++i)
+        if (i < nv) dst[i] = v[i];
+    }
   }
   __device__ void col_sums(int, double, double) const {}
 };
