@@ -458,6 +458,10 @@ def main():
     roof["excluded_zero_byte_kernels"] = {k: round(v["total_ms"] / prof_total, 4)
                                           for k, v in cats.items() if v["bytes"] <= 0}
     roof["peak_source"] = peak_src
+    roof["timing"] = ("profiled pass: every launch bracketed by CUDA events on its stream, the backward "
+                      "on one stream; in the timed step the weight-gradient kernels (conv*_wgrad, "
+                      "reduce_wgrad) run on a side stream overlapping the data-gradient chain, and the "
+                      "1x1 wgrad is sized to half the SMs for that overlap")
     F_img, B_img = algorithmic_per_image(shapes)
     t_roof = max(F_img / (bf16_peak * 1e12), B_img / (hbm_peak * 1e9))
     # SURVEY 8(d) byte / FLOP model of the dense blocks: measured against the
