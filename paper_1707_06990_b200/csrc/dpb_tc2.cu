@@ -148,7 +148,10 @@ bool tc2_conv1x1_fwd(Block* b, const LayerArgs<float>& a, int l) {
 
 // ---- 1x1 backward data on the v2 engine ------------------------------------------
 // Column-tile width bound of Dgrad1x1 for a block (0: not supported).
-int tc2_bwd_bn(const dpb_block_desc& d) { return d.bk <= 64 ? 256 : 128; }
+// 128 columns: its two TMEM accumulators then take 256 of the SM's 512 columns,
+// so a CTA can start beside a side-stream 3x3 wgrad CTA (which holds 256)
+// instead of waiting for the SM to empty (measured +0.6 % over 256 at BC-100).
+int tc2_bwd_bn(const dpb_block_desc&) { return 128; }
 
 int64_t tc2_w1b_layer_bytes(const dpb_block_desc& d, int l) {
   const int bn = tc2_bwd_bn(d);
@@ -161,10 +164,7 @@ void tc2_pretile_w1t(Block* b, const float* params) {
   const dpb_block_desc& d = b->d;
   if (!b->w1b) return;
   const dim3 grid(16, d.m);
-  if (tc2_bwd_bn(d) == 256)
-    launch(tc2::k_pretile_w1t_all<256>, grid, 256, 0, b->stream, params, d.c0, d.k, d.bk, b->w1b);
-  else
-    launch(tc2::k_pretile_w1t_all<128>, grid, 256, 0, b->stream, params, d.c0, d.k, d.bk, b->w1b);
+  launch(tc2::k_pretile_w1t_all<128>, grid, 256, 0, b->stream, params, d.c0, d.k, d.bk, b->w1b);
   b->launches++;
 }
 
@@ -191,7 +191,7 @@ bool tc2_conv1x1_dgrad(Block* b, const LayerArgs<float>& a, int l) {
     launch2(b, op, dim3(gx, nn), aux);
     return true;
   };
-  return tc2_bwd_bn(b->d) == 256 ? go(tc2::Dgrad1x1<256>{}) : go(tc2::Dgrad1x1<128>{});
+  return go(tc2::Dgrad1x1<128>{});
 }
 
 // ---- 1x1 backward weights on the v2 engine -----------------------------------------
