@@ -116,6 +116,26 @@ static int balanced_ctas(int ntiles, int slots) {
   return std::max(1, (ntiles + rounds - 1) / rounds);
 }
 
+// Column tiles per pixel tile for the streamed 1x1 forward over a W1 image of
+// bimg columns: tiles of nw = bimg / ns columns (a multiple of 16, the MMA's N
+// step, >= 32 and <= bnmax, the kernel's tile bound).  When the pixel tiles
+// alone fill half the GPU, the fewest column tiles; otherwise the most that
+// still fit one wave (ntiles * ns <= SMs).  0: no valid split.
+// DPB_FWD_NO_SPLIT=1: the fewest column tiles always.
+static int fwd1x1_col_split(int bimg, int bnmax, int ntiles, int sms) {
+  static const bool off = std::getenv("DPB_FWD_NO_SPLIT") != nullptr;
+  int lo = 0, best = 0;
+  for (int ns = 1; ns <= 6; ++ns) {
+    const int nw = bimg / ns;
+    if (bimg % ns || nw % 16 || nw > bnmax || (ns > 1 && nw < 32)) continue;
+    if (!lo) lo = ns;
+    if (ntiles * ns <= sms) best = ns;
+  }
+  if (!lo) return 0;
+  if (off || 2 * ntiles > sms || best < lo) return lo;
+  return best;
+}
+
 // 1x1 forward on the v2 engine; false when the shape is not supported (the
 // caller then uses the v1 kernel).
 bool tc2_conv1x1_fwd(Block* b, const LayerArgs<float>& a, int l) {
@@ -131,7 +151,13 @@ bool tc2_conv1x1_fwd(Block* b, const LayerArgs<float>& a, int l) {
     if (!make_map_f32(&op.xmap, a.feat, a.C, a.M, a.C, 32, tc::kBM)) return false;
     op.a = a;
     op.w1t = w1t;
-    launch2(b, op, dim3(balanced_ctas(ntiles, num_sms())), aux);
+    if constexpr (Op::kMmaReadsRaw) {  // streamed W1: column-split small blocks
+      op.bimg = tc2_bn_1x1(a.bk);
+      op.ns = fwd1x1_col_split(op.bimg, Op::BN, ntiles, num_sms());
+      if (!op.ns) return false;
+      op.nw = op.bimg / op.ns;
+    }
+    launch2(b, op, dim3(balanced_ctas(ntiles * op.ns, num_sms())), aux);
     return true;
   };
   // B resident in shared memory when all of W1's tiles fit, else streamed
@@ -140,8 +166,12 @@ bool tc2_conv1x1_fwd(Block* b, const LayerArgs<float>& a, int l) {
     case 32: return go(tc2::Fwd1x1<32, true>{}) || go(tc2::Fwd1x1<32, false>{});
     case 48: return go(tc2::Fwd1x1<48, true>{}) || go(tc2::Fwd1x1<48, false>{});
     case 64: return go(tc2::Fwd1x1<64, true>{}) || go(tc2::Fwd1x1<64, false>{});
-    case 128: return go(tc2::Fwd1x1<128, true>{}) || go(tc2::Fwd1x1<128, false>{});
-    case 192: return go(tc2::Fwd1x1<192, true>{}) || go(tc2::Fwd1x1<192, false>{});
+    // wide inputs: W1's streamed stage at the full width no longer fits beside
+    // the BN table, so the stages hold half-width (or narrower) column tiles
+    case 128: return go(tc2::Fwd1x1<128, true>{}) || go(tc2::Fwd1x1<128, false>{}) ||
+                     go(tc2::Fwd1x1<64, false>{});
+    case 192: return go(tc2::Fwd1x1<192, true>{}) || go(tc2::Fwd1x1<192, false>{}) ||
+                     go(tc2::Fwd1x1<96, false>{});
     default: return false;
   }
 }

@@ -400,17 +400,27 @@ struct Fwd1x1 {
   CUtensorMap xmap;        // feat [M][C] fp32, box {32, 128}, swizzle 128B
   LayerArgs<float> a;
   const uint8_t* w1t;      // pre-tiled W1: per K block, hi tile | lo tile (Tile<BN> K-major)
+  // Column split (streamed W1 only): each pixel tile's BN output columns are
+  // cut into ns tiles of nw columns, so a block with few pixel tiles (7x7 at
+  // batch 64: 25) still spreads over the SMs.  tile = pixel tile * ns + column
+  // tile: the ns CTAs of one pixel tile run side by side and share its feature
+  // boxes through L2; each streams only its nw columns of W1.  bimg: the
+  // column count of the pre-tiled W1 image (>= BN when the template's BN only
+  // bounds the column tile, so the streamed stages fit shared memory).
+  int ns = 1, nw = BN, bimg = BN;
 
+  __device__ int mtile(int tile) const { return tile / ns; }
+  __device__ int ncol0(int tile) const { return (tile % ns) * nw; }
   __device__ void prefetch() const { prefetch_tmap(&xmap); }
-  __device__ int num_tiles() const { return static_cast<int>((a.M + kBM - 1) / kBM); }
+  __device__ int num_tiles() const { return static_cast<int>((a.M + kBM - 1) / kBM) * ns; }
   __device__ int num_kb(int) const { return (a.c + kBK - 1) / kBK; }
   __device__ int boxes(int kb) const { return a.c - kb * kBK > 32 ? 2 : 1; }
-  __device__ int epi_chunks(int) const { return BN / 8; }
+  __device__ int epi_chunks(int) const { return nw / 8; }
   __device__ int epi_boxes(int) const { return 0; }
   __device__ void epi_tma(int, int, uint32_t, uint64_t*) const {}
   __device__ void epi_store(int, int, uint32_t) const {}
   __device__ uint32_t raw_bytes(int, int kb) const {
-    return boxes(kb) * kBox + (RES ? 0 : 2 * kBBytes);
+    return boxes(kb) * kBox + (RES ? 0 : 2 * nw * kBK * 2);
   }
   __device__ uint32_t b_all() const { return static_cast<uint32_t>(num_kb(0) * 2 * kBBytes); }
   __device__ const BnAff* bn_table(const uint8_t* aux) const {
@@ -427,9 +437,23 @@ struct Fwd1x1 {
     fill_bn_aff(const_cast<BnAff*>(bn_table(aux)), a.c, 0, a.amean, a.avar, a.gamma_a, a.beta_a);
   }
   __device__ void tma(int tile, int kb, uint32_t raw, uint64_t* bar) const {
-    tma_load_2d(raw, &xmap, kb * kBK, tile * kBM, bar);
-    if (boxes(kb) == 2) tma_load_2d(raw + kBox, &xmap, kb * kBK + 32, tile * kBM, bar);
-    if (!RES) bulk_load(raw + 2 * kBox, w1t + static_cast<int64_t>(kb) * 2 * kBBytes, 2 * kBBytes, bar);
+    const int m0 = mtile(tile) * kBM;
+    tma_load_2d(raw, &xmap, kb * kBK, m0, bar);
+    if (boxes(kb) == 2) tma_load_2d(raw + kBox, &xmap, kb * kBK + 32, m0, bar);
+    if (!RES) {
+      const uint8_t* src = w1t + static_cast<int64_t>(kb) * 2 * (bimg * kBK * 2);
+      if (ns == 1 && bimg == BN) {
+        bulk_load(raw + 2 * kBox, src, 2 * kBBytes, bar);
+      } else {
+        // rows [n0, n0 + nw) of each of the 8 K chunks of the hi and lo tiles:
+        // one contiguous nw * 16-byte run each (canonical K-major layout)
+        const int n0 = ncol0(tile);
+        const uint32_t run = static_cast<uint32_t>(nw) * 16;
+#pragma unroll 1
+        for (int q = 0; q < 2 * (kBK / 8); ++q)
+          bulk_load(raw + 2 * kBox + q * run, src + q * (bimg * 16) + n0 * 16, run, bar);
+      }
+    }
   }
   __device__ void transform(int, int kb, const uint8_t* raw, uint8_t* op, const uint8_t* aux,
                             int xt) const {
@@ -471,31 +495,51 @@ struct Fwd1x1 {
     }
   }
   __device__ void mma(uint32_t op, uint32_t raw, uint32_t aux, uint32_t tmem, int kb) const {
-    constexpr uint32_t idesc = tc::make_idesc(BN, 0, 0);
     const uint32_t ah = op, al = op + kABytes;
-    const uint32_t bh = RES ? aux + kb * 2 * kBBytes : raw + 2 * kBox, bl = bh + kBBytes;
+    if (RES || (ns == 1 && bimg == BN)) {
+      constexpr uint32_t idesc = tc::make_idesc(BN, 0, 0);
+      const uint32_t bh = RES ? aux + kb * 2 * kBBytes : raw + 2 * kBox, bl = bh + kBBytes;
 #pragma unroll
-    for (int k16 = 0; k16 < kBK / 16; ++k16) {
-      const uint32_t acc = (kb | k16) ? 1u : 0u;
-      tc::mma_bf16(tmem, tc::Tile<kBM>::desc(ah, k16), tc::Tile<BN>::desc(bh, k16), idesc, acc);
-      tc::mma_bf16(tmem, tc::Tile<kBM>::desc(ah, k16), tc::Tile<BN>::desc(bl, k16), idesc, 1u);
-      tc::mma_bf16(tmem, tc::Tile<kBM>::desc(al, k16), tc::Tile<BN>::desc(bh, k16), idesc, 1u);
+      for (int k16 = 0; k16 < kBK / 16; ++k16) {
+        const uint32_t acc = (kb | k16) ? 1u : 0u;
+        tc::mma_bf16(tmem, tc::Tile<kBM>::desc(ah, k16), tc::Tile<BN>::desc(bh, k16), idesc, acc);
+        tc::mma_bf16(tmem, tc::Tile<kBM>::desc(ah, k16), tc::Tile<BN>::desc(bl, k16), idesc, 1u);
+        tc::mma_bf16(tmem, tc::Tile<kBM>::desc(al, k16), tc::Tile<BN>::desc(bh, k16), idesc, 1u);
+      }
+    } else {
+      // streamed column tile: a canonical K-major tile of nw rows
+      const uint32_t idesc = tc::make_idesc(nw, 0, 0);
+      const uint32_t tb = static_cast<uint32_t>(nw) * kBK * 2;
+      const uint32_t bh = raw + 2 * kBox, bl = bh + tb;
+      const uint32_t k16_step = 2 * static_cast<uint32_t>(nw) * 16, lbo = static_cast<uint32_t>(nw) * 16;
+#pragma unroll
+      for (int k16 = 0; k16 < kBK / 16; ++k16) {
+        const uint32_t acc = (kb | k16) ? 1u : 0u;
+        const uint64_t dh = tc::make_sdesc(bh + k16 * k16_step, lbo, 128);
+        const uint64_t dl = tc::make_sdesc(bl + k16 * k16_step, lbo, 128);
+        tc::mma_bf16(tmem, tc::Tile<kBM>::desc(ah, k16), dh, idesc, acc);
+        tc::mma_bf16(tmem, tc::Tile<kBM>::desc(ah, k16), dl, idesc, 1u);
+        tc::mma_bf16(tmem, tc::Tile<kBM>::desc(al, k16), dh, idesc, 1u);
+      }
     }
   }
   __device__ void epilogue(int tile, int row, int col0, const float (&v)[8], const uint8_t*,
                            uint8_t*, float (&s1)[8], float (&s2)[8]) const {
-    const int64_t p = static_cast<int64_t>(tile) * kBM + row;
-    const int nv = p < a.M ? a.bk - col0 : 0;
+    const int64_t p = static_cast<int64_t>(mtile(tile)) * kBM + row;
+    const int gc = ncol0(tile) + col0;
+    const int nv = p < a.M ? min(a.bk - gc, nw - col0) : 0;
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
       const bool ok = i < nv;
       s1[i] = ok ? v[i] : 0.f;
       s2[i] = ok ? v[i] * v[i] : 0.f;
     }
-    if (nv > 0) tc::store8(a.z + p * a.bk + col0, nv, (a.bk & 3) == 0, v);
+    if (nv > 0) tc::store8(a.z + p * a.bk + gc, nv, (a.bk & 3) == 0, v);
   }
   __device__ void col_sums(int tile, int c, double s1, double s2) const {
-    if (c < a.bk) a.part[static_cast<int64_t>(tile) * a.bk + c] = make_double2(s1, s2);
+    const int gc = ncol0(tile) + c;
+    if (c < nw && gc < a.bk)
+      a.part[static_cast<int64_t>(mtile(tile)) * a.bk + gc] = make_double2(s1, s2);
   }
 };
 

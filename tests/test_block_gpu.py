@@ -164,6 +164,10 @@ def test_block_matches_oracle_medium(dtype, layout):
     (2, 9, 7, 13, 3, 5, 20),     # ragged channels, odd field, bk not a multiple of 16
     (3, 14, 14, 40, 2, 32, 128), # k=32 geometry (DenseNet-121/264-k32), bk=128 > 64 (N tiling)
     (1, 7, 7, 96, 2, 48, 192),   # k=48 geometry (DenseNet-264-k48), 7x7 field, batch 1
+    # wide inputs at 7x7 (DenseNet-264 block 4): W1 streamed per K block, and so
+    # few pixel tiles that the 1x1 forward splits its 192 columns across CTAs
+    (2, 7, 7, 520, 2, 48, 192),
+    (16, 7, 7, 1728, 1, 48, 192),
 ])
 @pytest.mark.parametrize("dtype", ["fp32", "bf16"])
 def test_block_matches_oracle_shapes(s, dtype):
