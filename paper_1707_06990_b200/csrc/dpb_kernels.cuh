@@ -104,7 +104,7 @@ k_channel_partials(const S* __restrict__ src, int pitch, int c_off, int64_t M,
 // Block-wide fixed-order fold for the finalize kernels: a CTA of kFinThreads
 // owns kFinCh channels; thread (lane, ch) sums partials p = lane, lane +
 // kFinLanes, ... (each row read is kFinCh consecutive double2: coalesced), then
-// thread (0, ch) adds the kFinLanes sums in a fixed order.  Deterministic; at most
+// thread (0, ch) adds the kFinLanes sums in lane order.  Deterministic; at most
 // ~P / 64 loads per thread, all independent (the finalize sits on the
 // critical path between two big kernels, so its latency is what matters).
 constexpr int kFinCh = 16, kFinLanes = 64, kFinThreads = kFinCh * kFinLanes;
@@ -124,18 +124,13 @@ __device__ __forceinline__ bool fold_block(const double2* part, int P, int nch, 
   red[ty][tx] = make_double2(a, b);
   __syncthreads();
   if (ty != 0 || ch >= nch) return false;
-  // four interleaved chains (lane i into chain i % 4), combined in a fixed
-  // order: a quarter of the dependent-add latency of one serial chain
-  double sa[4] = {0.0, 0.0, 0.0, 0.0}, sb[4] = {0.0, 0.0, 0.0, 0.0};
-#pragma unroll
-  for (int i = 0; i < kFinLanes; i += 4) {
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      sa[j] += red[i + j][tx].x;
-      sb[j] += red[i + j][tx].y;
-    }
+  double sa = 0.0, sb = 0.0;
+#pragma unroll 16
+  for (int i = 0; i < kFinLanes; ++i) {
+    sa += red[i][tx].x;
+    sb += red[i][tx].y;
   }
-  out = make_double2((sa[0] + sa[1]) + (sa[2] + sa[3]), (sb[0] + sb[1]) + (sb[2] + sb[3]));
+  out = make_double2(sa, sb);
   return true;
 }
 
