@@ -253,10 +253,15 @@ int tc2_conv1x1_wgrad(Block* b, const LayerArgs<float>& a) {
     tc2::bwd_ntiles(a.c, Op::BN, nn, nw);
     op.nw = nw;
     op.nblk = static_cast<int>((a.M + Op::kBoxP - 1) / Op::kBoxP);
-    // Half the SMs: this runs on the side stream next to the data-gradient
-    // chain, and a smaller footprint leaves that chain its SMs (measured +1.5 %
-    // over one CTA per SM at BC-100; a quarter is slower again).
-    const int target = std::max(1, num_sms() / (2 * nn));
+    // Half the SMs at bk <= 64: this runs on the side stream next to the
+    // data-gradient chain, and a smaller footprint leaves that chain its SMs
+    // (measured +1.5 % over one CTA per SM at BC-100; a quarter is slower
+    // again).  At bk >= 128 (DenseNet-121/264) the weight branch carries more
+    // work per pixel and every SM pays: +5 % at d121, +8 % at d264k48 over
+    // half.  DPB_WGRAD_SM_DIV=<d>: 1/d of the SMs for every shape.
+    static const char* env_div = std::getenv("DPB_WGRAD_SM_DIV");
+    const int div = env_div ? std::max(1, std::atoi(env_div)) : (a.bk <= 64 ? 2 : 1);
+    const int target = std::max(1, num_sms() / (div * nn));
     op.kchunk = (op.nblk + target - 1) / target;
     const int gx = (op.nblk + op.kchunk - 1) / op.kchunk;  // every CTA owns >= 1 block
     launch2(b, op, dim3(gx, nn), aux);
