@@ -132,6 +132,9 @@ static int fwd1x1_col_split(int bimg, int bnmax, int ntiles, int sms) {
     if (ntiles * ns <= sms) best = ns;
   }
   if (!lo) return 0;
+  static const int force = std::getenv("DPB_FWD_NS") ? std::atoi(std::getenv("DPB_FWD_NS")) : 0;
+  if (force >= lo && force <= 6 && bimg % force == 0 && (bimg / force) % 16 == 0 && bimg / force >= 32)
+    return force;
   if (off || 2 * ntiles > sms || best < lo) return lo;
   return best;
 }
