@@ -54,6 +54,8 @@ def main():
     ap.add_argument("--round", default="r01")
     ap.add_argument("--config", default="bc100")
     ap.add_argument("--dtype", default="bf16")
+    ap.add_argument("--what", default="model", choices=["model", "blocks"],
+                    help="what the captured step covered (bench.py --ncu-what)")
     ap.add_argument("--out", default=os.path.join(ROOT, "profiles"))
     args = ap.parse_args()
 
@@ -81,14 +83,23 @@ def main():
     total_launches = sum(c["launches"] for c in cats.values())
 
     os.makedirs(args.out, exist_ok=True)
-    md = [f"# {args.round}: ncu launch list of one whole-network training step ({args.config}, {args.dtype}, "
-          f"batch 64)",
+    if args.what == "model":
+        title = "one whole-network training step"
+        src = ("`bash tools/ncu_round.sh` on one B200 (`ncu --profile-from-start off --metrics "
+               "gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none` over "
+               "`python bench.py --ncu-step --ncu-what model --no-cpu-baseline`, which replays ONE CUDA-graph "
+               "training step (stem, dense blocks, transitions, head, loss, backward) plus the SGD update between "
+               "cudaProfilerStart/Stop).")
+    else:
+        title = "one dense-blocks training step"
+        src = ("one B200 (`ncu --profile-from-start off --metrics "
+               "gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none` over "
+               f"`python bench.py --ncu-step --ncu-what blocks --config {args.config} --no-cpu-baseline "
+               "--no-naive`, which replays ONE step of every dense block, forward and backward, between "
+               "cudaProfilerStart/Stop).")
+    md = [f"# {args.round}: ncu launch list of {title} ({args.config}, {args.dtype}, batch 64)",
           "",
-          "Source: `bash tools/ncu_round.sh` on one B200 (`ncu --profile-from-start off --metrics "
-          "gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none` over "
-          "`python bench.py --ncu-step --ncu-what model --no-cpu-baseline`, which replays ONE CUDA-graph "
-          "training step (stem, dense blocks, transitions, head, loss, backward) plus the SGD update between "
-          "cudaProfilerStart/Stop).  ncu serialises launches and flushes caches before each: times are "
+          "Source: " + src + "  ncu serialises launches and flushes caches before each: times are "
           "cold-cache and sum above the graph-timed step; compare SHARES with bench.py `kernels`.",
           "",
           f"Launches in the step: {total_launches}; serialised kernel time {total_us / 1e3:.3f} ms.",
