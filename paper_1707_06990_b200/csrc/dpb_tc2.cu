@@ -224,7 +224,8 @@ bool tc2_conv1x1_dgrad(Block* b, const LayerArgs<float>& a, int l) {
     launch2(b, op, dim3(gx, nn), aux);
     return true;
   };
-  return go(tc2::Dgrad1x1<128>{});
+  // bk = 192: the resident W1^T (48 KB) fits only beside a 4-deep epilogue ring
+  return go(tc2::Dgrad1x1<128>{}) || go(tc2::Dgrad1x1<128, 4>{});
 }
 
 // ---- 1x1 backward weights on the v2 engine -----------------------------------------

@@ -562,7 +562,9 @@ __host__ __device__ inline int bwd_nkb(int bk) { return (bk + 31) / 32; }
 // load warp: whole 128-byte lines, clipped at M and c) and writes the BN_a
 // backward column sums (sum g, sum g*xhat) to the tile's partial slot.
 // graph.hpp:920-932 / ops.hpp:268-287, 206-243.
-template <int BN_>
+// NE_: depth of the feature-box epilogue ring (5: one box of look-ahead over
+// the four epilogue groups; 4 frees 16 KB for bk = 192's resident W1^T).
+template <int BN_, int NE_ = 5>
 struct Dgrad1x1 {
   static constexpr int BN = BN_;
   static constexpr int kTmemCols = BN;
@@ -574,7 +576,7 @@ struct Dgrad1x1 {
   static constexpr int kNR = 2;
   static constexpr int kOpBytes = kBM * 32 * 2;    // t1, bf16, 32 K
   static constexpr int kNS = 3;
-  static constexpr int kNE = 5, kEpiBytes = kBox;  // feature boxes, rewritten with g1
+  static constexpr int kNE = NE_, kEpiBytes = kBox;  // feature boxes, rewritten with g1
   static constexpr bool kEpiStore = true;
   static constexpr int kEpiWarps = 16, kXfWarps = 4;
   static constexpr int kXfThreads = 32 * kXfWarps;
