@@ -1,17 +1,18 @@
-"""Benchmark of the memory-efficient dense-block hot path on B200.
+"""Benchmark of the memory-efficient DenseNet training step on B200.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-                    [--config bc100|cfg1|d121|d264k32|d264k48]
+                    [--config d264k32|d264k48|d121|bc100|cfg1|...]
 
-One step = one whole training step of the configuration (BASELINE.json
-configs[1] by default: DenseNet-BC-100, k=12, batch 64 per GPU, 3x32x32
-input): stem, dense blocks, transitions, head, softmax cross-entropy, forward
-+ backward and the momentum-SGD update, on synthetic inputs resident in HBM,
-through libdpb.so (bf16 tensor-core GEMMs, fp32 arena and gradients), CUDA-
-graph captured.  The dense blocks alone (the hot path) are reported beside it
-under "dense_blocks".  ImageNet-shaped configs, whose 7x7/2 stem is not built,
-time the dense blocks only.  Prints ONE JSON line on rank 0; see DESIGN.md §5
-for every field.
+One step = one whole training step of the configuration, by default
+BASELINE.json configs[3]: DenseNet-264 (k=32, 33M parameters) at 3x224x224,
+batch 64 per GPU, ImageNet stem (7x7/2 conv, BN, ReLU, 3x3/2 max-pool), four
+dense blocks at 56/28/14/7, transitions, head, softmax cross-entropy, forward
++ backward, the DP gradient allreduce (N > 1) and the momentum-SGD update —
+through the public C ABI (ModelPlan -> dpb_model_step, replayed as a CUDA
+graph; bf16 tensor-core GEMMs, fp32 arena and gradients) on synthetic inputs
+resident in HBM.  The dense blocks alone (the hot path) are timed and
+profiled beside it ("dense_blocks", "roofline", "kernels").  Prints ONE JSON
+line on rank 0; DESIGN.md §5 documents every field.
 """
 from __future__ import annotations
 
@@ -28,6 +29,7 @@ sys.path.insert(0, ROOT)
 
 BATCH = 64
 METRIC = "DenseNet train images/sec"
+DEFAULT_CONFIG = "d264k32"   # BASELINE.json configs[3]: DenseNet-264 (k=32, 33M params), 224x224
 
 
 def load_peaks():
@@ -42,8 +44,7 @@ def load_peaks():
 def block_shapes(config: str, batch: int):
     from paper_1707_06990_b200.model import CONFIGS
     cfg = CONFIGS[config]
-    stem_stride = 4 if cfg.in_shape[1] >= 224 else 1   # ImageNet 7x7/2 + maxpool geometry (F4)
-    return [(s.n, s.h, s.w, s.c0, s.m, s.k, s.bk) for s in cfg.block_shapes(batch, stem_stride)]
+    return [(s.n, s.h, s.w, s.c0, s.m, s.k, s.bk) for s in cfg.block_shapes(batch)]
 
 
 def algorithmic_per_image(shapes, S=2):
@@ -113,18 +114,25 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sms)}
 
 
-def cpu_runner(config: str):
-    """The reference CPU workload matching the GPU arm: its whole training step
-    (GraphPlan::step_trace, one image per process) for CIFAR-type networks,
-    else one image of every dense block (fwd+bwd)."""
-    from oracle import cpu_bench as CB
+def reference_config(config: str):
+    """The configuration the reference itself runs for `config`: the
+    ImageNet-stem networks at the reference's own geometry (its 3x3/1 stem on
+    3x56x56 gives the same dense blocks, transitions and head as the 7x7/2 +
+    max-pool stem on 224x224)."""
     from paper_1707_06990_b200.model import CONFIGS
-    cfg = CONFIGS[config]
-    if cfg.in_shape[1] < 64 and CB.kind() == "reference":
-        net = (tuple(cfg.block_sizes), cfg.growth_rate, cfg.compression, cfg.num_classes, cfg.c0,
-               tuple(cfg.in_shape))
-        return CB.CpuModelRunner(net, batch=1), f"1 image, {config} full training step (GraphPlan::step_trace)"
-    return CB.CpuRunner(block_shapes(config, 1)), f"1 image of each {config} dense block (fwd+bwd, f32)"
+    name = config + "@56" if CONFIGS[config].stem == "imagenet" else config
+    return name, CONFIGS[name]
+
+
+def cpu_runner(config: str):
+    """The reference CPU workload matching the GPU arm: its whole training
+    step (GraphPlan::step_trace, the reference's public API), one image per
+    process, one process per host core (the reference is single-threaded)."""
+    from oracle import cpu_bench as CB
+    name, cfg = reference_config(config)
+    net = (tuple(cfg.block_sizes), cfg.growth_rate, cfg.compression, cfg.num_classes, cfg.c0, tuple(cfg.in_shape))
+    geo = "x".join(str(v) for v in cfg.in_shape)
+    return CB.CpuModelRunner(net, batch=1), f"1 image, {name} ({geo}) full training step (GraphPlan::step_trace)"
 
 
 def measure_naive_block(shape, dtype):
@@ -170,7 +178,9 @@ def run_reference(args):
     from oracle import cpu_bench as CB
     runner, what = cpu_runner(args.config)
     shapes = block_shapes(args.config, 1)
-    for i in range(args.warmup):
+    # the reference is CPU code with no warm-up effects beyond page-in; one
+    # untimed step keeps the whole arm within minutes at DenseNet-264 scale
+    for i in range(min(args.warmup, 1)):
         runner.step(seed=i)
     imgs = secs = 0.0
     t_budget = time.perf_counter()
@@ -203,18 +213,17 @@ def run_reference(args):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
-    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="bc100")
+    ap.add_argument("--config", default=DEFAULT_CONFIG)
     ap.add_argument("--dtype", default="bf16", choices=["bf16", "fp32"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-graph", action="store_true", help="launch kernels directly (no CUDA graph)")
-    ap.add_argument("--cpu-budget-s", type=float, default=25.0)
-    ap.add_argument("--ref-budget-s", type=float, default=180.0)
-    ap.add_argument("--no-naive", action="store_true",
-                    help="skip the measured Naive store-everything block (memory comparison)")
-    ap.add_argument("--ncu-what", default="blocks", choices=["blocks", "model"],
+    ap.add_argument("--ref-budget-s", type=float, default=240.0)
+    ap.add_argument("--no-blocks", action="store_true", help="skip the dense-blocks-only timing and profile")
+    ap.add_argument("--no-naive", action="store_true", help="skip the naive store-everything memory replay")
+    ap.add_argument("--ncu-what", default="model", choices=["blocks", "model"],
                     help="with --ncu-step: the dense blocks alone or the whole network step")
     ap.add_argument("--ncu-step", action="store_true",
                     help="after warm-up, run ONE step inside cudaProfilerStart/Stop and exit "
@@ -224,11 +233,12 @@ def main():
     if args.impl == "reference":
         return run_reference(args)
 
-    import numpy as np
     import torch
     import torch.distributed as dist
 
     import paper_1707_06990_b200 as P
+    from paper_1707_06990_b200.model import CONFIGS, ModelPlan
+    from paper_1707_06990_b200.ops import sgd_step
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -239,98 +249,14 @@ def main():
         dist.init_process_group("nccl", device_id=dev)
 
     hbm_peak, bf16_peak, bf16_sust, peak_src = load_peaks()
+    cfg = CONFIGS[args.config]
     shapes = block_shapes(args.config, BATCH)
     stream = torch.cuda.Stream(device=dev)
     g = torch.Generator(device="cpu").manual_seed(1234 + rank)
 
-    from paper_1707_06990_b200.dp import GradientBuckets
-    buckets = GradientBuckets([P.BlockShape(*s).param_elems for s in shapes], device=dev)
-    blocks = []
-    with torch.cuda.stream(stream):
-        for s in shapes:
-            shp = P.BlockShape(*s)
-            plan = P.BlockPlan(shp, dtype=args.dtype, layout="nhwc", device=local, stream=stream)
-            params = torch.randn(shp.param_elems, generator=g) * 0.1
-            for l, o in enumerate(shp.param_offsets()):
-                c = shp.c_in(l)
-                params[o:o + c] += 1.0
-                gb = o + 2 * c + shp.bk * c
-                params[gb:gb + shp.bk] += 1.0
-            blocks.append(dict(
-                shape=shp, plan=plan, params=params.to(dev),
-                running=shp.initial_running(dev),
-                x=torch.randn(shp.pixels, shp.c0, generator=g).to(dev),
-                gup=torch.randn(shp.pixels, shp.c_out, generator=g).to(dev),
-                acc=torch.empty(shp.pixels, shp.c_out, device=dev),
-                grads=buckets.view(len(blocks))))   # block grads are views of one flat buffer
-
-    def step():
-        for b in blocks:
-            b["plan"].forward(b["x"], b["params"], b["running"], True)
-        for b in reversed(blocks):
-            b["acc"].copy_(b["gup"])          # consumer BN backward writes the block-output grad
-            b["plan"].backward(b["params"], b["acc"], b["grads"])
-
-    def reduce_grads():
-        # data-parallel gradient allreduce (per-GPU BN); outside the
-        # CUDA graph: one NCCL allreduce of the flat fp32 buffer, scaled by 1/P
-        if world > 1:
-            buckets.reduce_all()
-
-    with torch.cuda.stream(stream):
-        for _ in range(args.warmup):
-            step()
-            reduce_grads()
-    torch.cuda.synchronize(dev)
-    launches_per_step = sum(b["plan"].launch_count for b in blocks)  # last backward only
-    # count forward+backward launches of one step precisely
-    with torch.cuda.stream(stream):
-        fwd_launches = 0
-        for b in blocks:
-            b["plan"].forward(b["x"], b["params"], b["running"], True)
-            fwd_launches += b["plan"].launch_count
-        bwd_launches = 0
-        for b in reversed(blocks):
-            b["acc"].copy_(b["gup"])
-            b["plan"].backward(b["params"], b["acc"], b["grads"])
-            bwd_launches += b["plan"].launch_count
-    launches_per_step = fwd_launches + bwd_launches
-    torch.cuda.synchronize(dev)
-
-    # ---- capture one step as a CUDA graph (launch overhead off the host) -----
-    graph = None
-    if not args.no_graph:
-        graph = torch.cuda.CUDAGraph()
-        with torch.cuda.graph(graph, stream=stream):
-            step()
-        with torch.cuda.stream(stream):
-            for _ in range(2):
-                graph.replay()
-        torch.cuda.synchronize(dev)
-
-    def timed_step():
-        if graph is not None:
-            graph.replay()
-        else:
-            step()
-        reduce_grads()
-
-    def ncu_step_and_exit(fn, what):
-        torch.cuda.synchronize(dev)
-        torch.cuda.profiler.start()
-        with torch.cuda.stream(stream):
-            fn()
-        torch.cuda.synchronize(dev)
-        torch.cuda.profiler.stop()
-        print(json.dumps({"ncu_step": what, "launches_per_step": launches_per_step}), flush=True)
-        return 0
-
-    if args.ncu_step and args.ncu_what == "blocks":
-        return ncu_step_and_exit(timed_step, "dense blocks")
-
-    def time_steps(fn):
-        """K steps of fn between barriers + syncs, CUDA events on `stream`, nvidia-smi
-        clocks sampled during the region; returns (ms per step, max over ranks; clocks)."""
+    def time_steps(fn, k):
+        """k steps of fn between barriers + syncs, CUDA events on `stream`,
+        nvidia-smi clocks sampled during the region; (ms per step, max over ranks; clocks)."""
         if world > 1:
             dist.barrier()
         torch.cuda.synchronize(dev)
@@ -340,7 +266,7 @@ def main():
         t1 = torch.cuda.Event(enable_timing=True)
         with torch.cuda.stream(stream):
             t0.record(stream)
-            for _ in range(args.steps):
+            for _ in range(k):
                 fn()
             t1.record(stream)
         torch.cuda.synchronize(dev)
@@ -353,265 +279,243 @@ def main():
             tt = torch.tensor([ms], device=dev)
             dist.all_reduce(tt, op=dist.ReduceOp.MAX)
             ms = float(tt.item())
-        return ms / args.steps, clk
+        return ms / k, clk
 
-    # ---- dense blocks alone (the hot path) --------------------------------------
-    blocks_ms, blocks_clk = time_steps(timed_step)
-    blocks_value = BATCH * world / (blocks_ms / 1000.0)
+    # ---- the whole training step through the public API (ModelPlan) ------------
+    free0 = torch.cuda.mem_get_info(dev)[0]
+    mplan = ModelPlan(cfg, BATCH, dtype=args.dtype, device=local, stream=stream)
+    torch.cuda.synchronize(dev)
+    model_alloc_bytes = free0 - torch.cuda.mem_get_info(dev)[0]
+    m_params = mplan.init_params(seed=7, device=dev)          # GraphPlan::build's init (rng replay)
+    m_run = mplan.initial_running(dev)
+    m_x = torch.randn(BATCH, *cfg.in_shape, generator=g).to(dev)
+    m_labels = (torch.arange(BATCH, dtype=torch.int32) % cfg.num_classes).to(dev)
+    m_grads = torch.empty(mplan.param_elems, device=dev)
+    m_vel = torch.zeros(mplan.param_elems, device=dev)
+    m_loss = torch.zeros(1, device=dev)
 
-    # ---- the whole network (headline for CIFAR-type configs: the 3x3 stem) -------
-    from paper_1707_06990_b200.model import CONFIGS, ModelPlan
-    cfg = CONFIGS[args.config]
-    whole = cfg.in_shape[1] < 64
-    mplan = None
-    if whole:
-        mplan = ModelPlan(cfg, BATCH, dtype=args.dtype, device=local, stream=stream)
-        m_params = mplan.init_params(seed=1234 + rank, device=dev)
-        m_run = mplan.initial_running(dev)
-        m_x = torch.randn(BATCH, *cfg.in_shape, generator=g).to(dev)
-        m_labels = (torch.arange(BATCH, dtype=torch.int32) % cfg.num_classes).to(dev)
-        m_grads = torch.empty(mplan.param_elems, device=dev)
-        m_vel = torch.zeros(mplan.param_elems, device=dev)
-        m_loss = torch.zeros(1, device=dev)
-        from paper_1707_06990_b200.ops import sgd_step
+    def model_update():
+        if world > 1:   # DP allreduce of the flat gradients (per-GPU BN)
+            dist.all_reduce(m_grads)
+            m_grads.mul_(1.0 / world)
+        # momentum SGD + weight decay (train.hpp:43-70)
+        sgd_step(m_params, m_grads, m_vel, lr=0.1, momentum=0.9, weight_decay=1e-4, stream=stream)
 
-        def model_step():
-            mplan.step(m_x, m_labels, m_params, m_run, m_grads, m_loss)
+    def model_step():
+        mplan.step(m_x, m_labels, m_params, m_run, m_grads, m_loss)   # graph-replayed by libdpb
+        model_update()
 
-        def model_reduce():
-            if world > 1:   # DP allreduce of the flat gradients (per-GPU BN), outside the graph
-                dist.all_reduce(m_grads)
-                m_grads.mul_(1.0 / world)
-            # momentum SGD + weight decay on the averaged gradients (train.hpp:43-70)
-            sgd_step(m_params, m_grads, m_vel, lr=0.1, momentum=0.9, weight_decay=1e-4, stream=stream)
-
-        with torch.cuda.stream(stream):
-            for _ in range(args.warmup):
-                model_step()
-                model_reduce()
-        torch.cuda.synchronize(dev)
-        m_graph = None
-        if not args.no_graph:
-            m_graph = torch.cuda.CUDAGraph()
-            with torch.cuda.graph(m_graph, stream=stream):
-                model_step()
-            with torch.cuda.stream(stream):
-                for _ in range(2):
-                    m_graph.replay()
-            torch.cuda.synchronize(dev)
-
-        def model_timed():
-            if m_graph is not None:
-                m_graph.replay()
-            else:
-                model_step()
-            model_reduce()
-
-        if args.ncu_step:
-            return ncu_step_and_exit(model_timed, "whole network")
-        ms_per_step, clk = time_steps(model_timed)
-        value = BATCH * world / (ms_per_step / 1000.0)
-        # block launches + stem / transitions / head kernels of dpb_model_step + SGD
-        launches_per_step += 11 + 9 * (len(cfg.block_sizes) - 1) + 1
-    else:
-        ms_per_step, clk, value = blocks_ms, blocks_clk, blocks_value
-
-    # ---- per-kernel roofline (separate profiled pass, events on `stream`) -----
-    for b in blocks:
-        b["plan"].profile(True)
     with torch.cuda.stream(stream):
-        for _ in range(2):
+        for _ in range(args.warmup):
+            model_step()
+    torch.cuda.synchronize(dev)
+    mplan.sync()
+    if args.ncu_step and args.ncu_what == "model":
+        torch.cuda.synchronize(dev)
+        torch.cuda.profiler.start()
+        with torch.cuda.stream(stream):
+            model_step()
+        torch.cuda.synchronize(dev)
+        torch.cuda.profiler.stop()
+        print(json.dumps({"ncu_step": "whole network"}), flush=True)
+        return 0
+    ms_per_step, clk = time_steps(model_step, args.steps)
+    value = BATCH * world / (ms_per_step / 1000.0)
+    mplan.sync()
+    launches_per_step = mplan.launch_count() + 1  # + SGD
+
+    # ---- end to end with host buffers: pinned images + labels in, loss out -------
+    x_h = torch.randn(BATCH, *cfg.in_shape, generator=g).pin_memory()
+    l_h = (torch.arange(BATCH, dtype=torch.int32) % cfg.num_classes).pin_memory()
+    loss_h = torch.empty(1).pin_memory()
+    e_x = torch.empty_like(m_x)
+    e_l = torch.empty_like(m_labels)
+
+    def e2e_step():
+        e_x.copy_(x_h, non_blocking=True)
+        e_l.copy_(l_h, non_blocking=True)
+        mplan.step(e_x, e_l, m_params, m_run, m_grads, m_loss)
+        model_update()
+        loss_h.copy_(m_loss, non_blocking=True)
+
+    with torch.cuda.stream(stream):
+        for _ in range(args.warmup):
+            e2e_step()
+    torch.cuda.synchronize(dev)
+    e_ms, _ = time_steps(e2e_step, args.steps)
+    e2e = {"value": BATCH * world / (e_ms / 1000.0), "unit": "images/s",
+           "h2d_bytes_per_step": x_h.numel() * 4 + l_h.numel() * 4, "d2h_bytes_per_step": 4,
+           "steps": args.steps,
+           "path": "ModelPlan.step (dpb_model_step, C ABI): pinned host images + labels -> H2D -> training "
+                   "step -> DP allreduce (N > 1) -> SGD -> D2H loss"}
+    mplan.sync()
+    loss_value = float(loss_h.item())
+
+    # ---- the dense blocks alone (the hot path) + per-kernel roofline -------------
+    blocks_value = blocks_ms = None
+    roof = kernels = step_roof = None
+    if not args.no_blocks:
+        blocks = []
+        with torch.cuda.stream(stream):
+            for s_ in shapes:
+                shp = P.BlockShape(*s_)
+                plan = P.BlockPlan(shp, dtype=args.dtype, layout="nhwc", device=local, stream=stream)
+                params = torch.randn(shp.param_elems, generator=g) * 0.1
+                for l, o in enumerate(shp.param_offsets()):
+                    c = shp.c_in(l)
+                    params[o:o + c] += 1.0
+                    gb = o + 2 * c + shp.bk * c
+                    params[gb:gb + shp.bk] += 1.0
+                blocks.append(dict(shape=shp, plan=plan, params=params.to(dev), running=shp.initial_running(dev),
+                                   x=torch.randn(shp.pixels, shp.c0, generator=g).to(dev),
+                                   gup=torch.randn(shp.pixels, shp.c_out, generator=g).to(dev),
+                                   acc=torch.empty(shp.pixels, shp.c_out, device=dev),
+                                   grads=torch.empty(shp.param_elems, device=dev)))
+
+        def blocks_step():
             for b in blocks:
                 b["plan"].forward(b["x"], b["params"], b["running"], True)
             for b in reversed(blocks):
-                b["acc"].copy_(b["gup"])
+                b["acc"].copy_(b["gup"])      # the consumer BN backward writes the block-output grad
                 b["plan"].backward(b["params"], b["acc"], b["grads"])
-    torch.cuda.synchronize(dev)
-    cats = {}
-    for b in blocks:
-        for name, st in b["plan"].profile_read().items():
-            c = cats.setdefault(name, {"launches": 0, "total_ms": 0.0, "bytes": 0.0, "flops": 0.0})
-            for key in c:
-                c[key] += st[key]
-        b["plan"].profile(False)
-    prof_total = sum(c["total_ms"] for c in cats.values())
-    # dominant kernel among the categories that move algorithmic HBM bytes
-    # (SURVEY 8(d) model); BN-statistic folds (finalize) carry none and are
-    # reported beside it
-    dom_name, dom = max(((k, v) for k, v in cats.items() if v["bytes"] > 0),
-                        key=lambda kv: kv[1]["total_ms"])
-    avg_ms = dom["total_ms"] / dom["launches"]
-    bytes_per_launch = dom["bytes"] / dom["launches"]
-    flops_per_launch = dom["flops"] / dom["launches"]
-    ridge = bf16_peak * 1e12 / (hbm_peak * 1e9)
-    intensity = flops_per_launch / max(bytes_per_launch, 1.0)
-    if intensity < ridge:
-        roof = {"bound": "hbm", "achieved": bytes_per_launch / (avg_ms * 1e-3) / 1e9, "peak": hbm_peak,
-                "unit": "GB/s"}
-    else:
-        roof = {"bound": "tensor", "achieved": flops_per_launch / (avg_ms * 1e-3) / 1e12,
-                "peak": bf16_sust, "unit": "TFLOP/s"}
-    roof["frac"] = roof["achieved"] / roof["peak"]
-    roof["traffic"] = committed_traffic(dom_name, args.config, args.dtype)
-    roof["kernel"] = dom_name
-    roof["kernel_share_of_step"] = dom["total_ms"] / prof_total
-    roof["excluded_zero_byte_kernels"] = {k: round(v["total_ms"] / prof_total, 4)
-                                          for k, v in cats.items() if v["bytes"] <= 0}
-    roof["peak_source"] = peak_src
-    roof["timing"] = ("profiled pass: every launch bracketed by CUDA events on its stream, the backward "
-                      "on one stream; in the timed step the weight-gradient kernels (conv*_wgrad, "
-                      "reduce_wgrad) run on a side stream overlapping the data-gradient chain, and the "
-                      "1x1 wgrad is sized to half the SMs for that overlap")
-    F_img, B_img = algorithmic_per_image(shapes)
-    t_roof = max(F_img / (bf16_peak * 1e12), B_img / (hbm_peak * 1e9))
-    # SURVEY 8(d) byte / FLOP model of the dense blocks: measured against the
-    # dense-blocks-only rate (the network's stem / transitions / head are outside it)
-    step_roof = {"scope": "dense blocks (SURVEY 8(d) model)",
-                 "algorithmic_gflop_per_img": F_img / 1e9, "algorithmic_mb_per_img": B_img / 1e6,
-                 "ceiling_img_per_s_per_gpu": 1.0 / t_roof,
-                 "frac": (blocks_value / world) * t_roof}
-    kernels = {k: {"launches": v["launches"], "ms": round(v["total_ms"] / 2, 4),
-                   "GB/s": round(v["bytes"] / max(v["total_ms"], 1e-9) / 1e6, 1),
-                   "TFLOP/s": round(v["flops"] / max(v["total_ms"], 1e-9) / 1e9, 2)}
-               for k, v in sorted(cats.items(), key=lambda kv: -kv[1]["total_ms"])}
-
-    # ---- end to end through the public API with host buffers --------------------
-    if whole:
-        # ModelPlan.step per step: H2D of the images and labels from pinned host
-        # memory, the training step, the DP allreduce (N > 1), D2H of the flat
-        # fp32 gradients and the loss
-        x_h = torch.randn(BATCH, *cfg.in_shape, generator=g).pin_memory()
-        l_h = (torch.arange(BATCH, dtype=torch.int32) % cfg.num_classes).pin_memory()
-        grads_h = torch.empty(mplan.param_elems).pin_memory()
-        loss_h = torch.empty(1).pin_memory()
-        e_x = torch.empty_like(m_x)
-        e_l = torch.empty_like(m_labels)
-
-        def e2e_step():
-            e_x.copy_(x_h, non_blocking=True)
-            e_l.copy_(l_h, non_blocking=True)
-            mplan.step(e_x, e_l, m_params, m_run, m_grads, m_loss)
-            model_reduce()
-            grads_h.copy_(m_grads, non_blocking=True)
-            loss_h.copy_(m_loss, non_blocking=True)
 
         with torch.cuda.stream(stream):
             for _ in range(args.warmup):
-                e2e_step()
+                blocks_step()
         torch.cuda.synchronize(dev)
-        ek = max(3, min(args.steps, 10))
-        e0 = torch.cuda.Event(enable_timing=True)
-        e1 = torch.cuda.Event(enable_timing=True)
-        with torch.cuda.stream(stream):
-            e0.record(stream)
-            for _ in range(ek):
-                e2e_step()
-            e1.record(stream)
-        torch.cuda.synchronize(dev)
-        ems = e0.elapsed_time(e1)
-        if world > 1:
-            tt = torch.tensor([ems], device=dev)
-            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-            ems = float(tt.item())
-        e2e = {"value": BATCH * world * ek / (ems / 1000.0), "unit": "images/s",
-               "h2d_bytes_per_step": x_h.numel() * 4 + l_h.numel() * 4,
-               "d2h_bytes_per_step": grads_h.numel() * 4 + 4, "steps": ek,
-               "path": "ModelPlan.step (dpb_model_step): pinned host images/labels -> training step -> "
-                       "host gradients and loss"}
-    else:
-        # HostBlockChain: per step, H2D of every block's input and upstream gradient
-        # from pinned host memory (copy stream, per-block events), the block
-        # forwards/backwards, the DP allreduce (N > 1) and the D2H of the flat fp32
-        # gradients, all inside the timed region.
-        from paper_1707_06990_b200.host import HostBlockChain
-        chain = HostBlockChain([b["shape"] for b in blocks], [b["params"] for b in blocks],
-                               [b["running"] for b in blocks], dtype=args.dtype, layout="nchw",
-                               device=dev, stream=stream, group=None)
-        x_h = [torch.randn(b["shape"].n, b["shape"].c0, b["shape"].h, b["shape"].w, generator=g).pin_memory()
-               for b in blocks]
-        g_h = [torch.randn(b["shape"].n, b["shape"].c_out, b["shape"].h, b["shape"].w, generator=g).pin_memory()
-               for b in blocks]
-        for _ in range(args.warmup):
-            chain.step(x_h, g_h)
-        torch.cuda.synchronize(dev)
-        ek = max(3, min(args.steps, 10))
-        e0 = torch.cuda.Event(enable_timing=True)
-        e1 = torch.cuda.Event(enable_timing=True)
-        with torch.cuda.stream(stream):
-            e0.record(stream)
-        for _ in range(ek):
-            chain.step(x_h, g_h)
-        with torch.cuda.stream(stream):
-            e1.record(stream)
-        torch.cuda.synchronize(dev)
-        ems = e0.elapsed_time(e1)
-        if world > 1:
-            tt = torch.tensor([ems], device=dev)
-            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-            ems = float(tt.item())
-        e2e = {"value": BATCH * world * ek / (ems / 1000.0), "unit": "images/s",
-               "h2d_bytes_per_step": chain.h2d_bytes(), "d2h_bytes_per_step": chain.d2h_bytes(), "steps": ek,
-               "path": "HostBlockChain.step: dpb_block_forward/backward (NCHW), pinned host buffers, "
-                       "H2D on a copy stream overlapping compute"}
-        chain.close()
+        graph = None
+        if not args.no_graph:
+            graph = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(graph, stream=stream):
+                blocks_step()
+        if args.ncu_step:
+            torch.cuda.synchronize(dev)
+            torch.cuda.profiler.start()
+            with torch.cuda.stream(stream):
+                graph.replay() if graph is not None else blocks_step()
+            torch.cuda.synchronize(dev)
+            torch.cuda.profiler.stop()
+            print(json.dumps({"ncu_step": "dense blocks"}), flush=True)
+            return 0
+        blocks_ms, _ = time_steps(lambda: graph.replay() if graph is not None else blocks_step(), args.steps)
+        blocks_value = BATCH * world / (blocks_ms / 1000.0)
 
+        # profiled pass: every launch bracketed by CUDA events on its stream
+        for b in blocks:
+            b["plan"].profile(True)
+        with torch.cuda.stream(stream):
+            for _ in range(2):
+                blocks_step()
+        torch.cuda.synchronize(dev)
+        cats = {}
+        for b in blocks:
+            for name, st in b["plan"].profile_read().items():
+                c = cats.setdefault(name, {"launches": 0, "total_ms": 0.0, "bytes": 0.0, "flops": 0.0,
+                                           "bytes_8d": 0.0})
+                for key in c:
+                    c[key] += st[key]
+            b["plan"].profile(False)
+            b["plan"].close()
+        prof_total = sum(c["total_ms"] for c in cats.values())
+        # dominant kernel: the largest share of the profiled pass, every category counted
+        dom_name, dom = max(cats.items(), key=lambda kv: kv[1]["total_ms"])
+        avg_s = dom["total_ms"] / dom["launches"] * 1e-3
+        b8 = dom["bytes_8d"] / dom["launches"]
+        b32 = dom["bytes"] / dom["launches"]
+        fl = dom["flops"] / dom["launches"]
+        ridge = bf16_peak * 1e12 / (hbm_peak * 1e9)
+        if fl / max(b8, 1.0) < ridge:
+            roof = {"bound": "hbm", "achieved": b8 / avg_s / 1e9, "peak": hbm_peak, "unit": "GB/s"}
+            roof["frac"] = roof["achieved"] / roof["peak"]
+            roof["achieved_fp32_storage"] = b32 / avg_s / 1e9
+            roof["frac_fp32_storage"] = roof["achieved_fp32_storage"] / hbm_peak
+        else:
+            roof = {"bound": "tensor", "achieved": fl / avg_s / 1e12, "peak": bf16_sust, "unit": "TFLOP/s"}
+            roof["frac"] = roof["achieved"] / roof["peak"]
+        roof.update({
+            "kernel": dom_name, "launches_per_pass": dom["launches"] // 2, "avg_launch_us": avg_s * 1e6,
+            "algorithmic_bytes_per_launch_8d": b8, "algorithmic_bytes_per_launch_fp32_storage": b32,
+            "traffic": committed_traffic(dom_name, args.config, args.dtype),
+            "kernel_share_of_pass": dom["total_ms"] / prof_total, "peak_source": peak_src,
+            "bytes_model": "achieved/frac: SURVEY 8(d) algorithmic bytes (2-byte activations, fp32 gradients); "
+                           "*_fp32_storage: the same traffic with this build's fp32 feature storage "
+                           "(DESIGN.md 2: bf16 storage breaks the 2e-2 gradient bound)",
+            "timing": "profiled pass of the dense blocks: CUDA events around every launch on its stream, "
+                      "backward on one stream"})
+        F_img, B_img = algorithmic_per_image(shapes)
+        t_roof = max(F_img / (bf16_peak * 1e12), B_img / (hbm_peak * 1e9))
+        step_roof = {"scope": "dense blocks (SURVEY 8(d) model)",
+                     "algorithmic_gflop_per_img": F_img / 1e9, "algorithmic_mb_per_img": B_img / 1e6,
+                     "ceiling_img_per_s_per_gpu": 1.0 / t_roof,
+                     "frac_dense_blocks": (blocks_value / world) * t_roof,
+                     "frac_whole_step": (value / world) * t_roof}
+        kernels = {k: {"launches": v["launches"] // 2, "ms": round(v["total_ms"] / 2, 4),
+                       "share": round(v["total_ms"] / prof_total, 4),
+                       "GB/s_8d": round(v["bytes_8d"] / max(v["total_ms"], 1e-9) / 1e6, 1),
+                       "GB/s_fp32_storage": round(v["bytes"] / max(v["total_ms"], 1e-9) / 1e6, 1),
+                       "TFLOP/s": round(v["flops"] / max(v["total_ms"], 1e-9) / 1e9, 2)}
+                   for k, v in sorted(cats.items(), key=lambda kv: -kv[1]["total_ms"])}
+        del blocks
+        torch.cuda.empty_cache()
 
-    # ---- memory: efficient arena vs naive store-everything ---------------------
-    eff = sum(P.block_memory(b["shape"], args.dtype)[0] for b in blocks)
-    naive = sum(P.block_memory(b["shape"], "fp32")[1] for b in blocks)
-    naive_measured = None
-    if rank == 0 and world == 1 and not args.no_naive and P.block_memory(blocks[0]["shape"], "fp32")[1] < 40e9:
-        naive_measured = measure_naive_block(blocks[0]["shape"], args.dtype)
+    # ---- memory: the efficient step's device footprint vs naive store-everything --
+    mem = mplan.memory()
+    peaks = {st: P.predict_peak_elements(cfg, st, BATCH, cfg.in_shape[0], shapes[0][1], shapes[0][2])
+             for st in ("naive", "shared-all")}
+    feat_elems = {st: sum(v for k, v in d.items() if k != "params") for st, d in peaks.items()}
+    memory = {
+        "efficient_activation_bytes": mem["activation_bytes"],
+        "efficient_total_allocated_bytes": mem["total_bytes"],
+        "efficient_allocated_measured_bytes": model_alloc_bytes,
+        "efficient_by_arena": mem["by_arena"],
+        "reference_peak_model_bytes_fp32": {st: 4 * v for st, v in feat_elems.items()},
+        "note": ("efficient: libdpb's device allocations for the whole step (tracked per arena; "
+                 "'measured' = cudaMemGetInfo delta around ModelPlan creation); reference_peak_model: "
+                 "predict_peak_elements (peak_model.hpp:37-158) feature arenas at this batch, fp32 — the "
+                 "reference's own geometry for the stem")}
+    if rank == 0 and world == 1 and not args.no_naive:
+        from paper_1707_06990_b200.naive import naive_network_replay
+        memory["naive_measured"] = naive_network_replay(cfg, BATCH, dev)
+        memory["ratio_efficient_over_naive"] = (mem["activation_bytes"] /
+                                                memory["naive_measured"]["allocator_peak_bytes"])
 
-    # ---- CPU baseline (rank 0, N=1 only) ---------------------------------------
+    # ---- CPU baseline (rank 0, N=1 only): the reference on the host cores --------
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
             from oracle import cpu_bench as CB
             runner, what = cpu_runner(args.config)
-            runner.step(seed=1)        # warm (spawn + page-in)
-            imgs, secs, n = 0, 0.0, 0
-            while secs < args.cpu_budget_s and n < 5:
-                a, s = runner.step(seed=10 + n)
-                imgs += a
-                secs += s
-                n += 1
+            a, secs = runner.step(seed=10)
             runner.close()
-            cpu = {"value": imgs / secs, "unit": "images/s", "cores": runner.procs, "kind": CB.kind(),
-                   "sample": f"{n} steps x {runner.procs} processes x {what}, {CB.cpu_model()}"}
+            cpu = {"value": a / secs, "unit": "images/s", "cores": runner.procs, "kind": CB.kind(),
+                   "sample": f"1 step x {runner.procs} processes x {what}, {CB.cpu_model()}"}
         except Exception as exc:  # the baseline is reported, never the target
             cpu = {"value": None, "unit": "images/s", "cores": 0, "kind": "port", "sample": f"failed: {exc}"}
 
     if rank == 0:
-        S = 2 if args.dtype == "bf16" else 4
-        ws_bytes = sum(P.plan_arena(b["shape"], args.dtype, "nhwc")["total_bytes"] for b in blocks)
+        ref_name, _ = reference_config(args.config)
         line = {
             "metric": METRIC, "value": value, "unit": "images/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
-            "vs_baseline": None, "dtype": args.dtype, "data": "synthetic",
-            "config": {"workload": (f"DenseNet-{args.config} full training step: stem, dense blocks, transitions, "
-                                    f"head, softmax-xent, fwd+bwd, momentum-SGD update" if whole else
-                                    f"DenseNet-{args.config} dense blocks, fwd+bwd (the {cfg.in_shape[1]}px "
-                                    f"7x7/2 stem is not built)"),
-                       "model": args.config, "global_batch": BATCH * world,
-                       "per_gpu_batch": BATCH, "blocks": [list(s) for s in shapes],
-                       "parallelism": f"dp{world}",
-                       "cuda_graph": graph is not None,
-                       "l2": f"working set {ws_bytes / 1e6:.0f} MB > 126 MB L2 (no explicit flush)"},
+            "vs_baseline": None, "dtype": args.dtype, "data": "synthetic (random-init weights, GraphPlan::build "
+                                                               "Rng replay; Gaussian images)",
+            "config": {"workload": (f"DenseNet-{args.config} whole training step at {'x'.join(map(str, cfg.in_shape))}"
+                                    f" ({cfg.stem} stem, dense blocks, transitions, head, softmax-xent, fwd+bwd, "
+                                    f"momentum-SGD update), batch {BATCH} per GPU"),
+                       "model": args.config, "global_batch": BATCH * world, "per_gpu_batch": BATCH,
+                       "blocks": [list(s_) for s_ in shapes], "parallelism": f"dp{world}",
+                       "reference_geometry": ref_name, "loss": loss_value,
+                       "cuda_graph": not args.no_graph,
+                       "l2": "inputs and working set (GBs of arena) far larger than the 126 MB L2; no flush"},
             "dense_blocks": {"value": blocks_value, "unit": "images/s", "ms_per_step": blocks_ms,
                              "note": "the dense blocks alone (the hot path), graph-captured"},
             "roofline": roof, "step_roofline": step_roof, "kernels": kernels,
             "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": launches_per_step * args.steps,
-            "memory": {"efficient_arena_bytes": eff, "naive_bytes": naive,
-                       "ratio": eff / naive, "naive_measured": naive_measured},
-            "clocks": clk,
+            "memory": memory, "clocks": clk,
         }
         print(json.dumps(line), flush=True)
-    for b in blocks:
-        b["plan"].close()
-    if mplan is not None:
-        mplan.close()
+    mplan.close()
     if world > 1:
         dist.destroy_process_group()
     return 0

@@ -162,6 +162,7 @@ class BlockPlan {
     cfg_ = o.cfg_;
     param_elems_ = o.param_elems_;
     stat_elems_ = o.stat_elems_;
+    freeze_running_ = o.freeze_running_;
     return *this;
   }
   BlockPlan(const BlockPlan&) = delete;

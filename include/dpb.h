@@ -124,6 +124,23 @@ typedef struct dpb_arena_sizes {
 
 typedef struct dpb_block dpb_block;
 
+/* Device-memory accounting of a handle (MemoryStats, alloctrace.hpp:40-50):
+ * live / peak bytes per arena tag (DPB_ARENA_*), the combined feature peak
+ * (every arena but Params) and the parameter bytes.  libdpb records every
+ * device allocation it makes, split by the regions it holds:
+ * FeatureOwned = features, bottleneck outputs, batch statistics (and, for a
+ * model, the stem / transition activations); SharedGrad = the block
+ * accumulators and the gradient transients; Scratch = reduction partials and
+ * the pre-tiled bf16 weight images.  Shared1 / Shared2 stay 0 (concat and
+ * BN+ReLU are recomputed inside the conv prologues).  Parameters and
+ * gradients are caller-owned and not counted. */
+typedef struct dpb_memory_stats {
+  int64_t live_bytes[6];
+  int64_t peak_bytes[6];
+  int64_t total_feature_peak_bytes;
+  int64_t param_bytes;
+} dpb_memory_stats;
+
 DPB_API const char* dpb_last_error(void);
 DPB_API const char* dpb_version(void);
 
@@ -168,6 +185,7 @@ DPB_API int dpb_block_read_z(dpb_block* blk, float* dst /* m x [n, bk, h, w] */)
 DPB_API int dpb_block_read_stats(dpb_block* blk, float* dst /* flat stats layout */);
 
 DPB_API int dpb_sync(dpb_block* blk);
+DPB_API int dpb_block_memory_stats(dpb_block* blk, dpb_memory_stats* out);
 
 /* Number of kernels the last forward/backward launched (bench accounting). */
 DPB_API int64_t dpb_block_launch_count(dpb_block* blk);
@@ -180,8 +198,9 @@ typedef struct dpb_kernel_stat {
   char name[32];
   int64_t launches;
   double total_ms;
-  double bytes;  /* algorithmic bytes summed over the launches */
+  double bytes;  /* algorithmic bytes summed over the launches (fp32 storage) */
   double flops;  /* algorithmic flops summed over the launches */
+  double bytes_8d; /* the same under SURVEY 8(d)'s model: 2-byte activations, fp32 gradients */
 } dpb_kernel_stat;
 DPB_API int dpb_block_profile(dpb_block* blk, int enable);
 DPB_API int dpb_block_profile_read(dpb_block* blk, dpb_kernel_stat* out, int max, int* count);
@@ -245,10 +264,11 @@ DPB_API int dpb_rng_fill_normal(uint64_t seed, float* host_dst, int64_t count);
  * avgpool before its 1x1 conv (the two commute), on a quarter of the pixels.
  * Parameters and gradients: one flat fp32 buffer in the reference's
  * registration order (graph.hpp:356-390, :456-600):
- *   stem.w[c0][in_c][3][3]; per block its dpb_block layout; per transition
+ *   stem.w[c0][in_c][3][3] (stem 1: stem.conv.w[c0][in_c][7][7]
+ *   stem.bn.gamma[c0] stem.bn.beta[c0]); per block its dpb_block layout; per transition
  *   bn.gamma[C] bn.beta[C] conv.w[c_out][C]; head.bn.gamma[C] head.bn.beta[C]
  *   head.linear.w[classes][C] head.linear.b[classes].
- * Running statistics in network order: block 0 (its dpb_block layout),
+ * Running statistics in network order: (stem 1: stem.bn mean[c0] var[c0]), block 0 (its dpb_block layout),
  * transition 0 mean[C] var[C], block 1, ..., last block, head mean[C] var[C].
  * Bottleneck networks only. */
 typedef struct dpb_model dpb_model;
@@ -262,9 +282,18 @@ typedef struct dpb_model_desc {
   int32_t in_c, in_h, in_w;
   int64_t batch;
   int32_t dtype;        /* DPB_FP32 | DPB_BF16 (dense blocks) */
+  int32_t stem;         /* 0: the reference's conv 3x3/1 stem (graph.hpp:430, :740-745);
+                           1: ImageNet stem conv 7x7/2 pad 3 -> BN -> ReLU -> max-pool
+                           3x3/2 pad 1 (extension; 224 -> 112 -> 56) */
 } dpb_model_desc;
 
 DPB_API int dpb_model_sizes(const dpb_model_desc* desc, int64_t* param_elems, int64_t* running_elems);
+/* GraphPlan<T>::build's parameter initialisation replayed draw for draw from
+ * Rng(seed) (graph.hpp:351-390, :405-600; rng.hpp:36-49) into a HOST buffer of
+ * dpb_model_sizes' param_elems floats: He-normal convs, BN gamma 1 / beta 0,
+ * classifier N(0, 1/C), bias 0 — bit-identical to the reference's params()
+ * for stem 0. */
+DPB_API int dpb_model_init_params(const dpb_model_desc* desc, uint64_t seed, float* host_params);
 DPB_API int dpb_model_create(const dpb_model_desc* desc, int device, void* stream, dpb_model** out);
 DPB_API void dpb_model_destroy(dpb_model* model);
 /* One training step: input NCHW [batch, in_c, in_h, in_w], labels int32
@@ -275,7 +304,15 @@ DPB_API void dpb_model_destroy(dpb_model* model);
  * replay it (DPB_MODEL_NO_GRAPH=1: always launch eagerly). */
 DPB_API int dpb_model_step(dpb_model* model, const float* input, const int32_t* labels,
                            const float* params, float* running, float* grads, float* loss);
+/* Waits for the step and surfaces its asynchronous errors: LabelError (8)
+ * when a label was outside [0, classes) — that sample's loss and gradients
+ * are NaN.  Gradients must not be used before dpb_model_sync succeeded. */
 DPB_API int dpb_model_sync(dpb_model* model);
+/* The model's device-memory accounting (every block arena + the stem,
+ * transition and head buffers) and the number of kernels one training step
+ * launches (the CUDA graph's kernel nodes once captured). */
+DPB_API int dpb_model_memory_stats(dpb_model* model, dpb_memory_stats* out);
+DPB_API int64_t dpb_model_launch_count(dpb_model* model);
 
 /* ---- optimizer -------------------------------------------
  * dpb_sgd_step replaces sgd_step (train.hpp:43-70) over a flat fp32 buffer:

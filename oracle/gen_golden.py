@@ -92,6 +92,12 @@ def kats():
     # denseplan::Rng (the reference's own engine + Box-Muller)
     d["rng_u64_seed7_first4"] = [int(v) for v in O.ref_rng_u64(7, 4)]
     d["rng_normal_seed106_first8"] = [float(v) for v in O.ref_rng_normal(106, 8)]
+    # GraphPlan::build's parameters at DenseNet-264 scale (tests/test_model_host.py)
+    import hashlib
+    d["params_sha256_seed7"] = {}
+    for name, (k, c0) in {"d264k32@56": (32, 64), "d264k48@56": (48, 96)}.items():
+        p, _ = O.ref_model_params([6, 12, 64, 48], k, 1, 0.5, 1000, c0, (1, 3, 56, 56), 7)
+        d["params_sha256_seed7"][name] = hashlib.sha256(p.tobytes()).hexdigest()
     return d
 
 
@@ -117,6 +123,49 @@ def make_model_case(name, blocks, k, comp, classes, c0, in_shape, seed):
     np.savez_compressed(os.path.join(OUT, f"{name}.npz"), blocks=np.array(blocks), k=k, compression=comp,
                         classes=classes, c0=c0, in_shape=np.array(in_shape), seed=seed, params=params,
                         x=x, labels=labels, loss=np.float64(loss), grads=grads)
+
+
+# Whole-network training steps with BN running statistics (F10), through the
+# reference's public forward / compute_loss / backward (ref_model_train_step).
+# Small cases store everything; the BASELINE-scale ones store per-tensor
+# sketches (norm, random projections, sampled elements: oracle.sketch).
+# Parameters are GraphPlan::build's for `seed` (libdpb replays them bit for
+# bit: tests/test_model_host.py); the ImageNet-stem cases use libdpb's init
+# for the stem-extended layout (dpb_model_init_params).  Input Rng(seed+99).
+TRAIN_CASES = {
+    # name: blocks, k, compression, classes, c0, (n, c, h, w), seed, stem, full
+    "train_small": ((2, 2, 2), 4, 0.5, 10, 8, (4, 3, 8, 8), 7, 0, True),
+    "train_imagenet_small": ((2, 2), 4, 0.5, 10, 8, (2, 3, 17, 19), 5, 1, True),
+    "train_imagenet_k32": ((2, 2), 32, 0.5, 10, 64, (2, 3, 32, 32), 9, 1, True),
+    # BASELINE configs[1]: DenseNet-BC-100 at its bench shape
+    "train_bc100_b64": ((16, 16, 16), 12, 0.5, 10, 24, (64, 3, 32, 32), 7, 0, True),
+    # BASELINE configs[3] / [4] in the reference's geometry (3x56x56)
+    "train_d264k32_56": ((6, 12, 64, 48), 32, 0.5, 1000, 64, (2, 3, 56, 56), 7, 0, False),
+    "train_d264k48_56": ((6, 12, 64, 48), 48, 0.5, 1000, 96, (2, 3, 56, 56), 7, 0, False),
+    # the bench headline network: DenseNet-264-k32 with the ImageNet stem at 224x224
+    "train_d264k32_224": ((6, 12, 64, 48), 32, 0.5, 1000, 64, (2, 3, 224, 224), 7, 1, False),
+}
+
+
+def make_train_case(name, blocks, k, comp, classes, c0, in_shape, seed, stem, full):
+    n, c, h, w = in_shape
+    params = None
+    if stem == 1:
+        sys.path.insert(0, os.path.dirname(OUT.rstrip("/").rsplit("/", 1)[0]))
+        from paper_1707_06990_b200.model import DenseNetConfig, init_params
+        params = init_params(DenseNetConfig(tuple(blocks), k, True, comp, classes, c0, (c, h, w), stem="imagenet"),
+                             seed)
+    loss, grads, running = O.ref_model_train_step(blocks, k, comp, classes, c0, in_shape, seed, stem, params)
+    meta = dict(blocks=np.array(blocks), k=k, compression=comp, classes=classes, c0=c0, in_shape=np.array(in_shape),
+                seed=seed, stem=stem, loss=np.float64(loss))
+    if full:
+        np.savez_compressed(os.path.join(OUT, f"{name}.npz"), grads=grads, running=running, **meta)
+        return
+    gs = O.sketch(grads, O.model_segments(blocks, k, comp, classes, c0, c, stem))
+    rs = O.sketch(running, O.running_segments(blocks, k, comp, c0, stem))
+    np.savez_compressed(os.path.join(OUT, f"{name}.npz"), **meta,
+                        **{f"grads_{key}": v for key, v in gs.items()},
+                        **{f"running_{key}": v for key, v in rs.items()})
 
 
 # Config text KATs (densenet.hpp:86-115, 276-377): every preset through
@@ -179,6 +228,10 @@ def main():
         json.dump(config_kats(), f, indent=1, sort_keys=True)
     if "--config-only" in sys.argv:
         return
+    if "--train" in sys.argv:  # one training-step case: python -m oracle.gen_golden --train NAME
+        name = sys.argv[sys.argv.index("--train") + 1]
+        make_train_case(name, *TRAIN_CASES[name])
+        return
     if "--model" in sys.argv:  # one model case only: python -m oracle.gen_golden --model NAME
         name = sys.argv[sys.argv.index("--model") + 1]
         make_model_case(name, *MODEL_CASES[name])
@@ -187,6 +240,8 @@ def main():
         make_case(name, s, src, dt)
     for name, args in MODEL_CASES.items():
         make_model_case(name, *args)
+    for name, args in TRAIN_CASES.items():
+        make_train_case(name, *args)
     with open(os.path.join(OUT, "kats.json"), "w") as f:
         json.dump(kats(), f, indent=1, sort_keys=True)
     print("wrote", sorted(os.listdir(OUT)))

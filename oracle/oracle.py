@@ -387,6 +387,123 @@ def ref_model_step(blocks, k, bottleneck, compression, classes, c0, in_shape, se
     return loss.value, secs.value
 
 
+def model_running_size(blocks, k, compression, c0, stem) -> int:
+    """Running-statistics elements of the libdpb model layout (include/dpb.h)."""
+    n, c = (2 * c0 if stem == 1 else 0), c0
+    for b, m in enumerate(blocks):
+        for l in range(m):
+            n += 2 * (c + l * k) + 2 * 4 * k
+        C = c + m * k
+        n += 2 * C
+        c = int(np.floor(compression * C))
+    return n
+
+
+def model_segments(blocks, k, compression, classes, c0, in_c=3, stem=0):
+    """(name, elements) of every parameter tensor in libdpb's registration
+    order (graph.hpp:405-600; the ImageNet stem's conv + BN first for stem=1)."""
+    bk = 4 * k
+    if stem == 1:
+        segs = [("stem.conv.w", c0 * in_c * 49), ("stem.bn.gamma", c0), ("stem.bn.beta", c0)]
+    else:
+        segs = [("stem.conv.w", c0 * in_c * 9)]
+    c = c0
+    for b, m in enumerate(blocks):
+        for l in range(m):
+            ci = c + l * k
+            segs += [(f"b{b}.l{l}.bn_a.gamma", ci), (f"b{b}.l{l}.bn_a.beta", ci), (f"b{b}.l{l}.conv_a.w", bk * ci),
+                     (f"b{b}.l{l}.bn_b.gamma", bk), (f"b{b}.l{l}.bn_b.beta", bk), (f"b{b}.l{l}.conv_b.w", k * bk * 9)]
+        C_ = c + m * k
+        if b + 1 < len(blocks):
+            cout = int(np.floor(compression * C_))
+            segs += [(f"t{b}.bn.gamma", C_), (f"t{b}.bn.beta", C_), (f"t{b}.conv.w", cout * C_)]
+            c = cout
+        else:
+            segs += [("head.bn.gamma", C_), ("head.bn.beta", C_), ("head.linear.w", classes * C_),
+                     ("head.linear.b", classes)]
+    return segs
+
+
+def running_segments(blocks, k, compression, c0, stem=0):
+    """(name, elements) of the running-statistics layout (include/dpb.h)."""
+    bk = 4 * k
+    segs = [("stem.bn.mean", c0), ("stem.bn.var", c0)] if stem == 1 else []
+    c = c0
+    for b, m in enumerate(blocks):
+        for l in range(m):
+            ci = c + l * k
+            segs += [(f"b{b}.l{l}.bn_a.mean", ci), (f"b{b}.l{l}.bn_a.var", ci), (f"b{b}.l{l}.bn_b.mean", bk),
+                     (f"b{b}.l{l}.bn_b.var", bk)]
+        C_ = c + m * k
+        nm = f"t{b}" if b + 1 < len(blocks) else "head"
+        segs += [(f"{nm}.bn.mean", C_), (f"{nm}.bn.var", C_)]
+        c = int(np.floor(compression * C_))
+    return segs
+
+
+def sketch(flat: np.ndarray, segs, nsample=256, nproj=4) -> dict:
+    """Size-independent fingerprint of a flat tensor list, per segment: the
+    2-norm, `nproj` projections onto fixed random +-1 vectors (their spread
+    estimates ||a - b||, so sqrt(mean(dproj^2)) / ||b|| is an unbiased
+    normwise-error estimate) and `nsample` elements at fixed indices."""
+    norms, projs, idx, vals = [], [], [], []
+    o = 0
+    for i, (_, n) in enumerate(segs):
+        seg = flat[o:o + n].astype(np.float64)
+        norms.append(np.linalg.norm(seg))
+        r = np.random.default_rng(7919 * i + 1)
+        projs.append([float(np.dot(np.where(r.random(n) < 0.5, -1.0, 1.0), seg)) for _ in range(nproj)])
+        take = np.arange(n) if n <= nsample else np.sort(r.choice(n, nsample, replace=False))
+        idx.append(o + take)
+        vals.append(flat[o + take])
+        o += n
+    assert o == flat.size
+    return {"norm": np.array(norms), "proj": np.array(projs), "idx": np.concatenate(idx),
+            "val": np.concatenate(vals)}
+
+
+def sketch_errors(got: np.ndarray, ref_sketch: dict, segs):
+    """Per-segment (normwise estimate from the projections, max elementwise
+    rel_err over the sampled elements) of `got` against a stored sketch."""
+    g = sketch(got, segs, nproj=ref_sketch["proj"].shape[1])
+    dproj = g["proj"] - ref_sketch["proj"]
+    est = np.sqrt(np.mean(dproj ** 2, axis=1)) / np.maximum(ref_sketch["norm"], 1e-30)
+    a = got[ref_sketch["idx"]].astype(np.float64)
+    b = ref_sketch["val"].astype(np.float64)
+    rel = np.abs(a - b) / np.maximum(1.0, np.maximum(np.abs(a), np.abs(b)))
+    return est, rel
+
+
+def ref_model_train_step(blocks, k, compression, classes, c0, in_shape, seed, stem=0, params=None, x=None):
+    """One reference training step through GraphPlan's public forward /
+    compute_loss / backward (ref_model_train_step_f32 in ref_driver.cpp),
+    composed with the ImageNet stem for stem=1.  Returns (loss, grads,
+    running) in libdpb's flat layouts; params None = GraphPlan::build's init
+    (stem 0 only), x None = Rng(seed + 99).normal()."""
+    L = ref_lib()
+    n, c, h, w = in_shape
+    count = ref_count_parameters(blocks, k, True, compression, classes, c0, c)
+    if stem == 1:
+        count += c0 * c * 49 - c0 * c * 9 + 2 * c0
+    if params is not None:
+        assert params.size == count and params.dtype == np.float32
+    grads = np.zeros(count, dtype=np.float32)
+    running = np.zeros(model_running_size(blocks, k, compression, c0, stem), dtype=np.float32)
+    loss = C.c_double()
+    arr = (C.c_int * len(blocks))(*blocks)
+    f = L.ref_model_train_step_f32
+    f.restype = C.c_int
+    f.argtypes = [C.c_int, _P, C.c_int, C.c_double, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, _I64,
+                  C.c_uint64, _P, _P, C.POINTER(C.c_double), _P, _P]
+    xx = None if x is None else np.ascontiguousarray(x, dtype=np.float32)
+    pp = None if params is None else np.ascontiguousarray(params)
+    rc = f(len(blocks), C.cast(arr, _P), k, compression, classes, c0, stem, c, h, w, n, seed, _ptr(pp), _ptr(xx),
+           C.byref(loss), _ptr(grads), _ptr(running))
+    if rc != 0:
+        raise RuntimeError(f"reference train step status {rc}: {L.ref_last_error().decode()}")
+    return loss.value, grads, running
+
+
 # ---- optimizer (SURVEY 8(f) row 2) -------------------------------------------------------
 def sgd_step(p, g, v, lr, momentum, weight_decay, nesterov):
     """train.hpp:43-70 restated in float32 numpy (every op rounded, no FMA):

@@ -496,6 +496,217 @@ int ref_model_step_f32(int nblocks, const int* blocks, int k, int bottleneck,
   });
 }
 
+}  // extern "C"
+
+// ---- one training step with running statistics (F10) and the ImageNet stem --------
+//
+// ref_model_train_step_f32 runs the reference's PUBLIC GraphPlan<float>
+// forward(Train) / compute_loss / backward (graph.hpp:726-826, 1065-1183) and
+// returns the loss, every parameter gradient and the BN running statistics
+// after the step.  GraphPlan keeps its BN states private and checkpoints omit
+// them, so the running statistics are derived from the public
+// StepState statistics with the reference's own momentum expression
+// (ops.hpp:185-194): r = (1 - 0.1f) * r0 + 0.1f * stat, r0 = (0, 1).
+//
+// stem 0: the reference network as is.  stem 1: the ImageNet stem (conv
+// 7x7/2 pad 3 -> BN -> ReLU -> max-pool 3x3/2 pad 1), which the reference does
+// not have, composed from the reference's public ops:: (conv2d_forward /
+// conv2d_backward with stride 2, batchnorm_forward / batchnorm_backward,
+// relu_inplace / relu_backward_inplace) plus a restated max-pool (first
+// maximum in (ky, kx) order wins; its backward scatters in (n, c, oy, ox)
+// order).  The rest of the network is the unmodified GraphPlan run on the
+// stem output with an identity 3x3 stem (centre tap 1: conv2d_forward then
+// returns its input exactly) under the Naive strategy — bitwise equal to
+// SharedAll (t/graph_test.cpp:99-111) — whose StepState.retained keeps the
+// block-0 gradient accumulator, the gradient w.r.t. the stem output.
+//
+// Flat layouts are libdpb's (include/dpb.h dpb_model_*): params / grads in
+// registration order with the stem first; running = (stem 1: stem mean, var)
+// then per block its per-layer (mean_a, var_a, mean_b, var_b), then the
+// transition / head (mean, var).  params may be null (GraphPlan::build init,
+// stem 0 only); x may be null (Rng(seed + 99).normal(), NCHW).
+namespace {
+
+float run_update(float r0, float stat) {  // ops.hpp:190-193, T = float
+  const float momentum = static_cast<float>(0.1);
+  return (float(1) - momentum) * r0 + momentum * stat;
+}
+
+void put_running(const ops::BatchStats<float>& st, float*& out) {
+  for (float v : st.mean) *out++ = run_update(0.f, v);
+  for (float v : st.var) *out++ = run_update(1.f, v);
+}
+
+struct MaxPool3 {  // 3x3 stride 2 pad 1 max-pool, restated (not in the reference)
+  std::vector<int> arg;  // per output: input flat index of the first maximum
+  Shape4 os;
+  void forward(const Tensor<float>& x, Tensor<float>& y) {
+    const Shape4& s = x.shape();
+    os = y.shape();
+    arg.assign(static_cast<std::size_t>(os.elems()), -1);
+    std::size_t o = 0;
+    for (std::int64_t i = 0; i < s.n; ++i)
+      for (std::int64_t c = 0; c < s.c; ++c)
+        for (std::int64_t oy = 0; oy < os.h; ++oy)
+          for (std::int64_t ox = 0; ox < os.w; ++ox, ++o) {
+            float best = 0.f;
+            int bi = -1;
+            for (std::int64_t ky = 0; ky < 3; ++ky) {
+              const std::int64_t iy = 2 * oy - 1 + ky;
+              if (iy < 0 || iy >= s.h) continue;
+              for (std::int64_t kx = 0; kx < 3; ++kx) {
+                const std::int64_t ix = 2 * ox - 1 + kx;
+                if (ix < 0 || ix >= s.w) continue;
+                const float v = x.at(i, c, iy, ix);
+                if (bi < 0 || v > best) {
+                  best = v;
+                  bi = static_cast<int>(((i * s.c + c) * s.h + iy) * s.w + ix);
+                }
+              }
+            }
+            y.at(i, c, oy, ox) = best;
+            arg[o] = bi;
+          }
+  }
+  void backward(const Tensor<float>& gy, Tensor<float>& gx) {
+    gx.fill(0.f);
+    std::size_t o = 0;
+    for (std::int64_t i = 0; i < os.n; ++i)
+      for (std::int64_t c = 0; c < os.c; ++c)
+        for (std::int64_t oy = 0; oy < os.h; ++oy)
+          for (std::int64_t ox = 0; ox < os.w; ++ox, ++o) gx.data()[arg[o]] += gy.at(i, c, oy, ox);
+  }
+};
+
+void model_train_step(int nblocks, const int* blocks, int k, double compression, int classes, int c0, int stem,
+                      int in_c, int in_h, int in_w, std::int64_t batch, std::uint64_t seed, const float* params,
+                      const float* x_in, double* loss, float* grads, float* running) {
+  const int kk = stem == 1 ? 7 : 3;
+  MemoryTracker tr;
+  const Shape4 in{batch, in_c, in_h, in_w};
+  Tensor<float> input = x_in ? from_flat(x_in, in, tr) : make_input<float>(in, seed + 99, tr);
+  const std::vector<int> labels = make_labels(static_cast<int>(batch), classes);
+
+  // ---- stem 1 forward (reference ops + restated max-pool) ----
+  ops::ConvParams<float> sconv;
+  ops::BatchNormState<float> sbn;
+  ops::BatchStats<float> sstats;
+  Tensor<float> sy, sact, spool;
+  MaxPool3 pool;
+  const std::int64_t swn = static_cast<std::int64_t>(c0) * in_c * kk * kk;
+  if (stem == 1) {
+    if (params == nullptr) throw ConfigError("the ImageNet stem needs explicit parameters");
+    sconv.weights = from_flat(params, Shape4{c0, in_c, 7, 7}, tr);
+    sconv.stride = 2;
+    sconv.padding = 3;
+    const std::vector<float> r0(static_cast<std::size_t>(c0), 0.f), r1(static_cast<std::size_t>(c0), 1.f);
+    sbn = make_bn(params + swn, params + swn + c0, r0.data(), r1.data(), c0, tr);
+    const Shape4 ys = ops::conv2d_out_shape(in, sconv);
+    sy = Tensor<float>::alloc(ys, ArenaTag::Scratch, tr);
+    ops::conv2d_forward(input, sconv, sy);
+    sact = Tensor<float>::alloc(ys, ArenaTag::Scratch, tr);
+    sstats = ops::batchnorm_forward(sy, sbn, ops::BnMode::Train, sact, true);
+    ops::relu_inplace(sact);
+    const Shape4 ps{batch, c0, (ys.h + 2 - 3) / 2 + 1, (ys.w + 2 - 3) / 2 + 1};
+    spool = Tensor<float>::alloc(ps, ArenaTag::Scratch, tr);
+    pool.forward(sact, spool);
+  }
+  const std::int64_t soff = stem == 1 ? swn + 2 * c0 : swn;  // params after the stem
+
+  // ---- the reference network ----
+  const DenseNetConfig cfg = model_cfg(nblocks, blocks, k, 1, compression, classes, c0);
+  const Shape4 gin = stem == 1 ? spool.shape() : in;
+  GraphPlan<float> plan =
+      GraphPlan<float>::build(cfg, stem == 1 ? ExecutionStrategy::Naive : ExecutionStrategy::SharedAll, gin, seed);
+  {
+    std::size_t off = 0;
+    for (auto& p : plan.params()) {
+      const std::int64_t n = p.value.elems();
+      if (p.name == "stem.conv.w") {
+        if (stem == 1) {  // identity 3x3: out[o] = in[o]
+          p.value.fill(0.f);
+          for (std::int64_t o = 0; o < c0; ++o) p.value.at(o, o, 1, 1) = 1.f;
+        } else if (params) {
+          std::memcpy(p.value.data(), params, sizeof(float) * static_cast<std::size_t>(n));
+        }
+        off = static_cast<std::size_t>(soff);
+        continue;
+      }
+      if (params) std::memcpy(p.value.data(), params + off, sizeof(float) * static_cast<std::size_t>(n));
+      off += static_cast<std::size_t>(n);
+    }
+  }
+  StepState<float> state = plan.forward(stem == 1 ? spool : input, ops::BnMode::Train);
+  *loss = plan.compute_loss(state, labels);
+  plan.backward(state);
+
+  // gradients (registration order), the stem's from the composition below
+  {
+    std::size_t off = 0;
+    for (const auto& p : plan.params()) {
+      const std::int64_t n = p.grad.elems();
+      if (p.name == "stem.conv.w") {
+        if (stem == 0) to_flat(p.grad, grads);
+        off = static_cast<std::size_t>(soff);
+        continue;
+      }
+      to_flat(p.grad, grads + off);
+      off += static_cast<std::size_t>(n);
+    }
+  }
+  // running statistics (F10)
+  float* r = running;
+  if (stem == 1) put_running(sstats, r);
+  for (std::size_t b = 0; b < state.blocks.size(); ++b) {
+    for (const auto& ls : state.blocks[b].layers) {
+      put_running(ls.stats_a, r);
+      put_running(ls.stats_b, r);
+    }
+    put_running(b + 1 < state.blocks.size() ? state.trans[b].stats : state.head.stats, r);
+  }
+
+  // ---- stem 1 backward ----
+  if (stem == 1) {
+    const Shape4 ps = spool.shape();
+    const std::int64_t C0out = c0 + static_cast<std::int64_t>(blocks[0]) * k;
+    const Tensor<float>* acc0 = nullptr;  // the last retained [N, C0out, H0, W0]: block-0 accumulator
+    for (const auto& t : state.retained)
+      if (t.shape() == Shape4{ps.n, C0out, ps.h, ps.w}) acc0 = &t;
+    if (acc0 == nullptr) throw AccountingError("block-0 accumulator not retained");
+    Tensor<float> gpool = Tensor<float>::alloc(ps, ArenaTag::Scratch, tr);
+    for (std::int64_t i = 0; i < ps.n; ++i)
+      for (std::int64_t c = 0; c < c0; ++c)
+        for (std::int64_t y = 0; y < ps.h; ++y)
+          for (std::int64_t x = 0; x < ps.w; ++x) gpool.at(i, c, y, x) = acc0->at(i, c, y, x);
+    Tensor<float> ga = Tensor<float>::alloc(sy.shape(), ArenaTag::Scratch, tr);
+    pool.backward(gpool, ga);
+    ops::relu_backward_inplace(ga, sact);
+    Tensor<float> gy = Tensor<float>::alloc(sy.shape(), ArenaTag::Scratch, tr);
+    Tensor<float> dg = Tensor<float>::alloc(Shape4{1, c0, 1, 1}, ArenaTag::Scratch, tr);
+    Tensor<float> db = Tensor<float>::alloc(Shape4{1, c0, 1, 1}, ArenaTag::Scratch, tr);
+    ops::batchnorm_backward(ga, sy, sbn, sstats, gy, dg, db);
+    Tensor<float> dw = Tensor<float>::alloc(sconv.weights.shape(), ArenaTag::Scratch, tr);
+    ops::conv2d_backward(gy, input, sconv, static_cast<Tensor<float>*>(nullptr), dw);
+    to_flat(dw, grads);
+    to_flat(dg, grads + swn);
+    to_flat(db, grads + swn + c0);
+  }
+}
+
+}  // namespace
+
+extern "C" int ref_model_train_step_f32(int nblocks, const int* blocks, int k, double compression, int classes,
+                                        int c0, int stem, int in_c, int in_h, int in_w, std::int64_t batch,
+                                        std::uint64_t seed, const float* params, const float* x, double* loss,
+                                        float* grads, float* running) {
+  return guarded([&] {
+    model_train_step(nblocks, blocks, k, compression, classes, c0, stem, in_c, in_h, in_w, batch, seed, params, x,
+                     loss, grads, running);
+  });
+}
+
+extern "C" {
+
 // The reference's sgd_step (train.hpp:43-70) over one flat parameter of n
 // elements: params / velocity updated in place from grads.
 int ref_sgd_step_f32(float* params, const float* grads, float* velocity, std::int64_t n, double lr,

@@ -38,13 +38,18 @@ class ArenaSizes(C.Structure):
 
 class KernelStat(C.Structure):
     _fields_ = [("name", C.c_char * 32), ("launches", _I64), ("total_ms", C.c_double),
-                ("bytes", C.c_double), ("flops", C.c_double)]
+                ("bytes", C.c_double), ("flops", C.c_double), ("bytes_8d", C.c_double)]
+
+
+class MemoryStats(C.Structure):
+    _fields_ = [("live_bytes", _I64 * 6), ("peak_bytes", _I64 * 6), ("total_feature_peak_bytes", _I64),
+                ("param_bytes", _I64)]
 
 
 class ModelDesc(C.Structure):
     _fields_ = [("nblocks", _I32), ("blocks", _I32 * 8), ("k", _I32), ("compression", C.c_double),
                 ("classes", _I32), ("c0", _I32), ("in_c", _I32), ("in_h", _I32), ("in_w", _I32),
-                ("batch", _I64), ("dtype", _I32)]
+                ("batch", _I64), ("dtype", _I32), ("stem", _I32)]
 
 
 # every symbol the header declares: (name, restype, argtypes)
@@ -80,10 +85,14 @@ SIGNATURES = {
                                             _I32, _I32, _I32, _P]),
     "dpb_rng_fill_normal": (C.c_int, [C.c_uint64, _P, _I64]),
     "dpb_model_sizes": (C.c_int, [C.POINTER(ModelDesc), C.POINTER(_I64), C.POINTER(_I64)]),
+    "dpb_model_init_params": (C.c_int, [C.POINTER(ModelDesc), C.c_uint64, _P]),
     "dpb_model_create": (C.c_int, [C.POINTER(ModelDesc), C.c_int, _P, C.POINTER(_P)]),
     "dpb_model_destroy": (None, [_P]),
     "dpb_model_step": (C.c_int, [_P, _P, _P, _P, _P, _P, _P]),
     "dpb_model_sync": (C.c_int, [_P]),
+    "dpb_model_memory_stats": (C.c_int, [_P, C.POINTER(MemoryStats)]),
+    "dpb_model_launch_count": (_I64, [_P]),
+    "dpb_block_memory_stats": (C.c_int, [_P, C.POINTER(MemoryStats)]),
     "dpb_sgd_step": (C.c_int, [_P, _P, _P, _I64, C.c_double, C.c_double, C.c_double, C.c_int, _P]),
     "dpb_lr_at": (C.c_int, [C.c_int, C.c_double, C.c_int, _P, C.c_int, C.c_double, C.c_double, C.c_int,
                             C.POINTER(C.c_double)]),

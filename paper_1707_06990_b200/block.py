@@ -178,12 +178,14 @@ class BlockPlan:
         check(lib().dpb_block_profile(self._h, int(enable)))
 
     def profile_read(self) -> dict:
-        """{category: {launches, total_ms, bytes, flops}} since profile(True)."""
+        """{category: {launches, total_ms, bytes, flops, bytes_8d}} since profile(True);
+        bytes with this build's fp32 storage, bytes_8d under SURVEY 8(d)'s model."""
         arr = (KernelStat * 32)()
         n = C.c_int()
         check(lib().dpb_block_profile_read(self._h, arr, 32, C.byref(n)))
         return {arr[i].name.decode(): {"launches": int(arr[i].launches), "total_ms": float(arr[i].total_ms),
-                                       "bytes": float(arr[i].bytes), "flops": float(arr[i].flops)}
+                                       "bytes": float(arr[i].bytes), "flops": float(arr[i].flops),
+                                       "bytes_8d": float(arr[i].bytes_8d)}
                 for i in range(n.value)}
 
     # -- read-back in the reference layout -------------------------------------

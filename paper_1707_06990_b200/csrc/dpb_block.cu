@@ -43,11 +43,12 @@ static cudaEvent_t next_event(Block* b) {
   return b->ev_pool[b->ev_used++];
 }
 
-LaunchScope::LaunchScope(Block* blk, int cat_, double bytes, double flops) : b(blk), cat(cat_) {
+LaunchScope::LaunchScope(Block* blk, int cat_, double bytes, double flops, double bytes_8d)
+    : b(blk), cat(cat_) {
   b->launches++;
   current_cat() = cat_;
   if (!b->prof) return;
-  ProfRec r{cat_, next_event(b), next_event(b), bytes, flops};
+  ProfRec r{cat_, next_event(b), next_event(b), bytes, flops, bytes_8d};
   cudaEventRecord(r.start, b->stream);
   idx = static_cast<int>(b->recs.size());
   b->recs.push_back(r);
@@ -301,9 +302,10 @@ static void forward_impl(Block* b, const float* x_in, const float* params, float
   S* feat = static_cast<S*>(b->feat);
   const int64_t hw = d.h * d.w;
   const double M = static_cast<double>(g.M), Sb = g.S;
-  // block input -> channels [0, c0) of the feature buffer (zero-copy concat)
-  {
-    LaunchScope ls(b, KC_PACK, M * d.c0 * (4 + Sb), 0);
+  // block input -> channels [0, c0) of the feature buffer (zero-copy concat);
+  // the whole-network step writes it there directly (x_in == feat, NHWC)
+  if (static_cast<const void*>(x_in) != b->feat || d.layout != DPB_NHWC) {
+    LaunchScope ls(b, KC_PACK, M * d.c0 * (4 + Sb), 0, M * d.c0 * (4 + 2.0));
     if (d.layout == DPB_NCHW) {
       dim3 grid(blocks_for(hw, 32), blocks_for(d.c0, 32), static_cast<unsigned>(d.n));
       launch(k_nchw_to_nhwc<S>, grid, dim3(32, 8), 0, b->stream, x_in, d.n, d.c0, hw, feat,
@@ -314,7 +316,7 @@ static void forward_impl(Block* b, const float* x_in, const float* params, float
     }
   }
   if (b->tc) {
-    LaunchScope ls(b, KC_PACK, 0, 0);
+    LaunchScope ls(b, KC_PACK, 0, 0, 0);
     b->launches--;  // counted inside tc2_pretile_w1
     tc2_pretile_w1(b, params);
     tc_pretile_w2(b, params, true);
@@ -324,11 +326,11 @@ static void forward_impl(Block* b, const float* x_in, const float* params, float
   float* fvar = b->fstat + g.Cp;
   if (!eval) {
     {
-      LaunchScope ls(b, KC_STATS, M * d.c0 * Sb, 0);
-      launch(k_channel_partials<S>, g.P, 256, 0, b->stream, feat, static_cast<int>(g.Cp), 0, g.M,
-                                                        d.c0, b->part);
+      LaunchScope ls(b, KC_STATS, M * d.c0 * Sb, 0, M * d.c0 * 2.0);
+      launch(k_channel_partials<S>, dim3(g.P, static_cast<unsigned>((d.c0 + 31) / 32)), 256, 0, b->stream, feat,
+             static_cast<int>(g.Cp), 0, g.M, d.c0, b->part);
     }
-    LaunchScope ls(b, KC_FINALIZE, 0, 0);
+    LaunchScope ls(b, KC_FINALIZE, 16.0 * g.P * d.c0, 0, 16.0 * g.P * d.c0);
     launch(k_finalize_stats, static_cast<unsigned>((d.c0 + kFinCh - 1) / kFinCh), kFinThreads, 0, b->stream, 
         b->part, g.P, d.c0, count, fmean, fvar, 0);
   }
@@ -343,32 +345,32 @@ static void forward_impl(Block* b, const float* x_in, const float* params, float
       a.bvar = r + 2 * a.c + d.bk;
     }
     {
-      LaunchScope ls(b, KC_C1_FWD, M * (a.c + d.bk) * Sb, 2.0 * M * a.c * d.bk);
+      LaunchScope ls(b, KC_C1_FWD, M * (a.c + d.bk) * Sb, 2.0 * M * a.c * d.bk, M * (a.c + d.bk) * 2.0);
       if (b->tc) {
         if (!tc2_conv1x1_fwd(b, a, l)) tc_conv1x1_fwd(b, a);
       }
       else gemm_bn<128, Conv1x1Fwd>(b, a, g.M, d.bk, 1);
     }
     if (!eval) {
-      LaunchScope ls(b, KC_FINALIZE, 0, 0);
+      LaunchScope ls(b, KC_FINALIZE, 16.0 * g.P * d.bk, 0, 16.0 * g.P * d.bk);
       float* zm = b->zstat + static_cast<int64_t>(l) * 2 * d.bk;
       launch(k_finalize_stats, static_cast<unsigned>((d.bk + kFinCh - 1) / kFinCh), kFinThreads, 0, b->stream, 
           b->part, g.P, d.bk, count, zm, zm + d.bk, 0);
     }
     int p3 = g.P;
     {
-      LaunchScope ls(b, KC_C3_FWD, M * (d.bk + d.k) * Sb, 2.0 * M * 9 * d.bk * d.k);
+      LaunchScope ls(b, KC_C3_FWD, M * (d.bk + d.k) * Sb, 2.0 * M * 9 * d.bk * d.k, M * (d.bk + d.k) * 2.0);
       if (b->tc) p3 = tc_conv3x3_fwd(b, a, l);
       else gemm_bn<128, Conv3x3Fwd>(b, a, g.M, d.k, 1);
     }
     if (!eval) {
-      LaunchScope ls(b, KC_FINALIZE, 0, 0);
+      LaunchScope ls(b, KC_FINALIZE, 16.0 * p3 * d.k, 0, 16.0 * p3 * d.k);
       launch(k_finalize_stats, static_cast<unsigned>((d.k + kFinCh - 1) / kFinCh), kFinThreads, 0, b->stream, 
           b->part, p3, d.k, count, fmean, fvar, a.c);
     }
   }
   if (!eval && update_running) {
-    LaunchScope ls(b, KC_RUNNING, 0, 0);
+    LaunchScope ls(b, KC_RUNNING, 0, 0, 0);
     launch(k_running_update, blocks_for(b->sz.stat_elems, 256), 256, 0, b->stream, 
         d.m, d.c0, d.k, d.bk, static_cast<int>(g.Cp), b->fstat, b->zstat, running,
         b->sz.stat_elems);
@@ -383,7 +385,7 @@ static void backward_impl(Block* b, const float* params, float* grad_acc, float*
   const double M = static_cast<double>(g.M), Sb = g.S;
   const double count = M;
   if (d.layout == DPB_NCHW) {
-    LaunchScope ls(b, KC_PACK, M * g.C * 8, 0);
+    LaunchScope ls(b, KC_PACK, M * g.C * 8, 0, M * g.C * 8);
     b->acc_cur = b->acc;
     dim3 grid(blocks_for(hw, 32), blocks_for(g.C, 32), static_cast<unsigned>(d.n));
     launch(k_nchw_to_nhwc<float>, grid, dim3(32, 8), 0, b->stream, grad_acc, d.n, g.C, hw,
@@ -392,7 +394,7 @@ static void backward_impl(Block* b, const float* params, float* grad_acc, float*
     b->acc_cur = grad_acc;
   }
   if (b->tc) {
-    LaunchScope ls(b, KC_PACK, 0, 0);
+    LaunchScope ls(b, KC_PACK, 0, 0, 0);
     b->launches--;
     tc_pretile_w2(b, params, false);  // each pretile counts its own launch
     tc2_pretile_w1t(b, params);
@@ -430,7 +432,7 @@ static void backward_impl(Block* b, const float* params, float* grad_acc, float*
       const int64_t rows = 9LL * d.bk;
       int splits;
       {
-        LaunchScope ls(b, KC_C3_WGRAD, M * (4.0 * d.k + Sb * d.bk), f3);
+        LaunchScope ls(b, KC_C3_WGRAD, M * (4.0 * d.k + Sb * d.bk), f3, M * (4.0 * d.k + 2.0 * d.bk));
         if (b->tc) {
           splits = tc_conv3x3_wgrad(b, a);
         } else {
@@ -441,7 +443,7 @@ static void backward_impl(Block* b, const float* params, float* grad_acc, float*
           gemm_bn<128, Conv3x3Wgrad>(b, a, rows, d.k, splits);
         }
       }
-      LaunchScope ls(b, KC_REDUCE_W, 4.0 * splits * rows * d.k, 0);
+      LaunchScope ls(b, KC_REDUCE_W, 4.0 * splits * rows * d.k, 0, 4.0 * splits * rows * d.k);
       launch(k_reduce_w2, blocks_for(9LL * d.k * d.bk, 32), dim3(32, 8), 0, b->stream, 
           b->wpart, splits, d.bk, d.k, d_w2);
     }
@@ -449,13 +451,13 @@ static void backward_impl(Block* b, const float* params, float* grad_acc, float*
     // ---- data chain: 3x3 dgrad (+ReLU mask by act_b, BN_b sums) ----
     int pd = g.P;
     {
-      LaunchScope ls(b, KC_C3_DGRAD, M * (4.0 * d.k + Sb * d.bk + 4.0 * d.bk), f3);
+      LaunchScope ls(b, KC_C3_DGRAD, M * (4.0 * d.k + Sb * d.bk + 4.0 * d.bk), f3, M * (4.0 * d.k + 2.0 * d.bk + 4.0 * d.bk));
       if (b->tc) pd = tc_conv3x3_dgrad(b, a, l);
       else gemm_bn<128, Conv3x3Dgrad>(b, a, g.M, d.bk, 1);
     }
     // BN_b backward sums -> dgamma_b, dbeta_b, coefficients (graph.hpp:913-916)
     {
-      LaunchScope ls(b, KC_FINALIZE, 0, 0);
+      LaunchScope ls(b, KC_FINALIZE, 16.0 * pd * d.bk, 0, 16.0 * pd * d.bk);
       launch(k_finalize_bn_bwd, static_cast<unsigned>((d.bk + kFinCh - 1) / kFinCh), kFinThreads, 0, b->stream, 
           b->part, pd, d.bk, count, d_gb, d_bb, const_cast<float*>(a.bnb_bwd));
     }
@@ -469,7 +471,7 @@ static void backward_impl(Block* b, const float* params, float* grad_acc, float*
       int splits;
       bool v2 = false;  // v2 partials are [split][j][i] like the SIMT ones
       {
-        LaunchScope ls(b, KC_C1_WGRAD, M * ((4.0 + Sb) * d.bk + Sb * a.c), f1);
+        LaunchScope ls(b, KC_C1_WGRAD, M * ((4.0 + Sb) * d.bk + Sb * a.c), f1, M * ((4.0 + 2.0) * d.bk + 2.0 * a.c));
         if (b->tc) {
           splits = tc2_conv1x1_wgrad(b, a);
           v2 = splits > 0;
@@ -481,7 +483,7 @@ static void backward_impl(Block* b, const float* params, float* grad_acc, float*
           gemm_bn2<64, Conv1x1Wgrad>(b, a, d.bk, a.c, splits);
         }
       }
-      LaunchScope ls(b, KC_REDUCE_W, 4.0 * splits * d.bk * a.c, 0);
+      LaunchScope ls(b, KC_REDUCE_W, 4.0 * splits * d.bk * a.c, 0, 4.0 * splits * d.bk * a.c);
       if (b->tc && !v2)
         launch(k_reduce_w1t, blocks_for(static_cast<int64_t>(d.bk) * a.c, 32), dim3(32, 8), 0, b->stream, b->wpart, splits, d.bk, a.c, d_w1);
       else
@@ -491,7 +493,7 @@ static void backward_impl(Block* b, const float* params, float* grad_acc, float*
     b->stream = main_st;
     // ---- data chain: 1x1 dgrad (+ReLU mask by act_a, BN_a sums) ----
     {
-      LaunchScope ls(b, KC_C1_DGRAD, M * ((4.0 + Sb) * d.bk + (Sb + 4.0) * a.c), f1);
+      LaunchScope ls(b, KC_C1_DGRAD, M * ((4.0 + Sb) * d.bk + (Sb + 4.0) * a.c), f1, M * ((4.0 + 2.0) * d.bk + (2.0 + 4.0) * a.c));
       if (b->tc) {
         if (!tc2_conv1x1_dgrad(b, a, l)) tc_conv1x1_dgrad(b, a);
       }
@@ -499,12 +501,12 @@ static void backward_impl(Block* b, const float* params, float* grad_acc, float*
     }
     // BN_a backward (graph.hpp:929-932) + concat-backward accumulate (:936-941)
     {
-      LaunchScope ls(b, KC_FINALIZE, 0, 0);
+      LaunchScope ls(b, KC_FINALIZE, 16.0 * g.P * a.c, 0, 16.0 * g.P * a.c);
       launch(k_finalize_bn_bwd, static_cast<unsigned>((a.c + kFinCh - 1) / kFinCh), kFinThreads, 0, b->stream, 
           b->part, g.P, a.c, count, d_ga, d_ba, b->bna_bwd);
     }
     {
-      LaunchScope ls(b, KC_BN_APPLY_ACC, M * a.c * (4.0 + Sb + 8.0), 0);
+      LaunchScope ls(b, KC_BN_APPLY_ACC, M * a.c * (4.0 + Sb + 8.0), 0, M * a.c * (4.0 + 2.0 + 8.0));
       const bool quads = std::is_same<S, float>::value && a.Ca % 4 == 0 &&
                          (reinterpret_cast<uintptr_t>(b->acc_cur) & 15) == 0;
       if (quads)
@@ -523,7 +525,7 @@ static void backward_impl(Block* b, const float* params, float* grad_acc, float*
     if (d.m > 1) cudaStreamWaitEvent(main_st, ev(1, 2), 0);
   }
   if (d.layout == DPB_NCHW) {
-    LaunchScope ls(b, KC_PACK, M * g.C * 8, 0);
+    LaunchScope ls(b, KC_PACK, M * g.C * 8, 0, M * g.C * 8);
     dim3 grid(blocks_for(hw, 32), blocks_for(g.C, 32), static_cast<unsigned>(d.n));
     launch(k_nhwc_to_nchw<float>, grid, dim3(32, 8), 0, b->stream, b->acc, static_cast<int>(g.Cp), 0,
                                                                d.n, g.C, hw, grad_acc);
@@ -538,6 +540,15 @@ void launch_finalize_bn_bwd(cudaStream_t st, const double2* part, int P, int nch
 }
 void launch_fold_splits(cudaStream_t st, const float* wpart, int splits, int64_t n, float* out) {
   launch(k_reduce_w1, blocks_for(n, 32), dim3(32, 8), 0, st, wpart, splits, 1, static_cast<int>(n), out);
+}
+void launch_channel_partials(cudaStream_t st, const float* src, int pitch, int64_t M, int nch, double2* part) {
+  launch(k_channel_partials<float>, dim3(blocks_for(M, 128), static_cast<unsigned>((nch + 31) / 32)), 256, 0, st,
+         src, pitch, 0, M, nch, part);
+}
+void launch_finalize_stats(cudaStream_t st, const double2* part, int P, int nch, double count, float* mean,
+                           float* var) {
+  launch(k_finalize_stats, static_cast<unsigned>((nch + kFinCh - 1) / kFinCh), kFinThreads, 0, st, part, P, nch,
+         count, mean, var, 0);
 }
 
 int block_forward(Block* b, const float* x_in, const float* params, float* running,
@@ -607,7 +618,7 @@ int read_stats(Block* b, float* dst) {
   return e == cudaSuccess ? DPB_OK : cuda_fail(e, "read_stats");
 }
 
-int create(const dpb_block_desc* desc, int device, void* stream, Block** out) {
+int create(const dpb_block_desc* desc, int device, void* stream, Block** out, DeviceTracker* tracker) {
   int rc = validate(desc);
   if (rc) return rc;
   if (out == nullptr) return fail(DPB_CONFIG_ERROR, "null output handle");
@@ -625,6 +636,14 @@ int create(const dpb_block_desc* desc, int device, void* stream, Block** out) {
   if (e != cudaSuccess) {
     delete b;
     return cuda_fail(e, "arena cudaMalloc");
+  }
+  if (tracker) b->tracker = tracker;
+  {
+    const dpb_arena_sizes& z = b->sz;
+    const int64_t owned = z.feat_bytes + z.z_bytes + z.stats_bytes, grad = z.acc_bytes + z.g0_bytes + z.g1_bytes;
+    b->tracker->alloc(DPB_ARENA_FEATURE_OWNED, owned);
+    b->tracker->alloc(DPB_ARENA_SHARED_GRAD, grad);
+    b->tracker->alloc(DPB_ARENA_SCRATCH, z.total_bytes - owned - grad);  // partials, weight images, alignment
   }
   char* base = static_cast<char*>(b->arena);
   b->feat = base + b->sz.feat_offset;
@@ -686,7 +705,14 @@ int create(const dpb_block_desc* desc, int device, void* stream, Block** out) {
 
 void destroy(Block* b) {
   if (!b) return;
-  if (b->arena) cudaFree(b->arena);
+  if (b->arena) {
+    cudaFree(b->arena);
+    const dpb_arena_sizes& z = b->sz;
+    const int64_t owned = z.feat_bytes + z.z_bytes + z.stats_bytes, grad = z.acc_bytes + z.g0_bytes + z.g1_bytes;
+    b->tracker->free(DPB_ARENA_FEATURE_OWNED, owned);
+    b->tracker->free(DPB_ARENA_SHARED_GRAD, grad);
+    b->tracker->free(DPB_ARENA_SCRATCH, z.total_bytes - owned - grad);
+  }
   for (cudaEvent_t e : b->ev_pool) cudaEventDestroy(e);
   for (cudaEvent_t e : b->fork_ev) cudaEventDestroy(e);
   if (b->side) cudaStreamDestroy(b->side);
@@ -713,6 +739,7 @@ int profile_read(Block* b, dpb_kernel_stat* out, int max, int* count) {
     acc[r.cat].total_ms += ms;
     acc[r.cat].bytes += r.bytes;
     acc[r.cat].flops += r.flops;
+    acc[r.cat].bytes_8d += r.bytes_8d;
   }
   int n = 0;
   for (int c = 0; c < KC_COUNT && n < max; ++c)

@@ -10,6 +10,7 @@
 
 #include "../../include/dpb.h"
 #include "dpb_internal.h"
+#include "dpb_launch.h"
 
 namespace dpb {
 int op_batch_statistics(const float*, int64_t, int64_t, int64_t, int64_t, float*, float*,
@@ -103,6 +104,7 @@ int dpb_block_param_elems(const dpb_block_desc* desc, int64_t* pe, int64_t* se) 
 
 int dpb_block_create(const dpb_block_desc* desc, int device, void* stream, dpb_block** out) {
   Block* b = nullptr;
+  dpb::DeviceGuard dg(device);
   const int rc = dpb::create(desc, device, stream, &b);
   if (rc) return rc;
   *out = reinterpret_cast<dpb_block*>(b);
@@ -110,6 +112,8 @@ int dpb_block_create(const dpb_block_desc* desc, int device, void* stream, dpb_b
 }
 
 int dpb_block_destroy(dpb_block* blk) {
+  if (!blk) return DPB_OK;
+  dpb::DeviceGuard dg(B(blk)->device);
   dpb::destroy(B(blk));
   return DPB_OK;
 }
@@ -131,41 +135,54 @@ int dpb_block_forward(dpb_block* blk, const float* x_in, const float* params, fl
                       int update_running) {
   if (!blk || !x_in || !params) return fail(DPB_CONFIG_ERROR, "null argument");
   if (update_running && !running) return fail(DPB_CONFIG_ERROR, "running stats required");
+  dpb::DeviceGuard dg(B(blk)->device);
   return dpb::block_forward(B(blk), x_in, params, running, update_running, 0);
 }
 
 int dpb_block_forward_eval(dpb_block* blk, const float* x_in, const float* params,
                            const float* running) {
   if (!blk || !x_in || !params || !running) return fail(DPB_CONFIG_ERROR, "null argument");
+  dpb::DeviceGuard dg(B(blk)->device);
   return dpb::block_forward(B(blk), x_in, params, const_cast<float*>(running), 0, 1);
 }
 
 int dpb_block_backward(dpb_block* blk, const float* params, float* grad_acc, float* grads) {
   if (!blk || !params || !grad_acc || !grads) return fail(DPB_CONFIG_ERROR, "null argument");
+  dpb::DeviceGuard dg(B(blk)->device);
   return dpb::block_backward(B(blk), params, grad_acc, grads);
 }
 
 int dpb_block_read_feats(dpb_block* blk, float* dst) {
   if (!blk || !dst) return fail(DPB_CONFIG_ERROR, "null argument");
+  dpb::DeviceGuard dg(B(blk)->device);
   return dpb::read_feats(B(blk), dst);
 }
 int dpb_block_read_z(dpb_block* blk, float* dst) {
   if (!blk || !dst) return fail(DPB_CONFIG_ERROR, "null argument");
+  dpb::DeviceGuard dg(B(blk)->device);
   return dpb::read_z(B(blk), dst);
 }
 int dpb_block_read_stats(dpb_block* blk, float* dst) {
   if (!blk || !dst) return fail(DPB_CONFIG_ERROR, "null argument");
+  dpb::DeviceGuard dg(B(blk)->device);
   return dpb::read_stats(B(blk), dst);
 }
 
 int dpb_sync(dpb_block* blk) {
   if (!blk) return fail(DPB_CONFIG_ERROR, "null block");
+  dpb::DeviceGuard dg(B(blk)->device);
   const cudaError_t e = cudaStreamSynchronize(B(blk)->stream);
   if (e != cudaSuccess) return dpb::cuda_fail(e, "stream synchronize");
   return DPB_OK;
 }
 
 int64_t dpb_block_launch_count(dpb_block* blk) { return blk ? B(blk)->launches : -1; }
+
+int dpb_block_memory_stats(dpb_block* blk, dpb_memory_stats* out) {
+  if (!blk || !out) return fail(DPB_CONFIG_ERROR, "null argument");
+  B(blk)->tracker->snapshot(out);
+  return DPB_OK;
+}
 
 int dpb_block_profile(dpb_block* blk, int enable) {
   if (!blk) return fail(DPB_CONFIG_ERROR, "null block");
@@ -175,6 +192,7 @@ int dpb_block_profile(dpb_block* blk, int enable) {
 
 int dpb_block_profile_read(dpb_block* blk, dpb_kernel_stat* out, int max, int* count) {
   if (!blk || !out || !count) return fail(DPB_CONFIG_ERROR, "null argument");
+  dpb::DeviceGuard dg(B(blk)->device);
   return dpb::profile_read(B(blk), out, max, count);
 }
 

@@ -11,6 +11,35 @@
 
 namespace dpb {
 
+// Exact device-byte accounting per arena (MemoryTracker, alloctrace.hpp:57-105):
+// live / peak per ArenaTag and the combined feature peak (every arena but
+// Params).  Every cudaMalloc of libdpb is recorded, split by the regions it
+// holds; one tracker per model (its blocks record into it) or per block.
+struct DeviceTracker {
+  int64_t live[6] = {}, peak[6] = {};
+  int64_t feature_live = 0, feature_peak = 0;
+  void alloc(int tag, int64_t bytes) {
+    live[tag] += bytes;
+    if (live[tag] > peak[tag]) peak[tag] = live[tag];
+    if (tag != DPB_ARENA_PARAMS) {
+      feature_live += bytes;
+      if (feature_live > feature_peak) feature_peak = feature_live;
+    }
+  }
+  void free(int tag, int64_t bytes) {
+    live[tag] -= bytes;
+    if (tag != DPB_ARENA_PARAMS) feature_live -= bytes;
+  }
+  void snapshot(dpb_memory_stats* out) const {
+    for (int i = 0; i < 6; ++i) {
+      out->live_bytes[i] = live[i];
+      out->peak_bytes[i] = peak[i];
+    }
+    out->total_feature_peak_bytes = feature_peak;
+    out->param_bytes = live[DPB_ARENA_PARAMS];
+  }
+};
+
 struct Geometry {
   int64_t M = 0;     // pixels N*H*W
   int64_t C = 0;     // block output channels c0 + m*k
@@ -33,6 +62,7 @@ struct ProfRec {
   int cat;
   cudaEvent_t start, stop;
   double bytes, flops;
+  double bytes_8d;  // SURVEY 8(d) model bytes (bf16 activations, fp32 gradients)
 };
 
 // Tile choices of the 3x3 halo kernels (dpb_tc_block.cu tc_halo_plan).
@@ -50,6 +80,8 @@ struct Block {
   int device = 0;
   cudaStream_t stream = nullptr;
   void* arena = nullptr;
+  DeviceTracker own_tracker;
+  DeviceTracker* tracker = &own_tracker;  // the owning model's tracker when part of one
   void* feat = nullptr;      // [M, C] S
   void* z = nullptr;         // m x [M, bk] S
   float* fstat = nullptr;    // mean[C] | var[C]
@@ -88,7 +120,9 @@ struct LaunchScope {
   Block* b;
   int idx = -1;
   int cat = 0;
-  LaunchScope(Block* blk, int cat, double bytes, double flops);
+  // bytes: algorithmic HBM bytes with this build's storage (fp32 features);
+  // bytes_8d: the same traffic under SURVEY 8(d)'s model (2-byte activations)
+  LaunchScope(Block* blk, int cat, double bytes, double flops, double bytes_8d);
   ~LaunchScope();
 };
 
@@ -98,7 +132,8 @@ int cuda_fail(cudaError_t e, const char* what);
 int validate(const dpb_block_desc* d);
 Geometry geometry(const dpb_block_desc& d);
 void plan_arena(const dpb_block_desc& d, dpb_arena_sizes* s);
-int create(const dpb_block_desc* desc, int device, void* stream, Block** out);
+int create(const dpb_block_desc* desc, int device, void* stream, Block** out,
+           DeviceTracker* tracker = nullptr);
 void destroy(Block* b);
 int block_forward(Block* b, const float* x_in, const float* params, float* running,
                   int update_running, int eval);
@@ -111,6 +146,11 @@ void profile_enable(Block* b, int on);
 void launch_finalize_bn_bwd(cudaStream_t st, const double2* part, int P, int nch, double count,
                             float* dgamma, float* dbeta, float* coef);
 void launch_fold_splits(cudaStream_t st, const float* wpart, int splits, int64_t n, float* out);
+// fp64 per-128-row partial sums of an NHWC fp32 buffer and their fold into
+// mean / biased variance (the block's statistics kernels, dpb_kernels.cuh)
+void launch_channel_partials(cudaStream_t st, const float* src, int pitch, int64_t M, int nch, double2* part);
+void launch_finalize_stats(cudaStream_t st, const double2* part, int P, int nch, double count, float* mean,
+                           float* var);
 int profile_read(Block* b, dpb_kernel_stat* out, int max, int* count);
 
 // tensor-core path (dpb_tc_block.cu)

@@ -66,8 +66,10 @@ __global__ void k_nhwc_copy(const float* __restrict__ src, int sp, int64_t M, in
 }
 
 // --- per-channel partial sums over rows of an NHWC buffer -------------------
-// grid.x = ceil(M / 128) CTAs (the same partial count as the GEMM epilogues);
-// 256 threads = 8 row groups x 32 channel lanes.  Writes part[cta][ch] =
+// grid.x = ceil(M / 128) CTAs (the same partial count as the GEMM epilogues),
+// grid.y = groups of 32 channels (wide block inputs at small M: block 4 of
+// DenseNet-264 has 25 row CTAs and 1,152-1,728 channels); 256 threads = 8 row
+// groups x 32 channel lanes.  Writes part[cta][ch] =
 // {sum x, sum x^2} in fp64.
 template <typename S>
 __global__ void __launch_bounds__(256)
@@ -77,7 +79,7 @@ k_channel_partials(const S* __restrict__ src, int pitch, int c_off, int64_t M,
   __shared__ double r1[8][33], r2[8][33];
   const int lane = threadIdx.x % 32, grp = threadIdx.x / 32;
   const int64_t m0 = static_cast<int64_t>(blockIdx.x) * 128;
-  for (int cb = 0; cb < nch; cb += 32) {
+  for (int cb = blockIdx.y * 32; cb < nch; cb += 32 * gridDim.y) {  // grid.y: channel groups
     const int ch = cb + lane;
     double s1 = 0.0, s2 = 0.0;
     if (ch < nch) {

@@ -6,7 +6,10 @@
 
 #include <cuda_runtime.h>
 
+#include <cstdint>
 #include <cstdlib>
+#include <mutex>
+#include <unordered_set>
 #include <utility>
 
 namespace dpb {
@@ -23,15 +26,56 @@ inline int skip_mask() {
   return m;
 }
 
+// Kernels launched by this thread through launch() (the model's step count).
+inline int64_t& launch_counter() {
+  static thread_local int64_t n = 0;
+  return n;
+}
+
 inline bool pdl_enabled() {
   static const bool on = std::getenv("DPB_NO_PDL") == nullptr;
   return on;
 }
 
+// Dynamic shared memory above 48 KB needs a per-kernel, per-DEVICE opt-in
+// (cudaFuncAttributeMaxDynamicSharedMemorySize).  Applied on first use of a
+// kernel on the current device, so handles on several GPUs of one process
+// each get it (the attribute does not carry across devices).
+inline void ensure_smem_optin(const void* kernel, size_t smem) {
+  if (smem <= 48 * 1024) return;
+  static std::mutex mu;
+  static std::unordered_set<uint64_t> done;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const uint64_t key = reinterpret_cast<uintptr_t>(kernel) * 64 + static_cast<uint64_t>(dev & 63);
+  std::lock_guard<std::mutex> lk(mu);
+  if (done.count(key)) return;
+  cudaFuncAttributes fa{};
+  cudaFuncGetAttributes(&fa, kernel);
+  cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       227 * 1024 - static_cast<int>(fa.sharedSizeBytes));
+  done.insert(key);
+}
+
+// Makes `device` current for the scope of a C-ABI call and restores the
+// caller's device on exit (one handle per GPU; the caller may be on another).
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int device) {
+    if (cudaGetDevice(&prev) == cudaSuccess && prev != device) cudaSetDevice(device);
+    else prev = -1;
+  }
+  ~DeviceGuard() {
+    if (prev >= 0) cudaSetDevice(prev);
+  }
+};
+
 template <typename... KArgs, typename... Args>
 inline void launch(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t stream,
                    Args&&... args) {
   if (current_cat() >= 0 && (skip_mask() >> current_cat() & 1)) return;
+  ensure_smem_optin(reinterpret_cast<const void*>(kernel), smem);
+  ++launch_counter();
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = grid;
   cfg.blockDim = block;

@@ -20,6 +20,7 @@
 #include <cmath>
 #include <cstdint>
 #include <cstring>
+#include <random>
 #include <vector>
 
 #include "dpb_common.cuh"
@@ -111,6 +112,259 @@ __global__ void k_stem_wgrad(const float* __restrict__ in, int64_t N, int cin, i
     for (int r = 0; r < np; ++r) acc += gs[r * c0 + o] * xs[r * nt + t];
     wpart[static_cast<int64_t>(blockIdx.x) * nw + wi] = acc;
   }
+}
+
+// ---- ImageNet stem (stem == 1; an extension: the reference has only the 3x3 stem) ----
+// conv 7x7 stride 2 pad 3 -> BN (batch statistics) -> ReLU -> max-pool 3x3
+// stride 2 pad 1, the DenseNet ImageNet stem.  224x224 -> 112x112 -> 56x56, so
+// the dense blocks run at 56/28/14/7.  The conv / BN / ReLU
+// semantics are the reference's ops (ops.hpp:315-387, :138-243, :248-287) with
+// stride 2; the max-pool is restated in oracle/ref_driver.cpp (first maximum
+// in (ky, kx) order wins, padding never does).
+constexpr int kS7 = 7, kS7Taps = 49;
+__host__ __device__ inline int stem7_out(int in) { return (in + 2 * 3 - kS7) / 2 + 1; }  // conv_out_dim
+__host__ __device__ inline int pool3_out(int in) { return (in + 2 * 1 - 3) / 2 + 1; }
+
+// y[p][o] (NHWC, pitch c0) = sum_{ci,ky,kx} x[n][ci][2oy-3+ky][2ox-3+kx] w[o][ci][ky][kx],
+// the reference's summation order (ops.hpp:321-341).  Thread = output pixel x
+// 32-channel group (blockIdx.y); weights transposed in shared memory [tap][c0p]
+// so a warp's 16-byte weight reads are broadcasts.
+__global__ void __launch_bounds__(128) k_stem7_conv(const float* __restrict__ in, int64_t N, int cin, int H,
+                                                    int W, int Ho, int Wo, const float* __restrict__ w, int c0,
+                                                    float* __restrict__ y) {
+  pdl_enter();
+  extern __shared__ __align__(16) float wsm[];  // [cin*49][c0p]
+  const int c0p = (c0 + 31) / 32 * 32, nt = cin * kS7Taps;
+  for (int i = threadIdx.x; i < nt * c0p; i += blockDim.x) {
+    const int t = i / c0p, o = i - t * c0p;
+    wsm[i] = o < c0 ? w[static_cast<int64_t>(o) * nt + t] : 0.f;
+  }
+  __syncthreads();
+  const int64_t p = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (p >= N * Ho * Wo) return;
+  const int grp = blockIdx.y;
+  const int hw = Ho * Wo;
+  const int n = static_cast<int>(p / hw);
+  const int r = static_cast<int>(p - static_cast<int64_t>(n) * hw);
+  const int oy = r / Wo, ox = r - (r / Wo) * Wo;
+  float acc[32];
+#pragma unroll
+  for (int j = 0; j < 32; ++j) acc[j] = 0.f;
+  for (int ci = 0; ci < cin; ++ci) {
+    const float* xc = in + (static_cast<int64_t>(n) * cin + ci) * H * W;
+    for (int ky = 0; ky < kS7; ++ky) {
+      const int iy = 2 * oy - 3 + ky;
+      if (iy < 0 || iy >= H) continue;
+      for (int kx = 0; kx < kS7; ++kx) {
+        const int ix = 2 * ox - 3 + kx;
+        if (ix < 0 || ix >= W) continue;
+        const float xv = __ldg(xc + static_cast<int64_t>(iy) * W + ix);
+        const float4* wr = reinterpret_cast<const float4*>(wsm + (ci * kS7Taps + ky * kS7 + kx) * c0p + grp * 32);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const float4 w4 = wr[j];
+          acc[4 * j] += xv * w4.x;
+          acc[4 * j + 1] += xv * w4.y;
+          acc[4 * j + 2] += xv * w4.z;
+          acc[4 * j + 3] += xv * w4.w;
+        }
+      }
+    }
+  }
+  float* yr = y + p * c0 + grp * 32;
+  const int nv = c0 - grp * 32 < 32 ? c0 - grp * 32 : 32;
+  if (nv == 32 && (c0 & 3) == 0) {
+#pragma unroll
+    for (int j = 0; j < 8; ++j)
+      reinterpret_cast<float4*>(yr)[j] = make_float4(acc[4 * j], acc[4 * j + 1], acc[4 * j + 2], acc[4 * j + 3]);
+  } else {
+#pragma unroll
+    for (int j = 0; j < 32; ++j)
+      if (j < nv) yr[j] = acc[j];
+  }
+}
+
+// x0[q][c] = max over the 3x3/2 window (pad 1) of relu(bn(y)); arg[q][c] = the
+// window tap (ky*3+kx) of the first maximum.  Thread = (q, c), c fastest.
+__global__ void k_stem_pool(const float* __restrict__ y, int64_t N, int H1, int W1, int H0, int W0, int c0,
+                            const float* __restrict__ mean, const float* __restrict__ var,
+                            const float* __restrict__ gamma, const float* __restrict__ beta, float* __restrict__ x0,
+                            int ld0, uint8_t* __restrict__ arg) {
+  pdl_enter();
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= N * H0 * W0 * c0) return;
+  const int64_t q = i / c0;
+  const int c = static_cast<int>(i - q * c0);
+  const int hw0 = H0 * W0;
+  const int n = static_cast<int>(q / hw0);
+  const int r = static_cast<int>(q - static_cast<int64_t>(n) * hw0);
+  const int oy = r / W0, ox = r - (r / W0) * W0;
+  const float mu = mean[c], inv = bn_inv(var[c]), ga = gamma[c], be = beta[c];
+  float best = 0.f;
+  int bt = -1;
+  for (int ky = 0; ky < 3; ++ky) {
+    const int iy = 2 * oy - 1 + ky;
+    if (iy < 0 || iy >= H1) continue;
+    for (int kx = 0; kx < 3; ++kx) {
+      const int ix = 2 * ox - 1 + kx;
+      if (ix < 0 || ix >= W1) continue;
+      const float v = fmaxf(bn_ref(y[((static_cast<int64_t>(n) * H1 + iy) * W1 + ix) * c0 + c], mu, inv, ga, be), 0.f);
+      if (bt < 0 || v > best) {
+        best = v;
+        bt = ky * 3 + kx;
+      }
+    }
+  }
+  x0[q * ld0 + c] = best;
+  arg[q * c0 + c] = static_cast<uint8_t>(bt);
+}
+
+// Gradient w.r.t. relu(bn(y)) at conv-output pixel p, channel c: the pooled
+// gradients g0[q][c] of every window q containing p whose first maximum is p,
+// summed in window order (the order the reference-side scatter adds them).
+__device__ __forceinline__ float stem_pool_grad(int64_t p, int c, int H1, int W1, int H0, int W0, int c0,
+                                                const float* __restrict__ g0, int ld0,
+                                                const uint8_t* __restrict__ arg) {
+  const int hw1 = H1 * W1;
+  const int n = static_cast<int>(p / hw1);
+  const int r = static_cast<int>(p - static_cast<int64_t>(n) * hw1);
+  const int iy = r / W1, ix = r - (r / W1) * W1;
+  // windows q = (oy, ox) with 2*oy-1 <= iy <= 2*oy+1 (and the same in x)
+  const int oy1 = min((iy + 1) / 2, H0 - 1), ox1 = min((ix + 1) / 2, W0 - 1);
+  float g = 0.f;
+  for (int oy = iy / 2; oy <= oy1; ++oy)
+    for (int ox = ix / 2; ox <= ox1; ++ox) {
+      const int t = (iy - 2 * oy + 1) * 3 + (ix - 2 * ox + 1);
+      const int64_t q = (static_cast<int64_t>(n) * H0 + oy) * W0 + ox;
+      if (arg[q * c0 + c] == t) g += g0[q * ld0 + c];
+    }
+  return g;
+}
+
+// BN backward partial sums of the stem: g = relu'(bn(y)) * stem_pool_grad,
+// sums (sum g, sum g*xhat) over pixel chunk blockIdx.x in fixed order; thread =
+// channel (blockIdx.y * blockDim.x + threadIdx.x), coalesced along c.
+__global__ void k_stem_bnb_partials(const float* __restrict__ y, int64_t M1, int H1, int W1, int H0, int W0, int c0,
+                                    const float* __restrict__ mean, const float* __restrict__ var,
+                                    const float* __restrict__ gamma, const float* __restrict__ beta,
+                                    const float* __restrict__ g0, int ld0, const uint8_t* __restrict__ arg,
+                                    int64_t chunk, double2* __restrict__ part) {
+  pdl_enter();
+  const int c = blockIdx.y * blockDim.x + threadIdx.x;
+  if (c >= c0) return;
+  const float mu = mean[c], inv = bn_inv(var[c]), ga = gamma[c], be = beta[c];
+  const int64_t p0 = static_cast<int64_t>(blockIdx.x) * chunk;
+  const int64_t p1 = p0 + chunk < M1 ? p0 + chunk : M1;
+  double s1 = 0.0, s2 = 0.0;
+  for (int64_t p = p0; p < p1; ++p) {
+    const float x = y[p * c0 + c];
+    if (!(bn_ref(x, mu, inv, ga, be) > 0.f)) continue;  // relu_backward (ops.hpp:268-287)
+    const float g = stem_pool_grad(p, c, H1, W1, H0, W0, c0, g0, ld0, arg);
+    s1 += g;
+    s2 += g * ((x - mu) * inv);
+  }
+  part[static_cast<int64_t>(blockIdx.x) * c0 + c] = make_double2(s1, s2);
+}
+
+// g_y = gamma*inv*(g - mg - xhat*mgx) (ops.hpp:232-241), written over y in
+// place (y is dead after this pass: the wgrad needs only g_y and the input).
+__global__ void k_stem_bnb_apply(float* __restrict__ y, int64_t M1, int H1, int W1, int H0, int W0, int c0,
+                                 const float* __restrict__ mean, const float* __restrict__ var,
+                                 const float* __restrict__ gamma, const float* __restrict__ beta,
+                                 const float* __restrict__ g0, int ld0, const uint8_t* __restrict__ arg,
+                                 const float* __restrict__ coef) {
+  pdl_enter();
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= M1 * c0) return;
+  const int64_t p = i / c0;
+  const int c = static_cast<int>(i - p * c0);
+  const float mu = mean[c], inv = bn_inv(var[c]), ga = gamma[c], be = beta[c];
+  const float x = y[i];
+  const float g = bn_ref(x, mu, inv, ga, be) > 0.f ? stem_pool_grad(p, c, H1, W1, H0, W0, c0, g0, ld0, arg) : 0.f;
+  y[i] = ga * inv * (g - coef[2 * c] - ((x - mu) * inv) * coef[2 * c + 1]);
+}
+
+// dW partials of the 7x7/2 stem: CTA s sums pixels [s*chunk, ...) in steps of
+// kS7Sub staged pixels (g_y rows and the im2col patches in shared memory);
+// thread = a 4-channel x 12-tap register tile of dW[o][t] (t = ci*49 + ky*7 + kx).
+constexpr int kS7Sub = 32, kS7TT = 12;
+__host__ __device__ inline int stem7_tiles(int c0, int cin) {
+  return ((c0 + 3) / 4) * ((cin * kS7Taps + kS7TT - 1) / kS7TT);
+}
+__global__ void k_stem7_wgrad(const float* __restrict__ in, int64_t N, int cin, int H, int W, int Ho, int Wo,
+                              const float* __restrict__ gy, int c0, int64_t chunk, float* __restrict__ wpart) {
+  pdl_enter();
+  extern __shared__ __align__(16) float sm7[];
+  const int nt = cin * kS7Taps;
+  const int c0p = (c0 + 3) / 4 * 4, ntp = (nt + kS7TT - 1) / kS7TT * kS7TT;
+  float* gs = sm7;                  // [kS7Sub][c0p]
+  float* xs = sm7 + kS7Sub * c0p;   // [kS7Sub][ntp]
+  const int ntt = ntp / kS7TT;
+  const int tile = threadIdx.x;
+  const bool active = tile < stem7_tiles(c0, cin);
+  const int og = active ? tile / ntt : 0, tg = active ? tile - og * ntt : 0;
+  float acc[4][kS7TT];
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int b = 0; b < kS7TT; ++b) acc[a][b] = 0.f;
+  const int64_t M1 = N * Ho * Wo;
+  const int64_t p0 = static_cast<int64_t>(blockIdx.x) * chunk;
+  const int64_t p1 = p0 + chunk < M1 ? p0 + chunk : M1;
+  const int hw = Ho * Wo;
+  for (int64_t pb = p0; pb < p1; pb += kS7Sub) {
+    const int np = p1 - pb < kS7Sub ? static_cast<int>(p1 - pb) : kS7Sub;
+    __syncthreads();
+    for (int e = threadIdx.x; e < kS7Sub * c0p; e += blockDim.x) {
+      const int rr = e / c0p, o = e - rr * c0p;
+      gs[e] = (rr < np && o < c0) ? gy[(pb + rr) * c0 + o] : 0.f;
+    }
+    for (int e = threadIdx.x; e < kS7Sub * ntp; e += blockDim.x) {
+      const int rr = e / ntp, t = e - rr * ntp;
+      float v = 0.f;
+      if (rr < np && t < nt) {
+        const int64_t p = pb + rr;
+        const int n = static_cast<int>(p / hw);
+        const int rem = static_cast<int>(p - static_cast<int64_t>(n) * hw);
+        const int oy = rem / Wo, ox = rem - (rem / Wo) * Wo;
+        const int ci = t / kS7Taps, tap = t - ci * kS7Taps;
+        const int iy = 2 * oy - 3 + tap / kS7, ix = 2 * ox - 3 + tap % kS7;
+        if (iy >= 0 && iy < H && ix >= 0 && ix < W)
+          v = __ldg(in + ((static_cast<int64_t>(n) * cin + ci) * H + iy) * W + ix);
+      }
+      xs[e] = v;
+    }
+    __syncthreads();
+    if (active) {
+      for (int rr = 0; rr < np; ++rr) {
+        const float4 g4 = *reinterpret_cast<const float4*>(gs + rr * c0p + og * 4);
+        const float gv[4] = {g4.x, g4.y, g4.z, g4.w};
+        const float4* xr = reinterpret_cast<const float4*>(xs + rr * ntp + tg * kS7TT);
+        float xv[kS7TT];
+#pragma unroll
+        for (int j = 0; j < kS7TT / 4; ++j) {
+          const float4 x4 = xr[j];
+          xv[4 * j] = x4.x;
+          xv[4 * j + 1] = x4.y;
+          xv[4 * j + 2] = x4.z;
+          xv[4 * j + 3] = x4.w;
+        }
+#pragma unroll
+        for (int a = 0; a < 4; ++a)
+#pragma unroll
+          for (int b = 0; b < kS7TT; ++b) acc[a][b] += gv[a] * xv[b];
+      }
+    }
+  }
+  if (!active) return;
+  float* out = wpart + static_cast<int64_t>(blockIdx.x) * c0 * nt;
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int b = 0; b < kS7TT; ++b) {
+      const int o = og * 4 + a, t = tg * kS7TT + b;
+      if (o < c0 && t < nt) out[static_cast<int64_t>(o) * nt + t] = acc[a][b];
+    }
 }
 
 // ---- transition forward: P = avgpool2x2(relu(bn(feat))) --------------------------------
@@ -362,7 +616,14 @@ __global__ void k_head_loss(const float* __restrict__ gap, int64_t N, int C, con
   const float log_sum = logf(red[0]) + mx;
   const int label = labels[n];
   if (label < 0 || label >= classes) {
-    if (threadIdx.x == 0) *bad_label = 1;
+    // LabelError (ops.hpp softmax_xent): flagged for dpb_model_sync, and the
+    // sample's loss and logit gradients are NaN so a step that ignores the
+    // flag cannot silently train on stale values
+    for (int o = threadIdx.x; o < classes; o += blockDim.x) g_logits[n * classes + o] = __int_as_float(0x7fc00000);
+    if (threadIdx.x == 0) {
+      *bad_label = 1;
+      loss_n[n] = __int_as_float(0x7fc00000);
+    }
     return;
   }
   for (int o = threadIdx.x; o < classes; o += blockDim.x) {
@@ -604,15 +865,29 @@ struct dpb_model {
   float* coef = nullptr;
   int* bad_label = nullptr;
   int64_t wpart_elems = 0, part_rows = 0;
+  // ImageNet stem (d.stem == 1): conv output y1 [M1, c0], max-pool taps,
+  // BN partials / statistics, parameter offsets
+  int H1 = 0, W1 = 0;
+  int64_t M1 = 0, P1 = 0;
+  int64_t stem_w = 0, stem_gamma = 0, stem_beta = 0;
+  float* y1 = nullptr;
+  uint8_t* arg = nullptr;
+  double2* spart = nullptr;
+  float* sstat = nullptr;  // mean[c0] | var[c0]
   // CUDA graph of the whole step, replayed while the step's buffers stay the same
   cudaGraphExec_t graph = nullptr;
   const void* graph_key[6] = {};
+  int64_t graph_kernels = 0;      // kernel nodes of the captured step
+  int64_t eager_launches = 0;     // launches of the last eager step
+  dpb::DeviceTracker tracker;     // every device allocation of the model
+  int64_t mem_tags[6] = {};       // bytes of m->mem per arena tag
 };
 
 namespace dpb {
 namespace {
 
 constexpr int kSplitsMax = 148;      // split-K of the transition dW GEMM
+constexpr int kStem7Splits = 296;    // pixel splits of the 7x7 stem dW
 constexpr int kRowSplitsMax = 2048;  // pixel chunks of the BN-backward sums and the stem dW
 
 int model_geometry(const dpb_model_desc* d, dpb_model* m) {
@@ -620,12 +895,29 @@ int model_geometry(const dpb_model_desc* d, dpb_model* m) {
   if (d->nblocks < 1 || d->nblocks > 8) return fail(DPB_CONFIG_ERROR, "nblocks must be in [1, 8]");
   if (d->k < 1 || d->c0 < 1 || d->classes < 1 || d->in_c < 1 || d->batch < 1)
     return fail(DPB_SHAPE_ERROR, "invalid network geometry");
-  if (d->in_c > 4) return fail(DPB_CONFIG_ERROR, "the 3x3 stem supports at most 4 input channels");
+  if (d->in_c > 4) return fail(DPB_CONFIG_ERROR, "the stem supports at most 4 input channels");
+  if (d->stem != 0 && d->stem != 1) return fail(DPB_CONFIG_ERROR, "stem must be 0 (3x3) or 1 (ImageNet 7x7/2)");
   if (!(d->compression > 0.0) || d->compression > 1.0)
     return fail(DPB_CONFIG_ERROR, "compression must be in (0, 1]");
   if (d->dtype != DPB_FP32 && d->dtype != DPB_BF16) return fail(DPB_CONFIG_ERROR, "dtype");
   int h = d->in_h, w = d->in_w, c = d->c0;
   int64_t po = static_cast<int64_t>(d->c0) * d->in_c * 9, ro = 0;
+  m->stem_w = 0;
+  if (d->stem == 1) {
+    // stem.conv.w [c0][in_c][7][7], stem.bn.gamma [c0], stem.bn.beta [c0];
+    // running statistics of the stem BN first
+    m->H1 = stem7_out(d->in_h);
+    m->W1 = stem7_out(d->in_w);
+    if (m->H1 < 1 || m->W1 < 1) return fail(DPB_SHAPE_ERROR, "stem conv output collapses to zero size");
+    h = pool3_out(m->H1);
+    w = pool3_out(m->W1);
+    m->M1 = d->batch * m->H1 * m->W1;
+    m->P1 = (m->M1 + 127) / 128;
+    m->stem_gamma = static_cast<int64_t>(d->c0) * d->in_c * kS7Taps;
+    m->stem_beta = m->stem_gamma + d->c0;
+    po = m->stem_beta + d->c0;
+    ro = 2 * d->c0;
+  }
   const int bk = 4 * d->k;
   m->blocks.clear();
   m->trans.clear();
@@ -700,14 +992,97 @@ DPB_API int dpb_model_sizes(const dpb_model_desc* desc, int64_t* param_elems, in
   return DPB_OK;
 }
 
+// GraphPlan<T>::build's parameter init, replayed draw for draw (graph.hpp:
+// 351-390 make_bn / make_conv, :405-600 registration order, rng.hpp:14-50):
+// one Rng(seed) stream; conv weights float(normal() * sqrt(2 / fan_in)) in
+// (oc, ic, ky, kx) order, BN gamma 1 / beta 0, classifier float(sqrt(1 / C) *
+// normal()), bias 0.  The ImageNet stem (stem 1, not in the reference) draws
+// its 7x7 weights in the same position the reference draws its 3x3 stem.
+namespace {
+struct HostRng {  // Rng (rng.hpp): mt19937_64, 53-bit uniform, Box-Muller with a spare
+  std::mt19937_64 eng;
+  bool have = false;
+  double spare = 0.0;
+  explicit HostRng(uint64_t seed) : eng(seed) {}
+  double uniform() { return static_cast<double>(eng() >> 11) * 0x1.0p-53; }
+  double normal() {
+    if (have) {
+      have = false;
+      return spare;
+    }
+    double u1 = uniform();
+    const double u2 = uniform();
+    while (u1 <= 0.0) u1 = uniform();
+    const double r = std::sqrt(-2.0 * std::log(u1));
+    const double th = 2.0 * 3.14159265358979323846 * u2;
+    spare = r * std::sin(th);
+    have = true;
+    return r * std::cos(th);
+  }
+};
+}  // namespace
+
+DPB_API int dpb_model_init_params(const dpb_model_desc* desc, uint64_t seed, float* host_params) {
+  if (host_params == nullptr) return fail(DPB_CONFIG_ERROR, "null parameter buffer");
+  dpb_model m;
+  const int rc = model_geometry(desc, &m);
+  if (rc) return rc;
+  HostRng rng(seed);
+  float* p = host_params;
+  auto conv = [&](int64_t out_c, int64_t in_c, int kk) {  // make_conv
+    const double stddev = std::sqrt(2.0 / (static_cast<double>(in_c) * kk * kk));
+    const int64_t n = out_c * in_c * kk * kk;
+    for (int64_t i = 0; i < n; ++i) *p++ = static_cast<float>(rng.normal() * stddev);
+  };
+  auto bn = [&](int64_t c) {  // make_bn: gamma 1, beta 0
+    for (int64_t i = 0; i < c; ++i) *p++ = 1.f;
+    for (int64_t i = 0; i < c; ++i) *p++ = 0.f;
+  };
+  const int bk = 4 * desc->k;
+  if (desc->stem == 1) {
+    conv(desc->c0, desc->in_c, kS7);
+    bn(desc->c0);
+  } else {
+    conv(desc->c0, desc->in_c, 3);
+  }
+  for (size_t b = 0; b < m.blocks.size(); ++b) {
+    const ModelBlock& mb = m.blocks[b];
+    for (int l = 0; l < mb.m; ++l) {
+      const int64_t c = mb.c0 + static_cast<int64_t>(l) * desc->k;
+      bn(c);
+      conv(bk, c, 1);
+      bn(bk);
+      conv(desc->k, bk, 3);
+    }
+    if (b + 1 < m.blocks.size()) {
+      bn(m.trans[b].C);
+      conv(m.trans[b].cout, m.trans[b].C, 1);
+    } else {
+      const int64_t C = mb.C;
+      bn(C);
+      const double w_std = std::sqrt(1.0 / static_cast<double>(C));
+      for (int64_t i = 0; i < static_cast<int64_t>(desc->classes) * C; ++i)
+        *p++ = static_cast<float>(w_std * rng.normal());
+      for (int64_t i = 0; i < desc->classes; ++i) *p++ = 0.f;
+    }
+  }
+  if (p - host_params != m.params) return fail(DPB_ACCOUNTING_ERROR, "parameter init count mismatch");
+  return DPB_OK;
+}
+
 DPB_API void dpb_model_destroy(dpb_model* m) {
   if (!m) return;
+  DeviceGuard dg(m->device);
   if (m->graph) cudaGraphExecDestroy(m->graph);
   for (cudaEvent_t e : m->ev) cudaEventDestroy(e);
   if (m->side) cudaStreamDestroy(m->side);
   for (auto& b : m->blocks)
     if (b.blk) destroy(b.blk);
-  if (m->mem) cudaFree(m->mem);
+  if (m->mem) {
+    cudaFree(m->mem);
+    for (int t = 0; t < 6; ++t)
+      if (m->mem_tags[t]) m->tracker.free(t, m->mem_tags[t]);
+  }
   delete m;
 }
 
@@ -723,6 +1098,7 @@ DPB_API int dpb_model_create(const dpb_model_desc* desc, int device, void* strea
   m->d = *desc;
   m->device = device;
   m->stream = static_cast<cudaStream_t>(stream);
+  DeviceGuard dg(device);
   cudaError_t e = cudaSetDevice(device);
   if (e != cudaSuccess) {
     delete m;
@@ -731,7 +1107,7 @@ DPB_API int dpb_model_create(const dpb_model_desc* desc, int device, void* strea
   const int bk = 4 * desc->k;
   for (auto& b : m->blocks) {
     dpb_block_desc bd{desc->batch, b.h, b.w, b.c0, b.m, desc->k, bk, desc->dtype, DPB_NHWC};
-    rc = create(&bd, device, stream, &b.blk);
+    rc = create(&bd, device, stream, &b.blk, &m->tracker);
     if (rc) {
       dpb_model_destroy(m);
       return rc;
@@ -740,25 +1116,26 @@ DPB_API int dpb_model_create(const dpb_model_desc* desc, int device, void* strea
   // device buffers: block inputs and accumulators, transition P / gP, head,
   // split-K partials, BN-backward partials and coefficients
   int64_t bytes = 0;
-  auto take = [&](int64_t n) {
+  int64_t tags[6] = {};
+  auto take = [&](int64_t n, int tag = DPB_ARENA_SCRATCH) {  // n floats, accounted under `tag`
     const int64_t o = bytes;
     bytes += (n * 4 + 255) / 256 * 256;
+    tags[tag] += bytes - o;
     return o;
   };
   std::vector<int64_t> off;
   for (auto& b : m->blocks) {
-    off.push_back(take(b.M * b.c0));
-    off.push_back(take(b.M * b.Cp));
+    off.push_back(take(b.M * b.Cp, DPB_ARENA_SHARED_GRAD));  // block-output gradient accumulator
   }
   for (auto& t : m->trans) {
-    off.push_back(take(t.Mq * t.C));
-    off.push_back(take(t.Mq * t.C));
+    off.push_back(take(t.Mq * t.C, DPB_ARENA_FEATURE_OWNED));  // pooled activations (saved for dW)
+    off.push_back(take(t.Mq * t.C, DPB_ARENA_SHARED_GRAD));    // their gradient
     off.push_back(take(static_cast<int64_t>(kSplitsMax) * t.cout * t.C));
   }
   const int Cl = m->blocks.back().C;
   const int64_t N = desc->batch;
-  const int64_t o_gap = take(N * Cl), o_log = take(N * desc->classes), o_glog = take(N * desc->classes),
-                o_ggap = take(N * Cl), o_loss = take(N);
+  const int64_t o_gap = take(N * Cl, DPB_ARENA_FEATURE_OWNED), o_log = take(N * desc->classes, DPB_ARENA_FEATURE_OWNED),
+                o_glog = take(N * desc->classes), o_ggap = take(N * Cl, DPB_ARENA_SHARED_GRAD), o_loss = take(N);
   int64_t wmax = static_cast<int64_t>(desc->c0) * desc->in_c * 9, cmax = Cl;
   for (auto& t : m->trans) {
     wmax = std::max<int64_t>(wmax, static_cast<int64_t>(t.cout) * t.C);
@@ -767,6 +1144,15 @@ DPB_API int dpb_model_create(const dpb_model_desc* desc, int device, void* strea
   const int64_t stem_splits = (m->blocks[0].M + stem_chunk(desc->c0, desc->in_c) - 1) /
                               stem_chunk(desc->c0, desc->in_c);
   m->wpart_elems = std::max<int64_t>(kSplitsMax * wmax, stem_splits * desc->c0 * desc->in_c * 9);
+  if (desc->stem == 1)
+    m->wpart_elems = std::max<int64_t>(m->wpart_elems, kStem7Splits * desc->c0 * desc->in_c * kS7Taps);
+  int64_t o_y1 = 0, o_arg = 0, o_spart = 0, o_sstat = 0;
+  if (desc->stem == 1) {
+    o_y1 = take(m->M1 * desc->c0, DPB_ARENA_FEATURE_OWNED);  // stem conv output (reused for its gradient)
+    o_arg = take((m->blocks[0].M * desc->c0 + 3) / 4, DPB_ARENA_FEATURE_OWNED);  // max-pool taps
+    o_spart = take(4 * m->P1 * desc->c0);
+    o_sstat = take(2 * desc->c0);
+  }
   const int64_t o_wpart = take(m->wpart_elems);
   m->part_rows = kRowSplitsMax;
   const int64_t o_part = take(4 * kRowSplitsMax * cmax);  // double2 = 4 floats
@@ -777,10 +1163,16 @@ DPB_API int dpb_model_create(const dpb_model_desc* desc, int device, void* strea
     dpb_model_destroy(m);
     return cuda_fail(e, "model cudaMalloc");
   }
+  for (int t = 0; t < 6; ++t) {
+    m->mem_tags[t] = tags[t];
+    if (tags[t]) m->tracker.alloc(t, tags[t]);
+  }
   char* base = static_cast<char*>(m->mem);
   size_t k = 0;
   for (auto& b : m->blocks) {
-    b.x = reinterpret_cast<float*>(base + off[k++]);
+    // the block input is written straight into channels [0, c0) of the
+    // block's feature arena (row pitch Cp): the block's own pack is skipped
+    b.x = static_cast<float*>(b.blk->feat);
     b.acc = reinterpret_cast<float*>(base + off[k++]);
   }
   for (auto& t : m->trans) {
@@ -797,6 +1189,12 @@ DPB_API int dpb_model_create(const dpb_model_desc* desc, int device, void* strea
   m->part = reinterpret_cast<double2*>(base + o_part);
   m->coef = reinterpret_cast<float*>(base + o_coef);
   m->bad_label = reinterpret_cast<int*>(base + o_bad);
+  if (desc->stem == 1) {
+    m->y1 = reinterpret_cast<float*>(base + o_y1);
+    m->arg = reinterpret_cast<uint8_t*>(base + o_arg);
+    m->spart = reinterpret_cast<double2*>(base + o_spart);
+    m->sstat = reinterpret_cast<float*>(base + o_sstat);
+  }
   if (cudaStreamCreateWithFlags(&m->side, cudaStreamNonBlocking) != cudaSuccess) m->side = nullptr;
   for (size_t i = 0; m->side && i < m->trans.size() + 1; ++i) {
     cudaEvent_t e;
@@ -807,8 +1205,20 @@ DPB_API int dpb_model_create(const dpb_model_desc* desc, int device, void* strea
   return DPB_OK;
 }
 
+DPB_API int dpb_model_memory_stats(dpb_model* m, dpb_memory_stats* out) {
+  if (!m || !out) return fail(DPB_CONFIG_ERROR, "null argument");
+  m->tracker.snapshot(out);
+  return DPB_OK;
+}
+
+DPB_API int64_t dpb_model_launch_count(dpb_model* m) {
+  if (!m) return -1;
+  return m->graph ? m->graph_kernels : m->eager_launches;
+}
+
 DPB_API int dpb_model_sync(dpb_model* m) {
   if (!m) return fail(DPB_CONFIG_ERROR, "null model");
+  DeviceGuard dg(m->device);
   const cudaError_t e = cudaStreamSynchronize(m->stream);
   if (e != cudaSuccess) return cuda_fail(e, "model sync");
   int bad = 0;
@@ -840,8 +1250,23 @@ int model_step_launch(dpb_model* m, const float* input, const int32_t* labels, c
 
   // ---- forward --------------------------------------------------------------------
   ModelBlock& b0 = m->blocks[0];
-  launch(k_stem_fwd, blocks_of(b0.M, 256), 256, sizeof(float) * d.c0 * d.in_c * 9, st, input, N, d.in_c,
-         d.in_h, d.in_w, params, d.c0, b0.x, b0.c0);
+  if (d.stem == 1) {
+    const int c0p = (d.c0 + 31) / 32 * 32;
+    launch(k_stem7_conv, dim3(blocks_of(m->M1, 128), static_cast<unsigned>(c0p / 32)), 128,
+           sizeof(float) * d.in_c * kS7Taps * c0p, st, input, N, d.in_c, d.in_h, d.in_w, m->H1, m->W1, params, d.c0,
+           m->y1);
+    launch_channel_partials(st, m->y1, d.c0, m->M1, d.c0, m->spart);
+    launch_finalize_stats(st, m->spart, static_cast<int>(m->P1), d.c0, static_cast<double>(m->M1), m->sstat,
+                          m->sstat + d.c0);
+    launch(k_running, blocks_of(d.c0, 256), 256, 0, st, d.c0, static_cast<const float*>(m->sstat),
+           static_cast<const float*>(m->sstat + d.c0), running, running + d.c0);
+    launch(k_stem_pool, blocks_of(b0.M * d.c0, 256), 256, 0, st, static_cast<const float*>(m->y1), N, m->H1, m->W1,
+           b0.h, b0.w, d.c0, static_cast<const float*>(m->sstat), static_cast<const float*>(m->sstat + d.c0),
+           params + m->stem_gamma, params + m->stem_beta, b0.x, b0.Cp, m->arg);
+  } else {
+    launch(k_stem_fwd, blocks_of(b0.M, 256), 256, sizeof(float) * d.c0 * d.in_c * 9, st, input, N, d.in_c,
+           d.in_h, d.in_w, params, d.c0, b0.x, b0.Cp);
+  }
   for (int b = 0; b < nb; ++b) {
     ModelBlock& mb = m->blocks[b];
     int rc = block_forward(mb.blk, mb.x, params + mb.poff, running + mb.roff, 1, 0);
@@ -855,11 +1280,11 @@ int model_step_launch(dpb_model* m, const float* input, const int32_t* labels, c
       launch(k_trans_pool, dim3(blocks_of(t.C, 128), static_cast<unsigned>(std::min<int64_t>(t.Mq, 65535))), 128,
              0, st, feat, mb.Cp, N, mb.h, mb.w, t.C, mean, var, params + t.gamma, params + t.beta, t.P);
       if (d.dtype == DPB_BF16)
-        trans_gemm<0>(st, static_cast<int>(t.Mq), t.cout, t.C, t.P, t.C, params + t.w, t.C, nx.x, nx.c0);
+        trans_gemm<0>(st, static_cast<int>(t.Mq), t.cout, t.C, t.P, t.C, params + t.w, t.C, nx.x, nx.Cp);
       else
         launch(k_gemm<false, true>, dim3(blocks_of(t.Mq, 64), blocks_of(t.cout, 64), 1), 256, 0, st,
                static_cast<int>(t.Mq), t.cout, t.C, static_cast<const float*>(t.P), t.C, params + t.w, t.C, nx.x,
-               nx.c0, t.C);
+               nx.Cp, t.C);
       launch(k_running, blocks_of(t.C, 256), 256, 0, st, t.C, mean, var, running + t.run,
              running + t.run + t.C);
     } else {
@@ -949,6 +1374,29 @@ int model_step_launch(dpb_model* m, const float* input, const int32_t* labels, c
                pv.Cp, pv.M, t.C, mean, var,
                params + t.gamma, params + t.beta, up, static_cast<const float*>(m->coef), pv.acc, pv.Cp);
       }
+    } else if (d.stem == 1) {
+      // block-input gradient mb.acc[:, :c0] -> max-pool backward -> ReLU mask
+      // -> stem BN backward -> 7x7/2 conv dW (no data gradient, graph.hpp:1170-1181)
+      const float* mean = m->sstat;
+      const float* var = m->sstat + d.c0;
+      int64_t chunk;
+      const int S = splits_of(m->M1, chunk, kRowSplitsMax, 16);
+      const int ct = d.c0 < 128 ? (d.c0 + 31) / 32 * 32 : 128;
+      launch(k_stem_bnb_partials, dim3(S, blocks_of(d.c0, ct)), ct, 0, st, static_cast<const float*>(m->y1), m->M1,
+             m->H1, m->W1, mb.h, mb.w, d.c0, mean, var, params + m->stem_gamma, params + m->stem_beta,
+             static_cast<const float*>(mb.acc), mb.Cp, static_cast<const uint8_t*>(m->arg), chunk, m->part);
+      launch_finalize_bn_bwd(st, m->part, S, d.c0, static_cast<double>(m->M1), grads + m->stem_gamma,
+                             grads + m->stem_beta, m->coef);
+      launch(k_stem_bnb_apply, blocks_of(m->M1 * d.c0, 256), 256, 0, st, m->y1, m->M1, m->H1, m->W1, mb.h, mb.w,
+             d.c0, mean, var, params + m->stem_gamma, params + m->stem_beta, static_cast<const float*>(mb.acc),
+             mb.Cp, static_cast<const uint8_t*>(m->arg), static_cast<const float*>(m->coef));
+      const int64_t c7 = (m->M1 + kStem7Splits - 1) / kStem7Splits;
+      const int S7 = static_cast<int>((m->M1 + c7 - 1) / c7);
+      const int th = (stem7_tiles(d.c0, d.in_c) + 31) / 32 * 32;
+      const int c0p4 = (d.c0 + 3) / 4 * 4, ntp = (d.in_c * kS7Taps + kS7TT - 1) / kS7TT * kS7TT;
+      launch(k_stem7_wgrad, S7, th, sizeof(float) * kS7Sub * (c0p4 + ntp), st, input, N, d.in_c, d.in_h, d.in_w,
+             m->H1, m->W1, static_cast<const float*>(m->y1), d.c0, c7, m->wpart);
+      launch_fold_splits(st, m->wpart, S7, static_cast<int64_t>(d.c0) * d.in_c * kS7Taps, grads);
     } else {
       const int chunk = stem_chunk(d.c0, d.in_c);
       const int S = static_cast<int>((mb.M + chunk - 1) / chunk);
@@ -980,12 +1428,18 @@ DPB_API int dpb_model_step(dpb_model* m, const float* input, const int32_t* labe
                            float* running, float* grads, float* loss) {
   if (!m || !input || !labels || !params || !running || !grads || !loss)
     return fail(DPB_CONFIG_ERROR, "null pointer argument");
+  DeviceGuard dg(m->device);
   cudaStream_t st = m->stream;
   static const bool no_graph = std::getenv("DPB_MODEL_NO_GRAPH") != nullptr;
   cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
   const bool legacy = st == nullptr || st == cudaStreamLegacy || st == cudaStreamPerThread;
   if (no_graph || legacy || cudaStreamIsCapturing(st, &cs) != cudaSuccess || cs != cudaStreamCaptureStatusNone)
-    return model_step_launch(m, input, labels, params, running, grads, loss);
+  {
+    const int64_t c0 = launch_counter();
+    const int rc = model_step_launch(m, input, labels, params, running, grads, loss);
+    m->eager_launches = launch_counter() - c0;
+    return rc;
+  }
   const void* key[6] = {input, labels, params, running, grads, loss};
   if (m->graph == nullptr || std::memcmp(key, m->graph_key, sizeof(key)) != 0) {
     if (m->graph) {
@@ -1002,6 +1456,19 @@ DPB_API int dpb_model_step(dpb_model* m, const float* input, const int32_t* labe
       return rc;
     }
     if (e != cudaSuccess) return cuda_fail(e, "model step capture");
+    {
+      size_t nn = 0;
+      cudaGraphGetNodes(g, nullptr, &nn);
+      std::vector<cudaGraphNode_t> nodes(nn);
+      cudaGraphGetNodes(g, nodes.data(), &nn);
+      int64_t kern = 0;
+      for (cudaGraphNode_t nd : nodes) {
+        cudaGraphNodeType ty;
+        cudaGraphNodeGetType(nd, &ty);
+        kern += ty == cudaGraphNodeTypeKernel;
+      }
+      m->graph_kernels = kern;
+    }
     e = cudaGraphInstantiate(&m->graph, g, 0);
     cudaGraphDestroy(g);
     if (e != cudaSuccess) {

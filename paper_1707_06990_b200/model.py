@@ -30,6 +30,9 @@ class DenseNetConfig:
     initial_channels: int = -1
     in_shape: tuple = (3, 32, 32)   # (c, h, w) of the network input
     activation: str = "pre"         # "pre" | "post" (densenet.hpp ActivationOrder)
+    # "3x3": the reference's conv 3x3/1 stem (graph.hpp:430); "imagenet": conv
+    # 7x7/2 -> BN -> ReLU -> max-pool 3x3/2 (extension; 224 -> 56)
+    stem: str = "3x3"
 
     @property
     def c0(self) -> int:
@@ -41,12 +44,22 @@ class DenseNetConfig:
                 int(self.bottleneck), float(self.compression), self.num_classes,
                 self.c0], arr
 
-    def block_shapes(self, batch: int, stem_stride: int = 1) -> list[BlockShape]:
-        """Per-block geometry (net_geometry, densenet.hpp:141-180).  The
-        reference stem is 3x3 stride 1 (graph.hpp:430); ``stem_stride`` 4
-        reproduces the ImageNet 7x7/2 + max-pool geometry."""
+    @property
+    def stem_id(self) -> int:
+        return {"3x3": 0, "imagenet": 1}[self.stem]
+
+    def stem_out_hw(self) -> tuple:
+        """Spatial size entering block 0: the reference's 3x3/1 stem keeps it
+        (graph.hpp:430); the ImageNet stem is conv 7x7/2 pad 3 then max-pool
+        3x3/2 pad 1 ((in + 2p - k) / s + 1 twice, ops.hpp:292-294)."""
         _, h, w = self.in_shape
-        h, w = h // stem_stride, w // stem_stride
+        if self.stem == "imagenet":
+            h, w = ((h - 1) // 2 + 1 - 1) // 2 + 1, ((w - 1) // 2 + 1 - 1) // 2 + 1
+        return h, w
+
+    def block_shapes(self, batch: int) -> list[BlockShape]:
+        """Per-block geometry (net_geometry, densenet.hpp:141-180) after the stem."""
+        h, w = self.stem_out_hw()
         c = self.c0
         out = []
         for b, m in enumerate(self.block_sizes):
@@ -83,13 +96,19 @@ def rng_normal(seed: int, count: int) -> np.ndarray:
     return out
 
 
-# BASELINE.json configs
+# BASELINE.json configs.  The ImageNet configs use the
+# 7x7/2 + max-pool stem at 224x224; their "@56" twins are the reference's own
+# geometry for the same networks (3x3/1 stem on a 3x56x56 input: identical
+# dense blocks, transitions and head — what GraphPlan can run).
 CONFIGS = {
     "cfg1": DenseNetConfig((12,), 12, True, 1.0, 10, 24, (3, 32, 32)),
     "bc100": DenseNetConfig((16, 16, 16), 12, True, 0.5, 10, 24, (3, 32, 32)),
-    "d121": DenseNetConfig((6, 12, 24, 16), 32, True, 0.5, 1000, 64, (3, 224, 224)),
-    "d264k32": DenseNetConfig((6, 12, 64, 48), 32, True, 0.5, 1000, 64, (3, 224, 224)),
-    "d264k48": DenseNetConfig((6, 12, 64, 48), 48, True, 0.5, 1000, 96, (3, 224, 224)),
+    "d121": DenseNetConfig((6, 12, 24, 16), 32, True, 0.5, 1000, 64, (3, 224, 224), stem="imagenet"),
+    "d264k32": DenseNetConfig((6, 12, 64, 48), 32, True, 0.5, 1000, 64, (3, 224, 224), stem="imagenet"),
+    "d264k48": DenseNetConfig((6, 12, 64, 48), 48, True, 0.5, 1000, 96, (3, 224, 224), stem="imagenet"),
+    "d121@56": DenseNetConfig((6, 12, 24, 16), 32, True, 0.5, 1000, 64, (3, 56, 56)),
+    "d264k32@56": DenseNetConfig((6, 12, 64, 48), 32, True, 0.5, 1000, 64, (3, 56, 56)),
+    "d264k48@56": DenseNetConfig((6, 12, 64, 48), 48, True, 0.5, 1000, 96, (3, 56, 56)),
 }
 
 
@@ -97,7 +116,11 @@ def param_segments(cfg: DenseNetConfig) -> list[tuple[str, int, int]]:
     """(name, elements, fan_in) of every parameter tensor in registration
     order; fan_in 0 marks BN gamma (1) / beta and the linear bias (0)."""
     k, bk, in_c = cfg.growth_rate, 4 * cfg.growth_rate, cfg.in_shape[0]
-    segs = [("stem.conv.w", cfg.c0 * in_c * 9, in_c * 9)]
+    if cfg.stem == "imagenet":
+        segs = [("stem.conv.w", cfg.c0 * in_c * 49, in_c * 49), ("stem.bn.gamma", cfg.c0, 0),
+                ("stem.bn.beta", cfg.c0, 0)]
+    else:
+        segs = [("stem.conv.w", cfg.c0 * in_c * 9, in_c * 9)]
     shapes = cfg.block_shapes(1)
     for b, shp in enumerate(shapes):
         for l in range(shp.m):
@@ -121,7 +144,8 @@ def param_shapes(cfg: DenseNetConfig) -> list[tuple[str, tuple]]:
     out = []
     for name, n, fan in param_segments(cfg):
         if name == "stem.conv.w":
-            shape = (cfg.c0, in_c, 3, 3)
+            kk = 7 if cfg.stem == "imagenet" else 3
+            shape = (cfg.c0, in_c, kk, kk)
         elif name.endswith(".conv_b.w"):
             shape = (k, bk, 3, 3)
         elif name.endswith(".conv_a.w"):
@@ -172,6 +196,43 @@ def load_checkpoint(cfg: DenseNetConfig, path: str, with_velocity: bool = False)
     return t, None, ep.value
 
 
+def model_desc(cfg: DenseNetConfig, batch: int, dtype: str = "fp32"):
+    """The dpb_model_desc of `cfg` (include/dpb.h)."""
+    from ._lib import ModelDesc
+    d = ModelDesc()
+    d.nblocks = len(cfg.block_sizes)
+    for i, m in enumerate(cfg.block_sizes):
+        d.blocks[i] = m
+    d.k = cfg.growth_rate
+    d.compression = float(cfg.compression)
+    d.classes = cfg.num_classes
+    d.c0 = cfg.c0
+    d.in_c, d.in_h, d.in_w = cfg.in_shape
+    d.batch = batch
+    d.dtype = {"fp32": 0, "bf16": 1}[dtype]
+    d.stem = cfg.stem_id
+    return d
+
+
+def model_sizes(cfg: DenseNetConfig) -> tuple:
+    """(param_elems, running_elems) of the whole network (dpb_model_sizes)."""
+    d = model_desc(cfg, 1)
+    pe, re_ = C.c_int64(), C.c_int64()
+    check(lib().dpb_model_sizes(C.byref(d), C.byref(pe), C.byref(re_)))
+    return pe.value, re_.value
+
+
+def init_params(cfg: DenseNetConfig, seed: int) -> np.ndarray:
+    """GraphPlan::build's parameters for `seed` in registration order, replayed
+    draw for draw on the host by libdpb (dpb_model_init_params; graph.hpp:
+    351-390, :405-600, rng.hpp:36-49): bit-identical to the reference's
+    params() for the 3x3 stem."""
+    d = model_desc(cfg, 1)
+    out = np.empty(model_sizes(cfg)[0], dtype=np.float32)
+    check(lib().dpb_model_init_params(C.byref(d), int(seed), C.c_void_p(out.ctypes.data)))
+    return out
+
+
 class ModelPlan:
     """Whole-network training step on the GPU (``dpb_model_*``): the stem,
     dense blocks, transitions, head and softmax cross-entropy of
@@ -183,20 +244,9 @@ class ModelPlan:
                  stream=None):
         import torch
 
-        from ._lib import ModelDesc
         self.cfg = cfg
         self.batch = batch
-        d = ModelDesc()
-        d.nblocks = len(cfg.block_sizes)
-        for i, m in enumerate(cfg.block_sizes):
-            d.blocks[i] = m
-        d.k = cfg.growth_rate
-        d.compression = float(cfg.compression)
-        d.classes = cfg.num_classes
-        d.c0 = cfg.c0
-        d.in_c, d.in_h, d.in_w = cfg.in_shape
-        d.batch = batch
-        d.dtype = {"fp32": 0, "bf16": 1}[dtype]
+        d = model_desc(cfg, batch, dtype)
         if not cfg.bottleneck or cfg.activation != "pre":
             from .errors import ConfigError
             raise ConfigError("ModelPlan implements pre-activation bottleneck (DenseNet-B/BC) networks only")
@@ -223,27 +273,18 @@ class ModelPlan:
         return load_checkpoint(self.cfg, path, with_velocity)
 
     def init_params(self, seed: int = 0, device="cuda"):
-        """Parameters drawn like GraphPlan::build (graph.hpp:351-390, 582-590):
-        He-normal convs, BN gamma 1 / beta 0, classifier N(0, 1/C), bias 0
-        (the distributions, not the reference's Rng stream)."""
+        """GraphPlan::build's parameters for `seed`, replayed draw for draw by
+        libdpb (dpb_model_init_params; graph.hpp:351-390, :405-600, rng.hpp):
+        bit-identical to the reference's params() for the 3x3 stem."""
         import torch
-        g = torch.Generator(device="cpu").manual_seed(seed)
-        parts = []
-        for name, n, fan in self.param_segments():
-            if fan > 0:
-                parts.append(torch.randn(n, generator=g) * float(np.sqrt(2.0 / fan)))
-            elif fan < 0:
-                parts.append(torch.randn(n, generator=g) * float(np.sqrt(1.0 / -fan)))
-            else:
-                parts.append(torch.ones(n) if name.endswith("gamma") else torch.zeros(n))
-        out = torch.cat(parts)
-        assert out.numel() == self.param_elems
-        return out.to(device)
+        return torch.from_numpy(init_params(self.cfg, seed)).to(device)
 
     def initial_running(self, device="cuda"):
         """Running means 0 / variances 1 in the model's running layout."""
         import torch
         parts = []
+        if self.cfg.stem == "imagenet":  # stem BN
+            parts.append(torch.cat([torch.zeros(self.cfg.c0), torch.ones(self.cfg.c0)]))
         shapes = self.cfg.block_shapes(self.batch)
         for b, shp in enumerate(shapes):
             parts.append(shp.initial_running("cpu"))
@@ -261,6 +302,21 @@ class ModelPlan:
 
     def sync(self) -> None:
         check(lib().dpb_model_sync(self._h))
+
+    def launch_count(self) -> int:
+        """Kernels one training step launches (the captured graph's kernel nodes)."""
+        return int(lib().dpb_model_launch_count(self._h))
+
+    def memory(self) -> dict:
+        """libdpb's device-memory accounting of the whole step (dpb_model_memory_stats,
+        MemoryStats of alloctrace.hpp): bytes per arena, the combined feature
+        (activation) peak and the total allocated."""
+        from ._lib import MemoryStats
+        st = MemoryStats()
+        check(lib().dpb_model_memory_stats(self._h, C.byref(st)))
+        by = {name: int(st.peak_bytes[i]) for i, name in enumerate(ARENAS)}
+        return {"by_arena": by, "activation_bytes": int(st.total_feature_peak_bytes),
+                "total_bytes": sum(by.values())}
 
     def close(self) -> None:
         if getattr(self, "_h", None) is not None and self._h.value:

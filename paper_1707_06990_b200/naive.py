@@ -146,3 +146,78 @@ class NaiveBlock:
 
     def retained_bytes(self) -> int:
         return 4 * sum(self.accounting().values())
+
+
+def naive_network_replay(cfg, batch: int, device="cuda") -> dict:
+    """The whole network under the reference's Naive strategy (graph.hpp:
+    279-310: every forward tensor and every gradient transient held until the
+    step ends), measured with the CUDA caching allocator's high-water mark.
+
+    The dense blocks run for real through `NaiveBlock` (unfused per-op
+    kernels, fp32), one after another, keeping their state, then backward in
+    reverse.  The stem, transition and head tensors the strategy would hold
+    (peak_model.hpp:57-133: conv / BN / pool outputs, their gradient
+    transients) are allocated at their shapes without being computed — they
+    are small next to the blocks.  Parameters and parameter gradients are
+    allocated before the baseline (peak_model counts them under Params).
+    Returns bytes: allocator peak, and the reference peak model's Naive
+    feature arenas for the same network, fp32."""
+    from .model import predict_peak_elements
+    dev = torch.device(device)
+    shapes = cfg.block_shapes(batch)
+    g = torch.Generator(device="cpu").manual_seed(11)
+    params = [(torch.randn(s.param_elems, generator=g) * 0.05 + 0.5).to(dev) for s in shapes]
+    grads = [torch.empty(s.param_elems, device=dev) for s in shapes]
+    torch.cuda.synchronize(dev)
+    base = torch.cuda.memory_allocated(dev)
+    torch.cuda.reset_peak_memory_stats(dev)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    hold = []
+    N, c0 = batch, cfg.c0
+    _, h, w = cfg.in_shape
+    if cfg.stem == "imagenet":
+        h1, w1 = (h - 1) // 2 + 1, (w - 1) // 2 + 1
+        hold += [torch.empty((N, c0, h1, w1), device=dev) for _ in range(2)]   # conv out, BN+ReLU out
+    else:
+        hold.append(torch.empty((N, c0, h, w), device=dev))                   # stem conv out
+    x = torch.randn((N, c0, shapes[0].h, shapes[0].w), device=dev)            # block-0 input (pool out)
+    blocks = []
+    for b, s in enumerate(shapes):
+        nb = NaiveBlock(s, "naive", dev)
+        nb.forward(x, params[b])
+        blocks.append(nb)
+        C = s.c_out
+        if b + 1 < len(shapes):  # transition: BN+ReLU out, conv out, pooled out
+            cout = shapes[b + 1].c0
+            hold += [torch.empty((N, C, s.h, s.w), device=dev), torch.empty((N, cout, s.h, s.w), device=dev)]
+            x = torch.randn((N, cout, shapes[b + 1].h, shapes[b + 1].w), device=dev)
+        else:                    # head: BN+ReLU out, pooled features, logits
+            hold += [torch.empty((N, C, s.h, s.w), device=dev), torch.empty((N, C), device=dev),
+                     torch.empty((N, cfg.num_classes), device=dev)]
+    for b in reversed(range(len(shapes))):
+        s = shapes[b]
+        C = s.c_out
+        if b + 1 == len(shapes):  # head backward transients: d(gap), d(act)
+            hold += [torch.empty((N, C), device=dev), torch.empty((N, C, s.h, s.w), device=dev)]
+        acc = torch.randn((N, C, s.h, s.w), device=dev)   # the block accumulator the consumer's BN bwd writes
+        hold.append(acc)
+        blocks[b].backward(params[b], acc, grads[b])
+        if b > 0:                 # transition b-1 backward transients: d(conv out), d(BN in)
+            p = shapes[b - 1]
+            hold += [torch.empty((N, s.c0, p.h, p.w), device=dev), torch.empty((N, p.c_out, p.h, p.w), device=dev)]
+    e1.record()
+    torch.cuda.synchronize(dev)
+    peak = torch.cuda.max_memory_allocated(dev) - base
+    # the reference's geometry: its 3x3/1 stem at the block-0 field (SURVEY F4)
+    pred = predict_peak_elements(cfg, "naive", batch, cfg.in_shape[0], shapes[0].h, shapes[0].w)
+    out = {"allocator_peak_bytes": int(peak),
+           "reference_peak_model_bytes": 4 * sum(v for k, v in pred.items() if k != "params"),
+           "blocks_ms": e0.elapsed_time(e1),
+           "note": ("reference Naive strategy, fp32: dense blocks computed by NaiveBlock (unfused per-op "
+                    "kernels), stem / transition / head tensors allocated at their shapes; CUDA caching "
+                    "allocator high-water above the parameters.  The peak model uses the reference's "
+                    "3x3/1 stem geometry; NaiveBlock keeps one extra accumulator copy per block")}
+    del blocks, hold
+    torch.cuda.empty_cache()
+    return out

@@ -21,8 +21,8 @@ def load_golden(name: str) -> dict:
     return d
 
 
-# dense-block cases (model_*.npz hold whole-network steps, tests/test_model_gpu.py)
-GOLDEN_CASES = sorted(f[:-4] for f in os.listdir(GOLDEN) if f.endswith(".npz") and not f.startswith("model_"))
+# dense-block cases (model_*.npz / train_*.npz hold whole-network steps, tests/test_model_gpu.py, test_train_gpu.py)
+GOLDEN_CASES = sorted(f[:-4] for f in os.listdir(GOLDEN) if f.endswith(".npz") and not f.startswith(("model_", "train_")))
 
 
 def rel_err(a, b):

@@ -147,7 +147,7 @@ def test_config_errors():
 
 
 def test_block_shapes_match_geometry():
-    shapes = model.CONFIGS["d264k48"].block_shapes(64, stem_stride=4)
+    shapes = model.CONFIGS["d264k48"].block_shapes(64)
     assert [(s.h, s.c0, s.m) for s in shapes] == [(56, 96, 6), (28, 192, 12), (14, 384, 64), (7, 1728, 48)]
     assert shapes[2].c_out == 384 + 64 * 48 == 3456
     bc = model.CONFIGS["bc100"].block_shapes(64)
