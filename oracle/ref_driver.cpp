@@ -669,10 +669,13 @@ void model_train_step(int nblocks, const int* blocks, int k, double compression,
   if (stem == 1) {
     const Shape4 ps = spool.shape();
     const std::int64_t C0out = c0 + static_cast<std::int64_t>(blocks[0]) * k;
-    const Tensor<float>* acc0 = nullptr;  // the last retained [N, C0out, H0, W0]: block-0 accumulator
-    for (const auto& t : state.retained)
-      if (t.shape() == Shape4{ps.n, C0out, ps.h, ps.w}) acc0 = &t;
-    if (acc0 == nullptr) throw AccountingError("block-0 accumulator not retained");
+    // Naive backward retains, in order, ..., the block-0 accumulator (acquired by
+    // transition 0 or the head), then block 0's four transients per layer
+    // (backward_layer, graph.hpp:905-935); the stem's wgrad acquires nothing.
+    const std::size_t nr = state.retained.size(), after = 4 * static_cast<std::size_t>(blocks[0]);
+    if (nr < after + 1) throw AccountingError("block-0 accumulator not retained");
+    const Tensor<float>* acc0 = &state.retained[nr - after - 1];
+    if (acc0->shape() != Shape4{ps.n, C0out, ps.h, ps.w}) throw AccountingError("block-0 accumulator shape");
     Tensor<float> gpool = Tensor<float>::alloc(ps, ArenaTag::Scratch, tr);
     for (std::int64_t i = 0; i < ps.n; ++i)
       for (std::int64_t c = 0; c < c0; ++c)
