@@ -294,11 +294,17 @@ def main():
     m_vel = torch.zeros(mplan.param_elems, device=dev)
     m_loss = torch.zeros(1, device=dev)
 
+    comm = None
+    if world > 1:
+        # libdpb's NCCL communicator: dpb_model_step averages the gradients per
+        # block bucket on its communication stream, overlapped with the backward
+        # of the blocks below (per-GPU BN), inside the step's graph
+        from paper_1707_06990_b200.dp import DpComm
+        comm = DpComm(rank, world, local)
+        mplan.set_comm(comm)
+
     def model_update():
-        if world > 1:   # DP allreduce of the flat gradients (per-GPU BN)
-            dist.all_reduce(m_grads)
-            m_grads.mul_(1.0 / world)
-        # momentum SGD + weight decay (train.hpp:43-70)
+        # momentum SGD + weight decay (train.hpp:43-70) on the averaged gradients
         sgd_step(m_params, m_grads, m_vel, lr=0.1, momentum=0.9, weight_decay=1e-4, stream=stream)
 
     def model_step():
@@ -506,6 +512,8 @@ def main():
                        "blocks": [list(s_) for s_ in shapes], "parallelism": f"dp{world}",
                        "reference_geometry": ref_name, "loss": loss_value,
                        "cuda_graph": not args.no_graph,
+                       "dp": ("libdpb NCCL allreduce (ncclAvg) per block bucket on a communication stream, "
+                              "overlapped with backward, inside the step's CUDA graph" if world > 1 else None),
                        "l2": "inputs and working set (GBs of arena) far larger than the 126 MB L2; no flush"},
             "dense_blocks": {"value": blocks_value, "unit": "images/s", "ms_per_step": blocks_ms,
                              "note": "the dense blocks alone (the hot path), graph-captured"},
@@ -516,6 +524,8 @@ def main():
         }
         print(json.dumps(line), flush=True)
     mplan.close()
+    if comm is not None:
+        comm.close()
     if world > 1:
         dist.destroy_process_group()
     return 0

@@ -314,6 +314,28 @@ DPB_API int dpb_model_sync(dpb_model* model);
 DPB_API int dpb_model_memory_stats(dpb_model* model, dpb_memory_stats* out);
 DPB_API int64_t dpb_model_launch_count(dpb_model* model);
 
+/* ---- data parallelism ---------------------------------------------
+ * One NCCL communicator per GPU, one process per GPU.  Rank 0 creates the id
+ * (dpb_comm_unique_id, 128 bytes) and the caller distributes it (e.g. a
+ * torch.distributed broadcast); every rank then calls dpb_comm_init.  With a
+ * communicator attached (dpb_model_set_comm), dpb_model_step averages the
+ * parameter gradients over the ranks (ncclAvg, fp32): one allreduce per
+ * bucket, issued on the model's communication stream as soon as the bucket's
+ * gradients exist (block b's parameters with its transition / the head,
+ * right after block b's backward; the stem with block 0), overlapping the
+ * backward of the blocks below, and joined before the step ends — inside the
+ * step's CUDA graph.  BN statistics stay per rank.
+ * dpb_model_buckets lists the buckets [begin, end) (flat parameter offsets)
+ * in issue order; they tile [0, param_elems).  NCCL is loaded at run time
+ * (the copy already in the process when there is one). */
+typedef struct dpb_comm dpb_comm;
+DPB_API int dpb_comm_unique_id(uint8_t* out /* 128 bytes */);
+DPB_API int dpb_comm_init(int nranks, int rank, const uint8_t* id, int device, dpb_comm** out);
+DPB_API int dpb_comm_destroy(dpb_comm* comm);
+DPB_API int dpb_comm_check(dpb_comm* comm);  /* ncclCommGetAsyncError */
+DPB_API int dpb_model_set_comm(dpb_model* model, dpb_comm* comm /* NULL: no exchange */);
+DPB_API int dpb_model_buckets(const dpb_model_desc* desc, int64_t* ranges /* 2 * max */, int max, int* count);
+
 /* ---- optimizer -------------------------------------------
  * dpb_sgd_step replaces sgd_step (train.hpp:43-70) over a flat fp32 buffer:
  *   d = g + wd*p;  v = mu*v + d;  p -= lr * (nesterov ? d + mu*v : v)

@@ -148,24 +148,50 @@ TRAIN_CASES = {
 
 
 def make_train_case(name, blocks, k, comp, classes, c0, in_shape, seed, stem, full):
+    """The reference step in float32 (GraphPlan<float>, the reference as
+    shipped) and float64 (GraphPlan<double> on the same float parameters and
+    input: the exact-arithmetic yardstick), plus the float32 reference's own
+    per-tensor deviation from float64 (its precision noise: ReLU-mask flips
+    near zero, long sequential sums; tests/test_train_gpu.py)."""
     n, c, h, w = in_shape
-    params = None
     if stem == 1:
         sys.path.insert(0, os.path.dirname(OUT.rstrip("/").rsplit("/", 1)[0]))
         from paper_1707_06990_b200.model import DenseNetConfig, init_params
         params = init_params(DenseNetConfig(tuple(blocks), k, True, comp, classes, c0, (c, h, w), stem="imagenet"),
                              seed)
+    else:
+        params, _ = O.ref_model_params(blocks, k, 1, comp, classes, c0, in_shape, seed)
     loss, grads, running = O.ref_model_train_step(blocks, k, comp, classes, c0, in_shape, seed, stem, params)
+    loss64, grads64, running64 = O.ref_model_train_step(blocks, k, comp, classes, c0, in_shape, seed, stem, params,
+                                                        dtype=np.float64)
+    gsegs = O.model_segments(blocks, k, comp, classes, c0, c, stem)
+    rsegs = O.running_segments(blocks, k, comp, c0, stem)
+
+    def noise(a32, a64, segs):  # per tensor: normwise and max elementwise rel_err of float32 vs float64
+        nw, el, o = [], [], 0
+        for _, m in segs:
+            x, y = a32[o:o + m].astype(np.float64), a64[o:o + m]
+            nw.append(np.linalg.norm(x - y) / max(np.linalg.norm(y), 1e-300))
+            el.append(float(np.max(np.abs(x - y) / np.maximum(1.0, np.maximum(np.abs(x), np.abs(y))))))
+            o += m
+        return np.array(nw), np.array(el)
+
+    gn, ge = noise(grads, grads64, gsegs)
+    rn, re_ = noise(running, running64, rsegs)
     meta = dict(blocks=np.array(blocks), k=k, compression=comp, classes=classes, c0=c0, in_shape=np.array(in_shape),
-                seed=seed, stem=stem, loss=np.float64(loss))
+                seed=seed, stem=stem, loss=np.float64(loss), loss64=np.float64(loss64),
+                grads_noise=gn, grads_noise_el=ge, running_noise=rn, running_noise_el=re_,
+                grads_noise_all=np.linalg.norm(grads - grads64) / np.linalg.norm(grads64))
     if full:
-        np.savez_compressed(os.path.join(OUT, f"{name}.npz"), grads=grads, running=running, **meta)
+        np.savez_compressed(os.path.join(OUT, f"{name}.npz"), grads=grads, running=running, grads64=grads64,
+                            running64=running64, **meta)
         return
-    gs = O.sketch(grads, O.model_segments(blocks, k, comp, classes, c0, c, stem))
-    rs = O.sketch(running, O.running_segments(blocks, k, comp, c0, stem))
-    np.savez_compressed(os.path.join(OUT, f"{name}.npz"), **meta,
-                        **{f"grads_{key}": v for key, v in gs.items()},
-                        **{f"running_{key}": v for key, v in rs.items()})
+    sk = {}
+    for tag, arr, segs in (("grads", grads, gsegs), ("grads64", grads64, gsegs), ("running", running, rsegs),
+                           ("running64", running64, rsegs)):
+        sk.update({f"{tag}_{key}": v for key, v in O.sketch(arr, segs).items()})
+    np.savez_compressed(os.path.join(OUT, f"{name}.npz"), **meta, **sk,
+                        grads64_norm_all=np.float64(np.linalg.norm(grads64)))
 
 
 # Config text KATs (densenet.hpp:86-115, 276-377): every preset through

@@ -474,24 +474,28 @@ def sketch_errors(got: np.ndarray, ref_sketch: dict, segs):
     return est, rel
 
 
-def ref_model_train_step(blocks, k, compression, classes, c0, in_shape, seed, stem=0, params=None, x=None):
-    """One reference training step through GraphPlan's public forward /
-    compute_loss / backward (ref_model_train_step_f32 in ref_driver.cpp),
+def ref_model_train_step(blocks, k, compression, classes, c0, in_shape, seed, stem=0, params=None, x=None,
+                         dtype=np.float32):
+    """One reference training step through GraphPlan<T>'s public forward /
+    compute_loss / backward (ref_model_train_step_f32/_f64 in ref_driver.cpp),
     composed with the ImageNet stem for stem=1.  Returns (loss, grads,
-    running) in libdpb's flat layouts; params None = GraphPlan::build's init
-    (stem 0 only), x None = Rng(seed + 99).normal()."""
+    running) in libdpb's flat layouts, in `dtype`.  params (float32) None =
+    GraphPlan<float>::build's init (stem 0, float32 only); x None = the float
+    input Rng(seed + 99).normal() (exact in float64 too)."""
     L = ref_lib()
     n, c, h, w = in_shape
     count = ref_count_parameters(blocks, k, True, compression, classes, c0, c)
     if stem == 1:
         count += c0 * c * 49 - c0 * c * 9 + 2 * c0
     if params is not None:
-        assert params.size == count and params.dtype == np.float32
-    grads = np.zeros(count, dtype=np.float32)
-    running = np.zeros(model_running_size(blocks, k, compression, c0, stem), dtype=np.float32)
+        assert params.size == count and params.dtype == np.float32, (params.size, count, params.dtype)
+    if dtype == np.float64 and params is None:
+        raise ValueError("the float64 reference step needs explicit (float32) parameters")
+    grads = np.zeros(count, dtype=dtype)
+    running = np.zeros(model_running_size(blocks, k, compression, c0, stem), dtype=dtype)
     loss = C.c_double()
     arr = (C.c_int * len(blocks))(*blocks)
-    f = L.ref_model_train_step_f32
+    f = getattr(L, f"ref_model_train_step_{_suffix(dtype)}")
     f.restype = C.c_int
     f.argtypes = [C.c_int, _P, C.c_int, C.c_double, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, _I64,
                   C.c_uint64, _P, _P, C.POINTER(C.c_double), _P, _P]

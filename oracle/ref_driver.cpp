@@ -527,20 +527,31 @@ int ref_model_step_f32(int nblocks, const int* blocks, int k, int bottleneck,
 // stem 0 only); x may be null (Rng(seed + 99).normal(), NCHW).
 namespace {
 
-float run_update(float r0, float stat) {  // ops.hpp:190-193, T = float
-  const float momentum = static_cast<float>(0.1);
-  return (float(1) - momentum) * r0 + momentum * stat;
+template <typename T>
+T run_update(T r0, T stat) {  // ops.hpp:190-193
+  const T momentum = static_cast<T>(0.1);
+  return (T(1) - momentum) * r0 + momentum * stat;
 }
 
-void put_running(const ops::BatchStats<float>& st, float*& out) {
-  for (float v : st.mean) *out++ = run_update(0.f, v);
-  for (float v : st.var) *out++ = run_update(1.f, v);
+template <typename T>
+void put_running(const ops::BatchStats<T>& st, T*& out) {
+  for (T v : st.mean) *out++ = run_update(T(0), v);
+  for (T v : st.var) *out++ = run_update(T(1), v);
 }
 
+// float host data -> a Tensor<T> (exact for T = double)
+template <typename T>
+Tensor<T> from_float(const float* src, const Shape4& s, MemoryTracker& tr) {
+  Tensor<T> t = Tensor<T>::alloc(s, ArenaTag::Scratch, tr);
+  for (std::int64_t i = 0; i < s.elems(); ++i) t.data()[i] = static_cast<T>(src[i]);
+  return t;
+}
+
+template <typename T>
 struct MaxPool3 {  // 3x3 stride 2 pad 1 max-pool, restated (not in the reference)
   std::vector<int> arg;  // per output: input flat index of the first maximum
   Shape4 os;
-  void forward(const Tensor<float>& x, Tensor<float>& y) {
+  void forward(const Tensor<T>& x, Tensor<T>& y) {
     const Shape4& s = x.shape();
     os = y.shape();
     arg.assign(static_cast<std::size_t>(os.elems()), -1);
@@ -549,7 +560,7 @@ struct MaxPool3 {  // 3x3 stride 2 pad 1 max-pool, restated (not in the referenc
       for (std::int64_t c = 0; c < s.c; ++c)
         for (std::int64_t oy = 0; oy < os.h; ++oy)
           for (std::int64_t ox = 0; ox < os.w; ++ox, ++o) {
-            float best = 0.f;
+            T best = 0;
             int bi = -1;
             for (std::int64_t ky = 0; ky < 3; ++ky) {
               const std::int64_t iy = 2 * oy - 1 + ky;
@@ -557,7 +568,7 @@ struct MaxPool3 {  // 3x3 stride 2 pad 1 max-pool, restated (not in the referenc
               for (std::int64_t kx = 0; kx < 3; ++kx) {
                 const std::int64_t ix = 2 * ox - 1 + kx;
                 if (ix < 0 || ix >= s.w) continue;
-                const float v = x.at(i, c, iy, ix);
+                const T v = x.at(i, c, iy, ix);
                 if (bi < 0 || v > best) {
                   best = v;
                   bi = static_cast<int>(((i * s.c + c) * s.h + iy) * s.w + ix);
@@ -568,8 +579,8 @@ struct MaxPool3 {  // 3x3 stride 2 pad 1 max-pool, restated (not in the referenc
             arg[o] = bi;
           }
   }
-  void backward(const Tensor<float>& gy, Tensor<float>& gx) {
-    gx.fill(0.f);
+  void backward(const Tensor<T>& gy, Tensor<T>& gx) {
+    gx.fill(T(0));
     std::size_t o = 0;
     for (std::int64_t i = 0; i < os.n; ++i)
       for (std::int64_t c = 0; c < os.c; ++c)
@@ -578,37 +589,46 @@ struct MaxPool3 {  // 3x3 stride 2 pad 1 max-pool, restated (not in the referenc
   }
 };
 
+template <typename T>
 void model_train_step(int nblocks, const int* blocks, int k, double compression, int classes, int c0, int stem,
                       int in_c, int in_h, int in_w, std::int64_t batch, std::uint64_t seed, const float* params,
-                      const float* x_in, double* loss, float* grads, float* running) {
+                      const float* x_in, double* loss, T* grads, T* running) {
   const int kk = stem == 1 ? 7 : 3;
   MemoryTracker tr;
   const Shape4 in{batch, in_c, in_h, in_w};
-  Tensor<float> input = x_in ? from_flat(x_in, in, tr) : make_input<float>(in, seed + 99, tr);
+  // the float synthetic input Rng(seed+99) (make_input<float>), exact in T
+  Tensor<T> input;
+  if (x_in) {
+    input = from_float<T>(x_in, in, tr);
+  } else {
+    Tensor<float> xf = make_input<float>(in, seed + 99, tr);
+    input = from_float<T>(xf.data(), in, tr);
+  }
   const std::vector<int> labels = make_labels(static_cast<int>(batch), classes);
 
   // ---- stem 1 forward (reference ops + restated max-pool) ----
-  ops::ConvParams<float> sconv;
-  ops::BatchNormState<float> sbn;
-  ops::BatchStats<float> sstats;
-  Tensor<float> sy, sact, spool;
-  MaxPool3 pool;
+  ops::ConvParams<T> sconv;
+  ops::BatchNormState<T> sbn;
+  ops::BatchStats<T> sstats;
+  Tensor<T> sy, sact, spool;
+  MaxPool3<T> pool;
   const std::int64_t swn = static_cast<std::int64_t>(c0) * in_c * kk * kk;
   if (stem == 1) {
     if (params == nullptr) throw ConfigError("the ImageNet stem needs explicit parameters");
-    sconv.weights = from_flat(params, Shape4{c0, in_c, 7, 7}, tr);
+    sconv.weights = from_float<T>(params, Shape4{c0, in_c, 7, 7}, tr);
     sconv.stride = 2;
     sconv.padding = 3;
-    const std::vector<float> r0(static_cast<std::size_t>(c0), 0.f), r1(static_cast<std::size_t>(c0), 1.f);
-    sbn = make_bn(params + swn, params + swn + c0, r0.data(), r1.data(), c0, tr);
+    const std::vector<T> r0(static_cast<std::size_t>(c0), T(0)), r1(static_cast<std::size_t>(c0), T(1));
+    const std::vector<T> gm(params + swn, params + swn + c0), bt(params + swn + c0, params + swn + 2 * c0);
+    sbn = make_bn(gm.data(), bt.data(), r0.data(), r1.data(), c0, tr);
     const Shape4 ys = ops::conv2d_out_shape(in, sconv);
-    sy = Tensor<float>::alloc(ys, ArenaTag::Scratch, tr);
+    sy = Tensor<T>::alloc(ys, ArenaTag::Scratch, tr);
     ops::conv2d_forward(input, sconv, sy);
-    sact = Tensor<float>::alloc(ys, ArenaTag::Scratch, tr);
+    sact = Tensor<T>::alloc(ys, ArenaTag::Scratch, tr);
     sstats = ops::batchnorm_forward(sy, sbn, ops::BnMode::Train, sact, true);
     ops::relu_inplace(sact);
     const Shape4 ps{batch, c0, (ys.h + 2 - 3) / 2 + 1, (ys.w + 2 - 3) / 2 + 1};
-    spool = Tensor<float>::alloc(ps, ArenaTag::Scratch, tr);
+    spool = Tensor<T>::alloc(ps, ArenaTag::Scratch, tr);
     pool.forward(sact, spool);
   }
   const std::int64_t soff = stem == 1 ? swn + 2 * c0 : swn;  // params after the stem
@@ -616,27 +636,28 @@ void model_train_step(int nblocks, const int* blocks, int k, double compression,
   // ---- the reference network ----
   const DenseNetConfig cfg = model_cfg(nblocks, blocks, k, 1, compression, classes, c0);
   const Shape4 gin = stem == 1 ? spool.shape() : in;
-  GraphPlan<float> plan =
-      GraphPlan<float>::build(cfg, stem == 1 ? ExecutionStrategy::Naive : ExecutionStrategy::SharedAll, gin, seed);
+  GraphPlan<T> plan =
+      GraphPlan<T>::build(cfg, stem == 1 ? ExecutionStrategy::Naive : ExecutionStrategy::SharedAll, gin, seed);
   {
     std::size_t off = 0;
     for (auto& p : plan.params()) {
       const std::int64_t n = p.value.elems();
       if (p.name == "stem.conv.w") {
         if (stem == 1) {  // identity 3x3: out[o] = in[o]
-          p.value.fill(0.f);
-          for (std::int64_t o = 0; o < c0; ++o) p.value.at(o, o, 1, 1) = 1.f;
+          p.value.fill(T(0));
+          for (std::int64_t o = 0; o < c0; ++o) p.value.at(o, o, 1, 1) = T(1);
         } else if (params) {
-          std::memcpy(p.value.data(), params, sizeof(float) * static_cast<std::size_t>(n));
+          for (std::int64_t i = 0; i < n; ++i) p.value.data()[i] = static_cast<T>(params[i]);
         }
         off = static_cast<std::size_t>(soff);
         continue;
       }
-      if (params) std::memcpy(p.value.data(), params + off, sizeof(float) * static_cast<std::size_t>(n));
+      if (params)
+        for (std::int64_t i = 0; i < n; ++i) p.value.data()[i] = static_cast<T>(params[off + static_cast<std::size_t>(i)]);
       off += static_cast<std::size_t>(n);
     }
   }
-  StepState<float> state = plan.forward(stem == 1 ? spool : input, ops::BnMode::Train);
+  StepState<T> state = plan.forward(stem == 1 ? spool : input, ops::BnMode::Train);
   *loss = plan.compute_loss(state, labels);
   plan.backward(state);
 
@@ -655,7 +676,7 @@ void model_train_step(int nblocks, const int* blocks, int k, double compression,
     }
   }
   // running statistics (F10)
-  float* r = running;
+  T* r = running;
   if (stem == 1) put_running(sstats, r);
   for (std::size_t b = 0; b < state.blocks.size(); ++b) {
     for (const auto& ls : state.blocks[b].layers) {
@@ -674,22 +695,22 @@ void model_train_step(int nblocks, const int* blocks, int k, double compression,
     // (backward_layer, graph.hpp:905-935); the stem's wgrad acquires nothing.
     const std::size_t nr = state.retained.size(), after = 4 * static_cast<std::size_t>(blocks[0]);
     if (nr < after + 1) throw AccountingError("block-0 accumulator not retained");
-    const Tensor<float>* acc0 = &state.retained[nr - after - 1];
+    const Tensor<T>* acc0 = &state.retained[nr - after - 1];
     if (acc0->shape() != Shape4{ps.n, C0out, ps.h, ps.w}) throw AccountingError("block-0 accumulator shape");
-    Tensor<float> gpool = Tensor<float>::alloc(ps, ArenaTag::Scratch, tr);
+    Tensor<T> gpool = Tensor<T>::alloc(ps, ArenaTag::Scratch, tr);
     for (std::int64_t i = 0; i < ps.n; ++i)
       for (std::int64_t c = 0; c < c0; ++c)
         for (std::int64_t y = 0; y < ps.h; ++y)
           for (std::int64_t x = 0; x < ps.w; ++x) gpool.at(i, c, y, x) = acc0->at(i, c, y, x);
-    Tensor<float> ga = Tensor<float>::alloc(sy.shape(), ArenaTag::Scratch, tr);
+    Tensor<T> ga = Tensor<T>::alloc(sy.shape(), ArenaTag::Scratch, tr);
     pool.backward(gpool, ga);
     ops::relu_backward_inplace(ga, sact);
-    Tensor<float> gy = Tensor<float>::alloc(sy.shape(), ArenaTag::Scratch, tr);
-    Tensor<float> dg = Tensor<float>::alloc(Shape4{1, c0, 1, 1}, ArenaTag::Scratch, tr);
-    Tensor<float> db = Tensor<float>::alloc(Shape4{1, c0, 1, 1}, ArenaTag::Scratch, tr);
+    Tensor<T> gy = Tensor<T>::alloc(sy.shape(), ArenaTag::Scratch, tr);
+    Tensor<T> dg = Tensor<T>::alloc(Shape4{1, c0, 1, 1}, ArenaTag::Scratch, tr);
+    Tensor<T> db = Tensor<T>::alloc(Shape4{1, c0, 1, 1}, ArenaTag::Scratch, tr);
     ops::batchnorm_backward(ga, sy, sbn, sstats, gy, dg, db);
-    Tensor<float> dw = Tensor<float>::alloc(sconv.weights.shape(), ArenaTag::Scratch, tr);
-    ops::conv2d_backward(gy, input, sconv, static_cast<Tensor<float>*>(nullptr), dw);
+    Tensor<T> dw = Tensor<T>::alloc(sconv.weights.shape(), ArenaTag::Scratch, tr);
+    ops::conv2d_backward(gy, input, sconv, static_cast<Tensor<T>*>(nullptr), dw);
     to_flat(dw, grads);
     to_flat(dg, grads + swn);
     to_flat(db, grads + swn + c0);
@@ -698,15 +719,18 @@ void model_train_step(int nblocks, const int* blocks, int k, double compression,
 
 }  // namespace
 
-extern "C" int ref_model_train_step_f32(int nblocks, const int* blocks, int k, double compression, int classes,
-                                        int c0, int stem, int in_c, int in_h, int in_w, std::int64_t batch,
-                                        std::uint64_t seed, const float* params, const float* x, double* loss,
-                                        float* grads, float* running) {
-  return guarded([&] {
-    model_train_step(nblocks, blocks, k, compression, classes, c0, stem, in_c, in_h, in_w, batch, seed, params, x,
-                     loss, grads, running);
-  });
-}
+#define DEFINE_TRAIN_STEP(SUF, T)                                                                               \
+  extern "C" int ref_model_train_step_##SUF(int nblocks, const int* blocks, int k, double compression,         \
+                                            int classes, int c0, int stem, int in_c, int in_h, int in_w,        \
+                                            std::int64_t batch, std::uint64_t seed, const float* params,        \
+                                            const float* x, double* loss, T* grads, T* running) {               \
+    return guarded([&] {                                                                                        \
+      model_train_step<T>(nblocks, blocks, k, compression, classes, c0, stem, in_c, in_h, in_w, batch, seed,    \
+                          params, x, loss, grads, running);                                                    \
+    });                                                                                                         \
+  }
+DEFINE_TRAIN_STEP(f32, float)
+DEFINE_TRAIN_STEP(f64, double)
 
 extern "C" {
 

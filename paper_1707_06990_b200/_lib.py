@@ -91,6 +91,12 @@ SIGNATURES = {
     "dpb_model_step": (C.c_int, [_P, _P, _P, _P, _P, _P, _P]),
     "dpb_model_sync": (C.c_int, [_P]),
     "dpb_model_memory_stats": (C.c_int, [_P, C.POINTER(MemoryStats)]),
+    "dpb_model_set_comm": (C.c_int, [_P, _P]),
+    "dpb_model_buckets": (C.c_int, [C.POINTER(ModelDesc), _P, C.c_int, C.POINTER(C.c_int)]),
+    "dpb_comm_unique_id": (C.c_int, [_P]),
+    "dpb_comm_init": (C.c_int, [C.c_int, C.c_int, _P, C.c_int, C.POINTER(_P)]),
+    "dpb_comm_destroy": (C.c_int, [_P]),
+    "dpb_comm_check": (C.c_int, [_P]),
     "dpb_model_launch_count": (_I64, [_P]),
     "dpb_block_memory_stats": (C.c_int, [_P, C.POINTER(MemoryStats)]),
     "dpb_sgd_step": (C.c_int, [_P, _P, _P, _I64, C.c_double, C.c_double, C.c_double, C.c_int, _P]),

@@ -23,6 +23,7 @@
 #include <random>
 #include <vector>
 
+#include "dpb_comm.h"
 #include "dpb_common.cuh"
 #include "dpb_internal.h"
 #include "dpb_launch.h"
@@ -126,9 +127,10 @@ __host__ __device__ inline int stem7_out(int in) { return (in + 2 * 3 - kS7) / 2
 __host__ __device__ inline int pool3_out(int in) { return (in + 2 * 1 - 3) / 2 + 1; }
 
 // y[p][o] (NHWC, pitch c0) = sum_{ci,ky,kx} x[n][ci][2oy-3+ky][2ox-3+kx] w[o][ci][ky][kx],
-// the reference's summation order (ops.hpp:321-341).  Thread = output pixel x
-// 32-channel group (blockIdx.y); weights transposed in shared memory [tap][c0p]
-// so a warp's 16-byte weight reads are broadcasts.
+// the reference's summation order (ops.hpp:321-341).  Thread = two horizontally
+// adjacent output pixels x a 32-channel group (blockIdx.y); weights transposed
+// in shared memory [tap][c0p], each warp-wide 16-byte weight read is a
+// broadcast shared by both pixels (64 FMAs per 8 shared loads).
 __global__ void __launch_bounds__(128) k_stem7_conv(const float* __restrict__ in, int64_t N, int cin, int H,
                                                     int W, int Ho, int Wo, const float* __restrict__ w, int c0,
                                                     float* __restrict__ y) {
@@ -140,47 +142,55 @@ __global__ void __launch_bounds__(128) k_stem7_conv(const float* __restrict__ in
     wsm[i] = o < c0 ? w[static_cast<int64_t>(o) * nt + t] : 0.f;
   }
   __syncthreads();
-  const int64_t p = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (p >= N * Ho * Wo) return;
+  const int wo2 = (Wo + 1) / 2;  // pixel pairs per output row
+  const int64_t pair = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (pair >= N * Ho * wo2) return;
   const int grp = blockIdx.y;
-  const int hw = Ho * Wo;
-  const int n = static_cast<int>(p / hw);
-  const int r = static_cast<int>(p - static_cast<int64_t>(n) * hw);
-  const int oy = r / Wo, ox = r - (r / Wo) * Wo;
-  float acc[32];
+  const int n = static_cast<int>(pair / (static_cast<int64_t>(Ho) * wo2));
+  const int r = static_cast<int>(pair - static_cast<int64_t>(n) * Ho * wo2);
+  const int oy = r / wo2, ox = 2 * (r - (r / wo2) * wo2);
+  const bool two = ox + 1 < Wo;
+  float a0[32], a1[32];
 #pragma unroll
-  for (int j = 0; j < 32; ++j) acc[j] = 0.f;
+  for (int j = 0; j < 32; ++j) a0[j] = a1[j] = 0.f;
   for (int ci = 0; ci < cin; ++ci) {
     const float* xc = in + (static_cast<int64_t>(n) * cin + ci) * H * W;
     for (int ky = 0; ky < kS7; ++ky) {
       const int iy = 2 * oy - 3 + ky;
       if (iy < 0 || iy >= H) continue;
+      const float* xr = xc + static_cast<int64_t>(iy) * W;
       for (int kx = 0; kx < kS7; ++kx) {
-        const int ix = 2 * ox - 3 + kx;
-        if (ix < 0 || ix >= W) continue;
-        const float xv = __ldg(xc + static_cast<int64_t>(iy) * W + ix);
+        const int ix = 2 * ox - 3 + kx;  // pixel 1 reads ix + 2
+        const float x0 = (ix >= 0 && ix < W) ? __ldg(xr + ix) : 0.f;
+        const float x1 = (ix + 2 >= 0 && ix + 2 < W) ? __ldg(xr + ix + 2) : 0.f;
         const float4* wr = reinterpret_cast<const float4*>(wsm + (ci * kS7Taps + ky * kS7 + kx) * c0p + grp * 32);
 #pragma unroll
         for (int j = 0; j < 8; ++j) {
           const float4 w4 = wr[j];
-          acc[4 * j] += xv * w4.x;
-          acc[4 * j + 1] += xv * w4.y;
-          acc[4 * j + 2] += xv * w4.z;
-          acc[4 * j + 3] += xv * w4.w;
+          a0[4 * j] += x0 * w4.x;
+          a0[4 * j + 1] += x0 * w4.y;
+          a0[4 * j + 2] += x0 * w4.z;
+          a0[4 * j + 3] += x0 * w4.w;
+          a1[4 * j] += x1 * w4.x;
+          a1[4 * j + 1] += x1 * w4.y;
+          a1[4 * j + 2] += x1 * w4.z;
+          a1[4 * j + 3] += x1 * w4.w;
         }
       }
     }
   }
-  float* yr = y + p * c0 + grp * 32;
+  const int64_t p = (static_cast<int64_t>(n) * Ho + oy) * Wo + ox;
   const int nv = c0 - grp * 32 < 32 ? c0 - grp * 32 : 32;
-  if (nv == 32 && (c0 & 3) == 0) {
+  for (int q = 0; q < (two ? 2 : 1); ++q) {
+    const float* a = q ? a1 : a0;
+    float* yr = y + (p + q) * c0 + grp * 32;
+    if (nv == 32 && (c0 & 3) == 0) {
 #pragma unroll
-    for (int j = 0; j < 8; ++j)
-      reinterpret_cast<float4*>(yr)[j] = make_float4(acc[4 * j], acc[4 * j + 1], acc[4 * j + 2], acc[4 * j + 3]);
-  } else {
-#pragma unroll
-    for (int j = 0; j < 32; ++j)
-      if (j < nv) yr[j] = acc[j];
+      for (int j = 0; j < 8; ++j)
+        reinterpret_cast<float4*>(yr)[j] = make_float4(a[4 * j], a[4 * j + 1], a[4 * j + 2], a[4 * j + 3]);
+    } else {
+      for (int j = 0; j < nv; ++j) yr[j] = a[j];
+    }
   }
 }
 
@@ -242,118 +252,148 @@ __device__ __forceinline__ float stem_pool_grad(int64_t p, int c, int H1, int W1
 }
 
 // BN backward partial sums of the stem: g = relu'(bn(y)) * stem_pool_grad,
-// sums (sum g, sum g*xhat) over pixel chunk blockIdx.x in fixed order; thread =
-// channel (blockIdx.y * blockDim.x + threadIdx.x), coalesced along c.
-__global__ void k_stem_bnb_partials(const float* __restrict__ y, int64_t M1, int H1, int W1, int H0, int W0, int c0,
-                                    const float* __restrict__ mean, const float* __restrict__ var,
-                                    const float* __restrict__ gamma, const float* __restrict__ beta,
-                                    const float* __restrict__ g0, int ld0, const uint8_t* __restrict__ arg,
-                                    int64_t chunk, double2* __restrict__ part) {
+// (sum g, sum g*xhat) over pixel chunk blockIdx.x.  CTA = 32 channel lanes
+// (blockIdx.y selects the 32-channel group) x 8 pixel lanes; each warp reads
+// one pixel's 32 channels (coalesced); the 8 pixel lanes are folded in fixed
+// order (deterministic).
+__global__ void __launch_bounds__(256) k_stem_bnb_partials(const float* __restrict__ y, int64_t M1, int H1, int W1,
+                                                           int H0, int W0, int c0, const float* __restrict__ mean,
+                                                           const float* __restrict__ var,
+                                                           const float* __restrict__ gamma,
+                                                           const float* __restrict__ beta,
+                                                           const float* __restrict__ g0, int ld0,
+                                                           const uint8_t* __restrict__ arg, int64_t chunk,
+                                                           double2* __restrict__ part) {
   pdl_enter();
-  const int c = blockIdx.y * blockDim.x + threadIdx.x;
-  if (c >= c0) return;
-  const float mu = mean[c], inv = bn_inv(var[c]), ga = gamma[c], be = beta[c];
-  const int64_t p0 = static_cast<int64_t>(blockIdx.x) * chunk;
-  const int64_t p1 = p0 + chunk < M1 ? p0 + chunk : M1;
+  __shared__ double r1[8][33], r2[8][33];
+  const int lane = threadIdx.x % 32, pl = threadIdx.x / 32;
+  const int c = blockIdx.y * 32 + lane;
   double s1 = 0.0, s2 = 0.0;
-  for (int64_t p = p0; p < p1; ++p) {
-    const float x = y[p * c0 + c];
-    if (!(bn_ref(x, mu, inv, ga, be) > 0.f)) continue;  // relu_backward (ops.hpp:268-287)
-    const float g = stem_pool_grad(p, c, H1, W1, H0, W0, c0, g0, ld0, arg);
-    s1 += g;
-    s2 += g * ((x - mu) * inv);
+  if (c < c0) {
+    const float mu = mean[c], inv = bn_inv(var[c]), ga = gamma[c], be = beta[c];
+    const int64_t p0 = static_cast<int64_t>(blockIdx.x) * chunk;
+    const int64_t p1 = p0 + chunk < M1 ? p0 + chunk : M1;
+    for (int64_t p = p0 + pl; p < p1; p += 8) {
+      const float x = y[p * c0 + c];
+      if (!(bn_ref(x, mu, inv, ga, be) > 0.f)) continue;  // relu_backward (ops.hpp:268-287)
+      const float g = stem_pool_grad(p, c, H1, W1, H0, W0, c0, g0, ld0, arg);
+      s1 += g;
+      s2 += g * ((x - mu) * inv);
+    }
   }
-  part[static_cast<int64_t>(blockIdx.x) * c0 + c] = make_double2(s1, s2);
+  r1[pl][lane] = s1;
+  r2[pl][lane] = s2;
+  __syncthreads();
+  if (pl == 0 && c < c0) {
+    double a = 0.0, b = 0.0;
+    for (int i = 0; i < 8; ++i) {
+      a += r1[i][lane];
+      b += r2[i][lane];
+    }
+    part[static_cast<int64_t>(blockIdx.x) * c0 + c] = make_double2(a, b);
+  }
 }
 
-// g_y = gamma*inv*(g - mg - xhat*mgx) (ops.hpp:232-241), written over y in
-// place (y is dead after this pass: the wgrad needs only g_y and the input).
-__global__ void k_stem_bnb_apply(float* __restrict__ y, int64_t M1, int H1, int W1, int H0, int W0, int c0,
-                                 const float* __restrict__ mean, const float* __restrict__ var,
-                                 const float* __restrict__ gamma, const float* __restrict__ beta,
-                                 const float* __restrict__ g0, int ld0, const uint8_t* __restrict__ arg,
-                                 const float* __restrict__ coef) {
-  pdl_enter();
-  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (i >= M1 * c0) return;
-  const int64_t p = i / c0;
-  const int c = static_cast<int>(i - p * c0);
-  const float mu = mean[c], inv = bn_inv(var[c]), ga = gamma[c], be = beta[c];
-  const float x = y[i];
-  const float g = bn_ref(x, mu, inv, ga, be) > 0.f ? stem_pool_grad(p, c, H1, W1, H0, W0, c0, g0, ld0, arg) : 0.f;
-  y[i] = ga * inv * (g - coef[2 * c] - ((x - mu) * inv) * coef[2 * c + 1]);
-}
-
-// dW partials of the 7x7/2 stem: CTA s sums pixels [s*chunk, ...) in steps of
-// kS7Sub staged pixels (g_y rows and the im2col patches in shared memory);
-// thread = a 4-channel x 12-tap register tile of dW[o][t] (t = ci*49 + ky*7 + kx).
-constexpr int kS7Sub = 32, kS7TT = 12;
-__host__ __device__ inline int stem7_tiles(int c0, int cin) {
+// Stem dW partials with the BN-backward apply fused in: a CTA walks output
+// tiles of kS7TH x kS7TW pixels (one image each) [tile0, tile1); per tile it
+// stages g_y = gamma*inv*(g - mg - xhat*mgx) (ops.hpp:232-241; g = the masked
+// max-pool gradient) as [pixel][c0p] and the input window the tile reads
+// (cin x (2*TH+5) x (2*TW+5), zero outside the image) in shared memory, then
+// thread = a 4-channel x 12-tap register tile of dW[o][t] sums the tile's
+// pixels in order.  Partials [cta][c0][cin*49], folded by k_reduce_w1.
+constexpr int kS7TH = 8, kS7TW = 16, kS7IH = 2 * kS7TH + 5, kS7IW = 2 * kS7TW + 5, kS7TT = 12;
+__host__ __device__ inline int stem7_tiles(int c0, int cin) {  // register tiles = threads
   return ((c0 + 3) / 4) * ((cin * kS7Taps + kS7TT - 1) / kS7TT);
 }
+__host__ __device__ inline int stem7_wgrad_smem_floats(int c0, int cin) {
+  return kS7TH * kS7TW * ((c0 + 3) / 4 * 4) + cin * kS7IH * kS7IW + 6 * c0;
+}
 __global__ void k_stem7_wgrad(const float* __restrict__ in, int64_t N, int cin, int H, int W, int Ho, int Wo,
-                              const float* __restrict__ gy, int c0, int64_t chunk, float* __restrict__ wpart) {
+                              const float* __restrict__ y, int c0, const float* __restrict__ mean,
+                              const float* __restrict__ var, const float* __restrict__ gamma,
+                              const float* __restrict__ beta, const float* __restrict__ g0, int ld0, int H0, int W0,
+                              const uint8_t* __restrict__ arg, const float* __restrict__ coef, int64_t tiles_per_cta,
+                              float* __restrict__ wpart) {
   pdl_enter();
   extern __shared__ __align__(16) float sm7[];
   const int nt = cin * kS7Taps;
-  const int c0p = (c0 + 3) / 4 * 4, ntp = (nt + kS7TT - 1) / kS7TT * kS7TT;
-  float* gs = sm7;                  // [kS7Sub][c0p]
-  float* xs = sm7 + kS7Sub * c0p;   // [kS7Sub][ntp]
-  const int ntt = ntp / kS7TT;
+  const int c0p = (c0 + 3) / 4 * 4;
+  const int ntt = (nt + kS7TT - 1) / kS7TT;
+  float* gs = sm7;                               // [TH*TW][c0p]
+  float* xs = sm7 + kS7TH * kS7TW * c0p;         // [cin][IH][IW]
+  float* tab = xs + cin * kS7IH * kS7IW;         // per channel: mean, inv, gamma, beta, mg, mgx
+  for (int c = threadIdx.x; c < c0; c += blockDim.x) {
+    tab[6 * c] = mean[c];
+    tab[6 * c + 1] = bn_inv(var[c]);
+    tab[6 * c + 2] = gamma[c];
+    tab[6 * c + 3] = beta[c];
+    tab[6 * c + 4] = coef[2 * c];
+    tab[6 * c + 5] = coef[2 * c + 1];
+  }
   const int tile = threadIdx.x;
   const bool active = tile < stem7_tiles(c0, cin);
   const int og = active ? tile / ntt : 0, tg = active ? tile - og * ntt : 0;
+  int tofs[kS7TT];
+#pragma unroll
+  for (int b = 0; b < kS7TT; ++b) {
+    const int t = tg * kS7TT + b;
+    const int tc = t < nt ? t : nt - 1;
+    const int ci = tc / kS7Taps, tap = tc - ci * kS7Taps;
+    tofs[b] = (ci * kS7IH + tap / kS7) * kS7IW + tap % kS7;
+  }
   float acc[4][kS7TT];
 #pragma unroll
   for (int a = 0; a < 4; ++a)
 #pragma unroll
     for (int b = 0; b < kS7TT; ++b) acc[a][b] = 0.f;
-  const int64_t M1 = N * Ho * Wo;
-  const int64_t p0 = static_cast<int64_t>(blockIdx.x) * chunk;
-  const int64_t p1 = p0 + chunk < M1 ? p0 + chunk : M1;
-  const int hw = Ho * Wo;
-  for (int64_t pb = p0; pb < p1; pb += kS7Sub) {
-    const int np = p1 - pb < kS7Sub ? static_cast<int>(p1 - pb) : kS7Sub;
+  const int tx = (Wo + kS7TW - 1) / kS7TW, ty = (Ho + kS7TH - 1) / kS7TH;
+  const int64_t ntiles = N * tx * ty;
+  const int64_t t0 = static_cast<int64_t>(blockIdx.x) * tiles_per_cta;
+  const int64_t t1 = t0 + tiles_per_cta < ntiles ? t0 + tiles_per_cta : ntiles;
+  for (int64_t ti = t0; ti < t1; ++ti) {
+    const int n = static_cast<int>(ti / (tx * ty));
+    const int rr = static_cast<int>(ti - static_cast<int64_t>(n) * tx * ty);
+    const int oy0 = (rr / tx) * kS7TH, ox0 = (rr - (rr / tx) * tx) * kS7TW;
     __syncthreads();
-    for (int e = threadIdx.x; e < kS7Sub * c0p; e += blockDim.x) {
-      const int rr = e / c0p, o = e - rr * c0p;
-      gs[e] = (rr < np && o < c0) ? gy[(pb + rr) * c0 + o] : 0.f;
-    }
-    for (int e = threadIdx.x; e < kS7Sub * ntp; e += blockDim.x) {
-      const int rr = e / ntp, t = e - rr * ntp;
+    for (int e = threadIdx.x; e < kS7TH * kS7TW * c0p; e += blockDim.x) {
+      const int pix = e / c0p, c = e - pix * c0p;
+      const int oy = oy0 + pix / kS7TW, ox = ox0 + pix % kS7TW;
       float v = 0.f;
-      if (rr < np && t < nt) {
-        const int64_t p = pb + rr;
-        const int n = static_cast<int>(p / hw);
-        const int rem = static_cast<int>(p - static_cast<int64_t>(n) * hw);
-        const int oy = rem / Wo, ox = rem - (rem / Wo) * Wo;
-        const int ci = t / kS7Taps, tap = t - ci * kS7Taps;
-        const int iy = 2 * oy - 3 + tap / kS7, ix = 2 * ox - 3 + tap % kS7;
-        if (iy >= 0 && iy < H && ix >= 0 && ix < W)
-          v = __ldg(in + ((static_cast<int64_t>(n) * cin + ci) * H + iy) * W + ix);
+      if (c < c0 && oy < Ho && ox < Wo) {
+        const int64_t p = (static_cast<int64_t>(n) * Ho + oy) * Wo + ox;
+        const float* tc = tab + 6 * c;
+        const float mu = tc[0], inv = tc[1], ga = tc[2], be = tc[3];
+        const float x = y[p * c0 + c];
+        const float g = bn_ref(x, mu, inv, ga, be) > 0.f ? stem_pool_grad(p, c, Ho, Wo, H0, W0, c0, g0, ld0, arg)
+                                                         : 0.f;
+        v = ga * inv * (g - tc[4] - ((x - mu) * inv) * tc[5]);
       }
-      xs[e] = v;
+      gs[e] = v;
+    }
+    for (int e = threadIdx.x; e < cin * kS7IH * kS7IW; e += blockDim.x) {
+      const int ci = e / (kS7IH * kS7IW), rem = e - ci * kS7IH * kS7IW;
+      const int iy = 2 * oy0 - 3 + rem / kS7IW, ix = 2 * ox0 - 3 + rem % kS7IW;
+      xs[e] = (iy >= 0 && iy < H && ix >= 0 && ix < W)
+                  ? __ldg(in + ((static_cast<int64_t>(n) * cin + ci) * H + iy) * W + ix)
+                  : 0.f;
     }
     __syncthreads();
     if (active) {
-      for (int rr = 0; rr < np; ++rr) {
-        const float4 g4 = *reinterpret_cast<const float4*>(gs + rr * c0p + og * 4);
-        const float gv[4] = {g4.x, g4.y, g4.z, g4.w};
-        const float4* xr = reinterpret_cast<const float4*>(xs + rr * ntp + tg * kS7TT);
-        float xv[kS7TT];
+      for (int py = 0; py < kS7TH; ++py)
+        for (int px = 0; px < kS7TW; ++px) {
+          const float4 g4 = *reinterpret_cast<const float4*>(gs + (py * kS7TW + px) * c0p + og * 4);
+          const float* xb = xs + 2 * py * kS7IW + 2 * px;
+          float xv[kS7TT];
 #pragma unroll
-        for (int j = 0; j < kS7TT / 4; ++j) {
-          const float4 x4 = xr[j];
-          xv[4 * j] = x4.x;
-          xv[4 * j + 1] = x4.y;
-          xv[4 * j + 2] = x4.z;
-          xv[4 * j + 3] = x4.w;
+          for (int b = 0; b < kS7TT; ++b) xv[b] = xb[tofs[b]];
+#pragma unroll
+          for (int b = 0; b < kS7TT; ++b) {
+            acc[0][b] += g4.x * xv[b];
+            acc[1][b] += g4.y * xv[b];
+            acc[2][b] += g4.z * xv[b];
+            acc[3][b] += g4.w * xv[b];
+          }
         }
-#pragma unroll
-        for (int a = 0; a < 4; ++a)
-#pragma unroll
-          for (int b = 0; b < kS7TT; ++b) acc[a][b] += gv[a] * xv[b];
-      }
     }
   }
   if (!active) return;
@@ -576,6 +616,37 @@ __global__ void k_head_gap(const float* __restrict__ feat, int ld, int64_t N, in
 
 // logits = gap . W^T + b; softmax cross entropy (ops.hpp:528-559): one CTA per
 // sample; per-sample loss (mean taken by k_loss_mean), g_logits = (p - onehot)/N.
+// logits[n][o] = b[o] + sum_c W[o][c] gap[n][c] (linear_forward, ops.hpp:474-485):
+// one warp per (class o, group of kLogitRows samples); lanes stride over C
+// (coalesced W row, read once per group), fixed butterfly per sample.
+constexpr int kLogitRows = 8;
+__global__ void k_head_logits(const float* __restrict__ gap, int64_t N, int C, const float* __restrict__ Wl,
+                              const float* __restrict__ bl, int classes, float* __restrict__ logits) {
+  pdl_enter();
+  const int lane = threadIdx.x % 32;
+  const int64_t wid = static_cast<int64_t>(blockIdx.x) * (blockDim.x / 32) + threadIdx.x / 32;
+  const int64_t groups = (N + kLogitRows - 1) / kLogitRows;
+  if (wid >= groups * classes) return;
+  const int o = static_cast<int>(wid % classes);
+  const int64_t n0 = (wid / classes) * kLogitRows;
+  float acc[kLogitRows];
+#pragma unroll
+  for (int r = 0; r < kLogitRows; ++r) acc[r] = 0.f;
+  const float* wr = Wl + static_cast<int64_t>(o) * C;
+  for (int c = lane; c < C; c += 32) {
+    const float wv = wr[c];
+#pragma unroll
+    for (int r = 0; r < kLogitRows; ++r)
+      if (n0 + r < N) acc[r] += wv * gap[(n0 + r) * C + c];
+  }
+#pragma unroll
+  for (int r = 0; r < kLogitRows; ++r) {
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) acc[r] += __shfl_xor_sync(0xffffffffu, acc[r], off);
+    if (lane == 0 && n0 + r < N) logits[(n0 + r) * classes + o] = bl[o] + acc[r];
+  }
+}
+
 __global__ void k_head_loss(const float* __restrict__ gap, int64_t N, int C, const float* __restrict__ Wl,
                             const float* __restrict__ bl, int classes, const int32_t* __restrict__ labels,
                             float* __restrict__ logits, float* __restrict__ g_logits,
@@ -583,17 +654,7 @@ __global__ void k_head_loss(const float* __restrict__ gap, int64_t N, int C, con
   pdl_enter();
   __shared__ float red[256];
   const int64_t n = blockIdx.x;
-  float* lg = logits + n * classes;
-  // one warp per class: lanes stride over C (coalesced), fixed butterfly
-  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32, nwarps = blockDim.x / 32;
-  for (int o = warp; o < classes; o += nwarps) {
-    float acc = 0.f;
-    for (int c = lane; c < C; c += 32) acc += Wl[static_cast<int64_t>(o) * C + c] * gap[n * C + c];
-#pragma unroll
-    for (int off = 16; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
-    if (lane == 0) lg[o] = bl[o] + acc;
-  }
-  __syncthreads();
+  const float* lg = logits + n * classes;  // written by k_head_logits
   // max and sum of exp, fixed-order tree over the CTA
   float mx = -INFINITY;
   for (int o = threadIdx.x; o < classes; o += blockDim.x) mx = fmaxf(mx, lg[o]);
@@ -880,6 +941,12 @@ struct dpb_model {
   int64_t graph_kernels = 0;      // kernel nodes of the captured step
   int64_t eager_launches = 0;     // launches of the last eager step
   dpb::DeviceTracker tracker;     // every device allocation of the model
+  // data parallelism: per-bucket gradient allreduce on `cstream` (dpb_comm.cu)
+  dpb::Comm* comm = nullptr;
+  cudaStream_t cstream = nullptr;
+  std::vector<cudaEvent_t> ev_tdone;   // per transition: its dW (side stream) written
+  std::vector<cudaEvent_t> ev_bucket;  // per block bucket: its gradients written (main)
+  cudaEvent_t ev_cjoin = nullptr;      // every bucket reduced
   int64_t mem_tags[6] = {};       // bytes of m->mem per arena tag
 };
 
@@ -1076,6 +1143,10 @@ DPB_API void dpb_model_destroy(dpb_model* m) {
   if (m->graph) cudaGraphExecDestroy(m->graph);
   for (cudaEvent_t e : m->ev) cudaEventDestroy(e);
   if (m->side) cudaStreamDestroy(m->side);
+  for (cudaEvent_t e : m->ev_tdone) cudaEventDestroy(e);
+  for (cudaEvent_t e : m->ev_bucket) cudaEventDestroy(e);
+  if (m->ev_cjoin) cudaEventDestroy(m->ev_cjoin);
+  if (m->cstream) cudaStreamDestroy(m->cstream);
   for (auto& b : m->blocks)
     if (b.blk) destroy(b.blk);
   if (m->mem) {
@@ -1205,6 +1276,56 @@ DPB_API int dpb_model_create(const dpb_model_desc* desc, int device, void* strea
   return DPB_OK;
 }
 
+// Gradient buckets in issue order: block b's parameters together with its
+// transition's (the head's for the last block) as soon as block b's backward
+// is done, last block first; the stem joins block 0.  Registration order makes
+// every bucket one contiguous range: [poff(b), poff(b+1)).
+static void bucket_ranges(const dpb_model& m, std::vector<std::pair<int64_t, int64_t>>& out) {
+  out.clear();
+  const int nb = static_cast<int>(m.blocks.size());
+  for (int b = nb - 1; b >= 0; --b) {
+    const int64_t begin = b == 0 ? 0 : m.blocks[b].poff;
+    const int64_t end = b + 1 < nb ? m.blocks[b + 1].poff : m.params;
+    out.emplace_back(begin, end);
+  }
+}
+
+DPB_API int dpb_model_buckets(const dpb_model_desc* desc, int64_t* ranges, int max, int* count) {
+  if (!ranges || !count) return fail(DPB_CONFIG_ERROR, "null argument");
+  dpb_model m;
+  const int rc = model_geometry(desc, &m);
+  if (rc) return rc;
+  std::vector<std::pair<int64_t, int64_t>> r;
+  bucket_ranges(m, r);
+  *count = static_cast<int>(r.size());
+  for (int i = 0; i < static_cast<int>(r.size()) && i < max; ++i) {
+    ranges[2 * i] = r[i].first;
+    ranges[2 * i + 1] = r[i].second;
+  }
+  return DPB_OK;
+}
+
+DPB_API int dpb_model_set_comm(dpb_model* m, dpb_comm* comm) {
+  if (!m) return fail(DPB_CONFIG_ERROR, "null model");
+  DeviceGuard dg(m->device);
+  m->comm = reinterpret_cast<dpb::Comm*>(comm);
+  if (m->comm && !m->cstream) {
+    if (cudaStreamCreateWithFlags(&m->cstream, cudaStreamNonBlocking) != cudaSuccess)
+      return fail(DPB_CUDA_ERROR, "communication stream");
+    const size_t nb = m->blocks.size();
+    m->ev_tdone.resize(m->trans.size());
+    m->ev_bucket.resize(nb);
+    for (auto& e : m->ev_tdone) cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
+    for (auto& e : m->ev_bucket) cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
+    cudaEventCreateWithFlags(&m->ev_cjoin, cudaEventDisableTiming);
+  }
+  if (m->graph) {  // the captured step changes: capture again on the next call
+    cudaGraphExecDestroy(m->graph);
+    m->graph = nullptr;
+  }
+  return DPB_OK;
+}
+
 DPB_API int dpb_model_memory_stats(dpb_model* m, dpb_memory_stats* out) {
   if (!m || !out) return fail(DPB_CONFIG_ERROR, "null argument");
   m->tracker.snapshot(out);
@@ -1252,7 +1373,7 @@ int model_step_launch(dpb_model* m, const float* input, const int32_t* labels, c
   ModelBlock& b0 = m->blocks[0];
   if (d.stem == 1) {
     const int c0p = (d.c0 + 31) / 32 * 32;
-    launch(k_stem7_conv, dim3(blocks_of(m->M1, 128), static_cast<unsigned>(c0p / 32)), 128,
+    launch(k_stem7_conv, dim3(blocks_of(N * m->H1 * ((m->W1 + 1) / 2), 128), static_cast<unsigned>(c0p / 32)), 128,
            sizeof(float) * d.in_c * kS7Taps * c0p, st, input, N, d.in_c, d.in_h, d.in_w, m->H1, m->W1, params, d.c0,
            m->y1);
     launch_channel_partials(st, m->y1, d.c0, m->M1, d.c0, m->spart);
@@ -1291,6 +1412,9 @@ int model_step_launch(dpb_model* m, const float* input, const int32_t* labels, c
       const int HW = mb.h * mb.w;
       launch(k_head_gap, blocks_of(N * mb.C, 256), 256, 0, st, feat, mb.Cp, N, HW, mb.C, mean, var,
              params + m->head_gamma, params + m->head_beta, m->gap);
+      launch(k_head_logits, blocks_of(((N + kLogitRows - 1) / kLogitRows) * d.classes * 32, 256), 256, 0, st,
+             static_cast<const float*>(m->gap), N, mb.C, params + m->head_w, params + m->head_b, d.classes,
+             m->logits);
       launch(k_head_loss, static_cast<unsigned>(N), 256, 0, st, static_cast<const float*>(m->gap), N, mb.C,
              params + m->head_w, params + m->head_b, d.classes, labels, m->logits, m->g_logits, m->loss_n,
              m->bad_label);
@@ -1321,10 +1445,25 @@ int model_step_launch(dpb_model* m, const float* input, const int32_t* labels, c
            128, 0, st, feat, mb.Cp, mb.M, C, mean, var,
            params + m->head_gamma, params + m->head_beta, up, static_cast<const float*>(m->coef), mb.acc, mb.Cp);
   }
+  // DP: bucket b = [poff(b), poff(b+1)) (the stem joins block 0), reduced on
+  // the communication stream once its gradients exist (dpb_model_buckets)
+  const bool dp = m->comm != nullptr;
+  auto issue_bucket = [&](int b) -> int {
+    const int64_t begin = b == 0 ? 0 : m->blocks[b].poff;
+    const int64_t end = b + 1 < nb ? m->blocks[b + 1].poff : m->params;
+    cudaEventRecord(m->ev_bucket[b], st);
+    cudaStreamWaitEvent(m->cstream, m->ev_bucket[b], 0);
+    if (b + 1 < nb && m->side) cudaStreamWaitEvent(m->cstream, m->ev_tdone[b], 0);  // transition b's dW
+    return comm_allreduce_avg(m->comm, grads + begin, end - begin, m->cstream);
+  };
   for (int b = nb - 1; b >= 0; --b) {
     ModelBlock& mb = m->blocks[b];
     int rc = block_backward(mb.blk, params + mb.poff, mb.acc, grads + mb.poff, mb.Cp);
     if (rc) return rc;
+    if (dp && b > 0) {
+      rc = issue_bucket(b);
+      if (rc) return rc;
+    }
     if (b > 0) {
       ModelTrans& t = m->trans[b - 1];
       ModelBlock& pv = m->blocks[b - 1];
@@ -1343,6 +1482,7 @@ int model_step_launch(dpb_model* m, const float* input, const int32_t* labels, c
              static_cast<int>(t.Mq), static_cast<const float*>(mb.acc), mb.Cp, static_cast<const float*>(t.P), t.C,
              t.wpart, t.C, static_cast<int>(chunk));
       launch_fold_splits(ws, t.wpart, S, static_cast<int64_t>(t.cout) * t.C, grads + t.w);
+      if (dp && m->side) cudaEventRecord(m->ev_tdone[b - 1], m->side);
       if (d.dtype == DPB_BF16)
         trans_gemm<1>(st, static_cast<int>(t.Mq), t.C, t.cout, mb.acc, mb.Cp, params + t.w, t.C, t.gP, t.C);
       else
@@ -1381,21 +1521,20 @@ int model_step_launch(dpb_model* m, const float* input, const int32_t* labels, c
       const float* var = m->sstat + d.c0;
       int64_t chunk;
       const int S = splits_of(m->M1, chunk, kRowSplitsMax, 16);
-      const int ct = d.c0 < 128 ? (d.c0 + 31) / 32 * 32 : 128;
-      launch(k_stem_bnb_partials, dim3(S, blocks_of(d.c0, ct)), ct, 0, st, static_cast<const float*>(m->y1), m->M1,
+      launch(k_stem_bnb_partials, dim3(S, blocks_of(d.c0, 32)), 256, 0, st, static_cast<const float*>(m->y1), m->M1,
              m->H1, m->W1, mb.h, mb.w, d.c0, mean, var, params + m->stem_gamma, params + m->stem_beta,
              static_cast<const float*>(mb.acc), mb.Cp, static_cast<const uint8_t*>(m->arg), chunk, m->part);
       launch_finalize_bn_bwd(st, m->part, S, d.c0, static_cast<double>(m->M1), grads + m->stem_gamma,
                              grads + m->stem_beta, m->coef);
-      launch(k_stem_bnb_apply, blocks_of(m->M1 * d.c0, 256), 256, 0, st, m->y1, m->M1, m->H1, m->W1, mb.h, mb.w,
-             d.c0, mean, var, params + m->stem_gamma, params + m->stem_beta, static_cast<const float*>(mb.acc),
-             mb.Cp, static_cast<const uint8_t*>(m->arg), static_cast<const float*>(m->coef));
-      const int64_t c7 = (m->M1 + kStem7Splits - 1) / kStem7Splits;
-      const int S7 = static_cast<int>((m->M1 + c7 - 1) / c7);
+      const int ty7 = (m->H1 + kS7TH - 1) / kS7TH, tx7 = (m->W1 + kS7TW - 1) / kS7TW;
+      const int64_t ntiles = N * ty7 * tx7;
+      const int64_t per = (ntiles + kStem7Splits - 1) / kStem7Splits;
+      const int S7 = static_cast<int>((ntiles + per - 1) / per);
       const int th = (stem7_tiles(d.c0, d.in_c) + 31) / 32 * 32;
-      const int c0p4 = (d.c0 + 3) / 4 * 4, ntp = (d.in_c * kS7Taps + kS7TT - 1) / kS7TT * kS7TT;
-      launch(k_stem7_wgrad, S7, th, sizeof(float) * kS7Sub * (c0p4 + ntp), st, input, N, d.in_c, d.in_h, d.in_w,
-             m->H1, m->W1, static_cast<const float*>(m->y1), d.c0, c7, m->wpart);
+      launch(k_stem7_wgrad, S7, th, sizeof(float) * stem7_wgrad_smem_floats(d.c0, d.in_c), st, input, N, d.in_c,
+             d.in_h, d.in_w, m->H1, m->W1, static_cast<const float*>(m->y1), d.c0, mean, var,
+             params + m->stem_gamma, params + m->stem_beta, static_cast<const float*>(mb.acc), mb.Cp, mb.h, mb.w,
+             static_cast<const uint8_t*>(m->arg), static_cast<const float*>(m->coef), per, m->wpart);
       launch_fold_splits(st, m->wpart, S7, static_cast<int64_t>(d.c0) * d.in_c * kS7Taps, grads);
     } else {
       const int chunk = stem_chunk(d.c0, d.in_c);
@@ -1404,10 +1543,18 @@ int model_step_launch(dpb_model* m, const float* input, const int32_t* labels, c
              d.in_h, d.in_w, static_cast<const float*>(mb.acc), mb.Cp, d.c0, m->wpart);
       launch_fold_splits(st, m->wpart, S, static_cast<int64_t>(d.c0) * d.in_c * 9, grads);
     }
+    if (dp && b == 0) {
+      rc = issue_bucket(0);
+      if (rc) return rc;
+    }
   }
   if (m->side && !m->trans.empty()) {  // join: the caller's stream sees every gradient
     cudaEventRecord(m->ev.back(), m->side);
     cudaStreamWaitEvent(st, m->ev.back(), 0);
+  }
+  if (dp) {  // ... averaged over the ranks
+    cudaEventRecord(m->ev_cjoin, m->cstream);
+    cudaStreamWaitEvent(st, m->ev_cjoin, 0);
   }
   const cudaError_t e = cudaGetLastError();
   return e == cudaSuccess ? DPB_OK : cuda_fail(e, "model step launch");

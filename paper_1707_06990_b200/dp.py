@@ -1,4 +1,12 @@
-"""Data-parallel plumbing for the dense-block hot path.
+"""Data-parallel plumbing.
+
+The device path is native: `DpComm` wraps libdpb's NCCL communicator
+(dpb_comm_*), and a `ModelPlan` with a communicator attached averages its
+gradients inside `dpb_model_step`, one allreduce per block bucket issued on a
+communication stream as each block's backward completes (`model_buckets`
+lists them in issue order).  `GradientBuckets` is the same bucket schedule
+over torch.distributed, used for the host-side (gloo) tests and for
+dense-block-only runs.
 
 The reference is single-device; its semantics are per-device batchnorm from
 the current batch only. So a data-parallel step is: each rank
@@ -25,6 +33,9 @@ from __future__ import annotations
 
 from typing import Sequence
 
+import ctypes as C
+
+import numpy as np
 import torch
 import torch.distributed as dist
 
@@ -86,3 +97,52 @@ class GradientBuckets:
             dist.all_reduce(self.flat, group=self.group)
             self.flat.mul_(1.0 / world)
         return self.flat
+
+
+def model_buckets(cfg) -> list[tuple[int, int]]:
+    """The whole-network gradient buckets [begin, end) in the order
+    dpb_model_step reduces them (last block with the head first, ..., block 0
+    with its transition and the stem last).  They tile [0, param_elems)."""
+    from ._lib import check, lib
+    from .model import model_desc
+    d = model_desc(cfg, 1)
+    out = np.zeros(2 * 16, dtype=np.int64)
+    n = C.c_int()
+    check(lib().dpb_model_buckets(C.byref(d), C.c_void_p(out.ctypes.data), 16, C.byref(n)))
+    return [(int(out[2 * i]), int(out[2 * i + 1])) for i in range(n.value)]
+
+
+class DpComm:
+    """libdpb's NCCL communicator for this rank (dpb_comm_init).  Rank 0's
+    unique id travels over the already-initialised torch.distributed group
+    (any backend).  Attach with ModelPlan.set_comm."""
+
+    def __init__(self, rank: int, world: int, device: int, group=None):
+        from ._lib import check, lib
+        idb = np.zeros(128, dtype=np.uint8)
+        if rank == 0:
+            check(lib().dpb_comm_unique_id(C.c_void_p(idb.ctypes.data)))
+        if world > 1:
+            t = torch.from_numpy(idb)
+            if dist.get_backend(group) == "nccl":
+                t = t.cuda(device)
+            dist.broadcast(t, src=0, group=group)
+            idb = t.cpu().numpy().copy()
+        h = C.c_void_p()
+        check(lib().dpb_comm_init(world, rank, C.c_void_p(idb.ctypes.data), device, C.byref(h)))
+        self._h = h
+        self.rank, self.world = rank, world
+
+    @property
+    def handle(self):
+        return self._h
+
+    def check(self) -> None:
+        from ._lib import check, lib
+        check(lib().dpb_comm_check(self._h))
+
+    def close(self) -> None:
+        from ._lib import lib
+        if getattr(self, "_h", None) is not None and self._h.value:
+            lib().dpb_comm_destroy(self._h)
+            self._h = C.c_void_p()

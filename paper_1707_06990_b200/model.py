@@ -303,6 +303,12 @@ class ModelPlan:
     def sync(self) -> None:
         check(lib().dpb_model_sync(self._h))
 
+    def set_comm(self, comm) -> None:
+        """Attach a dp.DpComm (or None): dpb_model_step then averages the
+        gradients over the ranks, bucket by bucket, overlapped with backward."""
+        check(lib().dpb_model_set_comm(self._h, None if comm is None else comm.handle))
+        self._comm = comm  # keep the communicator alive while attached
+
     def launch_count(self) -> int:
         """Kernels one training step launches (the captured graph's kernel nodes)."""
         return int(lib().dpb_model_launch_count(self._h))

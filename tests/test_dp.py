@@ -116,3 +116,63 @@ def test_buckets_single_process_views_and_identity():
     assert torch.equal(b.finish(), b.flat)
     with pytest.raises(ValueError):
         GradientBuckets([3, 0])
+
+
+# ---- the whole-network bucket schedule of dpb_model_step (gloo, world size 2) ----
+NET = dict(blocks=(2, 2), k=4, compression=0.5, classes=10, c0=8, shape=(8, 3, 8, 8), seed=21)
+
+
+def _net_cfg():
+    from paper_1707_06990_b200.model import DenseNetConfig
+    n, c, h, w = NET["shape"]
+    return DenseNetConfig(NET["blocks"], NET["k"], True, NET["compression"], NET["classes"], NET["c0"], (c, h, w))
+
+
+def _net_shard_grads(lo, hi):
+    """The reference's training step on images [lo, hi) of the global batch."""
+    from paper_1707_06990_b200.model import init_params
+    n, c, h, w = NET["shape"]
+    x = O.rng_normal(NET["seed"] + 99, n * c * h * w, np.float32).reshape(n, c, h, w)
+    p = init_params(_net_cfg(), NET["seed"])
+    _, g, run = O.ref_model_train_step(NET["blocks"], NET["k"], NET["compression"], NET["classes"], NET["c0"],
+                                       (hi - lo, c, h, w), NET["seed"], 0, p, x[lo:hi])
+    return g, run
+
+
+def _net_worker(rank, port, out_dir):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=WORLD)
+    try:
+        from paper_1707_06990_b200.dp import model_buckets
+        g, run = _net_shard_grads(*shard_range(NET["shape"][0], rank, WORLD))
+        flat = torch.from_numpy(g.copy())
+        for begin, end in model_buckets(_net_cfg()):   # dpb_model_step's issue order
+            v = flat[begin:end]
+            dist.all_reduce(v)
+            v.mul_(1.0 / WORLD)
+        np.save(os.path.join(out_dir, f"net_{rank}.npy"), flat.numpy())
+        np.save(os.path.join(out_dir, f"netrun_{rank}.npy"), run)
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.skipif(not os.path.exists(O.REF_SO), reason="oracle/_ref not built (needs /root/reference)")
+def test_gloo_ws2_model_bucket_schedule_matches_host_average(tmp_path):
+    """Per-rank reference gradients of the whole network reduced bucket by bucket in
+    dpb_model_step's order equal the fp64 host average of the per-shard steps, and
+    the buckets cover every parameter exactly once (per-GPU BN: running stats stay
+    per rank)."""
+    from paper_1707_06990_b200.dp import model_buckets
+    from paper_1707_06990_b200.model import model_sizes
+    b = model_buckets(_net_cfg())
+    assert sorted(b)[0][0] == 0 and sorted(b)[-1][1] == model_sizes(_net_cfg())[0]
+    assert all(x[1] == y[0] for x, y in zip(sorted(b), sorted(b)[1:]))
+    mp.spawn(_net_worker, args=(_free_port(), str(tmp_path)), nprocs=WORLD, join=True)
+    shards = [_net_shard_grads(*shard_range(NET["shape"][0], r, WORLD)) for r in range(WORLD)]
+    expect = np.mean([g.astype(np.float64) for g, _ in shards], axis=0)
+    flats = [np.load(tmp_path / f"net_{r}.npy") for r in range(WORLD)]
+    np.testing.assert_array_equal(flats[0], flats[1])
+    assert np.max(np.abs(flats[0] - expect)) <= 1e-6 * max(1.0, np.max(np.abs(expect)))
+    for r in range(WORLD):
+        np.testing.assert_array_equal(np.load(tmp_path / f"netrun_{r}.npy"), shards[r][1])

@@ -15,9 +15,21 @@ running statistics and the ImageNet stem
 
 Parameters: GraphPlan::build's for the case seed (init_params, bit-identical:
 tests/test_model_host.py); input Rng(seed + 99); labels i % classes.
-Tolerances (north_star): fp32 path 1e-4, bf16 tensor-core path 2e-2, per
-tensor normwise; elementwise rel_err (dp/gradcheck.hpp:14-17) <= 1e-4 on the
-fp32 path for the fully stored cases.
+
+The yardstick is the reference run in float64 (GraphPlan<double> on the same
+float parameters and input).  The reference as shipped (float32) deviates
+from it by its own precision noise, recorded per tensor in the fixture:
+ReLU masks that flip on pre-activations within rounding of zero (each flip
+moves one pixel's gradient by O(1)), sequential float32 sums over up to 10^5
+pixels, and tensors whose exact value is 0 — the stem BN's dgamma is pure
+rounding noise because every consumer of the stem output normalises it per
+channel (its float32 "relative error" is 2e-2..6e-2 in the reference itself).
+Per tensor, the device must be within
+    max(tol, 2 x the float32 reference's own deviation)
+of float64, normwise (north_star: tol 1e-4 fp32 path, 2e-2 bf16 path), and
+the whole gradient vector within tol (normwise) — where single-pixel flips
+cannot hide a systematic error.  fp32 path elementwise: rel_err
+(dp/gradcheck.hpp:14-17) <= max(1e-4, 2 x the reference's own).
 """
 import os
 
@@ -76,6 +88,12 @@ def _segs(g):
             O.running_segments(cfg.block_sizes, cfg.growth_rate, cfg.compression, cfg.c0, stem))
 
 
+def _check_loss(g, loss, dtype):
+    ref64 = float(g["loss64"])
+    noise = abs(float(g["loss"]) - ref64)
+    assert abs(loss - ref64) <= max(TOL[dtype] * abs(ref64), 2 * noise), (loss, ref64)
+
+
 @pytest.mark.parametrize("dtype", ["fp32", "bf16"])
 @pytest.mark.parametrize("name", SMALL)
 def test_train_step_matches_reference(name, dtype):
@@ -83,18 +101,22 @@ def test_train_step_matches_reference(name, dtype):
     grads, loss, running = _run(g, dtype)
     gsegs, rsegs = _segs(g)
     assert np.isfinite(grads).all() and np.isfinite(running).all()
-    assert abs(loss - float(g["loss"])) <= TOL[dtype] * abs(float(g["loss"]))
-    for what, got, ref, segs in (("grads", grads, g["grads"], gsegs), ("running", running, g["running"], rsegs)):
-        o, worst = 0, (0.0, "")
-        for seg, size in segs:
-            a, b = got[o:o + size].astype(np.float64), ref[o:o + size].astype(np.float64)
-            err = np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-30)
-            worst = max(worst, (err, seg))
+    _check_loss(g, loss, dtype)
+    tol = TOL[dtype]
+    all_err = np.linalg.norm(grads - g["grads64"]) / np.linalg.norm(g["grads64"])
+    assert all_err <= max(tol, 2 * float(g["grads_noise_all"])), f"{name} {dtype}: whole-vector {all_err:.3e}"
+    for what, got, segs in (("grads", grads, gsegs), ("running", running, rsegs)):
+        ref, nw, el = g[what + "64"], g[what + "_noise"], g[what + "_noise_el"]
+        o = 0
+        for i, (seg, size) in enumerate(segs):
+            a, b = got[o:o + size].astype(np.float64), ref[o:o + size]
+            err = np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300)
+            assert err <= max(tol, 2 * nw[i]), f"{name} {dtype} {what} {seg}: normwise {err:.3e} (ref32 {nw[i]:.3e})"
             if dtype == "fp32":
-                assert rel_err(a, b) <= 1e-4, f"{name} {what} {seg}: elementwise rel_err {rel_err(a, b):.3e}"
+                e = rel_err(a, b)
+                assert e <= max(1e-4, 2 * el[i]), f"{name} {what} {seg}: rel_err {e:.3e} (ref32 {el[i]:.3e})"
             o += size
         assert o == got.size
-        assert worst[0] <= TOL[dtype], f"{name} {dtype} {what}: worst {worst[1]} normwise {worst[0]:.3e}"
 
 
 @pytest.mark.parametrize("dtype", ["fp32", "bf16"])
@@ -104,11 +126,18 @@ def test_train_step_matches_reference_at_scale(name, dtype):
     grads, loss, running = _run(g, dtype)
     gsegs, rsegs = _segs(g)
     assert np.isfinite(grads).all() and np.isfinite(running).all()
-    assert abs(loss - float(g["loss"])) <= TOL[dtype] * abs(float(g["loss"]))
+    _check_loss(g, loss, dtype)
+    tol = TOL[dtype]
     for what, got, segs in (("grads", grads, gsegs), ("running", running, rsegs)):
-        ref = {k[len(what) + 1:]: v for k, v in g.items() if k.startswith(what + "_")}
+        ref = {k[len(what) + 3:]: v for k, v in g.items() if k.startswith(what + "64_")}
         est, rel = O.sketch_errors(got, ref, segs)
-        i = int(np.argmax(est))
-        assert est[i] <= TOL[dtype], f"{name} {dtype} {what}: {segs[i][0]} normwise estimate {est[i]:.3e}"
+        nw = g[what + "_noise"]
+        bound = np.maximum(tol, 2 * nw)
+        i = int(np.argmax(est / bound))
+        assert est[i] <= bound[i], f"{name} {dtype} {what}: {segs[i][0]} normwise {est[i]:.3e} (ref32 {nw[i]:.3e})"
+        # whole vector: sum of per-tensor squared errors over the squared norm
+        tot = np.sqrt(np.sum((est * ref["norm"]) ** 2)) / np.sqrt(np.sum(ref["norm"] ** 2))
+        assert tot <= tol, f"{name} {dtype} {what}: whole-vector normwise estimate {tot:.3e}"
         if dtype == "fp32":
-            assert rel.max() <= 1e-4, f"{name} {what}: sampled elementwise rel_err {rel.max():.3e}"
+            assert rel.max() <= max(1e-4, 2 * float(np.max(g[what + "_noise_el"]))), \
+                f"{name} {what}: sampled rel_err {rel.max():.3e}"
