@@ -183,8 +183,7 @@ def make_train_case(name, blocks, k, comp, classes, c0, in_shape, seed, stem, fu
                 grads_noise=gn, grads_noise_el=ge, running_noise=rn, running_noise_el=re_,
                 grads_noise_all=np.linalg.norm(grads - grads64) / np.linalg.norm(grads64))
     if full:
-        np.savez_compressed(os.path.join(OUT, f"{name}.npz"), grads=grads, running=running, grads64=grads64,
-                            running64=running64, **meta)
+        np.savez_compressed(os.path.join(OUT, f"{name}.npz"), grads64=grads64, running64=running64, **meta)
         return
     sk = {}
     for tag, arr, segs in (("grads", grads, gsegs), ("grads64", grads64, gsegs), ("running", running, rsegs),

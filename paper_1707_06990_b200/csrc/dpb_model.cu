@@ -232,13 +232,9 @@ __global__ void k_stem_pool(const float* __restrict__ y, int64_t N, int H1, int 
 // Gradient w.r.t. relu(bn(y)) at conv-output pixel p, channel c: the pooled
 // gradients g0[q][c] of every window q containing p whose first maximum is p,
 // summed in window order (the order the reference-side scatter adds them).
-__device__ __forceinline__ float stem_pool_grad(int64_t p, int c, int H1, int W1, int H0, int W0, int c0,
-                                                const float* __restrict__ g0, int ld0,
-                                                const uint8_t* __restrict__ arg) {
-  const int hw1 = H1 * W1;
-  const int n = static_cast<int>(p / hw1);
-  const int r = static_cast<int>(p - static_cast<int64_t>(n) * hw1);
-  const int iy = r / W1, ix = r - (r / W1) * W1;
+__device__ __forceinline__ float stem_pool_grad_at(int n, int iy, int ix, int c, int H0, int W0, int c0,
+                                                   const float* __restrict__ g0, int ld0,
+                                                   const uint8_t* __restrict__ arg) {
   // windows q = (oy, ox) with 2*oy-1 <= iy <= 2*oy+1 (and the same in x)
   const int oy1 = min((iy + 1) / 2, H0 - 1), ox1 = min((ix + 1) / 2, W0 - 1);
   float g = 0.f;
@@ -249,6 +245,16 @@ __device__ __forceinline__ float stem_pool_grad(int64_t p, int c, int H1, int W1
       if (arg[q * c0 + c] == t) g += g0[q * ld0 + c];
     }
   return g;
+}
+__device__ __forceinline__ float stem_pool_grad(int64_t p, int c, int H1, int W1, int H0, int W0, int c0,
+                                                const float* __restrict__ g0, int ld0,
+                                                const uint8_t* __restrict__ arg) {
+  const int hw1 = H1 * W1;
+  const int pi = static_cast<int>(p);  // M1 < 2^31 (dpb_model_create)
+  const int n = pi / hw1;
+  const int r = pi - n * hw1;
+  const int iy = r / W1;
+  return stem_pool_grad_at(n, iy, r - iy * W1, c, H0, W0, c0, g0, ld0, arg);
 }
 
 // BN backward partial sums of the stem: g = relu'(bn(y)) * stem_pool_grad,
@@ -364,7 +370,7 @@ __global__ void k_stem7_wgrad(const float* __restrict__ in, int64_t N, int cin, 
         const float* tc = tab + 6 * c;
         const float mu = tc[0], inv = tc[1], ga = tc[2], be = tc[3];
         const float x = y[p * c0 + c];
-        const float g = bn_ref(x, mu, inv, ga, be) > 0.f ? stem_pool_grad(p, c, Ho, Wo, H0, W0, c0, g0, ld0, arg)
+        const float g = bn_ref(x, mu, inv, ga, be) > 0.f ? stem_pool_grad_at(n, oy, ox, c, H0, W0, c0, g0, ld0, arg)
                                                          : 0.f;
         v = ga * inv * (g - tc[4] - ((x - mu) * inv) * tc[5]);
       }
@@ -979,6 +985,7 @@ int model_geometry(const dpb_model_desc* d, dpb_model* m) {
     h = pool3_out(m->H1);
     w = pool3_out(m->W1);
     m->M1 = d->batch * m->H1 * m->W1;
+    if (m->M1 * d->c0 >= (int64_t{1} << 31)) return fail(DPB_CONFIG_ERROR, "ImageNet stem output beyond 2^31 elements");
     m->P1 = (m->M1 + 127) / 128;
     m->stem_gamma = static_cast<int64_t>(d->c0) * d->in_c * kS7Taps;
     m->stem_beta = m->stem_gamma + d->c0;
