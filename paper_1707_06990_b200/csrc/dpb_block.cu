@@ -146,6 +146,21 @@ static int64_t weight_image_bytes(const dpb_block_desc& d) {
          align_up(hp.bwd_layer_bytes * d.m, 256) + align_up(w1b, 256);
 }
 
+// Partials of the split-K 1x1 forward (tensor-core path): the widest layer's
+// ks x M x bk fp32.
+static int64_t zsplit_bytes(const dpb_block_desc& d) {
+  if (d.dtype != DPB_BF16 || !tc_supported(d)) return 0;
+  const int64_t M = d.n * d.h * d.w;
+  int64_t most = 0;
+  for (int l = 0; l < d.m; ++l) {
+    for (int ns = 1; ns <= 2; ++ns) {  // the column split the stage width may need
+      const int ks = tc2_fwd_ksplit(M, d.c0 + l * d.k, 148, ns);
+      if (ks > 1) most = std::max<int64_t>(most, ks * M * d.bk * 4);
+    }
+  }
+  return most;
+}
+
 void plan_arena(const dpb_block_desc& d, dpb_arena_sizes* s) {
   const Geometry g = geometry(d);
   std::memset(s, 0, sizeof(*s));
@@ -191,7 +206,7 @@ void plan_arena(const dpb_block_desc& d, dpb_arena_sizes* s) {
   }
   const int64_t pbytes = static_cast<int64_t>(g.Pmax) * std::max<int64_t>(g.C, d.bk) * 16;
   const int64_t scratch = align_up(pbytes, 256) + align_up(wmax * 4, 256) +
-                          align_up((4LL * d.bk + 2 * g.cmaxp) * 4, 256);
+                          align_up((4LL * d.bk + 2 * g.cmaxp) * 4, 256) + align_up(zsplit_bytes(d), 256);
   take(scratch, &s->scratch_offset, &s->scratch_bytes);
   // pre-tiled bf16 weight operands of the tensor-core path (counted as scratch)
   if (d.dtype == DPB_BF16 && tc_supported(d)) {
@@ -216,14 +231,6 @@ void plan_arena(const dpb_block_desc& d, dpb_arena_sizes* s) {
 
 template <int BM, int BN, class Op>
 static void launch_gemm(Block* b, const Op& op, dim3 grid, size_t dyn) {
-  static bool configured = false;  // per template instance
-  if (!configured) {
-    cudaFuncAttributes fa{};
-    cudaFuncGetAttributes(&fa, gemm_kernel<BM, BN, Op>);
-    cudaFuncSetAttribute(gemm_kernel<BM, BN, Op>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         227 * 1024 - static_cast<int>(fa.sharedSizeBytes));
-    configured = true;
-  }
   launch(gemm_kernel<BM, BN, Op>, grid, kThreads, dyn, b->stream, op);
 }
 
@@ -661,7 +668,9 @@ int create(const dpb_block_desc* desc, int device, void* stream, Block** out, De
   // wgrad partial region size = scratch - pbytes - coef region
   const int64_t coef_bytes = align_up((4LL * desc->bk + 2 * b->g.cmaxp) * 4, 256);
   const int64_t wt_bytes = b->tc ? weight_image_bytes(*desc) : 0;
-  b->bnb_bwd = reinterpret_cast<float*>(sc + b->sz.scratch_bytes - wt_bytes - coef_bytes);
+  const int64_t zs_bytes = align_up(zsplit_bytes(*desc), 256);
+  b->bnb_bwd = reinterpret_cast<float*>(sc + b->sz.scratch_bytes - wt_bytes - zs_bytes - coef_bytes);
+  if (zs_bytes) b->zpart = reinterpret_cast<float*>(sc + b->sz.scratch_bytes - wt_bytes - zs_bytes);
   b->bna_bwd = b->bnb_bwd + 4 * desc->bk;
   if (b->tc) {
     // the pre-tiled weight images follow the scratch partials/coefficients

@@ -95,6 +95,7 @@ struct Block {
   float* g1 = nullptr;       // [M, cmax] fp32
   double2* part = nullptr;   // per-CTA partial sums
   float* wpart = nullptr;    // split-K weight-gradient partials
+  float* zpart = nullptr;    // split-K 1x1 forward partials [ks][M][bk] (null: no split)
   float* bnb_bwd = nullptr;  // [bk][2] (x2: double-buffered across layers)
   float* bna_bwd = nullptr;  // [cmax][2]
   std::vector<int64_t> param_off, stat_off;
@@ -168,6 +169,7 @@ int64_t tc_halo_wgrad_splits(const dpb_block_desc& d);
 void tc_conv1x1_dgrad(Block* b, const LayerArgs<float>& a);
 int tc_conv1x1_wgrad(Block* b, LayerArgs<float> a);
 bool tc2_conv1x1_fwd(Block* b, const LayerArgs<float>& a, int l);
+int tc2_fwd_ksplit(int64_t M, int c, int sms, int ns);
 int64_t tc2_w1_tile_bytes(const dpb_block_desc& d, int l);
 void tc2_pretile_w1(Block* b, const float* params);
 int tc2_bwd_bn(const dpb_block_desc& d);

@@ -515,6 +515,9 @@ template <int BMN>
 struct TransGemm {
   static constexpr int BN = 128;
   static constexpr bool kSplit = true;
+  // forward conv (BMN 0): fp16x3 like every forward GEMM (split8_h); the
+  // pooled-input gradient (BMN 1) keeps bf16x3 (gradients need bf16's range)
+  static constexpr bool kF16 = BMN == 0;
   static constexpr int kAMN = 0, kBMN = BMN;
   static constexpr bool kColSums = false;
   const float* A;
@@ -546,7 +549,8 @@ struct TransGemm {
       float v[8];
       load8(A, lda, blockIdx.x * tc::kBM + row, M, k0 + kc, K, v);
       uint4 h, l;
-      tc::split8_fast(v, h, l);
+      if constexpr (kF16) tc::split8_h(v, h, l);
+      else tc::split8_fast(v, h, l);
       const uint32_t off = tc::Tile<tc::kBM>::kmajor_chunk(row, kc);
       tc::st_shared16(a_hi, off, h);
       tc::st_shared16(a_lo, off, l);
@@ -566,7 +570,8 @@ struct TransGemm {
         off = tc::Tile<BN>::mnmajor_chunk(rg, kr);
       }
       uint4 h, l;
-      tc::split8_fast(v, h, l);
+      if constexpr (kF16) tc::split8_h(v, h, l);
+      else tc::split8_fast(v, h, l);
       tc::st_shared16(b_hi, off, h);
       tc::st_shared16(b_lo, off, l);
     }
@@ -592,12 +597,6 @@ template <int BMN>
 void trans_gemm(cudaStream_t st, int M, int N, int K, const float* A, int lda, const float* B, int ldb,
                 float* D, int ldd) {
   using Op = TransGemm<BMN>;
-  static bool init = false;
-  if (!init) {
-    cudaFuncSetAttribute(tc::tc_gemm_kernel<Op>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         static_cast<int>(tc::stage_bytes<Op>()));
-    init = true;
-  }
   const Op op{A, B, D, M, N, K, lda, ldb, ldd};
   launch(tc::tc_gemm_kernel<Op>, dim3((M + tc::kBM - 1) / tc::kBM, (N + Op::BN - 1) / Op::BN), tc::kThreads,
          tc::stage_bytes<Op>(), st, op);

@@ -20,6 +20,7 @@
 
 #include <cuda.h>
 #include <cuda_bf16.h>
+#include <cuda_fp16.h>
 #include <stdint.h>
 
 #include "dpb_common.cuh"
@@ -302,10 +303,12 @@ __device__ __forceinline__ void named_sync(int id, int count) {
 // ---- descriptors -----------------------------------------------------------------
 
 // Instruction descriptor: bf16 A/B, fp32 D, M=128, N, majors (0 = K, 1 = MN).
-__host__ __device__ constexpr uint32_t make_idesc(int n, int a_mn, int b_mn) {
+// kind::f16 operand formats: BF16 (1) by default; f16 = true selects F16 (0),
+// the forward GEMMs' fp16x3 split (below).
+__host__ __device__ constexpr uint32_t make_idesc(int n, int a_mn, int b_mn, bool f16 = false) {
   return (1u << 4)                                   // D format F32
-         | (1u << 7)                                 // A format BF16
-         | (1u << 10)                                // B format BF16
+         | ((f16 ? 0u : 1u) << 7)                    // A format F16 / BF16
+         | ((f16 ? 0u : 1u) << 10)                   // B format F16 / BF16
          | (static_cast<uint32_t>(a_mn) << 15)       // A major
          | (static_cast<uint32_t>(b_mn) << 16)       // B major
          | (static_cast<uint32_t>(n >> 3) << 17)     // N >> 3
@@ -397,6 +400,31 @@ __device__ __forceinline__ void split8_fast(const float (&v)[8], uint4& hi, uint
   lo = make_uint4(l[0], l[1], l[2], l[3]);
 }
 
+// Forward-GEMM operand split (fp16x3): hi = fp16_rn(x), lo = fp16_rn(x - hi),
+// so hi + lo == x to 2^-22 relative (11 + 11 significant bits) for |x| in
+// fp16's normal range; lo in the subnormals costs at most 2^-25 absolute.
+// Products hi.hi + hi.lo + lo.hi (kind::f16, F16 operands, fp32 accumulate)
+// carry ~21 bits, against ~16 for a bf16 hi/lo split: through 264 layers the
+// forward's rounding flips ReLU masks, and each flip moves a gradient by O(1)
+// (DESIGN.md 2), so the forward's precision sets the gradients' error.  The
+// activations (BN+ReLU outputs) and weights are far inside fp16's range.
+__device__ __forceinline__ uint32_t pack_f16(float a, float b) {
+  __half2 h = __floats2half2_rn(a, b);
+  return *reinterpret_cast<uint32_t*>(&h);
+}
+__device__ __forceinline__ void split8_h(const float (&v)[8], uint4& hi, uint4& lo) {
+  uint32_t h[4], l[4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const __half2 hh = __floats2half2_rn(v[2 * i], v[2 * i + 1]);
+    const float2 f = __half22float2(hh);
+    h[i] = *reinterpret_cast<const uint32_t*>(&hh);
+    l[i] = pack_f16(v[2 * i] - f.x, v[2 * i + 1] - f.y);
+  }
+  hi = make_uint4(h[0], h[1], h[2], h[3]);
+  lo = make_uint4(l[0], l[1], l[2], l[3]);
+}
+
 __device__ __forceinline__ uint4 to_bf16x8(const float (&v)[8]) {
   return make_uint4(pack_bf16(v[0], v[1]), pack_bf16(v[2], v[3]), pack_bf16(v[4], v[5]),
                     pack_bf16(v[6], v[7]));
@@ -423,7 +451,8 @@ __device__ __forceinline__ void load8(const float* p, int n, bool aligned, float
 //
 // Op interface (all device functions, called by every thread unless noted):
 //   static constexpr int BN;            N tile (multiple of 16, <= 256)
-//   static constexpr bool kSplit;       bf16x3 hi/lo operands (forward)
+//   static constexpr bool kSplit;       hi/lo operand planes, three MMAs per K step
+//   static constexpr bool kF16;         F16 operands (the forward's fp16x3) instead of BF16
 //   static constexpr int kAMN, kBMN;    operand majors (0 K-major, 1 MN-major)
 //   int num_kb() const;                 K blocks of kBK
 //   void prologue(uint8_t* aux) const;  fill coefficient tables
@@ -473,7 +502,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(const Op op) {
   tc_fence_after();
   const uint32_t tmem = tmem_base;
 
-  constexpr uint32_t idesc = make_idesc(BN, Op::kAMN, Op::kBMN);
+  constexpr uint32_t idesc = make_idesc(BN, Op::kAMN, Op::kBMN, Op::kF16);
   const int nkb = op.num_kb();
   for (int kb = 0; kb < nkb; ++kb) {
     const int s = kb & 1;

@@ -40,6 +40,8 @@ bool make_map_f32(CUtensorMap* m, const float* base, int64_t cols, int64_t rows,
             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+constexpr int kPlanSms = 148;  // B200: the arena plan sizes the split-K partials for it
+
 static int num_sms() {
   static int n = 0;
   if (!n) {
@@ -57,14 +59,6 @@ static constexpr size_t fixed_smem() {
 
 template <class Op>
 static void launch2(Block* b, const Op& op, dim3 grid, size_t aux) {
-  static bool configured = false;
-  if (!configured) {
-    cudaFuncAttributes fa{};
-    cudaFuncGetAttributes(&fa, tc2::tc2_kernel<Op>);
-    cudaFuncSetAttribute(tc2::tc2_kernel<Op>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         227 * 1024 - static_cast<int>(fa.sharedSizeBytes));
-    configured = true;
-  }
   launch(tc2::tc2_kernel<Op>, grid, tc2::Roles<Op>::kThreads, fixed_smem<Op>() + aux, b->stream, op);
 }
 
@@ -139,6 +133,28 @@ static int fwd1x1_col_split(int bimg, int bnmax, int ntiles, int sms) {
   return best;
 }
 
+// K splits of the streamed 1x1 forward for a layer with c input channels over
+// M pixels: the split count minimising the persistent grid's makespan
+// ceil(tiles * ks / SMs) / ks, taken when it beats no split by >= 25% (the
+// partials' second pass costs a launch).  1 = no split.  DPB_FWD_NO_KSPLIT=1.
+int tc2_fwd_ksplit(int64_t M, int c, int sms, int ns) {
+  static const bool off = std::getenv("DPB_FWD_NO_KSPLIT") != nullptr;
+  if (off) return 1;
+  const int64_t nt = (M + tc::kBM - 1) / tc::kBM * ns;  // tiles before the split
+  const int nkb = (c + tc::kBK - 1) / tc::kBK;
+  int best = 1;
+  double best_t = static_cast<double>((nt + sms - 1) / sms);
+  for (int ks = 2; ks <= 8 && ks <= nkb; ++ks) {
+    const double t = static_cast<double>((nt * ks + sms - 1) / sms) / ks;
+    if (t < best_t - 1e-9) {
+      best_t = t;
+      best = ks;
+    }
+  }
+  const double t1 = static_cast<double>((nt + sms - 1) / sms);
+  return best_t <= 0.75 * t1 ? best : 1;
+}
+
 // 1x1 forward on the v2 engine; false when the shape is not supported (the
 // caller then uses the v1 kernel).
 bool tc2_conv1x1_fwd(Block* b, const LayerArgs<float>& a, int l) {
@@ -154,13 +170,27 @@ bool tc2_conv1x1_fwd(Block* b, const LayerArgs<float>& a, int l) {
     if (!make_map_f32(&op.xmap, a.feat, a.C, a.M, a.C, 32, tc::kBM)) return false;
     op.a = a;
     op.w1t = w1t;
-    if constexpr (Op::kMmaReadsRaw) {  // streamed W1: column-split small blocks
+    if constexpr (Op::kMmaReadsRaw) {  // streamed W1: split-K or column-split small blocks
       op.bimg = tc2_bn_1x1(a.bk);
-      op.ns = fwd1x1_col_split(op.bimg, Op::BN, ntiles, num_sms());
-      if (!op.ns) return false;
+      // split-K over the narrowest column split the stage width allows
+      const int ns0 = (op.bimg + Op::BN - 1) / Op::BN;
+      const bool ok0 = op.bimg % ns0 == 0 && (op.bimg / ns0) % 16 == 0;
+      const int ks = (b->zpart && ok0) ? tc2_fwd_ksplit(a.M, a.c, kPlanSms, ns0) : 1;
+      if (ks > 1) {
+        op.kper = (nkb + ks - 1) / ks;
+        op.ks = (nkb + op.kper - 1) / op.kper;  // every split holds >= 1 K block
+        op.zpart = b->zpart;
+        op.ns = ns0;
+      } else {
+        op.ns = fwd1x1_col_split(op.bimg, Op::BN, ntiles, num_sms());
+        if (!op.ns) return false;
+      }
       op.nw = op.bimg / op.ns;
     }
-    launch2(b, op, dim3(balanced_ctas(ntiles * op.ns, num_sms())), aux);
+    launch2(b, op, dim3(balanced_ctas(ntiles * op.ns * op.ks, num_sms())), aux);
+    if (op.ks > 1)
+      launch(tc2::k_zsplit_reduce, ntiles, 256, 0, b->stream, static_cast<const float*>(b->zpart), op.ks, a.M, a.bk,
+             a.z, a.part);
     return true;
   };
   // B resident in shared memory when all of W1's tiles fit, else streamed

@@ -408,21 +408,34 @@ struct Fwd1x1 {
   // column count of the pre-tiled W1 image (>= BN when the template's BN only
   // bounds the column tile, so the streamed stages fit shared memory).
   int ns = 1, nw = BN, bimg = BN;
+  // Split-K (streamed W1 only): a pixel tile's K blocks are cut into ks runs
+  // of kper blocks, one tile each, so blocks with few pixel tiles (14x14 and
+  // 7x7 at batch 64: 98 and 25) spread over the SMs without re-reading the
+  // features (the column split re-reads them per column tile).  Each run
+  // writes its fp32 partial accumulator to zpart[split][M][bk];
+  // k_zsplit_reduce sums them in split order into z and the BN_b partials.
+  int ks = 1, kper = 0;
+  float* zpart = nullptr;
 
-  __device__ int mtile(int tile) const { return tile / ns; }
-  __device__ int ncol0(int tile) const { return (tile % ns) * nw; }
+  __device__ int mtile(int tile) const { return tile / (ns * ks); }
+  __device__ int ncol0(int tile) const { return ((tile / ks) % ns) * nw; }
+  __device__ int ksplit(int tile) const { return tile % ks; }
+  __device__ int kb0(int tile) const { return ks > 1 ? ksplit(tile) * kper : 0; }
   __device__ void prefetch() const { prefetch_tmap(&xmap); }
-  __device__ int num_tiles() const { return static_cast<int>((a.M + kBM - 1) / kBM) * ns; }
-  __device__ int num_kb(int) const { return (a.c + kBK - 1) / kBK; }
+  __device__ int num_tiles() const { return static_cast<int>((a.M + kBM - 1) / kBM) * ns * ks; }
+  __device__ int num_kb(int tile) const {
+    const int nkb = (a.c + kBK - 1) / kBK;
+    return ks > 1 ? min(kper, nkb - kb0(tile)) : nkb;
+  }
   __device__ int boxes(int kb) const { return a.c - kb * kBK > 32 ? 2 : 1; }
   __device__ int epi_chunks(int) const { return nw / 8; }
   __device__ int epi_boxes(int) const { return 0; }
   __device__ void epi_tma(int, int, uint32_t, uint64_t*) const {}
   __device__ void epi_store(int, int, uint32_t) const {}
-  __device__ uint32_t raw_bytes(int, int kb) const {
-    return boxes(kb) * kBox + (RES ? 0 : 2 * nw * kBK * 2);
+  __device__ uint32_t raw_bytes(int tile, int kb) const {
+    return boxes(kb0(tile) + kb) * kBox + (RES ? 0 : 2 * nw * kBK * 2);
   }
-  __device__ uint32_t b_all() const { return static_cast<uint32_t>(num_kb(0) * 2 * kBBytes); }
+  __device__ uint32_t b_all() const { return static_cast<uint32_t>(((a.c + kBK - 1) / kBK) * 2 * kBBytes); }
   __device__ const BnAff* bn_table(const uint8_t* aux) const {
     return reinterpret_cast<const BnAff*>(aux + (RES ? b_all() : 0));
   }
@@ -438,6 +451,7 @@ struct Fwd1x1 {
   }
   __device__ void tma(int tile, int kb, uint32_t raw, uint64_t* bar) const {
     const int m0 = mtile(tile) * kBM;
+    kb += kb0(tile);  // global K block
     tma_load_2d(raw, &xmap, kb * kBK, m0, bar);
     if (boxes(kb) == 2) tma_load_2d(raw + kBox, &xmap, kb * kBK + 32, m0, bar);
     if (!RES) {
@@ -455,11 +469,12 @@ struct Fwd1x1 {
       }
     }
   }
-  __device__ void transform(int, int kb, const uint8_t* raw, uint8_t* op, const uint8_t* aux,
+  __device__ void transform(int tile, int kb, const uint8_t* raw, uint8_t* op, const uint8_t* aux,
                             int xt) const {
     const BnAff* bn = bn_table(aux);
     uint8_t* ah = op;
     uint8_t* al = op + kABytes;
+    kb += kb0(tile);  // global K block
     // every chunk of this thread covers the same 8 channels (kmajor_coords):
     // BN as one FMA per element with per-stage register coefficients
     int row0, kc;
@@ -488,7 +503,7 @@ struct Fwd1x1 {
         tc::zero8(v);
       }
       uint4 h, l;
-      tc::split8_fast(v, h, l);
+      tc::split8_h(v, h, l);  // fp16x3 forward operands (dpb_tc.cuh)
       const uint32_t off = tc::Tile<kBM>::kmajor_chunk(row, kc);
       tc::st_shared16(ah, off, h);
       tc::st_shared16(al, off, l);
@@ -497,7 +512,7 @@ struct Fwd1x1 {
   __device__ void mma(uint32_t op, uint32_t raw, uint32_t aux, uint32_t tmem, int kb) const {
     const uint32_t ah = op, al = op + kABytes;
     if (RES || (ns == 1 && bimg == BN)) {
-      constexpr uint32_t idesc = tc::make_idesc(BN, 0, 0);
+      constexpr uint32_t idesc = tc::make_idesc(BN, 0, 0, true);
       const uint32_t bh = RES ? aux + kb * 2 * kBBytes : raw + 2 * kBox, bl = bh + kBBytes;
 #pragma unroll
       for (int k16 = 0; k16 < kBK / 16; ++k16) {
@@ -508,7 +523,7 @@ struct Fwd1x1 {
       }
     } else {
       // streamed column tile: a canonical K-major tile of nw rows
-      const uint32_t idesc = tc::make_idesc(nw, 0, 0);
+      const uint32_t idesc = tc::make_idesc(nw, 0, 0, true);
       const uint32_t tb = static_cast<uint32_t>(nw) * kBK * 2;
       const uint32_t bh = raw + 2 * kBox, bl = bh + tb;
       const uint32_t k16_step = 2 * static_cast<uint32_t>(nw) * 16, lbo = static_cast<uint32_t>(nw) * 16;
@@ -528,20 +543,64 @@ struct Fwd1x1 {
     const int64_t p = static_cast<int64_t>(mtile(tile)) * kBM + row;
     const int gc = ncol0(tile) + col0;
     const int nv = p < a.M ? min(a.bk - gc, nw - col0) : 0;
+    const bool part = ks > 1;  // split-K: the partial accumulator; z and its sums come from the reduce
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
-      const bool ok = i < nv;
+      const bool ok = i < nv && !part;
       s1[i] = ok ? v[i] : 0.f;
       s2[i] = ok ? v[i] * v[i] : 0.f;
     }
-    if (nv > 0) tc::store8(a.z + p * a.bk + gc, nv, (a.bk & 3) == 0, v);
+    if (nv > 0) {
+      float* dst = part ? zpart + (static_cast<int64_t>(ksplit(tile)) * a.M + p) * a.bk + gc : a.z + p * a.bk + gc;
+      tc::store8(dst, nv, (a.bk & 3) == 0, v);
+    }
   }
   __device__ void col_sums(int tile, int c, double s1, double s2) const {
     const int gc = ncol0(tile) + c;
-    if (c < nw && gc < a.bk)
+    if (ks == 1 && c < nw && gc < a.bk)
       a.part[static_cast<int64_t>(mtile(tile)) * a.bk + gc] = make_double2(s1, s2);
   }
 };
+
+// Split-K 1x1 forward, second pass: z[m][c] = sum over splits of zpart[s][m][c]
+// in split order, and the BN_b partial sums of each 128-row tile (the
+// epilogue's col_sums layout, part[tile][c] = {sum z, sum z^2}, fp64, fixed
+// order).  CTA = one 128-row tile; 256 threads = 32 channel lanes x 8 row
+// groups (coalesced rows).
+__global__ void __launch_bounds__(256) k_zsplit_reduce(const float* __restrict__ zpart, int ks, int64_t M, int bk,
+                                                       float* __restrict__ z, double2* __restrict__ part) {
+  pdl_enter();
+  __shared__ double r1[8][33], r2[8][33];
+  const int lane = threadIdx.x % 32, grp = threadIdx.x / 32;
+  const int64_t m0 = static_cast<int64_t>(blockIdx.x) * kBM;
+  for (int cb = 0; cb < bk; cb += 32) {
+    const int c = cb + lane;
+    double s1 = 0.0, s2 = 0.0;
+    if (c < bk) {
+      for (int r = grp; r < kBM; r += 8) {
+        const int64_t m = m0 + r;
+        if (m >= M) break;
+        float v = 0.f;
+        for (int sp = 0; sp < ks; ++sp) v += zpart[(static_cast<int64_t>(sp) * M + m) * bk + c];
+        z[m * bk + c] = v;
+        s1 += v;
+        s2 += static_cast<double>(v) * v;
+      }
+    }
+    r1[grp][lane] = s1;
+    r2[grp][lane] = s2;
+    __syncthreads();
+    if (grp == 0 && c < bk) {
+      double x = 0.0, y = 0.0;
+      for (int g = 0; g < 8; ++g) {
+        x += r1[g][lane];
+        y += r2[g][lane];
+      }
+      part[static_cast<int64_t>(blockIdx.x) * bk + c] = make_double2(x, y);
+    }
+    __syncthreads();
+  }
+}
 
 // ---- 1x1 backward data: g1 = relu'(act_a) * (t1 . W1) --------------------------------
 // N (the layer's c input channels) is split into nn balanced column tiles of nw
@@ -880,7 +939,7 @@ __global__ void k_pretile_w1_all(const float* __restrict__ params, int c0, int k
     for (int i = 0; i < 8; ++i)
       v[i] = (row < bk && i0 + i < c) ? w1[static_cast<int64_t>(row) * c + i0 + i] : 0.f;
     uint4 h, lo;
-    tc::split8(v, h, lo);
+    tc::split8_h(v, h, lo);  // W1 hi | lo, fp16 (the forward's fp16x3)
     uint8_t* t = out + toff + static_cast<int64_t>(kb) * 2 * tc::Tile<BN>::kBytes;
     const uint32_t off = tc::Tile<BN>::kmajor_chunk(row, kc);
     *reinterpret_cast<uint4*>(t + off) = h;

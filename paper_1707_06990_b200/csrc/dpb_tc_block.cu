@@ -23,15 +23,6 @@ bool tc_supported(const dpb_block_desc& d) {
 
 template <class Op>
 static void launch_tc(Block* b, const Op& op, dim3 grid, size_t aux) {
-  static int max_dyn = -1;
-  if (max_dyn < 0) {
-    // opt in to the full 227 KB minus the kernel's static shared memory
-    cudaFuncAttributes fa{};
-    cudaFuncGetAttributes(&fa, tc::tc_gemm_kernel<Op>);
-    max_dyn = 227 * 1024 - static_cast<int>(fa.sharedSizeBytes);
-    cudaFuncSetAttribute(tc::tc_gemm_kernel<Op>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         max_dyn);
-  }
   const size_t smem = tc::stage_bytes<Op>() + aux;
   launch(tc::tc_gemm_kernel<Op>, grid, tc::kThreads, smem, b->stream, op);
 }
@@ -89,14 +80,6 @@ void tc_conv1x1_fwd(Block* b, const LayerArgs<float>& a) {
 // ---- 3x3 halo kernels ----------------------------------------------------------
 template <class Op>
 static void launch_halo(Block* b, const Op& op, dim3 grid, size_t stage, int nst, size_t aux) {
-  static int max_dyn = -1;
-  if (max_dyn < 0) {
-    cudaFuncAttributes fa{};
-    cudaFuncGetAttributes(&fa, tc::tc_halo_kernel<Op>);
-    max_dyn = 227 * 1024 - static_cast<int>(fa.sharedSizeBytes);
-    cudaFuncSetAttribute(tc::tc_halo_kernel<Op>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         max_dyn);
-  }
   launch(tc::tc_halo_kernel<Op>, grid, tc::kThreads, stage * nst + aux, b->stream, op);
 }
 

@@ -295,7 +295,7 @@ __global__ void k_pretile_w2_fwd(const float* __restrict__ params, int c0, int k
     for (int i = 0; i < 8; ++i)
       v[i] = (o < k && j0 + i < bk) ? w2[(static_cast<int64_t>(o) * bk + j0 + i) * 9 + tap] : 0.f;
     uint4 h, lo;
-    split8(v, h, lo);
+    split8_h(v, h, lo);  // fp16x3 forward operands (dpb_tc.cuh)
     uint8_t* t = o_l + static_cast<int64_t>(kb) * 2 * plane;
     const uint32_t off = halo_kmajor(9 * BN, row, kk);
     *reinterpret_cast<uint4*>(t + off) = h;
@@ -396,7 +396,7 @@ struct Tc3x3FwdHalo {
 #pragma unroll
       for (int e = 0; e < 8; ++e) v[i][e] = ok[i] && j0 + e < a.bk ? bn_relu(bn[j0 + e], v[i][e]) : 0.f;
       uint4 hi, lo;
-      split8(v[i], hi, lo);
+      split8_h(v[i], hi, lo);
       const uint32_t off = halo_kmajor(h.g.R, rr[i], kk[i]);
       st_shared16(xh, off, hi);
       st_shared16(xl, off, lo);
@@ -404,7 +404,7 @@ struct Tc3x3FwdHalo {
     }
   }
   __device__ void issue(uint32_t st, int kb, uint32_t tmem_base, int part) const {
-    constexpr uint32_t idesc = make_idesc(BN, 0, 0);
+    constexpr uint32_t idesc = make_idesc(BN, 0, 0, true);
     const uint32_t tmem = tmem_base + part * BN;
     const uint32_t RB = static_cast<uint32_t>(h.g.R) * 16, WB = 9u * BN * 16;
     const uint32_t xh = sdesc_lo(st, RB), xl = sdesc_lo(st + halo_bytes(), RB);
@@ -475,7 +475,7 @@ struct Tc3x3FwdTaps : Tc3x3FwdHalo<16> {
     bulk_load(st + 2 * halo_bytes(), h.wt + static_cast<int64_t>(kb) * 2 * b_bytes(), 2 * b_bytes(), bar);
   }
   __device__ void issue(uint32_t st, int kb, uint32_t tmem_base, int part) const {
-    const uint32_t idesc = make_idesc(np(), 0, 0);
+    const uint32_t idesc = make_idesc(np(), 0, 0, true);
     const uint32_t tmem = tmem_base + part * kBM;
     const uint32_t RB = static_cast<uint32_t>(h.g.R) * 16, WB = static_cast<uint32_t>(np()) * 16;
     const uint32_t xh = sdesc_lo(st, RB), xl = sdesc_lo(st + halo_bytes(), RB);
@@ -522,7 +522,7 @@ __global__ void k_pretile_w2_taps(const float* __restrict__ params, int c0, int 
     for (int i = 0; i < 8; ++i)
       v[i] = (row < 9 * k && j0 + i < bk) ? w2[(static_cast<int64_t>(o) * bk + j0 + i) * 9 + tap] : 0.f;
     uint4 hh, lo;
-    split8(v, hh, lo);
+    split8_h(v, hh, lo);
     uint8_t* t = o_l + static_cast<int64_t>(kb) * 2 * plane;
     const uint32_t off = halo_kmajor(np, row, kk);
     *reinterpret_cast<uint4*>(t + off) = hh;

@@ -61,9 +61,9 @@ __device__ __forceinline__ void bnrelu8(const BnFwd* t, int ch0, int nvalid, flo
 
 template <bool SPLIT>
 __device__ __forceinline__ void put8(uint8_t* hi, uint8_t* lo, uint32_t off, const float (&v)[8]) {
-  if constexpr (SPLIT) {
+  if constexpr (SPLIT) {  // forward operands: fp16x3 (split8_h)
     uint4 h, l;
-    split8(v, h, l);
+    split8_h(v, h, l);
     st_shared16(hi, off, h);
     st_shared16(lo, off, l);
   } else {
@@ -91,7 +91,7 @@ __device__ __forceinline__ void store8(float* p, int n, bool aligned, const floa
 template <int BN_>
 struct Tc1x1Fwd {
   static constexpr int BN = BN_;
-  static constexpr bool kSplit = true, kColSums = true;
+  static constexpr bool kSplit = true, kColSums = true, kF16 = true;
   static constexpr int kAMN = 0, kBMN = 0;
   TcArgs t;
   __device__ int num_kb() const { return (t.a.c + kBK - 1) / kBK; }
@@ -155,7 +155,7 @@ struct Tc1x1Fwd {
 template <int BN_>
 struct Tc3x3Fwd {
   static constexpr int BN = BN_;
-  static constexpr bool kSplit = true, kColSums = true;
+  static constexpr bool kSplit = true, kColSums = true, kF16 = true;
   static constexpr int kAMN = 0, kBMN = 0;
   TcArgs t;
   __device__ int num_kb() const { return (9 * t.a.bk + kBK - 1) / kBK; }
@@ -231,7 +231,7 @@ struct Tc3x3Fwd {
 template <int BN_>
 struct Tc3x3Dgrad {
   static constexpr int BN = BN_;
-  static constexpr bool kSplit = false, kColSums = true;
+  static constexpr bool kSplit = false, kColSums = true, kF16 = false;
   static constexpr int kAMN = 0, kBMN = 0;
   TcArgs t;
   __device__ int num_kb() const { return (9 * t.kp + kBK - 1) / kBK; }
@@ -313,7 +313,7 @@ struct Tc3x3Dgrad {
 template <int BN_>
 struct Tc1x1Dgrad {
   static constexpr int BN = BN_;
-  static constexpr bool kSplit = false, kColSums = true;
+  static constexpr bool kSplit = false, kColSums = true, kF16 = false;
   static constexpr int kAMN = 0, kBMN = 1;
   TcArgs t;
   __device__ int num_kb() const { return (t.a.bk + kBK - 1) / kBK; }
@@ -399,7 +399,7 @@ struct Tc1x1Dgrad {
 template <int BN_>
 struct Tc1x1Wgrad {
   static constexpr int BN = BN_;
-  static constexpr bool kSplit = false, kColSums = false;
+  static constexpr bool kSplit = false, kColSums = false, kF16 = false;
   static constexpr int kAMN = 1, kBMN = 1;
   TcArgs t;
   __device__ int64_t kbeg() const { return static_cast<int64_t>(blockIdx.z) * t.a.kchunk; }
@@ -480,7 +480,7 @@ struct Tc1x1Wgrad {
 template <int BN_>
 struct Tc3x3Wgrad {
   static constexpr int BN = BN_;
-  static constexpr bool kSplit = false, kColSums = false;
+  static constexpr bool kSplit = false, kColSums = false, kF16 = false;
   static constexpr int kAMN = 1, kBMN = 1;
   TcArgs t;
   __device__ int64_t kbeg() const { return static_cast<int64_t>(blockIdx.z) * t.a.kchunk; }

@@ -15,6 +15,7 @@ template <int BN_, int AMN, int BMN, bool SPLIT>
 struct TestGemm {
   static constexpr int BN = BN_;
   static constexpr bool kSplit = SPLIT;
+  static constexpr bool kF16 = false;  // the engine diagnostic keeps bf16 (x3) operands
   static constexpr int kAMN = AMN, kBMN = BMN;
   static constexpr bool kColSums = true;
   const float* A;  // K-major: [M][K]; MN-major: [K][M]
