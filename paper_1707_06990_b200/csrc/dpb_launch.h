@@ -37,12 +37,12 @@ inline bool pdl_enabled() {
   return on;
 }
 
-// Dynamic shared memory above 48 KB needs a per-kernel, per-DEVICE opt-in
+// Shared memory above 48 KB (static + dynamic) needs a per-kernel, per-DEVICE opt-in
 // (cudaFuncAttributeMaxDynamicSharedMemorySize).  Applied on first use of a
 // kernel on the current device, so handles on several GPUs of one process
 // each get it (the attribute does not carry across devices).
-inline void ensure_smem_optin(const void* kernel, size_t smem) {
-  if (smem <= 48 * 1024) return;
+inline void ensure_smem_optin(const void* kernel, size_t) {
+  // every kernel: static + dynamic shared memory above 48 KB needs it too
   static std::mutex mu;
   static std::unordered_set<uint64_t> done;
   int dev = 0;

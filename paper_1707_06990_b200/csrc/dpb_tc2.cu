@@ -135,16 +135,21 @@ static int fwd1x1_col_split(int bimg, int bnmax, int ntiles, int sms) {
 
 // K splits of the streamed 1x1 forward for a layer with c input channels over
 // M pixels: the split count minimising the persistent grid's makespan
-// ceil(tiles * ks / SMs) / ks, taken when it beats no split by >= 25% (the
-// partials' second pass costs a launch).  1 = no split.  DPB_FWD_NO_KSPLIT=1.
+// ceil(tiles * ks / SMs) / ks, taken when it beats no split by >= 25% and the
+// tiles fill at most a quarter of the SMs (the partials' second pass costs a
+// launch).  1 = no split.  DPB_FWD_NO_KSPLIT=1.
 int tc2_fwd_ksplit(int64_t M, int c, int sms, int ns) {
   static const bool off = std::getenv("DPB_FWD_NO_KSPLIT") != nullptr;
   if (off) return 1;
   const int64_t nt = (M + tc::kBM - 1) / tc::kBM * ns;  // tiles before the split
+  // measured: a win where the column split left the SMs starved (7x7 at batch
+  // 64: 25 pixel tiles, 58 -> ~35 us per layer with the reduce), a loss at
+  // 14x14 (98 tiles): the reduce pass costs more than the balance gains
+  if (nt * 4 > sms) return 1;
   const int nkb = (c + tc::kBK - 1) / tc::kBK;
   int best = 1;
   double best_t = static_cast<double>((nt + sms - 1) / sms);
-  for (int ks = 2; ks <= 8 && ks <= nkb; ++ks) {
+  for (int ks = 2; ks <= tc2::kMaxKSplit && ks <= nkb; ++ks) {
     const double t = static_cast<double>((nt * ks + sms - 1) / sms) / ks;
     if (t < best_t - 1e-9) {
       best_t = t;
@@ -189,8 +194,8 @@ bool tc2_conv1x1_fwd(Block* b, const LayerArgs<float>& a, int l) {
     }
     launch2(b, op, dim3(balanced_ctas(ntiles * op.ns * op.ks, num_sms())), aux);
     if (op.ks > 1)
-      launch(tc2::k_zsplit_reduce, ntiles, 256, 0, b->stream, static_cast<const float*>(b->zpart), op.ks, a.M, a.bk,
-             a.z, a.part);
+      launch(tc2::k_zsplit_reduce, dim3(ntiles, (a.bk + 31) / 32), 256, 0, b->stream,
+             static_cast<const float*>(b->zpart), op.ks, a.M, a.bk, a.z, a.part);
     return true;
   };
   // B resident in shared memory when all of W1's tiles fit, else streamed

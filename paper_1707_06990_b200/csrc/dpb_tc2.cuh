@@ -565,40 +565,49 @@ struct Fwd1x1 {
 // Split-K 1x1 forward, second pass: z[m][c] = sum over splits of zpart[s][m][c]
 // in split order, and the BN_b partial sums of each 128-row tile (the
 // epilogue's col_sums layout, part[tile][c] = {sum z, sum z^2}, fp64, fixed
-// order).  CTA = one 128-row tile; 256 threads = 32 channel lanes x 8 row
-// groups (coalesced rows).
+// order).  CTA = one 128-row tile x 32 channels (grid.y); 256 threads = 32
+// channel lanes x 8 row groups, each thread's 16 rows x ks partials loaded
+// with full unrolling (all loads in flight: this pass is L2-latency bound).
+constexpr int kMaxKSplit = 8;
 __global__ void __launch_bounds__(256) k_zsplit_reduce(const float* __restrict__ zpart, int ks, int64_t M, int bk,
                                                        float* __restrict__ z, double2* __restrict__ part) {
   pdl_enter();
   __shared__ double r1[8][33], r2[8][33];
   const int lane = threadIdx.x % 32, grp = threadIdx.x / 32;
   const int64_t m0 = static_cast<int64_t>(blockIdx.x) * kBM;
-  for (int cb = 0; cb < bk; cb += 32) {
-    const int c = cb + lane;
-    double s1 = 0.0, s2 = 0.0;
-    if (c < bk) {
-      for (int r = grp; r < kBM; r += 8) {
-        const int64_t m = m0 + r;
-        if (m >= M) break;
-        float v = 0.f;
-        for (int sp = 0; sp < ks; ++sp) v += zpart[(static_cast<int64_t>(sp) * M + m) * bk + c];
-        z[m * bk + c] = v;
-        s1 += v;
-        s2 += static_cast<double>(v) * v;
+  const int c = blockIdx.y * 32 + lane;
+  double s1 = 0.0, s2 = 0.0;
+  if (c < bk) {
+    float v[kBM / 8];
+#pragma unroll
+    for (int i = 0; i < kBM / 8; ++i) {
+      const int64_t m = m0 + grp + 8 * i;
+      float acc = 0.f;
+#pragma unroll
+      for (int sp = 0; sp < kMaxKSplit; ++sp)
+        if (sp < ks && m < M) acc += zpart[(static_cast<int64_t>(sp) * M + m) * bk + c];
+      v[i] = acc;
+    }
+#pragma unroll
+    for (int i = 0; i < kBM / 8; ++i) {
+      const int64_t m = m0 + grp + 8 * i;
+      if (m < M) {
+        z[m * bk + c] = v[i];
+        s1 += v[i];
+        s2 += static_cast<double>(v[i]) * v[i];
       }
     }
-    r1[grp][lane] = s1;
-    r2[grp][lane] = s2;
-    __syncthreads();
-    if (grp == 0 && c < bk) {
-      double x = 0.0, y = 0.0;
-      for (int g = 0; g < 8; ++g) {
-        x += r1[g][lane];
-        y += r2[g][lane];
-      }
-      part[static_cast<int64_t>(blockIdx.x) * bk + c] = make_double2(x, y);
+  }
+  r1[grp][lane] = s1;
+  r2[grp][lane] = s2;
+  __syncthreads();
+  if (grp == 0 && c < bk) {
+    double x = 0.0, y = 0.0;
+    for (int g = 0; g < 8; ++g) {
+      x += r1[g][lane];
+      y += r2[g][lane];
     }
-    __syncthreads();
+    part[static_cast<int64_t>(blockIdx.x) * bk + c] = make_double2(x, y);
   }
 }
 
