@@ -240,6 +240,20 @@ DPB_API int dpb_op_conv2d_backward(const float* grad_y, const float* x, int64_t 
                            int64_t pad, float* grad_x /* may be NULL */,
                            float* grad_w, void* stream);
 
+/* concat_forward / concat_backward (ops.hpp:53-107): input i (NCHW [n, c_i,
+ * h, w]) <-> channels [sum_{j<i} c_j, ... + c_i) of the NCHW [n, c, h, w]
+ * whole; strided device copies.  ShapeError for zero inputs, CapacityError
+ * (forward) / ShapeError (backward) when the channels do not sum to c. */
+DPB_API int dpb_op_concat_forward(int count, const float* const* inputs, const int64_t* channels, int64_t n,
+                                  int64_t h, int64_t w, float* dst, int64_t dst_c, void* stream);
+DPB_API int dpb_op_concat_backward(const float* grad_out, int64_t n, int64_t c, int64_t h, int64_t w, int count,
+                                   const int64_t* channels, float* const* grads, void* stream);
+/* relu_forward / relu_inplace (dst == x) and relu_backward(_inplace)
+ * (ops.hpp:248-287): dst = x > 0 ? x : 0; grad_x = ref > 0 ? grad_y : 0. */
+DPB_API int dpb_op_relu_forward(const float* x, int64_t count, float* dst, void* stream);
+DPB_API int dpb_op_relu_backward(const float* grad_y, const float* ref, int64_t count, float* grad_x,
+                                 void* stream);
+
 /* ---- host-side model arithmetic (densenet.hpp / peak_model.hpp) -------- */
 DPB_API int dpb_count_parameters(int nblocks, const int32_t* blocks, int32_t k,
                          int32_t bottleneck, double compression,

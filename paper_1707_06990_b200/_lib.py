@@ -84,6 +84,10 @@ SIGNATURES = {
     "dpb_predict_peak_elements": (C.c_int, [C.c_int, _P, _I32, _I32, C.c_double, _I32, _I32, _I32, _I64,
                                             _I32, _I32, _I32, _P]),
     "dpb_rng_fill_normal": (C.c_int, [C.c_uint64, _P, _I64]),
+    "dpb_op_concat_forward": (C.c_int, [C.c_int, _P, _P, _I64, _I64, _I64, _P, _I64, _P]),
+    "dpb_op_concat_backward": (C.c_int, [_P, _I64, _I64, _I64, _I64, C.c_int, _P, _P, _P]),
+    "dpb_op_relu_forward": (C.c_int, [_P, _I64, _P, _P]),
+    "dpb_op_relu_backward": (C.c_int, [_P, _P, _I64, _P, _P]),
     "dpb_model_sizes": (C.c_int, [C.POINTER(ModelDesc), C.POINTER(_I64), C.POINTER(_I64)]),
     "dpb_model_init_params": (C.c_int, [C.POINTER(ModelDesc), C.c_uint64, _P]),
     "dpb_model_create": (C.c_int, [C.POINTER(ModelDesc), C.c_int, _P, C.POINTER(_P)]),

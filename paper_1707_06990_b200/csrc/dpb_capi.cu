@@ -6,6 +6,7 @@
 #include <cmath>
 #include <cstring>
 #include <random>
+#include <string>
 #include <vector>
 
 #include "../../include/dpb.h"
@@ -24,6 +25,9 @@ int op_conv2d_forward(const float*, int64_t, int64_t, int64_t, int64_t, const fl
                       int, int, float*, cudaStream_t);
 int op_conv2d_backward(const float*, const float*, int64_t, int64_t, int64_t, int64_t,
                        const float*, int64_t, int, int, float*, float*, cudaStream_t);
+int op_relu_forward(const float*, int64_t, float*, cudaStream_t);
+int op_relu_backward(const float*, const float*, int64_t, float*, cudaStream_t);
+int op_concat(int, const float* const*, const int64_t*, int64_t, int64_t, float*, int64_t, int, cudaStream_t);
 }  // namespace dpb
 
 using dpb::Block;
@@ -271,6 +275,48 @@ int dpb_op_conv2d_backward(const float* gy, const float* x, int64_t n, int64_t c
                                            static_cast<int>(kernel), static_cast<int>(pad), gx,
                                            gw, static_cast<cudaStream_t>(stream)),
                    "conv2d_backward");
+}
+
+static int concat_check(int count, const void* parts, const int64_t* channels, int64_t n, int64_t h, int64_t w,
+                        int64_t whole_c) {
+  if (count < 1 || !parts || !channels) return fail(DPB_SHAPE_ERROR, "concat of zero inputs");  // ops.hpp:55
+  if (int rc = check_nhw(n, whole_c, h, w)) return rc;
+  int64_t total = 0;
+  for (int i = 0; i < count; ++i) {
+    if (channels[i] < 1) return fail(DPB_SHAPE_ERROR, "concat input with no channels");
+    total += channels[i];
+  }
+  if (total != whole_c)  // ops.hpp:66-69 (forward) / :94-98 (backward)
+    return fail(DPB_CAPACITY_ERROR, "concat channel sum " + std::to_string(total) + " != dst channels " +
+                                        std::to_string(whole_c));
+  return DPB_OK;
+}
+
+int dpb_op_concat_forward(int count, const float* const* inputs, const int64_t* channels, int64_t n, int64_t h,
+                          int64_t w, float* dst, int64_t dst_c, void* stream) {
+  if (int rc = concat_check(count, inputs, channels, n, h, w, dst_c)) return rc;
+  return op_status(dpb::op_concat(count, inputs, channels, n, h * w, dst, dst_c, 0,
+                                  static_cast<cudaStream_t>(stream)),
+                   "concat_forward");
+}
+int dpb_op_concat_backward(const float* grad_out, int64_t n, int64_t c, int64_t h, int64_t w, int count,
+                           const int64_t* channels, float* const* grads, void* stream) {
+  if (int rc = concat_check(count, grads, channels, n, h, w, c)) {
+    if (rc == DPB_CAPACITY_ERROR) return fail(DPB_SHAPE_ERROR, dpb::g_last_error);  // ops.hpp:94-98: ShapeError
+    return rc;
+  }
+  return op_status(dpb::op_concat(count, grads, channels, n, h * w, const_cast<float*>(grad_out), c, 1,
+                                  static_cast<cudaStream_t>(stream)),
+                   "concat_backward");
+}
+int dpb_op_relu_forward(const float* x, int64_t count, float* dst, void* stream) {
+  if (count < 0) return fail(DPB_SHAPE_ERROR, "negative element count");
+  return op_status(dpb::op_relu_forward(x, count, dst, static_cast<cudaStream_t>(stream)), "relu_forward");
+}
+int dpb_op_relu_backward(const float* grad_y, const float* ref, int64_t count, float* grad_x, void* stream) {
+  if (count < 0) return fail(DPB_SHAPE_ERROR, "negative element count");
+  return op_status(dpb::op_relu_backward(grad_y, ref, count, grad_x, static_cast<cudaStream_t>(stream)),
+                   "relu_backward");
 }
 
 // --- host-side model arithmetic ----------------------------------------------------

@@ -172,7 +172,54 @@ op_conv2d_wgrad(const float* __restrict__ gy, const float* __restrict__ x, int64
   if (threadIdx.x == 0) gw[widx] = static_cast<float>(s);
 }
 
+// relu_forward / relu_inplace, ops.hpp:248-264 (v > 0 ? v : 0; dst may be x).
+__global__ void op_relu_forward(const float* x, int64_t count, float* dst) {
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i < count) {
+    const float v = x[i];
+    dst[i] = v > 0.f ? v : 0.f;
+  }
+}
+
+// relu_backward(_inplace), ops.hpp:268-287: grad_x = ref > 0 ? grad_y : 0
+// (subgradient 0 at 0; ref may be the ReLU input or output).
+__global__ void op_relu_backward(const float* gy, const float* __restrict__ ref, int64_t count, float* gx) {
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i < count) gx[i] = ref[i] > 0.f ? gy[i] : 0.f;
+}
+
 static unsigned nblk(int64_t n) { return static_cast<unsigned>((n + 255) / 256); }
+
+int op_relu_forward(const float* x, int64_t count, float* dst, cudaStream_t st) {
+  if (count > 0) op_relu_forward<<<nblk(count), 256, 0, st>>>(x, count, dst);
+  return cudaGetLastError();
+}
+int op_relu_backward(const float* gy, const float* ref, int64_t count, float* gx, cudaStream_t st) {
+  if (count > 0) op_relu_backward<<<nblk(count), 256, 0, st>>>(gy, ref, count, gx);
+  return cudaGetLastError();
+}
+
+// concat_forward / concat_backward, ops.hpp:53-107: per sample, input i's
+// c_i*h*w contiguous values go to channels [off_i, off_i + c_i) of the NCHW
+// destination (copy_into, tensor.hpp:168-180) — strided device copies, no
+// arithmetic.  backward copies the channel slices back out.
+int op_concat(int count, const float* const* parts, const int64_t* channels, int64_t n, int64_t hw, float* whole,
+              int64_t whole_c, int backward, cudaStream_t st) {
+  int64_t off = 0;
+  for (int i = 0; i < count; ++i) {
+    const size_t run = static_cast<size_t>(channels[i] * hw) * sizeof(float);
+    float* slot = whole + off * hw;
+    const size_t wp = static_cast<size_t>(whole_c * hw) * sizeof(float);
+    const cudaError_t e =
+        backward ? cudaMemcpy2DAsync(const_cast<float*>(parts[i]), run, slot, wp, run, static_cast<size_t>(n),
+                                     cudaMemcpyDeviceToDevice, st)
+                 : cudaMemcpy2DAsync(slot, wp, parts[i], run, run, static_cast<size_t>(n), cudaMemcpyDeviceToDevice,
+                                     st);
+    if (e != cudaSuccess) return e;
+    off += channels[i];
+  }
+  return cudaSuccess;
+}
 
 int op_batch_statistics(const float* x, int64_t n, int64_t c, int64_t h, int64_t w,
                         float* mean, float* var, cudaStream_t st) {

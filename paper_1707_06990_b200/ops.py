@@ -108,3 +108,49 @@ def lr_at(kind: str, base_lr: float, total_epochs: int, epoch: int, milestones=(
                           C.cast(arr, C.c_void_p), len(milestones), float(factor), float(floor), int(epoch),
                           C.byref(out)))
     return out.value
+
+
+def concat_forward(inputs: list) -> torch.Tensor:
+    """concat_forward (ops.hpp:53-88): NCHW inputs sharing (n, h, w) -> their
+    channel concatenation (a new tensor)."""
+    if not inputs:
+        raise errors.ShapeError("concat of zero inputs")
+    n, _, h, w = inputs[0].shape
+    for t in inputs:
+        if t.shape[0] != n or t.shape[2] != h or t.shape[3] != w:
+            raise errors.ShapeError(f"concat input {tuple(t.shape)} incompatible")
+    chans = [int(t.shape[1]) for t in inputs]
+    dst = torch.empty((n, sum(chans), h, w), device=inputs[0].device)
+    ptrs = (C.c_void_p * len(inputs))(*[t.data_ptr() for t in inputs])
+    ch = (C.c_int64 * len(inputs))(*chans)
+    check(lib().dpb_op_concat_forward(len(inputs), C.cast(ptrs, C.c_void_p), C.cast(ch, C.c_void_p), n, h, w,
+                                      _ptr(dst), dst.shape[1], _stream()))
+    return dst
+
+
+def concat_backward(grad_out: torch.Tensor, splits: list) -> list:
+    """concat_backward (ops.hpp:91-107): the gradient's channel slices as
+    separate tensors (copies; the reference returns views)."""
+    n, c, h, w = grad_out.shape
+    outs = [torch.empty((n, int(s), h, w), device=grad_out.device) for s in splits]
+    ptrs = (C.c_void_p * len(outs))(*[t.data_ptr() for t in outs])
+    ch = (C.c_int64 * max(1, len(outs)))(*[int(s) for s in splits])
+    check(lib().dpb_op_concat_backward(_ptr(grad_out), n, c, h, w, len(outs), C.cast(ch, C.c_void_p),
+                                       C.cast(ptrs, C.c_void_p), _stream()))
+    return outs
+
+
+def relu_forward(x: torch.Tensor, inplace: bool = False) -> torch.Tensor:
+    """relu_forward / relu_inplace (ops.hpp:248-264)."""
+    dst = x if inplace else torch.empty_like(x)
+    check(lib().dpb_op_relu_forward(_ptr(x), x.numel(), _ptr(dst), _stream()))
+    return dst
+
+
+def relu_backward(grad_y: torch.Tensor, ref: torch.Tensor, inplace: bool = False) -> torch.Tensor:
+    """relu_backward(_inplace) (ops.hpp:268-287): grad_y where ref > 0, else 0."""
+    if grad_y.shape != ref.shape:
+        raise errors.ShapeError("relu_backward shape mismatch")
+    gx = grad_y if inplace else torch.empty_like(grad_y)
+    check(lib().dpb_op_relu_backward(_ptr(grad_y), _ptr(ref), grad_y.numel(), _ptr(gx), _stream()))
+    return gx

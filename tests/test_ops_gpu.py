@@ -102,3 +102,34 @@ def test_batchnorm_backward_identities():
         assert abs(gx.cpu().numpy()[idx] - num[idx]) < 1e-3
     gx0, dg0, db0 = ops.batchnorm_backward(torch.zeros_like(T(x)), T(x), T(gam), m, v)
     assert torch.count_nonzero(gx0).item() == 0 and torch.count_nonzero(db0).item() == 0
+
+
+def test_concat_forward_backward_order_and_errors():
+    # t/ops_test.cpp:42-106: inputs land in order, channel by channel
+    a = torch.randn(2, 3, 4, 5, device="cuda")
+    b = torch.randn(2, 1, 4, 5, device="cuda")
+    c = torch.randn(2, 4, 4, 5, device="cuda")
+    out = ops.concat_forward([a, b, c])
+    assert torch.equal(out, torch.cat([a, b, c], dim=1))
+    parts = ops.concat_backward(out, [3, 1, 4])
+    for p, ref in zip(parts, (a, b, c)):
+        assert torch.equal(p, ref)
+    with pytest.raises(errors.ShapeError):
+        ops.concat_forward([])
+    with pytest.raises(errors.ShapeError):
+        ops.concat_forward([a, torch.randn(2, 1, 3, 5, device="cuda")])
+    with pytest.raises(errors.ShapeError):
+        ops.concat_backward(out, [3, 1, 3])
+
+
+def test_relu_forward_backward_subgradient_zero():
+    # t/ops_test.cpp:241-265: subgradient 0 at 0, in-place variants
+    x = torch.tensor([-2.0, -0.0, 0.0, 1e-30, 3.0], device="cuda")
+    y = ops.relu_forward(x)
+    assert y.tolist() == [0.0, 0.0, 0.0, 1e-30, 3.0]
+    g = torch.ones_like(x)
+    assert ops.relu_backward(g, x).tolist() == [0.0, 0.0, 0.0, 1.0, 1.0]
+    assert ops.relu_backward(g, y).tolist() == [0.0, 0.0, 0.0, 1.0, 1.0]
+    z = x.clone()
+    ops.relu_forward(z, inplace=True)
+    assert torch.equal(z, y)
