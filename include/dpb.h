@@ -186,6 +186,14 @@ DPB_API int dpb_block_read_stats(dpb_block* blk, float* dst /* flat stats layout
 
 DPB_API int dpb_sync(dpb_block* blk);
 DPB_API int dpb_block_memory_stats(dpb_block* blk, dpb_memory_stats* out);
+/* OpTrace of the last forward + backward (alloctrace.hpp:132-201, FLOP
+ * conventions ops.hpp:565-595): counts[3 * node + {0 forward, 1 backward,
+ * 2 recompute}] for nodes 7l + {concat, bn_a, relu_a, conv_a, bn_b, relu_b,
+ * conv_b} and 7m (block-output concat); flops[7 * {0,1,2} + OpKind] with
+ * OpKind concat 0, batchnorm 1, relu 2, conv 3.  The concat is a zero-copy
+ * view (no moves, 0 FLOPs); act_a and act_b are recomputed twice per layer
+ * (dgrad mask and wgrad operand), inside the kernels' prologues. */
+DPB_API int dpb_block_trace(dpb_block* blk, int32_t* counts, int max_nodes, double* flops, int* nodes);
 
 /* Number of kernels the last forward/backward launched (bench accounting). */
 DPB_API int64_t dpb_block_launch_count(dpb_block* blk);

@@ -98,6 +98,9 @@ def kats():
     for name, (k, c0) in {"d264k32@56": (32, 64), "d264k48@56": (48, 96)}.items():
         p, _ = O.ref_model_params([6, 12, 64, 48], k, 1, 0.5, 1000, c0, (1, 3, 56, 56), 7)
         d["params_sha256_seed7"][name] = hashlib.sha256(p.tobytes()).hexdigest()
+    # the reference's OpTrace of a single-block network (tests/test_trace*.py)
+    counts, flops = O.ref_single_block_trace(3, 4, 8, 2, 5, 6, strategy=2)
+    d["block_trace_m3k4c8_n2h5w6"] = {"counts": counts.tolist(), "flops": flops.tolist()}
     return d
 
 

@@ -474,6 +474,50 @@ def sketch_errors(got: np.ndarray, ref_sketch: dict, segs):
     return est, rel
 
 
+def ref_single_block_trace(m, k, c0, n, h, w, seed=5, strategy=2):
+    """The reference's OpTrace of one GraphPlan<double> step of the single-block
+    network blocks={m} (4 classes): (counts [nodes, 3] = forward, backward,
+    recompute; flops [3, 7] = forward / backward / recompute per OpKind)."""
+    L = ref_lib()
+    f = L.ref_single_block_trace
+    f.restype = C.c_int
+    f.argtypes = [C.c_int] * 6 + [C.c_uint64, C.c_int, _P, C.c_int, _P, C.POINTER(C.c_int)]
+    counts = np.zeros(3 * 4096, dtype=np.int32)
+    flops = np.zeros(21, dtype=np.float64)
+    nn = C.c_int()
+    rc = f(m, k, c0, n, h, w, seed, strategy, _ptr(counts), 4096, _ptr(flops), C.byref(nn))
+    if rc != 0:
+        raise RuntimeError(L.ref_last_error().decode())
+    return counts[:3 * nn.value].reshape(-1, 3), flops.reshape(3, 7)
+
+
+def block_trace_flops(s: "BlockShape"):
+    """Per-kind FLOPs of one dense block under the reference's conventions
+    (ops.hpp:565-595): forward / backward / one rematerialisation per layer
+    (concat, bn_a, relu_a over c channels; bn_b, relu_b over bk), as
+    GraphPlan::forward_layer / backward_layer / rematerialize count them."""
+    M = s.n * s.h * s.w
+    fwd = np.zeros(7)
+    bwd = np.zeros(7)
+    rem = np.zeros(7)
+    for l in range(s.m):
+        c = s.c_in(l)
+        f1, f3 = 2.0 * M * s.bk * c, 2.0 * M * s.k * 9 * s.bk
+        fwd[0] += M * c
+        fwd[1] += 8.0 * M * (c + s.bk)
+        fwd[2] += M * (c + s.bk)
+        fwd[3] += f1 + f3
+        bwd[0] += M * c
+        bwd[1] += 12.0 * M * (c + s.bk)
+        bwd[2] += M * (c + s.bk)
+        bwd[3] += 2.0 * (f1 + f3)
+        rem[0] += M * c
+        rem[1] += 8.0 * M * (c + s.bk)
+        rem[2] += M * (c + s.bk)
+    fwd[0] += M * s.c_out  # block-output concat
+    return fwd, bwd, rem
+
+
 def ref_model_train_step(blocks, k, compression, classes, c0, in_shape, seed, stem=0, params=None, x=None,
                          dtype=np.float32):
     """One reference training step through GraphPlan<T>'s public forward /

@@ -719,6 +719,34 @@ void model_train_step(int nblocks, const int* blocks, int k, double compression,
 
 }  // namespace
 
+// OpTrace of one GraphPlan<double> step (alloctrace.hpp:132-201) of the
+// single-block network blocks={m} (single_block_cfg, 4 classes), strategy
+// 0 naive / 1 shared-gradient / 2 shared-all: per-node {forward, backward,
+// recompute} counts and per-OpKind FLOPs {forward, backward, recompute}.
+extern "C" int ref_single_block_trace(int m, int k, int c0, int n, int h, int w, std::uint64_t seed, int strategy,
+                                      int32_t* counts, int max_nodes, double* flops, int* nodes) {
+  return guarded([&] {
+    const DenseNetConfig cfg = single_block_cfg(m, k, c0, 4);
+    const Shape4 in{n, 3, h, w};
+    MemoryTracker data_tr;
+    Tensor<double> input = make_input<double>(in, seed + 99, data_tr);
+    GraphPlan<double> plan = GraphPlan<double>::build(cfg, static_cast<ExecutionStrategy>(strategy), in, seed);
+    const StepResult<double> r = plan.step_trace(input, make_labels(n, 4));
+    *nodes = static_cast<int>(r.trace.node_count());
+    for (int i = 0; i < *nodes && i < max_nodes; ++i) {
+      const OpTrace::NodeCounts& c = r.trace.node(i);
+      counts[3 * i] = c.forward;
+      counts[3 * i + 1] = c.backward;
+      counts[3 * i + 2] = c.recompute;
+    }
+    for (int kk = 0; kk < kOpKindCount; ++kk) {
+      flops[kk] = r.trace.forward_flops(static_cast<OpKind>(kk));
+      flops[7 + kk] = r.trace.backward_flops(static_cast<OpKind>(kk));
+      flops[14 + kk] = r.trace.recompute_flops(static_cast<OpKind>(kk));
+    }
+  });
+}
+
 #define DEFINE_TRAIN_STEP(SUF, T)                                                                               \
   extern "C" int ref_model_train_step_##SUF(int nblocks, const int* blocks, int k, double compression,         \
                                             int classes, int c0, int stem, int in_c, int in_h, int in_w,        \

@@ -103,6 +103,7 @@ SIGNATURES = {
     "dpb_comm_check": (C.c_int, [_P]),
     "dpb_model_launch_count": (_I64, [_P]),
     "dpb_block_memory_stats": (C.c_int, [_P, C.POINTER(MemoryStats)]),
+    "dpb_block_trace": (C.c_int, [_P, _P, C.c_int, _P, C.POINTER(C.c_int)]),
     "dpb_sgd_step": (C.c_int, [_P, _P, _P, _I64, C.c_double, C.c_double, C.c_double, C.c_int, _P]),
     "dpb_lr_at": (C.c_int, [C.c_int, C.c_double, C.c_int, _P, C.c_int, C.c_double, C.c_double, C.c_int,
                             C.POINTER(C.c_double)]),

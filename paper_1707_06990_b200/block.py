@@ -188,6 +188,22 @@ class BlockPlan:
                                        "bytes_8d": float(arr[i].bytes_8d)}
                 for i in range(n.value)}
 
+    def trace(self) -> dict:
+        """OpTrace of the last forward + backward (dpb_block_trace): per-node
+        {forward, backward, recompute} counts and per-kind FLOPs."""
+        import numpy as np
+        n = C.c_int()
+        check(lib().dpb_block_trace(self._h, None, 0, None, C.byref(n)))
+        counts = np.zeros(3 * n.value, dtype=np.int32)
+        flops = np.zeros(21, dtype=np.float64)
+        check(lib().dpb_block_trace(self._h, C.c_void_p(counts.ctypes.data), n.value,
+                                    C.c_void_p(flops.ctypes.data), C.byref(n)))
+        kinds = ["concat", "batchnorm", "relu", "conv", "pool", "linear", "loss"]
+        f = flops.reshape(3, 7)
+        return {"nodes": counts.reshape(-1, 3),
+                "forward_flops": dict(zip(kinds, f[0])), "backward_flops": dict(zip(kinds, f[1])),
+                "recompute_flops": dict(zip(kinds, f[2]))}
+
     # -- read-back in the reference layout -------------------------------------
 
     def feats(self) -> torch.Tensor:

@@ -331,6 +331,8 @@ static void forward_impl(Block* b, const float* x_in, const float* params, float
   const double count = M;
   float* fmean = b->fstat;
   float* fvar = b->fstat + g.Cp;
+  BlockTrace& tr = b->trace;
+  tr.reset(7 * d.m + 1);
   if (!eval) {
     {
       LaunchScope ls(b, KC_STATS, M * d.c0 * Sb, 0, M * d.c0 * 2.0);
@@ -351,6 +353,15 @@ static void forward_impl(Block* b, const float* x_in, const float* params, float
       a.bmean = r + 2 * a.c;
       a.bvar = r + 2 * a.c + d.bk;
     }
+    // trace (ops.hpp:565-595 conventions): the concat is a zero-copy channel
+    // prefix (no moves: 0 FLOPs); BN_a + ReLU run in the 1x1 forward's transform
+    tr.on(0, 7 * l + 0, BlockTrace::kConcat, 0.0);
+    tr.on(0, 7 * l + 1, BlockTrace::kBatchNorm, 8.0 * M * a.c);
+    tr.on(0, 7 * l + 2, BlockTrace::kRelu, M * a.c);
+    tr.on(0, 7 * l + 3, BlockTrace::kConv, 2.0 * M * d.bk * a.c);
+    tr.on(0, 7 * l + 4, BlockTrace::kBatchNorm, 8.0 * M * d.bk);
+    tr.on(0, 7 * l + 5, BlockTrace::kRelu, M * d.bk);
+    tr.on(0, 7 * l + 6, BlockTrace::kConv, 2.0 * M * d.k * 9.0 * d.bk);
     {
       LaunchScope ls(b, KC_C1_FWD, M * (a.c + d.bk) * Sb, 2.0 * M * a.c * d.bk, M * (a.c + d.bk) * 2.0);
       if (b->tc) {
@@ -376,6 +387,7 @@ static void forward_impl(Block* b, const float* x_in, const float* params, float
           b->part, p3, d.k, count, fmean, fvar, a.c);
     }
   }
+  tr.on(0, 7 * d.m, BlockTrace::kConcat, 0.0);  // block-output concat: the feature buffer itself
   if (!eval && update_running) {
     LaunchScope ls(b, KC_RUNNING, 0, 0, 0);
     launch(k_running_update, blocks_for(b->sz.stat_elems, 256), 256, 0, b->stream, 
@@ -428,6 +440,29 @@ static void backward_impl(Block* b, const float* params, float* grad_acc, float*
     float* d_bb = d_gb + d.bk;
     float* d_w2 = d_bb + d.bk;
     const double f3 = 2.0 * M * 9 * d.bk * d.k, f1 = 2.0 * M * a.c * d.bk;
+    {
+      // trace: the 3x3 dgrad prologue and the 3x3 wgrad each recompute act_b =
+      // relu(bn_b(z)) (the mask, the operand); the 1x1 dgrad epilogue and the
+      // 1x1 wgrad each recompute act_a (mask, operand) from the feature prefix
+      // (graph.hpp:856-945 does it once, into Shared1/Shared2); conv backward
+      // = dgrad + wgrad at 2x the forward FLOPs; the accumulate is the concat
+      // backward (one add per element)
+      BlockTrace& tr = b->trace;
+      const double Mc = M * a.c, Mb = M * d.bk;
+      for (int rep = 0; rep < 2; ++rep) {
+        tr.on(2, 7 * l + 4, BlockTrace::kBatchNorm, 8.0 * Mb);
+        tr.on(2, 7 * l + 5, BlockTrace::kRelu, Mb);
+        tr.on(2, 7 * l + 1, BlockTrace::kBatchNorm, 8.0 * Mc);
+        tr.on(2, 7 * l + 2, BlockTrace::kRelu, Mc);
+      }
+      tr.on(1, 7 * l + 6, BlockTrace::kConv, 2.0 * f3);
+      tr.on(1, 7 * l + 5, BlockTrace::kRelu, Mb);
+      tr.on(1, 7 * l + 4, BlockTrace::kBatchNorm, 12.0 * Mb);
+      tr.on(1, 7 * l + 3, BlockTrace::kConv, 2.0 * f1);
+      tr.on(1, 7 * l + 2, BlockTrace::kRelu, Mc);
+      tr.on(1, 7 * l + 1, BlockTrace::kBatchNorm, 12.0 * Mc);
+      tr.on(1, 7 * l + 0, BlockTrace::kConcat, Mc);
+    }
     if (fork) {
       if (l + 2 < d.m) cudaStreamWaitEvent(main_st, ev(l + 2, 2), 0);  // buffers of parity l
       cudaEventRecord(ev(l, 0), main_st);

@@ -182,6 +182,19 @@ int dpb_sync(dpb_block* blk) {
 
 int64_t dpb_block_launch_count(dpb_block* blk) { return blk ? B(blk)->launches : -1; }
 
+int dpb_block_trace(dpb_block* blk, int32_t* counts, int max_nodes, double* flops, int* nodes) {
+  if (!blk || !nodes) return fail(DPB_CONFIG_ERROR, "null argument");
+  const dpb::BlockTrace& t = B(blk)->trace;
+  const int n = static_cast<int>(t.counts.size() / 3);
+  *nodes = n;
+  if (counts)
+    for (int i = 0; i < 3 * n && i < 3 * max_nodes; ++i) counts[i] = t.counts[static_cast<size_t>(i)];
+  if (flops)
+    for (int w = 0; w < 3; ++w)
+      for (int k = 0; k < dpb::BlockTrace::kKinds; ++k) flops[w * dpb::BlockTrace::kKinds + k] = t.flops[w][k];
+  return DPB_OK;
+}
+
 int dpb_block_memory_stats(dpb_block* blk, dpb_memory_stats* out) {
   if (!blk || !out) return fail(DPB_CONFIG_ERROR, "null argument");
   B(blk)->tracker->snapshot(out);

@@ -40,6 +40,26 @@ struct DeviceTracker {
   }
 };
 
+// OpTrace of the block (alloctrace.hpp:132-201): per-node forward / backward /
+// recompute counts and per-OpKind FLOPs with the reference's conventions
+// (ops.hpp:565-595), recorded by the host as the fused kernels run.  Nodes
+// per layer l: 7l + {0 concat, 1 bn_a, 2 relu_a, 3 conv_a, 4 bn_b, 5 relu_b,
+// 6 conv_b}; node 7m is the block-output concat.
+struct BlockTrace {
+  enum Kind { kConcat = 0, kBatchNorm = 1, kRelu = 2, kConv = 3, kKinds = 7 };
+  std::vector<int32_t> counts;  // 3 per node: forward, backward, recompute
+  double flops[3][kKinds] = {};
+  void reset(int nodes) {
+    counts.assign(3 * static_cast<size_t>(nodes), 0);
+    for (auto& r : flops)
+      for (double& f : r) f = 0.0;
+  }
+  void on(int what, int node, int kind, double f) {  // what: 0 fwd, 1 bwd, 2 recompute
+    counts[3 * static_cast<size_t>(node) + what]++;
+    flops[what][kind] += f;
+  }
+};
+
 struct Geometry {
   int64_t M = 0;     // pixels N*H*W
   int64_t C = 0;     // block output channels c0 + m*k
@@ -110,6 +130,7 @@ struct Block {
   bool fwd_done = false;
   int64_t launches = 0;
   bool prof = false;
+  BlockTrace trace;                   // OpTrace of the last forward + backward
   std::vector<ProfRec> recs;          // recorded launches (profiling on)
   std::vector<cudaEvent_t> ev_pool;   // reusable events
   size_t ev_used = 0;
