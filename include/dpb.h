@@ -112,7 +112,7 @@ typedef struct dpb_arena_sizes {
   /* SharedGrad: block accumulator + two transient slots */
   int64_t acc_offset, acc_bytes;     /* [M, c_out] fp32                          */
   int64_t g0_offset, g0_bytes;       /* [M, bk]   fp32 masked 3x3 dgrad          */
-  int64_t g1_offset, g1_bytes;       /* [M, c_max] fp32 masked 1x1 dgrad         */
+  int64_t g1_offset, g1_bytes;       /* 2 x [M, c_max] fp32 masked 1x1 dgrad (layer parity) */
   /* Scratch: reduction partials, GEMM-layout weight copies */
   int64_t scratch_offset, scratch_bytes;
   /* Shared1/Shared2 of the reference are 0: concat is a zero-copy channel

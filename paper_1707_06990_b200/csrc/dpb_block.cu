@@ -175,7 +175,9 @@ void plan_arena(const dpb_block_desc& d, dpb_arena_sizes* s) {
   take((2 * g.Cp + 2LL * d.m * d.bk) * 4, &s->stats_offset, &s->stats_bytes);
   take(d.layout == DPB_NCHW ? g.M * g.Cp * 4 : 0, &s->acc_offset, &s->acc_bytes);
   take(2 * g.M * d.bk * 4, &s->g0_offset, &s->g0_bytes);
-  take(g.M * g.cmaxp * 4, &s->g1_offset, &s->g1_bytes);
+  // g1 double-buffered by layer parity: the tail of layer l's accumulate
+  // overlaps layer l-1's dgrads (split_apply)
+  take(2 * g.M * g.cmaxp * 4, &s->g1_offset, &s->g1_bytes);
   // scratch: partials | wgrad partials | BN-backward coefficients
   int64_t wmax = 0;
   for (int l = 0; l < d.m; ++l) {
@@ -206,7 +208,7 @@ void plan_arena(const dpb_block_desc& d, dpb_arena_sizes* s) {
   }
   const int64_t pbytes = static_cast<int64_t>(g.Pmax) * std::max<int64_t>(g.C, d.bk) * 16;
   const int64_t scratch = align_up(pbytes, 256) + align_up(wmax * 4, 256) +
-                          align_up((4LL * d.bk + 2 * g.cmaxp) * 4, 256) + align_up(zsplit_bytes(d), 256);
+                          align_up((4LL * d.bk + 4 * g.cmaxp) * 4, 256) + align_up(zsplit_bytes(d), 256);
   take(scratch, &s->scratch_offset, &s->scratch_bytes);
   // pre-tiled bf16 weight operands of the tensor-core path (counted as scratch)
   if (d.dtype == DPB_BF16 && tc_supported(d)) {
@@ -294,7 +296,7 @@ static LayerArgs<S> layer_args(Block* b, const float* params, int l) {
   a.bvar = a.bmean + d.bk;
   a.acc = b->acc_cur;
   a.g0 = b->g0;
-  a.g1 = b->g1;
+  a.g1 = b->g1 + (l & 1) * g.M * g.cmaxp;  // parity buffer
   a.bnb_bwd = b->bnb_bwd;
   a.part = b->part;
   a.wpart = b->wpart;
@@ -428,6 +430,10 @@ static void backward_impl(Block* b, const float* params, float* grad_acc, float*
   const bool fork = b->side != nullptr && !b->prof && !no_fork;
   cudaStream_t main_st = b->stream;
   auto ev = [&](int l, int which) { return b->fork_ev[3 * l + which]; };
+  // split_apply: the accumulate's tail on side2 (DPB_NO_SPLIT_APPLY=1: off)
+  static const bool no_split = std::getenv("DPB_NO_SPLIT_APPLY") != nullptr;
+  const bool split = fork && b->side2 != nullptr && !no_split && d.k % 4 == 0 && d.c0 % 4 == 0 && d.m > 1;
+  auto aev = [&](int l, int which) { return b->apply_ev[2 * l + which]; };
   for (int l = d.m - 1; l >= 0; --l) {
     LayerArgs<S> a = layer_args<S>(b, params, l);
     a.g0 = b->g0 + (l & 1) * g.M * d.bk;
@@ -533,6 +539,8 @@ static void backward_impl(Block* b, const float* params, float* grad_acc, float*
     }
     if (fork) cudaEventRecord(ev(l, 2), b->side);
     b->stream = main_st;
+    // the tail accumulate of layer l+2 read this layer's g1 / coefficient buffers
+    if (split && l + 2 < d.m) cudaStreamWaitEvent(main_st, aev(l + 2, 1), 0);
     // ---- data chain: 1x1 dgrad (+ReLU mask by act_a, BN_a sums) ----
     {
       LaunchScope ls(b, KC_C1_DGRAD, M * ((4.0 + Sb) * d.bk + (Sb + 4.0) * a.c), f1, M * ((4.0 + 2.0) * d.bk + (2.0 + 4.0) * a.c));
@@ -542,24 +550,46 @@ static void backward_impl(Block* b, const float* params, float* grad_acc, float*
       else gemm_bn2<128, Conv1x1Dgrad>(b, a, g.M, a.c, 1);
     }
     // BN_a backward (graph.hpp:929-932) + concat-backward accumulate (:936-941)
+    float* bna = b->bna_bwd + (l & 1) * 2 * g.cmaxp;  // parity buffer (split_apply)
     {
       LaunchScope ls(b, KC_FINALIZE, 16.0 * g.P * a.c, 0, 16.0 * g.P * a.c);
-      launch(k_finalize_bn_bwd, static_cast<unsigned>((a.c + kFinCh - 1) / kFinCh), kFinThreads, 0, b->stream, 
-          b->part, g.P, a.c, count, d_ga, d_ba, b->bna_bwd);
+      launch(k_finalize_bn_bwd, static_cast<unsigned>((a.c + kFinCh - 1) / kFinCh), kFinThreads, 0, b->stream,
+             b->part, g.P, a.c, count, d_ga, d_ba, bna);
     }
-    {
-      LaunchScope ls(b, KC_BN_APPLY_ACC, M * a.c * (4.0 + Sb + 8.0), 0, M * a.c * (4.0 + 2.0 + 8.0));
-      const bool quads = std::is_same<S, float>::value && a.Ca % 4 == 0 &&
+    // The accumulate of layer l updates channels [0, c_l); only its last k,
+    // [c_l - k, c_l), feed layer l-1's 3x3 dgrad next.  With split_apply that
+    // head runs on the main chain and the tail [0, c_l - k) on side2,
+    // overlapping layer l-1's dgrads; per channel the accumulation order is
+    // unchanged (tail l precedes head / tail l-1 through events), so results
+    // are bit-identical to one accumulate per layer.
+    const int c_head = (split && l > 0) ? a.c - d.k : 0;
+    auto apply = [&](int c_lo, int c_hi, cudaStream_t st) {
+      if (c_hi <= c_lo) return;
+      LaunchScope ls(b, KC_BN_APPLY_ACC, M * (c_hi - c_lo) * (4.0 + Sb + 8.0), 0,
+                     M * (c_hi - c_lo) * (4.0 + 2.0 + 8.0));
+      const bool quads = std::is_same<S, float>::value && a.Ca % 4 == 0 && c_lo % 4 == 0 &&
                          (reinterpret_cast<uintptr_t>(b->acc_cur) & 15) == 0;
       if (quads)
         launch(k_bn_apply_accumulate4,
-               blocks_for((g.M + kApplyRows - 1) / kApplyRows * ((a.c + 3) / 4), 256), 256, 0, b->stream,
-               g.M, a.c, a.C, a.Ca, a.cg, static_cast<const float*>(b->feat), b->g1, a.amean,
-               a.avar, a.gamma_a, b->bna_bwd, b->acc_cur);
+               blocks_for((g.M + kApplyRows - 1) / kApplyRows * ((c_hi + 3) / 4 - c_lo / 4), 256), 256, 0, st, g.M,
+               c_lo, c_hi, a.C, a.Ca, a.cg, static_cast<const float*>(b->feat), a.g1, a.amean, a.avar, a.gamma_a,
+               static_cast<const float*>(bna), b->acc_cur);
       else
-        launch(k_bn_apply_accumulate<S>, blocks_for(g.M * a.c, 256), 256, 0, b->stream,
-               g.M, a.c, a.C, a.Ca, a.cg, static_cast<const S*>(b->feat), b->g1, a.amean,
-               a.avar, a.gamma_a, b->bna_bwd, b->acc_cur);
+        launch(k_bn_apply_accumulate<S>, blocks_for(g.M * (c_hi - c_lo), 256), 256, 0, st, g.M, c_lo, c_hi, a.C,
+               a.Ca, a.cg, static_cast<const S*>(b->feat), a.g1, a.amean, a.avar, a.gamma_a,
+               static_cast<const float*>(bna), b->acc_cur);
+    };
+    if (split) {
+      cudaEventRecord(aev(l, 0), main_st);                                   // g1 + coefficients of layer l
+      if (l + 1 < d.m) cudaStreamWaitEvent(main_st, aev(l + 1, 1), 0);      // tail of layer l+1
+    }
+    apply(c_head, a.c, main_st);
+    if (split && l > 0) {
+      cudaStreamWaitEvent(b->side2, aev(l, 0), 0);
+      b->stream = b->side2;
+      apply(0, c_head, b->side2);
+      b->stream = main_st;
+      cudaEventRecord(aev(l, 1), b->side2);
     }
   }
   if (fork) {  // join: the caller's stream sees every weight gradient
@@ -701,7 +731,7 @@ int create(const dpb_block_desc* desc, int device, void* stream, Block** out, De
       align_up(static_cast<int64_t>(b->g.Pmax) * std::max<int64_t>(b->g.C, desc->bk) * 16, 256);
   b->wpart = reinterpret_cast<float*>(sc + pbytes);
   // wgrad partial region size = scratch - pbytes - coef region
-  const int64_t coef_bytes = align_up((4LL * desc->bk + 2 * b->g.cmaxp) * 4, 256);
+  const int64_t coef_bytes = align_up((4LL * desc->bk + 4 * b->g.cmaxp) * 4, 256);
   const int64_t wt_bytes = b->tc ? weight_image_bytes(*desc) : 0;
   const int64_t zs_bytes = align_up(zsplit_bytes(*desc), 256);
   b->bnb_bwd = reinterpret_cast<float*>(sc + b->sz.scratch_bytes - wt_bytes - zs_bytes - coef_bytes);
@@ -730,6 +760,12 @@ int create(const dpb_block_desc* desc, int device, void* stream, Block** out, De
     if (w1b > 0) b->w1b = p;
   }
   if (cudaStreamCreateWithFlags(&b->side, cudaStreamNonBlocking) != cudaSuccess) b->side = nullptr;
+  if (b->side && cudaStreamCreateWithFlags(&b->side2, cudaStreamNonBlocking) != cudaSuccess) b->side2 = nullptr;
+  for (int i = 0; b->side2 && i < 2 * desc->m; ++i) {
+    cudaEvent_t e;
+    cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
+    b->apply_ev.push_back(e);
+  }
   for (int i = 0; b->side && i < 3 * desc->m; ++i) {
     cudaEvent_t e;
     cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
@@ -759,7 +795,9 @@ void destroy(Block* b) {
   }
   for (cudaEvent_t e : b->ev_pool) cudaEventDestroy(e);
   for (cudaEvent_t e : b->fork_ev) cudaEventDestroy(e);
+  for (cudaEvent_t e : b->apply_ev) cudaEventDestroy(e);
   if (b->side) cudaStreamDestroy(b->side);
+  if (b->side2) cudaStreamDestroy(b->side2);
   delete b;
 }
 

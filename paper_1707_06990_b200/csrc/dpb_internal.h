@@ -112,12 +112,14 @@ struct Block {
   float* g0 = nullptr;       // [M, bk] fp32 (x2: double-buffered across layers)
   cudaStream_t side = nullptr;        // weight-gradient branch of the backward
   std::vector<cudaEvent_t> fork_ev;   // per layer: start, bn_b done, side done
-  float* g1 = nullptr;       // [M, cmax] fp32
+  cudaStream_t side2 = nullptr;       // the accumulate's tail (split apply)
+  std::vector<cudaEvent_t> apply_ev;  // per layer: g1 ready, tail done
+  float* g1 = nullptr;       // 2 x [M, cmax] fp32 (layer parity)
   double2* part = nullptr;   // per-CTA partial sums
   float* wpart = nullptr;    // split-K weight-gradient partials
   float* zpart = nullptr;    // split-K 1x1 forward partials [ks][M][bk] (null: no split)
   float* bnb_bwd = nullptr;  // [bk][2] (x2: double-buffered across layers)
-  float* bna_bwd = nullptr;  // [cmax][2]
+  float* bna_bwd = nullptr;  // [cmax][2] (x2: layer parity)
   std::vector<int64_t> param_off, stat_off;
   uint8_t* wtile = nullptr;           // pre-tiled bf16 W1 operands (tensor-core path)
   std::vector<int64_t> wtile_off;

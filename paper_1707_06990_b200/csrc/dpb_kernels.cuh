@@ -177,16 +177,17 @@ __global__ void __launch_bounds__(kFinThreads) k_finalize_bn_bwd(const double2* 
 // t2 (fp32) and x, read-modify-writes acc.  One thread per 4 channels.
 template <typename S>
 __global__ void __launch_bounds__(256)
-k_bn_apply_accumulate(int64_t M, int c, int C, int Ca, int cg, const S* __restrict__ feat,
+k_bn_apply_accumulate(int64_t M, int c_lo, int c, int C, int Ca, int cg, const S* __restrict__ feat,
                       const float* __restrict__ g1, const float* __restrict__ amean,
                       const float* __restrict__ avar,
                       const float* __restrict__ gamma, const float* __restrict__ coef,
                       float* __restrict__ acc) {
   pdl_enter();
+  const int nc = c - c_lo;  // channels [c_lo, c)
   const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (i >= M * c) return;
-  const int64_t p = i / c;
-  const int ch = static_cast<int>(i - p * c);
+  if (i >= M * nc) return;
+  const int64_t p = i / nc;
+  const int ch = c_lo + static_cast<int>(i - p * nc);
   const float mean = amean[ch];
   const float inv = bn_inv(avar[ch]);
   const float xh = (to_f(feat[p * C + ch]) - mean) * inv;
@@ -201,14 +202,15 @@ k_bn_apply_accumulate(int64_t M, int c, int C, int Ca, int cg, const S* __restri
 // of a layer with c % 4 != 0 updates only its channels < c.
 constexpr int kApplyRows = 8;
 __global__ void __launch_bounds__(256)
-k_bn_apply_accumulate4(int64_t M, int c, int C, int Ca, int cg, const float* __restrict__ feat,
+k_bn_apply_accumulate4(int64_t M, int c_lo, int c, int C, int Ca, int cg, const float* __restrict__ feat,
                        const float* __restrict__ g1, const float* __restrict__ amean,
                        const float* __restrict__ avar, const float* __restrict__ gamma,
                        const float* __restrict__ coef, float* __restrict__ acc) {
-  const int cq = (c + 3) >> 2;
+  const int q0 = c_lo >> 2;  // channels [c_lo, c) (c_lo % 4 == 0)
+  const int cq = ((c + 3) >> 2) - q0;
   const int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   const int64_t pg = t / cq;
-  const int q = static_cast<int>(t - pg * cq);
+  const int q = q0 + static_cast<int>(t - pg * cq);
   const int64_t p0 = pg * kApplyRows;
   if (p0 >= M) {
     pdl_enter();

@@ -103,7 +103,7 @@ def test_arena_plan_offsets_and_sizes_exact():
         assert a["z_bytes"] == 12 * M * 48 * S
         assert a["acc_bytes"] == M * C * 4
         # g0 is double-buffered across layers (two-stream backward)
-        assert a["g0_bytes"] == 2 * M * 48 * 4 and a["g1_bytes"] == M * cmax * 4
+        assert a["g0_bytes"] == 2 * M * 48 * 4 and a["g1_bytes"] == 2 * M * cmax * 4
         assert a["shared1_bytes"] == 0 and a["shared2_bytes"] == 0
         assert a["param_elems"] == s.param_elems and a["stat_elems"] == s.stat_elems
         # regions are 256-byte aligned, ordered and disjoint
