@@ -168,6 +168,13 @@ def test_block_matches_oracle_medium(dtype, layout):
     # few pixel tiles that the 1x1 forward splits its 192 columns across CTAs
     (2, 7, 7, 520, 2, 48, 192),
     (16, 7, 7, 1728, 1, 48, 192),
+    # the real widths of DenseNet-264: block 3's widest layer (c = 3,408), block
+    # 4's (c = 3,936 + 48) at k = 48 / bk = 192 (Dgrad1x1<128, 4>: 32 column
+    # tiles), and k = 32 / bk = 128 blocks 3-4 (c0 >= 512: 256-column dgrad tiles)
+    (2, 14, 14, 3408, 1, 48, 192),
+    (4, 7, 7, 3936, 1, 48, 192),
+    (4, 14, 14, 2240, 1, 32, 128),
+    (8, 7, 7, 1120, 2, 32, 128),
 ])
 @pytest.mark.parametrize("dtype", ["fp32", "bf16"])
 def test_block_matches_oracle_shapes(s, dtype):
