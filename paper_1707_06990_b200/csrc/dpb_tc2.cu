@@ -219,15 +219,10 @@ bool tc2_conv1x1_fwd(Block* b, const LayerArgs<float>& a, int l) {
 // 128 columns: its two TMEM accumulators then take 256 of the SM's 512 columns,
 // so a CTA can start beside a side-stream 3x3 wgrad CTA (which holds 256)
 // instead of waiting for the SM to empty (measured +0.6 % over 256 at BC-100).
-// Wide blocks (c0 >= 512: DenseNet-121/264 blocks 3-4, up to 32 column tiles of
-// 128) take 256-column tiles: every column tile re-forms t1 from g0 and z, so
-// halving the tiles halves that work and those loads; the CTA then holds all
-// of TMEM.  DPB_DGRAD_BN=128|256 forces one.
-int tc2_bwd_bn(const dpb_block_desc& d) {
-  static const int force = std::getenv("DPB_DGRAD_BN") ? std::atoi(std::getenv("DPB_DGRAD_BN")) : 0;
-  if (force == 128 || force == 256) return d.bk <= 128 ? force : 128;
-  return (d.c0 >= 512 && d.bk <= 128) ? 256 : 128;
-}
+// (256-column tiles for wide blocks, forming t1 half as often, were tried:
+// the 64 KB W1^T image leaves room for only a 3-deep epilogue ring, fewer
+// boxes than the four epilogue groups need in flight — it stalls.)
+int tc2_bwd_bn(const dpb_block_desc&) { return 128; }
 
 int64_t tc2_w1b_layer_bytes(const dpb_block_desc& d, int l) {
   const int bn = tc2_bwd_bn(d);
@@ -240,10 +235,7 @@ void tc2_pretile_w1t(Block* b, const float* params) {
   const dpb_block_desc& d = b->d;
   if (!b->w1b) return;
   const dim3 grid(16, d.m);
-  if (tc2_bwd_bn(d) == 256)
-    launch(tc2::k_pretile_w1t_all<256>, grid, 256, 0, b->stream, params, d.c0, d.k, d.bk, b->w1b);
-  else
-    launch(tc2::k_pretile_w1t_all<128>, grid, 256, 0, b->stream, params, d.c0, d.k, d.bk, b->w1b);
+  launch(tc2::k_pretile_w1t_all<128>, grid, 256, 0, b->stream, params, d.c0, d.k, d.bk, b->w1b);
   b->launches++;
 }
 
@@ -270,9 +262,7 @@ bool tc2_conv1x1_dgrad(Block* b, const LayerArgs<float>& a, int l) {
     launch2(b, op, dim3(gx, nn), aux);
     return true;
   };
-  // bk = 192: the resident W1^T (48 KB) fits only beside a 4-deep epilogue ring;
-  // 256-column tiles (64 KB of W1^T) beside a 3-deep one
-  if (tc2_bwd_bn(b->d) == 256) return go(tc2::Dgrad1x1<256, 3>{});
+  // bk = 192: the resident W1^T (48 KB) fits only beside a 4-deep epilogue ring
   return go(tc2::Dgrad1x1<128>{}) || go(tc2::Dgrad1x1<128, 4>{});
 }
 
