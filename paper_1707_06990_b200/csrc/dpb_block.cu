@@ -206,7 +206,8 @@ void plan_arena(const dpb_block_desc& d, dpb_arena_sizes* s) {
       wmax = std::max<int64_t>(wmax, tc2_wgrad_wpart_elems(d, l));
     }
   }
-  const int64_t pbytes = static_cast<int64_t>(g.Pmax) * std::max<int64_t>(g.C, d.bk) * 16;
+  const int64_t pbytes = std::max<int64_t>(static_cast<int64_t>(g.Pmax) * std::max<int64_t>(g.C, d.bk) * 16,
+                                          zsplit_bytes(d) > 0 ? (g.M + 31) / 32 * d.bk * 16 : 0);
   const int64_t scratch = align_up(pbytes, 256) + align_up(wmax * 4, 256) +
                           align_up((4LL * d.bk + 4 * g.cmaxp) * 4, 256) + align_up(zsplit_bytes(d), 256);
   take(scratch, &s->scratch_offset, &s->scratch_bytes);
@@ -364,18 +365,19 @@ static void forward_impl(Block* b, const float* x_in, const float* params, float
     tr.on(0, 7 * l + 4, BlockTrace::kBatchNorm, 8.0 * M * d.bk);
     tr.on(0, 7 * l + 5, BlockTrace::kRelu, M * d.bk);
     tr.on(0, 7 * l + 6, BlockTrace::kConv, 2.0 * M * d.k * 9.0 * d.bk);
+    int p1 = g.P;  // BN_b partial rows
     {
       LaunchScope ls(b, KC_C1_FWD, M * (a.c + d.bk) * Sb, 2.0 * M * a.c * d.bk, M * (a.c + d.bk) * 2.0);
       if (b->tc) {
-        if (!tc2_conv1x1_fwd(b, a, l)) tc_conv1x1_fwd(b, a);
+        if (!tc2_conv1x1_fwd(b, a, l, &p1)) tc_conv1x1_fwd(b, a);
       }
       else gemm_bn<128, Conv1x1Fwd>(b, a, g.M, d.bk, 1);
     }
     if (!eval) {
-      LaunchScope ls(b, KC_FINALIZE, 16.0 * g.P * d.bk, 0, 16.0 * g.P * d.bk);
+      LaunchScope ls(b, KC_FINALIZE, 16.0 * p1 * d.bk, 0, 16.0 * p1 * d.bk);
       float* zm = b->zstat + static_cast<int64_t>(l) * 2 * d.bk;
       launch(k_finalize_stats, static_cast<unsigned>((d.bk + kFinCh - 1) / kFinCh), kFinThreads, 0, b->stream, 
-          b->part, g.P, d.bk, count, zm, zm + d.bk, 0);
+          b->part, p1, d.bk, count, zm, zm + d.bk, 0);
     }
     int p3 = g.P;
     {
@@ -728,7 +730,8 @@ int create(const dpb_block_desc* desc, int device, void* stream, Block** out, De
   char* sc = base + b->sz.scratch_offset;
   b->part = reinterpret_cast<double2*>(sc);
   const int64_t pbytes =
-      align_up(static_cast<int64_t>(b->g.Pmax) * std::max<int64_t>(b->g.C, desc->bk) * 16, 256);
+      align_up(std::max<int64_t>(static_cast<int64_t>(b->g.Pmax) * std::max<int64_t>(b->g.C, desc->bk) * 16,
+                                 zsplit_bytes(*desc) > 0 ? (b->g.M + 31) / 32 * desc->bk * 16 : 0), 256);
   b->wpart = reinterpret_cast<float*>(sc + pbytes);
   // wgrad partial region size = scratch - pbytes - coef region
   const int64_t coef_bytes = align_up((4LL * desc->bk + 4 * b->g.cmaxp) * 4, 256);

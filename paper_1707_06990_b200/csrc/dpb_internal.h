@@ -191,7 +191,8 @@ int64_t tc_halo_partials(const dpb_block_desc& d);
 int64_t tc_halo_wgrad_splits(const dpb_block_desc& d);
 void tc_conv1x1_dgrad(Block* b, const LayerArgs<float>& a);
 int tc_conv1x1_wgrad(Block* b, LayerArgs<float> a);
-bool tc2_conv1x1_fwd(Block* b, const LayerArgs<float>& a, int l);
+// prows: BN_b partial rows written (left unchanged = the 128-row tile count)
+bool tc2_conv1x1_fwd(Block* b, const LayerArgs<float>& a, int l, int* prows = nullptr);
 int tc2_fwd_ksplit(int64_t M, int c, int sms, int ns);
 int64_t tc2_w1_tile_bytes(const dpb_block_desc& d, int l);
 void tc2_pretile_w1(Block* b, const float* params);

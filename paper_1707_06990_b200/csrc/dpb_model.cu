@@ -959,7 +959,7 @@ namespace dpb {
 namespace {
 
 constexpr int kSplitsMax = 148;      // split-K of the transition dW GEMM
-constexpr int kStem7Splits = 888;    // CTAs (tile ranges) of the 7x7 stem dW: 6 per SM
+constexpr int kStem7Splits = 296;    // CTAs (tile ranges) of the 7x7 stem dW (888 measured slower)
 constexpr int kRowSplitsMax = 2048;  // pixel chunks of the BN-backward sums and the stem dW
 
 int model_geometry(const dpb_model_desc* d, dpb_model* m) {

@@ -162,7 +162,7 @@ int tc2_fwd_ksplit(int64_t M, int c, int sms, int ns) {
 
 // 1x1 forward on the v2 engine; false when the shape is not supported (the
 // caller then uses the v1 kernel).
-bool tc2_conv1x1_fwd(Block* b, const LayerArgs<float>& a, int l) {
+bool tc2_conv1x1_fwd(Block* b, const LayerArgs<float>& a, int l, int* prows) {
   if (a.C % 4 != 0 || !b->wtile) return false;
   const int ntiles = static_cast<int>((a.M + tc::kBM - 1) / tc::kBM);
   const uint8_t* w1t = b->wtile + b->wtile_off[l];
@@ -193,9 +193,12 @@ bool tc2_conv1x1_fwd(Block* b, const LayerArgs<float>& a, int l) {
       op.nw = op.bimg / op.ns;
     }
     launch2(b, op, dim3(balanced_ctas(ntiles * op.ns * op.ks, num_sms())), aux);
-    if (op.ks > 1)
-      launch(tc2::k_zsplit_reduce, dim3(ntiles, (a.bk + 31) / 32), 256, 0, b->stream,
+    if (op.ks > 1) {
+      const int zb = static_cast<int>((a.M + tc2::kZRows - 1) / tc2::kZRows);
+      launch(tc2::k_zsplit_reduce, dim3(zb, (a.bk + 31) / 32), 256, 0, b->stream,
              static_cast<const float*>(b->zpart), op.ks, a.M, a.bk, a.z, a.part);
+      if (prows) *prows = zb;
+    }
     return true;
   };
   // B resident in shared memory when all of W1's tiles fit, else streamed

@@ -563,24 +563,24 @@ struct Fwd1x1 {
 };
 
 // Split-K 1x1 forward, second pass: z[m][c] = sum over splits of zpart[s][m][c]
-// in split order, and the BN_b partial sums of each 128-row tile (the
-// epilogue's col_sums layout, part[tile][c] = {sum z, sum z^2}, fp64, fixed
-// order).  CTA = one 128-row tile x 32 channels (grid.y); 256 threads = 32
-// channel lanes x 8 row groups, each thread's 16 rows x ks partials loaded
-// with full unrolling (all loads in flight: this pass is L2-latency bound).
-constexpr int kMaxKSplit = 8;
+// in split order, and the BN_b partial sums (sum z, sum z^2, fp64, fixed
+// order) of every kZRows-row block, part[block][c] (the finalize folds
+// ceil(M / kZRows) rows).  CTA = kZRows rows x 32 channels (grid.y); 256
+// threads = 32 channel lanes x 8 row groups; many small CTAs keep the
+// partials' loads in flight (the pass is latency bound).
+constexpr int kMaxKSplit = 8, kZRows = 32;
 __global__ void __launch_bounds__(256) k_zsplit_reduce(const float* __restrict__ zpart, int ks, int64_t M, int bk,
                                                        float* __restrict__ z, double2* __restrict__ part) {
   pdl_enter();
   __shared__ double r1[8][33], r2[8][33];
   const int lane = threadIdx.x % 32, grp = threadIdx.x / 32;
-  const int64_t m0 = static_cast<int64_t>(blockIdx.x) * kBM;
+  const int64_t m0 = static_cast<int64_t>(blockIdx.x) * kZRows;
   const int c = blockIdx.y * 32 + lane;
   double s1 = 0.0, s2 = 0.0;
   if (c < bk) {
-    float v[kBM / 8];
+    float v[kZRows / 8];
 #pragma unroll
-    for (int i = 0; i < kBM / 8; ++i) {
+    for (int i = 0; i < kZRows / 8; ++i) {
       const int64_t m = m0 + grp + 8 * i;
       float acc = 0.f;
 #pragma unroll
@@ -589,7 +589,7 @@ __global__ void __launch_bounds__(256) k_zsplit_reduce(const float* __restrict__
       v[i] = acc;
     }
 #pragma unroll
-    for (int i = 0; i < kBM / 8; ++i) {
+    for (int i = 0; i < kZRows / 8; ++i) {
       const int64_t m = m0 + grp + 8 * i;
       if (m < M) {
         z[m * bk + c] = v[i];
