@@ -307,7 +307,7 @@ __global__ void __launch_bounds__(256) k_stem_bnb_partials(const float* __restri
 // (cin x (2*TH+5) x (2*TW+5), zero outside the image) in shared memory, then
 // thread = a 4-channel x 12-tap register tile of dW[o][t] sums the tile's
 // pixels in order.  Partials [cta][c0][cin*49], folded by k_reduce_w1.
-constexpr int kS7TH = 8, kS7TW = 16, kS7IH = 2 * kS7TH + 5, kS7IW = 2 * kS7TW + 5, kS7TT = 12;
+constexpr int kS7TH = 8, kS7TW = 16, kS7IH = 2 * kS7TH + 5, kS7IW = 2 * kS7TW + 5, kS7TT = 6;
 __host__ __device__ inline int stem7_tiles(int c0, int cin) {  // register tiles = threads
   return ((c0 + 3) / 4) * ((cin * kS7Taps + kS7TT - 1) / kS7TT);
 }
