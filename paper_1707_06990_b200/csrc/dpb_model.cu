@@ -958,7 +958,18 @@ struct dpb_model {
 namespace dpb {
 namespace {
 
-constexpr int kSplitsMax = 148;      // split-K of the transition dW GEMM
+constexpr int kSplitsMax = 148;      // split-K of the transition dW GEMM (upper bound)
+
+// Split-K of the transition dW GEMM [cout x C] over its Mq pooled pixels: as
+// many splits as bring its 64x64 output tiles to ~4 waves (at least 64 pixels
+// per split) — wide transitions have thousands of tiles and need no split,
+// and their partials (splits x cout x C fp32) would otherwise run to GBs.
+int trans_dw_splits(const ModelTrans& t, int64_t& chunk) {
+  const int64_t tiles = ((t.cout + 63) / 64) * ((t.C + 63) / 64);
+  const int64_t want = std::max<int64_t>(1, std::min<int64_t>(kSplitsMax, (4 * 148 + tiles - 1) / tiles));
+  chunk = std::max<int64_t>(64, (t.Mq + want - 1) / want);
+  return static_cast<int>((t.Mq + chunk - 1) / chunk);
+}
 constexpr int kStem7Splits = 296;    // CTAs (tile ranges) of the 7x7 stem dW (888 measured slower)
 constexpr int kRowSplitsMax = 2048;  // pixel chunks of the BN-backward sums and the stem dW
 
@@ -1207,7 +1218,8 @@ DPB_API int dpb_model_create(const dpb_model_desc* desc, int device, void* strea
   for (auto& t : m->trans) {
     off.push_back(take(t.Mq * t.C, DPB_ARENA_FEATURE_OWNED));  // pooled activations (saved for dW)
     off.push_back(take(t.Mq * t.C, DPB_ARENA_SHARED_GRAD));    // their gradient
-    off.push_back(take(static_cast<int64_t>(kSplitsMax) * t.cout * t.C));
+    int64_t tchunk;
+    off.push_back(take(static_cast<int64_t>(trans_dw_splits(t, tchunk)) * t.cout * t.C));
   }
   const int Cl = m->blocks.back().C;
   const int64_t N = desc->batch;
@@ -1220,7 +1232,8 @@ DPB_API int dpb_model_create(const dpb_model_desc* desc, int device, void* strea
   }
   const int64_t stem_splits = (m->blocks[0].M + stem_chunk(desc->c0, desc->in_c) - 1) /
                               stem_chunk(desc->c0, desc->in_c);
-  m->wpart_elems = std::max<int64_t>(kSplitsMax * wmax, stem_splits * desc->c0 * desc->in_c * 9);
+  (void)wmax;  // the transitions' dW partials are their own (t.wpart); m->wpart: the stem's
+  m->wpart_elems = stem_splits * desc->c0 * desc->in_c * 9;
   if (desc->stem == 1)
     m->wpart_elems = std::max<int64_t>(m->wpart_elems, kStem7Splits * desc->c0 * desc->in_c * kS7Taps);
   int64_t o_y1 = 0, o_arg = 0, o_spart = 0, o_sstat = 0;
@@ -1475,7 +1488,7 @@ int model_step_launch(dpb_model* m, const float* input, const int32_t* labels, c
       ModelBlock& pv = m->blocks[b - 1];
       // g_pool = mb.acc[:, :t.cout] (pitch mb.C); dW = g_pool^T . P (split-K), g_P = g_pool . W
       int64_t chunk;
-      const int S = splits_of(t.Mq, chunk);
+      const int S = trans_dw_splits(t, chunk);
       // dW (gradient-only) on the side stream, overlapping g_P / BN backward and the
       // next block's backward; t.wpart is private to this transition
       cudaStream_t ws = st;
