@@ -67,6 +67,9 @@ for s in [(16,32,32,24,12,12,48),(4,14,14,96,6,48,192)]:
     acc=O.rng_normal(107,shp.n*shp.c_out*shp.h*shp.w,np.float32).reshape(shp.n,shp.c_out,shp.h,shp.w)
     ref=run(s,params,x,acc,"none","none","none")
     res=[]
-    for fwd,bwd,store in [("m16","bf16","none"),("m13","bf16","none"),("none","bf16","none")]:
+    # storage variants (features / bottleneck outputs stored bf16 or
+    # TF32 vs fp32) and forward-product precisions (m16 ~ bf16x3, m13 ~ TF32)
+    for fwd,bwd,store in [("none","none","bf16"),("none","none","tf32"),("m16","bf16","none"),
+                          ("m13","bf16","none"),("none","bf16","none")]:
         r=run(s,params,x,acc,fwd,bwd,store); res.append(f"f:{fwd}/b:{bwd}/s:{store}={np.linalg.norm(r-ref)/np.linalg.norm(ref):.4f}")
     print(s,*res,flush=True)
