@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 
 #include "dpb_internal.h"
 #include "dpb_launch.h"
@@ -101,8 +102,23 @@ HaloPlan tc_halo_plan(const dpb_block_desc& d) {
   HaloPlan p{};
   const tc::HaloGeom g = tc::HaloGeom::make(static_cast<int>(d.h), static_cast<int>(d.w));
   const int bn = pick_bn(d.k);
+  // The largest K chunk whose double-buffered stages let two CTAs share an SM
+  // (the per-CTA produce -> MMA -> epilogue chain is latency-bound: a second
+  // resident CTA overlaps it), else the largest that fits one CTA.
+  // DPB_HALO_KC=<kc> forces a chunk (when it fits).
+  static const int force_kc = std::getenv("DPB_HALO_KC") ? std::atoi(std::getenv("DPB_HALO_KC")) : 0;
+  auto fwd_fits = [&](int kc, size_t lim) {
+    const size_t stage = 2ull * (static_cast<size_t>(g.R) * kc * 2 + 9ull * bn * kc * 2);
+    const int nkb = (d.bk + kc - 1) / kc;
+    return stage * (nkb > 1 ? 2 : 1) + sizeof(BnFwd) * d.bk <= lim;
+  };
+  int kc_pick = 0;
+  for (int kc = std::min(64, d.bk); d.bk % 16 == 0 && bn <= 64 && kc >= 16 && !kc_pick; kc /= 2)
+    if (kc % 16 == 0 && fwd_fits(kc, kHaloSmemMax / 2 - 1024)) kc_pick = kc;
+  if (force_kc >= 16 && force_kc % 16 == 0 && force_kc <= 64 && fwd_fits(force_kc, kHaloSmemMax)) kc_pick = force_kc;
   for (int kc = std::min(64, d.bk); d.bk % 16 == 0 && bn <= 64 && kc >= 16; kc /= 2) {
     if (kc % 16 != 0) continue;
+    if (kc_pick && kc != kc_pick) continue;
     const size_t stage = 2ull * (static_cast<size_t>(g.R) * kc * 2 + 9ull * bn * kc * 2);
     const int nkb = (d.bk + kc - 1) / kc;
     const int nst = nkb > 1 ? 2 : 1;
