@@ -104,7 +104,8 @@ HaloPlan tc_halo_plan(const dpb_block_desc& d) {
   const int bn = pick_bn(d.k);
   // The largest K chunk whose double-buffered stages let two CTAs share an SM
   // (the per-CTA produce -> MMA -> epilogue chain is latency-bound: a second
-  // resident CTA overlaps it), else the largest that fits one CTA.
+  // resident CTA overlaps it) for multi-wave grids, else the largest that
+  // fits one CTA.
   // DPB_HALO_KC=<kc> forces a chunk (when it fits).
   static const int force_kc = std::getenv("DPB_HALO_KC") ? std::atoi(std::getenv("DPB_HALO_KC")) : 0;
   auto fwd_fits = [&](int kc, size_t lim) {
@@ -113,7 +114,11 @@ HaloPlan tc_halo_plan(const dpb_block_desc& d) {
     return stage * (nkb > 1 ? 2 : 1) + sizeof(BnFwd) * d.bk <= lim;
   };
   int kc_pick = 0;
-  for (int kc = std::min(64, d.bk); d.bk % 16 == 0 && bn <= 64 && kc >= 16 && !kc_pick; kc /= 2)
+  // only when the tiles fill more than one wave at one CTA per SM (measured:
+  // 56x56 and 28x28 gain 16 % / 10 %; 14x14 and 7x7, under one wave, lose to
+  // the smaller chunks' extra rounds)
+  const int64_t tiles = d.n * g.tpi;
+  for (int kc = std::min(64, d.bk); d.bk % 16 == 0 && bn <= 64 && kc >= 16 && !kc_pick && tiles > 148; kc /= 2)
     if (kc % 16 == 0 && fwd_fits(kc, kHaloSmemMax / 2 - 1024)) kc_pick = kc;
   if (force_kc >= 16 && force_kc % 16 == 0 && force_kc <= 64 && fwd_fits(force_kc, kHaloSmemMax)) kc_pick = force_kc;
   for (int kc = std::min(64, d.bk); d.bk % 16 == 0 && bn <= 64 && kc >= 16; kc /= 2) {
