@@ -183,7 +183,9 @@ __global__ void __launch_bounds__(Roles<Op>::kThreads, 1) tc2_kernel(const __gri
   // barriers itself, and the ring starts empty.
   int early = 0;
   if constexpr (Op::kEarlyLoads) {
-    if (tid == 0) {
+    // not when the predecessor is the producer of these operands (its BN
+    // finalize folded into it: the operands are one launch old, not two)
+    if (tid == 0 && !op.a.no_early) {
       op.prefetch();
       const int nt = op.num_tiles();
       for (int tile = blockIdx.x; tile < nt && early < NR; tile += gridDim.x)
