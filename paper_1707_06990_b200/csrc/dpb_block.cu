@@ -370,7 +370,6 @@ static void forward_impl(Block* b, const float* x_in, const float* params, float
   float* fvar = b->fstat + g.Cp;
   BlockTrace& tr = b->trace;
   tr.reset(7 * d.m + 1);
-  bool prev_folded = false;  // the previous launch folded its finalize (operands one launch old)
   if (!eval) {
     {
       LaunchScope ls(b, KC_STATS, M * d.c0 * Sb, 0, M * d.c0 * 2.0);
@@ -407,7 +406,6 @@ static void forward_impl(Block* b, const float* x_in, const float* params, float
       if (b->tc) {
         LayerArgs<S> af = a;  // z statistics of this layer, folded in
         if (!eval) af.fold = stats_fold(b, 0, d.bk, b->zstat + static_cast<int64_t>(l) * 2 * d.bk, d.bk, 0);
-        af.no_early = prev_folded ? 1 : 0;  // the 3x3 forward just wrote the newest channels
         if (!tc2_conv1x1_fwd(b, af, l, &p1, &folded)) tc_conv1x1_fwd(b, a);
       }
       else gemm_bn<128, Conv1x1Fwd>(b, a, g.M, d.bk, 1);
@@ -426,7 +424,6 @@ static void forward_impl(Block* b, const float* x_in, const float* params, float
         LayerArgs<S> af = a;  // the new k channels' statistics, folded in
         if (!eval) af.fold = stats_fold(b, 1, d.k, fmean, g.Cp, a.c);
         p3 = tc_conv3x3_fwd(b, af, l, &folded);
-        prev_folded = folded;
       }
       else gemm_bn<128, Conv3x3Fwd>(b, a, g.M, d.k, 1);
     }
@@ -599,7 +596,6 @@ static void backward_impl(Block* b, const float* params, float* grad_acc, float*
       if (b->tc) {
         LayerArgs<S> af = a;  // BN_a backward sums folded per column tile
         af.fold = bwd_fold(b, 8, a.c, d_ga, d_ba, b->bna_bwd + (l & 1) * 2 * g.cmaxp);
-        af.no_early = folded ? 1 : 0;  // the 3x3 dgrad just wrote g0
         folded = false;
         if (!tc2_conv1x1_dgrad(b, af, l, &folded)) tc_conv1x1_dgrad(b, a);
       }
@@ -607,8 +603,7 @@ static void backward_impl(Block* b, const float* params, float* grad_acc, float*
     }
     // BN_a backward (graph.hpp:929-932) + concat-backward accumulate (:936-941)
     float* bna = b->bna_bwd + (l & 1) * 2 * g.cmaxp;  // parity buffer (split_apply)
-    const bool dgrad_folded = b->tc && folded;  // the head accumulate's predecessor wrote g1
-    if (!dgrad_folded) {
+    if (!(b->tc && folded)) {
       LaunchScope ls(b, KC_FINALIZE, 16.0 * g.P * a.c, 0, 16.0 * g.P * a.c);
       launch(k_finalize_bn_bwd, static_cast<unsigned>((a.c + kFinCh - 1) / kFinCh), kFinThreads, 0, b->stream,
              b->part, g.P, a.c, count, d_ga, d_ba, bna);
@@ -620,7 +615,7 @@ static void backward_impl(Block* b, const float* params, float* grad_acc, float*
     // unchanged (tail l precedes head / tail l-1 through events), so results
     // are bit-identical to one accumulate per layer.
     const int c_head = (split && l > 0) ? a.c - d.k : 0;
-    auto apply = [&](int c_lo, int c_hi, cudaStream_t st, int pre_ok) {
+    auto apply = [&](int c_lo, int c_hi, cudaStream_t st) {
       if (c_hi <= c_lo) return;
       LaunchScope ls(b, KC_BN_APPLY_ACC, M * (c_hi - c_lo) * (4.0 + Sb + 8.0), 0,
                      M * (c_hi - c_lo) * (4.0 + 2.0 + 8.0));
@@ -629,7 +624,7 @@ static void backward_impl(Block* b, const float* params, float* grad_acc, float*
       if (quads)
         launch(k_bn_apply_accumulate4,
                blocks_for((g.M + kApplyRows - 1) / kApplyRows * ((c_hi + 3) / 4 - c_lo / 4), 256), 256, 0, st, g.M,
-               c_lo, c_hi, a.C, a.Ca, a.cg, pre_ok, static_cast<const float*>(b->feat), a.g1, a.amean, a.avar, a.gamma_a,
+               c_lo, c_hi, a.C, a.Ca, a.cg, static_cast<const float*>(b->feat), a.g1, a.amean, a.avar, a.gamma_a,
                static_cast<const float*>(bna), b->acc_cur);
       else
         launch(k_bn_apply_accumulate<S>, blocks_for(g.M * (c_hi - c_lo), 256), 256, 0, st, g.M, c_lo, c_hi, a.C,
@@ -640,11 +635,11 @@ static void backward_impl(Block* b, const float* params, float* grad_acc, float*
       cudaEventRecord(aev(l, 0), main_st);                                   // g1 + coefficients of layer l
       if (l + 1 < d.m) cudaStreamWaitEvent(main_st, aev(l + 1, 1), 0);      // tail of layer l+1
     }
-    apply(c_head, a.c, main_st, dgrad_folded ? 0 : 1);
+    apply(c_head, a.c, main_st);
     if (split && l > 0) {
       cudaStreamWaitEvent(b->side2, aev(l, 0), 0);
       b->stream = b->side2;
-      apply(0, c_head, b->side2, 1);  // behind an event, not a PDL edge
+      apply(0, c_head, b->side2);
       b->stream = main_st;
       cudaEventRecord(aev(l, 1), b->side2);
     }

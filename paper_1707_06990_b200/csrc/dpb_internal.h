@@ -60,11 +60,6 @@ struct BlockTrace {
   }
 };
 
-// Folded BN finalizes (FoldSpec): only when the producer writes at most this
-// many partial rows — the fold runs in ONE CTA at the producer's tail, so at
-// 56x56 (1,568 rows) a separate many-CTA finalize is faster.
-constexpr int kFoldMaxP = 256;
-
 struct Geometry {
   int64_t M = 0;     // pixels N*H*W
   int64_t C = 0;     // block output channels c0 + m*k

@@ -202,7 +202,7 @@ k_bn_apply_accumulate(int64_t M, int c_lo, int c, int C, int Ca, int cg, const S
 // of a layer with c % 4 != 0 updates only its channels < c.
 constexpr int kApplyRows = 8;
 __global__ void __launch_bounds__(256)
-k_bn_apply_accumulate4(int64_t M, int c_lo, int c, int C, int Ca, int cg, int pre_ok, const float* __restrict__ feat,
+k_bn_apply_accumulate4(int64_t M, int c_lo, int c, int C, int Ca, int cg, const float* __restrict__ feat,
                        const float* __restrict__ g1, const float* __restrict__ amean,
                        const float* __restrict__ avar, const float* __restrict__ gamma,
                        const float* __restrict__ coef, float* __restrict__ acc) {
@@ -220,9 +220,7 @@ k_bn_apply_accumulate4(int64_t M, int c_lo, int c, int C, int Ca, int cg, int pr
   // Only the BN_a coefficients come from the predecessor (the finalize); g1 is
   // the 1x1 dgrad's output two launches back, and the features, statistics and
   // accumulator are older.  So the first rows are loaded before the
-  // grid-dependency wait — unless the finalize was folded into the 1x1 dgrad,
-  // which is then the predecessor (pre_ok = 0).
-  if (!pre_ok) pdl_enter();
+  // grid-dependency wait.
   const float4 mean = *reinterpret_cast<const float4*>(amean + ch);
   const float4 var = *reinterpret_cast<const float4*>(avar + ch);
   constexpr int kPre = 2;
@@ -233,7 +231,7 @@ k_bn_apply_accumulate4(int64_t M, int c_lo, int c, int C, int Ca, int cg, int pr
     xp[i] = *reinterpret_cast<const float4*>(feat + p * C + ch);
     gp[i] = *reinterpret_cast<const float4*>(g1 + p * cg + ch);
   }
-  if (pre_ok) pdl_enter();
+  pdl_enter();
   const float4 c01 = *reinterpret_cast<const float4*>(coef + 2 * ch);      // mg0 mgx0 mg1 mgx1
   const float4 c23 = *reinterpret_cast<const float4*>(coef + 2 * ch + 4);  // mg2 mgx2 mg3 mgx3
   const float m[4] = {mean.x, mean.y, mean.z, mean.w};

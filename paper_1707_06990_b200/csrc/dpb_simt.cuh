@@ -225,7 +225,6 @@ struct LayerArgs {
   float* wpart;         // split-K weight-gradient partials
   int64_t kchunk;       // pixels per split for the wgrad ops
   FoldSpec fold;        // the producer's BN finalize, folded into its last CTA (mode 0: none)
-  int no_early;         // 1: the predecessor launch wrote this op's operands (no loads before the wait)
 };
 
 __device__ __forceinline__ void fill_bn_fwd(BnFwd* t, int count, int first,

@@ -194,8 +194,8 @@ bool tc2_conv1x1_fwd(Block* b, const LayerArgs<float>& a, int l, int* prows, boo
     }
     // the BN_b statistics fold into the last CTA unless split-K (partials
     // come from the reduce pass)
+    if (op.ks > 1) op.a.fold.mode = 0;
     op.a.fold.P = ntiles;
-    if (op.ks > 1 || ntiles > kFoldMaxP) op.a.fold.mode = 0;
     if (folded) *folded = op.a.fold.mode != 0;
     launch2(b, op, dim3(balanced_ctas(ntiles * op.ns * op.ks, num_sms())), aux);
     if (op.ks > 1) {
@@ -268,7 +268,6 @@ bool tc2_conv1x1_dgrad(Block* b, const LayerArgs<float>& a, int l, bool* folded)
     op.nw = nw;
     op.a.fold.P = ntiles;  // BN_a backward sums fold per column tile (grid y)
     op.a.fold.gw = nw;
-    if (ntiles > kFoldMaxP) op.a.fold.mode = 0;
     if (folded) *folded = op.a.fold.mode != 0;
     const int gx = balanced_ctas(ntiles, std::max(1, num_sms() / nn));
     launch2(b, op, dim3(gx, nn), aux);

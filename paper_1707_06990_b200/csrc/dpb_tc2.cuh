@@ -183,9 +183,7 @@ __global__ void __launch_bounds__(Roles<Op>::kThreads, 1) tc2_kernel(const __gri
   // barriers itself, and the ring starts empty.
   int early = 0;
   if constexpr (Op::kEarlyLoads) {
-    // not when the predecessor is the producer of these operands (its BN
-    // finalize folded into it: the operands are one launch old, not two)
-    if (tid == 0 && !op.a.no_early) {
+    if (tid == 0) {
       op.prefetch();
       const int nt = op.num_tiles();
       for (int tile = blockIdx.x; tile < nt && early < NR; tile += gridDim.x)

@@ -190,7 +190,6 @@ int tc_conv3x3_fwd(Block* b, const LayerArgs<float>& a, int l, bool* folded) {
     tc::HaloArgs h = halo_args(a, kc);
     h.wt = b->w2f + static_cast<int64_t>(l) * b->halo.fwd_layer_bytes;
     h.a.fold.P = static_cast<int>(nimg(a) * h.g.tpi);  // one partial row per CTA
-    if (h.a.fold.P > kFoldMaxP) h.a.fold.mode = 0;      // a one-CTA fold of many rows is slower
     if (folded) *folded = h.a.fold.mode != 0;
     const size_t stage = 2ull * (static_cast<size_t>(h.g.R) * kc * 2 + 9ull * bn * kc * 2);
     const int nst = (a.bk + kc - 1) / kc > 1 ? 2 : 1;
@@ -229,7 +228,6 @@ int tc_conv3x3_dgrad(Block* b, const LayerArgs<float>& a, int l, bool* folded) {
     tc::HaloArgs h = halo_args(a, kc);
     h.wt = b->w2b + static_cast<int64_t>(l) * b->halo.bwd_layer_bytes;
     h.a.fold.P = static_cast<int>(nimg(a) * h.g.tpi);
-    if (h.a.fold.P > kFoldMaxP) h.a.fold.mode = 0;
     if (folded) *folded = h.a.fold.mode != 0;
     const size_t stage = static_cast<size_t>(h.g.R) * kc * 2 + 9ull * bn * kc * 2;
     const size_t aux = sizeof(BnFwd) * a.bk;
