@@ -161,12 +161,6 @@ static int64_t zsplit_bytes(const dpb_block_desc& d) {
   return most;
 }
 
-// Counters of the folded finalizes: sites 0-2 and one per 1x1-dgrad column tile from 8.
-static int64_t fold_ctr_bytes(const dpb_block_desc& d) {
-  const int64_t cmax = d.c0 + static_cast<int64_t>(d.m - 1) * d.k;
-  return align_up((8 + cmax / 32 + 2) * 4, 256);
-}
-
 void plan_arena(const dpb_block_desc& d, dpb_arena_sizes* s) {
   const Geometry g = geometry(d);
   std::memset(s, 0, sizeof(*s));
@@ -215,8 +209,7 @@ void plan_arena(const dpb_block_desc& d, dpb_arena_sizes* s) {
   const int64_t pbytes = std::max<int64_t>(static_cast<int64_t>(g.Pmax) * std::max<int64_t>(g.C, d.bk) * 16,
                                           zsplit_bytes(d) > 0 ? (g.M + 31) / 32 * d.bk * 16 : 0);
   const int64_t scratch = align_up(pbytes, 256) + align_up(wmax * 4, 256) +
-                          align_up((4LL * d.bk + 4 * g.cmaxp) * 4, 256) + align_up(zsplit_bytes(d), 256) +
-                          fold_ctr_bytes(d);
+                          align_up((4LL * d.bk + 4 * g.cmaxp) * 4, 256) + align_up(zsplit_bytes(d), 256);
   take(scratch, &s->scratch_offset, &s->scratch_bytes);
   // pre-tiled bf16 weight operands of the tensor-core path (counted as scratch)
   if (d.dtype == DPB_BF16 && tc_supported(d)) {
@@ -311,33 +304,6 @@ static LayerArgs<S> layer_args(Block* b, const float* params, int l) {
   return a;
 }
 
-// Fold specs of the BN finalizes run inside their producers (FoldSpec,
-// dpb_simt.cuh).  site: first counter of the producer (one per channel group).
-static FoldSpec stats_fold(Block* b, int site, int nch, float* mean, int64_t var_off, int first) {
-  FoldSpec f;
-  f.mode = 1;
-  f.counter = b->fold_ctr + site;
-  f.nch = nch;
-  f.gw = nch;
-  f.count = static_cast<double>(b->g.M);
-  f.out_a = mean;
-  f.out_b = mean + var_off;
-  f.first = first;
-  return f;
-}
-static FoldSpec bwd_fold(Block* b, int site, int nch, float* dgamma, float* dbeta, float* coef) {
-  FoldSpec f;
-  f.mode = 2;
-  f.counter = b->fold_ctr + site;
-  f.nch = nch;
-  f.gw = nch;
-  f.count = static_cast<double>(b->g.M);
-  f.out_a = dgamma;
-  f.out_b = dbeta;
-  f.coef = coef;
-  return f;
-}
-
 template <typename S>
 static void forward_impl(Block* b, const float* x_in, const float* params, float* running,
                          int update_running, int eval) {
@@ -400,34 +366,26 @@ static void forward_impl(Block* b, const float* x_in, const float* params, float
     tr.on(0, 7 * l + 5, BlockTrace::kRelu, M * d.bk);
     tr.on(0, 7 * l + 6, BlockTrace::kConv, 2.0 * M * d.k * 9.0 * d.bk);
     int p1 = g.P;  // BN_b partial rows
-    bool folded = false;  // the finalize ran in the producer's last CTA
     {
       LaunchScope ls(b, KC_C1_FWD, M * (a.c + d.bk) * Sb, 2.0 * M * a.c * d.bk, M * (a.c + d.bk) * 2.0);
       if (b->tc) {
-        LayerArgs<S> af = a;  // z statistics of this layer, folded in
-        if (!eval) af.fold = stats_fold(b, 0, d.bk, b->zstat + static_cast<int64_t>(l) * 2 * d.bk, d.bk, 0);
-        if (!tc2_conv1x1_fwd(b, af, l, &p1, &folded)) tc_conv1x1_fwd(b, a);
+        if (!tc2_conv1x1_fwd(b, a, l, &p1)) tc_conv1x1_fwd(b, a);
       }
       else gemm_bn<128, Conv1x1Fwd>(b, a, g.M, d.bk, 1);
     }
-    if (!eval && !folded) {
+    if (!eval) {
       LaunchScope ls(b, KC_FINALIZE, 16.0 * p1 * d.bk, 0, 16.0 * p1 * d.bk);
       float* zm = b->zstat + static_cast<int64_t>(l) * 2 * d.bk;
       launch(k_finalize_stats, static_cast<unsigned>((d.bk + kFinCh - 1) / kFinCh), kFinThreads, 0, b->stream, 
           b->part, p1, d.bk, count, zm, zm + d.bk, 0);
     }
     int p3 = g.P;
-    folded = false;
     {
       LaunchScope ls(b, KC_C3_FWD, M * (d.bk + d.k) * Sb, 2.0 * M * 9 * d.bk * d.k, M * (d.bk + d.k) * 2.0);
-      if (b->tc) {
-        LayerArgs<S> af = a;  // the new k channels' statistics, folded in
-        if (!eval) af.fold = stats_fold(b, 1, d.k, fmean, g.Cp, a.c);
-        p3 = tc_conv3x3_fwd(b, af, l, &folded);
-      }
+      if (b->tc) p3 = tc_conv3x3_fwd(b, a, l);
       else gemm_bn<128, Conv3x3Fwd>(b, a, g.M, d.k, 1);
     }
-    if (!eval && !folded) {
+    if (!eval) {
       LaunchScope ls(b, KC_FINALIZE, 16.0 * p3 * d.k, 0, 16.0 * p3 * d.k);
       launch(k_finalize_stats, static_cast<unsigned>((d.k + kFinCh - 1) / kFinCh), kFinThreads, 0, b->stream, 
           b->part, p3, d.k, count, fmean, fvar, a.c);
@@ -542,18 +500,13 @@ static void backward_impl(Block* b, const float* params, float* grad_acc, float*
     b->stream = main_st;
     // ---- data chain: 3x3 dgrad (+ReLU mask by act_b, BN_b sums) ----
     int pd = g.P;
-    bool folded = false;  // the BN backward finalize ran in the producer's last CTA
     {
       LaunchScope ls(b, KC_C3_DGRAD, M * (4.0 * d.k + Sb * d.bk + 4.0 * d.bk), f3, M * (4.0 * d.k + 2.0 * d.bk + 4.0 * d.bk));
-      if (b->tc) {
-        LayerArgs<S> af = a;
-        af.fold = bwd_fold(b, 2, d.bk, d_gb, d_bb, const_cast<float*>(a.bnb_bwd));
-        pd = tc_conv3x3_dgrad(b, af, l, &folded);
-      }
+      if (b->tc) pd = tc_conv3x3_dgrad(b, a, l);
       else gemm_bn<128, Conv3x3Dgrad>(b, a, g.M, d.bk, 1);
     }
     // BN_b backward sums -> dgamma_b, dbeta_b, coefficients (graph.hpp:913-916)
-    if (!folded) {
+    {
       LaunchScope ls(b, KC_FINALIZE, 16.0 * pd * d.bk, 0, 16.0 * pd * d.bk);
       launch(k_finalize_bn_bwd, static_cast<unsigned>((d.bk + kFinCh - 1) / kFinCh), kFinThreads, 0, b->stream, 
           b->part, pd, d.bk, count, d_gb, d_bb, const_cast<float*>(a.bnb_bwd));
@@ -594,16 +547,13 @@ static void backward_impl(Block* b, const float* params, float* grad_acc, float*
     {
       LaunchScope ls(b, KC_C1_DGRAD, M * ((4.0 + Sb) * d.bk + (Sb + 4.0) * a.c), f1, M * ((4.0 + 2.0) * d.bk + (2.0 + 4.0) * a.c));
       if (b->tc) {
-        LayerArgs<S> af = a;  // BN_a backward sums folded per column tile
-        af.fold = bwd_fold(b, 8, a.c, d_ga, d_ba, b->bna_bwd + (l & 1) * 2 * g.cmaxp);
-        folded = false;
-        if (!tc2_conv1x1_dgrad(b, af, l, &folded)) tc_conv1x1_dgrad(b, a);
+        if (!tc2_conv1x1_dgrad(b, a, l)) tc_conv1x1_dgrad(b, a);
       }
       else gemm_bn2<128, Conv1x1Dgrad>(b, a, g.M, a.c, 1);
     }
     // BN_a backward (graph.hpp:929-932) + concat-backward accumulate (:936-941)
     float* bna = b->bna_bwd + (l & 1) * 2 * g.cmaxp;  // parity buffer (split_apply)
-    if (!(b->tc && folded)) {
+    {
       LaunchScope ls(b, KC_FINALIZE, 16.0 * g.P * a.c, 0, 16.0 * g.P * a.c);
       launch(k_finalize_bn_bwd, static_cast<unsigned>((a.c + kFinCh - 1) / kFinCh), kFinThreads, 0, b->stream,
              b->part, g.P, a.c, count, d_ga, d_ba, bna);
@@ -787,11 +737,8 @@ int create(const dpb_block_desc* desc, int device, void* stream, Block** out, De
   const int64_t coef_bytes = align_up((4LL * desc->bk + 4 * b->g.cmaxp) * 4, 256);
   const int64_t wt_bytes = b->tc ? weight_image_bytes(*desc) : 0;
   const int64_t zs_bytes = align_up(zsplit_bytes(*desc), 256);
-  const int64_t fc_bytes = fold_ctr_bytes(*desc);
-  b->fold_ctr = reinterpret_cast<int*>(sc + b->sz.scratch_bytes - wt_bytes - fc_bytes);
-  b->bnb_bwd = reinterpret_cast<float*>(sc + b->sz.scratch_bytes - wt_bytes - fc_bytes - zs_bytes - coef_bytes);
-  if (zs_bytes) b->zpart = reinterpret_cast<float*>(sc + b->sz.scratch_bytes - wt_bytes - fc_bytes - zs_bytes);
-  cudaMemset(b->fold_ctr, 0, static_cast<size_t>(fc_bytes));
+  b->bnb_bwd = reinterpret_cast<float*>(sc + b->sz.scratch_bytes - wt_bytes - zs_bytes - coef_bytes);
+  if (zs_bytes) b->zpart = reinterpret_cast<float*>(sc + b->sz.scratch_bytes - wt_bytes - zs_bytes);
   b->bna_bwd = b->bnb_bwd + 4 * desc->bk;
   if (b->tc) {
     // the pre-tiled weight images follow the scratch partials/coefficients

@@ -118,7 +118,6 @@ struct Block {
   double2* part = nullptr;   // per-CTA partial sums
   float* wpart = nullptr;    // split-K weight-gradient partials
   float* zpart = nullptr;    // split-K 1x1 forward partials [ks][M][bk] (null: no split)
-  int* fold_ctr = nullptr;   // last-CTA counters of the folded BN finalizes (zero between launches)
   float* bnb_bwd = nullptr;  // [bk][2] (x2: double-buffered across layers)
   float* bna_bwd = nullptr;  // [cmax][2] (x2: layer parity)
   std::vector<int64_t> param_off, stat_off;
@@ -184,9 +183,8 @@ struct LayerArgs;
 bool tc_supported(const dpb_block_desc& d);
 int64_t tc_wgrad_chunk(int64_t M, int64_t tiles);
 void tc_conv1x1_fwd(Block* b, const LayerArgs<float>& a);
-// folded: the op's BN finalize (a.fold) ran in its last CTA
-int tc_conv3x3_fwd(Block* b, const LayerArgs<float>& a, int l, bool* folded = nullptr);    // returns partial rows
-int tc_conv3x3_dgrad(Block* b, const LayerArgs<float>& a, int l, bool* folded = nullptr);  // returns partial rows
+int tc_conv3x3_fwd(Block* b, const LayerArgs<float>& a, int l);    // returns partial rows
+int tc_conv3x3_dgrad(Block* b, const LayerArgs<float>& a, int l);  // returns partial rows
 HaloPlan tc_halo_plan(const dpb_block_desc& d);
 void tc_pretile_w2(Block* b, const float* params, bool fwd);
 int64_t tc_halo_partials(const dpb_block_desc& d);
@@ -194,14 +192,14 @@ int64_t tc_halo_wgrad_splits(const dpb_block_desc& d);
 void tc_conv1x1_dgrad(Block* b, const LayerArgs<float>& a);
 int tc_conv1x1_wgrad(Block* b, LayerArgs<float> a);
 // prows: BN_b partial rows written (left unchanged = the 128-row tile count)
-bool tc2_conv1x1_fwd(Block* b, const LayerArgs<float>& a, int l, int* prows = nullptr, bool* folded = nullptr);
+bool tc2_conv1x1_fwd(Block* b, const LayerArgs<float>& a, int l, int* prows = nullptr);
 int tc2_fwd_ksplit(int64_t M, int c, int sms, int ns);
 int64_t tc2_w1_tile_bytes(const dpb_block_desc& d, int l);
 void tc2_pretile_w1(Block* b, const float* params);
 int tc2_bwd_bn(const dpb_block_desc& d);
 int64_t tc2_w1b_layer_bytes(const dpb_block_desc& d, int l);
 void tc2_pretile_w1t(Block* b, const float* params);
-bool tc2_conv1x1_dgrad(Block* b, const LayerArgs<float>& a, int l, bool* folded = nullptr);
+bool tc2_conv1x1_dgrad(Block* b, const LayerArgs<float>& a, int l);
 int64_t tc2_wgrad_wpart_elems(const dpb_block_desc& d, int l);
 int tc2_conv1x1_wgrad(Block* b, const LayerArgs<float>& a);
 int tc_conv3x3_wgrad(Block* b, LayerArgs<float> a);

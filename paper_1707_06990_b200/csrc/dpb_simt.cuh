@@ -126,79 +126,6 @@ __global__ void __launch_bounds__(kThreads) gemm_kernel(Op op) {
 }
 
 // ---------------------------------------------------------------------------
-// The BN finalize folded into its producer: the last CTA of the producer's
-// grid (per channel group) folds the partial rows in fixed order and writes
-// the statistics / the BN-backward results, so no separate finalize launch
-// sits between the producer and its consumer.  mode 0: not folded (the host
-// launches k_finalize_*).
-struct FoldSpec {
-  int mode = 0;            // 1: forward statistics (mean, biased var); 2: BN backward
-  int* counter = nullptr;  // per group; zero between launches (the folding CTA resets it)
-  int P = 0;               // partial rows
-  int nch = 0;             // channels (row length of the partials)
-  int gw = 0;              // channels per group: group g = [g*gw, min(nch, (g+1)*gw))
-  double count = 0.0;      // elements per channel (N*H*W)
-  float* out_a = nullptr;  // mode 1: mean (at first + ch); mode 2: dgamma
-  float* out_b = nullptr;  // mode 1: var (at first + ch);  mode 2: dbeta
-  float* coef = nullptr;   // mode 2: [nch][2] mg, mgx
-  int first = 0;           // mode 1: output channel offset
-};
-
-// Called by every thread of every CTA at the end of a producer kernel whose
-// partial rows are written.  `group` / `ctas` select the CTA's channel group
-// and how many CTAs write it; `scratch` is >= blockDim.x double2 of dead
-// shared memory.  Deterministic: the fold order is fixed (the k_finalize_*
-// kernels' semantics, dpb_kernels.cuh).
-__device__ __forceinline__ void fold_tail(const FoldSpec& f, const double2* part, int group, int ctas,
-                                          double2* scratch) {
-  __shared__ int s_last;
-  __threadfence();  // this thread's partial stores before the ticket
-  __syncthreads();
-  if (threadIdx.x == 0) s_last = atomicAdd(f.counter + group, 1) == ctas - 1;
-  __syncthreads();
-  if (!s_last) return;
-  __threadfence();
-  const int c0 = group * f.gw;
-  const int n = (f.nch - c0 < f.gw ? f.nch - c0 : f.gw);
-  for (int cb = 0; cb < n; cb += blockDim.x) {
-    const int nc = n - cb < static_cast<int>(blockDim.x) ? n - cb : static_cast<int>(blockDim.x);
-    const int lanes = static_cast<int>(blockDim.x) / nc;
-    const int ch = threadIdx.x % nc, lane = threadIdx.x / nc;
-    double a = 0.0, b = 0.0;
-    if (lane < lanes)
-      for (int p = lane; p < f.P; p += lanes) {
-        const double2 v = part[static_cast<int64_t>(p) * f.nch + c0 + cb + ch];
-        a += v.x;
-        b += v.y;
-      }
-    if (lane < lanes) scratch[lane * nc + ch] = make_double2(a, b);
-    __syncthreads();
-    if (lane == 0) {
-      double sa = 0.0, sb = 0.0;
-      for (int i = 0; i < lanes; ++i) {
-        sa += scratch[i * nc + ch].x;
-        sb += scratch[i * nc + ch].y;
-      }
-      const int c = c0 + cb + ch;
-      if (f.mode == 1) {
-        const double mean = sa / f.count;
-        double var = sb / f.count - mean * mean;
-        if (var < 0.0) var = 0.0;
-        f.out_a[f.first + c] = static_cast<float>(mean);
-        f.out_b[f.first + c] = static_cast<float>(var);
-      } else {
-        f.out_a[c] = static_cast<float>(sb);  // dgamma = sum g*xhat (ops.hpp:229-230)
-        f.out_b[c] = static_cast<float>(sa);  // dbeta = sum g
-        f.coef[2 * c] = static_cast<float>(sa / f.count);
-        f.coef[2 * c + 1] = static_cast<float>(sb / f.count);
-      }
-    }
-    __syncthreads();
-  }
-  if (threadIdx.x == 0) f.counter[group] = 0;  // ready for the next launch (stream order)
-}
-
-// ---------------------------------------------------------------------------
 // Layer arguments shared by every op of one bottleneck layer.
 template <typename S>
 struct LayerArgs {
@@ -224,7 +151,6 @@ struct LayerArgs {
   double2* part;        // per-CTA partial sums
   float* wpart;         // split-K weight-gradient partials
   int64_t kchunk;       // pixels per split for the wgrad ops
-  FoldSpec fold;        // the producer's BN finalize, folded into its last CTA (mode 0: none)
 };
 
 __device__ __forceinline__ void fill_bn_fwd(BnFwd* t, int count, int first,

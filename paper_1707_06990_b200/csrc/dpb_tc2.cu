@@ -162,7 +162,7 @@ int tc2_fwd_ksplit(int64_t M, int c, int sms, int ns) {
 
 // 1x1 forward on the v2 engine; false when the shape is not supported (the
 // caller then uses the v1 kernel).
-bool tc2_conv1x1_fwd(Block* b, const LayerArgs<float>& a, int l, int* prows, bool* folded) {
+bool tc2_conv1x1_fwd(Block* b, const LayerArgs<float>& a, int l, int* prows) {
   if (a.C % 4 != 0 || !b->wtile) return false;
   const int ntiles = static_cast<int>((a.M + tc::kBM - 1) / tc::kBM);
   const uint8_t* w1t = b->wtile + b->wtile_off[l];
@@ -192,11 +192,6 @@ bool tc2_conv1x1_fwd(Block* b, const LayerArgs<float>& a, int l, int* prows, boo
       }
       op.nw = op.bimg / op.ns;
     }
-    // the BN_b statistics fold into the last CTA unless split-K (partials
-    // come from the reduce pass)
-    if (op.ks > 1) op.a.fold.mode = 0;
-    op.a.fold.P = ntiles;
-    if (folded) *folded = op.a.fold.mode != 0;
     launch2(b, op, dim3(balanced_ctas(ntiles * op.ns * op.ks, num_sms())), aux);
     if (op.ks > 1) {
       const int zb = static_cast<int>((a.M + tc2::kZRows - 1) / tc2::kZRows);
@@ -247,7 +242,7 @@ void tc2_pretile_w1t(Block* b, const float* params) {
   b->launches++;
 }
 
-bool tc2_conv1x1_dgrad(Block* b, const LayerArgs<float>& a, int l, bool* folded) {
+bool tc2_conv1x1_dgrad(Block* b, const LayerArgs<float>& a, int l) {
   if (a.C % 4 != 0 || a.cg % 4 != 0 || !b->w1b) return false;
   const int ntiles = static_cast<int>((a.M + tc::kBM - 1) / tc::kBM);
   auto go = [&](auto tag) -> bool {
@@ -266,9 +261,6 @@ bool tc2_conv1x1_dgrad(Block* b, const LayerArgs<float>& a, int l, bool* folded)
     int nn, nw;
     tc2::bwd_ntiles(a.c, Op::BN, nn, nw);
     op.nw = nw;
-    op.a.fold.P = ntiles;  // BN_a backward sums fold per column tile (grid y)
-    op.a.fold.gw = nw;
-    if (folded) *folded = op.a.fold.mode != 0;
     const int gx = balanced_ctas(ntiles, std::max(1, num_sms() / nn));
     launch2(b, op, dim3(gx, nn), aux);
     return true;

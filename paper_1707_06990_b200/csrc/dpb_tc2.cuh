@@ -369,12 +369,6 @@ __global__ void __launch_bounds__(Roles<Op>::kThreads, 1) tc2_kernel(const __gri
     tc::tc_fence_after();
     tc::tmem_dealloc<2 * TC>(tmem);
   }
-  // the BN finalize, folded into the last CTA (per column group for ops whose
-  // grid y is the column tile); the rings are dead: their shared memory is scratch
-  if (op.a.fold.mode)
-    fold_tail(op.a.fold, op.a.part, Op::kFoldByY ? static_cast<int>(blockIdx.y) : 0,
-              Op::kFoldByY ? static_cast<int>(gridDim.x) : static_cast<int>(gridDim.x * gridDim.y),
-              reinterpret_cast<double2*>(smem));
   if (dbg && tid == 0) clk[22] = dbg_now();
 }
 
@@ -388,7 +382,6 @@ __global__ void __launch_bounds__(Roles<Op>::kThreads, 1) tc2_kernel(const __gri
 template <int BN_, bool RES>
 struct Fwd1x1 {
   static constexpr int BN = BN_;
-  static constexpr bool kFoldByY = false;
   static constexpr int kTmemCols = BN;
   static constexpr bool kEarlyLoads = true;  // features / g0 / z: >= two launches old
   static constexpr bool kColSums = true;
@@ -642,7 +635,6 @@ __host__ __device__ inline int bwd_nkb(int bk) { return (bk + 31) / 32; }
 template <int BN_, int NE_ = 5>
 struct Dgrad1x1 {
   static constexpr int BN = BN_;
-  static constexpr bool kFoldByY = true;  // grid y = column tile = channel group
   static constexpr int kTmemCols = BN;
   static constexpr bool kEarlyLoads = true;  // g0 (3x3 dgrad) and z: >= two launches old
   static constexpr bool kColSums = true;
@@ -779,7 +771,6 @@ struct Dgrad1x1 {
 // width); k_reduce_w1 folds the splits.  graph.hpp:920-922, ops.hpp:330-387.
 template <int BN_, int JB>
 struct Wgrad1x1 {
-  static constexpr bool kFoldByY = false;
   static constexpr int BN = BN_;
   static constexpr int kMT = (JB * 32 + 127) / 128;
   static constexpr int kTmemCols = kMT * BN;

@@ -183,14 +183,12 @@ void tc_pretile_w2(Block* b, const float* params, bool fwd) {
 }
 
 // Returns the number of per-CTA partial rows written (for the finalize).
-int tc_conv3x3_fwd(Block* b, const LayerArgs<float>& a, int l, bool* folded) {
+int tc_conv3x3_fwd(Block* b, const LayerArgs<float>& a, int l) {
   const int bn = pick_bn(a.k);
   if (b->halo.fwd_ok && b->w2f) {
     const int kc = b->halo.fwd_kc;
     tc::HaloArgs h = halo_args(a, kc);
     h.wt = b->w2f + static_cast<int64_t>(l) * b->halo.fwd_layer_bytes;
-    h.a.fold.P = static_cast<int>(nimg(a) * h.g.tpi);  // one partial row per CTA
-    if (folded) *folded = h.a.fold.mode != 0;
     const size_t stage = 2ull * (static_cast<size_t>(h.g.R) * kc * 2 + 9ull * bn * kc * 2);
     const int nst = (a.bk + kc - 1) / kc > 1 ? 2 : 1;
     const size_t aux = sizeof(BnFwd) * a.bk;
@@ -221,14 +219,12 @@ int tc_conv3x3_fwd(Block* b, const LayerArgs<float>& a, int l, bool* folded) {
   return static_cast<int>(mtiles(a.M));
 }
 
-int tc_conv3x3_dgrad(Block* b, const LayerArgs<float>& a, int l, bool* folded) {
+int tc_conv3x3_dgrad(Block* b, const LayerArgs<float>& a, int l) {
   const int bn = pick_bn(a.bk);
   const int kc = round_up(a.k, 16);
   if (b->halo.bwd_ok && b->w2b) {
     tc::HaloArgs h = halo_args(a, kc);
     h.wt = b->w2b + static_cast<int64_t>(l) * b->halo.bwd_layer_bytes;
-    h.a.fold.P = static_cast<int>(nimg(a) * h.g.tpi);
-    if (folded) *folded = h.a.fold.mode != 0;
     const size_t stage = static_cast<size_t>(h.g.R) * kc * 2 + 9ull * bn * kc * 2;
     const size_t aux = sizeof(BnFwd) * a.bk;
     {

@@ -248,9 +248,6 @@ __global__ void __launch_bounds__(kThreads, Op::kMinBlocks) tc_halo_kernel(const
     tc_fence_after();
     tmem_dealloc<TCOLS>(tmem);
   }
-  // the BN finalize, folded into the last CTA (the stages are dead: scratch)
-  if (op.h.a.fold.mode)
-    fold_tail(op.h.a.fold, op.h.a.part, 0, static_cast<int>(gridDim.x * gridDim.y), reinterpret_cast<double2*>(smem));
   if (dbg) g_phase_clock[dbg_id][8] = clock64();
 }
 
