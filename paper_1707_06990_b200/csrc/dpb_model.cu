@@ -593,6 +593,231 @@ struct TransGemm {
   __device__ void col_sums(int, double, double) const {}
 };
 
+// The ImageNet stem conv (7x7 stride 2 pad 3) on the tcgen05 engine for the
+// tensor-core path: y[p][o] = sum_t im2col(x)[p][t] W[o][t] over the cin*49
+// taps (K padded to 64-multiples with zeros), fp16x3 products like every
+// forward GEMM (dpb_tc.cuh split8_h), fp32 accumulation; the producer gathers
+// the im2col tile straight from the NCHW input.  The epilogue stores y (NHWC,
+// pitch c0) and the BN column sums of the 128-row tile (part[tile][c]: the
+// layout k_channel_partials writes, folded by the same finalize).  The fp32
+// path keeps k_stem7_conv.
+template <int BN_>
+struct StemConvGemm {
+  static constexpr int BN = BN_;
+  static constexpr bool kSplit = true, kF16 = true, kColSums = true;
+  static constexpr int kAMN = 0, kBMN = 0;
+  const float* x;
+  const float* w;
+  float* y;
+  double2* part;
+  int cin, H, W, Ho, Wo, c0;
+  int64_t M1;
+
+  __device__ int num_kb() const { return (cin * kS7Taps + tc::kBK - 1) / tc::kBK; }
+  __device__ void prologue(uint8_t*) const {}
+  __device__ void produce(uint8_t* a_hi, uint8_t* a_lo, uint8_t* b_hi, uint8_t* b_lo, int kb,
+                          const uint8_t*) const {
+    const int k0 = kb * tc::kBK, nt = cin * kS7Taps;
+    for (int q = threadIdx.x; q < tc::kBM * tc::kBK / 8; q += tc::kThreads) {
+      int row, kc;
+      tc::kmajor_coords(q, row, kc);
+      const int64_t p = static_cast<int64_t>(blockIdx.x) * tc::kBM + row;
+      float v[8];
+      if (p < M1) {
+        const int hw = Ho * Wo;
+        const int n = static_cast<int>(p / hw);
+        const int r = static_cast<int>(p - static_cast<int64_t>(n) * hw);
+        const int oy = r / Wo, ox = r - (r / Wo) * Wo;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          const int t = k0 + kc + i;
+          float xv = 0.f;
+          if (t < nt) {
+            const int ci = t / kS7Taps, tap = t - ci * kS7Taps;
+            const int iy = 2 * oy - 3 + tap / kS7, ix = 2 * ox - 3 + tap % kS7;
+            if (iy >= 0 && iy < H && ix >= 0 && ix < W)
+              xv = __ldg(x + ((static_cast<int64_t>(n) * cin + ci) * H + iy) * W + ix);
+          }
+          v[i] = xv;
+        }
+      } else {
+#pragma unroll
+        for (int i = 0; i < 8; ++i) v[i] = 0.f;
+      }
+      uint4 h, l;
+      tc::split8_h(v, h, l);
+      const uint32_t off = tc::Tile<tc::kBM>::kmajor_chunk(row, kc);
+      tc::st_shared16(a_hi, off, h);
+      tc::st_shared16(a_lo, off, l);
+    }
+    for (int q = threadIdx.x; q < BN * tc::kBK / 8; q += tc::kThreads) {
+      int row, kc;
+      tc::kmajor_coords(q, row, kc);
+      float v[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const int t = k0 + kc + i;
+        v[i] = (row < c0 && t < nt) ? __ldg(w + static_cast<int64_t>(row) * nt + t) : 0.f;
+      }
+      uint4 h, l;
+      tc::split8_h(v, h, l);
+      const uint32_t off = tc::Tile<BN>::kmajor_chunk(row, kc);
+      tc::st_shared16(b_hi, off, h);
+      tc::st_shared16(b_lo, off, l);
+    }
+  }
+  __device__ void epilogue(int row, int col0, const float (&v)[8], const uint8_t*, float (&s1)[8],
+                           float (&s2)[8]) const {
+    const int64_t p = static_cast<int64_t>(blockIdx.x) * tc::kBM + row;
+    const int nv = p < M1 ? (c0 - col0 < 8 ? c0 - col0 : 8) : 0;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const bool ok = i < nv;
+      s1[i] = ok ? v[i] : 0.f;
+      s2[i] = ok ? v[i] * v[i] : 0.f;
+    }
+    if (nv > 0) {
+      float* dst = y + p * c0 + col0;
+      if (nv == 8 && (c0 & 3) == 0) {
+        reinterpret_cast<float4*>(dst)[0] = make_float4(v[0], v[1], v[2], v[3]);
+        reinterpret_cast<float4*>(dst)[1] = make_float4(v[4], v[5], v[6], v[7]);
+      } else {
+        for (int i = 0; i < nv; ++i) dst[i] = v[i];
+      }
+    }
+  }
+  __device__ void col_sums(int c, double s1, double s2) const {
+    if (c < c0) part[static_cast<int64_t>(blockIdx.x) * c0 + c] = make_double2(s1, s2);
+  }
+};
+
+// The stem dW on the tcgen05 engine (bf16 path, c0 % 8 == 0, c0 <= 128,
+// cin*49 <= 160): dW[o][t] = sum_p G[p][o] im2col(x)[p][t], K = pixels split
+// over blockIdx.z (partials wpart[z][o][t], folded by launch_fold_splits).
+// A rows = the c0 channels of G = gamma*inv*(g - mg - xhat*mgx) (ops.hpp:232-241,
+// g the ReLU-masked max-pool gradient summed in window order exactly like
+// stem_pool_grad_at), built in the producer from y1, the pool argmax and the
+// block-0 input gradient; B rows = the cin*49 taps gathered from the NCHW
+// image.  Both MN-major; single bf16 products like the other backward GEMMs.
+struct StemWgradGemm {
+  static constexpr int BN = 160;
+  static constexpr bool kSplit = false, kF16 = false, kColSums = false;
+  static constexpr int kAMN = 1, kBMN = 1;
+  const float* x;    // NCHW image
+  const float* y1;   // stem conv output [M1][c0]
+  const float* g0;   // block-0 input gradient, pitch ld0
+  const uint8_t* arg;
+  const float *mean, *var, *gamma, *beta, *coef;
+  float* wpart;
+  int cin, H, W, Ho, Wo, H0, W0, c0, ld0;
+  int64_t M1, kchunk;
+
+  __device__ int64_t kbeg() const { return static_cast<int64_t>(blockIdx.z) * kchunk; }
+  __device__ int64_t kend() const { return kbeg() + kchunk < M1 ? kbeg() + kchunk : M1; }
+  __device__ int num_kb() const { return static_cast<int>((kend() - kbeg() + tc::kBK - 1) / tc::kBK); }
+  __device__ void prologue(uint8_t* aux) const {
+    float* tab = reinterpret_cast<float*>(aux);  // per channel: mean, inv, gamma, beta, mg, mgx
+    for (int c = threadIdx.x; c < c0; c += tc::kThreads) {
+      tab[6 * c] = mean[c];
+      tab[6 * c + 1] = bn_inv(var[c]);
+      tab[6 * c + 2] = gamma[c];
+      tab[6 * c + 3] = beta[c];
+      tab[6 * c + 4] = coef[2 * c];
+      tab[6 * c + 5] = coef[2 * c + 1];
+    }
+  }
+  __device__ void produce(uint8_t* ah, uint8_t*, uint8_t* bh, uint8_t*, int kb, const uint8_t* aux) const {
+    const float* tab = reinterpret_cast<const float*>(aux);
+    const int64_t pk = kbeg() + static_cast<int64_t>(kb) * tc::kBK, pe = kend();
+    const int hw = Ho * Wo, nt = cin * kS7Taps;
+    // A: 8 channels of G at one pixel (rows >= c0 stay zero after each stage's first fill)
+    for (int q = threadIdx.x; q < tc::kBM * tc::kBK / 8; q += tc::kThreads) {
+      int rg, kr;
+      tc::mnmajor_coords<tc::kBM>(q, rg, kr);
+      if (rg >= c0 && kb >= 2) continue;
+      const int64_t p = pk + kr;
+      float v[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) v[i] = 0.f;
+      if (p < pe && rg < c0) {
+        const int pi = static_cast<int>(p);
+        const int n = pi / hw, r = pi - (pi / hw) * hw;
+        const int iy = r / Wo, ix = r - (r / Wo) * Wo;
+        float g[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) g[i] = 0.f;
+        const int oy1 = min((iy + 1) / 2, H0 - 1), ox1 = min((ix + 1) / 2, W0 - 1);
+        for (int oy = iy / 2; oy <= oy1; ++oy)
+          for (int ox = ix / 2; ox <= ox1; ++ox) {
+            const uint32_t t = static_cast<uint32_t>((iy - 2 * oy + 1) * 3 + (ix - 2 * ox + 1));
+            const int64_t qq = (static_cast<int64_t>(n) * H0 + oy) * W0 + ox;
+            const uint2 a8 = __ldg(reinterpret_cast<const uint2*>(arg + qq * c0 + rg));
+            float gv[8];
+            tc::load8(g0 + qq * ld0 + rg, 8, (ld0 & 3) == 0, gv);
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+              const uint32_t ai = ((i < 4 ? a8.x : a8.y) >> (8 * (i & 3))) & 0xFFu;
+              if (ai == t) g[i] += gv[i];
+            }
+          }
+        float yv[8];
+        tc::load8(y1 + p * c0 + rg, 8, true, yv);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          const float* tc_ = tab + 6 * (rg + i);
+          const float mu = tc_[0], inv = tc_[1], ga = tc_[2], be = tc_[3];
+          const float gi = bn_ref(yv[i], mu, inv, ga, be) > 0.f ? g[i] : 0.f;
+          v[i] = ga * inv * (gi - tc_[4] - ((yv[i] - mu) * inv) * tc_[5]);
+        }
+      }
+      tc::st_shared16(ah, tc::Tile<tc::kBM>::mnmajor_chunk(rg, kr), tc::to_bf16x8(v));
+    }
+    // B: 8 consecutive taps at one pixel, gathered from the image
+    for (int q = threadIdx.x; q < BN * tc::kBK / 8; q += tc::kThreads) {
+      int rg, kr;
+      tc::mnmajor_coords<BN>(q, rg, kr);
+      if (rg >= nt && kb >= 2) continue;
+      const int64_t p = pk + kr;
+      float v[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) v[i] = 0.f;
+      if (p < pe && rg < nt) {
+        const int pi = static_cast<int>(p);
+        const int n = pi / hw, r = pi - (pi / hw) * hw;
+        const int oy = r / Wo, ox = r - (r / Wo) * Wo;
+        int ci = rg / kS7Taps, tap = rg - ci * kS7Taps;
+        int ky = tap / kS7, kx = tap - ky * kS7;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          if (rg + i < nt) {
+            const int iy = 2 * oy - 3 + ky, ix = 2 * ox - 3 + kx;
+            if (iy >= 0 && iy < H && ix >= 0 && ix < W)
+              v[i] = __ldg(x + ((static_cast<int64_t>(n) * cin + ci) * H + iy) * W + ix);
+          }
+          if (++kx == kS7) {
+            kx = 0;
+            if (++ky == kS7) {
+              ky = 0;
+              ++ci;
+            }
+          }
+        }
+      }
+      tc::st_shared16(bh, tc::Tile<BN>::mnmajor_chunk(rg, kr), tc::to_bf16x8(v));
+    }
+  }
+  __device__ void epilogue(int row, int col0, const float (&v)[8], const uint8_t*, float (&)[8],
+                           float (&)[8]) const {
+    const int nt = cin * kS7Taps;
+    const int nv = row < c0 ? nt - col0 : 0;
+    if (nv > 0) {
+      float* dst = wpart + (static_cast<int64_t>(blockIdx.z) * c0 + row) * nt + col0;
+      for (int i = 0; i < 8 && i < nv; ++i) dst[i] = v[i];
+    }
+  }
+  __device__ void col_sums(int, double, double) const {}
+};
+
 template <int BMN>
 void trans_gemm(cudaStream_t st, int M, int N, int K, const float* A, int lda, const float* B, int ldb,
                 float* D, int ldd) {
@@ -1392,10 +1617,22 @@ int model_step_launch(dpb_model* m, const float* input, const int32_t* labels, c
   ModelBlock& b0 = m->blocks[0];
   if (d.stem == 1) {
     const int c0p = (d.c0 + 31) / 32 * 32;
-    launch(k_stem7_conv, dim3(blocks_of(N * m->H1 * ((m->W1 + 1) / 2), 128), static_cast<unsigned>(c0p / 32)), 128,
-           sizeof(float) * d.in_c * kS7Taps * c0p, st, input, N, d.in_c, d.in_h, d.in_w, m->H1, m->W1, params, d.c0,
-           m->y1);
-    launch_channel_partials(st, m->y1, d.c0, m->M1, d.c0, m->spart);
+    auto tc_stem = [&](auto tag) {
+      using Op = decltype(tag);
+      const Op op{input, params, m->y1, m->spart, d.in_c, d.in_h, d.in_w, m->H1, m->W1, d.c0, m->M1};
+      launch(tc::tc_gemm_kernel<Op>, dim3(static_cast<unsigned>(m->P1)), tc::kThreads, tc::stage_bytes<Op>(), st,
+             op);
+    };
+    if (d.dtype == DPB_BF16 && d.c0 <= 64) {
+      tc_stem(StemConvGemm<64>{});  // y and its BN partials in one pass
+    } else if (d.dtype == DPB_BF16 && d.c0 <= 128) {
+      tc_stem(StemConvGemm<128>{});
+    } else {
+      launch(k_stem7_conv, dim3(blocks_of(N * m->H1 * ((m->W1 + 1) / 2), 128), static_cast<unsigned>(c0p / 32)),
+             128, sizeof(float) * d.in_c * kS7Taps * c0p, st, input, N, d.in_c, d.in_h, d.in_w, m->H1, m->W1,
+             params, d.c0, m->y1);
+      launch_channel_partials(st, m->y1, d.c0, m->M1, d.c0, m->spart);
+    }
     launch_finalize_stats(st, m->spart, static_cast<int>(m->P1), d.c0, static_cast<double>(m->M1), m->sstat,
                           m->sstat + d.c0);
     launch(k_running, blocks_of(d.c0, 256), 256, 0, st, d.c0, static_cast<const float*>(m->sstat),
@@ -1545,6 +1782,18 @@ int model_step_launch(dpb_model* m, const float* input, const int32_t* labels, c
              static_cast<const float*>(mb.acc), mb.Cp, static_cast<const uint8_t*>(m->arg), chunk, m->part);
       launch_finalize_bn_bwd(st, m->part, S, d.c0, static_cast<double>(m->M1), grads + m->stem_gamma,
                              grads + m->stem_beta, m->coef);
+      const int64_t pkb = (m->M1 + tc::kBK - 1) / tc::kBK;
+      if (d.dtype == DPB_BF16 && d.c0 % 8 == 0 && d.c0 <= tc::kBM && d.in_c * kS7Taps <= StemWgradGemm::BN &&
+          mb.Cp % 4 == 0) {
+        const int64_t per = (pkb + kStem7Splits - 1) / kStem7Splits;
+        const int S7 = static_cast<int>((pkb + per - 1) / per);
+        const StemWgradGemm op{input, m->y1, mb.acc, m->arg, mean, var, params + m->stem_gamma,
+                               params + m->stem_beta, m->coef, m->wpart, d.in_c, d.in_h, d.in_w, m->H1, m->W1,
+                               mb.h, mb.w, d.c0, mb.Cp, m->M1, per * tc::kBK};
+        launch(tc::tc_gemm_kernel<StemWgradGemm>, dim3(1, 1, static_cast<unsigned>(S7)), tc::kThreads,
+               tc::stage_bytes<StemWgradGemm>() + sizeof(float) * 6 * d.c0, st, op);
+        launch_fold_splits(st, m->wpart, S7, static_cast<int64_t>(d.c0) * d.in_c * kS7Taps, grads);
+      } else {
       const int ty7 = (m->H1 + kS7TH - 1) / kS7TH, tx7 = (m->W1 + kS7TW - 1) / kS7TW;
       const int64_t ntiles = N * ty7 * tx7;
       const int64_t per = (ntiles + kStem7Splits - 1) / kStem7Splits;
@@ -1555,6 +1804,7 @@ int model_step_launch(dpb_model* m, const float* input, const int32_t* labels, c
              params + m->stem_gamma, params + m->stem_beta, static_cast<const float*>(mb.acc), mb.Cp, mb.h, mb.w,
              static_cast<const uint8_t*>(m->arg), static_cast<const float*>(m->coef), per, m->wpart);
       launch_fold_splits(st, m->wpart, S7, static_cast<int64_t>(d.c0) * d.in_c * kS7Taps, grads);
+      }
     } else {
       const int chunk = stem_chunk(d.c0, d.in_c);
       const int S = static_cast<int>((mb.M + chunk - 1) / chunk);
