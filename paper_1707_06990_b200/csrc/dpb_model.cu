@@ -229,6 +229,57 @@ __global__ void k_stem_pool(const float* __restrict__ y, int64_t N, int H1, int 
   arg[q * c0 + c] = static_cast<uint8_t>(bt);
 }
 
+// k_stem_pool for c0 % 4 == 0 (and a 16-byte aligned block-input pitch):
+// thread = (window q, 4 channels), float4 loads of y, the 3x3 window's nine
+// loads issued together; the same first-maximum rule per channel.
+__global__ void k_stem_pool4(const float* __restrict__ y, int nq, int H1, int W1, int H0, int W0, int c0,
+                             const float* __restrict__ mean, const float* __restrict__ var,
+                             const float* __restrict__ gamma, const float* __restrict__ beta,
+                             float* __restrict__ x0, int ld0, uint8_t* __restrict__ arg) {
+  pdl_enter();
+  const int cq = c0 / 4;
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= nq * cq) return;
+  const int q = i / cq, c = (i - q * cq) * 4;
+  const int hw0 = H0 * W0;
+  const int n = q / hw0, r = q - n * hw0;
+  const int oy = r / W0, ox = r - (r / W0) * W0;
+  const float4 mu = __ldg(reinterpret_cast<const float4*>(mean + c));
+  const float4 vr = __ldg(reinterpret_cast<const float4*>(var + c));
+  const float4 ga = __ldg(reinterpret_cast<const float4*>(gamma + c));
+  const float4 be = __ldg(reinterpret_cast<const float4*>(beta + c));
+  const float inv[4] = {bn_inv(vr.x), bn_inv(vr.y), bn_inv(vr.z), bn_inv(vr.w)};
+  float4 win[9];
+#pragma unroll
+  for (int t = 0; t < 9; ++t) {
+    const int iy = 2 * oy - 1 + t / 3, ix = 2 * ox - 1 + t % 3;
+    win[t] = (iy >= 0 && iy < H1 && ix >= 0 && ix < W1)
+                 ? __ldg(reinterpret_cast<const float4*>(y + ((static_cast<int64_t>(n) * H1 + iy) * W1 + ix) * c0 + c))
+                 : make_float4(0.f, 0.f, 0.f, 0.f);
+  }
+  float best[4] = {0.f, 0.f, 0.f, 0.f};
+  int bt[4] = {-1, -1, -1, -1};
+#pragma unroll
+  for (int t = 0; t < 9; ++t) {
+    const int iy = 2 * oy - 1 + t / 3, ix = 2 * ox - 1 + t % 3;
+    if (iy < 0 || iy >= H1 || ix < 0 || ix >= W1) continue;
+    const float w4[4] = {win[t].x, win[t].y, win[t].z, win[t].w};
+    const float m4[4] = {mu.x, mu.y, mu.z, mu.w}, g4[4] = {ga.x, ga.y, ga.z, ga.w}, b4[4] = {be.x, be.y, be.z, be.w};
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const float v = fmaxf(bn_ref(w4[j], m4[j], inv[j], g4[j], b4[j]), 0.f);
+      if (bt[j] < 0 || v > best[j]) {
+        best[j] = v;
+        bt[j] = t;
+      }
+    }
+  }
+  *reinterpret_cast<float4*>(x0 + static_cast<int64_t>(q) * ld0 + c) = make_float4(best[0], best[1], best[2], best[3]);
+  *reinterpret_cast<uchar4*>(arg + static_cast<int64_t>(q) * c0 + c) =
+      make_uchar4(static_cast<uint8_t>(bt[0]), static_cast<uint8_t>(bt[1]), static_cast<uint8_t>(bt[2]),
+                  static_cast<uint8_t>(bt[3]));
+}
+
 // Gradient w.r.t. relu(bn(y)) at conv-output pixel p, channel c: the pooled
 // gradients g0[q][c] of every window q containing p whose first maximum is p,
 // summed in window order (the order the reference-side scatter adds them).
@@ -297,6 +348,95 @@ __global__ void __launch_bounds__(256) k_stem_bnb_partials(const float* __restri
       b += r2[i][lane];
     }
     part[static_cast<int64_t>(blockIdx.x) * c0 + c] = make_double2(a, b);
+  }
+}
+
+// k_stem_bnb_partials for c0 % 4 == 0 that also stores the masked max-pool
+// gradient gm[p][c] = relu'(bn(y)) * stem_pool_grad (dense, pitch c0) for the
+// tensor-core dW (StemWgradGemm reads it instead of redoing the gather).
+// Thread = (pixel lane, 4 channels): the up-to-four windows' argmax and
+// gradient loads are issued together (branch-free), then summed in window
+// order (oy, ox ascending: stem_pool_grad_at's order, so g is bit-identical).
+// Partials part[cta][c] folded over the pixel lanes in fixed order.
+constexpr int kGatherThreads = 256;
+__global__ void __launch_bounds__(kGatherThreads) k_stem_bnb_gather(
+    const float* __restrict__ y, int64_t M1, int H1, int W1, int H0, int W0, int c0, const float* __restrict__ mean,
+    const float* __restrict__ var, const float* __restrict__ gamma, const float* __restrict__ beta,
+    const float* __restrict__ g0, int ld0, const uint8_t* __restrict__ arg, int64_t chunk, float* __restrict__ gm,
+    double2* __restrict__ part) {
+  pdl_enter();
+  extern __shared__ double gred[];  // [2][PL][c0]
+  const int cq = c0 / 4, PL = kGatherThreads / cq;
+  const int lane = threadIdx.x % cq, pl = threadIdx.x / cq;
+  const int c = lane * 4;
+  double s1[4] = {0.0, 0.0, 0.0, 0.0}, s2[4] = {0.0, 0.0, 0.0, 0.0};
+  if (pl < PL) {
+    const float4 mu4 = __ldg(reinterpret_cast<const float4*>(mean + c));
+    const float4 vr4 = __ldg(reinterpret_cast<const float4*>(var + c));
+    const float4 ga4 = __ldg(reinterpret_cast<const float4*>(gamma + c));
+    const float4 be4 = __ldg(reinterpret_cast<const float4*>(beta + c));
+    const float mu[4] = {mu4.x, mu4.y, mu4.z, mu4.w}, ga[4] = {ga4.x, ga4.y, ga4.z, ga4.w};
+    const float be[4] = {be4.x, be4.y, be4.z, be4.w};
+    const float inv[4] = {bn_inv(vr4.x), bn_inv(vr4.y), bn_inv(vr4.z), bn_inv(vr4.w)};
+    const int hw1 = H1 * W1;
+    const int64_t p0 = static_cast<int64_t>(blockIdx.x) * chunk;
+    const int64_t p1 = p0 + chunk < M1 ? p0 + chunk : M1;
+#pragma unroll 2
+    for (int64_t p = p0 + pl; p < p1; p += PL) {
+      const int pi = static_cast<int>(p);
+      const int n = pi / hw1, r = pi - n * hw1;
+      const int iy = r / W1, ix = r - (r / W1) * W1;
+      const float4 y4 = __ldg(reinterpret_cast<const float4*>(y + p * c0 + c));
+      const int oya = iy / 2, oxa = ix / 2;
+      const int oyb = min((iy + 1) / 2, H0 - 1), oxb = min((ix + 1) / 2, W0 - 1);
+      uint32_t a[4];
+      float4 gv[4];
+      int tt[4];
+      bool ok[4];
+#pragma unroll
+      for (int w = 0; w < 4; ++w) {  // window order (oya,oxa) (oya,oxb) (oyb,oxa) (oyb,oxb)
+        const int oy = w < 2 ? oya : oyb, ox = (w & 1) ? oxb : oxa;
+        ok[w] = (w < 2 || oyb != oya) && (!(w & 1) || oxb != oxa);
+        tt[w] = (iy - 2 * oy + 1) * 3 + (ix - 2 * ox + 1);
+        const int64_t q = (static_cast<int64_t>(n) * H0 + oy) * W0 + ox;
+        a[w] = ok[w] ? __ldg(reinterpret_cast<const uint32_t*>(arg + q * c0 + c)) : 0xFFFFFFFFu;
+        gv[w] = ok[w] ? __ldg(reinterpret_cast<const float4*>(g0 + q * ld0 + c)) : make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+      float g[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+      for (int w = 0; w < 4; ++w) {
+        const float v4[4] = {gv[w].x, gv[w].y, gv[w].z, gv[w].w};
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+          if (ok[w] && static_cast<int>((a[w] >> (8 * j)) & 0xFFu) == tt[w]) g[j] += v4[j];
+      }
+      const float yv[4] = {y4.x, y4.y, y4.z, y4.w};
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        if (!(bn_ref(yv[j], mu[j], inv[j], ga[j], be[j]) > 0.f)) g[j] = 0.f;  // relu_backward (ops.hpp:268-287)
+        s1[j] += g[j];
+        s2[j] += g[j] * ((yv[j] - mu[j]) * inv[j]);
+      }
+      *reinterpret_cast<float4*>(gm + p * c0 + c) = make_float4(g[0], g[1], g[2], g[3]);
+    }
+  }
+  double* r1 = gred;
+  double* r2 = gred + PL * c0;
+  if (pl < PL) {
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      r1[pl * c0 + c + j] = s1[j];
+      r2[pl * c0 + c + j] = s2[j];
+    }
+  }
+  __syncthreads();
+  for (int ch = threadIdx.x; ch < c0; ch += kGatherThreads) {
+    double x = 0.0, z = 0.0;
+    for (int l = 0; l < PL; ++l) {
+      x += r1[l * c0 + ch];
+      z += r2[l * c0 + ch];
+    }
+    part[static_cast<int64_t>(blockIdx.x) * c0 + ch] = make_double2(x, z);
   }
 }
 
@@ -618,6 +758,7 @@ struct StemConvGemm {
   __device__ void produce(uint8_t* a_hi, uint8_t* a_lo, uint8_t* b_hi, uint8_t* b_lo, int kb,
                           const uint8_t*) const {
     const int k0 = kb * tc::kBK, nt = cin * kS7Taps;
+#pragma unroll
     for (int q = threadIdx.x; q < tc::kBM * tc::kBK / 8; q += tc::kThreads) {
       int row, kc;
       tc::kmajor_coords(q, row, kc);
@@ -650,6 +791,7 @@ struct StemConvGemm {
       tc::st_shared16(a_hi, off, h);
       tc::st_shared16(a_lo, off, l);
     }
+#pragma unroll
     for (int q = threadIdx.x; q < BN * tc::kBK / 8; q += tc::kThreads) {
       int row, kc;
       tc::kmajor_coords(q, row, kc);
@@ -695,9 +837,8 @@ struct StemConvGemm {
 // cin*49 <= 160): dW[o][t] = sum_p G[p][o] im2col(x)[p][t], K = pixels split
 // over blockIdx.z (partials wpart[z][o][t], folded by launch_fold_splits).
 // A rows = the c0 channels of G = gamma*inv*(g - mg - xhat*mgx) (ops.hpp:232-241,
-// g the ReLU-masked max-pool gradient summed in window order exactly like
-// stem_pool_grad_at), built in the producer from y1, the pool argmax and the
-// block-0 input gradient; B rows = the cin*49 taps gathered from the NCHW
+// g the ReLU-masked max-pool gradient k_stem_bnb_gather stored), built in the
+// producer from y1 and g; B rows = the cin*49 taps gathered from the NCHW
 // image.  Both MN-major; single bf16 products like the other backward GEMMs.
 struct StemWgradGemm {
   static constexpr int BN = 160;
@@ -705,11 +846,10 @@ struct StemWgradGemm {
   static constexpr int kAMN = 1, kBMN = 1;
   const float* x;    // NCHW image
   const float* y1;   // stem conv output [M1][c0]
-  const float* g0;   // block-0 input gradient, pitch ld0
-  const uint8_t* arg;
+  const float* gm;   // masked max-pool gradient [M1][c0] (k_stem_bnb_gather)
   const float *mean, *var, *gamma, *beta, *coef;
   float* wpart;
-  int cin, H, W, Ho, Wo, H0, W0, c0, ld0;
+  int cin, H, W, Ho, Wo, c0;
   int64_t M1, kchunk;
 
   __device__ int64_t kbeg() const { return static_cast<int64_t>(blockIdx.z) * kchunk; }
@@ -731,6 +871,7 @@ struct StemWgradGemm {
     const int64_t pk = kbeg() + static_cast<int64_t>(kb) * tc::kBK, pe = kend();
     const int hw = Ho * Wo, nt = cin * kS7Taps;
     // A: 8 channels of G at one pixel (rows >= c0 stay zero after each stage's first fill)
+#pragma unroll
     for (int q = threadIdx.x; q < tc::kBM * tc::kBK / 8; q += tc::kThreads) {
       int rg, kr;
       tc::mnmajor_coords<tc::kBM>(q, rg, kr);
@@ -740,26 +881,8 @@ struct StemWgradGemm {
 #pragma unroll
       for (int i = 0; i < 8; ++i) v[i] = 0.f;
       if (p < pe && rg < c0) {
-        const int pi = static_cast<int>(p);
-        const int n = pi / hw, r = pi - (pi / hw) * hw;
-        const int iy = r / Wo, ix = r - (r / Wo) * Wo;
         float g[8];
-#pragma unroll
-        for (int i = 0; i < 8; ++i) g[i] = 0.f;
-        const int oy1 = min((iy + 1) / 2, H0 - 1), ox1 = min((ix + 1) / 2, W0 - 1);
-        for (int oy = iy / 2; oy <= oy1; ++oy)
-          for (int ox = ix / 2; ox <= ox1; ++ox) {
-            const uint32_t t = static_cast<uint32_t>((iy - 2 * oy + 1) * 3 + (ix - 2 * ox + 1));
-            const int64_t qq = (static_cast<int64_t>(n) * H0 + oy) * W0 + ox;
-            const uint2 a8 = __ldg(reinterpret_cast<const uint2*>(arg + qq * c0 + rg));
-            float gv[8];
-            tc::load8(g0 + qq * ld0 + rg, 8, (ld0 & 3) == 0, gv);
-#pragma unroll
-            for (int i = 0; i < 8; ++i) {
-              const uint32_t ai = ((i < 4 ? a8.x : a8.y) >> (8 * (i & 3))) & 0xFFu;
-              if (ai == t) g[i] += gv[i];
-            }
-          }
+        tc::load8(gm + p * c0 + rg, 8, true, g);
         float yv[8];
         tc::load8(y1 + p * c0 + rg, 8, true, yv);
 #pragma unroll
@@ -773,6 +896,7 @@ struct StemWgradGemm {
       tc::st_shared16(ah, tc::Tile<tc::kBM>::mnmajor_chunk(rg, kr), tc::to_bf16x8(v));
     }
     // B: 8 consecutive taps at one pixel, gathered from the image
+#pragma unroll
     for (int q = threadIdx.x; q < BN * tc::kBK / 8; q += tc::kThreads) {
       int rg, kr;
       tc::mnmajor_coords<BN>(q, rg, kr);
@@ -1164,6 +1288,7 @@ struct dpb_model {
   float* y1 = nullptr;
   uint8_t* arg = nullptr;
   double2* spart = nullptr;
+  float* gm = nullptr;  // stem: masked max-pool gradient (tensor-core dW path)
   float* sstat = nullptr;  // mean[c0] | var[c0]
   // CUDA graph of the whole step, replayed while the step's buffers stay the same
   cudaGraphExec_t graph = nullptr;
@@ -1461,8 +1586,11 @@ DPB_API int dpb_model_create(const dpb_model_desc* desc, int device, void* strea
   m->wpart_elems = stem_splits * desc->c0 * desc->in_c * 9;
   if (desc->stem == 1)
     m->wpart_elems = std::max<int64_t>(m->wpart_elems, kStem7Splits * desc->c0 * desc->in_c * kS7Taps);
-  int64_t o_y1 = 0, o_arg = 0, o_spart = 0, o_sstat = 0;
+  int64_t o_y1 = 0, o_arg = 0, o_spart = 0, o_sstat = 0, o_gm = -1;
   if (desc->stem == 1) {
+    if (desc->dtype == DPB_BF16 && desc->c0 % 8 == 0 && desc->c0 <= tc::kBM &&
+        desc->in_c * kS7Taps <= StemWgradGemm::BN && m->blocks[0].Cp % 4 == 0)
+      o_gm = take(m->M1 * desc->c0);  // masked max-pool gradient for the tensor-core dW
     o_y1 = take(m->M1 * desc->c0, DPB_ARENA_FEATURE_OWNED);  // stem conv output (reused for its gradient)
     o_arg = take((m->blocks[0].M * desc->c0 + 3) / 4, DPB_ARENA_FEATURE_OWNED);  // max-pool taps
     o_spart = take(4 * m->P1 * desc->c0);
@@ -1509,6 +1637,7 @@ DPB_API int dpb_model_create(const dpb_model_desc* desc, int device, void* strea
     m->arg = reinterpret_cast<uint8_t*>(base + o_arg);
     m->spart = reinterpret_cast<double2*>(base + o_spart);
     m->sstat = reinterpret_cast<float*>(base + o_sstat);
+    if (o_gm >= 0) m->gm = reinterpret_cast<float*>(base + o_gm);
   }
   if (cudaStreamCreateWithFlags(&m->side, cudaStreamNonBlocking) != cudaSuccess) m->side = nullptr;
   for (size_t i = 0; m->side && i < m->trans.size() + 1; ++i) {
@@ -1637,9 +1766,17 @@ int model_step_launch(dpb_model* m, const float* input, const int32_t* labels, c
                           m->sstat + d.c0);
     launch(k_running, blocks_of(d.c0, 256), 256, 0, st, d.c0, static_cast<const float*>(m->sstat),
            static_cast<const float*>(m->sstat + d.c0), running, running + d.c0);
-    launch(k_stem_pool, blocks_of(b0.M * d.c0, 256), 256, 0, st, static_cast<const float*>(m->y1), N, m->H1, m->W1,
-           b0.h, b0.w, d.c0, static_cast<const float*>(m->sstat), static_cast<const float*>(m->sstat + d.c0),
-           params + m->stem_gamma, params + m->stem_beta, b0.x, b0.Cp, m->arg);
+    if (d.c0 % 4 == 0 && b0.Cp % 4 == 0) {
+      launch(k_stem_pool4, blocks_of(b0.M * (d.c0 / 4), 256), 256, 0, st, static_cast<const float*>(m->y1),
+             static_cast<int>(b0.M), m->H1, m->W1, b0.h, b0.w, d.c0, static_cast<const float*>(m->sstat),
+             static_cast<const float*>(m->sstat + d.c0), params + m->stem_gamma, params + m->stem_beta, b0.x, b0.Cp,
+             m->arg);
+    } else {
+      launch(k_stem_pool, blocks_of(b0.M * d.c0, 256), 256, 0, st, static_cast<const float*>(m->y1), N, m->H1,
+             m->W1, b0.h, b0.w, d.c0, static_cast<const float*>(m->sstat),
+             static_cast<const float*>(m->sstat + d.c0), params + m->stem_gamma, params + m->stem_beta, b0.x, b0.Cp,
+             m->arg);
+    }
   } else {
     launch(k_stem_fwd, blocks_of(b0.M, 256), 256, sizeof(float) * d.c0 * d.in_c * 9, st, input, N, d.in_c,
            d.in_h, d.in_w, params, d.c0, b0.x, b0.Cp);
@@ -1777,19 +1914,26 @@ int model_step_launch(dpb_model* m, const float* input, const int32_t* labels, c
       const float* var = m->sstat + d.c0;
       int64_t chunk;
       const int S = splits_of(m->M1, chunk, kRowSplitsMax, 16);
-      launch(k_stem_bnb_partials, dim3(S, blocks_of(d.c0, 32)), 256, 0, st, static_cast<const float*>(m->y1), m->M1,
-             m->H1, m->W1, mb.h, mb.w, d.c0, mean, var, params + m->stem_gamma, params + m->stem_beta,
-             static_cast<const float*>(mb.acc), mb.Cp, static_cast<const uint8_t*>(m->arg), chunk, m->part);
+      if (m->gm != nullptr) {
+        const int PL = kGatherThreads / (d.c0 / 4);
+        launch(k_stem_bnb_gather, S, kGatherThreads, sizeof(double) * 2 * PL * d.c0, st,
+               static_cast<const float*>(m->y1), m->M1, m->H1, m->W1, mb.h, mb.w, d.c0, mean, var,
+               params + m->stem_gamma, params + m->stem_beta, static_cast<const float*>(mb.acc), mb.Cp,
+               static_cast<const uint8_t*>(m->arg), chunk, m->gm, m->part);
+      } else {
+        launch(k_stem_bnb_partials, dim3(S, blocks_of(d.c0, 32)), 256, 0, st, static_cast<const float*>(m->y1),
+               m->M1, m->H1, m->W1, mb.h, mb.w, d.c0, mean, var, params + m->stem_gamma, params + m->stem_beta,
+               static_cast<const float*>(mb.acc), mb.Cp, static_cast<const uint8_t*>(m->arg), chunk, m->part);
+      }
       launch_finalize_bn_bwd(st, m->part, S, d.c0, static_cast<double>(m->M1), grads + m->stem_gamma,
                              grads + m->stem_beta, m->coef);
       const int64_t pkb = (m->M1 + tc::kBK - 1) / tc::kBK;
-      if (d.dtype == DPB_BF16 && d.c0 % 8 == 0 && d.c0 <= tc::kBM && d.in_c * kS7Taps <= StemWgradGemm::BN &&
-          mb.Cp % 4 == 0) {
+      if (m->gm != nullptr) {
         const int64_t per = (pkb + kStem7Splits - 1) / kStem7Splits;
         const int S7 = static_cast<int>((pkb + per - 1) / per);
-        const StemWgradGemm op{input, m->y1, mb.acc, m->arg, mean, var, params + m->stem_gamma,
-                               params + m->stem_beta, m->coef, m->wpart, d.in_c, d.in_h, d.in_w, m->H1, m->W1,
-                               mb.h, mb.w, d.c0, mb.Cp, m->M1, per * tc::kBK};
+        const StemWgradGemm op{input, m->y1, m->gm, mean, var, params + m->stem_gamma, params + m->stem_beta,
+                               m->coef, m->wpart, d.in_c, d.in_h, d.in_w, m->H1, m->W1, d.c0, m->M1,
+                               per * tc::kBK};
         launch(tc::tc_gemm_kernel<StemWgradGemm>, dim3(1, 1, static_cast<unsigned>(S7)), tc::kThreads,
                tc::stage_bytes<StemWgradGemm>() + sizeof(float) * 6 * d.c0, st, op);
         launch_fold_splits(st, m->wpart, S7, static_cast<int64_t>(d.c0) * d.in_c * kS7Taps, grads);
