@@ -733,60 +733,129 @@ struct TransGemm {
   __device__ void col_sums(int, double, double) const {}
 };
 
-// The ImageNet stem conv (7x7 stride 2 pad 3) on the tcgen05 engine for the
-// tensor-core path: y[p][o] = sum_t im2col(x)[p][t] W[o][t] over the cin*49
-// taps (K padded to 64-multiples with zeros), fp16x3 products like every
-// forward GEMM (dpb_tc.cuh split8_h), fp32 accumulation; the producer gathers
-// the im2col tile straight from the NCHW input.  The epilogue stores y (NHWC,
-// pitch c0) and the BN column sums of the 128-row tile (part[tile][c]: the
-// layout k_channel_partials writes, folded by the same finalize).  The fp32
-// path keeps k_stem7_conv.
+// ---- the ImageNet stem on the tcgen05 engine (bf16 path) ---------------------------
+// The 7x7 stride-2 pad-3 conv is recast as a stride-1 4x4 conv over the
+// space-to-depth image: phase (py, px) of input channel ci is x[ci][2a+py][2b+px],
+// and tap (ky, kx) of output pixel (oy, ox) reads phase py = (ky+1)&1 at row
+// a = oy + dy with ky = 2*dy + py + 3 (dy in [-2, 1]).  k_stem_s2d writes the
+// phases NHWC, zero-padded (2 rows/columns before, 1 after), 16 channel-phases
+// per position (cp = (py*2+px)*cin + ci, cin <= 4, the rest zero) as 16-byte
+// rows of 8 halves, so every MMA operand chunk of the conv (8 channel-phases of
+// one pixel at one (dy, dx)) is ONE 16-byte load: no per-element im2col
+// arithmetic, no bounds checks.  Three planes: fp16 hi/lo (the forward's fp16x3
+// split, dpb_tc.cuh split8_h) and bf16 (the dW's single bf16 operand).  Tap
+// order t' = ((dy+2)*4 + (dx+2))*16 + cp: K = 256, 49*cin of them real.
+struct StemS2d {
+  int cin, H, W, Ho, Wo;
+  __host__ __device__ int rows() const { return Ho + 3; }
+  __host__ __device__ int cols() const { return Wo + 3; }
+};
+__device__ __forceinline__ bool stem_tap_of(int tp, int cin, int& t) {  // t' -> original ci*49 + ky*7 + kx
+  const int dd = tp >> 4, cp = tp & 15;
+  if (cp >= 4 * cin) return false;
+  const int ph = cp / cin, ci = cp - ph * cin;
+  const int ky = 2 * (dd >> 2) + (ph >> 1) - 1, kx = 2 * (dd & 3) + (ph & 1) - 1;
+  if (ky < 0 || ky >= kS7 || kx < 0 || kx >= kS7) return false;
+  t = ci * kS7Taps + ky * kS7 + kx;
+  return true;
+}
+// Blocks [0, img_blocks): thread = one padded position (n, a, b) -> its 16
+// channel-phases in the three planes.  Blocks past them: thread = one (o, t')
+// of the forward weights in the same tap order (fp16 hi/lo, rows of 256).
+__global__ void k_stem_s2d(const float* __restrict__ x, int64_t N, StemS2d g, const float* __restrict__ w, int c0,
+                           int wrows, int img_blocks, uint4* __restrict__ xh, uint4* __restrict__ xl,
+                           uint4* __restrict__ xb, __half* __restrict__ wh, __half* __restrict__ wl) {
+  pdl_enter();
+  if (static_cast<int>(blockIdx.x) >= img_blocks) {
+    const int i = (blockIdx.x - img_blocks) * blockDim.x + threadIdx.x;
+    if (i >= wrows * 256) return;
+    const int o = i >> 8, tp = i & 255;
+    int t;
+    const float v = (o < c0 && stem_tap_of(tp, g.cin, t)) ? w[static_cast<int64_t>(o) * g.cin * kS7Taps + t] : 0.f;
+    const __half h = __float2half_rn(v);
+    wh[i] = h;
+    wl[i] = __float2half_rn(v - __half2float(h));
+    return;
+  }
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int64_t per = static_cast<int64_t>(g.rows()) * g.cols();
+  if (i >= N * per) return;
+  const int n = static_cast<int>(i / per);
+  const int r = static_cast<int>(i - n * per);
+  const int a = r / g.cols(), b = r - (r / g.cols()) * g.cols();
+  float v[16];
+#pragma unroll
+  for (int cp = 0; cp < 16; ++cp) {
+    v[cp] = 0.f;
+    if (cp < 4 * g.cin) {
+      const int ph = cp / g.cin, ci = cp - ph * g.cin;
+      const int iy = 2 * (a - 2) + (ph >> 1), ix = 2 * (b - 2) + (ph & 1);
+      if (iy >= 0 && iy < g.H && ix >= 0 && ix < g.W)
+        v[cp] = __ldg(x + ((static_cast<int64_t>(n) * g.cin + ci) * g.H + iy) * g.W + ix);
+    }
+  }
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    float e[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) e[j] = v[8 * h + j];
+    uint4 hi, lo;
+    tc::split8_h(e, hi, lo);
+    xh[2 * i + h] = hi;
+    xl[2 * i + h] = lo;
+    xb[2 * i + h] = tc::to_bf16x8(e);
+  }
+}
+
+// y[p][o] = sum_t' s2d(x)[p][t'] W'[o][t'], fp16x3 (hi.hi + hi.lo + lo.hi), fp32
+// accumulate; K = 256 in four blocks (kb = dy + 2, the 16 B chunk at K offset
+// kc = (dx + 2)*16 + 8*half).  The epilogue stores y (NHWC, pitch c0) and the
+// tile's BN column sums (part[tile][c]: k_channel_partials' layout, folded by
+// the same finalize).
 template <int BN_>
 struct StemConvGemm {
   static constexpr int BN = BN_;
   static constexpr bool kSplit = true, kF16 = true, kColSums = true;
   static constexpr int kAMN = 0, kBMN = 0;
-  const float* x;
-  const float* w;
+  const uint4 *xh, *xl;    // s2d planes (16-byte rows)
+  const uint4 *wh, *wl;    // W' [BN][256] halves
   float* y;
   double2* part;
-  int cin, H, W, Ho, Wo, c0;
+  StemS2d g;
+  int c0;
   int64_t M1;
 
-  __device__ int num_kb() const { return (cin * kS7Taps + tc::kBK - 1) / tc::kBK; }
-  __device__ void prologue(uint8_t*) const {}
+  __device__ int num_kb() const { return 4; }
+  __device__ void prologue(uint8_t* aux) const {
+    int* base = reinterpret_cast<int*>(aux);  // per tile row: 16-byte row index of (n, oy, ox) at dy = dx = -2
+    const int hw = g.Ho * g.Wo;
+    for (int row = threadIdx.x; row < tc::kBM; row += tc::kThreads) {
+      const int64_t p = static_cast<int64_t>(blockIdx.x) * tc::kBM + row;
+      int v = -1;
+      if (p < M1) {
+        const int pi = static_cast<int>(p);
+        const int n = pi / hw, r = pi - n * hw;
+        const int oy = r / g.Wo, ox = r - (r / g.Wo) * g.Wo;
+        v = ((n * g.rows() + oy) * g.cols() + ox) * 2;
+      }
+      base[row] = v;
+    }
+  }
   __device__ void produce(uint8_t* a_hi, uint8_t* a_lo, uint8_t* b_hi, uint8_t* b_lo, int kb,
-                          const uint8_t*) const {
-    const int k0 = kb * tc::kBK, nt = cin * kS7Taps;
+                          const uint8_t* aux) const {
+    const int* base = reinterpret_cast<const int*>(aux);
+    const int rowstep = kb * g.cols() * 2;
 #pragma unroll
     for (int q = threadIdx.x; q < tc::kBM * tc::kBK / 8; q += tc::kThreads) {
       int row, kc;
       tc::kmajor_coords(q, row, kc);
-      const int64_t p = static_cast<int64_t>(blockIdx.x) * tc::kBM + row;
-      float v[8];
-      if (p < M1) {
-        const int hw = Ho * Wo;
-        const int n = static_cast<int>(p / hw);
-        const int r = static_cast<int>(p - static_cast<int64_t>(n) * hw);
-        const int oy = r / Wo, ox = r - (r / Wo) * Wo;
-#pragma unroll
-        for (int i = 0; i < 8; ++i) {
-          const int t = k0 + kc + i;
-          float xv = 0.f;
-          if (t < nt) {
-            const int ci = t / kS7Taps, tap = t - ci * kS7Taps;
-            const int iy = 2 * oy - 3 + tap / kS7, ix = 2 * ox - 3 + tap % kS7;
-            if (iy >= 0 && iy < H && ix >= 0 && ix < W)
-              xv = __ldg(x + ((static_cast<int64_t>(n) * cin + ci) * H + iy) * W + ix);
-          }
-          v[i] = xv;
-        }
-      } else {
-#pragma unroll
-        for (int i = 0; i < 8; ++i) v[i] = 0.f;
+      const int b0 = base[row];
+      uint4 h = make_uint4(0, 0, 0, 0), l = h;
+      if (b0 >= 0) {
+        const int idx = b0 + rowstep + (kc >> 4) * 2 + ((kc >> 3) & 1);
+        h = __ldg(xh + idx);
+        l = __ldg(xl + idx);
       }
-      uint4 h, l;
-      tc::split8_h(v, h, l);
       const uint32_t off = tc::Tile<tc::kBM>::kmajor_chunk(row, kc);
       tc::st_shared16(a_hi, off, h);
       tc::st_shared16(a_lo, off, l);
@@ -795,17 +864,10 @@ struct StemConvGemm {
     for (int q = threadIdx.x; q < BN * tc::kBK / 8; q += tc::kThreads) {
       int row, kc;
       tc::kmajor_coords(q, row, kc);
-      float v[8];
-#pragma unroll
-      for (int i = 0; i < 8; ++i) {
-        const int t = k0 + kc + i;
-        v[i] = (row < c0 && t < nt) ? __ldg(w + static_cast<int64_t>(row) * nt + t) : 0.f;
-      }
-      uint4 h, l;
-      tc::split8_h(v, h, l);
+      const int idx = (row * 256 + kb * tc::kBK + kc) >> 3;
       const uint32_t off = tc::Tile<BN>::kmajor_chunk(row, kc);
-      tc::st_shared16(b_hi, off, h);
-      tc::st_shared16(b_lo, off, l);
+      tc::st_shared16(b_hi, off, __ldg(wh + idx));
+      tc::st_shared16(b_lo, off, __ldg(wl + idx));
     }
   }
   __device__ void epilogue(int row, int col0, const float (&v)[8], const uint8_t*, float (&s1)[8],
@@ -818,14 +880,10 @@ struct StemConvGemm {
       s1[i] = ok ? v[i] : 0.f;
       s2[i] = ok ? v[i] * v[i] : 0.f;
     }
-    if (nv > 0) {
-      float* dst = y + p * c0 + col0;
-      if (nv == 8 && (c0 & 3) == 0) {
-        reinterpret_cast<float4*>(dst)[0] = make_float4(v[0], v[1], v[2], v[3]);
-        reinterpret_cast<float4*>(dst)[1] = make_float4(v[4], v[5], v[6], v[7]);
-      } else {
-        for (int i = 0; i < nv; ++i) dst[i] = v[i];
-      }
+    if (nv == 8) {
+      float4* dst = reinterpret_cast<float4*>(y + p * c0 + col0);
+      dst[0] = make_float4(v[0], v[1], v[2], v[3]);
+      dst[1] = make_float4(v[4], v[5], v[6], v[7]);
     }
   }
   __device__ void col_sums(int c, double s1, double s2) const {
@@ -833,23 +891,25 @@ struct StemConvGemm {
   }
 };
 
-// The stem dW on the tcgen05 engine (bf16 path, c0 % 8 == 0, c0 <= 128,
-// cin*49 <= 160): dW[o][t] = sum_p G[p][o] im2col(x)[p][t], K = pixels split
-// over blockIdx.z (partials wpart[z][o][t], folded by launch_fold_splits).
-// A rows = the c0 channels of G = gamma*inv*(g - mg - xhat*mgx) (ops.hpp:232-241,
-// g the ReLU-masked max-pool gradient k_stem_bnb_gather stored), built in the
-// producer from y1 and g; B rows = the cin*49 taps gathered from the NCHW
-// image.  Both MN-major; single bf16 products like the other backward GEMMs.
+// The stem dW: dW[o][t] = sum_p G[p][o] im2col(x)[p][t], K = pixels split over
+// blockIdx.z (partials wpart[z][o][t], folded by launch_fold_splits).  A rows =
+// the c0 channels of G = gamma*inv*(g - mg - xhat*mgx) (ops.hpp:232-241; g the
+// ReLU-masked max-pool gradient k_stem_bnb_gather stored), built in the
+// producer from y1 and g (MN-major: 8 channels of one pixel); B rows = the 256
+// s2d taps (MN-major: 8 channel-phases of one pixel at one (dy, dx) = one
+// 16-byte load of the bf16 plane).  Single bf16 products like the other
+// backward GEMMs.  The epilogue maps t' back to (ci, ky, kx).
 struct StemWgradGemm {
-  static constexpr int BN = 160;
+  static constexpr int BN = 256;
   static constexpr bool kSplit = false, kF16 = false, kColSums = false;
   static constexpr int kAMN = 1, kBMN = 1;
-  const float* x;    // NCHW image
+  const uint4* xb;   // bf16 s2d plane
   const float* y1;   // stem conv output [M1][c0]
-  const float* gm;   // masked max-pool gradient [M1][c0] (k_stem_bnb_gather)
+  const float* gm;   // masked max-pool gradient [M1][c0]
   const float *mean, *var, *gamma, *beta, *coef;
   float* wpart;
-  int cin, H, W, Ho, Wo, c0;
+  StemS2d g;
+  int c0;
   int64_t M1, kchunk;
 
   __device__ int64_t kbeg() const { return static_cast<int64_t>(blockIdx.z) * kchunk; }
@@ -868,8 +928,19 @@ struct StemWgradGemm {
   }
   __device__ void produce(uint8_t* ah, uint8_t*, uint8_t* bh, uint8_t*, int kb, const uint8_t* aux) const {
     const float* tab = reinterpret_cast<const float*>(aux);
+    int* base = const_cast<int*>(reinterpret_cast<const int*>(aux + sizeof(float) * 6 * tc::kBM));
     const int64_t pk = kbeg() + static_cast<int64_t>(kb) * tc::kBK, pe = kend();
-    const int hw = Ho * Wo, nt = cin * kS7Taps;
+    if (threadIdx.x < tc::kBK) {  // this K block's pixels -> s2d row index (the engine's barrier
+      const int64_t p = pk + threadIdx.x;  // after produce(kb - 1) ordered the previous readers)
+      int v = -1;
+      if (p < pe) {
+        const int hw = g.Ho * g.Wo, pi = static_cast<int>(p);
+        const int n = pi / hw, r = pi - n * hw;
+        const int oy = r / g.Wo, ox = r - (r / g.Wo) * g.Wo;
+        v = ((n * g.rows() + oy) * g.cols() + ox) * 2;
+      }
+      base[threadIdx.x] = v;
+    }
     // A: 8 channels of G at one pixel (rows >= c0 stay zero after each stage's first fill)
 #pragma unroll
     for (int q = threadIdx.x; q < tc::kBM * tc::kBK / 8; q += tc::kThreads) {
@@ -881,62 +952,40 @@ struct StemWgradGemm {
 #pragma unroll
       for (int i = 0; i < 8; ++i) v[i] = 0.f;
       if (p < pe && rg < c0) {
-        float g[8];
-        tc::load8(gm + p * c0 + rg, 8, true, g);
-        float yv[8];
+        float gv[8], yv[8];
+        tc::load8(gm + p * c0 + rg, 8, true, gv);
         tc::load8(y1 + p * c0 + rg, 8, true, yv);
 #pragma unroll
         for (int i = 0; i < 8; ++i) {
-          const float* tc_ = tab + 6 * (rg + i);
-          const float mu = tc_[0], inv = tc_[1], ga = tc_[2], be = tc_[3];
-          const float gi = bn_ref(yv[i], mu, inv, ga, be) > 0.f ? g[i] : 0.f;
-          v[i] = ga * inv * (gi - tc_[4] - ((yv[i] - mu) * inv) * tc_[5]);
+          const float* t = tab + 6 * (rg + i);
+          const float mu = t[0], inv = t[1], ga = t[2];
+          v[i] = ga * inv * (gv[i] - t[4] - ((yv[i] - mu) * inv) * t[5]);
         }
       }
       tc::st_shared16(ah, tc::Tile<tc::kBM>::mnmajor_chunk(rg, kr), tc::to_bf16x8(v));
     }
-    // B: 8 consecutive taps at one pixel, gathered from the image
-#pragma unroll
+    __syncthreads();  // the pixel table
+    // B: 8 channel-phases at one (pixel, dy, dx): one 16-byte load
+#pragma unroll 4
     for (int q = threadIdx.x; q < BN * tc::kBK / 8; q += tc::kThreads) {
       int rg, kr;
       tc::mnmajor_coords<BN>(q, rg, kr);
-      if (rg >= nt && kb >= 2) continue;
-      const int64_t p = pk + kr;
-      float v[8];
-#pragma unroll
-      for (int i = 0; i < 8; ++i) v[i] = 0.f;
-      if (p < pe && rg < nt) {
-        const int pi = static_cast<int>(p);
-        const int n = pi / hw, r = pi - (pi / hw) * hw;
-        const int oy = r / Wo, ox = r - (r / Wo) * Wo;
-        int ci = rg / kS7Taps, tap = rg - ci * kS7Taps;
-        int ky = tap / kS7, kx = tap - ky * kS7;
-#pragma unroll
-        for (int i = 0; i < 8; ++i) {
-          if (rg + i < nt) {
-            const int iy = 2 * oy - 3 + ky, ix = 2 * ox - 3 + kx;
-            if (iy >= 0 && iy < H && ix >= 0 && ix < W)
-              v[i] = __ldg(x + ((static_cast<int64_t>(n) * cin + ci) * H + iy) * W + ix);
-          }
-          if (++kx == kS7) {
-            kx = 0;
-            if (++ky == kS7) {
-              ky = 0;
-              ++ci;
-            }
-          }
-        }
-      }
-      tc::st_shared16(bh, tc::Tile<BN>::mnmajor_chunk(rg, kr), tc::to_bf16x8(v));
+      const int b0 = base[kr];
+      const int dd = rg >> 4;
+      const uint4 v = b0 >= 0 ? __ldg(xb + b0 + ((dd >> 2) * g.cols() + (dd & 3)) * 2 + ((rg >> 3) & 1))
+                              : make_uint4(0, 0, 0, 0);
+      tc::st_shared16(bh, tc::Tile<BN>::mnmajor_chunk(rg, kr), v);
     }
   }
   __device__ void epilogue(int row, int col0, const float (&v)[8], const uint8_t*, float (&)[8],
                            float (&)[8]) const {
-    const int nt = cin * kS7Taps;
-    const int nv = row < c0 ? nt - col0 : 0;
-    if (nv > 0) {
-      float* dst = wpart + (static_cast<int64_t>(blockIdx.z) * c0 + row) * nt + col0;
-      for (int i = 0; i < 8 && i < nv; ++i) dst[i] = v[i];
+    if (row >= c0) return;
+    const int nt = g.cin * kS7Taps;
+    float* dst = wpart + (static_cast<int64_t>(blockIdx.z) * c0 + row) * nt;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      int t;
+      if (stem_tap_of(col0 + i, g.cin, t)) dst[t] = v[i];
     }
   }
   __device__ void col_sums(int, double, double) const {}
@@ -1288,7 +1337,13 @@ struct dpb_model {
   float* y1 = nullptr;
   uint8_t* arg = nullptr;
   double2* spart = nullptr;
-  float* gm = nullptr;  // stem: masked max-pool gradient (tensor-core dW path)
+  // the tensor-core stem (bf16 path): space-to-depth image planes (fp16 hi/lo,
+  // bf16), forward weights in s2d tap order, masked max-pool gradient
+  bool tc_stem = false;
+  dpb::StemS2d s2d{};
+  uint4 *xh = nullptr, *xl = nullptr, *xb = nullptr;
+  __half *wh = nullptr, *wl = nullptr;
+  float* gm = nullptr;
   float* sstat = nullptr;  // mean[c0] | var[c0]
   // CUDA graph of the whole step, replayed while the step's buffers stay the same
   cudaGraphExec_t graph = nullptr;
@@ -1586,11 +1641,18 @@ DPB_API int dpb_model_create(const dpb_model_desc* desc, int device, void* strea
   m->wpart_elems = stem_splits * desc->c0 * desc->in_c * 9;
   if (desc->stem == 1)
     m->wpart_elems = std::max<int64_t>(m->wpart_elems, kStem7Splits * desc->c0 * desc->in_c * kS7Taps);
-  int64_t o_y1 = 0, o_arg = 0, o_spart = 0, o_sstat = 0, o_gm = -1;
+  int64_t o_y1 = 0, o_arg = 0, o_spart = 0, o_sstat = 0, o_gm = -1, o_s2d = -1, o_ws2d = -1;
   if (desc->stem == 1) {
-    if (desc->dtype == DPB_BF16 && desc->c0 % 8 == 0 && desc->c0 <= tc::kBM &&
-        desc->in_c * kS7Taps <= StemWgradGemm::BN && m->blocks[0].Cp % 4 == 0)
-      o_gm = take(m->M1 * desc->c0);  // masked max-pool gradient for the tensor-core dW
+    m->s2d = StemS2d{desc->in_c, desc->in_h, desc->in_w, m->H1, m->W1};
+    const int64_t s2d_rows = desc->batch * m->s2d.rows() * m->s2d.cols() * 2;  // 16-byte rows per plane
+    if (desc->dtype == DPB_BF16 && desc->c0 % 8 == 0 && desc->c0 <= tc::kBM && desc->in_c <= 4 &&
+        m->blocks[0].Cp % 4 == 0 && s2d_rows < (int64_t{1} << 31)) {
+      // the tensor-core stem: space-to-depth planes, forward weights, masked pool gradient
+      m->tc_stem = true;
+      o_s2d = take(3 * 4 * s2d_rows);
+      o_ws2d = take(tc::kBM * 256);  // two fp16 planes of [BN][256]
+      o_gm = take(m->M1 * desc->c0);
+    }
     o_y1 = take(m->M1 * desc->c0, DPB_ARENA_FEATURE_OWNED);  // stem conv output (reused for its gradient)
     o_arg = take((m->blocks[0].M * desc->c0 + 3) / 4, DPB_ARENA_FEATURE_OWNED);  // max-pool taps
     o_spart = take(4 * m->P1 * desc->c0);
@@ -1637,7 +1699,15 @@ DPB_API int dpb_model_create(const dpb_model_desc* desc, int device, void* strea
     m->arg = reinterpret_cast<uint8_t*>(base + o_arg);
     m->spart = reinterpret_cast<double2*>(base + o_spart);
     m->sstat = reinterpret_cast<float*>(base + o_sstat);
-    if (o_gm >= 0) m->gm = reinterpret_cast<float*>(base + o_gm);
+    if (m->tc_stem) {
+      m->gm = reinterpret_cast<float*>(base + o_gm);
+      const int64_t rows = desc->batch * m->s2d.rows() * m->s2d.cols() * 2;
+      m->xh = reinterpret_cast<uint4*>(base + o_s2d);
+      m->xl = m->xh + rows;
+      m->xb = m->xl + rows;
+      m->wh = reinterpret_cast<__half*>(base + o_ws2d);
+      m->wl = m->wh + tc::kBM * 256;
+    }
   }
   if (cudaStreamCreateWithFlags(&m->side, cudaStreamNonBlocking) != cudaSuccess) m->side = nullptr;
   for (size_t i = 0; m->side && i < m->trans.size() + 1; ++i) {
@@ -1748,13 +1818,18 @@ int model_step_launch(dpb_model* m, const float* input, const int32_t* labels, c
     const int c0p = (d.c0 + 31) / 32 * 32;
     auto tc_stem = [&](auto tag) {
       using Op = decltype(tag);
-      const Op op{input, params, m->y1, m->spart, d.in_c, d.in_h, d.in_w, m->H1, m->W1, d.c0, m->M1};
-      launch(tc::tc_gemm_kernel<Op>, dim3(static_cast<unsigned>(m->P1)), tc::kThreads, tc::stage_bytes<Op>(), st,
-             op);
+      const int64_t pos = N * m->s2d.rows() * m->s2d.cols();
+      const int img_blocks = static_cast<int>((pos + 255) / 256);
+      launch(k_stem_s2d, img_blocks + Op::BN, 256, 0, st, input, N, m->s2d, params, d.c0, Op::BN, img_blocks,
+             m->xh, m->xl, m->xb, m->wh, m->wl);
+      const Op op{m->xh, m->xl, reinterpret_cast<const uint4*>(m->wh), reinterpret_cast<const uint4*>(m->wl),
+                  m->y1, m->spart, m->s2d, static_cast<int>(d.c0), m->M1};
+      launch(tc::tc_gemm_kernel<Op>, dim3(static_cast<unsigned>(m->P1)), tc::kThreads,
+             tc::stage_bytes<Op>() + sizeof(int) * tc::kBM, st, op);
     };
-    if (d.dtype == DPB_BF16 && d.c0 <= 64) {
+    if (m->tc_stem && d.c0 <= 64) {
       tc_stem(StemConvGemm<64>{});  // y and its BN partials in one pass
-    } else if (d.dtype == DPB_BF16 && d.c0 <= 128) {
+    } else if (m->tc_stem) {
       tc_stem(StemConvGemm<128>{});
     } else {
       launch(k_stem7_conv, dim3(blocks_of(N * m->H1 * ((m->W1 + 1) / 2), 128), static_cast<unsigned>(c0p / 32)),
@@ -1914,7 +1989,7 @@ int model_step_launch(dpb_model* m, const float* input, const int32_t* labels, c
       const float* var = m->sstat + d.c0;
       int64_t chunk;
       const int S = splits_of(m->M1, chunk, kRowSplitsMax, 16);
-      if (m->gm != nullptr) {
+      if (m->tc_stem) {
         const int PL = kGatherThreads / (d.c0 / 4);
         launch(k_stem_bnb_gather, S, kGatherThreads, sizeof(double) * 2 * PL * d.c0, st,
                static_cast<const float*>(m->y1), m->M1, m->H1, m->W1, mb.h, mb.w, d.c0, mean, var,
@@ -1928,14 +2003,13 @@ int model_step_launch(dpb_model* m, const float* input, const int32_t* labels, c
       launch_finalize_bn_bwd(st, m->part, S, d.c0, static_cast<double>(m->M1), grads + m->stem_gamma,
                              grads + m->stem_beta, m->coef);
       const int64_t pkb = (m->M1 + tc::kBK - 1) / tc::kBK;
-      if (m->gm != nullptr) {
+      if (m->tc_stem) {
         const int64_t per = (pkb + kStem7Splits - 1) / kStem7Splits;
         const int S7 = static_cast<int>((pkb + per - 1) / per);
-        const StemWgradGemm op{input, m->y1, m->gm, mean, var, params + m->stem_gamma, params + m->stem_beta,
-                               m->coef, m->wpart, d.in_c, d.in_h, d.in_w, m->H1, m->W1, d.c0, m->M1,
-                               per * tc::kBK};
+        const StemWgradGemm op{m->xb, m->y1, m->gm, mean, var, params + m->stem_gamma, params + m->stem_beta,
+                               m->coef, m->wpart, m->s2d, static_cast<int>(d.c0), m->M1, per * tc::kBK};
         launch(tc::tc_gemm_kernel<StemWgradGemm>, dim3(1, 1, static_cast<unsigned>(S7)), tc::kThreads,
-               tc::stage_bytes<StemWgradGemm>() + sizeof(float) * 6 * d.c0, st, op);
+               tc::stage_bytes<StemWgradGemm>() + sizeof(float) * 6 * tc::kBM + sizeof(int) * tc::kBK, st, op);
         launch_fold_splits(st, m->wpart, S7, static_cast<int64_t>(d.c0) * d.in_c * kS7Taps, grads);
       } else {
       const int ty7 = (m->H1 + kS7TH - 1) / kS7TH, tx7 = (m->W1 + kS7TW - 1) / kS7TW;
