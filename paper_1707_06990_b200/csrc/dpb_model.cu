@@ -991,6 +991,59 @@ struct StemWgradGemm {
   __device__ void col_sums(int, double, double) const {}
 };
 
+// Transition dW partials on the tcgen05 engine (bf16 path): wpart[z][o][c] =
+// sum over pixel chunk z of g_pool[p][o] P[p][c] (graph.hpp transition conv
+// backward; the fp32 path keeps k_gemm<true, false>).  A rows = the cout
+// output channels, B rows = the C input channels, both MN-major (8 channels of
+// one pixel per 16-byte chunk), K = pooled pixels; single bf16 products like
+// the dense layers' dW GEMMs.
+struct TransWgradGemm {
+  static constexpr int BN = 128;
+  static constexpr bool kSplit = false, kF16 = false, kColSums = false;
+  static constexpr int kAMN = 1, kBMN = 1;
+  const float* G;  // [Mq][ldg] pooled-output gradient (channels [0, cout))
+  const float* P;  // [Mq][C] pooled activations
+  float* wpart;
+  int cout, C, ldg;
+  int64_t Mq, kchunk;
+
+  __device__ int64_t kbeg() const { return static_cast<int64_t>(blockIdx.z) * kchunk; }
+  __device__ int64_t kend() const { return kbeg() + kchunk < Mq ? kbeg() + kchunk : Mq; }
+  __device__ int num_kb() const { return static_cast<int>((kend() - kbeg() + tc::kBK - 1) / tc::kBK); }
+  __device__ void prologue(uint8_t*) const {}
+  __device__ void produce(uint8_t* ah, uint8_t*, uint8_t* bh, uint8_t*, int kb, const uint8_t*) const {
+    const int64_t pk = kbeg() + static_cast<int64_t>(kb) * tc::kBK, pe = kend();
+    const int m0 = blockIdx.x * tc::kBM, n0 = blockIdx.y * BN;
+#pragma unroll
+    for (int q = threadIdx.x; q < tc::kBM * tc::kBK / 8; q += tc::kThreads) {
+      int rg, kr;
+      tc::mnmajor_coords<tc::kBM>(q, rg, kr);
+      const int64_t p = pk + kr;
+      float v[8];
+      if (p < pe && m0 + rg < cout) tc::load8(G + p * ldg + m0 + rg, cout - m0 - rg, (ldg & 3) == 0, v);
+      else tc::zero8(v);
+      tc::st_shared16(ah, tc::Tile<tc::kBM>::mnmajor_chunk(rg, kr), tc::to_bf16x8(v));
+    }
+#pragma unroll
+    for (int q = threadIdx.x; q < BN * tc::kBK / 8; q += tc::kThreads) {
+      int rg, kr;
+      tc::mnmajor_coords<BN>(q, rg, kr);
+      const int64_t p = pk + kr;
+      float v[8];
+      if (p < pe && n0 + rg < C) tc::load8(P + p * C + n0 + rg, C - n0 - rg, (C & 3) == 0, v);
+      else tc::zero8(v);
+      tc::st_shared16(bh, tc::Tile<BN>::mnmajor_chunk(rg, kr), tc::to_bf16x8(v));
+    }
+  }
+  __device__ void epilogue(int row, int col0, const float (&v)[8], const uint8_t*, float (&)[8],
+                           float (&)[8]) const {
+    const int o = blockIdx.x * tc::kBM + row, c = blockIdx.y * BN + col0;
+    if (o < cout && c < C)
+      tc::store8(wpart + (static_cast<int64_t>(blockIdx.z) * cout + o) * C + c, C - c, (C & 3) == 0, v);
+  }
+  __device__ void col_sums(int, double, double) const {}
+};
+
 template <int BMN>
 void trans_gemm(cudaStream_t st, int M, int N, int K, const float* A, int lda, const float* B, int ldb,
                 float* D, int ldd) {
@@ -1946,9 +1999,16 @@ int model_step_launch(dpb_model* m, const float* input, const int32_t* labels, c
         cudaStreamWaitEvent(m->side, m->ev[b - 1], 0);
         ws = m->side;
       }
-      launch(k_gemm<true, false>, dim3(blocks_of(t.cout, 64), blocks_of(t.C, 64), S), 256, 0, ws, t.cout, t.C,
-             static_cast<int>(t.Mq), static_cast<const float*>(mb.acc), mb.Cp, static_cast<const float*>(t.P), t.C,
-             t.wpart, t.C, static_cast<int>(chunk));
+      if (d.dtype == DPB_BF16) {
+        const TransWgradGemm op{mb.acc, t.P, t.wpart, t.cout, t.C, mb.Cp, t.Mq, chunk};
+        launch(tc::tc_gemm_kernel<TransWgradGemm>,
+               dim3(blocks_of(t.cout, tc::kBM), blocks_of(t.C, TransWgradGemm::BN), S), tc::kThreads,
+               tc::stage_bytes<TransWgradGemm>(), ws, op);
+      } else {
+        launch(k_gemm<true, false>, dim3(blocks_of(t.cout, 64), blocks_of(t.C, 64), S), 256, 0, ws, t.cout, t.C,
+               static_cast<int>(t.Mq), static_cast<const float*>(mb.acc), mb.Cp, static_cast<const float*>(t.P),
+               t.C, t.wpart, t.C, static_cast<int>(chunk));
+      }
       launch_fold_splits(ws, t.wpart, S, static_cast<int64_t>(t.cout) * t.C, grads + t.w);
       if (dp && m->side) cudaEventRecord(m->ev_tdone[b - 1], m->side);
       if (d.dtype == DPB_BF16)

@@ -434,6 +434,22 @@ __device__ __forceinline__ void st_shared16(uint8_t* base, uint32_t off, uint4 v
   *reinterpret_cast<uint4*>(base + off) = v;
 }
 
+__device__ __forceinline__ void zero8(float (&v)[8]) {
+#pragma unroll
+  for (int i = 0; i < 8; ++i) v[i] = 0.f;
+}
+
+__device__ __forceinline__ void store8(float* p, int n, bool aligned, const float (&v)[8]) {
+  if (aligned && n >= 8) {
+    reinterpret_cast<float4*>(p)[0] = make_float4(v[0], v[1], v[2], v[3]);
+    reinterpret_cast<float4*>(p)[1] = make_float4(v[4], v[5], v[6], v[7]);
+  } else {
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+      if (i < n) p[i] = v[i];
+  }
+}
+
 // 8 consecutive fp32 values, vectorised when 16-byte aligned, zero past `n`.
 __device__ __forceinline__ void load8(const float* p, int n, bool aligned, float (&v)[8]) {
   if (aligned && n >= 8) {

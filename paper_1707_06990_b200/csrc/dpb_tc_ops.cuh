@@ -71,22 +71,6 @@ __device__ __forceinline__ void put8(uint8_t* hi, uint8_t* lo, uint32_t off, con
   }
 }
 
-__device__ __forceinline__ void zero8(float (&v)[8]) {
-#pragma unroll
-  for (int i = 0; i < 8; ++i) v[i] = 0.f;
-}
-
-__device__ __forceinline__ void store8(float* p, int n, bool aligned, const float (&v)[8]) {
-  if (aligned && n >= 8) {
-    reinterpret_cast<float4*>(p)[0] = make_float4(v[0], v[1], v[2], v[3]);
-    reinterpret_cast<float4*>(p)[1] = make_float4(v[4], v[5], v[6], v[7]);
-  } else {
-#pragma unroll
-    for (int i = 0; i < 8; ++i)
-      if (i < n) p[i] = v[i];
-  }
-}
-
 // ---- forward 1x1: z = relu(bn_a(x)) . W1^T, bf16x3 -------------------------------
 template <int BN_>
 struct Tc1x1Fwd {
