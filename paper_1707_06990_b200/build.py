@@ -30,6 +30,8 @@ FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler", 
 # build carries no debug reads on the kernels' critical path.
 if os.environ.get("DPB_PHASE_CLOCKS"):
     FLAGS.append("-DDPB_PHASE_CLOCKS")
+# DPB_EXTRA_FLAGS="-DX ..." (timing experiments only)
+FLAGS += os.environ.get("DPB_EXTRA_FLAGS", "").split()
 
 
 def _deps_mtime() -> float:

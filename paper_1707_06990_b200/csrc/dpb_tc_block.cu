@@ -108,10 +108,14 @@ HaloPlan tc_halo_plan(const dpb_block_desc& d) {
   // fits one CTA.
   // DPB_HALO_KC=<kc> forces a chunk (when it fits).
   static const int force_kc = std::getenv("DPB_HALO_KC") ? std::atoi(std::getenv("DPB_HALO_KC")) : 0;
+  auto fwd_aux = [&](int kc) {  // BN table + the raw fp32 halo ring (Tc3x3FwdHalo::fetch)
+    using Op = tc::Tc3x3FwdHalo<16>;
+    return static_cast<size_t>(Op::raw_offset(static_cast<int>(d.bk))) + Op::kRawDepth * Op::raw_bytes(g.R, kc);
+  };
   auto fwd_fits = [&](int kc, size_t lim) {
     const size_t stage = 2ull * (static_cast<size_t>(g.R) * kc * 2 + 9ull * bn * kc * 2);
     const int nkb = (d.bk + kc - 1) / kc;
-    return stage * (nkb > 1 ? 2 : 1) + sizeof(BnFwd) * d.bk <= lim;
+    return stage * (nkb > 1 ? 2 : 1) + fwd_aux(kc) <= lim;
   };
   int kc_pick = 0;
   // only when the tiles fill more than one wave at one CTA per SM (measured:
@@ -127,7 +131,7 @@ HaloPlan tc_halo_plan(const dpb_block_desc& d) {
     const size_t stage = 2ull * (static_cast<size_t>(g.R) * kc * 2 + 9ull * bn * kc * 2);
     const int nkb = (d.bk + kc - 1) / kc;
     const int nst = nkb > 1 ? 2 : 1;
-    if (stage * nst + sizeof(BnFwd) * d.bk <= kHaloSmemMax) {
+    if (stage * nst + fwd_aux(kc) <= kHaloSmemMax) {
       p.fwd_ok = true;
       p.fwd_bn = bn;
       p.fwd_kc = kc;
@@ -138,14 +142,21 @@ HaloPlan tc_halo_plan(const dpb_block_desc& d) {
       break;
     }
   }
-  const int bnd = pick_bn(d.bk);
+  int bnd = pick_bn(d.bk);
   const int kcd = round_up(d.k, 16);
+  // under two waves of tiles, 64-column groups per tile (grid.y): twice the
+  // CTAs, each with half the epilogue (the dgrad's epilogue is its longest
+  // phase and is latency-bound at one CTA per SM)
+  if (d.bk > 64 && d.bk % 64 == 0 && d.n * g.tpi <= 2 * 148) {
+    p.bwd_split = static_cast<int>(d.bk / 64);
+    bnd = 64;
+  }
   const size_t stage_d = static_cast<size_t>(g.R) * kcd * 2 + 9ull * bnd * kcd * 2;
   if (kcd <= 64 && stage_d + sizeof(BnFwd) * d.bk <= kHaloSmemMax) {
     p.bwd_ok = true;
     p.bwd_bn = bnd;
     p.bwd_kc = kcd;
-    p.bwd_layer_bytes = 9LL * bnd * kcd * 2;
+    p.bwd_layer_bytes = 9LL * bnd * kcd * 2 * p.bwd_split;
   }
   return p;
 }
@@ -170,13 +181,13 @@ void tc_pretile_w2(Block* b, const float* params, bool fwd) {
   }
   if (!fwd && p.bwd_ok && b->w2b) {
     switch (p.bwd_bn) {
-      case 16: launch(tc::k_pretile_w2_bwd<16>, grid, 256, 0, b->stream, params, d.c0, d.k, d.bk, p.bwd_kc, b->w2b); break;
-      case 32: launch(tc::k_pretile_w2_bwd<32>, grid, 256, 0, b->stream, params, d.c0, d.k, d.bk, p.bwd_kc, b->w2b); break;
-      case 48: launch(tc::k_pretile_w2_bwd<48>, grid, 256, 0, b->stream, params, d.c0, d.k, d.bk, p.bwd_kc, b->w2b); break;
-      case 64: launch(tc::k_pretile_w2_bwd<64>, grid, 256, 0, b->stream, params, d.c0, d.k, d.bk, p.bwd_kc, b->w2b); break;
-      case 128: launch(tc::k_pretile_w2_bwd<128>, grid, 256, 0, b->stream, params, d.c0, d.k, d.bk, p.bwd_kc, b->w2b); break;
-      case 192: launch(tc::k_pretile_w2_bwd<192>, grid, 256, 0, b->stream, params, d.c0, d.k, d.bk, p.bwd_kc, b->w2b); break;
-      default: launch(tc::k_pretile_w2_bwd<256>, grid, 256, 0, b->stream, params, d.c0, d.k, d.bk, p.bwd_kc, b->w2b); break;
+      case 16: launch(tc::k_pretile_w2_bwd<16>, grid, 256, 0, b->stream, params, d.c0, d.k, d.bk, p.bwd_kc, p.bwd_split, b->w2b); break;
+      case 32: launch(tc::k_pretile_w2_bwd<32>, grid, 256, 0, b->stream, params, d.c0, d.k, d.bk, p.bwd_kc, p.bwd_split, b->w2b); break;
+      case 48: launch(tc::k_pretile_w2_bwd<48>, grid, 256, 0, b->stream, params, d.c0, d.k, d.bk, p.bwd_kc, p.bwd_split, b->w2b); break;
+      case 64: launch(tc::k_pretile_w2_bwd<64>, grid, 256, 0, b->stream, params, d.c0, d.k, d.bk, p.bwd_kc, p.bwd_split, b->w2b); break;
+      case 128: launch(tc::k_pretile_w2_bwd<128>, grid, 256, 0, b->stream, params, d.c0, d.k, d.bk, p.bwd_kc, p.bwd_split, b->w2b); break;
+      case 192: launch(tc::k_pretile_w2_bwd<192>, grid, 256, 0, b->stream, params, d.c0, d.k, d.bk, p.bwd_kc, p.bwd_split, b->w2b); break;
+      default: launch(tc::k_pretile_w2_bwd<256>, grid, 256, 0, b->stream, params, d.c0, d.k, d.bk, p.bwd_kc, p.bwd_split, b->w2b); break;
     }
     b->launches++;
   }
@@ -191,7 +202,8 @@ int tc_conv3x3_fwd(Block* b, const LayerArgs<float>& a, int l) {
     h.wt = b->w2f + static_cast<int64_t>(l) * b->halo.fwd_layer_bytes;
     const size_t stage = 2ull * (static_cast<size_t>(h.g.R) * kc * 2 + 9ull * bn * kc * 2);
     const int nst = (a.bk + kc - 1) / kc > 1 ? 2 : 1;
-    const size_t aux = sizeof(BnFwd) * a.bk;
+    using FH = tc::Tc3x3FwdHalo<16>;
+    const size_t aux = FH::raw_offset(a.bk) + FH::kRawDepth * FH::raw_bytes(h.g.R, kc);
     if (b->halo.fwd_taps) {
       const dim3 grid(static_cast<unsigned>(nimg(a) * h.g.tpi));
       const size_t np = (9 * a.k + 15) / 16 * 16;
@@ -220,7 +232,7 @@ int tc_conv3x3_fwd(Block* b, const LayerArgs<float>& a, int l) {
 }
 
 int tc_conv3x3_dgrad(Block* b, const LayerArgs<float>& a, int l) {
-  const int bn = pick_bn(a.bk);
+  const int bn = b->halo.bwd_ok ? b->halo.bwd_bn : pick_bn(a.bk);
   const int kc = round_up(a.k, 16);
   if (b->halo.bwd_ok && b->w2b) {
     tc::HaloArgs h = halo_args(a, kc);
@@ -228,7 +240,7 @@ int tc_conv3x3_dgrad(Block* b, const LayerArgs<float>& a, int l) {
     const size_t stage = static_cast<size_t>(h.g.R) * kc * 2 + 9ull * bn * kc * 2;
     const size_t aux = sizeof(BnFwd) * a.bk;
     {
-      const dim3 grid(static_cast<unsigned>(nimg(a) * h.g.tpi));
+      const dim3 grid(static_cast<unsigned>(nimg(a) * h.g.tpi), static_cast<unsigned>(b->halo.bwd_split));
       switch (bn) {
         case 16: launch_halo(b, tc::Tc3x3DgradHalo<16>{h}, grid, stage, 1, aux); break;
         case 32: launch_halo(b, tc::Tc3x3DgradHalo<32>{h}, grid, stage, 1, aux); break;
@@ -332,5 +344,7 @@ extern "C" __attribute__((visibility("default"))) int dpb_debug_phase_clocks(int
     cudaMemcpyToSymbol(dpb::tc::g_phase_on, &on, sizeof(int));
     return 0;
   }
+  if (n < 0)  // per-K-chunk stamps: [cta][8][4]
+    return cudaMemcpyFromSymbol(host, dpb::tc::g_kb_clock, sizeof(long long) * 32 * (-n));
   return cudaMemcpyFromSymbol(host, dpb::tc::g_phase_clock, sizeof(long long) * 9 * n);
 }

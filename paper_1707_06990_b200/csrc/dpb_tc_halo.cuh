@@ -70,6 +70,7 @@ __device__ __forceinline__ uint32_t halo_mnmajor(int R, int j, int pos) {
 // last produce, last issue, MMAs complete, epilogue loop done, epilogue
 // barrier passed, column sums written, exit.
 __device__ long long g_phase_clock[4096][9];
+__device__ long long g_kb_clock[4096][8][4];  // per K chunk: stage free, produced, barrier, weights landed
 __device__ int g_phase_on;
 
 // ---- engine ----------------------------------------------------------------------
@@ -125,12 +126,15 @@ __global__ void __launch_bounds__(kThreads, Op::kMinBlocks) tc_halo_kernel(const
   for (int kb = 0; kb < nkb; ++kb) {
     const int s = kb & 1;
     if (kb >= 2) mbar_wait(&mbar[s], ((kb - 2) >> 1) & 1);
+    if (dbg && kb < 8) g_kb_clock[dbg_id][kb][0] = clock64();
     uint8_t* st = smem + s * SB;
     if constexpr (Op::kBulk)
       if (tid == 0) op.bulk(smem_u32(st), kb, &bbar[s]);
     op.produce(st, kb, aux);
+    if (dbg && kb < 8) g_kb_clock[dbg_id][kb][1] = clock64();
     fence_proxy_async();
     __syncthreads();
+    if (dbg && kb < 8) g_kb_clock[dbg_id][kb][2] = clock64();
     if (dbg && kb == nkb - 1) g_phase_clock[dbg_id][2] = clock64();
     // the MMAs are issued by lane 0 of kIssuers warps in parallel (each into
     // its own accumulator or disjoint columns): a tcgen05.mma issue costs
@@ -138,6 +142,7 @@ __global__ void __launch_bounds__(kThreads, Op::kMinBlocks) tc_halo_kernel(const
     // of these narrow-N MMAs
     if (lane == 0 && warp < Op::kIssuers) {
       if constexpr (Op::kBulk) mbar_wait(&bbar[s], (kb >> 1) & 1);
+      if (dbg && kb < 8) g_kb_clock[dbg_id][kb][3] = clock64();
       tc_fence_after();
       op.issue(smem_u32(st), kb, tmem, warp);
       mma_commit(&mbar[s]);
@@ -188,7 +193,37 @@ __global__ void __launch_bounds__(kThreads, Op::kMinBlocks) tc_halo_kernel(const
     __syncthreads();
   }
   constexpr int kOutCols = Op::kTapCols ? BN : Op::kTmemCols / Op::kAccCopies;  // summed copies
-  for (int cc = half; cc < kOutCols / 8; cc += 2) {
+  if constexpr (Op::kEpiPrefetch > 0) {
+    // the op's per-row global operand (e.g. the dgrad's z) for kEpiPrefetch
+    // column groups is loaded before their TMEM reads: one memory latency per
+    // batch instead of one per group
+    constexpr int PF = Op::kEpiPrefetch;
+    for (int cb = half; cb < kOutCols / 8; cb += 2 * PF) {
+      float pre[PF][8];
+#pragma unroll
+      for (int i = 0; i < PF; ++i)
+        if (cb + 2 * i < kOutCols / 8) op.epi_load(row, (cb + 2 * i) * 8, pre[i]);
+#pragma unroll
+      for (int i = 0; i < PF; ++i) {
+        const int cc = cb + 2 * i;
+        if (cc >= kOutCols / 8) break;
+        float v[8];
+        tmem_ld8(tmem + (static_cast<uint32_t>(quarter * 32) << 16) + cc * 8, v);
+        float s1[8], s2[8];
+        op.epilogue_pre(row, cc * 8, v, aux, pre[i], s1, s2);
+        if constexpr (Op::kColSums) {
+          const float x = warp_colsum8(s1, lane);
+          const float y = warp_colsum8(s2, lane);
+          if ((lane & 3) == 0) {
+            const int col = cc * 8 + colsum8_column(lane);
+            red[0][quarter][col] = x;
+            red[1][quarter][col] = y;
+          }
+        }
+      }
+    }
+  }
+  for (int cc = half; Op::kEpiPrefetch == 0 && cc < kOutCols / 8; cc += 2) {
     float v[8];
     if constexpr (Op::kTapCols) {
       // 16-byte reads (row stride k floats, k % 4 == 0: conflict-free phases)
@@ -305,7 +340,7 @@ __global__ void k_pretile_w2_fwd(const float* __restrict__ params, int c0, int k
 
 // W2^T for the halo dgrad: rows tap*BN + j, K = o (kc = k padded), bf16.
 template <int BN>
-__global__ void k_pretile_w2_bwd(const float* __restrict__ params, int c0, int k, int bk, int kc,
+__global__ void k_pretile_w2_bwd(const float* __restrict__ params, int c0, int k, int bk, int kc, int nh,
                                  uint8_t* __restrict__ out) {
   pdl_enter();
   const int l = blockIdx.y;
@@ -316,16 +351,19 @@ __global__ void k_pretile_w2_bwd(const float* __restrict__ params, int c0, int k
   }
   const int c = c0 + l * k;
   const float* w2 = params + poff + 2 * c + static_cast<int64_t>(bk) * c + 2 * bk;
-  uint8_t* o_l = out + static_cast<int64_t>(l) * 9 * BN * kc * 2;
+  // nh column groups of BN (the dgrad's grid.y), each its own contiguous image
+  uint8_t* o_l = out + static_cast<int64_t>(l) * nh * 9 * BN * kc * 2;
   const int kcn = kc / 8;
-  for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < 9 * BN * kcn; q += gridDim.x * blockDim.x) {
-    const int row = q / kcn, kk = (q % kcn) * 8;
-    const int tap = row / BN, j = row - tap * BN;
+  for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < nh * 9 * BN * kcn; q += gridDim.x * blockDim.x) {
+    const int hg = q / (9 * BN * kcn), qr = q - hg * (9 * BN * kcn);
+    const int row = qr / kcn, kk = (qr % kcn) * 8;
+    const int tap = row / BN, j = hg * BN + row - tap * BN;
     float v[8];
 #pragma unroll
     for (int i = 0; i < 8; ++i)
       v[i] = (j < bk && kk + i < k) ? w2[(static_cast<int64_t>(kk + i) * bk + j) * 9 + tap] : 0.f;
-    *reinterpret_cast<uint4*>(o_l + halo_kmajor(9 * BN, row, kk)) = to_bf16x8(v);
+    *reinterpret_cast<uint4*>(o_l + static_cast<int64_t>(hg) * 9 * BN * kc * 2 + halo_kmajor(9 * BN, row, kk)) =
+        to_bf16x8(v);
   }
 }
 
@@ -347,7 +385,7 @@ struct Tc3x3FwdHalo {
   static constexpr int kMinBlocks = 2;
   static constexpr bool kColSums = true;
   static constexpr bool kBulk = true;
-  static constexpr int kMaxChunks = 5;  // W=32 halos (1188 chunks) in one load batch
+  static constexpr int kEpiPrefetch = 0;  // (see Tc3x3DgradHalo)
   HaloArgs h;
   __device__ uint32_t halo_bytes() const { return static_cast<uint32_t>(h.g.R * h.kc * 2); }
   __device__ uint32_t b_bytes() const { return static_cast<uint32_t>(9 * BN * h.kc * 2); }
@@ -364,43 +402,75 @@ struct Tc3x3FwdHalo {
     bulk_load(st + 2 * halo_bytes(), h.wt + static_cast<int64_t>(kb) * 2 * b_bytes(), 2 * b_bytes(),
               bar);
   }
-  __device__ void produce(uint8_t* st, int kb, const uint8_t* aux) const {
+  // Raw fp32 halo chunks stream through a kRawDepth-deep ring after the BN
+  // table (cp.async, issued one K chunk ahead): chunk kb+1's loads are in
+  // flight while chunk kb is transformed and its MMAs issued, so a K chunk
+  // costs its transform, not a memory latency.  Each thread copies and then
+  // transforms the same chunks (thread-local groups: no barrier).
+  static constexpr int kRawDepth = 2;
+  __host__ __device__ static uint32_t raw_offset(int bk) { return (sizeof(BnFwd) * bk + 127) / 128 * 128; }
+  __host__ __device__ static uint32_t raw_bytes(int R, int kc) { return static_cast<uint32_t>(R) * kc * 4; }
+  __device__ void fetch(int kb, uint8_t* aux) const {
     const LayerArgs<float>& a = h.a;
-    const BnFwd* bn = reinterpret_cast<const BnFwd*>(aux);
-    uint8_t* xh = st;
-    uint8_t* xl = st + halo_bytes();
+    const uint32_t ring = smem_u32(aux + raw_offset(a.bk) + (kb % kRawDepth) * raw_bytes(h.g.R, h.kc));
     const int t = tile();
     const int64_t pix0 = static_cast<int64_t>(img()) * h.g.H * h.g.W;
     const int j_base = kb * h.kc;
     const int kcn = h.kc / 8;
     const int nchunk = h.g.R * kcn;
-    for (int base = 0; base < nchunk; base += kMaxChunks * kThreads) {
-    float v[kMaxChunks][8];
-    int rr[kMaxChunks], kk[kMaxChunks];
-    bool ok[kMaxChunks];
-#pragma unroll
-    for (int i = 0; i < kMaxChunks; ++i) {  // all loads first
-      const int q = base + threadIdx.x + i * kThreads;
-      rr[i] = (q & 7) + 8 * (q / (8 * kcn));
-      kk[i] = ((q >> 3) % kcn) * 8;
-      const int pp = q < nchunk ? h.g.pixel(h.g.pos(t, rr[i])) : -1;
-      const int j0 = j_base + kk[i];
-      ok[i] = pp >= 0 && j0 < a.bk;  // false: zero padding (after activation)
-      if (ok[i]) load8(a.z + (pix0 + pp) * a.bk + j0, a.bk - j0, (a.bk & 3) == 0, v[i]);
-      if (q >= nchunk) rr[i] = -1;
+    for (int q = threadIdx.x; q < nchunk; q += kThreads) {
+      const int r = (q & 7) + 8 * (q / (8 * kcn));
+      const int j0 = j_base + ((q >> 3) % kcn) * 8;
+      const int pp = h.g.pixel(h.g.pos(t, r));
+      if (pp >= 0 && j0 < a.bk) {
+        const float* src = a.z + (pix0 + pp) * a.bk + j0;
+        cp_async16(ring + q * 32, src);
+        cp_async16(ring + q * 32 + 16, src + 4);
+      }
     }
+    cp_async_commit();
+  }
+  __device__ void produce(uint8_t* st, int kb, const uint8_t* aux) const {
+    const LayerArgs<float>& a = h.a;
+    const BnFwd* bn = reinterpret_cast<const BnFwd*>(aux);
+    uint8_t* xh = st;
+    uint8_t* xl = st + halo_bytes();
+    const int nkb = num_kb();
+    uint8_t* waux = const_cast<uint8_t*>(aux);
+    if (kb == 0) fetch(0, waux);
+    if (kb + 1 < nkb) {  // slot (kb+1) % 2 held chunk kb-1, transformed by this thread already
+      fetch(kb + 1, waux);
+      cp_async_wait<1>();
+    } else {
+      cp_async_wait<0>();
+    }
+    const float* ring = reinterpret_cast<const float*>(aux + raw_offset(a.bk) + (kb % kRawDepth) * raw_bytes(h.g.R, h.kc));
+    const int t = tile();
+    const int j_base = kb * h.kc;
+    const int kcn = h.kc / 8;
+    const int nchunk = h.g.R * kcn;
+    for (int q = threadIdx.x; q < nchunk; q += kThreads) {
+      const int r = (q & 7) + 8 * (q / (8 * kcn));
+      const int kk = ((q >> 3) % kcn) * 8;
+      const int j0 = j_base + kk;
+      const bool ok = h.g.pixel(h.g.pos(t, r)) >= 0 && j0 < a.bk;  // false: zero padding (after activation)
+      float v[8];
+      if (ok) {
+        const float4 x0 = *reinterpret_cast<const float4*>(ring + q * 8);
+        const float4 x1 = *reinterpret_cast<const float4*>(ring + q * 8 + 4);
+        v[0] = x0.x; v[1] = x0.y; v[2] = x0.z; v[3] = x0.w;
+        v[4] = x1.x; v[5] = x1.y; v[6] = x1.z; v[7] = x1.w;
 #pragma unroll
-    for (int i = 0; i < kMaxChunks; ++i) {
-      if (rr[i] < 0) continue;
-      const int j0 = j_base + kk[i];
+        for (int e = 0; e < 8; ++e) v[e] = j0 + e < a.bk ? bn_relu(bn[j0 + e], v[e]) : 0.f;
+      } else {
 #pragma unroll
-      for (int e = 0; e < 8; ++e) v[i][e] = ok[i] && j0 + e < a.bk ? bn_relu(bn[j0 + e], v[i][e]) : 0.f;
+        for (int e = 0; e < 8; ++e) v[e] = 0.f;
+      }
       uint4 hi, lo;
-      split8_h(v[i], hi, lo);
-      const uint32_t off = halo_kmajor(h.g.R, rr[i], kk[i]);
+      split8_h(v, hi, lo);
+      const uint32_t off = halo_kmajor(h.g.R, r, kk);
       st_shared16(xh, off, hi);
       st_shared16(xl, off, lo);
-    }
     }
   }
   __device__ void issue(uint32_t st, int kb, uint32_t tmem_base, int part) const {
@@ -554,13 +624,14 @@ struct Tc3x3DgradHalo {
   __device__ int num_kb() const { return 1; }
   __device__ int tile() const { return blockIdx.x % h.g.tpi; }
   __device__ int img() const { return blockIdx.x / h.g.tpi; }
+  __device__ int n0() const { return blockIdx.y * BN; }  // first output column (channel j) of this CTA
   __device__ void prologue(uint8_t* aux) const {
     fill_bn_fwd(reinterpret_cast<BnFwd*>(aux), h.a.bk, 0, h.a.bmean, h.a.bvar, h.a.gamma_b,
                 h.a.beta_b);
   }
   __device__ void bulk(uint32_t st, int, uint64_t* bar) const {
     mbar_expect_tx(bar, b_bytes());
-    bulk_load(st + halo_bytes(), h.wt, b_bytes(), bar);
+    bulk_load(st + halo_bytes(), h.wt + static_cast<int64_t>(blockIdx.y) * b_bytes(), b_bytes(), bar);
   }
   __device__ void produce(uint8_t* st, int, const uint8_t*) const {
     const LayerArgs<float>& a = h.a;
@@ -609,15 +680,29 @@ struct Tc3x3DgradHalo {
       }
     }
   }
-  __device__ void epilogue(int row, int col0, const float (&v)[8], const uint8_t* aux,
-                           float (&s1)[8], float (&s2)[8]) const {
+  static constexpr int kEpiPrefetch = BN <= 64 ? 2 : 4;  // z column groups per load batch (register cap)
+  __device__ void epi_load(int row, int col0, float (&zv)[8]) const {
     const LayerArgs<float>& a = h.a;
-    const BnFwd* bn = reinterpret_cast<const BnFwd*>(aux);
+    col0 += n0();
     const int pp = h.g.pixel(h.g.g_s0(tile()) + row);
     const int nv = pp >= 0 ? a.bk - col0 : 0;
-    float zv[8], g[8];
     const int64_t p = static_cast<int64_t>(img()) * h.g.H * h.g.W + (pp >= 0 ? pp : 0);
+#ifdef DPB_EXP_NOZ
+    for (int i = 0; i < 8; ++i) zv[i] = 1.f + row * 1e-3f;
+#else
     if (nv > 0) load8(a.z + p * a.bk + col0, nv, (a.bk & 3) == 0, zv);
+#endif
+  }
+  __device__ void epilogue(int, int, const float (&)[8], const uint8_t*, float (&)[8], float (&)[8]) const {}
+  __device__ void epilogue_pre(int row, int col0, const float (&v)[8], const uint8_t* aux, const float (&zv)[8],
+                               float (&s1)[8], float (&s2)[8]) const {
+    const LayerArgs<float>& a = h.a;
+    const BnFwd* bn = reinterpret_cast<const BnFwd*>(aux);
+    col0 += n0();
+    const int pp = h.g.pixel(h.g.g_s0(tile()) + row);
+    const int nv = pp >= 0 ? a.bk - col0 : 0;
+    float g[8];
+    const int64_t p = static_cast<int64_t>(img()) * h.g.H * h.g.W + (pp >= 0 ? pp : 0);
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
       if (i < nv) {
@@ -631,7 +716,11 @@ struct Tc3x3DgradHalo {
         s2[i] = 0.f;
       }
     }
+#ifdef DPB_EXP_NOSTORE
+    if (false) {
+#else
     if (nv > 0) {
+#endif
       float* dst = a.g0 + p * a.bk + col0;
       if ((a.bk & 3) == 0 && nv >= 8) {
         reinterpret_cast<float4*>(dst)[0] = make_float4(g[0], g[1], g[2], g[3]);
@@ -644,7 +733,7 @@ struct Tc3x3DgradHalo {
     }
   }
   __device__ void col_sums(int c, double s1, double s2) const {
-    if (c < h.a.bk) h.a.part[static_cast<int64_t>(blockIdx.x) * h.a.bk + c] = make_double2(s1, s2);
+    if (n0() + c < h.a.bk) h.a.part[static_cast<int64_t>(blockIdx.x) * h.a.bk + n0() + c] = make_double2(s1, s2);
   }
 };
 
@@ -664,6 +753,7 @@ struct Tc3x3WgradHalo {
   static constexpr int kTmemCols = 9 * BN;
   static constexpr bool kColSums = false;
   static constexpr bool kBulk = false;
+  static constexpr int kEpiPrefetch = 0;  // (see Tc3x3DgradHalo)
   static constexpr int kMaxChunks = 6;  // bk = 48 at W = 32: 1456 chunks, one load batch
   HaloArgs h;
   int tpc;      // tiles per CTA

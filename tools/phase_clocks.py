@@ -1,7 +1,7 @@
 """Debug: per-phase CTA timing of the halo 3x3 forward (dpb_debug_phase_clocks).
 Needs a build with the stamps compiled in: rm -rf paper_1707_06990_b200/_build &&
 DPB_PHASE_CLOCKS=1 python -m paper_1707_06990_b200.build (the default build has none)."""
-import ctypes as C, sys
+import ctypes as C, os, sys
 import numpy as np, torch
 sys.path.insert(0, ".")
 import paper_1707_06990_b200 as P
@@ -9,7 +9,7 @@ from paper_1707_06990_b200._lib import lib
 L = lib()
 f = L.dpb_debug_phase_clocks
 f.argtypes = [C.c_int, C.c_void_p, C.c_int]
-shp = P.BlockShape(64, 32, 32, 24, 4, 12, 48)
+shp = P.BlockShape(*[int(v) for v in os.environ.get("SHAPE", "64,32,32,24,4,12,48").split(",")])
 plan = P.BlockPlan(shp, dtype="bf16", layout="nhwc")
 p = torch.randn(shp.param_elems, device="cuda") * 0.1 + 0.5
 x = torch.randn(shp.pixels, shp.c0, device="cuda")
@@ -22,11 +22,24 @@ plan.forward(x, p, run, True)   # the last halo forward launch wins (layer 3)
 torch.cuda.synchronize()
 f(0, None, 0)
 buf = np.zeros((4096, 9), dtype=np.int64)
-f(-1, C.c_void_p(buf.ctypes.data), 576)
-b = buf[:576]
+f(-1, C.c_void_p(buf.ctypes.data), 4096)
+b = buf[(buf[:, 0] != 0) & (buf[:, 8] != 0)]
+if len(b) == 0:
+    print("no stamps (build with DPB_PHASE_CLOCKS=1)")
+    sys.exit(0)
 t0 = b[:, 0].min()
 ph = np.diff(b, axis=1)
 print("CTAs", len(b), "span cycles", b[:, 8].max() - t0)
 for i, name in enumerate(["prologue+alloc", "produce", "issue", "mma wait", "epilogue loop", "epi barrier", "col sums", "dealloc"]):
     print(f"{name:18s} mean {ph[:, i].mean():8.0f}  p50 {np.median(ph[:, i]):8.0f}  max {ph[:, i].max():8.0f}")
 print("CTA lifetime mean", (b[:, 8] - b[:, 0]).mean(), "start spread", np.percentile(b[:, 0] - t0, [0, 50, 100]))
+kbb = np.zeros((4096, 8, 4), dtype=np.int64)
+f(-1, C.c_void_p(kbb.ctypes.data), -4096)
+kbb = kbb[(buf[:, 0] != 0) & (buf[:, 8] != 0)]
+base = b[:, 1][:, None]
+for kb in range(8):
+    k = kbb[:, kb, :]
+    if not k[:, 0].any():
+        break
+    rel = (k - base).mean(axis=0)
+    print(f"kb {kb}: stage free {rel[0]:7.0f}  produced {rel[1]:7.0f}  barrier {rel[2]:7.0f}  weights {rel[3]:7.0f}")
