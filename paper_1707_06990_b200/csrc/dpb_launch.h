@@ -7,6 +7,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdio>
 #include <cstdlib>
 #include <mutex>
 #include <unordered_set>
@@ -87,6 +88,16 @@ inline void launch(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem,
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
+  static const bool dbg_sync = std::getenv("DPB_DEBUG_SYNC") != nullptr;  // debugging aid: fault attribution
+  if (dbg_sync) {
+    const cudaError_t e = cudaDeviceSynchronize();
+    const char* name = nullptr;
+    cudaFuncGetName(&name, reinterpret_cast<const void*>(kernel));
+    if (std::getenv("DPB_DEBUG_SYNC")[0] == '2') fprintf(stderr, "DPB_DEBUG_SYNC: ok %s\n", name ? name : "?");
+    if (e != cudaSuccess) {
+      fprintf(stderr, "DPB_DEBUG_SYNC: %s after %s\n", cudaGetErrorString(e), name ? name : "?");
+    }
+  }
 }
 
 }  // namespace dpb

@@ -110,7 +110,7 @@ HaloPlan tc_halo_plan(const dpb_block_desc& d) {
   static const int force_kc = std::getenv("DPB_HALO_KC") ? std::atoi(std::getenv("DPB_HALO_KC")) : 0;
   auto fwd_aux = [&](int kc) {  // BN table + the raw fp32 halo ring (Tc3x3FwdHalo::fetch)
     using Op = tc::Tc3x3FwdHalo<16>;
-    return static_cast<size_t>(Op::raw_offset(static_cast<int>(d.bk))) + Op::kRawDepth * Op::raw_bytes(g.R, kc);
+    return static_cast<size_t>(Op::aux_bytes(static_cast<int>(d.bk), g.R, kc));
   };
   auto fwd_fits = [&](int kc, size_t lim) {
     const size_t stage = 2ull * (static_cast<size_t>(g.R) * kc * 2 + 9ull * bn * kc * 2);
@@ -203,7 +203,7 @@ int tc_conv3x3_fwd(Block* b, const LayerArgs<float>& a, int l) {
     const size_t stage = 2ull * (static_cast<size_t>(h.g.R) * kc * 2 + 9ull * bn * kc * 2);
     const int nst = (a.bk + kc - 1) / kc > 1 ? 2 : 1;
     using FH = tc::Tc3x3FwdHalo<16>;
-    const size_t aux = FH::raw_offset(a.bk) + FH::kRawDepth * FH::raw_bytes(h.g.R, kc);
+    const size_t aux = FH::aux_bytes(a.bk, h.g.R, kc);
     if (b->halo.fwd_taps) {
       const dim3 grid(static_cast<unsigned>(nimg(a) * h.g.tpi));
       const size_t np = (9 * a.k + 15) / 16 * 16;

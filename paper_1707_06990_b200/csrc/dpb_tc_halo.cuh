@@ -83,6 +83,7 @@ __global__ void __launch_bounds__(kThreads, Op::kMinBlocks) tc_halo_kernel(const
   extern __shared__ __align__(1024) uint8_t smem[];
   __shared__ uint64_t mbar[2];
   __shared__ uint64_t bbar[2];  // async bulk copies of pre-tiled weight images
+  __shared__ uint64_t fbar[2];  // kSpecialized: stage's halo produced (one arrive per producer warp)
   __shared__ uint32_t tmem_base;
   __shared__ float red[2][4][BN];
 
@@ -109,6 +110,8 @@ __global__ void __launch_bounds__(kThreads, Op::kMinBlocks) tc_halo_kernel(const
     mbar_init(&mbar[1], Op::kIssuers);
     mbar_init(&bbar[0], 1);
     mbar_init(&bbar[1], 1);
+    mbar_init(&fbar[0], 8 - Op::kIssuers);
+    mbar_init(&fbar[1], 8 - Op::kIssuers);
     fence_barrier_init();
   }
   // tables built from data two or more launches old (see dpb_tc2.cuh) are
@@ -123,7 +126,45 @@ __global__ void __launch_bounds__(kThreads, Op::kMinBlocks) tc_halo_kernel(const
   if (dbg) g_phase_clock[dbg_id][1] = clock64();
 
   const int nkb = op.num_kb();
-  for (int kb = 0; kb < nkb; ++kb) {
+  if constexpr (Op::kSpecialized) {
+    // warps [0, kIssuers) issue, the others produce; stages are handed off by
+    // mbarriers (fbar: halo produced, bbar: weights landed, mbar: MMAs done),
+    // so the producers build chunk kb+1 while chunk kb's MMAs are issued and
+    // run, and weights for kb+1 load as soon as kb-1's MMAs release the stage
+    if (warp < Op::kIssuers) {
+      if (lane == 0) {
+        if (tid == 0) {
+          op.bulk(smem_u32(smem), 0, &bbar[0]);
+          if (nkb > 1) op.bulk(smem_u32(smem + SB), 1, &bbar[1]);
+        }
+        for (int kb = 0; kb < nkb; ++kb) {
+          const int s = kb & 1;
+          mbar_wait(&fbar[s], (kb >> 1) & 1);
+          mbar_wait(&bbar[s], (kb >> 1) & 1);
+          if (dbg && kb < 8) g_kb_clock[dbg_id][kb][3] = clock64();
+          tc_fence_after();
+          op.issue(smem_u32(smem + s * SB), kb, tmem, warp);
+          mma_commit(&mbar[s]);
+          if (tid == 0 && kb >= 1 && kb + 1 < nkb) {  // stage (kb+1)&1 free once kb-1's MMAs completed
+            const int s1 = (kb + 1) & 1;
+            mbar_wait(&mbar[s1], ((kb - 1) >> 1) & 1);
+            op.bulk(smem_u32(smem + s1 * SB), kb + 1, &bbar[s1]);
+          }
+        }
+      }
+    } else {
+      for (int kb = 0; kb < nkb; ++kb) {
+        const int s = kb & 1;
+        if (kb >= 2) mbar_wait(&mbar[s], ((kb - 2) >> 1) & 1);
+        op.produce(smem + s * SB, kb, aux);
+        fence_proxy_async();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&fbar[s]);
+      }
+    }
+    if (dbg) g_phase_clock[dbg_id][2] = g_phase_clock[dbg_id][3] = clock64();
+  }
+  for (int kb = 0; !Op::kSpecialized && kb < nkb; ++kb) {
     const int s = kb & 1;
     if (kb >= 2) mbar_wait(&mbar[s], ((kb - 2) >> 1) & 1);
     if (dbg && kb < 8) g_kb_clock[dbg_id][kb][0] = clock64();
@@ -372,13 +413,20 @@ __global__ void k_pretile_w2_bwd(const float* __restrict__ params, int c0, int k
 // halo (hi, lo) and W2 for all 9 taps (hi, lo).  The W2 image arrives by an
 // asynchronous bulk copy while the threads build the halo; each thread issues
 // all of its halo loads before converting any (one memory latency per stage).
+#ifndef DPB_FWD_ISSUERS
+#define DPB_FWD_ISSUERS 2
+#endif
 template <int BN_>
 struct Tc3x3FwdHalo {
   static constexpr int BN = BN_;
   // (tap, k16) pairs are dealt round-robin to kIssuers warps, each issuing into
   // its own accumulator copy (summed by the epilogue): eight issuers while the
   // copies fit two CTAs' TMEM, else three
-  static constexpr int kIssuers = BN <= 32 ? 8 : 3, kAccCopies = kIssuers;
+  static constexpr int kIssuers = DPB_FWD_ISSUERS, kAccCopies = kIssuers;
+  // producer threads: the warps past the issuers (an issuing warp is held by
+  // the tensor pipe's issue rate; the others build the next K chunk meanwhile)
+  static constexpr int kProd0 = 32 * kIssuers, kProdThreads = kThreads - kProd0;
+  static constexpr bool kSpecialized = kIssuers < 8;
   static constexpr int kTmemCols = BN * kAccCopies;
   static constexpr bool kTapCols = false;
   static constexpr bool kEarlyPrologue = false;  // BN_b statistics: the predecessor's output
@@ -393,37 +441,61 @@ struct Tc3x3FwdHalo {
   __device__ int num_kb() const { return (h.a.bk + h.kc - 1) / h.kc; }
   __device__ int tile() const { return blockIdx.x % h.g.tpi; }
   __device__ int img() const { return blockIdx.x / h.g.tpi; }
+  // aux: BN table | raw fp32 halo ring (kRawDepth K chunks) | halo row table
+  static constexpr int kRawDepth = 2;
+  __host__ __device__ static uint32_t raw_offset(int bk) { return (sizeof(BnFwd) * bk + 127) / 128 * 128; }
+  __host__ __device__ static uint32_t raw_bytes(int R, int kc) { return static_cast<uint32_t>(R) * kc * 4; }
+  __host__ __device__ static uint32_t rows_offset(int bk, int R, int kc) {
+    return raw_offset(bk) + kRawDepth * raw_bytes(R, kc);
+  }
+  __host__ __device__ static uint32_t aux_bytes(int bk, int R, int kc) { return rows_offset(bk, R, kc) + 4 * R; }
   __device__ void prologue(uint8_t* aux) const {
     fill_bn_fwd(reinterpret_cast<BnFwd*>(aux), h.a.bk, 0, h.a.bmean, h.a.bvar, h.a.gamma_b,
                 h.a.beta_b);
+    // halo row r -> element offset of its pixel's z row within the image, or -1 (padding)
+    int* rowoff = reinterpret_cast<int*>(aux + rows_offset(h.a.bk, h.g.R, h.kc));
+    const int t = tile();
+    for (int r = threadIdx.x; r < h.g.R; r += kThreads) {
+      const int pp = h.g.pixel(h.g.pos(t, r));
+      rowoff[r] = pp >= 0 ? pp * h.a.bk : -1;
+    }
   }
   __device__ void bulk(uint32_t st, int kb, uint64_t* bar) const {
     mbar_expect_tx(bar, 2 * b_bytes());
     bulk_load(st + 2 * halo_bytes(), h.wt + static_cast<int64_t>(kb) * 2 * b_bytes(), 2 * b_bytes(),
               bar);
   }
-  // Raw fp32 halo chunks stream through a kRawDepth-deep ring after the BN
-  // table (cp.async, issued one K chunk ahead): chunk kb+1's loads are in
-  // flight while chunk kb is transformed and its MMAs issued, so a K chunk
-  // costs its transform, not a memory latency.  Each thread copies and then
-  // transforms the same chunks (thread-local groups: no barrier).
-  static constexpr int kRawDepth = 2;
-  __host__ __device__ static uint32_t raw_offset(int bk) { return (sizeof(BnFwd) * bk + 127) / 128 * 128; }
-  __host__ __device__ static uint32_t raw_bytes(int R, int kc) { return static_cast<uint32_t>(R) * kc * 4; }
+  // chunk q of a K chunk -> (halo row r, channel offset kk): eight consecutive
+  // chunks cover eight rows of one 8-channel group (conflict-free 16-byte
+  // stores); shifts when kcn is a power of two (kc = 16, 32, 64), else divisions
+  __device__ static void chunk_coords(int q, int kcn, int& r, int& kk) {
+    if ((kcn & (kcn - 1)) == 0) {
+      const int kcs = __ffs(kcn) - 1;
+      r = (q & 7) | ((q >> (3 + kcs)) << 3);
+      kk = ((q >> 3) & (kcn - 1)) << 3;
+    } else {
+      r = (q & 7) + 8 * (q / (8 * kcn));
+      kk = ((q >> 3) % kcn) * 8;
+    }
+  }
+  // Raw fp32 halo chunks stream through the ring (cp.async, issued one K chunk
+  // ahead): chunk kb+1's loads are in flight while chunk kb is transformed.
+  // Each producer thread copies and then transforms the same chunks
+  // (thread-local groups: no barrier).
   __device__ void fetch(int kb, uint8_t* aux) const {
     const LayerArgs<float>& a = h.a;
     const uint32_t ring = smem_u32(aux + raw_offset(a.bk) + (kb % kRawDepth) * raw_bytes(h.g.R, h.kc));
-    const int t = tile();
-    const int64_t pix0 = static_cast<int64_t>(img()) * h.g.H * h.g.W;
+    const int* rowoff = reinterpret_cast<const int*>(aux + rows_offset(a.bk, h.g.R, h.kc));
+    const int kcn = h.kc >> 3;
     const int j_base = kb * h.kc;
-    const int kcn = h.kc / 8;
+    const float* zb = a.z + static_cast<int64_t>(img()) * h.g.H * h.g.W * a.bk + j_base;
     const int nchunk = h.g.R * kcn;
-    for (int q = threadIdx.x; q < nchunk; q += kThreads) {
-      const int r = (q & 7) + 8 * (q / (8 * kcn));
-      const int j0 = j_base + ((q >> 3) % kcn) * 8;
-      const int pp = h.g.pixel(h.g.pos(t, r));
-      if (pp >= 0 && j0 < a.bk) {
-        const float* src = a.z + (pix0 + pp) * a.bk + j0;
+    for (int q = static_cast<int>(threadIdx.x) - kProd0; q < nchunk; q += kProdThreads) {
+      int r, kk;
+      chunk_coords(q, kcn, r, kk);
+      const int ro = rowoff[r];
+      if (ro >= 0 && j_base + kk < a.bk) {
+        const float* src = zb + ro + kk;
         cp_async16(ring + q * 32, src);
         cp_async16(ring + q * 32 + 16, src + 4);
       }
@@ -431,6 +503,7 @@ struct Tc3x3FwdHalo {
     cp_async_commit();
   }
   __device__ void produce(uint8_t* st, int kb, const uint8_t* aux) const {
+    if (static_cast<int>(threadIdx.x) < kProd0) return;
     const LayerArgs<float>& a = h.a;
     const BnFwd* bn = reinterpret_cast<const BnFwd*>(aux);
     uint8_t* xh = st;
@@ -445,23 +518,47 @@ struct Tc3x3FwdHalo {
       cp_async_wait<0>();
     }
     const float* ring = reinterpret_cast<const float*>(aux + raw_offset(a.bk) + (kb % kRawDepth) * raw_bytes(h.g.R, h.kc));
-    const int t = tile();
+    const int* rowoff = reinterpret_cast<const int*>(aux + rows_offset(a.bk, h.g.R, h.kc));
     const int j_base = kb * h.kc;
-    const int kcn = h.kc / 8;
+    const int kcn = h.kc >> 3;
     const int nchunk = h.g.R * kcn;
-    for (int q = threadIdx.x; q < nchunk; q += kThreads) {
-      const int r = (q & 7) + 8 * (q / (8 * kcn));
-      const int kk = ((q >> 3) % kcn) * 8;
+    const int q0 = static_cast<int>(threadIdx.x) - kProd0;
+    // a thread's channel group is the same for all its chunks when the stride
+    // is a multiple of 8 * kcn: its BN constants are loaded once per K chunk
+    const bool fixed = (kProdThreads >> 3) % kcn == 0;
+    float mu[8], sc[8], be[8];
+    {
+      int r0, kk;
+      chunk_coords(q0, kcn, r0, kk);
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        const int j = min(j_base + kk + e, a.bk - 1);
+        mu[e] = bn[j].mean;
+        sc[e] = bn[j].scale;
+        be[e] = bn[j].beta;
+      }
+    }
+    for (int q = q0; q < nchunk; q += kProdThreads) {
+      int r, kk;
+      chunk_coords(q, kcn, r, kk);
       const int j0 = j_base + kk;
-      const bool ok = h.g.pixel(h.g.pos(t, r)) >= 0 && j0 < a.bk;  // false: zero padding (after activation)
+      const bool ok = rowoff[r] >= 0 && j0 < a.bk;  // false: zero padding (after activation)
       float v[8];
       if (ok) {
         const float4 x0 = *reinterpret_cast<const float4*>(ring + q * 8);
         const float4 x1 = *reinterpret_cast<const float4*>(ring + q * 8 + 4);
         v[0] = x0.x; v[1] = x0.y; v[2] = x0.z; v[3] = x0.w;
         v[4] = x1.x; v[5] = x1.y; v[6] = x1.z; v[7] = x1.w;
+        if (fixed) {
 #pragma unroll
-        for (int e = 0; e < 8; ++e) v[e] = j0 + e < a.bk ? bn_relu(bn[j0 + e], v[e]) : 0.f;
+          for (int e = 0; e < 8; ++e) {
+            const float t = fmaf(v[e] - mu[e], sc[e], be[e]);  // bn_relu
+            v[e] = j0 + e < a.bk && t > 0.f ? t : 0.f;
+          }
+        } else {
+#pragma unroll
+          for (int e = 0; e < 8; ++e) v[e] = j0 + e < a.bk ? bn_relu(bn[j0 + e], v[e]) : 0.f;
+        }
       } else {
 #pragma unroll
         for (int e = 0; e < 8; ++e) v[e] = 0.f;
@@ -530,6 +627,7 @@ struct Tc3x3FwdHalo {
 // output epilogue are those of Tc3x3FwdHalo.
 struct Tc3x3FwdTaps : Tc3x3FwdHalo<16> {
   static constexpr int kIssuers = 2, kAccCopies = 1;  // one issuer per M block
+  static constexpr bool kSpecialized = false;
   static constexpr int kTmemCols = 2 * kBM;           // M block b at columns [128 b, 128 b + N)
   static constexpr bool kTapCols = true;
   static constexpr int kMinBlocks = 2;
@@ -610,6 +708,7 @@ struct Tc3x3DgradHalo {
   // small TMEM / register / smem footprint lets three CTAs share an SM, whose
   // phases (halo loads, MMAs, the z-dependent epilogue) then overlap
   static constexpr int kIssuers = 1, kAccCopies = 1;
+  static constexpr bool kSpecialized = false;
   static constexpr bool kTapCols = false;
   static constexpr bool kEarlyPrologue = true;  // BN_b forward statistics and parameters
   static constexpr int kMinBlocks = BN <= 64 ? 4 : 2;
@@ -747,6 +846,7 @@ template <int BN_>
 struct Tc3x3WgradHalo {
   static constexpr int BN = BN_;
   static constexpr int kIssuers = 3, kAccCopies = 1;  // taps t = warp, warp+3, warp+6
+  static constexpr bool kSpecialized = false;
   static constexpr bool kTapCols = false;
   static constexpr bool kEarlyPrologue = true;  // BN_b forward statistics and parameters
   static constexpr int kMinBlocks = 2;
