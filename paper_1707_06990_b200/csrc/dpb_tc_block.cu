@@ -308,7 +308,7 @@ int tc_conv3x3_wgrad(Block* b, LayerArgs<float> a) {
     const int bn = pick_bn(a.k);
     const tc::HaloArgs h = halo_args(a, bn);
     const size_t stage = static_cast<size_t>(h.g.R) * tc::kBM * 2 + static_cast<size_t>(tc::kBM) * bn * 2;
-    const size_t aux = sizeof(BnFwd) * a.bk;
+    const size_t aux = tc::Tc3x3WgradHalo<16>::aux_bytes(a.bk, h.g.R);
     if (bn <= 48 && 2 * stage + aux <= kHaloSmemMax) {
       const int64_t ntiles = nimg(a) * h.g.tpi;
       const int64_t gy = (a.bk + tc::kBM - 1) / tc::kBM;

@@ -866,48 +866,61 @@ struct Tc3x3WgradHalo {
     const int n = ntiles - t0;
     return n < 0 ? 0 : (n < tpc ? n : tpc);
   }
+  // aux: BN table as float4 {mean, scale, beta, -} | two halo row tables
+  // (stage parity): row r -> image-local pixel of the tile's halo row, or -1
+  __host__ __device__ static uint32_t rows_offset(int bk) { return (16 * bk + 127) / 128 * 128; }
+  __host__ __device__ static uint32_t aux_bytes(int bk, int R) { return rows_offset(bk) + 2 * 4 * R; }
   __device__ void prologue(uint8_t* aux) const {
-    fill_bn_fwd(reinterpret_cast<BnFwd*>(aux), h.a.bk, 0, h.a.bmean, h.a.bvar, h.a.gamma_b,
-                h.a.beta_b);
+    float4* bq = reinterpret_cast<float4*>(aux);
+    for (int j = threadIdx.x; j < h.a.bk; j += kThreads) {
+      const float inv = bn_inv(h.a.bvar[j]);
+      bq[j] = make_float4(h.a.bmean[j], h.a.gamma_b[j] * inv, h.a.beta_b[j], 0.f);  // fill_bn_fwd's fields
+    }
   }
   __device__ void bulk(uint32_t, int, uint64_t*) const {}
   __device__ void produce(uint8_t* st, int kb, const uint8_t* aux) const {
     const LayerArgs<float>& a = h.a;
-    const BnFwd* bn = reinterpret_cast<const BnFwd*>(aux);
+    const float4* bq = reinterpret_cast<const float4*>(aux);
+    int* rows = const_cast<int*>(reinterpret_cast<const int*>(aux + rows_offset(a.bk))) + (kb & 1) * h.g.R;
     uint8_t* xs = st;
     uint8_t* dys = st + halo_bytes();
     const int gt = blockIdx.x * tpc + kb;
     const int im = gt / h.g.tpi, t = gt - im * h.g.tpi;
-    const int64_t pix0 = static_cast<int64_t>(im) * h.g.H * h.g.W;
+    for (int r = threadIdx.x; r < h.g.R; r += kThreads) rows[r] = h.g.pixel(h.g.pos(t, r));
+    __syncthreads();  // (the parity-(kb-2) table's readers finished before produce(kb-1)'s barrier)
+    const float* zb = a.z + static_cast<int64_t>(im) * h.g.H * h.g.W * a.bk;
+    const float* gb = a.acc + static_cast<int64_t>(im) * h.g.H * h.g.W * a.Ca + a.c;
     const int j_base = blockIdx.y * kBM;
     // only the channel groups below bk: the A rows j >= bk feed only D rows the
     // epilogue drops (an MMA row depends on its own A row), so they stay unwritten
     const int jn = a.bk - j_base < kBM ? a.bk - j_base : kBM;
     const int groups = (jn + 7) / 8;
+    const bool gp2 = (groups & (groups - 1)) == 0;
+    const int gs = __ffs(groups) - 1;
     const int nchunk = h.g.R * groups;  // act_b halo chunks; then dY chunks
     const int og = BN / 8;
     const int ndy = kBM * og;
-    const int s0 = h.g.g_s0(t);
+    const int dy0 = h.g.W2 + 1;  // halo row of the tile's first output position
     const int total = nchunk + ndy;
     for (int base = 0; base < total; base += kMaxChunks * kThreads) {
       float v[kMaxChunks][8];
       uint32_t off[kMaxChunks];
-      uint8_t kind[kMaxChunks];  // 0 skip, 1 halo, 2 dY
+      uint8_t kind[kMaxChunks];  // 0 skip, 1 halo, 2 dY, 3 zero
       int jj[kMaxChunks];
 #pragma unroll
       for (int i = 0; i < kMaxChunks; ++i) {
         const int q = base + threadIdx.x + i * kThreads;
         kind[i] = 0;
-#pragma unroll
-        for (int e = 0; e < 8; ++e) v[i][e] = 0.f;
+        jj[i] = 0;
+        off[i] = 0;
         if (q < nchunk) {
           // act_b halo, MN-major: phase = 8 consecutive positions of one group
-          const int pos = (q & 7) + 8 * (q / (8 * groups));
-          const int jg = ((q >> 3) % groups) * 8;
+          const int pos = gp2 ? ((q & 7) | ((q >> (3 + gs)) << 3)) : (q & 7) + 8 * (q / (8 * groups));
+          const int jg = gp2 ? ((q >> 3) & (groups - 1)) << 3 : ((q >> 3) % groups) * 8;
           const int j0 = j_base + jg;
-          const int pp = h.g.pixel(h.g.pos(t, pos));
+          const int pp = rows[pos];
           const bool valid = pp >= 0 && j0 < a.bk;
-          if (valid) load8(a.z + (pix0 + pp) * a.bk + j0, a.bk - j0, (a.bk & 3) == 0, v[i]);
+          if (valid) load8(zb + static_cast<int64_t>(pp) * a.bk + j0, a.bk - j0, (a.bk & 3) == 0, v[i]);
           kind[i] = valid ? 1 : 3;  // 3: zero padding (after activation)
           jj[i] = j0;
           off[i] = halo_mnmajor(h.g.R, jg, pos);
@@ -915,8 +928,11 @@ struct Tc3x3WgradHalo {
           const int r = q - nchunk;
           const int pos = (r & 7) + 8 * (r / (8 * og));
           const int o0 = ((r >> 3) % og) * 8;
-          const int pp = h.g.pixel(s0 + pos);
-          if (pp >= 0 && o0 < a.k) load8(a.acc + (pix0 + pp) * a.Ca + a.c + o0, a.k - o0, h.vec, v[i]);
+          const int pp = rows[dy0 + pos];
+          if (pp >= 0 && o0 < a.k) load8(gb + static_cast<int64_t>(pp) * a.Ca + o0, a.k - o0, h.vec, v[i]);
+          else
+#pragma unroll
+            for (int e = 0; e < 8; ++e) v[i][e] = 0.f;
           kind[i] = 2;
           off[i] = halo_mnmajor(kBM, o0, pos);
         }
@@ -925,8 +941,11 @@ struct Tc3x3WgradHalo {
       for (int i = 0; i < kMaxChunks; ++i) {
         if (kind[i] == 1) {
 #pragma unroll
-          for (int e = 0; e < 8; ++e)
-            v[i][e] = jj[i] + e < a.bk ? bn_relu(bn[jj[i] + e], v[i][e]) : 0.f;
+          for (int e = 0; e < 8; ++e) {
+            const float4 b = bq[min(jj[i] + e, a.bk - 1)];
+            const float tt = fmaf(v[i][e] - b.x, b.y, b.z);  // bn_relu
+            v[i][e] = jj[i] + e < a.bk && tt > 0.f ? tt : 0.f;
+          }
           st_shared16(xs, off[i], to_bf16x8(v[i]));
         } else if (kind[i] == 2) {
           st_shared16(dys, off[i], to_bf16x8(v[i]));

@@ -47,3 +47,13 @@ ph = np.diff(b, axis=1)
 for i, name in enumerate(["prologue+alloc", "produce", "issue", "mma wait", "epilogue loop", "epi barrier", "col sums", "dealloc"]):
     print(f"{name:18s} mean {ph[:, i].mean():8.0f}  p50 {np.median(ph[:, i]):8.0f}  max {ph[:, i].max():8.0f}")
 print("CTA lifetime mean", (b[:, 8] - b[:, 0]).mean())
+kbb = np.zeros((4096, 8, 4), dtype=np.int64)
+f(-1, C.c_void_p(kbb.ctypes.data), -4096)
+kbb = kbb[(buf[:, 0] != 0) & (buf[:, 8] != 0)]
+base = b[:, 1][:, None]
+for kb in range(8):
+    k = kbb[:, kb, :]
+    if not k[:, 0].any():
+        break
+    rel = (k - base).mean(axis=0)
+    print(f"kb {kb}: stage free {rel[0]:7.0f}  produced {rel[1]:7.0f}  barrier {rel[2]:7.0f}  issued {rel[3]:7.0f}")

@@ -28,7 +28,8 @@ blk = int(sys.argv[4]) if len(sys.argv) > 4 else 0
 L = lib()
 f = L.dpb_debug_tc2_clocks
 f.argtypes = [C.c_int, C.c_void_p]
-shp = P.BlockShape(*block_shapes("bc100", 64)[blk])
+import os  # noqa: E402
+shp = P.BlockShape(*block_shapes(os.environ.get("CFG", "bc100"), 64)[blk])
 plan = P.BlockPlan(shp, dtype="bf16", layout="nhwc")
 p = torch.randn(shp.param_elems, device="cuda") * 0.1 + 0.5
 x = torch.randn(shp.pixels, shp.c0, device="cuda")
