@@ -76,6 +76,28 @@ __device__ __forceinline__ void raw_write8(uint8_t* box, int row, int ch, const 
   *reinterpret_cast<float4*>(box + row * 128 + (((c4 + 1) ^ (row & 7)) << 4)) = make_float4(v[4], v[5], v[6], v[7]);
 }
 
+// BN_a tables of the backward kernels as one float4 per channel (one 16-byte
+// shared load per element instead of a 20-byte BnFwd's scalar loads):
+//   mask form  {mean, inv, gamma, beta}   relu_mask_ref's exact expression
+//   apply form {mean, gamma*inv, beta, 0}  bn_relu's fmaf(x - mean, scale, beta)
+__device__ __forceinline__ void fill_bn_mask4(float4* t, int count, int first, const float* mean,
+                                              const float* var, const float* gamma, const float* beta) {
+  for (int i = threadIdx.x; i < count; i += blockDim.x) {
+    const int ch = first + i;
+    t[i] = make_float4(mean[ch], bn_inv(var[ch]), gamma[ch], beta[ch]);
+  }
+}
+__device__ __forceinline__ void fill_bn_apply4(float4* t, int count, int first, const float* mean,
+                                               const float* var, const float* gamma, const float* beta) {
+  for (int i = threadIdx.x; i < count; i += blockDim.x) {
+    const int ch = first + i;
+    t[i] = make_float4(mean[ch], gamma[ch] * bn_inv(var[ch]), beta[ch], 0.f);
+  }
+}
+__device__ __forceinline__ bool relu_mask4(const float4& b, float x) {  // == relu_mask_ref
+  const float t = __fmul_rn(__fmul_rn(b.z, __fsub_rn(x, b.x)), b.y);
+  return __fadd_rn(t, b.w) > 0.f;
+}
 using tc::colsum8_column;
 using tc::warp_colsum8;
 
@@ -674,15 +696,15 @@ struct Dgrad1x1 {
   __device__ const BnBwd* bnb(const uint8_t* aux) const {
     return reinterpret_cast<const BnBwd*>(aux + nkb() * kBTile);
   }
-  __device__ const BnFwd* bna(const uint8_t* aux) const {
-    return reinterpret_cast<const BnFwd*>(aux + nkb() * kBTile + ((sizeof(BnBwd) * a.bk + 15) / 16) * 16);
+  __device__ const float4* bna(const uint8_t* aux) const {  // mask form (fill_bn_mask4)
+    return reinterpret_cast<const float4*>(aux + nkb() * kBTile + ((sizeof(BnBwd) * a.bk + 15) / 16) * 16);
   }
   __device__ void prologue_early(uint8_t* aux) const {
     const uint4* src = reinterpret_cast<const uint4*>(w1t + static_cast<int64_t>(blockIdx.y) * nkb() * kBTile);
     uint4* dst = reinterpret_cast<uint4*>(aux);
     for (int q = threadIdx.x; q < nkb() * kBTile / 16; q += blockDim.x) dst[q] = __ldg(src + q);
     // BN_a forward statistics and parameters: old
-    fill_bn_fwd(const_cast<BnFwd*>(bna(aux)), ncols(), n0(), a.amean, a.avar, a.gamma_a, a.beta_a);
+    fill_bn_mask4(const_cast<float4*>(bna(aux)), ncols(), n0(), a.amean, a.avar, a.gamma_a, a.beta_a);
   }
   __device__ void prologue(uint8_t* aux) const {
     fill_bn_bwd(const_cast<BnBwd*>(bnb(aux)), a);  // the BN_b coefficients: the predecessor's output
@@ -731,7 +753,7 @@ struct Dgrad1x1 {
   }
   __device__ void epilogue(int tile, int row, int col0, const float (&v)[8], const uint8_t* aux,
                            uint8_t* ebox, float (&s1)[8], float (&s2)[8]) const {
-    const BnFwd* bn = bna(aux);
+    const float4* bn = bna(aux);
     const int64_t p = static_cast<int64_t>(tile) * kBM + row;
     const int rem = ncols() - col0;
     const int nv = p < a.M ? (rem < 8 ? rem : 8) : 0;
@@ -740,10 +762,10 @@ struct Dgrad1x1 {
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
       if (i < nv) {
-        const BnFwd b = bn[col0 + i];
-        g[i] = relu_mask_ref(b, x[i]) ? v[i] : 0.f;  // relu_backward by act_a
+        const float4 b = bn[col0 + i];
+        g[i] = relu_mask4(b, x[i]) ? v[i] : 0.f;  // relu_backward by act_a
         s1[i] = g[i];
-        s2[i] = g[i] * ((x[i] - b.mean) * b.inv);
+        s2[i] = g[i] * ((x[i] - b.x) * b.y);
       } else {
         g[i] = 0.f;
         s1[i] = 0.f;
@@ -814,13 +836,13 @@ struct Wgrad1x1 {
   __device__ void epi_tma(int, int, uint32_t, uint64_t*) const {}
   __device__ void epi_store(int, int, uint32_t) const {}
   __device__ const BnBwd* bnb(const uint8_t* aux) const { return reinterpret_cast<const BnBwd*>(aux); }
-  __device__ const BnFwd* bna(const uint8_t* aux) const {
-    return reinterpret_cast<const BnFwd*>(aux + ((sizeof(BnBwd) * a.bk + 15) / 16) * 16);
+  __device__ const float4* bna(const uint8_t* aux) const {  // apply form (fill_bn_apply4)
+    return reinterpret_cast<const float4*>(aux + ((sizeof(BnBwd) * a.bk + 15) / 16) * 16);
   }
   __device__ void prologue_early(uint8_t*) const {}
   __device__ void prologue(uint8_t* aux) const {
     fill_bn_bwd(const_cast<BnBwd*>(bnb(aux)), a);
-    fill_bn_fwd(const_cast<BnFwd*>(bna(aux)), ncols(), n0(), a.amean, a.avar, a.gamma_a, a.beta_a);
+    fill_bn_apply4(const_cast<float4*>(bna(aux)), ncols(), n0(), a.amean, a.avar, a.gamma_a, a.beta_a);
   }
   __device__ void tma(int tile, int kb, uint32_t raw, uint64_t* bar) const {
     const int p0 = (tile * kchunk + kb) * kBoxP;
@@ -835,7 +857,7 @@ struct Wgrad1x1 {
     const int64_t p0 = static_cast<int64_t>(tile * kchunk + kb) * kBoxP;
     const int jc = (a.bk + 7) / 8, ic = (ncols() + 7) / 8;
     const BnBwd* bb = bnb(aux);
-    const BnFwd* bn = bna(aux);
+    const float4* bn = bna(aux);
     // 8 consecutive chunks = 8 consecutive pixels of one channel group: one
     // whole MN-major core matrix per store phase, conflict-free box reads
     for (int q = xt; q < kBoxP * (jc + ic); q += kXfThreads) {
@@ -856,8 +878,8 @@ struct Wgrad1x1 {
         raw_read8(raw + (2 * JB + (i0 >> 5)) * kBox, p, i0 & 31, v);
 #pragma unroll
         for (int e = 0; e < 8; ++e) {
-          const BnFwd b = bn[i0 + e < ncols() ? i0 + e : 0];
-          v[e] = fmaxf(fmaf(v[e] - b.mean, b.scale, b.beta), 0.f);  // act_a (t1 is 0 past M)
+          const float4 b = bn[i0 + e < ncols() ? i0 + e : 0];
+          v[e] = fmaxf(fmaf(v[e] - b.x, b.y, b.z), 0.f);  // act_a (t1 is 0 past M)
         }
         tc::st_shared16(op + kMT * kATile, tc::Tile<BN>::mnmajor_chunk(i0, p), tc::to_bf16x8(v));
       }
