@@ -571,10 +571,13 @@ static void backward_impl(Block* b, const float* params, float* grad_acc, float*
                      M * (c_hi - c_lo) * (4.0 + 2.0 + 8.0));
       const bool quads = std::is_same<S, float>::value && a.Ca % 4 == 0 && c_lo % 4 == 0 &&
                          (reinterpret_cast<uintptr_t>(b->acc_cur) & 15) == 0;
+      const int nq = (c_hi + 3) / 4 - c_lo / 4;
+      const bool narrow = nq <= 16;  // <= 64 channels: the main-chain head
+      const int rows = narrow ? kApplyRowsNarrow : kApplyRows;
       if (quads)
-        launch(k_bn_apply_accumulate4,
-               blocks_for((g.M + kApplyRows - 1) / kApplyRows * ((c_hi + 3) / 4 - c_lo / 4), 256), 256, 0, st, g.M,
-               c_lo, c_hi, a.C, a.Ca, a.cg, static_cast<const float*>(b->feat), a.g1, a.amean, a.avar, a.gamma_a,
+        launch(narrow ? k_bn_apply_accumulate4<kApplyRowsNarrow> : k_bn_apply_accumulate4<kApplyRows>,
+               blocks_for((g.M + rows - 1) / rows * nq, 256), 256, 0, st, g.M, c_lo, c_hi, a.C, a.Ca, a.cg,
+               static_cast<const float*>(b->feat), a.g1, a.amean, a.avar, a.gamma_a,
                static_cast<const float*>(bna), b->acc_cur);
       else
         launch(k_bn_apply_accumulate<S>, blocks_for(g.M * (c_hi - c_lo), 256), 256, 0, st, g.M, c_lo, c_hi, a.C,

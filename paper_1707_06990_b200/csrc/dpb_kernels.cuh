@@ -197,10 +197,13 @@ k_bn_apply_accumulate(int64_t M, int c_lo, int c, int C, int Ca, int cg, const S
 
 // As k_bn_apply_accumulate with 16-byte rows (feature pitch C, accumulator
 // pitch Ca, g1 pitch cg all multiples of 4; fp32 storage): a thread owns one
-// 4-channel quad for kApplyRows consecutive pixels (coefficients computed
-// once, 16-byte loads/stores, warps coalesced along the row).  The last quad
-// of a layer with c % 4 != 0 updates only its channels < c.
-constexpr int kApplyRows = 8;
+// 4-channel quad for kRows consecutive pixels (coefficients computed once,
+// 16-byte loads/stores, warps coalesced along the row).  The last quad of a
+// layer with c % 4 != 0 updates only its channels < c.  kRows = 8 for wide
+// launches; the narrow head on the main chain (k channels) takes 2 rows per
+// thread so its few quads still fill the SMs (a 4x shorter latency chain).
+constexpr int kApplyRows = 8, kApplyRowsNarrow = 2;
+template <int kRows>
 __global__ void __launch_bounds__(256)
 k_bn_apply_accumulate4(int64_t M, int c_lo, int c, int C, int Ca, int cg, const float* __restrict__ feat,
                        const float* __restrict__ g1, const float* __restrict__ amean,
@@ -211,7 +214,7 @@ k_bn_apply_accumulate4(int64_t M, int c_lo, int c, int C, int Ca, int cg, const 
   const int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   const int64_t pg = t / cq;
   const int q = q0 + static_cast<int>(t - pg * cq);
-  const int64_t p0 = pg * kApplyRows;
+  const int64_t p0 = pg * kRows;
   if (p0 >= M) {
     pdl_enter();
     return;
@@ -223,7 +226,7 @@ k_bn_apply_accumulate4(int64_t M, int c_lo, int c, int C, int Ca, int cg, const 
   // grid-dependency wait.
   const float4 mean = *reinterpret_cast<const float4*>(amean + ch);
   const float4 var = *reinterpret_cast<const float4*>(avar + ch);
-  constexpr int kPre = 2;
+  constexpr int kPre = kRows < 2 ? kRows : 2;
   float4 xp[kPre], gp[kPre];
 #pragma unroll
   for (int i = 0; i < kPre; ++i) {
@@ -242,7 +245,7 @@ k_bn_apply_accumulate4(int64_t M, int c_lo, int c, int C, int Ca, int cg, const 
   float gi[4];
 #pragma unroll
   for (int e = 0; e < 4; ++e) gi[e] = e < live ? gamma[ch + e] * inv[e] : 0.f;
-  const int64_t pe = p0 + kApplyRows < M ? p0 + kApplyRows : M;
+  const int64_t pe = p0 + kRows < M ? p0 + kRows : M;
   auto row = [&](int64_t p, const float4 x4, const float4 g4) {
     const float x[4] = {x4.x, x4.y, x4.z, x4.w};
     const float g[4] = {g4.x, g4.y, g4.z, g4.w};
