@@ -265,11 +265,16 @@ int64_t tc_halo_partials(const dpb_block_desc& d) {
 }
 
 // split count of the halo 3x3 wgrad for a block (used by the arena plan)
+// CTAs (tile ranges x channel groups) of the 3x3 wgrad; DPB_WGRAD3_CTAS overrides
+static int64_t wgrad3_target() {
+  static const int64_t t = std::getenv("DPB_WGRAD3_CTAS") ? std::atoll(std::getenv("DPB_WGRAD3_CTAS")) : 296;
+  return t;
+}
 int64_t tc_halo_wgrad_splits(const dpb_block_desc& d) {
   const tc::HaloGeom g = tc::HaloGeom::make(static_cast<int>(d.h), static_cast<int>(d.w));
   const int64_t ntiles = d.n * g.tpi;
   const int64_t gy = (d.bk + tc::kBM - 1) / tc::kBM;
-  const int64_t target = std::max<int64_t>(1, 296 / gy);
+  const int64_t target = std::max<int64_t>(1, wgrad3_target() / gy);
   const int64_t tpc = std::max<int64_t>(1, (ntiles + target - 1) / target);
   return (ntiles + tpc - 1) / tpc;
 }
@@ -312,7 +317,7 @@ int tc_conv3x3_wgrad(Block* b, LayerArgs<float> a) {
     if (bn <= 48 && 2 * stage + aux <= kHaloSmemMax) {
       const int64_t ntiles = nimg(a) * h.g.tpi;
       const int64_t gy = (a.bk + tc::kBM - 1) / tc::kBM;
-      const int64_t target = std::max<int64_t>(1, 296 / gy);
+      const int64_t target = std::max<int64_t>(1, wgrad3_target() / gy);
       const int tpc = static_cast<int>(std::max<int64_t>(1, (ntiles + target - 1) / target));
       const int gx = static_cast<int>((ntiles + tpc - 1) / tpc);
       const dim3 grid(gx, static_cast<unsigned>(gy));
