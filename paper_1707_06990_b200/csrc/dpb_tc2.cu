@@ -160,6 +160,11 @@ int tc2_fwd_ksplit(int64_t M, int c, int sms, int ns) {
   return best_t <= 0.75 * t1 ? best : 1;
 }
 
+static bool fwd_in_place() {  // DPB_FWD_NO_INPLACE=1: the two-stage ring with an operand ring
+  static const bool on = std::getenv("DPB_FWD_NO_INPLACE") == nullptr;
+  return on;
+}
+
 // 1x1 forward on the v2 engine; false when the shape is not supported (the
 // caller then uses the v1 kernel).
 bool tc2_conv1x1_fwd(Block* b, const LayerArgs<float>& a, int l, int* prows) {
@@ -209,8 +214,8 @@ bool tc2_conv1x1_fwd(Block* b, const LayerArgs<float>& a, int l, int* prows) {
     case 64: return go(tc2::Fwd1x1<64, true>{}) || go(tc2::Fwd1x1<64, false>{});
     // wide inputs: W1's streamed stage at the full width no longer fits beside
     // the BN table, so the stages hold half-width (or narrower) column tiles
-    case 128: return go(tc2::Fwd1x1<128, true>{}) || go(tc2::Fwd1x1<128, false>{}) ||
-                     go(tc2::Fwd1x1<64, false>{});
+    case 128: return go(tc2::Fwd1x1<128, true>{}) || (fwd_in_place() && go(tc2::Fwd1x1<128, false, true>{})) ||
+                     go(tc2::Fwd1x1<128, false>{}) || go(tc2::Fwd1x1<64, false>{});
     case 192: return go(tc2::Fwd1x1<192, true>{}) || go(tc2::Fwd1x1<192, false>{}) ||
                      go(tc2::Fwd1x1<96, false>{});
     default: return false;

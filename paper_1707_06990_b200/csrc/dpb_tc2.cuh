@@ -147,7 +147,10 @@ __device__ int g_tc2_dbg_c;
 template <class Op>
 __global__ void __launch_bounds__(Roles<Op>::kThreads, 1) tc2_kernel(const __grid_constant__ Op op) {
   using R = Roles<Op>;
-  constexpr int NR = Op::kNR, NS = Op::kNS, BN = Op::BN, NE = Op::kNE > 0 ? Op::kNE : 1;
+  // kInPlace ops transform each raw stage into its own UMMA operand (no operand
+  // ring): stage r's op_full[r] hands it to the MMA, whose commit frees it.
+  constexpr bool IP = Op::kInPlace;
+  constexpr int NR = Op::kNR, NS = IP ? NR : Op::kNS, BN = Op::BN, NE = Op::kNE > 0 ? Op::kNE : 1;
   constexpr uint32_t TC = tc::TmemCols<Op::kTmemCols>::value;
   static_assert(2 * TC <= 512, "two TMEM accumulators");
   extern __shared__ __align__(1024) uint8_t smem_dyn[];
@@ -160,8 +163,8 @@ __global__ void __launch_bounds__(Roles<Op>::kThreads, 1) tc2_kernel(const __gri
   __shared__ float red[2][4][BN];
 
   uint8_t* raw_ring = smem;
-  uint8_t* op_ring = smem + NR * Op::kRawBytes;
-  uint8_t* epi_ring = op_ring + NS * Op::kOpBytes;
+  uint8_t* op_ring = IP ? raw_ring : smem + NR * Op::kRawBytes;
+  uint8_t* epi_ring = smem + NR * Op::kRawBytes + (IP ? 0 : NS * Op::kOpBytes);
   uint8_t* aux = epi_ring + Op::kNE * Op::kEpiBytes;  // op tables; resident B images first
 
   const int tid = threadIdx.x;
@@ -179,7 +182,7 @@ __global__ void __launch_bounds__(Roles<Op>::kThreads, 1) tc2_kernel(const __gri
   if (tid == 0) {
     for (int i = 0; i < NR; ++i) {
       tc::mbar_init(&raw_full[i], 1);
-      tc::mbar_init(&raw_empty[i], R::kXf + (Op::kMmaReadsRaw ? 1 : 0));
+      tc::mbar_init(&raw_empty[i], IP ? 1 : R::kXf + (Op::kMmaReadsRaw ? 1 : 0));
     }
     for (int i = 0; i < NS; ++i) {
       tc::mbar_init(&op_full[i], R::kXf);
@@ -253,10 +256,11 @@ __global__ void __launch_bounds__(Roles<Op>::kThreads, 1) tc2_kernel(const __gri
           const int s = it % NS, r = it % NR;
           tc::mbar_wait(&op_full[s], (it / NS) & 1);
           tc::tc_fence_after();
-          op.mma(tc::smem_u32(op_ring + s * Op::kOpBytes), tc::smem_u32(raw_ring + r * Op::kRawBytes),
-                 tc::smem_u32(aux), tmem + a * TC, kb);
-          tc::mma_commit(&op_empty[s]);
-          if constexpr (Op::kMmaReadsRaw) tc::mma_commit(&raw_empty[r]);
+          const uint8_t* opnd = IP ? raw_ring + r * Op::kRawBytes : op_ring + s * Op::kOpBytes;
+          op.mma(tc::smem_u32(opnd), tc::smem_u32(raw_ring + r * Op::kRawBytes), tc::smem_u32(aux),
+                 tmem + a * TC, kb);
+          if constexpr (!IP) tc::mma_commit(&op_empty[s]);
+          if constexpr (Op::kMmaReadsRaw || IP) tc::mma_commit(&raw_empty[r]);
         }
         tc::mma_commit(&acc_full[a]);
         if (dbg && at < 4) clk[10 + at] = dbg_now();
@@ -367,17 +371,18 @@ __global__ void __launch_bounds__(Roles<Op>::kThreads, 1) tc2_kernel(const __gri
         const long long w0 = dbg ? dbg_now() : 0;
         tc::mbar_wait(&raw_full[r], (it / NR) & 1);
         const long long w1 = dbg ? dbg_now() : 0;
-        tc::mbar_wait(&op_empty[s], ((it / NS) & 1) ^ 1);
+        if constexpr (!IP) tc::mbar_wait(&op_empty[s], ((it / NS) & 1) ^ 1);
         if (dbg && tid == R::kXfWarp0 * 32) {
           clk[25] += w1 - w0;
           clk[26] += dbg_now() - w1;
         }
-        op.transform(tile, kb, raw_ring + r * Op::kRawBytes, op_ring + s * Op::kOpBytes, aux, xt);
+        uint8_t* rs = raw_ring + r * Op::kRawBytes;
+        op.transform(tile, kb, rs, IP ? rs : op_ring + s * Op::kOpBytes, aux, xt);
         tc::fence_proxy_async();
         __syncwarp();
         if (lane == 0) {
           mbar_arrive(&op_full[s]);
-          mbar_arrive(&raw_empty[r]);
+          if constexpr (!IP) mbar_arrive(&raw_empty[r]);
         }
         if (dbg && tid == R::kXfWarp0 * 32 && kb == op.num_kb(tile) - 1) {
           const int t = (tile - static_cast<int>(blockIdx.x)) / static_cast<int>(gridDim.x);
@@ -401,9 +406,13 @@ __global__ void __launch_bounds__(Roles<Op>::kThreads, 1) tc2_kernel(const __gri
 // for the whole persistent CTA (RES: copied once in the prologue) or
 // streamed per K block into the raw stage by a 1D bulk copy (large c).
 // Operand stage: A hi | A lo.
-template <int BN_, bool RES>
+template <int BN_, bool RES, bool IP_ = false>
 struct Fwd1x1 {
   static constexpr int BN = BN_;
+  // IP_: in place — the operand A hi | A lo overwrites the stage's two fp32
+  // boxes (32 KB each way), so the operand ring's shared memory buys a third
+  // raw stage (streamed W1 only: one more stage of TMA latency in flight)
+  static constexpr bool kInPlace = IP_;
   static constexpr int kTmemCols = BN;
   static constexpr bool kEarlyLoads = true;  // features / g0 / z: >= two launches old
   static constexpr bool kColSums = true;
@@ -411,10 +420,11 @@ struct Fwd1x1 {
   static constexpr int kBox = 32 * kBM * 4;                    // 16 KB
   static constexpr int kBBytes = tc::Tile<BN>::kBytes;
   static constexpr int kRawBytes = 2 * kBox + (RES ? 0 : 2 * kBBytes);
-  static constexpr int kNR = RES ? 3 : (BN <= 64 ? 3 : 2);
+  static constexpr int kNR = IP_ ? 3 : RES ? 3 : (BN <= 64 ? 3 : 2);
   static constexpr int kABytes = tc::Tile<kBM>::kBytes;         // 16 KB
   static constexpr int kOpBytes = 2 * kABytes;
-  static constexpr int kNS = 2;
+  static constexpr int kNS = IP_ ? 0 : 2;
+  static_assert(!IP_ || (!RES && 2 * kBox == kOpBytes), "in place: streamed W1, boxes = operand");
   static constexpr int kNE = 0, kEpiBytes = 0;
   static constexpr bool kEpiStore = false;
   static constexpr int kEpiWarps = 8, kXfWarps = 8;
@@ -513,8 +523,35 @@ struct Fwd1x1 {
         sh[i] = 0.f;
       }
     }
+    constexpr int kChunks = kBM * kBK / 8 / kXfThreads;
+    if constexpr (IP_) {
+      // every transform thread reads all of its chunks, the transform warps
+      // meet, then the operand overwrites the boxes
+      float v[kChunks][8];
 #pragma unroll
-    for (int i = 0; i < kBM * kBK / 8 / kXfThreads; ++i) {
+      for (int i = 0; i < kChunks; ++i) {
+        const int row = row0 + i * (kXfThreads / 8);
+        if (ch0 < a.c) {
+          raw_read8(raw + (kc >> 5) * kBox, row, kc & 31, v[i]);
+#pragma unroll
+          for (int e = 0; e < 8; ++e) v[i][e] = fmaxf(fmaf(v[i][e], sc[e], sh[e]), 0.f);
+        } else {
+          tc::zero8(v[i]);
+        }
+      }
+      named_sync(2, kXfThreads);
+#pragma unroll
+      for (int i = 0; i < kChunks; ++i) {
+        const int row = row0 + i * (kXfThreads / 8);
+        uint4 h, l;
+        tc::split8_h(v[i], h, l);  // fp16x3 forward operands (dpb_tc.cuh)
+        const uint32_t off = tc::Tile<kBM>::kmajor_chunk(row, kc);
+        tc::st_shared16(ah, off, h);
+        tc::st_shared16(al, off, l);
+      }
+    } else {
+#pragma unroll
+    for (int i = 0; i < kChunks; ++i) {
       const int row = row0 + i * (kXfThreads / 8);
       float v[8];
       if (ch0 < a.c) {
@@ -529,6 +566,7 @@ struct Fwd1x1 {
       const uint32_t off = tc::Tile<kBM>::kmajor_chunk(row, kc);
       tc::st_shared16(ah, off, h);
       tc::st_shared16(al, off, l);
+    }
     }
   }
   __device__ void mma(uint32_t op, uint32_t raw, uint32_t aux, uint32_t tmem, int kb) const {
@@ -656,6 +694,7 @@ __host__ __device__ inline int bwd_nkb(int bk) { return (bk + 31) / 32; }
 // the four epilogue groups; 4 frees 16 KB for bk = 192's resident W1^T).
 template <int BN_, int NE_ = 5>
 struct Dgrad1x1 {
+  static constexpr bool kInPlace = false;
   static constexpr int BN = BN_;
   static constexpr int kTmemCols = BN;
   static constexpr bool kEarlyLoads = true;  // g0 (3x3 dgrad) and z: >= two launches old
@@ -793,6 +832,7 @@ struct Dgrad1x1 {
 // width); k_reduce_w1 folds the splits.  graph.hpp:920-922, ops.hpp:330-387.
 template <int BN_, int JB>
 struct Wgrad1x1 {
+  static constexpr bool kInPlace = false;
   static constexpr int BN = BN_;
   static constexpr int kMT = (JB * 32 + 127) / 128;
   static constexpr int kTmemCols = kMT * BN;
