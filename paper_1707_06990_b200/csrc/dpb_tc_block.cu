@@ -211,7 +211,9 @@ int tc_conv3x3_fwd(Block* b, const LayerArgs<float>& a, int l) {
       // the epilogue's per-tap output slices [9][128][k] fp32 reuse the stages
       const size_t ytap = 9ull * tc::kBM * a.k * 4;
       const size_t taux = std::max(aux, ytap > tstage * nst ? ytap - tstage * nst : size_t{0});
-      launch_halo(b, tc::Tc3x3FwdTaps{h}, grid, tstage, nst, taux);
+      tc::Tc3x3FwdTaps op{h};
+      op.prod0 = 0;  // every warp produces (the taps GEMM keeps the shared-barrier engine path)
+      launch_halo(b, op, grid, tstage, nst, taux);
       return static_cast<int>(grid.x);
     }
     {

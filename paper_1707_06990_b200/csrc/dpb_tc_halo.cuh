@@ -425,7 +425,6 @@ struct Tc3x3FwdHalo {
   static constexpr int kIssuers = DPB_FWD_ISSUERS, kAccCopies = kIssuers;
   // producer threads: the warps past the issuers (an issuing warp is held by
   // the tensor pipe's issue rate; the others build the next K chunk meanwhile)
-  static constexpr int kProd0 = 32 * kIssuers, kProdThreads = kThreads - kProd0;
   static constexpr bool kSpecialized = kIssuers < 8;
   static constexpr int kTmemCols = BN * kAccCopies;
   static constexpr bool kTapCols = false;
@@ -435,6 +434,9 @@ struct Tc3x3FwdHalo {
   static constexpr bool kBulk = true;
   static constexpr int kEpiPrefetch = 0;  // (see Tc3x3DgradHalo)
   HaloArgs h;
+  // producer threads [prod0, kThreads): past the issuer warps here; all of
+  // them for Tc3x3FwdTaps (non-specialised engine path), set by the host
+  int prod0 = 32 * kIssuers;
   __device__ uint32_t halo_bytes() const { return static_cast<uint32_t>(h.g.R * h.kc * 2); }
   __device__ uint32_t b_bytes() const { return static_cast<uint32_t>(9 * BN * h.kc * 2); }
   __device__ uint32_t stage_bytes() const { return 2 * (halo_bytes() + b_bytes()); }
@@ -445,8 +447,9 @@ struct Tc3x3FwdHalo {
   static constexpr int kRawDepth = 2;
   __host__ __device__ static uint32_t raw_offset(int bk) { return (sizeof(BnFwd) * bk + 127) / 128 * 128; }
   __host__ __device__ static uint32_t raw_bytes(int R, int kc) { return static_cast<uint32_t>(R) * kc * 4; }
-  __host__ __device__ static uint32_t rows_offset(int bk, int R, int kc) {
-    return raw_offset(bk) + kRawDepth * raw_bytes(R, kc);
+  __host__ __device__ static uint32_t rows_offset(int bk, int R, int kc) {  // one ring slot when nkb == 1
+    const int nkb = (bk + kc - 1) / kc;
+    return raw_offset(bk) + (nkb < kRawDepth ? nkb : kRawDepth) * raw_bytes(R, kc);
   }
   __host__ __device__ static uint32_t aux_bytes(int bk, int R, int kc) { return rows_offset(bk, R, kc) + 4 * R; }
   __device__ void prologue(uint8_t* aux) const {
@@ -490,7 +493,8 @@ struct Tc3x3FwdHalo {
     const int j_base = kb * h.kc;
     const float* zb = a.z + static_cast<int64_t>(img()) * h.g.H * h.g.W * a.bk + j_base;
     const int nchunk = h.g.R * kcn;
-    for (int q = static_cast<int>(threadIdx.x) - kProd0; q < nchunk; q += kProdThreads) {
+    const int pthreads = kThreads - prod0;
+    for (int q = static_cast<int>(threadIdx.x) - prod0; q < nchunk; q += pthreads) {
       int r, kk;
       chunk_coords(q, kcn, r, kk);
       const int ro = rowoff[r];
@@ -503,7 +507,8 @@ struct Tc3x3FwdHalo {
     cp_async_commit();
   }
   __device__ void produce(uint8_t* st, int kb, const uint8_t* aux) const {
-    if (static_cast<int>(threadIdx.x) < kProd0) return;
+    if (static_cast<int>(threadIdx.x) < prod0) return;
+    const int pthreads = kThreads - prod0;
     const LayerArgs<float>& a = h.a;
     const BnFwd* bn = reinterpret_cast<const BnFwd*>(aux);
     uint8_t* xh = st;
@@ -522,10 +527,10 @@ struct Tc3x3FwdHalo {
     const int j_base = kb * h.kc;
     const int kcn = h.kc >> 3;
     const int nchunk = h.g.R * kcn;
-    const int q0 = static_cast<int>(threadIdx.x) - kProd0;
+    const int q0 = static_cast<int>(threadIdx.x) - prod0;
     // a thread's channel group is the same for all its chunks when the stride
     // is a multiple of 8 * kcn: its BN constants are loaded once per K chunk
-    const bool fixed = (kProdThreads >> 3) % kcn == 0;
+    const bool fixed = (pthreads >> 3) % kcn == 0;
     float mu[8], sc[8], be[8];
     {
       int r0, kk;
@@ -538,7 +543,7 @@ struct Tc3x3FwdHalo {
         be[e] = bn[j].beta;
       }
     }
-    for (int q = q0; q < nchunk; q += kProdThreads) {
+    for (int q = q0; q < nchunk; q += pthreads) {
       int r, kk;
       chunk_coords(q, kcn, r, kk);
       const int j0 = j_base + kk;
@@ -870,12 +875,22 @@ struct Tc3x3WgradHalo {
   // (stage parity): row r -> image-local pixel of the tile's halo row, or -1
   __host__ __device__ static uint32_t rows_offset(int bk) { return (16 * bk + 127) / 128 * 128; }
   __host__ __device__ static uint32_t aux_bytes(int bk, int R) { return rows_offset(bk) + 2 * 4 * R; }
+  // halo row table of K block kb (the CTA's kb-th tile) into table kb & 1:
+  // the prologue fills table 0, produce(kb) fills table kb+1 after its own
+  // loads, so no extra barrier (the engine's barrier after produce orders it)
+  __device__ void fill_rows(const uint8_t* aux, int kb) const {
+    int* rows = const_cast<int*>(reinterpret_cast<const int*>(aux + rows_offset(h.a.bk))) + (kb & 1) * h.g.R;
+    const int gt = blockIdx.x * tpc + kb;
+    const int t = gt - (gt / h.g.tpi) * h.g.tpi;
+    for (int r = threadIdx.x; r < h.g.R; r += kThreads) rows[r] = h.g.pixel(h.g.pos(t, r));
+  }
   __device__ void prologue(uint8_t* aux) const {
     float4* bq = reinterpret_cast<float4*>(aux);
     for (int j = threadIdx.x; j < h.a.bk; j += kThreads) {
       const float inv = bn_inv(h.a.bvar[j]);
       bq[j] = make_float4(h.a.bmean[j], h.a.gamma_b[j] * inv, h.a.beta_b[j], 0.f);  // fill_bn_fwd's fields
     }
+    fill_rows(aux, 0);
   }
   __device__ void bulk(uint32_t, int, uint64_t*) const {}
   __device__ void produce(uint8_t* st, int kb, const uint8_t* aux) const {
@@ -885,9 +900,7 @@ struct Tc3x3WgradHalo {
     uint8_t* xs = st;
     uint8_t* dys = st + halo_bytes();
     const int gt = blockIdx.x * tpc + kb;
-    const int im = gt / h.g.tpi, t = gt - im * h.g.tpi;
-    for (int r = threadIdx.x; r < h.g.R; r += kThreads) rows[r] = h.g.pixel(h.g.pos(t, r));
-    __syncthreads();  // (the parity-(kb-2) table's readers finished before produce(kb-1)'s barrier)
+    const int im = gt / h.g.tpi;
     const float* zb = a.z + static_cast<int64_t>(im) * h.g.H * h.g.W * a.bk;
     const float* gb = a.acc + static_cast<int64_t>(im) * h.g.H * h.g.W * a.Ca + a.c;
     const int j_base = blockIdx.y * kBM;
@@ -954,6 +967,7 @@ struct Tc3x3WgradHalo {
         }
       }
     }
+    if (kb + 1 < num_kb()) fill_rows(aux, kb + 1);
   }
   __device__ void issue(uint32_t st, int kb, uint32_t tmem, int part) const {
     constexpr uint32_t idesc = make_idesc(BN, 1, 1);

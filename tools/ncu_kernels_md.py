@@ -41,10 +41,13 @@ else:  # r02: DenseNet-264-k32 at batch 64 (the SPECS of tools/ncu_round.sh in r
     b3f = {kk[0]: kk for kk in block_kernels(12544, 1216, 128, 32)}
     b3b = {kk[0]: kk for kk in block_kernels(12544, 1312, 128, 32)}
     b1 = {kk[0]: kk for kk in block_kernels(200704, 64 + 3 * 32, 128, 32)}
+    M1 = 802816  # stem conv output pixels (64 x 112 x 112)
     KERNELS = [b3f["Fwd1x1"], b1["Tc3x3FwdHalo"], b3b["Tc3x3DgradHalo"], b3b["Dgrad1x1"], b3b["Wgrad1x1"],
                b3b["Tc3x3WgradHalo"], b3b["k_bn_apply_accumulate4"],
-               ("k_stem7_wgrad", "ImageNet stem dW (SIMT, fused BN-backward apply)",
-                802816 * (4 * 64 + 4 * 64) + 64 * 3 * 224 * 224 * 4, 2 * 802816 * 64 * 147)]
+               ("StemConvGemm", "ImageNet stem conv 7x7/2 (tcgen05, space-to-depth operands, fp16x3)",
+                M1 * 64 * 4 + 64 * 3 * 224 * 224 * 4, 2 * M1 * 64 * 147),
+               ("StemWgradGemm", "ImageNet stem dW (tcgen05, BN-backward apply in the producer)",
+                M1 * (4 * 64 + 4 * 64) + 64 * 3 * 224 * 224 * 4, 2 * M1 * 64 * 147)]
 KEYS = {"dur": "gpu__time_duration.sum", "rd": "dram__bytes_read.sum", "wr": "dram__bytes_write.sum",
         "dram": "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed",
         "tensor": "sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed",
@@ -102,10 +105,10 @@ if R != "r01":
            "44 FLOP/B against a ridge of 254).  At 14x14 and batch 64 a layer has 98 pixel tiles: the "
            "persistent 1x1 kernels run one or two tiles per CTA, and their per-SM operand intake (features "
            "+ the streamed W1 image) is the limit (fwd 0.26, dgrad 0.37, wgrad 0.25 of HBM).  The 3x3 halo "
-           "kernels hold ~140 KB of shared memory, so one CTA per SM (12 % warps active) runs "
-           "produce -> MMA -> epilogue in sequence: 0.05-0.11 of HBM, 2-9 % tensor pipe.  The BN_a "
-           "apply + accumulate streams at 0.89 of HBM.  The SIMT stem dW is latency-bound (128 "
-           "registers, 21 % warps active)."]
+           "kernels run one CTA per SM; the forward's producer warps now build K chunk kb+1 while "
+           "two issuer warps drive chunk kb's MMAs (mbarrier hand-off), the dgrad splits its 128 "
+           "output columns over two CTAs per tile under two waves.  The BN_a apply + accumulate "
+           "streams near HBM speed.  The stem runs on the tensor cores (space-to-depth operands)."]
 md += [] if R != "r01" else ["", "Reading: every kernel is HBM/latency-bound (intensity 18-66 FLOP/B against a bf16 ridge of "
        "254 FLOP/B).  So the tensor pipe idles by construction: at the HBM roofline these shapes reach "
        "at most 7-26 % tensor-pipe utilisation.  The gap to the roofline is per-tile latency (the 3x3 halo "

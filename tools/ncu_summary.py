@@ -27,6 +27,7 @@ CATEGORIES = [
     ("Tc3x3FwdHalo", "conv3x3_fwd"), ("Tc3x3Fwd", "conv3x3_fwd"), ("Conv3x3Fwd", "conv3x3_fwd"),
     ("Tc1x1Dgrad", "conv1x1_dgrad"), ("Tc1x1Wgrad", "conv1x1_wgrad"),
     ("Dgrad1x1", "conv1x1_dgrad"), ("Wgrad1x1", "conv1x1_wgrad"),
+    ("StemConvGemm", "model: stem"), ("StemWgradGemm", "model: stem"), ("TransWgradGemm", "model: transition GEMMs"),
     ("k_zsplit_reduce", "conv1x1_fwd"), ("k_stem", "model: stem"), ("k_trans_pool", "model: transition fwd"), ("k_gemm", "model: transition GEMMs"),
     ("TransGemm", "model: transition GEMMs"), ("k_pool_bnb_", "model: transition/head BN bwd"),
     ("k_bnb_", "model: transition/head BN bwd"), ("k_head", "model: head"), ("k_loss", "model: head"),
