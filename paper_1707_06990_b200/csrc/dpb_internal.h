@@ -91,6 +91,7 @@ struct HaloPlan {
   bool fwd_taps = false;  // forward as one GEMM over all 9 taps (Tc3x3FwdTaps)
   int fwd_bn = 0, fwd_kc = 0, bwd_bn = 0, bwd_kc = 0;
   int bwd_split = 1;  // 3x3 dgrad: output-column groups of bwd_bn per tile (grid.y)
+  int fwd_ring = 2;   // 3x3 forward: raw halo ring depth (1 when that fits two CTAs per SM)
   int64_t fwd_layer_bytes = 0, bwd_layer_bytes = 0;  // pre-tiled W2 image per layer
 };
 

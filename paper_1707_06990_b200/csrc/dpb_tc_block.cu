@@ -108,9 +108,10 @@ HaloPlan tc_halo_plan(const dpb_block_desc& d) {
   // fits one CTA.
   // DPB_HALO_KC=<kc> forces a chunk (when it fits).
   static const int force_kc = std::getenv("DPB_HALO_KC") ? std::atoi(std::getenv("DPB_HALO_KC")) : 0;
+  int ring = 2;  // raw halo ring depth of the forward producer
   auto fwd_aux = [&](int kc) {  // BN table + the raw fp32 halo ring (Tc3x3FwdHalo::fetch)
     using Op = tc::Tc3x3FwdHalo<16>;
-    return static_cast<size_t>(Op::aux_bytes(static_cast<int>(d.bk), g.R, kc));
+    return static_cast<size_t>(Op::aux_bytes(static_cast<int>(d.bk), g.R, kc, ring));
   };
   auto fwd_fits = [&](int kc, size_t lim) {
     const size_t stage = 2ull * (static_cast<size_t>(g.R) * kc * 2 + 9ull * bn * kc * 2);
@@ -122,8 +123,13 @@ HaloPlan tc_halo_plan(const dpb_block_desc& d) {
   // 56x56 and 28x28 gain 16 % / 10 %; 14x14 and 7x7, under one wave, lose to
   // the smaller chunks' extra rounds)
   const int64_t tiles = d.n * g.tpi;
-  for (int kc = std::min(64, d.bk); d.bk % 16 == 0 && bn <= 64 && kc >= 16 && !kc_pick && tiles > 148; kc /= 2)
-    if (kc % 16 == 0 && fwd_fits(kc, kHaloSmemMax / 2 - 1024)) kc_pick = kc;
+  // (two CTAs per SM first with the two-slot raw ring, then with one slot)
+  for (int want = 2; want >= 1 && !kc_pick; --want) {
+    ring = want;
+    for (int kc = std::min(64, d.bk); d.bk % 16 == 0 && bn <= 64 && kc >= 16 && !kc_pick && tiles > 148; kc /= 2)
+      if (kc % 16 == 0 && fwd_fits(kc, kHaloSmemMax / 2 - 1024)) kc_pick = kc;
+  }
+  if (!kc_pick) ring = 2;
   if (force_kc >= 16 && force_kc % 16 == 0 && force_kc <= 64 && fwd_fits(force_kc, kHaloSmemMax)) kc_pick = force_kc;
   for (int kc = std::min(64, d.bk); d.bk % 16 == 0 && bn <= 64 && kc >= 16; kc /= 2) {
     if (kc % 16 != 0) continue;
@@ -135,6 +141,7 @@ HaloPlan tc_halo_plan(const dpb_block_desc& d) {
       p.fwd_ok = true;
       p.fwd_bn = bn;
       p.fwd_kc = kc;
+      p.fwd_ring = ring;
       p.fwd_layer_bytes = static_cast<int64_t>(nkb) * 2 * (9LL * bn * kc * 2);
       // all taps as GEMM columns: N = 9k <= 128 (two 128-column accumulators),
       // 4-column TMEM loads per tap, both 128-row M blocks inside the halo
@@ -193,6 +200,13 @@ void tc_pretile_w2(Block* b, const float* params, bool fwd) {
   }
 }
 
+template <int BN>
+static tc::Tc3x3FwdHalo<BN> fwd_op(const tc::HaloArgs& h, int ring) {
+  tc::Tc3x3FwdHalo<BN> op{h};
+  op.raw_want = ring;
+  return op;
+}
+
 // Returns the number of per-CTA partial rows written (for the finalize).
 int tc_conv3x3_fwd(Block* b, const LayerArgs<float>& a, int l) {
   const int bn = pick_bn(a.k);
@@ -203,7 +217,8 @@ int tc_conv3x3_fwd(Block* b, const LayerArgs<float>& a, int l) {
     const size_t stage = 2ull * (static_cast<size_t>(h.g.R) * kc * 2 + 9ull * bn * kc * 2);
     const int nst = (a.bk + kc - 1) / kc > 1 ? 2 : 1;
     using FH = tc::Tc3x3FwdHalo<16>;
-    const size_t aux = FH::aux_bytes(a.bk, h.g.R, kc);
+    const int ring = b->halo.fwd_ring;
+    const size_t aux = FH::aux_bytes(a.bk, h.g.R, kc, ring);
     if (b->halo.fwd_taps) {
       const dim3 grid(static_cast<unsigned>(nimg(a) * h.g.tpi));
       const size_t np = (9 * a.k + 15) / 16 * 16;
@@ -213,16 +228,17 @@ int tc_conv3x3_fwd(Block* b, const LayerArgs<float>& a, int l) {
       const size_t taux = std::max(aux, ytap > tstage * nst ? ytap - tstage * nst : size_t{0});
       tc::Tc3x3FwdTaps op{h};
       op.prod0 = 0;  // every warp produces (the taps GEMM keeps the shared-barrier engine path)
+      op.raw_want = ring;
       launch_halo(b, op, grid, tstage, nst, taux);
       return static_cast<int>(grid.x);
     }
     {
       const dim3 grid(static_cast<unsigned>(nimg(a) * h.g.tpi));
       switch (bn) {
-        case 16: launch_halo(b, tc::Tc3x3FwdHalo<16>{h}, grid, stage, nst, aux); break;
-        case 32: launch_halo(b, tc::Tc3x3FwdHalo<32>{h}, grid, stage, nst, aux); break;
-        case 48: launch_halo(b, tc::Tc3x3FwdHalo<48>{h}, grid, stage, nst, aux); break;
-        default: launch_halo(b, tc::Tc3x3FwdHalo<64>{h}, grid, stage, nst, aux); break;
+        case 16: launch_halo(b, fwd_op<16>(h, ring), grid, stage, nst, aux); break;
+        case 32: launch_halo(b, fwd_op<32>(h, ring), grid, stage, nst, aux); break;
+        case 48: launch_halo(b, fwd_op<48>(h, ring), grid, stage, nst, aux); break;
+        default: launch_halo(b, fwd_op<64>(h, ring), grid, stage, nst, aux); break;
       }
       return static_cast<int>(grid.x);
     }

@@ -437,26 +437,33 @@ struct Tc3x3FwdHalo {
   // producer threads [prod0, kThreads): past the issuer warps here; all of
   // them for Tc3x3FwdTaps (non-specialised engine path), set by the host
   int prod0 = 32 * kIssuers;
+  int raw_want = 2;  // raw ring depth requested by the host (HaloPlan::fwd_ring)
   __device__ uint32_t halo_bytes() const { return static_cast<uint32_t>(h.g.R * h.kc * 2); }
   __device__ uint32_t b_bytes() const { return static_cast<uint32_t>(9 * BN * h.kc * 2); }
   __device__ uint32_t stage_bytes() const { return 2 * (halo_bytes() + b_bytes()); }
   __device__ int num_kb() const { return (h.a.bk + h.kc - 1) / h.kc; }
   __device__ int tile() const { return blockIdx.x % h.g.tpi; }
   __device__ int img() const { return blockIdx.x / h.g.tpi; }
-  // aux: BN table | raw fp32 halo ring (kRawDepth K chunks) | halo row table
-  static constexpr int kRawDepth = 2;
+  // aux: BN table | raw fp32 halo ring (depth K chunks) | halo row table.
+  // depth 2 fetches chunk kb+1 while kb is transformed; depth 1 (the host's
+  // choice when that is what lets two CTAs share an SM) fetches chunk by chunk
   __host__ __device__ static uint32_t raw_offset(int bk) { return (sizeof(BnFwd) * bk + 127) / 128 * 128; }
   __host__ __device__ static uint32_t raw_bytes(int R, int kc) { return static_cast<uint32_t>(R) * kc * 4; }
-  __host__ __device__ static uint32_t rows_offset(int bk, int R, int kc) {  // one ring slot when nkb == 1
+  __host__ __device__ static int ring_depth(int bk, int kc, int want) {  // one slot when nkb == 1
     const int nkb = (bk + kc - 1) / kc;
-    return raw_offset(bk) + (nkb < kRawDepth ? nkb : kRawDepth) * raw_bytes(R, kc);
+    return nkb < want ? nkb : want;
   }
-  __host__ __device__ static uint32_t aux_bytes(int bk, int R, int kc) { return rows_offset(bk, R, kc) + 4 * R; }
+  __host__ __device__ static uint32_t rows_offset(int bk, int R, int kc, int want) {
+    return raw_offset(bk) + ring_depth(bk, kc, want) * raw_bytes(R, kc);
+  }
+  __host__ __device__ static uint32_t aux_bytes(int bk, int R, int kc, int want) {
+    return rows_offset(bk, R, kc, want) + 4 * R;
+  }
   __device__ void prologue(uint8_t* aux) const {
     fill_bn_fwd(reinterpret_cast<BnFwd*>(aux), h.a.bk, 0, h.a.bmean, h.a.bvar, h.a.gamma_b,
                 h.a.beta_b);
     // halo row r -> element offset of its pixel's z row within the image, or -1 (padding)
-    int* rowoff = reinterpret_cast<int*>(aux + rows_offset(h.a.bk, h.g.R, h.kc));
+    int* rowoff = reinterpret_cast<int*>(aux + rows_offset(h.a.bk, h.g.R, h.kc, raw_want));
     const int t = tile();
     for (int r = threadIdx.x; r < h.g.R; r += kThreads) {
       const int pp = h.g.pixel(h.g.pos(t, r));
@@ -487,8 +494,9 @@ struct Tc3x3FwdHalo {
   // (thread-local groups: no barrier).
   __device__ void fetch(int kb, uint8_t* aux) const {
     const LayerArgs<float>& a = h.a;
-    const uint32_t ring = smem_u32(aux + raw_offset(a.bk) + (kb % kRawDepth) * raw_bytes(h.g.R, h.kc));
-    const int* rowoff = reinterpret_cast<const int*>(aux + rows_offset(a.bk, h.g.R, h.kc));
+    const int depth = ring_depth(a.bk, h.kc, raw_want);
+    const uint32_t ring = smem_u32(aux + raw_offset(a.bk) + (kb % depth) * raw_bytes(h.g.R, h.kc));
+    const int* rowoff = reinterpret_cast<const int*>(aux + rows_offset(a.bk, h.g.R, h.kc, raw_want));
     const int kcn = h.kc >> 3;
     const int j_base = kb * h.kc;
     const float* zb = a.z + static_cast<int64_t>(img()) * h.g.H * h.g.W * a.bk + j_base;
@@ -515,15 +523,21 @@ struct Tc3x3FwdHalo {
     uint8_t* xl = st + halo_bytes();
     const int nkb = num_kb();
     uint8_t* waux = const_cast<uint8_t*>(aux);
-    if (kb == 0) fetch(0, waux);
-    if (kb + 1 < nkb) {  // slot (kb+1) % 2 held chunk kb-1, transformed by this thread already
-      fetch(kb + 1, waux);
-      cp_async_wait<1>();
-    } else {
+    const int depth = ring_depth(a.bk, h.kc, raw_want);
+    if (depth >= 2) {
+      if (kb == 0) fetch(0, waux);
+      if (kb + 1 < nkb) {  // slot (kb+1) % 2 held chunk kb-1, transformed by this thread already
+        fetch(kb + 1, waux);
+        cp_async_wait<1>();
+      } else {
+        cp_async_wait<0>();
+      }
+    } else {  // one slot: this chunk's copies, then its transform
+      fetch(kb, waux);
       cp_async_wait<0>();
     }
-    const float* ring = reinterpret_cast<const float*>(aux + raw_offset(a.bk) + (kb % kRawDepth) * raw_bytes(h.g.R, h.kc));
-    const int* rowoff = reinterpret_cast<const int*>(aux + rows_offset(a.bk, h.g.R, h.kc));
+    const float* ring = reinterpret_cast<const float*>(aux + raw_offset(a.bk) + (kb % depth) * raw_bytes(h.g.R, h.kc));
+    const int* rowoff = reinterpret_cast<const int*>(aux + rows_offset(a.bk, h.g.R, h.kc, raw_want));
     const int j_base = kb * h.kc;
     const int kcn = h.kc >> 3;
     const int nchunk = h.g.R * kcn;
