@@ -343,8 +343,7 @@ static void forward_impl(Block* b, const float* x_in, const float* params, float
              static_cast<int>(g.Cp), 0, g.M, d.c0, b->part);
     }
     LaunchScope ls(b, KC_FINALIZE, 16.0 * g.P * d.c0, 0, 16.0 * g.P * d.c0);
-    launch(k_finalize_stats, static_cast<unsigned>((d.c0 + kFinCh - 1) / kFinCh), kFinThreads, 0, b->stream, 
-        b->part, g.P, d.c0, count, fmean, fvar, 0);
+    launch_finalize_stats_at(b->stream, b->part, g.P, d.c0, count, fmean, fvar, 0);
   }
   for (int l = 0; l < d.m; ++l) {
     LayerArgs<S> a = layer_args<S>(b, params, l);
@@ -376,8 +375,7 @@ static void forward_impl(Block* b, const float* x_in, const float* params, float
     if (!eval) {
       LaunchScope ls(b, KC_FINALIZE, 16.0 * p1 * d.bk, 0, 16.0 * p1 * d.bk);
       float* zm = b->zstat + static_cast<int64_t>(l) * 2 * d.bk;
-      launch(k_finalize_stats, static_cast<unsigned>((d.bk + kFinCh - 1) / kFinCh), kFinThreads, 0, b->stream, 
-          b->part, p1, d.bk, count, zm, zm + d.bk, 0);
+      launch_finalize_stats_at(b->stream, b->part, p1, d.bk, count, zm, zm + d.bk, 0);
     }
     int p3 = g.P;
     {
@@ -387,8 +385,7 @@ static void forward_impl(Block* b, const float* x_in, const float* params, float
     }
     if (!eval) {
       LaunchScope ls(b, KC_FINALIZE, 16.0 * p3 * d.k, 0, 16.0 * p3 * d.k);
-      launch(k_finalize_stats, static_cast<unsigned>((d.k + kFinCh - 1) / kFinCh), kFinThreads, 0, b->stream, 
-          b->part, p3, d.k, count, fmean, fvar, a.c);
+      launch_finalize_stats_at(b->stream, b->part, p3, d.k, count, fmean, fvar, a.c);
     }
   }
   tr.on(0, 7 * d.m, BlockTrace::kConcat, 0.0);  // block-output concat: the feature buffer itself
@@ -508,8 +505,7 @@ static void backward_impl(Block* b, const float* params, float* grad_acc, float*
     // BN_b backward sums -> dgamma_b, dbeta_b, coefficients (graph.hpp:913-916)
     {
       LaunchScope ls(b, KC_FINALIZE, 16.0 * pd * d.bk, 0, 16.0 * pd * d.bk);
-      launch(k_finalize_bn_bwd, static_cast<unsigned>((d.bk + kFinCh - 1) / kFinCh), kFinThreads, 0, b->stream, 
-          b->part, pd, d.bk, count, d_gb, d_bb, const_cast<float*>(a.bnb_bwd));
+      launch_finalize_bn_bwd(b->stream, b->part, pd, d.bk, count, d_gb, d_bb, const_cast<float*>(a.bnb_bwd));
     }
     if (fork) {
       cudaEventRecord(ev(l, 1), main_st);
@@ -555,8 +551,7 @@ static void backward_impl(Block* b, const float* params, float* grad_acc, float*
     float* bna = b->bna_bwd + (l & 1) * 2 * g.cmaxp;  // parity buffer (split_apply)
     {
       LaunchScope ls(b, KC_FINALIZE, 16.0 * g.P * a.c, 0, 16.0 * g.P * a.c);
-      launch(k_finalize_bn_bwd, static_cast<unsigned>((a.c + kFinCh - 1) / kFinCh), kFinThreads, 0, b->stream,
-             b->part, g.P, a.c, count, d_ga, d_ba, bna);
+      launch_finalize_bn_bwd(b->stream, b->part, g.P, a.c, count, d_ga, d_ba, bna);
     }
     // The accumulate of layer l updates channels [0, c_l); only its last k,
     // [c_l - k, c_l), feed layer l-1's 3x3 dgrad next.  With split_apply that
@@ -610,10 +605,26 @@ static void backward_impl(Block* b, const float* params, float* grad_acc, float*
 }
 
 // Folds shared with the whole-network step (dpb_model.cu).
+// Many partial rows (the 56x56 blocks, the stem): 4 channels per CTA, so four
+// times the CTAs share the fold.
+constexpr int kFinWideP = 512;
 void launch_finalize_bn_bwd(cudaStream_t st, const double2* part, int P, int nch, double count,
                             float* dgamma, float* dbeta, float* coef) {
-  launch(k_finalize_bn_bwd, static_cast<unsigned>((nch + kFinCh - 1) / kFinCh), kFinThreads, 0, st, part, P, nch, count, dgamma, dbeta,
-         coef);
+  if (P > kFinWideP)
+    launch(k_finalize_bn_bwd<4>, static_cast<unsigned>((nch + 3) / 4), kFinThreads, 0, st, part, P, nch, count,
+           dgamma, dbeta, coef);
+  else
+    launch(k_finalize_bn_bwd<kFinCh>, static_cast<unsigned>((nch + kFinCh - 1) / kFinCh), kFinThreads, 0, st, part,
+           P, nch, count, dgamma, dbeta, coef);
+}
+void launch_finalize_stats_at(cudaStream_t st, const double2* part, int P, int nch, double count, float* mean,
+                              float* var, int first) {
+  if (P > kFinWideP)
+    launch(k_finalize_stats<4>, static_cast<unsigned>((nch + 3) / 4), kFinThreads, 0, st, part, P, nch, count, mean,
+           var, first);
+  else
+    launch(k_finalize_stats<kFinCh>, static_cast<unsigned>((nch + kFinCh - 1) / kFinCh), kFinThreads, 0, st, part, P,
+           nch, count, mean, var, first);
 }
 void launch_fold_splits(cudaStream_t st, const float* wpart, int splits, int64_t n, float* out) {
   launch(k_reduce_w1, blocks_for(n, 32), dim3(32, 8), 0, st, wpart, splits, 1, static_cast<int>(n), out);
@@ -624,8 +635,7 @@ void launch_channel_partials(cudaStream_t st, const float* src, int pitch, int64
 }
 void launch_finalize_stats(cudaStream_t st, const double2* part, int P, int nch, double count, float* mean,
                            float* var) {
-  launch(k_finalize_stats, static_cast<unsigned>((nch + kFinCh - 1) / kFinCh), kFinThreads, 0, st, part, P, nch,
-         count, mean, var, 0);
+  launch_finalize_stats_at(st, part, P, nch, count, mean, var, 0);
 }
 
 int block_forward(Block* b, const float* x_in, const float* params, float* running,

@@ -177,6 +177,8 @@ void launch_fold_splits(cudaStream_t st, const float* wpart, int splits, int64_t
 void launch_channel_partials(cudaStream_t st, const float* src, int pitch, int64_t M, int nch, double2* part);
 void launch_finalize_stats(cudaStream_t st, const double2* part, int P, int nch, double count, float* mean,
                            float* var);
+void launch_finalize_stats_at(cudaStream_t st, const double2* part, int P, int nch, double count, float* mean,
+                              float* var, int first);
 int profile_read(Block* b, dpb_kernel_stat* out, int max, int* count);
 
 // tensor-core path (dpb_tc_block.cu)

@@ -110,14 +110,20 @@ k_channel_partials(const S* __restrict__ src, int pitch, int c_off, int64_t M,
 // ~P / 64 loads per thread, all independent (the finalize sits on the
 // critical path between two big kernels, so its latency is what matters).
 constexpr int kFinCh = 16, kFinLanes = 64, kFinThreads = kFinCh * kFinLanes;
+// CH channels per CTA (kFinCh, or 4 when there are many partial rows: four
+// times the CTAs pulling them), kFinThreads / CH lanes.  The lane sums are
+// added in lane order (CH = kFinCh), or in 16 runs of 16 lanes then the 16
+// run sums in order (CH = 4): fixed either way.
+template <int CH>
 __device__ __forceinline__ bool fold_block(const double2* part, int P, int nch, int& ch, double2& out) {
-  __shared__ double2 red[kFinLanes][kFinCh + 1];
-  const int tx = threadIdx.x % kFinCh, ty = threadIdx.x / kFinCh;
-  ch = blockIdx.x * kFinCh + tx;
+  constexpr int L = kFinThreads / CH;
+  __shared__ double2 red[L][CH + 1];
+  const int tx = threadIdx.x % CH, ty = threadIdx.x / CH;
+  ch = blockIdx.x * CH + tx;
   double a = 0.0, b = 0.0;
   if (ch < nch) {
 #pragma unroll 9
-    for (int p = ty; p < P; p += kFinLanes) {
+    for (int p = ty; p < P; p += L) {
       const double2 v = part[static_cast<int64_t>(p) * nch + ch];
       a += v.x;
       b += v.y;
@@ -125,27 +131,50 @@ __device__ __forceinline__ bool fold_block(const double2* part, int P, int nch, 
   }
   red[ty][tx] = make_double2(a, b);
   __syncthreads();
-  if (ty != 0 || ch >= nch) return false;
-  double sa = 0.0, sb = 0.0;
+  if constexpr (L > 64) {
+    constexpr int R = L / 16;  // lanes per run
+    if (ty < 16) {
+      double sa = 0.0, sb = 0.0;
+      for (int i = 0; i < R; ++i) {
+        sa += red[ty * R + i][tx].x;
+        sb += red[ty * R + i][tx].y;
+      }
+      __syncwarp();
+      red[ty * R][tx] = make_double2(sa, sb);  // run sum in its first lane's slot
+    }
+    __syncthreads();
+    if (ty != 0 || ch >= nch) return false;
+    double sa = 0.0, sb = 0.0;
+    for (int i = 0; i < 16; ++i) {
+      sa += red[i * R][tx].x;
+      sb += red[i * R][tx].y;
+    }
+    out = make_double2(sa, sb);
+    return true;
+  } else {
+    if (ty != 0 || ch >= nch) return false;
+    double sa = 0.0, sb = 0.0;
 #pragma unroll 16
-  for (int i = 0; i < kFinLanes; ++i) {
-    sa += red[i][tx].x;
-    sb += red[i][tx].y;
+    for (int i = 0; i < L; ++i) {
+      sa += red[i][tx].x;
+      sb += red[i][tx].y;
+    }
+    out = make_double2(sa, sb);
+    return true;
   }
-  out = make_double2(sa, sb);
-  return true;
 }
 
 // Forward statistics: mean = S1/count, biased var = S2/count - mean^2
 // (ops.hpp:138-162 semantics) -> mean_out[first+ch], var_out[first+ch].
-// Grid ceil(nch / kFinCh) x kFinThreads.
+// Grid ceil(nch / CH) x kFinThreads.
+template <int CH = kFinCh>
 __global__ void __launch_bounds__(kFinThreads) k_finalize_stats(const double2* __restrict__ part, int P, int nch,
                                  double count, float* __restrict__ mean_out,
                                  float* __restrict__ var_out, int first) {
   pdl_enter();
   int ch;
   double2 s;
-  if (fold_block(part, P, nch, ch, s)) {
+  if (fold_block<CH>(part, P, nch, ch, s)) {
     const double mean = s.x / count;
     double var = s.y / count - mean * mean;
     if (var < 0.0) var = 0.0;
@@ -156,13 +185,14 @@ __global__ void __launch_bounds__(kFinThreads) k_finalize_stats(const double2* _
 
 // BN backward sums -> dgamma = sum g*xhat, dbeta = sum g (written, ops.hpp:229-230)
 // and the apply coefficients coef[2*ch] = mg, [2*ch+1] = mgx.
+template <int CH = kFinCh>
 __global__ void __launch_bounds__(kFinThreads) k_finalize_bn_bwd(const double2* __restrict__ part, int P, int nch,
                                   double count, float* __restrict__ dgamma,
                                   float* __restrict__ dbeta, float* __restrict__ coef) {
   pdl_enter();
   int ch;
   double2 s;
-  if (fold_block(part, P, nch, ch, s)) {
+  if (fold_block<CH>(part, P, nch, ch, s)) {
     const float sum_g = static_cast<float>(s.x);
     const float sum_gx = static_cast<float>(s.y);
     dgamma[ch] = sum_gx;
