@@ -330,6 +330,11 @@ DPB_API int dpb_model_step(dpb_model* model, const float* input, const int32_t* 
  * when a label was outside [0, classes) — that sample's loss and gradients
  * are NaN.  Gradients must not be used before dpb_model_sync succeeded. */
 DPB_API int dpb_model_sync(dpb_model* model);
+/* Makes `stream` (a cudaStream_t) wait until the last enqueued step has read
+ * its input images and labels (the tensor-core stem: after the forward's loss;
+ * otherwise after the step), so the next batch can be copied into the same
+ * buffers while that step's backward still runs. */
+DPB_API int dpb_model_wait_input(dpb_model* model, void* stream);
 /* The model's device-memory accounting (every block arena + the stem,
  * transition and head buffers) and the number of kernels one training step
  * launches (the CUDA graph's kernel nodes once captured). */

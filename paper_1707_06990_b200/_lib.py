@@ -94,6 +94,7 @@ SIGNATURES = {
     "dpb_model_destroy": (None, [_P]),
     "dpb_model_step": (C.c_int, [_P, _P, _P, _P, _P, _P, _P]),
     "dpb_model_sync": (C.c_int, [_P]),
+    "dpb_model_wait_input": (C.c_int, [_P, _P]),
     "dpb_model_memory_stats": (C.c_int, [_P, C.POINTER(MemoryStats)]),
     "dpb_model_set_comm": (C.c_int, [_P, _P]),
     "dpb_model_buckets": (C.c_int, [C.POINTER(ModelDesc), _P, C.c_int, C.POINTER(C.c_int)]),

@@ -1410,6 +1410,10 @@ struct dpb_model {
   std::vector<cudaEvent_t> ev_tdone;   // per transition: its dW (side stream) written
   std::vector<cudaEvent_t> ev_bucket;  // per block bucket: its gradients written (main)
   cudaEvent_t ev_cjoin = nullptr;      // every bucket reduced
+  // the step's last read of its input images and labels (an external event
+  // node inside the captured graph): dpb_model_wait_input lets the caller's
+  // copy stream bring in the next batch while the rest of the step runs
+  cudaEvent_t ev_input = nullptr;
   int64_t mem_tags[6] = {};       // bytes of m->mem per arena tag
 };
 
@@ -1621,6 +1625,7 @@ DPB_API void dpb_model_destroy(dpb_model* m) {
   for (cudaEvent_t e : m->ev_tdone) cudaEventDestroy(e);
   for (cudaEvent_t e : m->ev_bucket) cudaEventDestroy(e);
   if (m->ev_cjoin) cudaEventDestroy(m->ev_cjoin);
+  if (m->ev_input) cudaEventDestroy(m->ev_input);
   if (m->cstream) cudaStreamDestroy(m->cstream);
   for (auto& b : m->blocks)
     if (b.blk) destroy(b.blk);
@@ -1763,6 +1768,7 @@ DPB_API int dpb_model_create(const dpb_model_desc* desc, int device, void* strea
     }
   }
   if (cudaStreamCreateWithFlags(&m->side, cudaStreamNonBlocking) != cudaSuccess) m->side = nullptr;
+  cudaEventCreateWithFlags(&m->ev_input, cudaEventDisableTiming);
   for (size_t i = 0; m->side && i < m->trans.size() + 1; ++i) {
     cudaEvent_t e;
     cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
@@ -1822,6 +1828,13 @@ DPB_API int dpb_model_set_comm(dpb_model* m, dpb_comm* comm) {
   return DPB_OK;
 }
 
+DPB_API int dpb_model_wait_input(dpb_model* m, void* stream) {
+  if (!m) return fail(DPB_CONFIG_ERROR, "null model");
+  DeviceGuard dg(m->device);
+  const cudaError_t e = cudaStreamWaitEvent(static_cast<cudaStream_t>(stream), m->ev_input, 0);
+  return e == cudaSuccess ? DPB_OK : cuda_fail(e, "model wait input");
+}
+
 DPB_API int dpb_model_memory_stats(dpb_model* m, dpb_memory_stats* out) {
   if (!m || !out) return fail(DPB_CONFIG_ERROR, "null argument");
   m->tracker.snapshot(out);
@@ -1852,6 +1865,17 @@ DPB_API int dpb_model_sync(dpb_model* m) {
 namespace {
 
 // Every launch of one training step on m->stream (and the side stream).
+// dpb_model_wait_input's event: an external event node when the step is being
+// captured into its graph (so replays record it), a plain record otherwise
+static void record_input_event(dpb_model* m, cudaStream_t st) {
+  if (!m->ev_input) return;
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  if (cudaStreamIsCapturing(st, &cs) == cudaSuccess && cs == cudaStreamCaptureStatusActive)
+    cudaEventRecordWithFlags(m->ev_input, st, cudaEventRecordExternal);
+  else
+    cudaEventRecord(m->ev_input, st);
+}
+
 int model_step_launch(dpb_model* m, const float* input, const int32_t* labels, const float* params,
                       float* running, float* grads, float* loss) {
   const dpb_model_desc& d = m->d;
@@ -1940,6 +1964,9 @@ int model_step_launch(dpb_model* m, const float* input, const int32_t* labels, c
              params + m->head_w, params + m->head_b, d.classes, labels, m->logits, m->g_logits, m->loss_n,
              m->bad_label);
       launch(k_loss_mean, 1, 32, 0, st, static_cast<const float*>(m->loss_n), N, loss);
+      // labels are read; the images too when the stem keeps its own copy (the
+      // tensor-core stem's space-to-depth planes) — else after the backward
+      if (m->tc_stem) record_input_event(m, st);
       launch(k_running, blocks_of(mb.C, 256), 256, 0, st, mb.C, mean, var, running + m->head_run,
              running + m->head_run + mb.C);
     }
@@ -2104,6 +2131,7 @@ int model_step_launch(dpb_model* m, const float* input, const int32_t* labels, c
     cudaStreamWaitEvent(st, m->ev_cjoin, 0);
   }
   const cudaError_t e = cudaGetLastError();
+  if (!m->tc_stem) record_input_event(m, st);
   return e == cudaSuccess ? DPB_OK : cuda_fail(e, "model step launch");
 }
 

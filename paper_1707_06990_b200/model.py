@@ -303,6 +303,13 @@ class ModelPlan:
     def sync(self) -> None:
         check(lib().dpb_model_sync(self._h))
 
+    def wait_input(self, stream) -> None:
+        """Make `stream` (a torch.cuda.Stream) wait until the last enqueued step
+        has read its input images and labels (dpb_model_wait_input): the next
+        batch's host-to-device copy may then overwrite them while that step
+        finishes."""
+        check(lib().dpb_model_wait_input(self._h, C.c_void_p(stream.cuda_stream)))
+
     def set_comm(self, comm) -> None:
         """Attach a dp.DpComm (or None): dpb_model_step then averages the
         gradients over the ranks, bucket by bucket, overlapped with backward."""

@@ -150,3 +150,52 @@ def test_model_graph_replay_matches_eager():
         for t_a, t_b, what in zip(a, b, ("grads", "loss", "running")):
             assert np.isfinite(t_b).all(), f"step {step} {what}"
             assert np.array_equal(t_a, t_b), f"step {step} {what} differs between graph replay and eager"
+
+
+@pytest.mark.parametrize("stem", ["3x3", "imagenet"])
+def test_model_input_refill_overlapped_with_the_step(stem):
+    """dpb_model_wait_input: the next batch copied into the same input buffers on
+    another stream once the previous step has read them (the tensor-core
+    ImageNet stem releases them after the forward's loss, the 3x3 stem after the
+    whole step) gives the same losses and gradients, bit for bit, as copying
+    between fully synchronised steps."""
+    n = 4
+    in_shape = (3, 32, 32) if stem == "imagenet" else (3, 16, 16)
+    cfg = DenseNetConfig((2, 2), 8, True, 0.5, 10, 16, in_shape, stem=stem)
+    gen = torch.Generator().manual_seed(3)
+    xa = torch.randn(n, *in_shape, generator=gen).cuda()
+    xb = torch.randn(n, *in_shape, generator=gen).cuda()
+    labels = (torch.arange(n, dtype=torch.int32) % 10).cuda()
+    s, cs = torch.cuda.Stream(), torch.cuda.Stream()
+
+    def run(overlap):
+        plan = ModelPlan(cfg, n, dtype="bf16", stream=s)
+        params = plan.init_params(seed=5)
+        running = plan.initial_running()
+        grads = torch.empty(plan.param_elems, device="cuda")
+        loss = torch.zeros(1, device="cuda")
+        x = xa.clone()
+        torch.cuda.synchronize()
+        plan.step(x, labels, params, running, grads, loss)
+        with torch.cuda.stream(s):
+            g1, l1 = grads.clone(), loss.clone()
+        if overlap:
+            plan.wait_input(cs)
+            with torch.cuda.stream(cs):
+                x.copy_(xb)
+                ev = torch.cuda.Event()
+                ev.record(cs)
+            s.wait_event(ev)
+        else:
+            torch.cuda.synchronize()
+            x.copy_(xb)
+            torch.cuda.synchronize()
+        plan.step(x, labels, params, running, grads, loss)
+        plan.sync()
+        torch.cuda.synchronize()
+        out = [t.cpu().numpy() for t in (g1, l1, grads, loss, running)]
+        plan.close()
+        return out
+
+    for a, b in zip(run(False), run(True)):
+        np.testing.assert_array_equal(a, b)
