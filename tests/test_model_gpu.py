@@ -85,6 +85,13 @@ def test_model_step_matches_reference(name, dtype):
         o += size
     assert o == grads.size
     assert worst[0] <= TOL[dtype], f"{name} {dtype}: worst {worst[1]} normwise error {worst[0]:.3e}"
+    if dtype == "fp32":
+        # and elementwise with the reference's own measure, rel_err(a, b) =
+        # |a - b| / max(1, |a|, |b|) (gradcheck.hpp:14-17), at its 1e-4 contract
+        ref = g["grads"].astype(np.float64)
+        got = grads.astype(np.float64)
+        rel = np.abs(got - ref) / np.maximum(1.0, np.maximum(np.abs(got), np.abs(ref)))
+        assert rel.max() <= 1e-4, f"{name}: elementwise rel_err {rel.max():.3e} at {int(rel.argmax())}"
 
 
 def test_model_step_is_deterministic():
