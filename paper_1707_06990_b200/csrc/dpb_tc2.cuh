@@ -271,6 +271,7 @@ __global__ void __launch_bounds__(Roles<Op>::kThreads, 1) tc2_kernel(const __gri
     const int grp = (warp - kEpiWarp0) >> 2;      // first 32-column box of this warp's group
     const int row = quarter * 32 + lane;
     const int et = tid - kEpiWarp0 * 32;
+    const bool sums = op.want_col_sums();  // (the split-K forward's come from its reduce pass)
     int at = 0, e0 = 0;
     for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++at) {
       const int a = at & 1;
@@ -302,7 +303,7 @@ __global__ void __launch_bounds__(Roles<Op>::kThreads, 1) tc2_kernel(const __gri
             float s1[8], s2[8];
             op.epilogue(tile, row, cc * 8, *reinterpret_cast<const float(*)[8]>(&v[q2 * 8]), aux, ebox,
                         s1, s2);
-            if constexpr (Op::kColSums) {
+            if (Op::kColSums && sums) {
               const float x = warp_colsum8(s1, lane);
               const float y = warp_colsum8(s2, lane);
               if ((lane & 3) == 0) {
@@ -326,7 +327,7 @@ __global__ void __launch_bounds__(Roles<Op>::kThreads, 1) tc2_kernel(const __gri
       tc::tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&acc_empty[a]);
-      if constexpr (Op::kColSums) {
+      if (Op::kColSums && sums) {
         named_sync(1, 32 * R::kEpi);
         for (int c = et; c < BN; c += 32 * R::kEpi) {
           const double x = static_cast<double>(red[0][0][c]) + red[0][1][c] + red[0][2][c] + red[0][3][c];
@@ -416,6 +417,7 @@ struct Fwd1x1 {
   static constexpr int kTmemCols = BN;
   static constexpr bool kEarlyLoads = true;  // features / g0 / z: >= two launches old
   static constexpr bool kColSums = true;
+  __device__ bool want_col_sums() const { return ks == 1; }
   static constexpr bool kMmaReadsRaw = !RES;
   static constexpr int kBox = 32 * kBM * 4;                    // 16 KB
   static constexpr int kBBytes = tc::Tile<BN>::kBytes;
@@ -699,6 +701,7 @@ struct Dgrad1x1 {
   static constexpr int kTmemCols = BN;
   static constexpr bool kEarlyLoads = true;  // g0 (3x3 dgrad) and z: >= two launches old
   static constexpr bool kColSums = true;
+  __device__ bool want_col_sums() const { return true; }
   static constexpr bool kMmaReadsRaw = false;
   static constexpr int kBox = 32 * kBM * 4;        // 16 KB: 128 rows x 32 fp32 channels
   static constexpr int kRawBytes = 2 * kBox;       // g0 | z
@@ -838,6 +841,7 @@ struct Wgrad1x1 {
   static constexpr int kTmemCols = kMT * BN;
   static constexpr bool kEarlyLoads = false;  // side stream: behind an event, not a PDL edge
   static constexpr bool kColSums = false;
+  __device__ bool want_col_sums() const { return false; }
   static constexpr bool kMmaReadsRaw = false;
   static constexpr int kBoxP = 32;                       // pixels per K block
   static constexpr int kBox = kBoxP * 32 * 4;            // 4 KB
