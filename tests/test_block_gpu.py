@@ -175,6 +175,11 @@ def test_block_matches_oracle_medium(dtype, layout):
     (4, 7, 7, 3936, 1, 48, 192),
     (4, 14, 14, 2240, 1, 32, 128),
     (8, 7, 7, 1120, 2, 32, 128),
+    # 56x56 with more halo tiles than SMs: the 3x3 forward picks K chunks for
+    # two CTAs per SM — with the two-slot raw ring at k = 32, the one-slot
+    # ring at k = 48 (bk = 192)
+    (8, 56, 56, 64, 1, 32, 128),
+    (8, 56, 56, 64, 1, 48, 192),
 ])
 @pytest.mark.parametrize("dtype", ["fp32", "bf16"])
 def test_block_matches_oracle_shapes(s, dtype):
