@@ -147,6 +147,8 @@ TRAIN_CASES = {
     "train_d264k48_56": ((6, 12, 64, 48), 48, 0.5, 1000, 96, (2, 3, 56, 56), 7, 0, False),
     # the bench headline network: DenseNet-264-k32 with the ImageNet stem at 224x224
     "train_d264k32_224": ((6, 12, 64, 48), 32, 0.5, 1000, 64, (2, 3, 224, 224), 7, 1, False),
+    # BASELINE configs[2]: DenseNet-121 with the ImageNet stem at 224x224
+    "train_d121_224": ((6, 12, 24, 16), 32, 0.5, 1000, 64, (2, 3, 224, 224), 11, 1, False),
 }
 
 

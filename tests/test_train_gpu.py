@@ -46,7 +46,7 @@ pytestmark = pytest.mark.gpu
 GOLD = os.path.join(os.path.dirname(__file__), "golden")
 TOL = {"fp32": 1e-4, "bf16": 2e-2}
 SMALL = ["train_small", "train_imagenet_small", "train_imagenet_k32", "train_bc100_b64"]
-LARGE = ["train_d264k32_56", "train_d264k48_56", "train_d264k32_224"]
+LARGE = ["train_d264k32_56", "train_d264k48_56", "train_d264k32_224", "train_d121_224"]
 
 
 def _load(name):
