@@ -92,6 +92,7 @@ struct HaloPlan {
   int fwd_bn = 0, fwd_kc = 0, bwd_bn = 0, bwd_kc = 0;
   int bwd_split = 1;  // 3x3 dgrad: output-column groups of bwd_bn per tile (grid.y)
   int fwd_ring = 2;   // 3x3 forward: raw halo ring depth (1 when that fits two CTAs per SM)
+  int fwd_kpair = 0;  // 3x3 forward: K chunks split over a (1, 2) cluster per tile (few tiles)
   int64_t fwd_layer_bytes = 0, bwd_layer_bytes = 0;  // pre-tiled W2 image per layer
 };
 

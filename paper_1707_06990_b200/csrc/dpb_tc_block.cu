@@ -142,6 +142,12 @@ HaloPlan tc_halo_plan(const dpb_block_desc& d) {
       p.fwd_bn = bn;
       p.fwd_kc = kc;
       p.fwd_ring = ring;
+      // under half a wave of tiles, a CTA pair per tile (cluster (1, 2), DSMEM
+      // sum of the two K halves) when its exchange buffer fits too
+      static const bool no_pair = std::getenv("DPB_HALO_NO_KPAIR") != nullptr;
+      const bool taps = bn == 16 && d.k % 4 == 0 && 9 * d.k <= 128 && g.R <= 2 * tc::kBM;
+      p.fwd_kpair = !no_pair && !taps && 2 * tiles <= 148 && nkb >= 2 && nkb % 2 == 0 &&
+                    stage * nst + fwd_aux(kc) + 16 + static_cast<size_t>(tc::kBM) * bn * 4 <= kHaloSmemMax;
       p.fwd_layer_bytes = static_cast<int64_t>(nkb) * 2 * (9LL * bn * kc * 2);
       // all taps as GEMM columns: N = 9k <= 128 (two 128-column accumulators),
       // 4-column TMEM loads per tap, both 128-row M blocks inside the halo
@@ -230,6 +236,22 @@ int tc_conv3x3_fwd(Block* b, const LayerArgs<float>& a, int l) {
       op.prod0 = 0;  // every warp produces (the taps GEMM keeps the shared-barrier engine path)
       op.raw_want = ring;
       launch_halo(b, op, grid, tstage, nst, taux);
+      return static_cast<int>(grid.x);
+    }
+    if (b->halo.fwd_kpair) {
+      const dim3 grid(static_cast<unsigned>(nimg(a) * h.g.tpi), 2);
+      const size_t paux = (aux + 15) / 16 * 16 + static_cast<size_t>(tc::kBM) * bn * 4;
+      auto go = [&](auto op) {
+        op.kpair = 1;
+        launch_cluster(tc::tc_halo_kernel<decltype(op)>, grid, tc::kThreads, stage * nst + paux, b->stream,
+                       dim3(1, 2, 1), op);
+      };
+      switch (bn) {
+        case 16: go(fwd_op<16>(h, ring)); break;
+        case 32: go(fwd_op<32>(h, ring)); break;
+        case 48: go(fwd_op<48>(h, ring)); break;
+        default: go(fwd_op<64>(h, ring)); break;
+      }
       return static_cast<int>(grid.x);
     }
     {

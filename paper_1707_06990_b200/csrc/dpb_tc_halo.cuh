@@ -198,6 +198,45 @@ __global__ void __launch_bounds__(kThreads, Op::kMinBlocks) tc_halo_kernel(const
 
   const int quarter = warp & 3, half = warp >> 2;
   const int row = quarter * 32 + lane;
+  // K pair (ops with kKPair, op.kpair set): the two CTAs of a cluster (1, 2)
+  // each accumulated half of the K chunks of one tile; rank 1 adds its
+  // accumulator into rank 0's shared exchange buffer over DSMEM and leaves,
+  // rank 0 runs the epilogue on the sum.  (Fixed order: rank 0 + rank 1.)
+  const float* xsum = nullptr;
+  if constexpr (Op::kKPair) {
+    if (op.kpair) {
+      constexpr int kCols = Op::kTmemCols / Op::kAccCopies;
+      float* xbuf = reinterpret_cast<float*>(aux + op.xbuf_offset());  // [kBM][kCols]
+      const uint32_t rank = cluster_ctarank();
+      if (rank == 1) {
+        for (int cc = half; cc < kCols / 8; cc += 2) {
+          float v[8];
+          tmem_ld8(tmem + (static_cast<uint32_t>(quarter * 32) << 16) + cc * 8, v);
+#pragma unroll
+          for (int c2 = 1; c2 < Op::kAccCopies; ++c2) {
+            float w[8];
+            tmem_ld8(tmem + (static_cast<uint32_t>(quarter * 32) << 16) + c2 * kCols + cc * 8, w);
+#pragma unroll
+            for (int i = 0; i < 8; ++i) v[i] += w[i];
+          }
+          const uint32_t dst = mapa_cluster(smem_u32(xbuf + row * kCols + cc * 8), 0);
+          st_cluster_v4(dst, v[0], v[1], v[2], v[3]);
+          st_cluster_v4(dst + 16, v[4], v[5], v[6], v[7]);
+        }
+      }
+      cluster_sync();  // release rank 1's stores / acquire them on rank 0
+      if (rank == 1) {
+        tc_fence_before();
+        __syncthreads();
+        if (warp == 0) {
+          tc_fence_after();
+          tmem_dealloc<TCOLS>(tmem);
+        }
+        return;
+      }
+      xsum = xbuf;
+    }
+  }
   float* ytap = reinterpret_cast<float*>(smem);  // kTapCols: [9][128][k], over the dead stages
   if constexpr (Op::kTapCols) {
     // all taps in one GEMM: D[r][tap*k + o] over halo rows r (M blocks of 128);
@@ -292,6 +331,12 @@ __global__ void __launch_bounds__(kThreads, Op::kMinBlocks) tc_halo_kernel(const
         tmem_ld8(tmem + (static_cast<uint32_t>(quarter * 32) << 16) + c2 * kOutCols + cc * 8, w);
 #pragma unroll
         for (int i = 0; i < 8; ++i) v[i] += w[i];
+      }
+      if (xsum) {  // K pair: + the partner CTA's half
+        const float4 a = *reinterpret_cast<const float4*>(xsum + row * kOutCols + cc * 8);
+        const float4 b = *reinterpret_cast<const float4*>(xsum + row * kOutCols + cc * 8 + 4);
+        v[0] += a.x; v[1] += a.y; v[2] += a.z; v[3] += a.w;
+        v[4] += b.x; v[5] += b.y; v[6] += b.z; v[7] += b.w;
       }
     } else {
       for (int i = 0; i < 8; ++i) v[i] = 0.f;
@@ -433,15 +478,19 @@ struct Tc3x3FwdHalo {
   static constexpr bool kColSums = true;
   static constexpr bool kBulk = true;
   static constexpr int kEpiPrefetch = 0;  // (see Tc3x3DgradHalo)
+  static constexpr bool kKPair = true;  // launched as cluster (1, 2) pairs when kpair
   HaloArgs h;
   // producer threads [prod0, kThreads): past the issuer warps here; all of
   // them for Tc3x3FwdTaps (non-specialised engine path), set by the host
   int prod0 = 32 * kIssuers;
   int raw_want = 2;  // raw ring depth requested by the host (HaloPlan::fwd_ring)
+  int kpair = 0;     // 1: CTA (x, y) of a (1, 2) cluster takes K chunks [y * nkb / 2, (y + 1) * nkb / 2)
   __device__ uint32_t halo_bytes() const { return static_cast<uint32_t>(h.g.R * h.kc * 2); }
   __device__ uint32_t b_bytes() const { return static_cast<uint32_t>(9 * BN * h.kc * 2); }
   __device__ uint32_t stage_bytes() const { return 2 * (halo_bytes() + b_bytes()); }
-  __device__ int num_kb() const { return (h.a.bk + h.kc - 1) / h.kc; }
+  __device__ int nkb_all() const { return (h.a.bk + h.kc - 1) / h.kc; }
+  __device__ int num_kb() const { return kpair ? nkb_all() / 2 : nkb_all(); }
+  __device__ int kb0() const { return kpair ? static_cast<int>(blockIdx.y) * (nkb_all() / 2) : 0; }
   __device__ int tile() const { return blockIdx.x % h.g.tpi; }
   __device__ int img() const { return blockIdx.x / h.g.tpi; }
   // aux: BN table | raw fp32 halo ring (depth K chunks) | halo row table.
@@ -459,6 +508,9 @@ struct Tc3x3FwdHalo {
   __host__ __device__ static uint32_t aux_bytes(int bk, int R, int kc, int want) {
     return rows_offset(bk, R, kc, want) + 4 * R;
   }
+  // K pair: rank 0's exchange buffer [kBM][BN] fp32 after the other tables
+  __host__ __device__ static uint32_t xbuf_bytes() { return kBM * BN * 4; }
+  __device__ uint32_t xbuf_offset() const { return (aux_bytes(h.a.bk, h.g.R, h.kc, raw_want) + 15) / 16 * 16; }
   __device__ void prologue(uint8_t* aux) const {
     fill_bn_fwd(reinterpret_cast<BnFwd*>(aux), h.a.bk, 0, h.a.bmean, h.a.bvar, h.a.gamma_b,
                 h.a.beta_b);
@@ -472,7 +524,7 @@ struct Tc3x3FwdHalo {
   }
   __device__ void bulk(uint32_t st, int kb, uint64_t* bar) const {
     mbar_expect_tx(bar, 2 * b_bytes());
-    bulk_load(st + 2 * halo_bytes(), h.wt + static_cast<int64_t>(kb) * 2 * b_bytes(), 2 * b_bytes(),
+    bulk_load(st + 2 * halo_bytes(), h.wt + static_cast<int64_t>(kb0() + kb) * 2 * b_bytes(), 2 * b_bytes(),
               bar);
   }
   // chunk q of a K chunk -> (halo row r, channel offset kk): eight consecutive
@@ -498,7 +550,7 @@ struct Tc3x3FwdHalo {
     const uint32_t ring = smem_u32(aux + raw_offset(a.bk) + (kb % depth) * raw_bytes(h.g.R, h.kc));
     const int* rowoff = reinterpret_cast<const int*>(aux + rows_offset(a.bk, h.g.R, h.kc, raw_want));
     const int kcn = h.kc >> 3;
-    const int j_base = kb * h.kc;
+    const int j_base = (kb0() + kb) * h.kc;
     const float* zb = a.z + static_cast<int64_t>(img()) * h.g.H * h.g.W * a.bk + j_base;
     const int nchunk = h.g.R * kcn;
     const int pthreads = kThreads - prod0;
@@ -538,7 +590,7 @@ struct Tc3x3FwdHalo {
     }
     const float* ring = reinterpret_cast<const float*>(aux + raw_offset(a.bk) + (kb % depth) * raw_bytes(h.g.R, h.kc));
     const int* rowoff = reinterpret_cast<const int*>(aux + rows_offset(a.bk, h.g.R, h.kc, raw_want));
-    const int j_base = kb * h.kc;
+    const int j_base = (kb0() + kb) * h.kc;
     const int kcn = h.kc >> 3;
     const int nchunk = h.g.R * kcn;
     const int q0 = static_cast<int>(threadIdx.x) - prod0;
@@ -799,6 +851,7 @@ struct Tc3x3DgradHalo {
     }
   }
   static constexpr int kEpiPrefetch = BN <= 64 ? 2 : 4;  // z column groups per load batch (register cap)
+  static constexpr bool kKPair = false;
   __device__ void epi_load(int row, int col0, float (&zv)[8]) const {
     const LayerArgs<float>& a = h.a;
     col0 += n0();
@@ -873,6 +926,7 @@ struct Tc3x3WgradHalo {
   static constexpr bool kColSums = false;
   static constexpr bool kBulk = false;
   static constexpr int kEpiPrefetch = 0;  // (see Tc3x3DgradHalo)
+  static constexpr bool kKPair = false;
   static constexpr int kMaxChunks = 6;  // bk = 48 at W = 32: 1456 chunks, one load batch
   HaloArgs h;
   int tpc;      // tiles per CTA
