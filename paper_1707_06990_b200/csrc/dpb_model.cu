@@ -580,6 +580,50 @@ __global__ void k_trans_pool(const float* __restrict__ feat, int ld, int64_t N, 
   }
 }
 
+// k_trans_pool with 16-byte rows (C % 4 == 0, ld % 4 == 0): thread = (pooled
+// pixel, 4 channels), the window's four float4 loads issued together.
+__global__ void k_trans_pool4(const float* __restrict__ feat, int ld, int64_t Mq, int H, int W, int C,
+                              const float* __restrict__ mean, const float* __restrict__ var,
+                              const float* __restrict__ gamma, const float* __restrict__ beta,
+                              float* __restrict__ P) {
+  pdl_enter();
+  const int cq = C / 4;
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= Mq * cq) return;
+  const int64_t q = i / cq;
+  const int c = static_cast<int>(i - q * cq) * 4;
+  const int Ho = H / 2, Wo = W / 2;
+  const int n = static_cast<int>(q / (Ho * Wo));
+  const int r = static_cast<int>(q - static_cast<int64_t>(n) * Ho * Wo);
+  const int oy = r / Wo, ox = r - (r / Wo) * Wo;
+  const int64_t p = (static_cast<int64_t>(n) * H + 2 * oy) * W + 2 * ox;
+  const float4 x0 = __ldg(reinterpret_cast<const float4*>(feat + p * ld + c));
+  const float4 x1 = __ldg(reinterpret_cast<const float4*>(feat + (p + 1) * ld + c));
+  const float4 x2 = __ldg(reinterpret_cast<const float4*>(feat + (p + W) * ld + c));
+  const float4 x3 = __ldg(reinterpret_cast<const float4*>(feat + (p + W + 1) * ld + c));
+  float m4[4], g4[4], b4[4], inv[4];  // (parameter offsets need not be 16-byte aligned)
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    m4[j] = __ldg(mean + c + j);
+    inv[j] = bn_inv(__ldg(var + c + j));
+    g4[j] = __ldg(gamma + c + j);
+    b4[j] = __ldg(beta + c + j);
+  }
+  const float a0[4] = {x0.x, x0.y, x0.z, x0.w}, a1[4] = {x1.x, x1.y, x1.z, x1.w};
+  const float a2[4] = {x2.x, x2.y, x2.z, x2.w}, a3[4] = {x3.x, x3.y, x3.z, x3.w};
+  float o[4];
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {  // the same sum order as k_trans_pool
+    float acc = 0.f;
+    acc += fmaxf(bn_ref(a0[j], m4[j], inv[j], g4[j], b4[j]), 0.f);
+    acc += fmaxf(bn_ref(a1[j], m4[j], inv[j], g4[j], b4[j]), 0.f);
+    acc += fmaxf(bn_ref(a2[j], m4[j], inv[j], g4[j], b4[j]), 0.f);
+    acc += fmaxf(bn_ref(a3[j], m4[j], inv[j], g4[j], b4[j]), 0.f);
+    o[j] = acc * 0.25f;
+  }
+  *reinterpret_cast<float4*>(P + q * C + c) = make_float4(o[0], o[1], o[2], o[3]);
+}
+
 // running statistics momentum update from a block's batch statistics (biased var)
 __global__ void k_running(int C, const float* __restrict__ mean, const float* __restrict__ var,
                           float* __restrict__ run_mean, float* __restrict__ run_var) {
@@ -1943,8 +1987,12 @@ int model_step_launch(dpb_model* m, const float* input, const int32_t* labels, c
     if (b + 1 < nb) {
       ModelTrans& t = m->trans[b];
       ModelBlock& nx = m->blocks[b + 1];
-      launch(k_trans_pool, dim3(blocks_of(t.C, 128), static_cast<unsigned>(std::min<int64_t>(t.Mq, 65535))), 128,
-             0, st, feat, mb.Cp, N, mb.h, mb.w, t.C, mean, var, params + t.gamma, params + t.beta, t.P);
+      if (t.C % 4 == 0 && mb.Cp % 4 == 0)
+        launch(k_trans_pool4, blocks_of(t.Mq * (t.C / 4), 256), 256, 0, st, feat, mb.Cp, t.Mq, mb.h, mb.w, t.C, mean,
+               var, params + t.gamma, params + t.beta, t.P);
+      else
+        launch(k_trans_pool, dim3(blocks_of(t.C, 128), static_cast<unsigned>(std::min<int64_t>(t.Mq, 65535))), 128,
+               0, st, feat, mb.Cp, N, mb.h, mb.w, t.C, mean, var, params + t.gamma, params + t.beta, t.P);
       if (d.dtype == DPB_BF16)
         trans_gemm<0>(st, static_cast<int>(t.Mq), t.cout, t.C, t.P, t.C, params + t.w, t.C, nx.x, nx.Cp);
       else
